@@ -1,0 +1,211 @@
+/*
+ * sdgr.h — C ABI of the B200-native SAR Differentiable Gaussian Rasterizer.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   sarsplat.render / render_forward / backward
+ * (/root/reference/pkg/src/sarsplat/forward.py:256-285, backward.py:243-290).
+ * The reference is pure Python/NumPy, so its "FFI" for this path is the set of
+ * stage functions its own tests call directly; each entry point below replaces
+ * one of them (file:line cited per function).  INTEGRATION.md shows the ctypes
+ * binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - Every pointer in the structs is a DEVICE pointer unless stated otherwise;
+ *    all buffers are caller-allocated (the library never allocates).
+ *  - Every call is asynchronous on the caller's `stream` (a cudaStream_t passed
+ *    as void*; NULL = legacy default stream).  No call synchronises the host.
+ *  - Return value: an sdgr_status code.  Device-side failures (a non-finite
+ *    intensity, forward.py:192-196) are reported through the int32 status word
+ *    the caller passes, read back once per step by the host wrapper.
+ *  - Arrays indexed by Gaussian are N-sized in scene order (no compaction);
+ *    culled / skipped Gaussians carry flags instead of being dropped.
+ */
+#ifndef SDGR_H_
+#define SDGR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDGR_ABI_VERSION 1
+#define SDGR_TILE 16          /* tile edge in cells / pixels (16x16 = 256 rays) */
+#define SDGR_TILE_RAYS 256
+#define SDGR_MAX_PLANE 32767  /* plane dims must fit int16 bboxes */
+
+typedef enum sdgr_status {
+  SDGR_OK = 0,
+  SDGR_ERR_INVALID = 1,   /* InvalidParameterError  (validation.py:16) */
+  SDGR_ERR_NUMERICAL = 2, /* NumericalError         (validation.py:24) */
+  SDGR_ERR_STATE = 3,     /* StateError             (validation.py:28) */
+  SDGR_ERR_CUDA = 4,      /* a CUDA launch / runtime error               */
+  SDGR_ERR_CAPACITY = 5   /* caller buffer too small (resize and retry)  */
+} sdgr_status;
+
+/* Gaussian flag bits (sdgr_projection.flags). */
+#define SDGR_FLAG_VISIBLE 1u  /* passed skip + cull: Projection.indices (geometry.py:306) */
+#define SDGR_FLAG_SKIPPED 2u  /* non-finite or det <= 0 (geometry.py:280-290)            */
+#define SDGR_FLAG_CULLED 4u   /* outside the comp-plane 3-sigma frustum (geometry.py:293-305) */
+
+/* Device status word layout (int32[4]) written by the compositing kernels. */
+#define SDGR_STATUS_NONFINITE 0 /* != 0 when any per-pair contribution was non-finite */
+
+/*
+ * Per-view constants, filled on the host in FP64 with the reference's own
+ * expressions (geometry.py:35-128) so they are bit-identical to it.
+ */
+typedef struct sdgr_view {
+  double R[9];     /* world->radar rotation, row-major   (geometry.py:35-47)   */
+  double T[3];     /* x_r = R x + T                       (geometry.py:59-62)   */
+  double cam[3];   /* platform position                   (geometry.py:50-56)   */
+  double mc[6];    /* jac_comp @ R, 2x3 row-major         (geometry.py:267)     */
+  double mi[6];    /* jac_img  @ R                        (geometry.py:268)     */
+  double den_u;    /* azimuth_res * n_azimuth             (geometry.py:85)      */
+  double den_v;    /* range_res * n_range * tan(el)       (geometry.py:86,102)  */
+  double off_vi;   /* 2 * altitude / (range_res*n_range*sin(el)) (geometry.py:103) */
+  double cov_reg;  /* added to both 2D covariance diagonals (geometry.py:275-278) */
+  double cutoff;   /* footprint radius; +inf = dense all-pairs mode (forward.py:80-84) */
+  int32_t n_u, n_v;   /* computation-plane ray grid (radar.py:55-58) */
+  int32_t n_az, n_rg; /* imaging-plane width (azimuth) / height (range) */
+} sdgr_view;
+
+/* Scene parameters, SoA like sarsplat.Scene (scene.py:132-158). */
+typedef struct sdgr_scene {
+  int64_t n;
+  int32_t dtype;          /* 0 = float32, 1 = float64 */
+  int32_t pad_;
+  const void* positions;  /* (n,3) */
+  const void* rotations;  /* (n,4) w,x,y,z (need not be unit) */
+  const void* log_scales; /* (n,3) */
+  const void* sh_coeffs;  /* (n,16) */
+  const void* ke_raw;     /* (n,2) softplus pre-activations */
+} sdgr_scene;
+
+/* One projection plane's footprint records (N-sized). */
+typedef struct sdgr_plane {
+  double* uv;           /* (n,2) pixel-space center                          */
+  double* inv_cov;      /* (n,4) a00, a01, a11, 0  (forward.py:33-42)        */
+  double* cov;          /* (n,4) c00, c01, c11, 0  optional (NULL = skip)     */
+  int16_t* bbox;        /* (n,4) x0, x1, y0, y1 clipped cell bbox (forward.py:76-79) */
+  uint64_t* cell_mask;  /* (n) members in the 8x8 cell window at (x0,y0), bit = (iv-y0)*8+(iu-x0) */
+  uint64_t* tile_mask;  /* (n) member tiles in the 8x8 tile window at (x0/16,y0/16) */
+  int32_t* n_tiles;     /* (n) number of 16x16 tiles holding >= 1 member cell */
+} sdgr_plane;
+
+/* Output of sdgr_project (geometry.Projection, geometry.py:185-230). */
+typedef struct sdgr_projection {
+  int64_t n;
+  sdgr_plane comp;       /* computation plane (n_u x n_v)   */
+  sdgr_plane img;        /* imaging plane (n_az x n_rg)     */
+  uint64_t* depth_key;   /* (n) order-preserving FP64 depth key; UINT64_MAX if not visible */
+  float* kappa;          /* (n) ke_fwd + ke_bwd (geometry.py:317, Projection.ke_sum) */
+  float* phase;          /* (n) max(0, P~)                  (geometry.py:316) */
+  float* phase_raw;      /* (n) P~ (backward clamp gate)    (geometry.py:315) */
+  uint8_t* flags;        /* (n) SDGR_FLAG_* */
+  int32_t* counters;     /* (4) [0] visible, [1] skipped, [2] culled; zeroed by sdgr_project */
+  /* optional accessors (NULL to skip) */
+  float* ke_act;         /* (n,2) softplus(ke_raw)          */
+  double* look;          /* (n,4) unit look dir xyz, distance (geometry.py:308-313) */
+} sdgr_projection;
+
+/* (tile, Gaussian) binning of one plane: the per-tile key lists. */
+typedef struct sdgr_tiles {
+  int32_t plane;        /* 0 = computation (depth order), 1 = imaging (index order) */
+  int32_t tiles_x, tiles_y, n_tiles;
+  int64_t n_pairs;      /* T16: number of (tile, Gaussian) member pairs */
+  uint32_t* pair_tile;  /* (n_pairs) tile id, sorted ascending              */
+  int32_t* pair_prim;   /* (n_pairs) scene index; per tile by (depth, index) or index */
+  int32_t* tile_range;  /* (n_tiles,2) [start, end) into the pair arrays      */
+  int32_t seg_len;      /* max Gaussians per work item (depth segment)       */
+  int32_t max_items;    /* capacity of items                                  */
+  int32_t* items;       /* (max_items,4) tile, start, end, first item of tile */
+  int32_t* tile_first;  /* (n_tiles) index of each tile's first work item     */
+  int32_t* n_items;     /* (4) device: [0] work items, [1] overflow flag, [2] walk counter */
+} sdgr_tiles;
+
+/* Scene gradients (backward.SceneGradients, backward.py:25-50), float32. */
+typedef struct sdgr_grads {
+  float* positions;     /* (n,3)  */
+  float* rotations;     /* (n,4)  */
+  float* log_scales;    /* (n,3)  */
+  float* sh_coeffs;     /* (n,16) */
+  float* ke_raw;        /* (n,2)  */
+  float* uv_grad_norm;  /* (n)    */
+  int32_t* visible;     /* (n) 1 if visible (accumulate mode: count of views) */
+} sdgr_grads;
+
+/* ---------------------------------------------------------------- misc -- */
+int sdgr_version(void);
+const char* sdgr_status_string(int status);
+/* Kernels launched by this library since load (the bench's gpu_launches). */
+uint64_t sdgr_launch_count(void);
+/* Bytes of scratch the binning calls need for n Gaussians / max pairs. */
+size_t sdgr_workspace_bytes(int64_t n, int64_t max_pairs);
+
+/* ------------------------------------------------ preprocess (K1) -------- */
+/* geometry.project_all (geometry.py:233-340) + the footprint bbox / member
+ * tests of forward._footprint_pairs (forward.py:60-109) for both planes. */
+int sdgr_project(const sdgr_scene* scene, const sdgr_view* view,
+                 sdgr_projection* proj, void* stream);
+
+/* --------------------------------------------------- binning (K2-K5) ----- */
+/* Stable sort of the visible Gaussians by (depth, index): order[rank] = g.
+ * The depth half of np.lexsort((prim, depth, cell)) (forward.py:147). */
+int sdgr_depth_order(const sdgr_projection* proj, int32_t* order,
+                     void* ws, size_t ws_bytes, void* stream);
+/* offsets[i] = exclusive prefix of member-tile counts in rank order (plane 0,
+ * `order` given) or scene order (plane 1, order == NULL); offsets has n+1
+ * entries, offsets[n] = T16 for the plane. */
+int sdgr_count_pairs(const sdgr_projection* proj, int32_t plane,
+                     const int32_t* order, int32_t* offsets,
+                     void* ws, size_t ws_bytes, void* stream);
+/* Emit (tile, Gaussian) pairs, stable-sort them by tile, extract tile
+ * ranges and depth-segment work items: the per-tile key lists
+ * (forward.py:138-155 at 16x16 granularity; _build_splat_pairs :213-224). */
+int sdgr_bin_pairs(const sdgr_projection* proj, const sdgr_view* view,
+                   const int32_t* order, const int32_t* offsets,
+                   sdgr_tiles* tiles, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------- forward (K6, K7) ------ */
+/* compute_intensities (forward.py:178-199): per-ray emission-absorption walk.
+ * seg_sum / seg_base: (max_items*256) FP64 per-(item, ray) optical-depth
+ * segment sums and exclusive prefixes (kept for the backward).  intensity (n)
+ * is overwritten.  s_stop: rays stop once their log-transmittance exceeds it
+ * (+inf = never, the reference's behaviour).  status: int32[4]. */
+int sdgr_composite_forward(const sdgr_view* view, const sdgr_projection* proj,
+                           const sdgr_tiles* comp, double s_stop,
+                           double* seg_sum, double* seg_base, float* intensity,
+                           int32_t* status, void* stream);
+/* splat_image (forward.py:227-240): image (n_rg, n_az) float32 overwritten.
+ * part: (max_items*256) FP64 scratch. */
+int sdgr_splat(const sdgr_view* view, const sdgr_projection* proj,
+               const sdgr_tiles* img, const float* intensity, double* part,
+               float* image, void* stream);
+
+/* ------------------------------------------------ backward (K8-K10) ------ */
+/* grad_image_stage (backward.py:86-104).  acc_img (6,n): dL/dI, dL/dA(3),
+ * dL/duv(2) on the imaging plane (A = inverse covariance). */
+int sdgr_grad_image(const sdgr_view* view, const sdgr_projection* proj,
+                    const float* intensity, const float* dL_dS, float* acc_img,
+                    void* stream);
+/* grad_intensity_stage (backward.py:107-148).  acc_comp (7,n): dL/dP,
+ * dL/dkappa, dL/dA(3), dL/duv(2) on the computation plane.  dL_dI = acc_img
+ * row 0.  seg_g / seg_d: (max_items*256) FP64 scratch. */
+int sdgr_grad_intensity(const sdgr_view* view, const sdgr_projection* proj,
+                        const sdgr_tiles* comp, double s_stop,
+                        const double* seg_base, const float* dL_dI,
+                        double* seg_g, double* seg_d, float* acc_comp,
+                        void* stream);
+/* grad_geometry_stage + grad_sh_stage + the final scatter (backward.py:171-290).
+ * accumulate = 0 overwrites `out`, 1 adds into it (multi-view steps). */
+int sdgr_grad_geometry(const sdgr_scene* scene, const sdgr_view* view,
+                       const sdgr_projection* proj, const float* acc_img,
+                       const float* acc_comp, sdgr_grads* out, int accumulate,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDGR_H_ */

@@ -1,0 +1,121 @@
+"""ctypes binding of libsdgr.so (the C ABI declared in include/sdgr.h).
+
+This module is the only place the shared library is loaded.  There is no
+fallback: if the library is missing or its ABI version does not match,
+importing the rasterizer raises ImportError.  Build it with
+``python -m paper_2506_21633_b200.csrc.build`` (or ``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+ABI_VERSION = 1
+LIB_PATH = Path(__file__).resolve().parent / "libsdgr.so"
+
+OK, ERR_INVALID, ERR_NUMERICAL, ERR_STATE, ERR_CUDA, ERR_CAPACITY = range(6)
+FLAG_VISIBLE, FLAG_SKIPPED, FLAG_CULLED = 1, 2, 4
+TILE = 16
+
+_p = C.c_void_p
+
+
+class View(C.Structure):
+    _fields_ = [
+        ("R", C.c_double * 9), ("T", C.c_double * 3), ("cam", C.c_double * 3),
+        ("mc", C.c_double * 6), ("mi", C.c_double * 6),
+        ("den_u", C.c_double), ("den_v", C.c_double), ("off_vi", C.c_double),
+        ("cov_reg", C.c_double), ("cutoff", C.c_double),
+        ("n_u", C.c_int32), ("n_v", C.c_int32), ("n_az", C.c_int32), ("n_rg", C.c_int32),
+    ]
+
+
+class SceneDesc(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("dtype", C.c_int32), ("pad_", C.c_int32),
+        ("positions", _p), ("rotations", _p), ("log_scales", _p), ("sh_coeffs", _p), ("ke_raw", _p),
+    ]
+
+
+class Plane(C.Structure):
+    _fields_ = [
+        ("uv", _p), ("inv_cov", _p), ("cov", _p), ("bbox", _p),
+        ("cell_mask", _p), ("tile_mask", _p), ("n_tiles", _p),
+    ]
+
+
+class ProjectionDesc(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("comp", Plane), ("img", Plane),
+        ("depth_key", _p), ("kappa", _p), ("phase", _p), ("phase_raw", _p),
+        ("flags", _p), ("counters", _p), ("ke_act", _p), ("look", _p),
+    ]
+
+
+class TilesDesc(C.Structure):
+    _fields_ = [
+        ("plane", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("n_tiles", C.c_int32),
+        ("n_pairs", C.c_int64), ("pair_tile", _p), ("pair_prim", _p), ("tile_range", _p),
+        ("seg_len", C.c_int32), ("max_items", C.c_int32), ("items", _p), ("tile_first", _p),
+        ("n_items", _p),
+    ]
+
+
+class GradsDesc(C.Structure):
+    _fields_ = [
+        ("positions", _p), ("rotations", _p), ("log_scales", _p), ("sh_coeffs", _p),
+        ("ke_raw", _p), ("uv_grad_norm", _p), ("visible", _p),
+    ]
+
+
+# (name, restype, argtypes) for every symbol include/sdgr.h declares
+SIGNATURES = [
+    ("sdgr_version", C.c_int, []),
+    ("sdgr_status_string", C.c_char_p, [C.c_int]),
+    ("sdgr_launch_count", C.c_uint64, []),
+    ("sdgr_workspace_bytes", C.c_size_t, [C.c_int64, C.c_int64]),
+    ("sdgr_project", C.c_int, [C.POINTER(SceneDesc), C.POINTER(View), C.POINTER(ProjectionDesc), _p]),
+    ("sdgr_depth_order", C.c_int, [C.POINTER(ProjectionDesc), _p, _p, C.c_size_t, _p]),
+    ("sdgr_count_pairs", C.c_int, [C.POINTER(ProjectionDesc), C.c_int32, _p, _p, _p, C.c_size_t, _p]),
+    ("sdgr_bin_pairs", C.c_int, [C.POINTER(ProjectionDesc), C.POINTER(View), _p, _p,
+                                 C.POINTER(TilesDesc), _p, C.c_size_t, _p]),
+    ("sdgr_composite_forward", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc),
+                                         C.c_double, _p, _p, _p, _p, _p]),
+    ("sdgr_splat", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc), _p, _p, _p, _p]),
+    ("sdgr_grad_image", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), _p, _p, _p, _p]),
+    ("sdgr_grad_intensity", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc),
+                                      C.c_double, _p, _p, _p, _p, _p, _p]),
+    ("sdgr_grad_geometry", C.c_int, [C.POINTER(SceneDesc), C.POINTER(View), C.POINTER(ProjectionDesc),
+                                     _p, _p, C.POINTER(GradsDesc), C.c_int, _p]),
+]
+
+
+def load(path: Path | str = LIB_PATH) -> C.CDLL:
+    path = Path(path)
+    if not path.exists():
+        raise ImportError(
+            f"libsdgr.so not found at {path}; build it with "
+            "`python -m paper_2506_21633_b200.csrc.build` (there is no CPU fallback)")
+    lib = C.CDLL(str(path))
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.sdgr_version() != ABI_VERSION:
+        raise ImportError(f"libsdgr ABI {lib.sdgr_version()} != expected {ABI_VERSION}")
+    return lib
+
+
+_LIB = None
+
+
+def lib() -> C.CDLL:
+    global _LIB
+    if _LIB is None:
+        _LIB = load()
+    return _LIB
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None for None)."""
+    return None if t is None else t.data_ptr()

@@ -1,0 +1,279 @@
+// backward.cu — K8 (imaging-plane backward) and K10 (per-Gaussian epilogue).
+//
+// K8 replaces grad_image_stage (backward.py:86-104).  The imaging splat is an
+// unordered sum, so its adjoint is a gather: one thread per Gaussian visits
+// its own member pixels (cell bit-window from K1) and accumulates dL/dI, the
+// quadratic-form gradient and the center gradient in FP64 registers.  No
+// atomics, no pair lists, deterministic.
+//
+// K10 replaces grad_geometry_stage + grad_sh_stage + the scatter/activation
+// epilogue of backward() (backward.py:151-290): inverse chain
+// dSigma2 = -A G A, the two projection sandwiches, the covariance
+// factorisation (log-scales, quaternion with the normalisation projector),
+// the position terms (two planes + phase-function look direction), SH
+// coefficients, softplus' and the densification statistic.
+#include "common.cuh"
+
+namespace sdgr {
+
+template <typename T>
+__device__ __forceinline__ double ldv(const void* p, int64_t i) {
+  return (double)__ldg(static_cast<const T*>(p) + i);
+}
+
+__global__ void __launch_bounds__(256) k_grad_image(sdgr_view view, sdgr_plane pl, const uint8_t* flags,
+                                                    const float* intensity, const float* dLdS,
+                                                    float* acc, int64_t n) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  double dI = 0, g00 = 0, g01 = 0, g11 = 0, gu = 0, gv = 0;
+  if (flags[g] & SDGR_FLAG_VISIBLE) {
+    const double2 uv = reinterpret_cast<const double2*>(pl.uv)[g];
+    const double4 A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
+    const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
+    const double I = (double)intensity[g];
+    const bool dense = !isfinite(view.cutoff);
+    const double cut2 = dmul(view.cutoff, view.cutoff);
+    auto visit = [&](int iu, int iv, double dx, double dy, double q) {
+      const double G = (double)__ldg(dLdS + (int64_t)iv * view.n_az + iu);
+      const double w = (double)expf(-(float)q);
+      dI += G * w;
+      const double dq = -(G * I) * w;
+      g00 += dq * dx * dx;
+      g01 += dq * dx * dy;
+      g11 += dq * dy * dy;
+      gu += -2.0 * dq * (A.x * dx + A.y * dy);
+      gv += -2.0 * dq * (A.y * dx + A.z * dy);
+    };
+    if (bb.x <= bb.y && bb.z <= bb.w) {
+      if ((bb.y - bb.x) < 8 && (bb.w - bb.z) < 8) {
+        uint64_t cm = pl.cell_mask[g];
+        while (cm) {
+          const int b = __ffsll((long long)cm) - 1;
+          cm &= cm - 1;
+          const int iu = bb.x + (b & 7), iv = bb.z + (b >> 3);
+          const double dx = dsub((double)iu, uv.x), dy = dsub((double)iv, uv.y);
+          visit(iu, iv, dx, dy, quadform(A.x, A.y, A.z, dx, dy));
+        }
+      } else {
+        for (int iv = bb.z; iv <= bb.w; ++iv)
+          for (int iu = bb.x; iu <= bb.y; ++iu) {
+            const double dx = dsub((double)iu, uv.x), dy = dsub((double)iv, uv.y);
+            const double q = quadform(A.x, A.y, A.z, dx, dy);
+            if (dense || q <= cut2) visit(iu, iv, dx, dy, q);
+          }
+      }
+    }
+  }
+  acc[g] = (float)dI;
+  acc[n + g] = (float)g00;
+  acc[2 * n + g] = (float)g01;
+  acc[3 * n + g] = (float)g11;
+  acc[4 * n + g] = (float)gu;
+  acc[5 * n + g] = (float)gv;
+}
+
+// d(basis)/d(dir) for the 16 real SH functions (sh.py:68-113), contracted
+// with the coefficients: returns sum_k c_k grad Y_k.
+__device__ __forceinline__ void sh_grad_contract(double x, double y, double z, const double* c,
+                                                 double* out, double* basis) {
+  const double C0 = 0.28209479177387814, C1 = 0.4886025119029199;
+  const double C20 = 1.0925484305920792, C21 = 0.31539156525252005, C22 = 0.5462742152960396;
+  const double C30 = 0.5900435899266435, C31 = 2.890611442640554, C32 = 0.4570457994644658,
+               C33 = 0.3731763325901154, C34 = 1.445305721320277;
+  const double xx = x * x, yy = y * y, zz = z * z;
+  basis[0] = C0; basis[1] = C1 * y; basis[2] = C1 * z; basis[3] = C1 * x;
+  basis[4] = C20 * x * y; basis[5] = C20 * y * z; basis[6] = C21 * (2.0 * zz - xx - yy);
+  basis[7] = C20 * x * z; basis[8] = C22 * (xx - yy);
+  basis[9] = C30 * y * (3.0 * xx - yy); basis[10] = C31 * x * y * z;
+  basis[11] = C32 * y * (4.0 * zz - xx - yy); basis[12] = C33 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+  basis[13] = C32 * x * (4.0 * zz - xx - yy); basis[14] = C34 * z * (xx - yy);
+  basis[15] = C30 * x * (xx - 3.0 * yy);
+  double gx = 0, gy = 0, gz = 0;
+  gy += c[1] * C1;
+  gz += c[2] * C1;
+  gx += c[3] * C1;
+  gx += c[4] * C20 * y;            gy += c[4] * C20 * x;
+  gy += c[5] * C20 * z;            gz += c[5] * C20 * y;
+  gx += c[6] * (-2.0 * C21 * x);   gy += c[6] * (-2.0 * C21 * y);  gz += c[6] * (4.0 * C21 * z);
+  gx += c[7] * C20 * z;            gz += c[7] * C20 * x;
+  gx += c[8] * (2.0 * C22 * x);    gy += c[8] * (-2.0 * C22 * y);
+  gx += c[9] * (C30 * 6.0 * x * y); gy += c[9] * (C30 * (3.0 * xx - 3.0 * yy));
+  gx += c[10] * (C31 * y * z);     gy += c[10] * (C31 * x * z);    gz += c[10] * (C31 * x * y);
+  gx += c[11] * (C32 * (-2.0 * x * y));
+  gy += c[11] * (C32 * (4.0 * zz - xx - 3.0 * yy));
+  gz += c[11] * (C32 * 8.0 * y * z);
+  gx += c[12] * (C33 * (-6.0 * x * z));
+  gy += c[12] * (C33 * (-6.0 * y * z));
+  gz += c[12] * (C33 * (6.0 * zz - 3.0 * xx - 3.0 * yy));
+  gx += c[13] * (C32 * (4.0 * zz - 3.0 * xx - yy));
+  gy += c[13] * (C32 * (-2.0 * x * y));
+  gz += c[13] * (C32 * 8.0 * x * z);
+  gx += c[14] * (C34 * 2.0 * x * z); gy += c[14] * (-C34 * 2.0 * y * z); gz += c[14] * (C34 * (xx - yy));
+  gx += c[15] * (C30 * (3.0 * xx - 3.0 * yy)); gy += c[15] * (C30 * (-6.0 * x * y));
+  out[0] = gx; out[1] = gy; out[2] = gz;
+}
+
+// dL/dSigma2 = -A G A for symmetric 2x2 A = (a,b,c), G = (g0,g1,g2)
+__device__ __forceinline__ void inverse_chain(double a, double b, double c, double g0, double g1,
+                                              double g2, double* d) {
+  const double p00 = a * g0 + b * g1, p01 = a * g1 + b * g2;
+  const double p10 = b * g0 + c * g1, p11 = b * g1 + c * g2;
+  d[0] = -(p00 * a + p01 * b);
+  d[1] = -(p00 * b + p01 * c);
+  d[2] = -(p10 * a + p11 * b);
+  d[3] = -(p10 * b + p11 * c);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view view,
+                                                       sdgr_projection proj, const float* acc_img,
+                                                       const float* acc_comp, sdgr_grads out,
+                                                       int accumulate) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = sc.n;
+  if (g >= n) return;
+  float res[30];
+#pragma unroll
+  for (int k = 0; k < 30; ++k) res[k] = 0.f;
+  const bool vis = proj.flags[g] & SDGR_FLAG_VISIBLE;
+  if (vis) {
+    // plane-space gradients
+    const double4 Ac = reinterpret_cast<const double4*>(proj.comp.inv_cov)[g];
+    const double4 Ai = reinterpret_cast<const double4*>(proj.img.inv_cov)[g];
+    double dSc[4], dSi[4];
+    inverse_chain(Ac.x, Ac.y, Ac.z, acc_comp[2 * n + g], acc_comp[3 * n + g], acc_comp[4 * n + g], dSc);
+    inverse_chain(Ai.x, Ai.y, Ai.z, acc_img[1 * n + g], acc_img[2 * n + g], acc_img[3 * n + g], dSi);
+    const double duc[2] = {acc_comp[5 * n + g], acc_comp[6 * n + g]};
+    const double dui[2] = {acc_img[4 * n + g], acc_img[5 * n + g]};
+    const double dP = acc_comp[g], dk = acc_comp[n + g];
+    // G3 = mc^T dSc mc + mi^T dSi mi   (backward.py:191-193)
+    double G3[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            s += view.mc[3 * b + a] * dSc[2 * b + c] * view.mc[3 * c + d] +
+                 view.mi[3 * b + a] * dSi[2 * b + c] * view.mi[3 * c + d];
+        G3[3 * a + d] = s;
+      }
+    // covariance factor M = R(q) diag(e^s)   (backward.py:195-213)
+    double q[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = ldv<T>(sc.rotations, 4 * g + k);
+    const double nrm = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    const double w = q[0] / nrm, x = q[1] / nrm, y = q[2] / nrm, z = q[3] / nrm;
+    double Rq[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                    2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                    2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+    double s[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) s[j] = exp(ldv<T>(sc.log_scales, 3 * g + j));
+    double M[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) M[3 * i + j] = Rq[3 * i + j] * s[j];
+    double dM[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        dM[3 * i + j] = 2.0 * (G3[3 * i] * M[j] + G3[3 * i + 1] * M[3 + j] + G3[3 * i + 2] * M[6 + j]);
+    double dls[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dls[j] = dM[j] * M[j] + dM[3 + j] * M[3 + j] + dM[6 + j] * M[6 + j];
+    double dR[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) dR[3 * i + j] = dM[3 * i + j] * s[j];
+    // dR/dq-hat partials (backward.py:151-168)
+    const double dqw = 2.0 * (-z * dR[1] + y * dR[2] + z * dR[3] - x * dR[5] - y * dR[6] + x * dR[7]);
+    const double dqx = 2.0 * (y * dR[1] + z * dR[2] + y * dR[3] - 2 * x * dR[4] - w * dR[5] + z * dR[6] +
+                              w * dR[7] - 2 * x * dR[8]);
+    const double dqy = 2.0 * (-2 * y * dR[0] + x * dR[1] + w * dR[2] + x * dR[3] + z * dR[5] - w * dR[6] +
+                              z * dR[7] - 2 * y * dR[8]);
+    const double dqz = 2.0 * (-2 * z * dR[0] - w * dR[1] + x * dR[2] + w * dR[3] - 2 * z * dR[4] + y * dR[5] +
+                              x * dR[6] + y * dR[7]);
+    const double dot = dqw * w + dqx * x + dqy * y + dqz * z;
+    res[3] = (float)((dqw - dot * w) / nrm);
+    res[4] = (float)((dqx - dot * x) / nrm);
+    res[5] = (float)((dqy - dot * y) / nrm);
+    res[6] = (float)((dqz - dot * z) / nrm);
+    res[7] = (float)dls[0]; res[8] = (float)dls[1]; res[9] = (float)dls[2];
+    // position: both affine plane projections + phase look direction
+    double dpos[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      dpos[k] = duc[0] * view.mc[k] + duc[1] * view.mc[3 + k] + dui[0] * view.mi[k] + dui[1] * view.mi[3 + k];
+    const double p0 = ldv<T>(sc.positions, 3 * g), p1 = ldv<T>(sc.positions, 3 * g + 1),
+                 p2 = ldv<T>(sc.positions, 3 * g + 2);
+    const double r0 = p0 - view.cam[0], r1 = p1 - view.cam[1], r2 = p2 - view.cam[2];
+    double dist = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
+    if (dist == 0.0) dist = 1.0;
+    const double d0 = r0 / dist, d1 = r1 / dist, d2 = r2 / dist;
+    double c[16], basis[16], gP[3];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) c[k] = ldv<T>(sc.sh_coeffs, 16 * g + k);
+    sh_grad_contract(d0, d1, d2, c, gP, basis);
+    const bool active = proj.phase_raw[g] > 0.f;
+    if (active) {
+      const double proj_d = gP[0] * d0 + gP[1] * d1 + gP[2] * d2;
+      dpos[0] += dP * (gP[0] - proj_d * d0) / dist;
+      dpos[1] += dP * (gP[1] - proj_d * d1) / dist;
+      dpos[2] += dP * (gP[2] - proj_d * d2) / dist;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) res[10 + k] = (float)(dP * basis[k]);
+    }
+    res[0] = (float)dpos[0]; res[1] = (float)dpos[1]; res[2] = (float)dpos[2];
+    // softplus' = sigmoid (scene.py:36-39)
+    const double k0 = ldv<T>(sc.ke_raw, 2 * g), k1 = ldv<T>(sc.ke_raw, 2 * g + 1);
+    res[26] = (float)(dk * 0.5 * (1.0 + tanh(0.5 * k0)));
+    res[27] = (float)(dk * 0.5 * (1.0 + tanh(0.5 * k1)));
+    // densification statistic in NDC units (backward.py:285-289)
+    const double gx = duc[0] * (view.n_u / 2.0) + dui[0] * (view.n_az / 2.0);
+    const double gy = duc[1] * (view.n_v / 2.0) + dui[1] * (view.n_rg / 2.0);
+    res[28] = (float)sqrt(gx * gx + gy * gy);
+  }
+  float* dst[5] = {out.positions, out.rotations, out.log_scales, out.sh_coeffs, out.ke_raw};
+  const int width[5] = {3, 4, 3, 16, 2};
+  int o = 0;
+#pragma unroll
+  for (int grp = 0; grp < 5; ++grp) {
+#pragma unroll
+    for (int k = 0; k < width[grp]; ++k) {
+      float* pp = dst[grp] + width[grp] * g + k;
+      *pp = accumulate ? *pp + res[o + k] : res[o + k];
+    }
+    o += width[grp];
+  }
+  out.uv_grad_norm[g] = accumulate ? out.uv_grad_norm[g] + res[28] : res[28];
+  out.visible[g] = accumulate ? out.visible[g] + (int)vis : (int)vis;
+}
+
+int launch_grad_image(const sdgr_view& v, const sdgr_projection& p, const float* intensity,
+                      const float* dLdS, float* acc, cudaStream_t st) {
+  k_grad_image<<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(v, p.img, p.flags, intensity, dLdS, acc, p.n);
+  note_launch();
+  return check_launch();
+}
+
+int launch_grad_geometry(const sdgr_scene& sc, const sdgr_view& v, const sdgr_projection& p,
+                         const float* acc_img, const float* acc_comp, const sdgr_grads& out,
+                         int accumulate, cudaStream_t st) {
+  const unsigned blocks = (unsigned)((sc.n + 127) / 128);
+  if (sc.dtype == 0)
+    k_grad_geometry<float><<<blocks, 128, 0, st>>>(sc, v, p, acc_img, acc_comp, out, accumulate);
+  else
+    k_grad_geometry<double><<<blocks, 128, 0, st>>>(sc, v, p, acc_img, acc_comp, out, accumulate);
+  note_launch();
+  return check_launch();
+}
+
+}  // namespace sdgr

@@ -1,0 +1,505 @@
+// binning.cu — K2-K5: depth-rank sort, (tile, Gaussian) pair emission,
+// stable tile sort, per-tile ranges and depth-segment work items.
+//
+// Reference: forward.build_ray_lists (forward.py:138-155) sorts every
+// (cell, Gaussian) pair with np.lexsort((prim, depth, cell)); the splat pairs
+// use np.lexsort((prim, pixel)) (forward.py:220).  Here the same orders are
+// produced at 16x16-tile granularity:
+//   1. one stable LSD radix sort of the N FP64 depth keys (+ index) -> rank
+//   2. pairs emitted in rank order (comp) or index order (imaging)
+//   3. one stable LSD radix sort of the pairs by tile id
+// so each tile's list is ordered by (depth, index) / index, bit-exactly the
+// order the reference walks each ray.
+//
+// The radix sort is a single-pass-per-digit "onesweep" design: one upfront
+// histogram kernel for all digits, then per 8-bit digit one kernel that ranks
+// its 4096-key tile with warp match-ranking, resolves its global offset by
+// decoupled look-back, and scatters through shared memory.
+#include "common.cuh"
+
+namespace sdgr {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortIpt = 16;
+constexpr int kSortTile = kSortThreads * kSortIpt;  // 4096
+constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kCountMask = (1u << 30) - 1;
+
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ------------------------------------------------------------ histogram ----
+template <typename K>
+__global__ void __launch_bounds__(256) k_radix_hist(const K* __restrict__ keys, int64_t n,
+                                                    int begin_bit, int npass,
+                                                    uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[8][256];
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const K k = keys[i];
+    for (int p = 0; p < npass; ++p) atomicAdd(&sh[p][(uint32_t)(k >> (begin_bit + 8 * p)) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) {
+    const uint32_t c = (&sh[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+// exclusive scan of each 256-bin digit histogram; one block per pass
+__global__ void k_radix_hist_scan(const uint32_t* __restrict__ hist, uint32_t* __restrict__ base) {
+  __shared__ uint32_t s[256];
+  const int p = blockIdx.x, t = threadIdx.x;
+  s[t] = hist[p * 256 + t];
+  __syncthreads();
+  for (int off = 1; off < 256; off <<= 1) {
+    const uint32_t v = t >= off ? s[t - off] : 0u;
+    __syncthreads();
+    s[t] += v;
+    __syncthreads();
+  }
+  base[p * 256 + t] = s[t] - hist[p * 256 + t];
+}
+
+// ------------------------------------------------------------- onesweep ----
+template <typename K, bool kIota>
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(
+    const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
+    uint32_t* __restrict__ vout, int64_t n, int shift, const uint32_t* __restrict__ base,
+    uint32_t* status, uint32_t* counter) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  K* skeys = reinterpret_cast<K*>(dyn);
+  uint32_t* svals = reinterpret_cast<uint32_t*>(dyn + sizeof(K) * kSortTile);
+  __shared__ uint32_t whist[kSortThreads / 32][256];
+  __shared__ uint32_t dstart[256];
+  __shared__ int64_t goff[256];
+  __shared__ uint32_t scan_tmp[8];
+  __shared__ int bid_s;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) bid_s = (int)atomicAdd(counter, 1u);
+  for (int i = tid; i < (kSortThreads / 32) * 256; i += kSortThreads) (&whist[0][0])[i] = 0;
+  __syncthreads();
+  const int bid = bid_s;
+  const int64_t tile0 = (int64_t)bid * kSortTile;
+  const uint32_t lt = (1u << lane) - 1u;
+
+  K keys[kSortIpt];
+  uint32_t vals[kSortIpt];
+  uint32_t rank[kSortIpt];
+  uint32_t dig[kSortIpt];
+#pragma unroll
+  for (int i = 0; i < kSortIpt; ++i) {
+    const int64_t idx = tile0 + warp * (32 * kSortIpt) + i * 32 + lane;
+    const bool valid = idx < n;
+    keys[i] = valid ? kin[idx] : K(0);
+    vals[i] = valid ? (kIota ? (uint32_t)idx : vin[idx]) : 0u;
+    dig[i] = valid ? ((uint32_t)(keys[i] >> shift) & 255u) : 256u;
+  }
+#pragma unroll
+  for (int i = 0; i < kSortIpt; ++i) {
+    const uint32_t d = dig[i];
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    uint32_t before = 0;
+    if (d < 256) before = whist[warp][d];
+    rank[i] = before + __popc(peers & lt);
+    __syncwarp();
+    if (d < 256 && lane == __ffs(peers) - 1) whist[warp][d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive offsets across warps, block total
+  const int t = tid;  // digit owned by this thread
+  uint32_t total = 0;
+#pragma unroll
+  for (int w = 0; w < kSortThreads / 32; ++w) {
+    const uint32_t c = whist[w][t];
+    whist[w][t] = total;
+    total += c;
+  }
+  // publish aggregate / inclusive prefix
+  volatile uint32_t* vstat = status;
+  if (bid == 0) vstat[t] = kFlagP | total;
+  else vstat[(int64_t)bid * 256 + t] = kFlagA | total;
+  // block-local exclusive scan of totals over digits
+  uint32_t x = total;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) scan_tmp[warp] = x;
+  __syncthreads();
+  uint32_t wpre = 0;
+  for (int w = 0; w < warp; ++w) wpre += scan_tmp[w];
+  const uint32_t excl = wpre + x - total;
+  dstart[t] = excl;
+  // decoupled look-back for this digit
+  uint32_t prefix = 0;
+  if (bid > 0) {
+    int64_t j = bid - 1;
+    while (true) {
+      const uint32_t s = vstat[j * 256 + t];
+      const uint32_t f = s & ~kCountMask;
+      if (f == 0) continue;
+      prefix += s & kCountMask;
+      if (f == kFlagP) break;
+      --j;
+    }
+    vstat[(int64_t)bid * 256 + t] = kFlagP | (prefix + total);
+  }
+  goff[t] = (int64_t)base[t] + prefix - excl;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kSortIpt; ++i) {
+    const uint32_t d = dig[i];
+    if (d < 256) {
+      const uint32_t lp = dstart[d] + whist[warp][d] + rank[i];
+      skeys[lp] = keys[i];
+      svals[lp] = vals[i];
+    }
+  }
+  __syncthreads();
+  const int64_t rem = n - tile0;
+  const int cnt = rem < kSortTile ? (int)rem : kSortTile;
+  for (int i = tid; i < cnt; i += kSortThreads) {
+    const K k = skeys[i];
+    const uint32_t d = (uint32_t)(k >> shift) & 255u;
+    const int64_t gp = goff[d] + i;
+    kout[gp] = k;
+    vout[gp] = svals[i];
+  }
+}
+
+template <typename K>
+size_t radix_ws_bytes(int64_t n, int npass) {
+  const int64_t nblk = (n + kSortTile - 1) / kSortTile;
+  size_t b = 0;
+  b += align_up(sizeof(uint32_t) * 8 * 256);                  // hist
+  b += align_up(sizeof(uint32_t) * 8 * 256);                  // base
+  b += align_up(sizeof(uint32_t) * 8);                        // counters
+  b += align_up(sizeof(uint32_t) * (size_t)npass * nblk * 256);  // status
+  b += align_up(sizeof(K) * (size_t)n);                       // alt keys
+  b += align_up(sizeof(uint32_t) * (size_t)n);                // alt vals
+  return b;
+}
+
+template <typename K>
+void set_sort_smem() {
+  static bool done = false;
+  if (done) return;
+  const int bytes = (int)((sizeof(K) + 4) * kSortTile);
+  cudaFuncSetAttribute(k_onesweep<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_onesweep<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done = true;
+}
+
+// Stable sort of (key, value) by key bits [begin_bit, end_bit).  vin == NULL
+// means values are the input positions.  Output lands in kout/vout.
+template <typename K>
+int radix_sort(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64_t n,
+               int begin_bit, int end_bit, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (n <= 0) return SDGR_OK;
+  const int npass = (end_bit - begin_bit + 7) / 8;
+  if (npass < 1 || npass > 8) return SDGR_ERR_INVALID;
+  if (ws_bytes < radix_ws_bytes<K>(n, npass)) return SDGR_ERR_CAPACITY;
+  set_sort_smem<K>();
+  const int64_t nblk = (n + kSortTile - 1) / kSortTile;
+  char* p = static_cast<char*>(ws);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * 8 * 256);
+  uint32_t* base = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * 8 * 256);
+  uint32_t* ctr = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * 8);
+  uint32_t* status = reinterpret_cast<uint32_t*>(p);
+  const size_t status_bytes = sizeof(uint32_t) * (size_t)npass * nblk * 256;
+  p += align_up(status_bytes);
+  K* kalt = reinterpret_cast<K*>(p); p += align_up(sizeof(K) * (size_t)n);
+  uint32_t* valt = reinterpret_cast<uint32_t*>(p);
+  // hist, base, counters and status are contiguous: one memset
+  if (cudaMemsetAsync(hist, 0, (size_t)((char*)status - (char*)hist) + status_bytes, st) !=
+      cudaSuccess)
+    return SDGR_ERR_CUDA;
+  const int hist_blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_radix_hist<K><<<hist_blocks, 256, 0, st>>>(kin, n, begin_bit, npass, hist);
+  k_radix_hist_scan<<<npass, 256, 0, st>>>(hist, base);
+  note_launch(2);
+  const size_t smem = (sizeof(K) + 4) * kSortTile;
+  const K* ki = kin;
+  const uint32_t* vi = vin;
+  for (int pass = 0; pass < npass; ++pass) {
+    // the last pass must land in kout: alternate so that it does
+    const bool to_out = ((npass - 1 - pass) % 2) == 0;
+    K* ko = to_out ? kout : kalt;
+    uint32_t* vo = to_out ? vout : valt;
+    uint32_t* stat = status + (size_t)pass * nblk * 256;
+    if (pass == 0 && vin == nullptr)
+      k_onesweep<K, true><<<(unsigned)nblk, kSortThreads, smem, st>>>(
+          ki, vi, ko, vo, n, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
+    else
+      k_onesweep<K, false><<<(unsigned)nblk, kSortThreads, smem, st>>>(
+          ki, vi, ko, vo, n, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
+    note_launch();
+    ki = ko;
+    vi = vo;
+  }
+  return check_launch();
+}
+
+template int radix_sort<uint64_t>(const uint64_t*, const uint32_t*, uint64_t*, uint32_t*,
+                                  int64_t, int, int, void*, size_t, cudaStream_t);
+template int radix_sort<uint32_t>(const uint32_t*, const uint32_t*, uint32_t*, uint32_t*,
+                                  int64_t, int, int, void*, size_t, cudaStream_t);
+template size_t radix_ws_bytes<uint64_t>(int64_t, int);
+template size_t radix_ws_bytes<uint32_t>(int64_t, int);
+
+// --------------------------------------------------------------- scan ------
+// Exclusive scan of v(i) = ntiles[order ? order[i] : i] into out[0..n],
+// out[n] = total.  Three phases: tile sums, scan of sums, tile rescans.
+constexpr int kScanTile = 2048;  // 256 threads x 8
+
+struct TileCount {
+  const int32_t* ntiles;
+  const int32_t* order;
+  __device__ __forceinline__ int32_t operator()(int64_t i) const {
+    return ntiles[order ? order[i] : i];
+  }
+};
+
+__device__ __forceinline__ int32_t block_excl_scan(int32_t x, int32_t* tmp, int32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t s = x;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, s, off);
+    if (lane >= off) s += y;
+  }
+  if (lane == 31) tmp[warp] = s;
+  __syncthreads();
+  int32_t pre = 0, tot = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    if (w < warp) pre += tmp[w];
+    tot += tmp[w];
+  }
+  __syncthreads();
+  total = tot;
+  return pre + s - x;
+}
+
+__global__ void __launch_bounds__(256) k_scan_reduce(TileCount f, int64_t n, int32_t* sums) {
+  __shared__ int32_t tmp[8];
+  const int64_t t0 = (int64_t)blockIdx.x * kScanTile;
+  int32_t acc = 0;
+  for (int i = 0; i < 8; ++i) {
+    const int64_t idx = t0 + i * 256 + threadIdx.x;
+    if (idx < n) acc += f(idx);
+  }
+  int32_t total;
+  block_excl_scan(acc, tmp, total);
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums(int32_t* sums, int64_t nb) {
+  __shared__ int32_t tmp[32];
+  int32_t carry = 0;
+  for (int64_t b0 = 0; b0 < nb; b0 += 1024) {
+    const int64_t i = b0 + threadIdx.x;
+    const int32_t v = i < nb ? sums[i] : 0;
+    int32_t total;
+    const int32_t e = block_excl_scan(v, tmp, total);
+    if (i < nb) sums[i] = carry + e;
+    carry += total;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scan_down(TileCount f, int64_t n, const int32_t* sums,
+                                                   int32_t* out) {
+  __shared__ int32_t tmp[8];
+  const int64_t t0 = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 8;  // blocked
+  int32_t v[8];
+  int32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t idx = t0 + i;
+    v[i] = idx < n ? f(idx) : 0;
+    acc += v[i];
+  }
+  int32_t total;
+  int32_t run = sums[blockIdx.x] + block_excl_scan(acc, tmp, total);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t idx = t0 + i;
+    if (idx < n) out[idx] = run;
+    run += v[i];
+    if (idx == n - 1) out[n] = run;
+  }
+}
+
+size_t scan_ws_bytes(int64_t n) { return align_up(sizeof(int32_t) * ((n + kScanTile - 1) / kScanTile + 1)); }
+
+int scan_counts(const int32_t* ntiles, const int32_t* order, int64_t n, int32_t* out, void* ws,
+                cudaStream_t st) {
+  const int64_t nb = (n + kScanTile - 1) / kScanTile;
+  int32_t* sums = static_cast<int32_t*>(ws);
+  TileCount f{ntiles, order};
+  k_scan_reduce<<<(unsigned)nb, 256, 0, st>>>(f, n, sums);
+  k_scan_sums<<<1, 1024, 0, st>>>(sums, nb);
+  k_scan_down<<<(unsigned)nb, 256, 0, st>>>(f, n, sums, out);
+  note_launch(3);
+  return check_launch();
+}
+
+// --------------------------------------------------------- pair emission ----
+// One thread per list position i (rank for the comp plane, index for the
+// imaging plane): emit the member tiles of Gaussian g = order[i] at
+// offsets[i].  Tiles come from the 8x8 tile window bitmask, or for huge
+// footprints from an exact FP64 re-enumeration (same test as k_project).
+__global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t* order,
+                                                    const int32_t* offsets, int64_t n,
+                                                    int tiles_x, double cutoff,
+                                                    uint32_t* keys, uint32_t* vals) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t g = order ? order[i] : (int32_t)i;
+  const int32_t cnt = pl.n_tiles[g];
+  if (cnt == 0) return;
+  int64_t o = offsets[i];
+  const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
+  const int tx0 = bb.x >> 4, tx1 = bb.y >> 4, ty0 = bb.z >> 4, ty1 = bb.w >> 4;
+  if ((tx1 - tx0) < 8 && (ty1 - ty0) < 8) {
+    uint64_t m = pl.tile_mask[g];
+    while (m) {
+      const int b = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      const int tx = tx0 + (b & 7), ty = ty0 + (b >> 3);
+      keys[o] = (uint32_t)(ty * tiles_x + tx);
+      vals[o] = (uint32_t)g;
+      ++o;
+    }
+    return;
+  }
+  const bool dense = !isfinite(cutoff);
+  const double2 uv = reinterpret_cast<const double2*>(pl.uv)[g];
+  const double4 A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
+  const double cut2 = dmul(cutoff, cutoff), a01x2 = dmul(2.0, A.y);
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      bool hit = dense;
+      const int cx0 = max((int)bb.x, tx * kTile), cx1 = min((int)bb.y, tx * kTile + kTile - 1);
+      const int cy0 = max((int)bb.z, ty * kTile), cy1 = min((int)bb.w, ty * kTile + kTile - 1);
+      for (int iv = cy0; iv <= cy1 && !hit; ++iv) {
+        const double dy = dsub((double)iv, uv.y);
+        const double t3 = dmul(A.z, dmul(dy, dy));
+        for (int iu = cx0; iu <= cx1; ++iu) {
+          const double dx = dsub((double)iu, uv.x);
+          const double q = dadd(dadd(dmul(A.x, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
+          if (q <= cut2) { hit = true; break; }
+        }
+      }
+      if (hit) {
+        keys[o] = (uint32_t)(ty * tiles_x + tx);
+        vals[o] = (uint32_t)g;
+        ++o;
+      }
+    }
+}
+
+// tile ranges from the sorted keys: range[t] = [first, last+1)
+__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, int64_t n, int32_t* range) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t k = keys[i];
+  if (i == 0 || keys[i - 1] != k) range[2 * k] = (int32_t)i;
+  if (i == n - 1 || keys[i + 1] != k) range[2 * k + 1] = (int32_t)(i + 1);
+}
+
+// depth-segment work items: each tile list is cut into segments of at most
+// seg_len Gaussians; items are tile-major, segment-minor.
+__global__ void __launch_bounds__(1024) k_make_items(const int32_t* range, int n_tiles, int seg_len,
+                                                     int max_items, int32_t* items,
+                                                     int32_t* tile_first, int32_t* n_items,
+                                                     int32_t* overflow) {
+  __shared__ int32_t tmp[32];
+  int32_t carry = 0;
+  for (int t0 = 0; t0 < n_tiles; t0 += 1024) {
+    const int t = t0 + threadIdx.x;
+    int32_t nseg = 0, s = 0, e = 0;
+    if (t < n_tiles) {
+      s = range[2 * t];
+      e = range[2 * t + 1];
+      nseg = (e - s + seg_len - 1) / seg_len;
+    }
+    int32_t total;
+    const int32_t first = carry + block_excl_scan(nseg, tmp, total);
+    if (t < n_tiles) {
+      tile_first[t] = first;
+      for (int k = 0; k < nseg; ++k) {
+        const int it = first + k;
+        if (it < max_items) {
+          items[4 * it + 0] = t;
+          items[4 * it + 1] = s + k * seg_len;
+          items[4 * it + 2] = min(e, s + (k + 1) * seg_len);
+          items[4 * it + 3] = first;
+        }
+      }
+    }
+    carry += total;
+  }
+  if (threadIdx.x == 0) {
+    *n_items = carry < max_items ? carry : max_items;
+    if (carry > max_items) *overflow = 1;
+  }
+}
+
+int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, const int32_t* order,
+                         const int32_t* offsets, sdgr_tiles& tl, void* ws, size_t ws_bytes,
+                         cudaStream_t st) {
+  const sdgr_plane& pl = tl.plane == 0 ? proj.comp : proj.img;
+  const int64_t n = proj.n, np = tl.n_pairs;
+  if (cudaMemsetAsync(tl.tile_range, 0, sizeof(int32_t) * 2 * (size_t)tl.n_tiles, st) != cudaSuccess)
+    return SDGR_ERR_CUDA;
+  int32_t* overflow = tl.n_items + 1;
+  if (cudaMemsetAsync(tl.n_items, 0, 2 * sizeof(int32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
+  if (np > 0) {
+    char* p = static_cast<char*>(ws);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * np);
+    uint32_t* vals = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * np);
+    const size_t used = (size_t)(p - static_cast<char*>(ws));
+    if (used > ws_bytes) return SDGR_ERR_CAPACITY;
+    k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,
+                                                              view.cutoff, keys, vals);
+    note_launch();
+    int bits = 1;
+    while ((1 << bits) < tl.n_tiles) ++bits;
+    const int rc = radix_sort<uint32_t>(keys, vals, tl.pair_tile,
+                                        reinterpret_cast<uint32_t*>(tl.pair_prim), np, 0, bits, p,
+                                        ws_bytes - used, st);
+    if (rc != SDGR_OK) return rc;
+    k_tile_ranges<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(tl.pair_tile, np, tl.tile_range);
+    note_launch();
+  }
+  k_make_items<<<1, 1024, 0, st>>>(tl.tile_range, tl.n_tiles, tl.seg_len, tl.max_items, tl.items,
+                                   tl.tile_first, tl.n_items, overflow);
+  note_launch();
+  return check_launch();
+}
+
+size_t binning_ws_bytes(int64_t n, int64_t max_pairs) {
+  // depth sort: sorted keys + radix scratch (8 passes of 64-bit keys)
+  const size_t depth = align_up(sizeof(uint64_t) * (size_t)n) + radix_ws_bytes<uint64_t>(n, 8);
+  // pair sort: keys + vals + radix scratch (up to 2 passes of 32-bit keys)
+  const size_t pairs = 2 * align_up(sizeof(uint32_t) * (size_t)max_pairs) +
+                       radix_ws_bytes<uint32_t>(max_pairs, 2);
+  const size_t scan = scan_ws_bytes(n);
+  return std::max(std::max(depth, pairs), scan) + 4096;
+}
+
+int launch_depth_order(const sdgr_projection& proj, int32_t* order, void* ws, size_t ws_bytes,
+                       cudaStream_t st) {
+  const int64_t n = proj.n;
+  uint64_t* ksorted = static_cast<uint64_t*>(ws);
+  const size_t used = align_up(sizeof(uint64_t) * (size_t)n);
+  if (used > ws_bytes) return SDGR_ERR_CAPACITY;
+  return radix_sort<uint64_t>(proj.depth_key, nullptr, ksorted, reinterpret_cast<uint32_t*>(order), n,
+                              0, 64, static_cast<char*>(ws) + used, ws_bytes - used, st);
+}
+
+}  // namespace sdgr

@@ -1,0 +1,151 @@
+// capi.cu — extern "C" entry points of libsdgr (include/sdgr.h).
+//
+// Thin argument checking + dispatch to the stream-ordered launchers.  No
+// host synchronisation, no allocation, no C++ exceptions across the ABI.
+#include <atomic>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace sdgr {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+int check_launch() { return cudaPeekAtLastError() == cudaSuccess ? SDGR_OK : SDGR_ERR_CUDA; }
+
+int launch_project(const sdgr_scene&, const sdgr_view&, sdgr_projection&, cudaStream_t);
+int launch_depth_order(const sdgr_projection&, int32_t*, void*, size_t, cudaStream_t);
+int scan_counts(const int32_t*, const int32_t*, int64_t, int32_t*, void*, cudaStream_t);
+size_t scan_ws_bytes(int64_t);
+size_t binning_ws_bytes(int64_t, int64_t);
+int launch_emit_and_sort(const sdgr_projection&, const sdgr_view&, const int32_t*, const int32_t*,
+                         sdgr_tiles&, void*, size_t, cudaStream_t);
+int launch_composite_forward(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, double,
+                             double*, double*, float*, int32_t*, cudaStream_t);
+int launch_splat(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, const float*, double*,
+                 float*, cudaStream_t);
+int launch_grad_image(const sdgr_view&, const sdgr_projection&, const float*, const float*, float*,
+                      cudaStream_t);
+int launch_grad_intensity(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, double,
+                          const double*, const float*, double*, double*, float*, cudaStream_t);
+int launch_grad_geometry(const sdgr_scene&, const sdgr_view&, const sdgr_projection&, const float*,
+                         const float*, const sdgr_grads&, int, cudaStream_t);
+
+static bool view_ok(const sdgr_view* v) {
+  if (!v) return false;
+  if (v->n_u < 1 || v->n_v < 1 || v->n_az < 1 || v->n_rg < 1) return false;
+  if (v->n_u > SDGR_MAX_PLANE || v->n_v > SDGR_MAX_PLANE || v->n_az > SDGR_MAX_PLANE ||
+      v->n_rg > SDGR_MAX_PLANE)
+    return false;
+  if (std::isnan(v->cutoff) || v->cutoff < 0) return false;
+  return true;
+}
+
+static bool tiles_ok(const sdgr_tiles* t) {
+  return t && t->n_tiles >= 1 && t->tiles_x >= 1 && t->seg_len >= 1 && t->max_items >= 1 &&
+         t->tile_range && t->items && t->tile_first && t->n_items;
+}
+
+}  // namespace sdgr
+
+using namespace sdgr;
+
+extern "C" {
+
+int sdgr_version(void) { return SDGR_ABI_VERSION; }
+
+const char* sdgr_status_string(int s) {
+  switch (s) {
+    case SDGR_OK: return "ok";
+    case SDGR_ERR_INVALID: return "invalid parameter";
+    case SDGR_ERR_NUMERICAL: return "non-finite value";
+    case SDGR_ERR_STATE: return "invalid state";
+    case SDGR_ERR_CUDA: return cudaGetErrorString(cudaGetLastError());
+    case SDGR_ERR_CAPACITY: return "buffer capacity exceeded";
+    default: return "unknown status";
+  }
+}
+
+uint64_t sdgr_launch_count(void) { return g_launches.load(); }
+
+size_t sdgr_workspace_bytes(int64_t n, int64_t max_pairs) {
+  return binning_ws_bytes(n < 1 ? 1 : n, max_pairs < 1 ? 1 : max_pairs);
+}
+
+int sdgr_project(const sdgr_scene* scene, const sdgr_view* view, sdgr_projection* proj, void* stream) {
+  if (!scene || !proj || !view_ok(view)) return SDGR_ERR_INVALID;
+  if (scene->n < 1 || proj->n != scene->n) return SDGR_ERR_INVALID;
+  if (scene->dtype != 0 && scene->dtype != 1) return SDGR_ERR_INVALID;
+  return launch_project(*scene, *view, *proj, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_depth_order(const sdgr_projection* proj, int32_t* order, void* ws, size_t ws_bytes,
+                     void* stream) {
+  if (!proj || !order || !ws || proj->n < 1) return SDGR_ERR_INVALID;
+  return launch_depth_order(*proj, order, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_count_pairs(const sdgr_projection* proj, int32_t plane, const int32_t* order,
+                     int32_t* offsets, void* ws, size_t ws_bytes, void* stream) {
+  if (!proj || !offsets || !ws || proj->n < 1 || (plane != 0 && plane != 1)) return SDGR_ERR_INVALID;
+  if (ws_bytes < scan_ws_bytes(proj->n)) return SDGR_ERR_CAPACITY;
+  const sdgr_plane& pl = plane == 0 ? proj->comp : proj->img;
+  return scan_counts(pl.n_tiles, order, proj->n, offsets, ws, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_bin_pairs(const sdgr_projection* proj, const sdgr_view* view, const int32_t* order,
+                   const int32_t* offsets, sdgr_tiles* tiles, void* ws, size_t ws_bytes,
+                   void* stream) {
+  if (!proj || !view_ok(view) || !offsets || !tiles_ok(tiles) || !ws) return SDGR_ERR_INVALID;
+  if (tiles->plane == 0 && !order) return SDGR_ERR_INVALID;
+  if (tiles->n_pairs > 0 && (!tiles->pair_tile || !tiles->pair_prim)) return SDGR_ERR_INVALID;
+  if (tiles->n_pairs > 0x7fffffffLL) return SDGR_ERR_CAPACITY;
+  return launch_emit_and_sort(*proj, *view, tiles->plane == 0 ? order : nullptr, offsets, *tiles, ws,
+                              ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_composite_forward(const sdgr_view* view, const sdgr_projection* proj, const sdgr_tiles* comp,
+                           double s_stop, double* seg_sum, double* seg_base, float* intensity,
+                           int32_t* status, void* stream) {
+  if (!view_ok(view) || !proj || !tiles_ok(comp) || comp->plane != 0 || !intensity || !status)
+    return SDGR_ERR_INVALID;
+  if (comp->n_pairs > 0 && (!seg_sum || !seg_base)) return SDGR_ERR_INVALID;
+  if (std::isnan(s_stop)) return SDGR_ERR_INVALID;
+  return launch_composite_forward(*view, *proj, *comp, s_stop, seg_sum, seg_base, intensity, status,
+                                  static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_splat(const sdgr_view* view, const sdgr_projection* proj, const sdgr_tiles* img,
+               const float* intensity, double* part, float* image, void* stream) {
+  if (!view_ok(view) || !proj || !tiles_ok(img) || img->plane != 1 || !intensity || !image)
+    return SDGR_ERR_INVALID;
+  if (img->n_pairs > 0 && !part) return SDGR_ERR_INVALID;
+  return launch_splat(*view, *proj, *img, intensity, part, image, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_grad_image(const sdgr_view* view, const sdgr_projection* proj, const float* intensity,
+                    const float* dL_dS, float* acc_img, void* stream) {
+  if (!view_ok(view) || !proj || !intensity || !dL_dS || !acc_img) return SDGR_ERR_INVALID;
+  return launch_grad_image(*view, *proj, intensity, dL_dS, acc_img, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_grad_intensity(const sdgr_view* view, const sdgr_projection* proj, const sdgr_tiles* comp,
+                        double s_stop, const double* seg_base, const float* dL_dI, double* seg_g,
+                        double* seg_d, float* acc_comp, void* stream) {
+  if (!view_ok(view) || !proj || !tiles_ok(comp) || comp->plane != 0 || !dL_dI || !acc_comp)
+    return SDGR_ERR_INVALID;
+  if (comp->n_pairs > 0 && (!seg_base || !seg_g || !seg_d)) return SDGR_ERR_INVALID;
+  return launch_grad_intensity(*view, *proj, *comp, s_stop, seg_base, dL_dI, seg_g, seg_d, acc_comp,
+                               static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_grad_geometry(const sdgr_scene* scene, const sdgr_view* view, const sdgr_projection* proj,
+                       const float* acc_img, const float* acc_comp, sdgr_grads* out, int accumulate,
+                       void* stream) {
+  if (!scene || !view_ok(view) || !proj || !acc_img || !acc_comp || !out) return SDGR_ERR_INVALID;
+  if (scene->n != proj->n) return SDGR_ERR_STATE;
+  return launch_grad_geometry(*scene, *view, *proj, acc_img, acc_comp, *out, accumulate,
+                              static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

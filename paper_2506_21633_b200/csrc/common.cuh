@@ -1,0 +1,98 @@
+// common.cuh — shared device helpers for the SDGR sm_100a kernels.
+//
+// The FP64 "key chain" (everything that decides which (cell, Gaussian) pairs
+// exist and in which order) is written with explicit round-to-nearest
+// intrinsics so nvcc can neither contract nor reassociate it.  The op order
+// follows the reference exactly as measured on its host:
+//   x_r = fma(p2, R2, fma(p1, R1, p0*R0)) + T   (OpenBLAS dgemm, geometry.py:249)
+//   Sigma = M M^T with the same FMA chain         (scene.py:96)
+//   mc Sigma mc^T summed sequentially over (b,c)  (np.einsum, geometry.py:271)
+// and is mirrored bit-for-bit by the C oracle (oracle/keychain.c).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/sdgr.h"
+
+namespace sdgr {
+
+constexpr int kTile = SDGR_TILE;        // 16
+constexpr int kRays = SDGR_TILE_RAYS;   // 256 rays (cells) per tile
+constexpr int kChunk = 256;             // Gaussians staged per tile-walk chunk
+
+// ---- explicit-rounding FP64 helpers (no contraction) -----------------------
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+
+// np.maximum(x, 0.0): NaN propagates (fmax would drop it).
+__device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
+
+// Deterministic FP64 exp shared with the oracle (oracle/keychain.c:sdgr_exp).
+// Cody-Waite reduction by ln2, degree-13 Taylor polynomial in Horner/FMA
+// form, exact power-of-two scaling.  <= ~0.75 ulp; identical bits on host and
+// device because every step is a single IEEE operation.
+__device__ __forceinline__ double sdgr_exp(double x) {
+  if (!(x == x)) return x;
+  if (x > 709.782712893384) return __longlong_as_double(0x7ff0000000000000ll);
+  if (x < -745.1332191019412) return 0.0;
+  const double kInvLn2 = 1.4426950408889634;
+  const double kLn2Hi = 6.93147180369123816490e-01;
+  const double kLn2Lo = 1.90821492927058770002e-10;
+  double n = rint(dmul(x, kInvLn2));
+  double r = dfma(-n, kLn2Hi, x);
+  r = dfma(-n, kLn2Lo, r);
+  double p = 1.0 / 6227020800.0;          // 1/13!
+  p = dfma(p, r, 1.0 / 479001600.0);      // 1/12!
+  p = dfma(p, r, 1.0 / 39916800.0);
+  p = dfma(p, r, 1.0 / 3628800.0);
+  p = dfma(p, r, 1.0 / 362880.0);
+  p = dfma(p, r, 1.0 / 40320.0);
+  p = dfma(p, r, 1.0 / 5040.0);
+  p = dfma(p, r, 1.0 / 720.0);
+  p = dfma(p, r, 1.0 / 120.0);
+  p = dfma(p, r, 1.0 / 24.0);
+  p = dfma(p, r, 1.0 / 6.0);
+  p = dfma(p, r, 0.5);
+  double r2 = dmul(r, r);
+  double t = dfma(r2, p, r);
+  double e = dadd(1.0, t);
+  return scalbn(e, (int)n);
+}
+
+// Order-preserving uint64 key of an FP64 depth (-0.0 canonicalised to +0.0 so
+// that ties fall back to the index, as np.lexsort compares -0.0 == 0.0).
+__device__ __forceinline__ uint64_t depth_key(double d) {
+  if (d == 0.0) d = 0.0;
+  uint64_t b = (uint64_t)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// Mahalanobis form in the reference's op order (forward.py:101-105):
+//   q = a00*dx^2 + (2*a01)*dx*dy + a11*dy^2, left to right, no FMA.
+__device__ __forceinline__ double quadform(double a00, double a01, double a11,
+                                           double dx, double dy) {
+  double t1 = dmul(a00, dmul(dx, dx));
+  double t2 = dmul(dmul(dmul(2.0, a01), dx), dy);
+  double t3 = dmul(a11, dmul(dy, dy));
+  return dadd(dadd(t1, t2), t3);
+}
+
+__device__ __forceinline__ float softplusf64(double x) {
+  // np.logaddexp(0, x) = max(x,0) + log1p(exp(-|x|))  (scene.py:22-25)
+  double ax = fabs(x);
+  return (float)(fmax(x, 0.0) + log1p(exp(-ax)));
+}
+
+// Launch accounting (sdgr_launch_count).
+void note_launch(int n = 1);
+int check_launch();  // returns SDGR_OK or SDGR_ERR_CUDA after a launch
+
+template <typename T>
+__device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
+
+}  // namespace sdgr

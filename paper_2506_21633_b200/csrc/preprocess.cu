@@ -1,0 +1,299 @@
+// preprocess.cu — K1: one thread per Gaussian projects it onto both planes.
+//
+// Replaces geometry.project_all (geometry.py:233-340) plus the per-Gaussian
+// half of forward._footprint_pairs (forward.py:60-109): the clipped cell
+// bbox, the exact membership test of every bbox cell (q <= cutoff^2) and the
+// set of 16x16 tiles that hold at least one member cell.  Membership is
+// decided once here, in FP64 with the reference's op order, and stored as an
+// 8x8 cell bit-window so no later kernel repeats FP64 work for small
+// footprints.
+#include "common.cuh"
+
+namespace sdgr {
+
+// Real SH basis degrees 0-3 in the reference's (non-3DGS) ordering and
+// signs (sh.py:15-65): Y1 = C1*(y, z, x).
+__device__ __forceinline__ void sh_basis(double x, double y, double z, double* b) {
+  const double C0 = 0.28209479177387814, C1 = 0.4886025119029199;
+  const double C20 = 1.0925484305920792, C21 = 0.31539156525252005, C22 = 0.5462742152960396;
+  const double C30 = 0.5900435899266435, C31 = 2.890611442640554, C32 = 0.4570457994644658,
+               C33 = 0.3731763325901154, C34 = 1.445305721320277;
+  double xx = x * x, yy = y * y, zz = z * z;
+  b[0] = C0;
+  b[1] = C1 * y;
+  b[2] = C1 * z;
+  b[3] = C1 * x;
+  b[4] = C20 * x * y;
+  b[5] = C20 * y * z;
+  b[6] = C21 * (2.0 * zz - xx - yy);
+  b[7] = C20 * x * z;
+  b[8] = C22 * (xx - yy);
+  b[9] = C30 * y * (3.0 * xx - yy);
+  b[10] = C31 * x * y * z;
+  b[11] = C32 * y * (4.0 * zz - xx - yy);
+  b[12] = C33 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+  b[13] = C32 * x * (4.0 * zz - xx - yy);
+  b[14] = C34 * z * (xx - yy);
+  b[15] = C30 * x * (xx - 3.0 * yy);
+}
+
+template <typename T>
+__device__ __forceinline__ double ld(const T* p, int64_t i) { return (double)__ldg(p + i); }
+
+// Footprint of one plane: inverse covariance, clipped bbox, member masks.
+// Writes the plane records for Gaussian g.  (forward.py:33-42, 60-109)
+__device__ void plane_footprint(const sdgr_plane& pl, int64_t g, double u, double v,
+                                double c00, double c01, double c11, int nu, int nv,
+                                double cutoff, bool dense) {
+  // invert_cov2d (forward.py:33-42)
+  double det = dsub(dmul(c00, c11), dmul(c01, c01));
+  double a00 = ddiv(c11, det), a01 = ddiv(-c01, det), a11 = ddiv(c00, det);
+  reinterpret_cast<double2*>(pl.uv)[g] = make_double2(u, v);
+  reinterpret_cast<double4*>(pl.inv_cov)[g] = make_double4(a00, a01, a11, 0.0);
+  if (pl.cov) reinterpret_cast<double4*>(pl.cov)[g] = make_double4(c00, c01, c11, 0.0);
+
+  int x0, x1, y0, y1;
+  if (!dense) {
+    double ru = dmul(cutoff, dsqrt(np_max0(c00)));
+    double rv = dmul(cutoff, dsqrt(np_max0(c11)));
+    double fx0 = fmax(ceil(dsub(u, ru)), 0.0);
+    double fx1 = fmin(floor(dadd(u, ru)), (double)nu - 1.0);
+    double fy0 = fmax(ceil(dsub(v, rv)), 0.0);
+    double fy1 = fmin(floor(dadd(v, rv)), (double)nv - 1.0);
+    // visible Gaussians have finite u, r; clamp into int16 range safely
+    fx0 = fmin(fx0, 32767.0); fy0 = fmin(fy0, 32767.0);
+    fx1 = fmax(fx1, -32768.0); fy1 = fmax(fy1, -32768.0);
+    x0 = (int)fx0; x1 = (int)fx1; y0 = (int)fy0; y1 = (int)fy1;
+  } else {
+    x0 = 0; x1 = nu - 1; y0 = 0; y1 = nv - 1;
+  }
+  uint64_t cmask = 0, tmask = 0;
+  int ntiles = 0;
+  if (x0 <= x1 && y0 <= y1) {
+    const int tx0 = x0 >> 4, ty0 = y0 >> 4, tx1 = x1 >> 4, ty1 = y1 >> 4;
+    const bool small = (x1 - x0) < 8 && (y1 - y0) < 8;
+    const bool tsmall = (tx1 - tx0) < 8 && (ty1 - ty0) < 8;
+    const double cut2 = dmul(cutoff, cutoff);
+    if (small) {
+      const double a01x2 = dmul(2.0, a01);
+      for (int iv = y0; iv <= y1; ++iv) {
+        const double dy = dsub((double)iv, v);
+        const double t3 = dmul(a11, dmul(dy, dy));
+        for (int iu = x0; iu <= x1; ++iu) {
+          const double dx = dsub((double)iu, u);
+          const double q = dadd(dadd(dmul(a00, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
+          if (dense || q <= cut2) {
+            cmask |= 1ull << ((iv - y0) * 8 + (iu - x0));
+            tmask |= 1ull << (((iv >> 4) - ty0) * 8 + ((iu >> 4) - tx0));
+          }
+        }
+      }
+      ntiles = __popcll(tmask);
+    } else if (dense) {
+      ntiles = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+      if (tsmall)
+        for (int ty = ty0; ty <= ty1; ++ty)
+          for (int tx = tx0; tx <= tx1; ++tx) tmask |= 1ull << ((ty - ty0) * 8 + (tx - tx0));
+    } else {
+      // large footprint: per tile, stop at the first member cell
+      const double a01x2 = dmul(2.0, a01);
+      for (int ty = ty0; ty <= ty1; ++ty) {
+        for (int tx = tx0; tx <= tx1; ++tx) {
+          const int cx0 = max(x0, tx * kTile), cx1 = min(x1, tx * kTile + kTile - 1);
+          const int cy0 = max(y0, ty * kTile), cy1 = min(y1, ty * kTile + kTile - 1);
+          bool hit = false;
+          for (int iv = cy0; iv <= cy1 && !hit; ++iv) {
+            const double dy = dsub((double)iv, v);
+            const double t3 = dmul(a11, dmul(dy, dy));
+            for (int iu = cx0; iu <= cx1; ++iu) {
+              const double dx = dsub((double)iu, u);
+              const double q = dadd(dadd(dmul(a00, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
+              if (q <= cut2) { hit = true; break; }
+            }
+          }
+          if (hit) {
+            ++ntiles;
+            if (tsmall) tmask |= 1ull << ((ty - ty0) * 8 + (tx - tx0));
+          }
+        }
+      }
+    }
+  }
+  reinterpret_cast<short4*>(pl.bbox)[g] = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
+  pl.cell_mask[g] = cmask;
+  pl.tile_mask[g] = tmask;
+  pl.n_tiles[g] = ntiles;
+}
+
+__device__ void plane_empty(const sdgr_plane& pl, int64_t g) {
+  reinterpret_cast<short4*>(pl.bbox)[g] = make_short4(1, 0, 1, 0);
+  pl.cell_mask[g] = 0;
+  pl.tile_mask[g] = 0;
+  pl.n_tiles[g] = 0;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_project(sdgr_scene scene, sdgr_view view,
+                                                 sdgr_projection proj) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int n_vis = 0, n_skip = 0, n_cull = 0;
+  if (g < scene.n) {
+    const T* P = static_cast<const T*>(scene.positions);
+    const T* Q = static_cast<const T*>(scene.rotations);
+    const T* L = static_cast<const T*>(scene.log_scales);
+    const double p0 = ld(P, 3 * g), p1 = ld(P, 3 * g + 1), p2 = ld(P, 3 * g + 2);
+    const double* R = view.R;
+    // x_r = positions @ R.T + T  (geometry.py:249; OpenBLAS FMA chain)
+    double xr[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      xr[i] = dadd(dfma(p2, R[3 * i + 2], dfma(p1, R[3 * i + 1], dmul(p0, R[3 * i]))), view.T[i]);
+    // plane coordinates (geometry.py:78-105) and ndc_to_pixel (:73-75)
+    const double undc = ddiv(dmul(2.0, xr[0]), view.den_u);
+    const double vcndc = ddiv(dmul(2.0, xr[1]), view.den_v);
+    const double vindc = dsub(ddiv(dmul(2.0, xr[2]), view.den_v), view.off_vi);
+    const double uc = dsub(dmul(dmul(dadd(undc, 1.0), 0.5), (double)view.n_u), 0.5);
+    const double vc = dsub(dmul(dmul(dadd(vcndc, 1.0), 0.5), (double)view.n_v), 0.5);
+    const double ui = dsub(dmul(dmul(dadd(undc, 1.0), 0.5), (double)view.n_az), 0.5);
+    const double vi = dsub(dmul(dmul(dadd(vindc, 1.0), 0.5), (double)view.n_rg), 0.5);
+    const double depth = xr[2];
+
+    // covariance R(q) diag(e^s)^2 R(q)^T  (scene.py:49-97)
+    double q[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = ld(Q, 4 * g + k);
+    const double nrm = dsqrt(dadd(dadd(dadd(dmul(q[0], q[0]), dmul(q[1], q[1])), dmul(q[2], q[2])),
+                                  dmul(q[3], q[3])));
+    const double w = ddiv(q[0], nrm), x = ddiv(q[1], nrm), y = ddiv(q[2], nrm), z = ddiv(q[3], nrm);
+    double Rq[9];
+    Rq[0] = dsub(1.0, dmul(2.0, dadd(dmul(y, y), dmul(z, z))));
+    Rq[1] = dmul(2.0, dsub(dmul(x, y), dmul(w, z)));
+    Rq[2] = dmul(2.0, dadd(dmul(x, z), dmul(w, y)));
+    Rq[3] = dmul(2.0, dadd(dmul(x, y), dmul(w, z)));
+    Rq[4] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(z, z))));
+    Rq[5] = dmul(2.0, dsub(dmul(y, z), dmul(w, x)));
+    Rq[6] = dmul(2.0, dsub(dmul(x, z), dmul(w, y)));
+    Rq[7] = dmul(2.0, dadd(dmul(y, z), dmul(w, x)));
+    Rq[8] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(y, y))));
+    double s[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) s[j] = sdgr_exp(ld(L, 3 * g + j));
+    double M[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) M[3 * i + j] = dmul(Rq[3 * i + j], s[j]);
+    double C[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        C[3 * i + j] = dfma(M[3 * i + 2], M[3 * j + 2],
+                            dfma(M[3 * i + 1], M[3 * j + 1], dmul(M[3 * i], M[3 * j])));
+    // sandwich mc C mc^T (geometry.py:269-278): sequential over (b, c)
+    double cc[4], ci[4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        double accc = 0.0, acci = 0.0;
+        bool first = true;
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double tc = dmul(dmul(view.mc[3 * a + b], C[3 * b + c]), view.mc[3 * d + c]);
+            const double ti = dmul(dmul(view.mi[3 * a + b], C[3 * b + c]), view.mi[3 * d + c]);
+            accc = first ? tc : dadd(accc, tc);
+            acci = first ? ti : dadd(acci, ti);
+            first = false;
+          }
+        cc[2 * a + d] = accc;
+        ci[2 * a + d] = acci;
+      }
+    const double cc00 = dadd(cc[0], view.cov_reg), cc11 = dadd(cc[3], view.cov_reg);
+    const double cc01 = dmul(0.5, dadd(cc[1], cc[2]));
+    const double ci00 = dadd(ci[0], view.cov_reg), ci11 = dadd(ci[3], view.cov_reg);
+    const double ci01 = dmul(0.5, dadd(ci[1], ci[2]));
+    const double detc = dsub(dmul(cc00, cc11), dmul(cc01, cc01));
+    const double deti = dsub(dmul(ci00, ci11), dmul(ci01, ci01));
+    const bool finite = isfinite(uc) && isfinite(vc) && isfinite(ui) && isfinite(vi) &&
+                        isfinite(depth) && isfinite(detc) && isfinite(deti);
+    const bool ok = finite && detc > 0.0 && deti > 0.0;
+    const bool dense = !isfinite(view.cutoff);
+    bool inside = true;
+    if (!dense) {
+      // frustum cull (geometry.py:293-305)
+      const double ru = dmul(view.cutoff, dsqrt(np_max0(cc00)));
+      const double rv = dmul(view.cutoff, dsqrt(np_max0(cc11)));
+      inside = (dadd(uc, ru) >= 0.0) && (dsub(uc, ru) <= (double)view.n_u - 1.0) &&
+               (dadd(vc, rv) >= 0.0) && (dsub(vc, rv) <= (double)view.n_v - 1.0);
+    }
+    const bool vis = ok && inside;
+    n_vis = vis; n_skip = !ok; n_cull = ok && !inside;
+    proj.flags[g] = (uint8_t)((vis ? SDGR_FLAG_VISIBLE : 0) | (!ok ? SDGR_FLAG_SKIPPED : 0) |
+                              ((ok && !inside) ? SDGR_FLAG_CULLED : 0));
+    if (vis) {
+      plane_footprint(proj.comp, g, uc, vc, cc00, cc01, cc11, view.n_u, view.n_v, view.cutoff, dense);
+      plane_footprint(proj.img, g, ui, vi, ci00, ci01, ci11, view.n_az, view.n_rg, view.cutoff, dense);
+      proj.depth_key[g] = depth_key(depth);
+      // phase function and extinction (geometry.py:308-317)
+      const double r0 = p0 - view.cam[0], r1 = p1 - view.cam[1], r2 = p2 - view.cam[2];
+      double dist = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
+      if (dist == 0.0) dist = 1.0;
+      const double d0 = r0 / dist, d1 = r1 / dist, d2 = r2 / dist;
+      double b[16];
+      sh_basis(d0, d1, d2, b);
+      const T* S = static_cast<const T*>(scene.sh_coeffs);
+      double praw = 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) praw += b[k] * ld(S, 16 * g + k);
+      const T* K = static_cast<const T*>(scene.ke_raw);
+      const float kf = softplusf64(ld(K, 2 * g)), kb = softplusf64(ld(K, 2 * g + 1));
+      proj.kappa[g] = kf + kb;
+      proj.phase[g] = (float)fmax(praw, 0.0);
+      proj.phase_raw[g] = (float)praw;
+      if (!(praw == praw)) proj.phase[g] = (float)praw;  // NaN propagates (np.maximum)
+      if (proj.ke_act) reinterpret_cast<float2*>(proj.ke_act)[g] = make_float2(kf, kb);
+      if (proj.look) reinterpret_cast<double4*>(proj.look)[g] = make_double4(d0, d1, d2, dist);
+    } else {
+      plane_empty(proj.comp, g);
+      plane_empty(proj.img, g);
+      proj.depth_key[g] = ~0ull;
+      proj.kappa[g] = 0.f;
+      proj.phase[g] = 0.f;
+      proj.phase_raw[g] = 0.f;
+      // accessor arrays keep the raw projection for non-visible rows too
+      reinterpret_cast<double2*>(proj.comp.uv)[g] = make_double2(uc, vc);
+      reinterpret_cast<double2*>(proj.img.uv)[g] = make_double2(ui, vi);
+      if (proj.comp.cov) reinterpret_cast<double4*>(proj.comp.cov)[g] = make_double4(cc00, cc01, cc11, 0.0);
+      if (proj.img.cov) reinterpret_cast<double4*>(proj.img.cov)[g] = make_double4(ci00, ci01, ci11, 0.0);
+    }
+  }
+  // block-aggregated counters
+  n_vis = __syncthreads_count(n_vis);
+  n_skip = __syncthreads_count(n_skip);
+  n_cull = __syncthreads_count(n_cull);
+  if (threadIdx.x == 0) {
+    if (n_vis) atomicAdd(proj.counters + 0, n_vis);
+    if (n_skip) atomicAdd(proj.counters + 1, n_skip);
+    if (n_cull) atomicAdd(proj.counters + 2, n_cull);
+  }
+}
+
+int launch_project(const sdgr_scene& scene, const sdgr_view& view, sdgr_projection& proj,
+                   cudaStream_t stream) {
+  if (scene.n <= 0) return SDGR_ERR_INVALID;
+  if (cudaMemsetAsync(proj.counters, 0, 4 * sizeof(int32_t), stream) != cudaSuccess)
+    return SDGR_ERR_CUDA;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
+  if (scene.dtype == 0)
+    k_project<float><<<blocks, threads, 0, stream>>>(scene, view, proj);
+  else
+    k_project<double><<<blocks, threads, 0, stream>>>(scene, view, proj);
+  note_launch();
+  return check_launch();
+}
+
+}  // namespace sdgr

@@ -1,0 +1,613 @@
+"""SDGR forward + custom backward on B200: the drop-in for sarsplat's hot path.
+
+Public functions keep the reference's names, signatures and error
+behaviour (forward.py:138-285, backward.py:86-290):
+
+    render(scene, config, cov_reg=0.3, cutoff=3.0)           -> image
+    render_forward(scene, config, cov_reg=0.3, cutoff=3.0)   -> ForwardResult
+    backward(fwd, dL_dS)                                     -> SceneGradients
+    project_all / build_ray_lists / build_splat_lists /
+    compute_intensities / splat_image / grad_image_stage /
+    grad_intensity_stage / grad_geometry_stage               (stage functions)
+
+Every stage is a libsdgr call (include/sdgr.h) on the current torch CUDA
+stream; torch only provides device memory.  There is no CPU path: without a
+GPU or without libsdgr.so these functions raise.
+
+Host scenes (numpy, like the reference's) are uploaded as float64 and the
+results come back as numpy float64 arrays, so existing callers work
+unchanged.  DeviceScene inputs stay on the device and results are CUDA
+tensors (float32).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ptr
+from .errors import DeviceError, InvalidParameterError, NumericalError, StateError
+from .radar import n_rays, radar_rotation, view_constants
+from .scene import GROUPS, DeviceScene, as_device_scene
+
+DEFAULT_COV_REG = 0.3
+DEFAULT_CUTOFF = 3.0
+# Rays stop once their log-transmittance exceeds S_STOP: later pairs would
+# contribute < e^-40 * P ~ 4e-18 * P.  float("inf") = the reference's
+# exhaustive walk (bit-for-bit the same list traversal).
+S_STOP = 40.0
+TILE = _lib.TILE
+SMS_TARGET_ITEMS = 148 * 4
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _check(rc: int, what: str) -> None:
+    if rc == _lib.OK:
+        return
+    msg = _lib.lib().sdgr_status_string(rc).decode()
+    if rc == _lib.ERR_INVALID:
+        raise InvalidParameterError(f"{what}: {msg}")
+    if rc == _lib.ERR_NUMERICAL:
+        raise NumericalError(f"{what}: {msg}")
+    if rc == _lib.ERR_STATE:
+        raise StateError(f"{what}: {msg}")
+    raise DeviceError(f"{what}: {msg} (status {rc})")
+
+
+def _empty(shape, dtype, device):
+    return torch.empty(shape, dtype=dtype, device=device)
+
+
+def _scene_desc(ds: DeviceScene) -> _lib.SceneDesc:
+    d = _lib.SceneDesc()
+    d.n = len(ds)
+    d.dtype = 0 if ds.dtype == torch.float32 else 1
+    d.positions, d.rotations, d.log_scales, d.sh_coeffs, d.ke_raw = (ptr(t) for t in ds.arrays())
+    return d
+
+
+# ----------------------------------------------------------------------------
+# projection (K1)
+# ----------------------------------------------------------------------------
+class _PlaneRecords:
+    def __init__(self, n, device, with_cov):
+        self.uv = _empty((n, 2), torch.float64, device)
+        self.inv_cov = _empty((n, 4), torch.float64, device)
+        self.cov = _empty((n, 4), torch.float64, device) if with_cov else None
+        self.bbox = _empty((n, 4), torch.int16, device)
+        self.cell_mask = _empty((n,), torch.int64, device)
+        self.tile_mask = _empty((n,), torch.int64, device)
+        self.n_tiles = _empty((n,), torch.int32, device)
+
+    def desc(self) -> _lib.Plane:
+        p = _lib.Plane()
+        for f, _ in _lib.Plane._fields_:
+            setattr(p, f, ptr(getattr(self, f)))
+        return p
+
+
+class Projection:
+    """Device projection of one scene into one view (geometry.py:185-230).
+
+    Records are N-sized in scene order; the reference's compacted views
+    (``indices``, ``uv_comp``, ...) are exposed as properties that gather the
+    visible rows on demand.
+    """
+
+    def __init__(self, n: int, device, config, cov_reg: float, cutoff: float, accessors: bool):
+        self.n_scene = n
+        self.config = config
+        self.cov_reg = cov_reg
+        self.cutoff = cutoff
+        self.view = view_constants(config, cov_reg, cutoff)
+        self.comp = _PlaneRecords(n, device, accessors)
+        self.img = _PlaneRecords(n, device, accessors)
+        self.depth_key = _empty((n,), torch.int64, device)
+        self.kappa = _empty((n,), torch.float32, device)
+        self.phase_f = _empty((n,), torch.float32, device)
+        self.phase_raw = _empty((n,), torch.float32, device)
+        self.flags = _empty((n,), torch.uint8, device)
+        self.counters = torch.zeros((4,), dtype=torch.int32, device=device)
+        self.ke_act = _empty((n, 2), torch.float32, device) if accessors else None
+        self.look = _empty((n, 4), torch.float64, device) if accessors else None
+        self._vis_idx = None
+        self._counts = None
+
+    def desc(self) -> _lib.ProjectionDesc:
+        d = _lib.ProjectionDesc()
+        d.n = self.n_scene
+        d.comp = self.comp.desc()
+        d.img = self.img.desc()
+        d.depth_key, d.kappa, d.phase, d.phase_raw = (
+            ptr(self.depth_key), ptr(self.kappa), ptr(self.phase_f), ptr(self.phase_raw))
+        d.flags, d.counters, d.ke_act, d.look = ptr(self.flags), ptr(self.counters), ptr(self.ke_act), ptr(self.look)
+        return d
+
+    # -- reference-shaped accessors (compacted to the K visible rows) -------
+    @property
+    def visible(self) -> torch.Tensor:
+        return (self.flags & _lib.FLAG_VISIBLE) != 0
+
+    @property
+    def indices(self) -> torch.Tensor:
+        if self._vis_idx is None:
+            self._vis_idx = torch.nonzero(self.visible).flatten()
+        return self._vis_idx
+
+    def __len__(self) -> int:
+        return int(self.indices.numel())
+
+    def _counts_host(self):
+        if self._counts is None:
+            self._counts = self.counters.cpu().tolist()
+        return self._counts
+
+    @property
+    def n_culled(self) -> int:
+        return int(self._counts_host()[2])
+
+    @property
+    def n_skipped(self) -> int:
+        return int(self._counts_host()[1])
+
+    @property
+    def uv_comp(self):
+        return self.comp.uv[self.indices]
+
+    @property
+    def uv_img(self):
+        return self.img.uv[self.indices]
+
+    @property
+    def depth(self):
+        return decode_depth(self.depth_key[self.indices])
+
+    def _cov(self, pl):
+        if pl.cov is None:
+            raise StateError("projection was built without covariance accessors")
+        c = pl.cov[self.indices]
+        return torch.stack([torch.stack([c[:, 0], c[:, 1]], -1), torch.stack([c[:, 1], c[:, 2]], -1)], -2)
+
+    @property
+    def cov_comp(self):
+        return self._cov(self.comp)
+
+    @property
+    def cov_img(self):
+        return self._cov(self.img)
+
+    @property
+    def phase(self):
+        return self.phase_f[self.indices]
+
+    @property
+    def phase_unclamped(self):
+        return self.phase_raw[self.indices]
+
+    @property
+    def ke_sum(self):
+        return self.kappa[self.indices]
+
+    @property
+    def ke_fwd(self):
+        return self.ke_act[self.indices, 0]
+
+    @property
+    def ke_bwd(self):
+        return self.ke_act[self.indices, 1]
+
+    @property
+    def look_dirs(self):
+        return self.look[self.indices, :3]
+
+    @property
+    def look_dists(self):
+        return self.look[self.indices, 3]
+
+    @property
+    def rotation(self) -> np.ndarray:
+        return radar_rotation(self.config.azimuth_deg, self.config.elevation_deg)
+
+
+def decode_depth(key: torch.Tensor) -> torch.Tensor:
+    """Inverse of the device depth key (common.cuh:depth_key)."""
+    k = key.clone()
+    neg = k >= 0  # sign bit clear in the key <=> negative depth
+    k = torch.where(neg, ~k, k ^ torch.tensor(-0x8000000000000000, dtype=torch.int64, device=k.device))
+    return k.view(torch.float64)
+
+
+def project_all(scene, config, cov_reg: float = DEFAULT_COV_REG, cutoff: float = DEFAULT_CUTOFF,
+                accessors: bool = True) -> Projection:
+    """geometry.project_all (geometry.py:233-340) on the device."""
+    if len(scene) == 0:
+        raise InvalidParameterError("scene is empty")
+    ds, _ = as_device_scene(scene)
+    return _project(ds, config, cov_reg, cutoff, accessors)
+
+
+def _project(ds: DeviceScene, config, cov_reg, cutoff, accessors) -> Projection:
+    proj = Projection(len(ds), ds.device, config, cov_reg, cutoff, accessors)
+    proj._desc = proj.desc()
+    sd = _scene_desc(ds)
+    _check(_lib.lib().sdgr_project(C.byref(sd), C.byref(proj.view), C.byref(proj._desc), _stream()),
+           "sdgr_project")
+    return proj
+
+
+# ----------------------------------------------------------------------------
+# binning (K2-K5)
+# ----------------------------------------------------------------------------
+@dataclass
+class TileLists:
+    """Per-16x16-tile key lists of one plane.
+
+    plane 0 (computation): each tile's Gaussians in (depth, index) order --
+    the per-ray order of forward.build_ray_lists (forward.py:138-155);
+    plane 1 (imaging): index order (forward._build_splat_pairs :213-224).
+    """
+
+    plane: int
+    n_u: int
+    n_v: int
+    tiles_x: int
+    tiles_y: int
+    n_pairs: int
+    pair_tile: torch.Tensor
+    pair_prim: torch.Tensor
+    tile_range: torch.Tensor
+    seg_len: int
+    max_items: int
+    items: torch.Tensor
+    tile_first: torch.Tensor
+    n_items: torch.Tensor
+    _desc: object = field(default=None, repr=False)
+
+    @property
+    def n_tiles(self) -> int:
+        return self.tiles_x * self.tiles_y
+
+    def desc(self) -> _lib.TilesDesc:
+        if self._desc is None:
+            d = _lib.TilesDesc()
+            d.plane, d.tiles_x, d.tiles_y, d.n_tiles = self.plane, self.tiles_x, self.tiles_y, self.n_tiles
+            d.n_pairs = self.n_pairs
+            d.pair_tile, d.pair_prim, d.tile_range = ptr(self.pair_tile), ptr(self.pair_prim), ptr(self.tile_range)
+            d.seg_len, d.max_items = self.seg_len, self.max_items
+            d.items, d.tile_first, d.n_items = ptr(self.items), ptr(self.tile_first), ptr(self.n_items)
+            self._desc = d
+        return self._desc
+
+    def tile_list(self, tx: int, ty: int) -> torch.Tensor:
+        t = ty * self.tiles_x + tx
+        s, e = self.tile_range[t].tolist()
+        return self.pair_prim[s:e]
+
+    def __len__(self) -> int:
+        return self.n_pairs
+
+
+def _seg_len(n_pairs: int) -> int:
+    seg = -(-n_pairs // SMS_TARGET_ITEMS)
+    seg = -(-seg // 256) * 256
+    return int(min(max(seg, 256), 8192))
+
+
+class _Binner:
+    """Runs K2-K5 for both planes with one host read of the pair totals."""
+
+    def __init__(self, proj: Projection):
+        self.proj = proj
+        self.lib = _lib.lib()
+        self.dev = proj.flags.device
+
+    def run(self, planes=(0, 1)):
+        p, lib, st, dev = self.proj, self.lib, _stream(), self.dev
+        n = p.n_scene
+        ws_bytes = lib.sdgr_workspace_bytes(n, 1)
+        ws = _empty((ws_bytes,), torch.uint8, dev)
+        order = None
+        offsets = {}
+        if 0 in planes:
+            order = _empty((n,), torch.int32, dev)
+            _check(lib.sdgr_depth_order(C.byref(p._desc), ptr(order), ptr(ws), ws_bytes, st), "sdgr_depth_order")
+        for pl in planes:
+            off = _empty((n + 1,), torch.int32, dev)
+            _check(lib.sdgr_count_pairs(C.byref(p._desc), pl, ptr(order) if pl == 0 else None, ptr(off),
+                                        ptr(ws), ws_bytes, st), "sdgr_count_pairs")
+            offsets[pl] = off
+        totals = torch.stack([offsets[pl][n] for pl in planes]).cpu().tolist()
+        max_pairs = max(max(totals), 1)
+        ws_bytes = lib.sdgr_workspace_bytes(n, max_pairs)
+        ws = _empty((ws_bytes,), torch.uint8, dev)
+        out = {}
+        for pl, total in zip(planes, totals):
+            v = p.view
+            nu, nv = (v.n_u, v.n_v) if pl == 0 else (v.n_az, v.n_rg)
+            tx, ty = -(-nu // TILE), -(-nv // TILE)
+            seg = _seg_len(total)
+            max_items = -(-total // seg) + tx * ty
+            tl = TileLists(
+                plane=pl, n_u=nu, n_v=nv, tiles_x=tx, tiles_y=ty, n_pairs=int(total),
+                pair_tile=_empty((max(total, 1),), torch.int32, dev),
+                pair_prim=_empty((max(total, 1),), torch.int32, dev),
+                tile_range=_empty((tx * ty, 2), torch.int32, dev),
+                seg_len=seg, max_items=max_items,
+                items=_empty((max_items, 4), torch.int32, dev),
+                tile_first=_empty((tx * ty,), torch.int32, dev),
+                n_items=torch.zeros((4,), dtype=torch.int32, device=dev),
+            )
+            _check(lib.sdgr_bin_pairs(C.byref(p._desc), C.byref(p.view), ptr(order) if pl == 0 else None,
+                                      ptr(offsets[pl]), C.byref(tl.desc()), ptr(ws), ws_bytes, st),
+                   "sdgr_bin_pairs")
+            out[pl] = tl
+        self.order = order
+        return out
+
+
+def build_ray_lists(projection: Projection, config=None) -> TileLists:
+    """Computation-plane tile lists (forward.build_ray_lists, forward.py:138-155)."""
+    return _Binner(projection).run((0,))[0]
+
+
+def build_splat_lists(projection: Projection, config=None) -> TileLists:
+    """Imaging-plane tile lists (forward._build_splat_pairs, forward.py:213-224)."""
+    return _Binner(projection).run((1,))[1]
+
+
+# ----------------------------------------------------------------------------
+# forward compositing (K6, K7)
+# ----------------------------------------------------------------------------
+@dataclass
+class IntensityBuffer:
+    """Per-Gaussian intensities (N-sized, scene order) + per-ray segment state."""
+
+    intensity_n: torch.Tensor
+    seg_sum: torch.Tensor
+    seg_base: torch.Tensor
+    status: torch.Tensor
+    s_stop: float
+    indices: torch.Tensor | None = None
+
+    @property
+    def intensity(self) -> torch.Tensor:
+        """(K,) compacted like the reference's IntensityBuffer.intensity."""
+        return self.intensity_n if self.indices is None else self.intensity_n[self.indices]
+
+
+def compute_intensities(rays: TileLists, projection: Projection, s_stop: float = S_STOP,
+                        check: bool = True) -> IntensityBuffer:
+    """forward.compute_intensities (forward.py:178-199) on the device."""
+    dev = projection.flags.device
+    n = projection.n_scene
+    cap = max(rays.max_items, 1) * 256
+    buf = IntensityBuffer(
+        intensity_n=_empty((n,), torch.float32, dev),
+        seg_sum=_empty((cap,), torch.float64, dev),
+        seg_base=_empty((cap,), torch.float64, dev),
+        status=torch.zeros((4,), dtype=torch.int32, device=dev),
+        s_stop=float(s_stop),
+    )
+    _check(_lib.lib().sdgr_composite_forward(
+        C.byref(projection.view), C.byref(projection._desc), C.byref(rays.desc()), float(s_stop),
+        ptr(buf.seg_sum), ptr(buf.seg_base), ptr(buf.intensity_n), ptr(buf.status), _stream()),
+        "sdgr_composite_forward")
+    if check:
+        _raise_if_nonfinite(buf, projection, rays)
+    return buf
+
+
+def _raise_if_nonfinite(buf: IntensityBuffer, proj: Projection, rays: TileLists) -> None:
+    if int(buf.status[0].item()) == 0 and bool(torch.isfinite(buf.intensity_n).all().item()):
+        return
+    raise NumericalError(f"non-finite intensity at primitive {_first_bad_primitive(proj)}")
+
+
+def _first_bad_primitive(proj: Projection) -> int:
+    """The primitive the reference names (forward.py:193-196): the first
+    non-finite pair in (cell, depth, index) order.  Every member pair of a
+    Gaussian with non-finite P or kappa is non-finite, so it is the bad
+    Gaussian minimising (first member cell, depth, index).  Error path only."""
+    bad = proj.visible & ~(torch.isfinite(proj.phase_f) & torch.isfinite(proj.kappa))
+    cand = torch.nonzero(bad).flatten().cpu().numpy()
+    if cand.size == 0:
+        return -1
+    v = proj.view
+    uv = proj.comp.uv.cpu().numpy()
+    A = proj.comp.inv_cov.cpu().numpy()
+    bb = proj.comp.bbox.cpu().numpy().astype(np.int64)
+    dk = proj.depth_key.cpu().numpy().view(np.uint64)
+    cut2 = v.cutoff * v.cutoff
+    best = None
+    for g in cand:
+        x0, x1, y0, y1 = bb[g]
+        first = None
+        for iv in range(y0, y1 + 1):
+            for iu in range(x0, x1 + 1):
+                dx, dy = iu - uv[g, 0], iv - uv[g, 1]
+                q = A[g, 0] * dx * dx + 2.0 * A[g, 1] * dx * dy + A[g, 2] * dy * dy
+                if not math.isfinite(v.cutoff) or q <= cut2:
+                    first = iv * v.n_u + iu
+                    break
+            if first is not None:
+                break
+        if first is None:
+            continue
+        key = (first, int(dk[g]), int(g))
+        if best is None or key < best:
+            best = key
+    return -1 if best is None else best[2]
+
+
+def splat_image(intensities: IntensityBuffer, projection: Projection, config=None,
+                pairs: TileLists | None = None) -> torch.Tensor:
+    """forward.splat_image (forward.py:227-240): (n_range, n_azimuth) float32."""
+    if pairs is None:
+        pairs = build_splat_lists(projection, config)
+    v = projection.view
+    dev = projection.flags.device
+    image = _empty((v.n_rg, v.n_az), torch.float32, dev)
+    part = _empty((max(pairs.max_items, 1) * 256,), torch.float64, dev)
+    _check(_lib.lib().sdgr_splat(C.byref(v), C.byref(projection._desc), C.byref(pairs.desc()),
+                                 ptr(intensities.intensity_n), ptr(part), ptr(image), _stream()),
+           "sdgr_splat")
+    return image
+
+
+@dataclass
+class ForwardResult:
+    """A rendered image plus every buffer the backward pass needs (forward.py:243-253)."""
+
+    scene: object
+    device_scene: DeviceScene
+    config: object
+    projection: Projection
+    rays: TileLists
+    intensities: IntensityBuffer
+    splat: TileLists
+    image_t: torch.Tensor
+    host: bool = False
+
+    @property
+    def image(self):
+        return self.image_t.double().cpu().numpy() if self.host else self.image_t
+
+
+def render_forward(scene, config, cov_reg: float = DEFAULT_COV_REG, cutoff: float = DEFAULT_CUTOFF,
+                   s_stop: float = S_STOP, accessors: bool = True) -> ForwardResult:
+    """Render and retain the buffers for backward (forward.py:256-273)."""
+    if len(scene) == 0:
+        raise NumericalError("cannot retain buffers for an empty scene")
+    ds, host = as_device_scene(scene)
+    proj = _project(ds, config, cov_reg, cutoff, accessors)
+    binner = _Binner(proj)
+    lists = binner.run((0, 1))
+    buf = compute_intensities(lists[0], proj, s_stop=s_stop)
+    image = splat_image(buf, proj, config, pairs=lists[1])
+    buf.indices = proj.indices if accessors else None
+    return ForwardResult(scene=scene, device_scene=ds, config=config, projection=proj, rays=lists[0],
+                         intensities=buf, splat=lists[1], image_t=image, host=host)
+
+
+def render(scene, config, cov_reg: float = DEFAULT_COV_REG, cutoff: float = DEFAULT_CUTOFF,
+           s_stop: float = S_STOP):
+    """Forward-render into an (n_range, n_azimuth) image (forward.py:276-285)."""
+    host = not (isinstance(scene, DeviceScene) or (isinstance(scene.positions, torch.Tensor)
+                                                   and scene.positions.is_cuda))
+    if len(scene) == 0:
+        img = torch.zeros((config.n_range, config.n_azimuth), dtype=torch.float32)
+        return img.double().numpy() if host else img.cuda()
+    return render_forward(scene, config, cov_reg, cutoff, s_stop=s_stop, accessors=False).image
+
+
+# ----------------------------------------------------------------------------
+# backward (K8-K10)
+# ----------------------------------------------------------------------------
+@dataclass
+class SceneGradients:
+    """Per-primitive gradients + densification statistic (backward.py:25-50)."""
+
+    positions: object
+    rotations: object
+    log_scales: object
+    sh_coeffs: object
+    ke_raw: object
+    uv_grad_norm: object
+    visible: object
+
+    def param_arrays(self):
+        return (self.positions, self.rotations, self.log_scales, self.sh_coeffs, self.ke_raw)
+
+    @classmethod
+    def zeros_device(cls, n: int, device) -> "SceneGradients":
+        z = lambda *s: torch.zeros(s, dtype=torch.float32, device=device)  # noqa: E731
+        return cls(z(n, 3), z(n, 4), z(n, 3), z(n, 16), z(n, 2), z(n),
+                   torch.zeros((n,), dtype=torch.int32, device=device))
+
+    def desc(self) -> _lib.GradsDesc:
+        d = _lib.GradsDesc()
+        d.positions, d.rotations, d.log_scales = ptr(self.positions), ptr(self.rotations), ptr(self.log_scales)
+        d.sh_coeffs, d.ke_raw = ptr(self.sh_coeffs), ptr(self.ke_raw)
+        d.uv_grad_norm, d.visible = ptr(self.uv_grad_norm), ptr(self.visible)
+        return d
+
+    def to_numpy(self) -> "SceneGradients":
+        f = lambda t: t.double().cpu().numpy()  # noqa: E731
+        return SceneGradients(*(f(a) for a in self.param_arrays()), f(self.uv_grad_norm),
+                              self.visible.cpu().numpy() > 0)
+
+
+def grad_image_stage(fwd: ForwardResult, dL_dS: torch.Tensor) -> torch.Tensor:
+    """backward.grad_image_stage (backward.py:86-104): acc (6, N) =
+    [dL/dI, dL/dA00, dL/dA01, dL/dA11, dL/du, dL/dv] on the imaging plane."""
+    p = fwd.projection
+    acc = _empty((6, p.n_scene), torch.float32, p.flags.device)
+    _check(_lib.lib().sdgr_grad_image(C.byref(p.view), C.byref(p._desc), ptr(fwd.intensities.intensity_n),
+                                      ptr(dL_dS), ptr(acc), _stream()), "sdgr_grad_image")
+    return acc
+
+
+def grad_intensity_stage(fwd: ForwardResult, dL_dI: torch.Tensor) -> torch.Tensor:
+    """backward.grad_intensity_stage (backward.py:107-148): acc (7, N) =
+    [dL/dP, dL/dkappa, dL/dA00, dL/dA01, dL/dA11, dL/du, dL/dv] (comp plane)."""
+    p, rays, buf = fwd.projection, fwd.rays, fwd.intensities
+    dev = p.flags.device
+    acc = _empty((7, p.n_scene), torch.float32, dev)
+    cap = max(rays.max_items, 1) * 256
+    seg_g = _empty((cap,), torch.float64, dev)
+    seg_d = _empty((cap,), torch.float64, dev)
+    _check(_lib.lib().sdgr_grad_intensity(C.byref(p.view), C.byref(p._desc), C.byref(rays.desc()),
+                                          buf.s_stop, ptr(buf.seg_base), ptr(dL_dI), ptr(seg_g), ptr(seg_d),
+                                          ptr(acc), _stream()), "sdgr_grad_intensity")
+    return acc
+
+
+def grad_geometry_stage(fwd: ForwardResult, acc_img: torch.Tensor, acc_comp: torch.Tensor,
+                        out: SceneGradients | None = None, accumulate: bool = False) -> SceneGradients:
+    """grad_geometry_stage + grad_sh_stage + final scatter (backward.py:171-290)."""
+    p = fwd.projection
+    if out is None:
+        out = SceneGradients.zeros_device(p.n_scene, p.flags.device)
+    sd = _scene_desc(fwd.device_scene)
+    gd = out.desc()
+    _check(_lib.lib().sdgr_grad_geometry(C.byref(sd), C.byref(p.view), C.byref(p._desc), ptr(acc_img),
+                                         ptr(acc_comp), C.byref(gd), int(accumulate), _stream()),
+           "sdgr_grad_geometry")
+    return out
+
+
+def _as_device_grad(dL_dS, fwd: ForwardResult) -> torch.Tensor:
+    dev = fwd.projection.flags.device
+    if isinstance(dL_dS, torch.Tensor):
+        return dL_dS.to(device=dev, dtype=torch.float32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(dL_dS, dtype=np.float32)).to(dev)
+
+
+def backward(fwd: ForwardResult, dL_dS, out: SceneGradients | None = None, accumulate: bool = False,
+             validate: bool = True) -> SceneGradients:
+    """Full backward from an image gradient (backward.py:243-290)."""
+    shape = tuple(dL_dS.shape)
+    img_shape = (fwd.projection.view.n_rg, fwd.projection.view.n_az)
+    if shape != img_shape:
+        raise StateError(f"image gradient shape {shape} does not match forward {img_shape}")
+    if fwd.projection.n_scene != len(fwd.scene):
+        raise StateError("scene changed since the forward pass; buffers are stale")
+    g = _as_device_grad(dL_dS, fwd)
+    if validate and not bool(torch.isfinite(g).all().item()):
+        raise InvalidParameterError("dL_dS contains non-finite values")
+    acc_img = grad_image_stage(fwd, g)
+    acc_comp = grad_intensity_stage(fwd, acc_img[0])
+    grads = grad_geometry_stage(fwd, acc_img, acc_comp, out=out, accumulate=accumulate)
+    return grads.to_numpy() if fwd.host and out is None else grads
+
+
+def launch_count() -> int:
+    """Kernels libsdgr has launched in this process."""
+    return int(_lib.lib().sdgr_launch_count())

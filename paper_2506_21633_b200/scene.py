@@ -1,0 +1,98 @@
+"""Gaussian-scatterer scenes: host mirror and device-resident SoA.
+
+``Scene`` mirrors sarsplat.scene.Scene (scene.py:132-244): five contiguous
+float64 arrays.  ``DeviceScene`` holds the same five arrays as CUDA tensors
+(float32 or float64), 16-byte aligned, the layout the kernels read.  Every
+public entry point accepts either, or any object exposing the five
+attributes (e.g. the reference's own Scene).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+import torch
+
+GROUPS = (("positions", 3), ("rotations", 4), ("log_scales", 3), ("sh_coeffs", 16), ("ke_raw", 2))
+
+
+@dataclass
+class Scene:
+    """Host-side scene, float64 SoA (scene.py:132-158)."""
+
+    positions: np.ndarray
+    rotations: np.ndarray
+    log_scales: np.ndarray
+    sh_coeffs: np.ndarray
+    ke_raw: np.ndarray
+    metadata: dict[str, Any] = field(default_factory=dict)
+
+    def __post_init__(self):
+        n = len(self.positions)
+        for name, w in GROUPS:
+            setattr(self, name, np.ascontiguousarray(getattr(self, name), dtype=np.float64).reshape(n, w))
+
+    def __len__(self) -> int:
+        return self.positions.shape[0]
+
+    def copy(self) -> "Scene":
+        return Scene(*(getattr(self, g).copy() for g, _ in GROUPS), metadata=dict(self.metadata))
+
+    @classmethod
+    def empty(cls) -> "Scene":
+        return cls(*(np.zeros((0, w)) for _, w in GROUPS))
+
+
+@dataclass
+class DeviceScene:
+    """Device-resident scene: five (n, w) CUDA tensors of one dtype."""
+
+    positions: torch.Tensor
+    rotations: torch.Tensor
+    log_scales: torch.Tensor
+    sh_coeffs: torch.Tensor
+    ke_raw: torch.Tensor
+
+    def __len__(self) -> int:
+        return int(self.positions.shape[0])
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.positions.dtype
+
+    @property
+    def device(self) -> torch.device:
+        return self.positions.device
+
+    def arrays(self):
+        return tuple(getattr(self, g) for g, _ in GROUPS)
+
+    @classmethod
+    def from_host(cls, scene, dtype=torch.float64, device="cuda", pin: bool = False) -> "DeviceScene":
+        """Upload any Scene-like object (numpy or torch fields)."""
+        out = []
+        for g, w in GROUPS:
+            a = getattr(scene, g)
+            t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+            t = t.reshape(-1, w).to(dtype)
+            if pin and t.device.type == "cpu":
+                t = t.pin_memory()
+            out.append(t.to(device, non_blocking=True).contiguous())
+        return cls(*out)
+
+    def to_host(self) -> Scene:
+        return Scene(*(t.detach().double().cpu().numpy() for t in self.arrays()))
+
+
+def as_device_scene(scene, device=None) -> tuple[DeviceScene, bool]:
+    """(device scene, was_host).  Host scenes keep float64 on device so the
+    FP64 key chain sees the caller's exact values."""
+    if isinstance(scene, DeviceScene):
+        return scene, False
+    pos = scene.positions
+    if isinstance(pos, torch.Tensor) and pos.is_cuda:
+        dt = pos.dtype if pos.dtype in (torch.float32, torch.float64) else torch.float64
+        return DeviceScene(*(getattr(scene, g).reshape(-1, w).to(dt).contiguous() for g, w in GROUPS)), False
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    return DeviceScene.from_host(scene, dtype=torch.float64, device=dev), True

@@ -1,0 +1,194 @@
+"""CUDA path vs the oracle and the reference's golden outputs (B200 only).
+
+Bar (BASELINE.json north star): per-tile key lists and tile ranges
+bit-exact; image, per-Gaussian intensity and every gradient column within
+|gpu - ref| <= 1e-6 + 1e-4 |ref|.  Upstream gradients are O(1): N(0,1) and
+dL/dS = S (gradcheck.py:79), per SURVEY.md §7 hard part 9.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import GROUPS, assert_close, golden_files, load_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2506_21633_b200 as sdgr  # noqa: E402
+from paper_2506_21633_b200 import targets  # noqa: E402
+from paper_2506_21633_b200.rasterizer import decode_depth  # noqa: E402
+from oracle import sdgr_oracle as O  # noqa: E402
+
+GOLDEN = golden_files()
+
+
+def tiles_np(tl):
+    n = tl.n_pairs
+    return (tl.pair_tile[:n].cpu().numpy().astype(np.int64), tl.pair_prim[:n].cpu().numpy().astype(np.int64),
+            tl.tile_range.cpu().numpy().astype(np.int64))
+
+
+def check_tiles(tl, ref_tile, ref_prim, ref_range, what):
+    t, p, r = tiles_np(tl)
+    assert t.shape == ref_tile.shape, (what, t.shape, ref_tile.shape)
+    assert np.array_equal(t, ref_tile), what
+    assert np.array_equal(p, ref_prim), what
+    assert np.array_equal(r, ref_range), what
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[p.stem for p in GOLDEN])
+@pytest.mark.parametrize("s_stop", [math.inf, sdgr.S_STOP], ids=["exact", "stop"])
+def test_golden(path, s_stop):
+    z, scene, cfg, cutoff = load_golden(path)
+    fwd = sdgr.render_forward(scene, cfg, cutoff=cutoff, s_stop=s_stop)
+    p = fwd.projection
+    idx = p.indices.cpu().numpy()
+    assert np.array_equal(idx, z["indices"])
+    assert p.n_culled == int(z["n_culled"]) and p.n_skipped == int(z["n_skipped"])
+    # FP64 key chain: pixel centers and depth bit-identical to the reference
+    assert np.array_equal(p.uv_comp.cpu().numpy(), z["uv_comp"])
+    assert np.array_equal(p.uv_img.cpu().numpy(), z["uv_img"])
+    assert np.array_equal(p.depth.cpu().numpy(), z["depth"])
+    # covariances: exp(log-scale) is the only non-reference op (<= 1 ulp)
+    assert_close(p.cov_comp.cpu().numpy()[:, [0, 0, 1], [0, 1, 1]], z["cov_comp"], 0, 1e-13, "cov_comp")
+    assert_close(p.cov_img.cpu().numpy()[:, [0, 0, 1], [0, 1, 1]], z["cov_img"], 0, 1e-13, "cov_img")
+    # bit-exact per-tile key lists and ranges, both planes
+    check_tiles(fwd.rays, z["tiles0_tile"], z["tiles0_prim"], z["tiles0_range"], "comp tiles")
+    check_tiles(fwd.splat, z["tiles1_tile"], z["tiles1_prim"], z["tiles1_range"], "img tiles")
+    assert_close(fwd.intensities.intensity.cpu().numpy(), z["intensity"], what="intensity")
+    assert_close(fwd.image.cpu().numpy() if hasattr(fwd.image, "cpu") else fwd.image, z["image"], what="image")
+    rows = z["grad_rows"]
+    for tag, dlds in (("n", z["dLdS"]), ("s", z["image"])):
+        g = sdgr.backward(fwd, dlds)
+        for k in GROUPS + ("uv_grad_norm",):
+            assert_close(getattr(g, k)[rows], z[f"g{tag}_{k}"], what=f"{path.stem} grad {tag} {k}")
+        assert np.array_equal(g.visible[rows], z[f"g{tag}_visible"])
+
+
+def _oracle_compare(scene, cfg, cutoff, s_stop=sdgr.S_STOP, seed=0, device_scene=False):
+    fo = O.render_forward(scene, cfg, cutoff=cutoff, exp="device")
+    inp = sdgr.DeviceScene.from_host(scene, dtype=torch.float32) if device_scene else scene
+    fwd = sdgr.render_forward(inp, cfg, cutoff=cutoff, s_stop=s_stop)
+    img = fwd.image.cpu().numpy() if isinstance(fwd.image, torch.Tensor) else fwd.image
+    assert_close(img, fo.image, what="image")
+    for plane, pairs, tl in ((0, fo.rays, fwd.rays), (1, fo.spl, fwd.splat)):
+        tt, gi, rg = O.tile_lists(pairs, fo.proj, plane)
+        check_tiles(tl, tt, gi, rg, f"plane {plane}")
+    # FP64 key chain bit-identical to the oracle's device-exp restatement
+    p = fwd.projection
+    assert np.array_equal(p.cov_comp.cpu().numpy(), fo.proj.cov_comp)
+    assert np.array_equal(p.depth.cpu().numpy(), fo.proj.depth)
+    rng = np.random.default_rng(seed)
+    dlds = rng.normal(size=img.shape)
+    go = O.backward(fo, dlds)
+    g = sdgr.backward(fwd, torch.from_numpy(dlds).float().cuda() if device_scene else dlds)
+    if device_scene:
+        g = g.to_numpy()
+    for k in GROUPS + ("uv_grad_norm",):
+        assert_close(getattr(g, k), go[k], what=f"grad {k}")
+    assert np.array_equal(g.visible, go["visible"])
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("cutoff", [math.inf, 3.0], ids=["dense", "cut"])
+def test_random_small_vs_oracle(seed, cutoff):
+    rng = np.random.default_rng(100 + seed)
+    scene = targets.random_scene(rng, 4 + 3 * seed)
+    cfg = sdgr.RadarConfig(azimuth_deg=float(rng.uniform(0, 360)), elevation_deg=float(rng.uniform(38, 52)),
+                           altitude_m=float(rng.uniform(1, 4)), range_res_m=0.5, azimuth_res_m=0.5,
+                           n_range=16 + 8 * (seed % 3), n_azimuth=16 + 5 * (seed % 2))
+    _oracle_compare(scene, cfg, cutoff, seed=seed)
+
+
+def test_float32_device_scene_matches_oracle():
+    tank = targets.to_float32_exact(targets.composite_target(targets.tank_preset(), [3000, 1500, 500], seed=4))
+    cfg = sdgr.RadarConfig(azimuth_deg=10.0, elevation_deg=50.0, altitude_m=0.5, n_range=128, n_azimuth=128)
+    _oracle_compare(tank, cfg, 3.0, device_scene=True)
+
+
+@pytest.mark.parametrize("el", [15.0, 45.0, 75.0])
+def test_c2_tank_100k_vs_oracle(el):
+    tank = targets.composite_target(targets.tank_preset(), [60000, 30000, 10000], seed=3)
+    cfg = sdgr.RadarConfig(azimuth_deg=30.0, elevation_deg=el, altitude_m=0.5, n_range=256, n_azimuth=256)
+    _oracle_compare(tank, cfg, 3.0, seed=int(el))
+
+
+def test_perturbed_large_gaussians_vs_oracle():
+    # footprints wider than the 8x8 cell window exercise the exact FP64 fallback
+    rng = np.random.default_rng(9)
+    scene = targets.random_scene(rng, 300, spread=6.0, scale_low=0.3, scale_high=2.0)
+    cfg = sdgr.RadarConfig(azimuth_deg=33.0, elevation_deg=40.0, altitude_m=1.0, range_res_m=0.25,
+                           azimuth_res_m=0.25, n_range=64, n_azimuth=80)
+    _oracle_compare(scene, cfg, 3.0, seed=3)
+
+
+def test_depth_key_roundtrip():
+    d = torch.tensor([-3.5, -0.0, 0.0, 1e-300, 2.0, -1e-300, 7.25], dtype=torch.float64)
+    from paper_2506_21633_b200.rasterizer import decode_depth as dec
+    b = d.view(torch.int64)
+    sign = b < 0
+    key = torch.where(sign, ~b, b ^ torch.tensor(-0x8000000000000000, dtype=torch.int64))
+    out = dec(key)
+    assert torch.equal(out.abs(), d.abs())
+
+
+def test_empty_and_culled():
+    cfg = sdgr.RadarConfig(azimuth_deg=20.0, elevation_deg=40.0, altitude_m=2.0, range_res_m=0.5,
+                           azimuth_res_m=0.5, n_range=16, n_azimuth=16)
+    img = sdgr.render(sdgr.Scene.empty(), cfg)
+    assert img.shape == (16, 16) and np.all(img == 0)
+    with pytest.raises(sdgr.NumericalError):
+        sdgr.render_forward(sdgr.Scene.empty(), cfg)
+    with pytest.raises(sdgr.InvalidParameterError):
+        sdgr.project_all(sdgr.Scene.empty(), cfg)
+    far = targets.random_scene(np.random.default_rng(0), 3)
+    far.positions[:] = 100.0
+    fwd = sdgr.render_forward(far, cfg)
+    assert np.all(fwd.image == 0)
+    g = sdgr.backward(fwd, np.ones((16, 16)))
+    assert not g.visible.any() and np.all(g.positions == 0)
+
+
+def test_nonfinite_names_primitive():
+    cfg = sdgr.RadarConfig(azimuth_deg=20.0, elevation_deg=40.0, altitude_m=2.0, range_res_m=0.5,
+                           azimuth_res_m=0.5, n_range=16, n_azimuth=16)
+    scene = targets.random_scene(np.random.default_rng(3), 6)
+    scene.sh_coeffs[4, 0] = np.inf
+    with pytest.raises(sdgr.NumericalError, match="primitive 4"):
+        sdgr.render_forward(scene, cfg)
+
+
+def test_backward_state_errors():
+    cfg = sdgr.RadarConfig(azimuth_deg=20.0, elevation_deg=40.0, altitude_m=2.0, range_res_m=0.5,
+                           azimuth_res_m=0.5, n_range=16, n_azimuth=16)
+    scene = targets.random_scene(np.random.default_rng(4), 4)
+    fwd = sdgr.render_forward(scene, cfg)
+    with pytest.raises(sdgr.StateError):
+        sdgr.backward(fwd, np.zeros((3, 3)))
+    bad = np.zeros((16, 16))
+    bad[0, 0] = np.nan
+    with pytest.raises(sdgr.InvalidParameterError):
+        sdgr.backward(fwd, bad)
+    scene.positions = np.vstack([scene.positions, np.zeros((1, 3))])
+    with pytest.raises(sdgr.StateError):
+        sdgr.backward(fwd, np.zeros((16, 16)))
+
+
+def test_linearity_and_zero_gradient():
+    cfg = sdgr.RadarConfig(azimuth_deg=20.0, elevation_deg=40.0, altitude_m=2.0, range_res_m=0.5,
+                           azimuth_res_m=0.5, n_range=16, n_azimuth=16)
+    rng = np.random.default_rng(5)
+    scene = targets.random_scene(rng, 6)
+    fwd = sdgr.render_forward(scene, cfg)
+    z = sdgr.backward(fwd, np.zeros((16, 16)))
+    for a in z.param_arrays():
+        assert np.all(a == 0)
+    g1, g2 = rng.normal(size=(16, 16)), rng.normal(size=(16, 16))
+    lhs = sdgr.backward(fwd, 0.7 * g1 - 1.3 * g2)
+    r1, r2 = sdgr.backward(fwd, g1), sdgr.backward(fwd, g2)
+    for k in GROUPS:
+        assert_close(getattr(lhs, k), 0.7 * getattr(r1, k) - 1.3 * getattr(r2, k), atol=1e-5, what=k)
