@@ -100,24 +100,32 @@ typedef struct sdgr_projection {
   sdgr_plane comp;       /* computation plane (n_u x n_v)   */
   sdgr_plane img;        /* imaging plane (n_az x n_rg)     */
   uint64_t* depth_key;   /* (n) order-preserving FP64 depth key; UINT64_MAX if not visible */
-  float* kappa;          /* (n) ke_fwd + ke_bwd (geometry.py:317, Projection.ke_sum) */
-  float* phase;          /* (n) max(0, P~)                  (geometry.py:316) */
-  float* phase_raw;      /* (n) P~ (backward clamp gate)    (geometry.py:315) */
+  double* kappa;         /* (n) ke_fwd + ke_bwd (geometry.py:317, Projection.ke_sum) */
+  double* phase;         /* (n) max(0, P~)                  (geometry.py:316) */
+  double* phase_raw;     /* (n) P~ (backward clamp gate)    (geometry.py:315) */
   uint8_t* flags;        /* (n) SDGR_FLAG_* */
   int32_t* counters;     /* (4) [0] visible, [1] skipped, [2] culled; zeroed by sdgr_project */
   /* optional accessors (NULL to skip) */
-  float* ke_act;         /* (n,2) softplus(ke_raw)          */
+  double* ke_act;        /* (n,2) softplus(ke_raw)          */
   double* look;          /* (n,4) unit look dir xyz, distance (geometry.py:308-313) */
 } sdgr_projection;
 
-/* (tile, Gaussian) binning of one plane: the per-tile key lists. */
+/* (tile, Gaussian) binning of one plane: the per-tile key lists.
+ * Pairs are emitted per Gaussian in list order (rank order on the computation
+ * plane, index order on the imaging plane) at "pre-sort positions"; Gaussian g
+ * owns the contiguous pre-sort range [pair_start[g], pair_start[g]+n_tiles[g]).
+ * Per-pair partial sums are stored by pre-sort position so the per-Gaussian
+ * reductions run in a fixed order (deterministic, atomic-free). */
 typedef struct sdgr_tiles {
   int32_t plane;        /* 0 = computation (depth order), 1 = imaging (index order) */
   int32_t tiles_x, tiles_y, n_tiles;
   int64_t n_pairs;      /* T16: number of (tile, Gaussian) member pairs */
   uint32_t* pair_tile;  /* (n_pairs) tile id, sorted ascending              */
+  int32_t* pair_pos;    /* (n_pairs) pre-sort position of each sorted pair    */
   int32_t* pair_prim;   /* (n_pairs) scene index; per tile by (depth, index) or index */
-  int32_t* tile_range;  /* (n_tiles,2) [start, end) into the pair arrays      */
+  int32_t* pre_prim;    /* (n_pairs) scene index by pre-sort position         */
+  int32_t* pair_start;  /* (n) first pre-sort position of each Gaussian       */
+  int32_t* tile_range;  /* (n_tiles,2) [start, end) into the sorted arrays    */
   int32_t seg_len;      /* max Gaussians per work item (depth segment)       */
   int32_t max_items;    /* capacity of items                                  */
   int32_t* items;       /* (max_items,4) tile, start, end, first item of tile */
@@ -171,39 +179,44 @@ int sdgr_bin_pairs(const sdgr_projection* proj, const sdgr_view* view,
 /* ------------------------------------------------- forward (K6, K7) ------ */
 /* compute_intensities (forward.py:178-199): per-ray emission-absorption walk.
  * seg_sum / seg_base: (max_items*256) FP64 per-(item, ray) optical-depth
- * segment sums and exclusive prefixes (kept for the backward).  intensity (n)
- * is overwritten.  s_stop: rays stop once their log-transmittance exceeds it
- * (+inf = never, the reference's behaviour).  status: int32[4]. */
+ * segment sums and exclusive prefixes (kept for the backward).
+ * partial_I: (n_pairs) FP64 per-(tile, Gaussian) partial intensities.
+ * intensity: (n) FP64, overwritten.  s_stop: rays stop once their
+ * log-transmittance exceeds it (+inf = never, the reference's behaviour).
+ * status: int32[4]; [0] != 0 if any contribution was non-finite. */
 int sdgr_composite_forward(const sdgr_view* view, const sdgr_projection* proj,
                            const sdgr_tiles* comp, double s_stop,
-                           double* seg_sum, double* seg_base, float* intensity,
-                           int32_t* status, void* stream);
-/* splat_image (forward.py:227-240): image (n_rg, n_az) float32 overwritten.
+                           double* seg_sum, double* seg_base, double* partial_I,
+                           double* intensity, int32_t* status, void* stream);
+/* splat_image (forward.py:227-240): image (n_rg, n_az) FP64 overwritten.
  * part: (max_items*256) FP64 scratch. */
 int sdgr_splat(const sdgr_view* view, const sdgr_projection* proj,
-               const sdgr_tiles* img, const float* intensity, double* part,
-               float* image, void* stream);
+               const sdgr_tiles* img, const double* intensity, double* part,
+               double* image, void* stream);
 
 /* ------------------------------------------------ backward (K8-K10) ------ */
-/* grad_image_stage (backward.py:86-104).  acc_img (6,n): dL/dI, dL/dA(3),
- * dL/duv(2) on the imaging plane (A = inverse covariance). */
+/* grad_image_stage (backward.py:86-104).  dL_dS: (n_rg, n_az) FP64.
+ * acc_img (6,n) FP64: dL/dI, dL/dA(3), dL/duv(2) on the imaging plane
+ * (A = inverse covariance). */
 int sdgr_grad_image(const sdgr_view* view, const sdgr_projection* proj,
-                    const float* intensity, const float* dL_dS, float* acc_img,
+                    const double* intensity, const double* dL_dS, double* acc_img,
                     void* stream);
-/* grad_intensity_stage (backward.py:107-148).  acc_comp (7,n): dL/dP,
- * dL/dkappa, dL/dA(3), dL/duv(2) on the computation plane.  dL_dI = acc_img
- * row 0.  seg_g / seg_d: (max_items*256) FP64 scratch. */
+/* grad_intensity_stage (backward.py:107-148).  dL_dI = acc_img row 0.
+ * partial_g: (n_pairs, 8) FP64 per-(tile, Gaussian) partials of dL/dP,
+ * dL/dkappa, dL/dA(3), dL/duv(2) on the computation plane.
+ * seg_g / seg_d: (max_items*256) FP64 scratch. */
 int sdgr_grad_intensity(const sdgr_view* view, const sdgr_projection* proj,
                         const sdgr_tiles* comp, double s_stop,
-                        const double* seg_base, const float* dL_dI,
-                        double* seg_g, double* seg_d, float* acc_comp,
+                        const double* seg_base, const double* dL_dI,
+                        double* seg_g, double* seg_d, double* partial_g,
                         void* stream);
 /* grad_geometry_stage + grad_sh_stage + the final scatter (backward.py:171-290).
+ * Reduces partial_g per Gaussian (fixed order) and chains to parameters.
  * accumulate = 0 overwrites `out`, 1 adds into it (multi-view steps). */
 int sdgr_grad_geometry(const sdgr_scene* scene, const sdgr_view* view,
-                       const sdgr_projection* proj, const float* acc_img,
-                       const float* acc_comp, sdgr_grads* out, int accumulate,
-                       void* stream);
+                       const sdgr_projection* proj, const sdgr_tiles* comp,
+                       const double* acc_img, const double* partial_g,
+                       sdgr_grads* out, int accumulate, void* stream);
 
 #ifdef __cplusplus
 }

@@ -55,7 +55,8 @@ class ProjectionDesc(C.Structure):
 class TilesDesc(C.Structure):
     _fields_ = [
         ("plane", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("n_tiles", C.c_int32),
-        ("n_pairs", C.c_int64), ("pair_tile", _p), ("pair_prim", _p), ("tile_range", _p),
+        ("n_pairs", C.c_int64), ("pair_tile", _p), ("pair_pos", _p), ("pair_prim", _p),
+        ("pre_prim", _p), ("pair_start", _p), ("tile_range", _p),
         ("seg_len", C.c_int32), ("max_items", C.c_int32), ("items", _p), ("tile_first", _p),
         ("n_items", _p),
     ]
@@ -80,13 +81,13 @@ SIGNATURES = [
     ("sdgr_bin_pairs", C.c_int, [C.POINTER(ProjectionDesc), C.POINTER(View), _p, _p,
                                  C.POINTER(TilesDesc), _p, C.c_size_t, _p]),
     ("sdgr_composite_forward", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc),
-                                         C.c_double, _p, _p, _p, _p, _p]),
+                                         C.c_double, _p, _p, _p, _p, _p, _p]),
     ("sdgr_splat", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc), _p, _p, _p, _p]),
     ("sdgr_grad_image", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), _p, _p, _p, _p]),
     ("sdgr_grad_intensity", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc),
                                       C.c_double, _p, _p, _p, _p, _p, _p]),
     ("sdgr_grad_geometry", C.c_int, [C.POINTER(SceneDesc), C.POINTER(View), C.POINTER(ProjectionDesc),
-                                     _p, _p, C.POINTER(GradsDesc), C.c_int, _p]),
+                                     C.POINTER(TilesDesc), _p, _p, C.POINTER(GradsDesc), C.c_int, _p]),
 ]
 
 

@@ -22,8 +22,8 @@ __device__ __forceinline__ double ldv(const void* p, int64_t i) {
 }
 
 __global__ void __launch_bounds__(256) k_grad_image(sdgr_view view, sdgr_plane pl, const uint8_t* flags,
-                                                    const float* intensity, const float* dLdS,
-                                                    float* acc, int64_t n) {
+                                                    const double* intensity, const double* dLdS,
+                                                    double* acc, int64_t n) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n) return;
   double dI = 0, g00 = 0, g01 = 0, g11 = 0, gu = 0, gv = 0;
@@ -31,12 +31,12 @@ __global__ void __launch_bounds__(256) k_grad_image(sdgr_view view, sdgr_plane p
     const double2 uv = reinterpret_cast<const double2*>(pl.uv)[g];
     const double4 A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
     const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
-    const double I = (double)intensity[g];
+    const double I = intensity[g];
     const bool dense = !isfinite(view.cutoff);
     const double cut2 = dmul(view.cutoff, view.cutoff);
     auto visit = [&](int iu, int iv, double dx, double dy, double q) {
-      const double G = (double)__ldg(dLdS + (int64_t)iv * view.n_az + iu);
-      const double w = (double)expf(-(float)q);
+      const double G = __ldg(dLdS + (int64_t)iv * view.n_az + iu);
+      const double w = exp(-q);
       dI += G * w;
       const double dq = -(G * I) * w;
       g00 += dq * dx * dx;
@@ -65,12 +65,12 @@ __global__ void __launch_bounds__(256) k_grad_image(sdgr_view view, sdgr_plane p
       }
     }
   }
-  acc[g] = (float)dI;
-  acc[n + g] = (float)g00;
-  acc[2 * n + g] = (float)g01;
-  acc[3 * n + g] = (float)g11;
-  acc[4 * n + g] = (float)gu;
-  acc[5 * n + g] = (float)gv;
+  acc[g] = dI;
+  acc[n + g] = g00;
+  acc[2 * n + g] = g01;
+  acc[3 * n + g] = g11;
+  acc[4 * n + g] = gu;
+  acc[5 * n + g] = gv;
 }
 
 // d(basis)/d(dir) for the 16 real SH functions (sh.py:68-113), contracted
@@ -127,9 +127,9 @@ __device__ __forceinline__ void inverse_chain(double a, double b, double c, doub
 
 template <typename T>
 __global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view view,
-                                                       sdgr_projection proj, const float* acc_img,
-                                                       const float* acc_comp, sdgr_grads out,
-                                                       int accumulate) {
+                                                       sdgr_projection proj, const int32_t* pair_start,
+                                                       const double* acc_img, const double* partial,
+                                                       sdgr_grads out, int accumulate) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = sc.n;
   if (g >= n) return;
@@ -141,12 +141,23 @@ __global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view 
     // plane-space gradients
     const double4 Ac = reinterpret_cast<const double4*>(proj.comp.inv_cov)[g];
     const double4 Ai = reinterpret_cast<const double4*>(proj.img.inv_cov)[g];
+    // computation-plane partials: one record per member tile, fixed order
+    double c7[7] = {0, 0, 0, 0, 0, 0, 0};
+    {
+      const int s0 = pair_start[g], cnt = proj.comp.n_tiles[g];
+      for (int k = 0; k < cnt; ++k) {
+        const double4* rec = reinterpret_cast<const double4*>(partial + (int64_t)(s0 + k) * 8);
+        const double4 r0 = rec[0], r1 = rec[1];
+        c7[0] += r0.x; c7[1] += r0.y; c7[2] += r0.z; c7[3] += r0.w;
+        c7[4] += r1.x; c7[5] += r1.y; c7[6] += r1.z;
+      }
+    }
     double dSc[4], dSi[4];
-    inverse_chain(Ac.x, Ac.y, Ac.z, acc_comp[2 * n + g], acc_comp[3 * n + g], acc_comp[4 * n + g], dSc);
+    inverse_chain(Ac.x, Ac.y, Ac.z, c7[2], c7[3], c7[4], dSc);
     inverse_chain(Ai.x, Ai.y, Ai.z, acc_img[1 * n + g], acc_img[2 * n + g], acc_img[3 * n + g], dSi);
-    const double duc[2] = {acc_comp[5 * n + g], acc_comp[6 * n + g]};
+    const double duc[2] = {c7[5], c7[6]};
     const double dui[2] = {acc_img[4 * n + g], acc_img[5 * n + g]};
-    const double dP = acc_comp[g], dk = acc_comp[n + g];
+    const double dP = c7[0], dk = c7[1];
     // G3 = mc^T dSc mc + mi^T dSi mi   (backward.py:191-193)
     double G3[9];
 #pragma unroll
@@ -222,7 +233,7 @@ __global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view 
 #pragma unroll
     for (int k = 0; k < 16; ++k) c[k] = ldv<T>(sc.sh_coeffs, 16 * g + k);
     sh_grad_contract(d0, d1, d2, c, gP, basis);
-    const bool active = proj.phase_raw[g] > 0.f;
+    const bool active = proj.phase_raw[g] > 0.0;
     if (active) {
       const double proj_d = gP[0] * d0 + gP[1] * d1 + gP[2] * d2;
       dpos[0] += dP * (gP[0] - proj_d * d0) / dist;
@@ -257,21 +268,21 @@ __global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view 
   out.visible[g] = accumulate ? out.visible[g] + (int)vis : (int)vis;
 }
 
-int launch_grad_image(const sdgr_view& v, const sdgr_projection& p, const float* intensity,
-                      const float* dLdS, float* acc, cudaStream_t st) {
+int launch_grad_image(const sdgr_view& v, const sdgr_projection& p, const double* intensity,
+                      const double* dLdS, double* acc, cudaStream_t st) {
   k_grad_image<<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(v, p.img, p.flags, intensity, dLdS, acc, p.n);
   note_launch();
   return check_launch();
 }
 
 int launch_grad_geometry(const sdgr_scene& sc, const sdgr_view& v, const sdgr_projection& p,
-                         const float* acc_img, const float* acc_comp, const sdgr_grads& out,
-                         int accumulate, cudaStream_t st) {
+                         const sdgr_tiles& comp, const double* acc_img, const double* partial,
+                         const sdgr_grads& out, int accumulate, cudaStream_t st) {
   const unsigned blocks = (unsigned)((sc.n + 127) / 128);
   if (sc.dtype == 0)
-    k_grad_geometry<float><<<blocks, 128, 0, st>>>(sc, v, p, acc_img, acc_comp, out, accumulate);
+    k_grad_geometry<float><<<blocks, 128, 0, st>>>(sc, v, p, comp.pair_start, acc_img, partial, out, accumulate);
   else
-    k_grad_geometry<double><<<blocks, 128, 0, st>>>(sc, v, p, acc_img, acc_comp, out, accumulate);
+    k_grad_geometry<double><<<blocks, 128, 0, st>>>(sc, v, p, comp.pair_start, acc_img, partial, out, accumulate);
   note_launch();
   return check_launch();
 }

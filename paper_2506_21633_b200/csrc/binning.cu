@@ -355,13 +355,15 @@ int scan_counts(const int32_t* ntiles, const int32_t* order, int64_t n, int32_t*
 __global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t* order,
                                                     const int32_t* offsets, int64_t n,
                                                     int tiles_x, double cutoff,
-                                                    uint32_t* keys, uint32_t* vals) {
+                                                    uint32_t* keys, int32_t* vals,
+                                                    int32_t* pair_start) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int32_t g = order ? order[i] : (int32_t)i;
   const int32_t cnt = pl.n_tiles[g];
-  if (cnt == 0) return;
   int64_t o = offsets[i];
+  pair_start[g] = (int32_t)o;
+  if (cnt == 0) return;
   const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
   const int tx0 = bb.x >> 4, tx1 = bb.y >> 4, ty0 = bb.z >> 4, ty1 = bb.w >> 4;
   if ((tx1 - tx0) < 8 && (ty1 - ty0) < 8) {
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t
       m &= m - 1;
       const int tx = tx0 + (b & 7), ty = ty0 + (b >> 3);
       keys[o] = (uint32_t)(ty * tiles_x + tx);
-      vals[o] = (uint32_t)g;
+      vals[o] = g;
       ++o;
     }
     return;
@@ -396,19 +398,36 @@ __global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t
       }
       if (hit) {
         keys[o] = (uint32_t)(ty * tiles_x + tx);
-        vals[o] = (uint32_t)g;
+        vals[o] = g;
         ++o;
       }
     }
 }
 
-// tile ranges from the sorted keys: range[t] = [first, last+1)
-__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, int64_t n, int32_t* range) {
+// CSR tile ranges from the sorted keys: range[t] = [lower_bound(t),
+// lower_bound(t+1)); empty tiles get [s, s] like a CSR offsets array.
+__device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* k, int64_t n, uint32_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (k[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, int64_t n, int n_tiles,
+                                                     int32_t* range) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_tiles) return;
+  range[2 * t] = (int32_t)lower_bound_u32(keys, n, (uint32_t)t);
+  range[2 * t + 1] = (int32_t)lower_bound_u32(keys, n, (uint32_t)t + 1u);
+}
+
+// scene index of each sorted pair: pair_prim[i] = pre_prim[pair_pos[i]]
+__global__ void __launch_bounds__(256) k_gather_prim(const int32_t* pos, const int32_t* pre, int64_t n,
+                                                     int32_t* prim) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t k = keys[i];
-  if (i == 0 || keys[i - 1] != k) range[2 * k] = (int32_t)i;
-  if (i == n - 1 || keys[i + 1] != k) range[2 * k + 1] = (int32_t)(i + 1);
+  if (i < n) prim[i] = pre[pos[i]];
 }
 
 // depth-segment work items: each tile list is cut into segments of at most
@@ -461,19 +480,28 @@ int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, con
   if (np > 0) {
     char* p = static_cast<char*>(ws);
     uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * np);
-    uint32_t* vals = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * np);
     const size_t used = (size_t)(p - static_cast<char*>(ws));
     if (used > ws_bytes) return SDGR_ERR_CAPACITY;
     k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,
-                                                              view.cutoff, keys, vals);
+                                                              view.cutoff, keys, tl.pre_prim,
+                                                              tl.pair_start);
     note_launch();
     int bits = 1;
     while ((1 << bits) < tl.n_tiles) ++bits;
-    const int rc = radix_sort<uint32_t>(keys, vals, tl.pair_tile,
-                                        reinterpret_cast<uint32_t*>(tl.pair_prim), np, 0, bits, p,
+    // stable by tile; values = pre-sort positions (iota)
+    const int rc = radix_sort<uint32_t>(keys, nullptr, tl.pair_tile,
+                                        reinterpret_cast<uint32_t*>(tl.pair_pos), np, 0, bits, p,
                                         ws_bytes - used, st);
     if (rc != SDGR_OK) return rc;
-    k_tile_ranges<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(tl.pair_tile, np, tl.tile_range);
+    k_tile_ranges<<<(unsigned)((tl.n_tiles + 255) / 256), 256, 0, st>>>(tl.pair_tile, np, tl.n_tiles,
+                                                                        tl.tile_range);
+    k_gather_prim<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(tl.pair_pos, tl.pre_prim, np,
+                                                                tl.pair_prim);
+    note_launch(2);
+  } else {
+    k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,
+                                                              view.cutoff, nullptr, nullptr,
+                                                              tl.pair_start);
     note_launch();
   }
   k_make_items<<<1, 1024, 0, st>>>(tl.tile_range, tl.n_tiles, tl.seg_len, tl.max_items, tl.items,
@@ -485,8 +513,8 @@ int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, con
 size_t binning_ws_bytes(int64_t n, int64_t max_pairs) {
   // depth sort: sorted keys + radix scratch (8 passes of 64-bit keys)
   const size_t depth = align_up(sizeof(uint64_t) * (size_t)n) + radix_ws_bytes<uint64_t>(n, 8);
-  // pair sort: keys + vals + radix scratch (up to 2 passes of 32-bit keys)
-  const size_t pairs = 2 * align_up(sizeof(uint32_t) * (size_t)max_pairs) +
+  // pair sort: keys + radix scratch (up to 2 passes of 32-bit keys)
+  const size_t pairs = align_up(sizeof(uint32_t) * (size_t)max_pairs) +
                        radix_ws_bytes<uint32_t>(max_pairs, 2);
   const size_t scan = scan_ws_bytes(n);
   return std::max(std::max(depth, pairs), scan) + 4096;

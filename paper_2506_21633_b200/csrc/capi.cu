@@ -21,15 +21,15 @@ size_t binning_ws_bytes(int64_t, int64_t);
 int launch_emit_and_sort(const sdgr_projection&, const sdgr_view&, const int32_t*, const int32_t*,
                          sdgr_tiles&, void*, size_t, cudaStream_t);
 int launch_composite_forward(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, double,
-                             double*, double*, float*, int32_t*, cudaStream_t);
-int launch_splat(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, const float*, double*,
-                 float*, cudaStream_t);
-int launch_grad_image(const sdgr_view&, const sdgr_projection&, const float*, const float*, float*,
+                             double*, double*, double*, double*, int32_t*, cudaStream_t);
+int launch_splat(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, const double*, double*,
+                 double*, cudaStream_t);
+int launch_grad_image(const sdgr_view&, const sdgr_projection&, const double*, const double*, double*,
                       cudaStream_t);
 int launch_grad_intensity(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, double,
-                          const double*, const float*, double*, double*, float*, cudaStream_t);
-int launch_grad_geometry(const sdgr_scene&, const sdgr_view&, const sdgr_projection&, const float*,
-                         const float*, const sdgr_grads&, int, cudaStream_t);
+                          const double*, const double*, double*, double*, double*, cudaStream_t);
+int launch_grad_geometry(const sdgr_scene&, const sdgr_view&, const sdgr_projection&, const sdgr_tiles&,
+                         const double*, const double*, const sdgr_grads&, int, cudaStream_t);
 
 static bool view_ok(const sdgr_view* v) {
   if (!v) return false;
@@ -98,53 +98,61 @@ int sdgr_bin_pairs(const sdgr_projection* proj, const sdgr_view* view, const int
                    void* stream) {
   if (!proj || !view_ok(view) || !offsets || !tiles_ok(tiles) || !ws) return SDGR_ERR_INVALID;
   if (tiles->plane == 0 && !order) return SDGR_ERR_INVALID;
-  if (tiles->n_pairs > 0 && (!tiles->pair_tile || !tiles->pair_prim)) return SDGR_ERR_INVALID;
+  if (!tiles->pair_start) return SDGR_ERR_INVALID;
+  if (tiles->n_pairs > 0 && (!tiles->pair_tile || !tiles->pair_prim || !tiles->pair_pos || !tiles->pre_prim))
+    return SDGR_ERR_INVALID;
   if (tiles->n_pairs > 0x7fffffffLL) return SDGR_ERR_CAPACITY;
   return launch_emit_and_sort(*proj, *view, tiles->plane == 0 ? order : nullptr, offsets, *tiles, ws,
                               ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int sdgr_composite_forward(const sdgr_view* view, const sdgr_projection* proj, const sdgr_tiles* comp,
-                           double s_stop, double* seg_sum, double* seg_base, float* intensity,
-                           int32_t* status, void* stream) {
-  if (!view_ok(view) || !proj || !tiles_ok(comp) || comp->plane != 0 || !intensity || !status)
+                           double s_stop, double* seg_sum, double* seg_base, double* partial_I,
+                           double* intensity, int32_t* status, void* stream) {
+  if (!view_ok(view) || !proj || !tiles_ok(comp) || comp->plane != 0 || !intensity || !status ||
+      !comp->pair_start)
     return SDGR_ERR_INVALID;
-  if (comp->n_pairs > 0 && (!seg_sum || !seg_base)) return SDGR_ERR_INVALID;
+  if (comp->n_pairs > 0 && (!seg_sum || !seg_base || !partial_I || !comp->pair_pos))
+    return SDGR_ERR_INVALID;
   if (std::isnan(s_stop)) return SDGR_ERR_INVALID;
-  return launch_composite_forward(*view, *proj, *comp, s_stop, seg_sum, seg_base, intensity, status,
-                                  static_cast<cudaStream_t>(stream));
+  return launch_composite_forward(*view, *proj, *comp, s_stop, seg_sum, seg_base, partial_I, intensity,
+                                  status, static_cast<cudaStream_t>(stream));
 }
 
 int sdgr_splat(const sdgr_view* view, const sdgr_projection* proj, const sdgr_tiles* img,
-               const float* intensity, double* part, float* image, void* stream) {
+               const double* intensity, double* part, double* image, void* stream) {
   if (!view_ok(view) || !proj || !tiles_ok(img) || img->plane != 1 || !intensity || !image)
     return SDGR_ERR_INVALID;
   if (img->n_pairs > 0 && !part) return SDGR_ERR_INVALID;
   return launch_splat(*view, *proj, *img, intensity, part, image, static_cast<cudaStream_t>(stream));
 }
 
-int sdgr_grad_image(const sdgr_view* view, const sdgr_projection* proj, const float* intensity,
-                    const float* dL_dS, float* acc_img, void* stream) {
+int sdgr_grad_image(const sdgr_view* view, const sdgr_projection* proj, const double* intensity,
+                    const double* dL_dS, double* acc_img, void* stream) {
   if (!view_ok(view) || !proj || !intensity || !dL_dS || !acc_img) return SDGR_ERR_INVALID;
   return launch_grad_image(*view, *proj, intensity, dL_dS, acc_img, static_cast<cudaStream_t>(stream));
 }
 
 int sdgr_grad_intensity(const sdgr_view* view, const sdgr_projection* proj, const sdgr_tiles* comp,
-                        double s_stop, const double* seg_base, const float* dL_dI, double* seg_g,
-                        double* seg_d, float* acc_comp, void* stream) {
-  if (!view_ok(view) || !proj || !tiles_ok(comp) || comp->plane != 0 || !dL_dI || !acc_comp)
+                        double s_stop, const double* seg_base, const double* dL_dI, double* seg_g,
+                        double* seg_d, double* partial_g, void* stream) {
+  if (!view_ok(view) || !proj || !tiles_ok(comp) || comp->plane != 0 || !dL_dI) return SDGR_ERR_INVALID;
+  if (comp->n_pairs > 0 && (!seg_base || !seg_g || !seg_d || !partial_g || !comp->pair_pos))
     return SDGR_ERR_INVALID;
-  if (comp->n_pairs > 0 && (!seg_base || !seg_g || !seg_d)) return SDGR_ERR_INVALID;
-  return launch_grad_intensity(*view, *proj, *comp, s_stop, seg_base, dL_dI, seg_g, seg_d, acc_comp,
+  if (std::isnan(s_stop)) return SDGR_ERR_INVALID;
+  return launch_grad_intensity(*view, *proj, *comp, s_stop, seg_base, dL_dI, seg_g, seg_d, partial_g,
                                static_cast<cudaStream_t>(stream));
 }
 
 int sdgr_grad_geometry(const sdgr_scene* scene, const sdgr_view* view, const sdgr_projection* proj,
-                       const float* acc_img, const float* acc_comp, sdgr_grads* out, int accumulate,
-                       void* stream) {
-  if (!scene || !view_ok(view) || !proj || !acc_img || !acc_comp || !out) return SDGR_ERR_INVALID;
+                       const sdgr_tiles* comp, const double* acc_img, const double* partial_g,
+                       sdgr_grads* out, int accumulate, void* stream) {
+  if (!scene || !view_ok(view) || !proj || !comp || comp->plane != 0 || !comp->pair_start || !acc_img ||
+      !out)
+    return SDGR_ERR_INVALID;
+  if (comp->n_pairs > 0 && !partial_g) return SDGR_ERR_INVALID;
   if (scene->n != proj->n) return SDGR_ERR_STATE;
-  return launch_grad_geometry(*scene, *view, *proj, acc_img, acc_comp, *out, accumulate,
+  return launch_grad_geometry(*scene, *view, *proj, *comp, acc_img, partial_g, *out, accumulate,
                               static_cast<cudaStream_t>(stream));
 }
 

@@ -82,10 +82,10 @@ __device__ __forceinline__ double quadform(double a00, double a01, double a11,
   return dadd(dadd(t1, t2), t3);
 }
 
-__device__ __forceinline__ float softplusf64(double x) {
+__device__ __forceinline__ double softplus64(double x) {
   // np.logaddexp(0, x) = max(x,0) + log1p(exp(-|x|))  (scene.py:22-25)
-  double ax = fabs(x);
-  return (float)(fmax(x, 0.0) + log1p(exp(-ax)));
+  if (!(x == x)) return x;
+  return fmax(x, 0.0) + log1p(exp(-fabs(x)));
 }
 
 // Launch accounting (sdgr_launch_count).

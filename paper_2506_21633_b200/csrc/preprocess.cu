@@ -249,20 +249,19 @@ __global__ void __launch_bounds__(256) k_project(sdgr_scene scene, sdgr_view vie
 #pragma unroll
       for (int k = 0; k < 16; ++k) praw += b[k] * ld(S, 16 * g + k);
       const T* K = static_cast<const T*>(scene.ke_raw);
-      const float kf = softplusf64(ld(K, 2 * g)), kb = softplusf64(ld(K, 2 * g + 1));
+      const double kf = softplus64(ld(K, 2 * g)), kb = softplus64(ld(K, 2 * g + 1));
       proj.kappa[g] = kf + kb;
-      proj.phase[g] = (float)fmax(praw, 0.0);
-      proj.phase_raw[g] = (float)praw;
-      if (!(praw == praw)) proj.phase[g] = (float)praw;  // NaN propagates (np.maximum)
-      if (proj.ke_act) reinterpret_cast<float2*>(proj.ke_act)[g] = make_float2(kf, kb);
+      proj.phase[g] = (praw == praw) ? fmax(praw, 0.0) : praw;  // NaN propagates (np.maximum)
+      proj.phase_raw[g] = praw;
+      if (proj.ke_act) reinterpret_cast<double2*>(proj.ke_act)[g] = make_double2(kf, kb);
       if (proj.look) reinterpret_cast<double4*>(proj.look)[g] = make_double4(d0, d1, d2, dist);
     } else {
       plane_empty(proj.comp, g);
       plane_empty(proj.img, g);
       proj.depth_key[g] = ~0ull;
-      proj.kappa[g] = 0.f;
-      proj.phase[g] = 0.f;
-      proj.phase_raw[g] = 0.f;
+      proj.kappa[g] = 0.0;
+      proj.phase[g] = 0.0;
+      proj.phase_raw[g] = 0.0;
       // accessor arrays keep the raw projection for non-visible rows too
       reinterpret_cast<double2*>(proj.comp.uv)[g] = make_double2(uc, vc);
       reinterpret_cast<double2*>(proj.img.uv)[g] = make_double2(ui, vi);

@@ -110,12 +110,12 @@ class Projection:
         self.comp = _PlaneRecords(n, device, accessors)
         self.img = _PlaneRecords(n, device, accessors)
         self.depth_key = _empty((n,), torch.int64, device)
-        self.kappa = _empty((n,), torch.float32, device)
-        self.phase_f = _empty((n,), torch.float32, device)
-        self.phase_raw = _empty((n,), torch.float32, device)
+        self.kappa = _empty((n,), torch.float64, device)
+        self.phase_f = _empty((n,), torch.float64, device)
+        self.phase_raw = _empty((n,), torch.float64, device)
         self.flags = _empty((n,), torch.uint8, device)
         self.counters = torch.zeros((4,), dtype=torch.int32, device=device)
-        self.ke_act = _empty((n, 2), torch.float32, device) if accessors else None
+        self.ke_act = _empty((n, 2), torch.float64, device) if accessors else None
         self.look = _empty((n, 4), torch.float64, device) if accessors else None
         self._vis_idx = None
         self._counts = None
@@ -261,7 +261,10 @@ class TileLists:
     tiles_y: int
     n_pairs: int
     pair_tile: torch.Tensor
+    pair_pos: torch.Tensor
     pair_prim: torch.Tensor
+    pre_prim: torch.Tensor
+    pair_start: torch.Tensor
     tile_range: torch.Tensor
     seg_len: int
     max_items: int
@@ -279,7 +282,8 @@ class TileLists:
             d = _lib.TilesDesc()
             d.plane, d.tiles_x, d.tiles_y, d.n_tiles = self.plane, self.tiles_x, self.tiles_y, self.n_tiles
             d.n_pairs = self.n_pairs
-            d.pair_tile, d.pair_prim, d.tile_range = ptr(self.pair_tile), ptr(self.pair_prim), ptr(self.tile_range)
+            d.pair_tile, d.pair_pos, d.pair_prim = ptr(self.pair_tile), ptr(self.pair_pos), ptr(self.pair_prim)
+            d.pre_prim, d.pair_start, d.tile_range = ptr(self.pre_prim), ptr(self.pair_start), ptr(self.tile_range)
             d.seg_len, d.max_items = self.seg_len, self.max_items
             d.items, d.tile_first, d.n_items = ptr(self.items), ptr(self.tile_first), ptr(self.n_items)
             self._desc = d
@@ -337,7 +341,10 @@ class _Binner:
             tl = TileLists(
                 plane=pl, n_u=nu, n_v=nv, tiles_x=tx, tiles_y=ty, n_pairs=int(total),
                 pair_tile=_empty((max(total, 1),), torch.int32, dev),
+                pair_pos=_empty((max(total, 1),), torch.int32, dev),
                 pair_prim=_empty((max(total, 1),), torch.int32, dev),
+                pre_prim=_empty((max(total, 1),), torch.int32, dev),
+                pair_start=_empty((n,), torch.int32, dev),
                 tile_range=_empty((tx * ty, 2), torch.int32, dev),
                 seg_len=seg, max_items=max_items,
                 items=_empty((max_items, 4), torch.int32, dev),
@@ -372,6 +379,7 @@ class IntensityBuffer:
     intensity_n: torch.Tensor
     seg_sum: torch.Tensor
     seg_base: torch.Tensor
+    partial: torch.Tensor
     status: torch.Tensor
     s_stop: float
     indices: torch.Tensor | None = None
@@ -389,15 +397,16 @@ def compute_intensities(rays: TileLists, projection: Projection, s_stop: float =
     n = projection.n_scene
     cap = max(rays.max_items, 1) * 256
     buf = IntensityBuffer(
-        intensity_n=_empty((n,), torch.float32, dev),
+        intensity_n=_empty((n,), torch.float64, dev),
         seg_sum=_empty((cap,), torch.float64, dev),
         seg_base=_empty((cap,), torch.float64, dev),
+        partial=_empty((max(rays.n_pairs, 1),), torch.float64, dev),
         status=torch.zeros((4,), dtype=torch.int32, device=dev),
         s_stop=float(s_stop),
     )
     _check(_lib.lib().sdgr_composite_forward(
         C.byref(projection.view), C.byref(projection._desc), C.byref(rays.desc()), float(s_stop),
-        ptr(buf.seg_sum), ptr(buf.seg_base), ptr(buf.intensity_n), ptr(buf.status), _stream()),
+        ptr(buf.seg_sum), ptr(buf.seg_base), ptr(buf.partial), ptr(buf.intensity_n), ptr(buf.status), _stream()),
         "sdgr_composite_forward")
     if check:
         _raise_if_nonfinite(buf, projection, rays)
@@ -448,12 +457,12 @@ def _first_bad_primitive(proj: Projection) -> int:
 
 def splat_image(intensities: IntensityBuffer, projection: Projection, config=None,
                 pairs: TileLists | None = None) -> torch.Tensor:
-    """forward.splat_image (forward.py:227-240): (n_range, n_azimuth) float32."""
+    """forward.splat_image (forward.py:227-240): (n_range, n_azimuth) float64."""
     if pairs is None:
         pairs = build_splat_lists(projection, config)
     v = projection.view
     dev = projection.flags.device
-    image = _empty((v.n_rg, v.n_az), torch.float32, dev)
+    image = _empty((v.n_rg, v.n_az), torch.float64, dev)
     part = _empty((max(pairs.max_items, 1) * 256,), torch.float64, dev)
     _check(_lib.lib().sdgr_splat(C.byref(v), C.byref(projection._desc), C.byref(pairs.desc()),
                                  ptr(intensities.intensity_n), ptr(part), ptr(image), _stream()),
@@ -477,7 +486,7 @@ class ForwardResult:
 
     @property
     def image(self):
-        return self.image_t.double().cpu().numpy() if self.host else self.image_t
+        return self.image_t.cpu().numpy() if self.host else self.image_t
 
 
 def render_forward(scene, config, cov_reg: float = DEFAULT_COV_REG, cutoff: float = DEFAULT_CUTOFF,
@@ -502,7 +511,7 @@ def render(scene, config, cov_reg: float = DEFAULT_COV_REG, cutoff: float = DEFA
     host = not (isinstance(scene, DeviceScene) or (isinstance(scene.positions, torch.Tensor)
                                                    and scene.positions.is_cuda))
     if len(scene) == 0:
-        img = torch.zeros((config.n_range, config.n_azimuth), dtype=torch.float32)
+        img = torch.zeros((config.n_range, config.n_azimuth), dtype=torch.float64)
         return img.double().numpy() if host else img.cuda()
     return render_forward(scene, config, cov_reg, cutoff, s_stop=s_stop, accessors=False).image
 
@@ -545,31 +554,32 @@ class SceneGradients:
 
 
 def grad_image_stage(fwd: ForwardResult, dL_dS: torch.Tensor) -> torch.Tensor:
-    """backward.grad_image_stage (backward.py:86-104): acc (6, N) =
+    """backward.grad_image_stage (backward.py:86-104): acc (6, N) float64 =
     [dL/dI, dL/dA00, dL/dA01, dL/dA11, dL/du, dL/dv] on the imaging plane."""
     p = fwd.projection
-    acc = _empty((6, p.n_scene), torch.float32, p.flags.device)
+    acc = _empty((6, p.n_scene), torch.float64, p.flags.device)
     _check(_lib.lib().sdgr_grad_image(C.byref(p.view), C.byref(p._desc), ptr(fwd.intensities.intensity_n),
                                       ptr(dL_dS), ptr(acc), _stream()), "sdgr_grad_image")
     return acc
 
 
 def grad_intensity_stage(fwd: ForwardResult, dL_dI: torch.Tensor) -> torch.Tensor:
-    """backward.grad_intensity_stage (backward.py:107-148): acc (7, N) =
-    [dL/dP, dL/dkappa, dL/dA00, dL/dA01, dL/dA11, dL/du, dL/dv] (comp plane)."""
+    """backward.grad_intensity_stage (backward.py:107-148): per-(tile, Gaussian)
+    partials (T16, 8) float64 = [dL/dP, dL/dkappa, dL/dA00, dL/dA01, dL/dA11,
+    dL/du, dL/dv, 0] on the computation plane, indexed by pre-sort position."""
     p, rays, buf = fwd.projection, fwd.rays, fwd.intensities
     dev = p.flags.device
-    acc = _empty((7, p.n_scene), torch.float32, dev)
+    partial = _empty((max(rays.n_pairs, 1), 8), torch.float64, dev)
     cap = max(rays.max_items, 1) * 256
     seg_g = _empty((cap,), torch.float64, dev)
     seg_d = _empty((cap,), torch.float64, dev)
     _check(_lib.lib().sdgr_grad_intensity(C.byref(p.view), C.byref(p._desc), C.byref(rays.desc()),
                                           buf.s_stop, ptr(buf.seg_base), ptr(dL_dI), ptr(seg_g), ptr(seg_d),
-                                          ptr(acc), _stream()), "sdgr_grad_intensity")
-    return acc
+                                          ptr(partial), _stream()), "sdgr_grad_intensity")
+    return partial
 
 
-def grad_geometry_stage(fwd: ForwardResult, acc_img: torch.Tensor, acc_comp: torch.Tensor,
+def grad_geometry_stage(fwd: ForwardResult, acc_img: torch.Tensor, partial_comp: torch.Tensor,
                         out: SceneGradients | None = None, accumulate: bool = False) -> SceneGradients:
     """grad_geometry_stage + grad_sh_stage + final scatter (backward.py:171-290)."""
     p = fwd.projection
@@ -577,17 +587,17 @@ def grad_geometry_stage(fwd: ForwardResult, acc_img: torch.Tensor, acc_comp: tor
         out = SceneGradients.zeros_device(p.n_scene, p.flags.device)
     sd = _scene_desc(fwd.device_scene)
     gd = out.desc()
-    _check(_lib.lib().sdgr_grad_geometry(C.byref(sd), C.byref(p.view), C.byref(p._desc), ptr(acc_img),
-                                         ptr(acc_comp), C.byref(gd), int(accumulate), _stream()),
-           "sdgr_grad_geometry")
+    _check(_lib.lib().sdgr_grad_geometry(C.byref(sd), C.byref(p.view), C.byref(p._desc),
+                                         C.byref(fwd.rays.desc()), ptr(acc_img), ptr(partial_comp),
+                                         C.byref(gd), int(accumulate), _stream()), "sdgr_grad_geometry")
     return out
 
 
 def _as_device_grad(dL_dS, fwd: ForwardResult) -> torch.Tensor:
     dev = fwd.projection.flags.device
     if isinstance(dL_dS, torch.Tensor):
-        return dL_dS.to(device=dev, dtype=torch.float32).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(dL_dS, dtype=np.float32)).to(dev)
+        return dL_dS.to(device=dev, dtype=torch.float64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(dL_dS, dtype=np.float64)).to(dev)
 
 
 def backward(fwd: ForwardResult, dL_dS, out: SceneGradients | None = None, accumulate: bool = False,
@@ -603,8 +613,8 @@ def backward(fwd: ForwardResult, dL_dS, out: SceneGradients | None = None, accum
     if validate and not bool(torch.isfinite(g).all().item()):
         raise InvalidParameterError("dL_dS contains non-finite values")
     acc_img = grad_image_stage(fwd, g)
-    acc_comp = grad_intensity_stage(fwd, acc_img[0])
-    grads = grad_geometry_stage(fwd, acc_img, acc_comp, out=out, accumulate=accumulate)
+    partial = grad_intensity_stage(fwd, acc_img[0])
+    grads = grad_geometry_stage(fwd, acc_img, partial, out=out, accumulate=accumulate)
     return grads.to_numpy() if fwd.host and out is None else grads
 
 
