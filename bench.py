@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""SDGR benchmark: SAR views/s, forward + custom backward, 1M Gaussians at 512x512.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sdgr|reference]
+
+Workload (BASELINE.json configs[3] / SURVEY.md §8d c4): 16 tanks on a 4x4
+grid (20 m pitch), 1 000 000 Gaussians, 512x512 views at az 0:360:3 x el
+{30, 45, 60} (360 views).  A step = every rank renders and back-propagates
+its shard of `--views-per-rank` views (default 45, so 8 ranks cover all 360)
+with gradients accumulated on the device, then one NCCL all-reduce of the
+per-Gaussian gradients.  Weak scaling: per-GPU work is fixed as N grows.
+
+`value`  : views/s over all ranks, inputs resident in HBM, CUDA events, max
+           over ranks.
+`e2e`    : the same step through the public API from pinned host memory
+           (scene + upstream gradients H2D, accumulated gradients D2H).
+`roofline`: HBM roofline of the preprocess + sort + binning kernels with the
+           SURVEY.md §8d algorithmic byte formula.
+`cpu_baseline`: the oracle port (oracle/sdgr_oracle.py, the reference's
+           algorithm restated in NumPy + C) on the host cores, rank 0, N=1.
+`--impl reference`: the reference's CPU path (oracle port; the reference is
+           pure Python and cannot travel to the GPU box) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SAR views/sec fwd+bwd (1M Gaussians, 512² px) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "views/s"
+RSS_PER_ORACLE_PROC = 7.5e9   # bytes, oracle fwd+bwd at 1M Gaussians / 512^2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="sdgr", choices=("sdgr", "reference"))
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--size", type=int, default=512)
+    ap.add_argument("--views-per-rank", type=int, default=45)
+    ap.add_argument("--param-dtype", default="f32", choices=("f32", "f64"))
+    ap.add_argument("--s-stop", type=float, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-procs", type=int, default=0)
+    return ap.parse_args()
+
+
+def view_list(size: int):
+    from paper_2506_21633_b200.radar import RadarConfig
+    out = []
+    for az in range(0, 360, 3):
+        for el in (30.0, 45.0, 60.0):
+            out.append(RadarConfig(azimuth_deg=float(az), elevation_deg=el, altitude_m=0.5, range_res_m=0.3,
+                                   azimuth_res_m=0.3, n_range=size, n_azimuth=size))
+    return out
+
+
+def make_scene(n: int):
+    from paper_2506_21633_b200 import targets
+    # float32-exact so the float32 device scene and the FP64 oracle see the same Gaussians
+    return targets.to_float32_exact(targets.tank_grid(n_total=n))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        self.tmp.flush()
+        rows = []
+        for line in Path(self.tmp.name).read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((float(f[1]), float(f[2]), f[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = sorted(r[0] for r in rows)
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- CPU side
+_CPU_SCENE = None
+_CPU_CFGS = None
+
+
+def _oracle_view(i):
+    from oracle import sdgr_oracle as O
+    cfg = _CPU_CFGS[i % len(_CPU_CFGS)]
+    rng = np.random.default_rng(i)
+    t0 = time.perf_counter()
+    f = O.render_forward(_CPU_SCENE, cfg)
+    O.backward(f, rng.normal(size=f.image.shape))
+    return time.perf_counter() - t0
+
+
+def cpu_procs(requested: int = 0) -> int:
+    cores = len(os.sched_getaffinity(0))
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 64e9
+    by_ram = max(1, int(0.8 * avail // RSS_PER_ORACLE_PROC))
+    p = min(cores, by_ram)
+    return max(1, min(p, requested)) if requested else p
+
+
+def cpu_run(scene, cfgs, procs: int, views: int):
+    """Run `views` oracle fwd+bwd views on `procs` forked processes; returns wall s."""
+    import multiprocessing as mp
+    global _CPU_SCENE, _CPU_CFGS
+    _CPU_SCENE, _CPU_CFGS = scene, cfgs
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        pool.map(_oracle_view, range(min(procs, 2)))   # warm the workers (imports, C lib)
+        t0 = time.perf_counter()
+        pool.map(_oracle_view, range(views), chunksize=1)
+        return time.perf_counter() - t0
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import sdgr_oracle
+    sdgr_oracle.build()
+    scene = make_scene(args.n)
+    cfgs = view_list(args.size)
+    procs = cpu_procs(args.cpu_procs)
+    # warm-up: one-time costs only (fork, imports, page-in) on a small sample
+    from paper_2506_21633_b200 import targets
+    small = targets.to_float32_exact(targets.tank_grid(n_total=16_000))
+    for _ in range(max(1, min(args.warmup, 1))):
+        cpu_run(small, view_list(128), procs, procs)
+    times = [cpu_run(scene, cfgs, procs, procs) for _ in range(args.steps)]
+    ms = 1e3 * float(np.mean(times))
+    value = procs / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c4: 16-tank grid, 1M Gaussians, 512x512, 360 views (az 0:360:3 x el 30/45/60)",
+                   "views_per_step": procs, "gaussians": args.n, "image": [args.size, args.size]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": f"{procs} c4 views per step, one per forked process "
+                                   "(oracle/sdgr_oracle.py: NumPy + C key chain, OPENBLAS_NUM_THREADS=1)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU side
+def hbm_bytes_per_view(n: int, t16: dict, tiles: dict) -> float:
+    """B_pre + B_rank + B_bin (algorithmic bytes, FP32 params)."""
+    b_pre = 184.0 * n
+    b_rank = 192.0 * n
+    b_bin = 0.0
+    for p in (0, 1):
+        b = math.ceil(math.log2(max(tiles[p], 2))) + math.ceil(math.log2(max(n, 2)))
+        b_bin += t16[p] * (12 + 24 * math.ceil(b / 8) + 8)
+    return b_pre + b_rank + b_bin
+
+
+def run_sdgr(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2506_21633_b200 as sdgr
+    from paper_2506_21633_b200.multiview import MultiViewStep
+
+    pdt = torch.float32 if args.param_dtype == "f32" else torch.float64
+    host_scene = make_scene(args.n)
+    cfgs_all = view_list(args.size)
+    # rank r takes views r, r+W, ... and the first views_per_rank of them
+    mine = [c for i, c in enumerate(cfgs_all) if i % world == rank]
+    mine = (mine * (1 + args.views_per_rank // max(len(mine), 1)))[: args.views_per_rank]
+    V = len(mine)
+    scene = sdgr.DeviceScene.from_host(host_scene, dtype=pdt)
+    kw = {} if args.s_stop is None else {"s_stop": args.s_stop}
+    step = MultiViewStep(scene, mine, **kw)
+    totals = []
+    mx = step.calibrate()
+    g = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    dl_host = torch.randn((V, args.size, args.size), generator=g, dtype=torch.float32)
+    dlds = dl_host.to("cuda").double()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        step.run(dlds)
+    torch.cuda.synchronize()
+    barrier()
+    # ---------------- timed: inputs resident in HBM ----------------
+    l0 = sdgr.launch_count()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k in range(args.steps):
+            step.run(dlds, timing=(k == args.steps - 1), check=False)
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    step.check()
+    launches = (sdgr.launch_count() - l0) // args.steps
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * V / (ms_max / 1e3)
+    stages = step.stage_times_ms()
+
+    # ---------------- e2e: public API from pinned host memory ----------------
+    e2e = None
+    if not args.no_e2e:
+        pin = {gname: torch.from_numpy(np.ascontiguousarray(getattr(host_scene, gname))).to(pdt).pin_memory()
+               for gname in ("positions", "rotations", "log_scales", "sh_coeffs", "ke_raw")}
+        dl_pin = dl_host.pin_memory()
+        out_pin = torch.empty(step.flat_soa.shape, dtype=torch.float32).pin_memory()
+        dl_dev32 = torch.empty_like(dl_host, device="cuda")
+        h2d = sum(p.numel() * p.element_size() for p in pin.values()) + dl_pin.numel() * dl_pin.element_size()
+        d2h = out_pin.numel() * out_pin.element_size()
+
+        def e2e_step():
+            for gname, p in pin.items():
+                getattr(scene, gname).copy_(p, non_blocking=True)
+            dl_dev32.copy_(dl_pin, non_blocking=True)
+            dlds.copy_(dl_dev32)
+            step.run(dlds, check=False)
+            out_pin.copy_(step.flat_soa, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        f1.record()
+        torch.cuda.synchronize()
+        step.check()
+        t = torch.tensor([f0.elapsed_time(f1) / args.steps], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * V / (float(t.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t.item())}
+
+    # ---------------- roofline (preprocess + sort + binning) ----------------
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    v0 = step.views[0]
+    tiles = {0: -(-v0.n_u // 16) * -(-v0.n_v // 16), 1: -(-v0.n_az // 16) * -(-v0.n_rg // 16)}
+    bpv = hbm_bytes_per_view(args.n, step.calib_t16_mean, tiles)
+    t_hbm_ms = stages["project"] + stages["depth_sort"] + stages["binning"]
+    achieved = bpv * V / (t_hbm_ms / 1e3) / 1e9 if t_hbm_ms > 0 else None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "kernels": "k_project + radix sorts + count/emit/ranges/items (both planes)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
+                "bytes_per_view": bpv}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c4: 16-tank grid, 1M Gaussians, 512x512, 360 views (az 0:360:3 x el 30/45/60)",
+                   "views_per_rank": V, "gaussians": args.n, "image": [args.size, args.size],
+                   "param_dtype": args.param_dtype, "parallelism": f"view-sharded dp{world}",
+                   "s_stop": step.s_stop, "l2": "inputs larger than L2 (112 MB params + ~0.3 GB/view records)",
+                   "t16_per_view": step.calib_t16_mean},
+        "roofline": roofline,
+        "stage_ms_per_step": stages,
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        procs = cpu_procs(args.cpu_procs)
+        wall = cpu_run(host_scene, cfgs_all, procs, procs)
+        line["cpu_baseline"] = {"value": procs / wall, "unit": UNIT, "cores": procs, "kind": "port",
+                                "sample": f"{procs} c4 views (1M Gaussians, 512x512), one per forked process, "
+                                          f"{wall:.1f} s wall"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_sdgr(args)
+
+
+if __name__ == "__main__":
+    main()

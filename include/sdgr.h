@@ -128,6 +128,9 @@ typedef struct sdgr_tiles {
   int32_t* tile_range;  /* (n_tiles,2) [start, end) into the sorted arrays    */
   int32_t seg_len;      /* max Gaussians per work item (depth segment)       */
   int32_t max_items;    /* capacity of items                                  */
+  int32_t device_count; /* 1: n_pairs is a capacity; the exact count stays on the
+                           device (offsets[n]) so no host round trip is needed */
+  int32_t pad_;
   int32_t* items;       /* (max_items,4) tile, start, end, first item of tile */
   int32_t* tile_first;  /* (n_tiles) index of each tile's first work item     */
   int32_t* n_items;     /* (4) device: [0] work items, [1] overflow flag, [2] walk counter */

@@ -57,7 +57,8 @@ class TilesDesc(C.Structure):
         ("plane", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("n_tiles", C.c_int32),
         ("n_pairs", C.c_int64), ("pair_tile", _p), ("pair_pos", _p), ("pair_prim", _p),
         ("pre_prim", _p), ("pair_start", _p), ("tile_range", _p),
-        ("seg_len", C.c_int32), ("max_items", C.c_int32), ("items", _p), ("tile_first", _p),
+        ("seg_len", C.c_int32), ("max_items", C.c_int32), ("device_count", C.c_int32), ("pad_", C.c_int32),
+        ("items", _p), ("tile_first", _p),
         ("n_items", _p),
     ]
 

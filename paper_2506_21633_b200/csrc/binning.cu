@@ -27,11 +27,21 @@ constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kCountMask = (1u << 30)
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 // ------------------------------------------------------------ histogram ----
+// Item counts may live on the device (n_dev != NULL): the host passes a
+// capacity n and the kernels use min(*n_dev, n), so the whole binning chain
+// runs without a host round trip (and can be graph-captured).
+__device__ __forceinline__ int64_t eff_count(int64_t n, const int32_t* n_dev) {
+  if (!n_dev) return n;
+  const int64_t d = *n_dev;
+  return d < n ? d : n;
+}
+
 template <typename K>
-__global__ void __launch_bounds__(256) k_radix_hist(const K* __restrict__ keys, int64_t n,
-                                                    int begin_bit, int npass,
+__global__ void __launch_bounds__(256) k_radix_hist(const K* __restrict__ keys, int64_t n_cap,
+                                                    const int32_t* n_dev, int begin_bit, int npass,
                                                     uint32_t* __restrict__ hist) {
   __shared__ uint32_t sh[8][256];
+  const int64_t n = eff_count(n_cap, n_dev);
   for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -65,8 +75,9 @@ __global__ void k_radix_hist_scan(const uint32_t* __restrict__ hist, uint32_t* _
 template <typename K, bool kIota>
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
-    uint32_t* __restrict__ vout, int64_t n, int shift, const uint32_t* __restrict__ base,
-    uint32_t* status, uint32_t* counter) {
+    uint32_t* __restrict__ vout, int64_t n_cap, const int32_t* n_dev, int shift,
+    const uint32_t* __restrict__ base, uint32_t* status, uint32_t* counter) {
+  const int64_t n = eff_count(n_cap, n_dev);
   extern __shared__ __align__(16) unsigned char dyn[];
   K* skeys = reinterpret_cast<K*>(dyn);
   uint32_t* svals = reinterpret_cast<uint32_t*>(dyn + sizeof(K) * kSortTile);
@@ -82,6 +93,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   __syncthreads();
   const int bid = bid_s;
   const int64_t tile0 = (int64_t)bid * kSortTile;
+  if (tile0 >= n && bid > 0) return;  // beyond the device count: nobody waits on us
   const uint32_t lt = (1u << lane) - 1u;
 
   K keys[kSortIpt];
@@ -198,7 +210,8 @@ void set_sort_smem() {
 // means values are the input positions.  Output lands in kout/vout.
 template <typename K>
 int radix_sort(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64_t n,
-               int begin_bit, int end_bit, void* ws, size_t ws_bytes, cudaStream_t st) {
+               const int32_t* n_dev, int begin_bit, int end_bit, void* ws, size_t ws_bytes,
+               cudaStream_t st) {
   if (n <= 0) return SDGR_OK;
   const int npass = (end_bit - begin_bit + 7) / 8;
   if (npass < 1 || npass > 8) return SDGR_ERR_INVALID;
@@ -219,7 +232,7 @@ int radix_sort(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64
       cudaSuccess)
     return SDGR_ERR_CUDA;
   const int hist_blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  k_radix_hist<K><<<hist_blocks, 256, 0, st>>>(kin, n, begin_bit, npass, hist);
+  k_radix_hist<K><<<hist_blocks, 256, 0, st>>>(kin, n, n_dev, begin_bit, npass, hist);
   k_radix_hist_scan<<<npass, 256, 0, st>>>(hist, base);
   note_launch(2);
   const size_t smem = (sizeof(K) + 4) * kSortTile;
@@ -233,10 +246,10 @@ int radix_sort(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64
     uint32_t* stat = status + (size_t)pass * nblk * 256;
     if (pass == 0 && vin == nullptr)
       k_onesweep<K, true><<<(unsigned)nblk, kSortThreads, smem, st>>>(
-          ki, vi, ko, vo, n, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
+          ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
     else
       k_onesweep<K, false><<<(unsigned)nblk, kSortThreads, smem, st>>>(
-          ki, vi, ko, vo, n, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
+          ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
     note_launch();
     ki = ko;
     vi = vo;
@@ -245,9 +258,9 @@ int radix_sort(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64
 }
 
 template int radix_sort<uint64_t>(const uint64_t*, const uint32_t*, uint64_t*, uint32_t*,
-                                  int64_t, int, int, void*, size_t, cudaStream_t);
+                                  int64_t, const int32_t*, int, int, void*, size_t, cudaStream_t);
 template int radix_sort<uint32_t>(const uint32_t*, const uint32_t*, uint32_t*, uint32_t*,
-                                  int64_t, int, int, void*, size_t, cudaStream_t);
+                                  int64_t, const int32_t*, int, int, void*, size_t, cudaStream_t);
 template size_t radix_ws_bytes<uint64_t>(int64_t, int);
 template size_t radix_ws_bytes<uint32_t>(int64_t, int);
 
@@ -356,7 +369,8 @@ __global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t
                                                     const int32_t* offsets, int64_t n,
                                                     int tiles_x, double cutoff,
                                                     uint32_t* keys, int32_t* vals,
-                                                    int32_t* pair_start) {
+                                                    int32_t* pair_start, int64_t cap,
+                                                    int32_t* overflow) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int32_t g = order ? order[i] : (int32_t)i;
@@ -364,6 +378,10 @@ __global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t
   int64_t o = offsets[i];
   pair_start[g] = (int32_t)o;
   if (cnt == 0) return;
+  if (o + cnt > cap) {  // caller's pair buffers are too small: flag, emit nothing
+    *overflow = 1;
+    return;
+  }
   const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
   const int tx0 = bb.x >> 4, tx1 = bb.y >> 4, ty0 = bb.z >> 4, ty1 = bb.w >> 4;
   if ((tx1 - tx0) < 8 && (ty1 - ty0) < 8) {
@@ -415,19 +433,20 @@ __device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* k, int64_t n,
   return lo;
 }
 
-__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, int64_t n, int n_tiles,
-                                                     int32_t* range) {
+__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, int64_t n_cap,
+                                                     const int32_t* n_dev, int n_tiles, int32_t* range) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_tiles) return;
+  const int64_t n = eff_count(n_cap, n_dev);
   range[2 * t] = (int32_t)lower_bound_u32(keys, n, (uint32_t)t);
   range[2 * t + 1] = (int32_t)lower_bound_u32(keys, n, (uint32_t)t + 1u);
 }
 
 // scene index of each sorted pair: pair_prim[i] = pre_prim[pair_pos[i]]
-__global__ void __launch_bounds__(256) k_gather_prim(const int32_t* pos, const int32_t* pre, int64_t n,
-                                                     int32_t* prim) {
+__global__ void __launch_bounds__(256) k_gather_prim(const int32_t* pos, const int32_t* pre, int64_t n_cap,
+                                                     const int32_t* n_dev, int32_t* prim) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) prim[i] = pre[pos[i]];
+  if (i < eff_count(n_cap, n_dev)) prim[i] = pre[pos[i]];
 }
 
 // depth-segment work items: each tile list is cut into segments of at most
@@ -472,11 +491,14 @@ int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, con
                          const int32_t* offsets, sdgr_tiles& tl, void* ws, size_t ws_bytes,
                          cudaStream_t st) {
   const sdgr_plane& pl = tl.plane == 0 ? proj.comp : proj.img;
-  const int64_t n = proj.n, np = tl.n_pairs;
+  const int64_t n = proj.n, np = tl.n_pairs;  // np: exact count, or capacity with a device count
+  // device-side pair count = offsets[n] (the scan's total) when capacity mode is on
+  const int32_t* n_dev = tl.device_count ? offsets + n : nullptr;
   if (cudaMemsetAsync(tl.tile_range, 0, sizeof(int32_t) * 2 * (size_t)tl.n_tiles, st) != cudaSuccess)
     return SDGR_ERR_CUDA;
+  // n_items[0] is written by k_make_items; n_items[1] (overflow) is sticky
+  // until the caller clears it, so one check can cover many views.
   int32_t* overflow = tl.n_items + 1;
-  if (cudaMemsetAsync(tl.n_items, 0, 2 * sizeof(int32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
   if (np > 0) {
     char* p = static_cast<char*>(ws);
     uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * np);
@@ -484,24 +506,24 @@ int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, con
     if (used > ws_bytes) return SDGR_ERR_CAPACITY;
     k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,
                                                               view.cutoff, keys, tl.pre_prim,
-                                                              tl.pair_start);
+                                                              tl.pair_start, np, overflow);
     note_launch();
     int bits = 1;
     while ((1 << bits) < tl.n_tiles) ++bits;
     // stable by tile; values = pre-sort positions (iota)
     const int rc = radix_sort<uint32_t>(keys, nullptr, tl.pair_tile,
-                                        reinterpret_cast<uint32_t*>(tl.pair_pos), np, 0, bits, p,
-                                        ws_bytes - used, st);
+                                        reinterpret_cast<uint32_t*>(tl.pair_pos), np, n_dev, 0, bits,
+                                        p, ws_bytes - used, st);
     if (rc != SDGR_OK) return rc;
-    k_tile_ranges<<<(unsigned)((tl.n_tiles + 255) / 256), 256, 0, st>>>(tl.pair_tile, np, tl.n_tiles,
-                                                                        tl.tile_range);
-    k_gather_prim<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(tl.pair_pos, tl.pre_prim, np,
+    k_tile_ranges<<<(unsigned)((tl.n_tiles + 255) / 256), 256, 0, st>>>(tl.pair_tile, np, n_dev,
+                                                                        tl.n_tiles, tl.tile_range);
+    k_gather_prim<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(tl.pair_pos, tl.pre_prim, np, n_dev,
                                                                 tl.pair_prim);
     note_launch(2);
   } else {
     k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,
                                                               view.cutoff, nullptr, nullptr,
-                                                              tl.pair_start);
+                                                              tl.pair_start, 0, overflow);
     note_launch();
   }
   k_make_items<<<1, 1024, 0, st>>>(tl.tile_range, tl.n_tiles, tl.seg_len, tl.max_items, tl.items,
@@ -527,7 +549,7 @@ int launch_depth_order(const sdgr_projection& proj, int32_t* order, void* ws, si
   const size_t used = align_up(sizeof(uint64_t) * (size_t)n);
   if (used > ws_bytes) return SDGR_ERR_CAPACITY;
   return radix_sort<uint64_t>(proj.depth_key, nullptr, ksorted, reinterpret_cast<uint32_t*>(order), n,
-                              0, 64, static_cast<char*>(ws) + used, ws_bytes - used, st);
+                              nullptr, 0, 64, static_cast<char*>(ws) + used, ws_bytes - used, st);
 }
 
 }  // namespace sdgr

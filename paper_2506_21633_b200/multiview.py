@@ -1,0 +1,264 @@
+"""Multi-view SDGR steps: forward + backward over many views, one all-reduce.
+
+This is the reconstruction-loop shape of the reference's caller
+(optimize.train, optimize.py:395-425) scaled out: every rank holds the full
+(replicated) Gaussian scene, renders and back-propagates its own shard of the
+SAR views with gradients accumulated on the device, and the per-Gaussian
+gradients are summed across ranks with one NCCL all-reduce per step
+(SURVEY.md §8e).  GradAccumulator semantics (optimize.py:229-233) are kept by
+summing uv_grad_norm and visible counts too.
+
+Per view the whole chain -- K1 preprocess, K2-K5 binning, K6/K7 forward,
+K8-K10 backward -- is launched with no host round trip: pair buffers use
+capacities cached from a calibration pass and the exact counts stay on the
+device.  Capacity overflow is detected on the device and checked once per
+step; on overflow the step is recalibrated and re-run.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ptr
+from .errors import NumericalError
+from .radar import view_constants
+from .rasterizer import (DEFAULT_COV_REG, DEFAULT_CUTOFF, S_STOP, SceneGradients, TILE, _check, _empty,
+                         _scene_desc, _seg_len, _stream)
+from .scene import DeviceScene
+
+GRAD_WIDTH = 30  # 3 + 4 + 3 + 16 + 2 + uv_grad_norm + (visible as int32 view)
+
+
+def shard_views(configs, rank: int, world: int):
+    """Views for `rank`: {v : v mod world == rank} (interleaves elevations)."""
+    return [c for i, c in enumerate(configs) if i % world == rank]
+
+
+@dataclass
+class _PlaneBufs:
+    offsets: torch.Tensor
+    tiles: object  # TilesDesc
+    t: dict
+
+
+class MultiViewStep:
+    """Forward + backward of a list of views with on-device accumulation."""
+
+    def __init__(self, scene: DeviceScene, configs, cov_reg: float = DEFAULT_COV_REG,
+                 cutoff: float = DEFAULT_CUTOFF, s_stop: float = S_STOP, headroom: float = 1.3,
+                 group=None):
+        self.scene = scene
+        self.configs = list(configs)
+        self.views = [view_constants(c, cov_reg, cutoff) for c in self.configs]
+        self.s_stop = float(s_stop)
+        self.headroom = headroom
+        self.group = group
+        self.dev = scene.device
+        self.n = len(scene)
+        self.lib = _lib.lib()
+        self.sd = _scene_desc(scene)
+        n, dev = self.n, self.dev
+        shapes = {(v.n_rg, v.n_az) for v in self.views}
+        if len(shapes) != 1:
+            raise ValueError("all views of a step must share the image size")
+        self.img_shape = shapes.pop()
+        # per-view (reused) projection records
+        self.rec = {}
+        for name in ("comp", "img"):
+            self.rec[name] = dict(uv=_empty((n, 2), torch.float64, dev), inv_cov=_empty((n, 4), torch.float64, dev),
+                                  bbox=_empty((n, 4), torch.int16, dev), cell_mask=_empty((n,), torch.int64, dev),
+                                  tile_mask=_empty((n,), torch.int64, dev), n_tiles=_empty((n,), torch.int32, dev))
+        self.depth_key = _empty((n,), torch.int64, dev)
+        self.kappa = _empty((n,), torch.float64, dev)
+        self.phase = _empty((n,), torch.float64, dev)
+        self.phase_raw = _empty((n,), torch.float64, dev)
+        self.flags = _empty((n,), torch.uint8, dev)
+        self.counters = torch.zeros((4,), dtype=torch.int32, device=dev)
+        self.pd = _lib.ProjectionDesc()
+        self.pd.n = n
+        for name in ("comp", "img"):
+            pl = _lib.Plane()
+            r = self.rec[name]
+            pl.uv, pl.inv_cov, pl.cov, pl.bbox = ptr(r["uv"]), ptr(r["inv_cov"]), None, ptr(r["bbox"])
+            pl.cell_mask, pl.tile_mask, pl.n_tiles = ptr(r["cell_mask"]), ptr(r["tile_mask"]), ptr(r["n_tiles"])
+            setattr(self.pd, name, pl)
+        self.pd.depth_key, self.pd.kappa, self.pd.phase = ptr(self.depth_key), ptr(self.kappa), ptr(self.phase)
+        self.pd.phase_raw, self.pd.flags, self.pd.counters = ptr(self.phase_raw), ptr(self.flags), ptr(self.counters)
+        self.pd.ke_act = None
+        self.pd.look = None
+        self.order = _empty((n,), torch.int32, dev)
+        self.intensity = _empty((n,), torch.float64, dev)
+        self.image = _empty(self.img_shape, torch.float64, dev)
+        self.acc_img = _empty((6, n), torch.float64, dev)
+        self.status = torch.zeros((4,), dtype=torch.int32, device=dev)
+        # gradients: one flat float32 buffer so the all-reduce is one call
+        self.grads = self._grad_views()
+        self.gd = self.grads.desc()
+        self.cap = None
+        self.planes = None
+        self.stage_events = None
+
+    # -- buffers ------------------------------------------------------------
+    def _grad_views(self) -> SceneGradients:
+        n = self.n
+        # SoA views into one (30, n)-shaped storage keep each group contiguous
+        self.flat_soa = torch.zeros((GRAD_WIDTH * n,), dtype=torch.float32, device=self.dev)
+        s = self.flat_soa
+        o = 0
+        parts = []
+        for w in (3, 4, 3, 16, 2, 1):
+            parts.append(s[o:o + w * n].view(n, w) if w > 1 else s[o:o + n])
+            o += w * n
+        vis = s[o:o + n].view(torch.int32)
+        return SceneGradients(*parts, vis)
+
+    def _alloc_planes(self, cap_pairs: dict):
+        n, dev = self.n, self.dev
+        v = self.views[0]
+        self.planes = {}
+        ws_need = self.lib.sdgr_workspace_bytes(n, max(cap_pairs.values()))
+        self.ws = _empty((ws_need,), torch.uint8, dev)
+        self.ws_bytes = ws_need
+        for pl in (0, 1):
+            cap = cap_pairs[pl]
+            nu, nv = (v.n_u, v.n_v) if pl == 0 else (v.n_az, v.n_rg)
+            tx, ty = -(-nu // TILE), -(-nv // TILE)
+            seg = _seg_len(cap)
+            max_items = -(-cap // seg) + tx * ty
+            t = dict(
+                pair_tile=_empty((cap,), torch.int32, dev), pair_pos=_empty((cap,), torch.int32, dev),
+                pair_prim=_empty((cap,), torch.int32, dev), pre_prim=_empty((cap,), torch.int32, dev),
+                pair_start=_empty((n,), torch.int32, dev), tile_range=_empty((tx * ty, 2), torch.int32, dev),
+                items=_empty((max_items, 4), torch.int32, dev), tile_first=_empty((tx * ty,), torch.int32, dev),
+                n_items=torch.zeros((4,), dtype=torch.int32, device=dev),
+                seg_a=_empty((max_items * 256,), torch.float64, dev),
+                seg_b=_empty((max_items * 256,), torch.float64, dev),
+            )
+            if pl == 0:
+                t["partial_I"] = _empty((cap,), torch.float64, dev)
+                t["partial_g"] = _empty((cap, 8), torch.float64, dev)
+                t["seg_c"] = _empty((max_items * 256,), torch.float64, dev)
+            d = _lib.TilesDesc()
+            d.plane, d.tiles_x, d.tiles_y, d.n_tiles = pl, tx, ty, tx * ty
+            d.n_pairs = cap
+            for k in ("pair_tile", "pair_pos", "pair_prim", "pre_prim", "pair_start", "tile_range", "items",
+                      "tile_first", "n_items"):
+                setattr(d, k, ptr(t[k]))
+            d.seg_len, d.max_items, d.device_count = seg, max_items, 1
+            self.planes[pl] = _PlaneBufs(offsets=_empty((n + 1,), torch.int32, dev), tiles=d, t=t)
+        self.cap = dict(cap_pairs)
+
+    def calibrate(self):
+        """Measure the pair counts of every view (host syncs) and size buffers."""
+        mx = {0: 1, 1: 1}
+        st = _stream()
+        ws_bytes = self.lib.sdgr_workspace_bytes(self.n, 1)
+        ws = _empty((ws_bytes,), torch.uint8, self.dev)
+        off = {pl: _empty((self.n + 1,), torch.int32, self.dev) for pl in (0, 1)}
+        self.calib_t16 = []
+        for v in self.views:
+            _check(self.lib.sdgr_project(C.byref(self.sd), C.byref(v), C.byref(self.pd), st), "sdgr_project")
+            _check(self.lib.sdgr_depth_order(C.byref(self.pd), ptr(self.order), ptr(ws), ws_bytes, st),
+                   "sdgr_depth_order")
+            for pl in (0, 1):
+                _check(self.lib.sdgr_count_pairs(C.byref(self.pd), pl, ptr(self.order) if pl == 0 else None,
+                                                 ptr(off[pl]), ptr(ws), ws_bytes, st), "sdgr_count_pairs")
+            tot = torch.stack([off[0][self.n], off[1][self.n]]).cpu().tolist()
+            mx = {0: max(mx[0], tot[0]), 1: max(mx[1], tot[1])}
+            self.calib_t16.append(tot)
+        self.calib_t16_mean = {pl: float(np.mean([t[pl] for t in self.calib_t16])) for pl in (0, 1)}
+        self._alloc_planes({pl: int(mx[pl] * self.headroom) + 1024 for pl in (0, 1)})
+        return mx
+
+    # -- one view -----------------------------------------------------------
+    def _view(self, v, dlds: torch.Tensor, ev=None):
+        lib, st, pd = self.lib, _stream(), C.byref(self.pd)
+        P0, P1 = self.planes[0], self.planes[1]
+        t0, t1 = P0.t, P1.t
+
+        def mark(i):
+            if ev is not None:
+                ev[i].record()
+        mark(0)
+        _check(lib.sdgr_project(C.byref(self.sd), C.byref(v), pd, st), "sdgr_project")
+        mark(1)
+        _check(lib.sdgr_depth_order(pd, ptr(self.order), ptr(self.ws), self.ws_bytes, st), "sdgr_depth_order")
+        mark(2)
+        for pl, P in ((0, P0), (1, P1)):
+            _check(lib.sdgr_count_pairs(pd, pl, ptr(self.order) if pl == 0 else None, ptr(P.offsets),
+                                        ptr(self.ws), self.ws_bytes, st), "sdgr_count_pairs")
+            _check(lib.sdgr_bin_pairs(pd, C.byref(v), ptr(self.order) if pl == 0 else None, ptr(P.offsets),
+                                      C.byref(P.tiles), ptr(self.ws), self.ws_bytes, st), "sdgr_bin_pairs")
+        mark(3)
+        _check(lib.sdgr_composite_forward(C.byref(v), pd, C.byref(P0.tiles), self.s_stop, ptr(t0["seg_a"]),
+                                          ptr(t0["seg_b"]), ptr(t0["partial_I"]), ptr(self.intensity),
+                                          ptr(self.status), st), "sdgr_composite_forward")
+        mark(4)
+        _check(lib.sdgr_splat(C.byref(v), pd, C.byref(P1.tiles), ptr(self.intensity), ptr(t1["seg_a"]),
+                              ptr(self.image), st), "sdgr_splat")
+        mark(5)
+        _check(lib.sdgr_grad_image(C.byref(v), pd, ptr(self.intensity), ptr(dlds), ptr(self.acc_img), st),
+               "sdgr_grad_image")
+        mark(6)
+        # seg_b holds the forward's exclusive prefixes; seg_a is reused as scratch
+        _check(lib.sdgr_grad_intensity(C.byref(v), pd, C.byref(P0.tiles), self.s_stop, ptr(t0["seg_b"]),
+                                       ptr(self.acc_img[0]), ptr(t0["seg_a"]), ptr(t0["seg_c"]),
+                                       ptr(t0["partial_g"]), st), "sdgr_grad_intensity")
+        mark(7)
+        _check(lib.sdgr_grad_geometry(C.byref(self.sd), C.byref(v), pd, C.byref(P0.tiles), ptr(self.acc_img),
+                                      ptr(t0["partial_g"]), C.byref(self.gd), 1, st), "sdgr_grad_geometry")
+        mark(8)
+
+    def run(self, dlds: torch.Tensor, timing: bool = False, check: bool = True):
+        """Forward + backward of every view; dlds: (V, H, W) float64 on device.
+        Returns the accumulated SceneGradients (all-reduced if distributed)."""
+        if self.cap is None:
+            self.calibrate()
+        if dlds.shape[0] != len(self.views):
+            raise ValueError("one upstream image gradient per view")
+        self.flat_soa.zero_()
+        self.status.zero_()
+        for P in self.planes.values():
+            P.t["n_items"].zero_()   # sticky overflow flags: one check per step
+        evs = []
+        for i, v in enumerate(self.views):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)] if timing else None
+            self._view(v, dlds[i], ev)
+            if timing:
+                evs.append(ev)
+        self.stage_events = evs
+        if self.group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
+            self.allreduce()
+        if check:
+            self.check()
+        return self.grads
+
+    def allreduce(self):
+        import torch.distributed as dist
+        n = self.n
+        fl = self.flat_soa[: 29 * n]
+        dist.all_reduce(fl, group=self.group)
+        dist.all_reduce(self.flat_soa[29 * n:].view(torch.int32), group=self.group)
+
+    def check(self):
+        """One host read per step: capacity overflow and non-finite status."""
+        flags = torch.stack([self.planes[0].t["n_items"][1], self.planes[1].t["n_items"][1], self.status[0]])
+        ov0, ov1, bad = flags.cpu().tolist()
+        if ov0 or ov1:
+            raise OverflowError("pair capacity exceeded; recalibrate")
+        if bad:
+            raise NumericalError("non-finite intensity in a multi-view step")
+
+    def stage_times_ms(self):
+        """Per-stage device time summed over the last timed run's views."""
+        names = ("project", "depth_sort", "binning", "forward_comp", "splat", "grad_image",
+                 "grad_intensity", "grad_geometry")
+        out = dict.fromkeys(names, 0.0)
+        for ev in self.stage_events or []:
+            for i, nm in enumerate(names):
+                out[nm] += ev[i].elapsed_time(ev[i + 1])
+        return out
