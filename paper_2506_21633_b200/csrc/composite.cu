@@ -1,22 +1,28 @@
 // composite.cu — K6/K7/K9: the tile walks.
 //
 // A work item is one depth segment (<= seg_len Gaussians) of one 16x16 tile
-// list.  A persistent CTA of 256 threads pulls items from an atomic counter;
-// thread r owns ray (cell / pixel) r of the tile.  The segment is processed in
-// chunks of 256 Gaussians:
-//   1. thread j stages Gaussian j (center, inverse covariance, kappa, P, ...)
-//      in shared memory and derives its 256-bit in-tile member mask from the
-//      8x8 cell window K1 stored (the exact FP64 membership decision is
-//      reused, never recomputed); it ORs bit j into the rows of the
-//      cell-major 256x256 membership bitmap;
-//   2. thread r walks the set bits of its cell's row in ascending order --
-//      exactly its ray's member list in (depth, index) order -- and applies
-//      the mode's per-pair update in FP64;
-//   3. (kContrib, kGrad) per-pair values go to a shared-memory pool at a slot
-//      fixed by the Gaussian's member mask; thread j then reduces its own
-//      slots in cell order and writes ONE partial record per (tile, Gaussian)
-//      pair, indexed by the pair's pre-sort position.  No atomics on the
-//      common path and a fixed summation order: results are deterministic.
+// list.  A persistent CTA of 256 threads pulls items from an atomic counter.
+// Thread r owns ray (cell / pixel) r of the tile for the order-dependent
+// steps; thread j owns Gaussian j of the current chunk of 256.
+//
+// Per chunk:
+//   P0  thread j stages Gaussian j and derives its 256-bit in-tile member
+//       mask from the 8x8 cell window K1 stored (the exact FP64 membership is
+//       reused, never recomputed); bits go into a cell-major 256x256 bitmap.
+//   P1  thread r counts its ray's live members; a block scan lays every
+//       (ray, member) pair out in a flat shared array in ray-major,
+//       depth-minor order -- exactly the per-ray walk order of the reference.
+//   P2  thread j evaluates w = exp(-q) for each of its member cells (pair-
+//       parallel, full warps) into the pair's flat slot.
+//   P3  thread r runs the order-dependent part over its own slots: only
+//       additions (log-transmittance prefix, early ray termination).
+//   P4  flat pair-parallel pass: T = e^-S, 1 - e^-tau, contributions.
+//   P5  thread r: downstream suffix sums (backward only; additions).
+//   P7  thread j reduces its own pairs in cell order into ONE partial record
+//       per (tile, Gaussian) pair, indexed by the pair's pre-sort position:
+//       no atomics, fixed summation order => deterministic results.
+// If a chunk has more live pairs than the flat array holds it is processed
+// in sub-chunks of consecutive Gaussians (ray state carries over).
 //
 // Modes (reference stage they replace):
 //   kSum     segment optical-depth sums          (forward.py:182-187, cumsum)
@@ -35,7 +41,15 @@
 namespace sdgr {
 
 enum WalkMode { kSum = 0, kContrib = 1, kSplat = 2, kGSum = 3, kGrad = 4 };
-constexpr int kPool = 4096;  // pooled per-pair values per chunk
+
+template <int MODE>
+struct WalkCfg {
+  static constexpr int kCap = MODE == kGrad ? 2048 : 4096;            // flat pair slots
+  static constexpr bool kS = MODE == kContrib || MODE == kGSum || MODE == kGrad;
+  static constexpr bool kJ = kS;                                       // slot -> Gaussian
+  static constexpr bool kXY = MODE == kGrad;
+  static constexpr size_t kSmem = kCap * (8 + (kS ? 8 : 0) + (kXY ? 16 : 0) + (kJ ? 1 : 0));
+};
 
 struct WalkArgs {
   sdgr_plane pl;
@@ -101,7 +115,8 @@ __device__ __forceinline__ void member_mask(short4 bb, uint64_t cm, double2 uv, 
   }
 }
 
-__device__ __forceinline__ int block_excl_scan_i32(int x, int32_t* tmp) {
+// exclusive block scan (256 threads); also returns the block total
+__device__ __forceinline__ int block_scan(int x, int32_t* tmp, int& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int s = x;
 #pragma unroll
@@ -109,12 +124,26 @@ __device__ __forceinline__ int block_excl_scan_i32(int x, int32_t* tmp) {
     const int y = __shfl_up_sync(0xffffffffu, s, off);
     if (lane >= off) s += y;
   }
+  __syncthreads();
   if (lane == 31) tmp[warp] = s;
   __syncthreads();
-  int pre = 0;
-  for (int w = 0; w < warp; ++w) pre += tmp[w];
-  __syncthreads();
+  int pre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const int v = tmp[w];
+    pre += w < warp ? v : 0;
+    tot += v;
+  }
+  total = tot;
   return pre + s - x;
+}
+
+// bits of 32-bit word w that belong to Gaussians [j0, j1)
+__device__ __forceinline__ uint32_t range_mask(int w, int j0, int j1) {
+  const int lo = max(j0 - 32 * w, 0), hi = min(j1 - 32 * w, 32);
+  if (hi <= lo) return 0u;
+  const uint32_t upper = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+  return upper & ~((1u << lo) - 1u);
 }
 
 // Gradient terms of one computation-plane pair (backward.py:122-148) given
@@ -133,21 +162,25 @@ __device__ __forceinline__ void grad_terms(double y1, double y2, double kap, dou
 
 template <int MODE>
 __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
-  constexpr bool kPooled = MODE == kContrib || MODE == kGrad;
-  constexpr int kVals = MODE == kGrad ? 2 : 1;
-  constexpr int kGW = kPooled ? kChunk : 1;
-  __shared__ uint32_t cellbits[8 * kRays];
-  __shared__ uint64_t gbits[4 * kGW];
-  __shared__ uint32_t gpre[kGW];
-  __shared__ int32_t pool_off[kGW];
-  __shared__ int32_t spos[kGW];
+  using Cfg = WalkCfg<MODE>;
+  constexpr int kCap = Cfg::kCap;
+  __shared__ uint32_t rows[8 * kRays];   // rows[w*256 + r]: bit (j&31) of word w = Gaussian j covers ray r
+  __shared__ uint32_t wpre[2 * kRays];   // per ray: byte prefix counts of the masked words
+  __shared__ int32_t ray_off[kRays];
+  __shared__ uint32_t alive_bits[8];
   __shared__ double su[kChunk], sv[kChunk], sa0[kChunk], sa1[kChunk], sa2[kChunk];
   __shared__ double sk[kChunk], sp[kChunk], sg[kChunk];
   __shared__ int32_t scan_tmp[8];
+  __shared__ int32_t base_s;
   __shared__ int item_s;
-  extern __shared__ double pool[];
+  extern __shared__ double dyn[];
+  double* fw = dyn;                                         // w (kSum: tau, kSplat: w*I)
+  double* fs = fw + kCap;                                   // S / contrib / g*contrib / D
+  double* fx = fs + (Cfg::kS ? kCap : 0);                   // kGrad: g*T*a*P
+  double* fy = fx + (Cfg::kXY ? kCap : 0);                  // kGrad: T*(1-a)
+  uint8_t* fj = reinterpret_cast<uint8_t*>(fy + (Cfg::kXY ? kCap : 0));
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_items = *a.n_items;
   while (true) {
     __syncthreads();
@@ -160,23 +193,22 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     const int iu = tx * kTile + (tid & 15), iv = ty * kTile + (tid >> 4);
     const bool valid = iu < a.n_cols && iv < a.n_rows;
-    const double du = (double)iu, dv = (double)iv;
     const int64_t slot_ray = (int64_t)item * kRays + tid;
     double S = 0.0, accd = 0.0, rem = 0.0;
-    if (MODE == kContrib || MODE == kGSum || MODE == kGrad) S = a.seg_base[slot_ray];
+    if (Cfg::kS) S = a.seg_base[slot_ray];
     if (MODE == kGrad) rem = a.seg_d[slot_ray] + a.seg_g[slot_ray];
     bool alive = valid && (MODE == kSplat || S < a.s_stop);
     bool bad = false;
-    const int rw = tid >> 6;
-    const uint64_t rlow = (1ull << (tid & 63)) - 1ull;
 
     int cs = start;
     for (; cs < end; cs += kChunk) {
       if (!__syncthreads_or(alive)) break;
+      // ---- P0: stage Gaussian j = tid, build its member mask, scatter bits
 #pragma unroll
-      for (int w = 0; w < 8; ++w) cellbits[w * kRays + tid] = 0u;
+      for (int w = 0; w < 8; ++w) rows[w * kRays + tid] = 0u;
       const int idx = cs + tid;
-      const bool have = idx < end;
+      const int nG = min(kChunk, end - cs);
+      const bool have = tid < nG;
       uint64_t gm[4] = {0, 0, 0, 0};
       int pos = 0;
       if (have) {
@@ -189,20 +221,12 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
         sa0[tid] = A.x; sa1[tid] = A.y; sa2[tid] = A.z;
         if (MODE != kSplat) { sk[tid] = a.kappa[g]; sp[tid] = a.phase[g]; }
         if (MODE == kSplat || MODE == kGSum || MODE == kGrad) sg[tid] = a.gvec[g];
-        if (kPooled) {
-          pos = a.pair_pos[idx];
-          spos[tid] = pos;
-          const int c0 = __popcll(gm[0]), c1 = __popcll(gm[1]), c2 = __popcll(gm[2]);
-#pragma unroll
-          for (int w = 0; w < 4; ++w) gbits[w * kGW + tid] = gm[w];
-          gpre[tid] = (uint32_t)c0 << 8 | (uint32_t)(c0 + c1) << 16 | (uint32_t)(c0 + c1 + c2) << 24;
-        }
+        if (MODE == kContrib || MODE == kGrad) pos = a.pair_pos[idx];
       }
       __syncthreads();
-      // scatter this Gaussian into the cell-major bitmap
       {
-        const uint32_t bit = 1u << (tid & 31);
-        uint32_t* col = cellbits + (tid >> 5) * kRays;
+        const uint32_t bit = 1u << lane;
+        uint32_t* col = rows + warp * kRays;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           uint64_t m = gm[w];
@@ -213,121 +237,162 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
           }
         }
       }
-      int cnt = 0, off = 0;
-      if (kPooled) {
-        cnt = __popcll(gm[0]) + __popcll(gm[1]) + __popcll(gm[2]) + __popcll(gm[3]);
-        off = block_excl_scan_i32(cnt, scan_tmp);
-        pool_off[tid] = off;
-        for (int k = off; k < min(off + cnt, kPool); ++k)
+      double racc[7] = {0, 0, 0, 0, 0, 0, 0};  // P7 accumulators of Gaussian tid
+      int j0 = 0;
+      while (j0 < nG) {
+        // ---- live rays and the sub-chunk [j0, j1) that fits the flat array
+        const uint32_t ab = __ballot_sync(0xffffffffu, alive);
+        if (lane == 0) alive_bits[warp] = ab;
+        __syncthreads();
+        uint64_t lm[4];
 #pragma unroll
-          for (int v = 0; v < kVals; ++v) pool[k * kVals + v] = 0.0;
-        if (have && off + cnt > kPool) {  // overflow: ray threads add into the record
-          if (MODE == kContrib) a.partial[pos] = 0.0;
-          else
+        for (int w = 0; w < 4; ++w)
+          lm[w] = gm[w] & ((uint64_t)alive_bits[2 * w] | ((uint64_t)alive_bits[2 * w + 1] << 32));
+        const int cnt_g = (have && tid >= j0)
+                              ? __popcll(lm[0]) + __popcll(lm[1]) + __popcll(lm[2]) + __popcll(lm[3])
+                              : 0;
+        int tot_g;
+        const int excl_g = block_scan(cnt_g, scan_tmp, tot_g);
+        if (tid == j0) base_s = excl_g;
+        __syncthreads();
+        const bool fits = have && tid >= j0 && (excl_g + cnt_g - base_s) <= kCap;
+        const int j1 = j0 + __syncthreads_count(fits);
+        // ---- P1: per-ray counts of members in [j0, j1), flat offsets
+        int cnt_r = 0;
+        uint32_t pre_lo = 0, pre_hi = 0;
+        if (alive) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) a.partial[(int64_t)pos * 8 + k] = 0.0;
-        }
-      }
-      __syncthreads();
-      if (alive) {
-#pragma unroll 1
-        for (int w = 0; w < 8 && alive; ++w) {
-          uint32_t bits = cellbits[w * kRays + tid];
-          while (bits) {
-            const int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int jj = w * 32 + b;
-            const double dx = dsub(du, su[jj]), dy = dsub(dv, sv[jj]);
-            const double q = quadform(sa0[jj], sa1[jj], sa2[jj], dx, dy);
-            const double wgt = exp(-q);
-            if (MODE == kSplat) {
-              accd += wgt * sg[jj];
-              continue;
-            }
-            const double tau = sk[jj] * wgt;
-            if (MODE == kSum) {
-              S += tau;
-              if (S > a.s_stop) { alive = false; break; }
-              continue;
-            }
-            if (!(S < a.s_stop)) { alive = false; break; }
-            const double T = exp(-S);
-            const double oma = -expm1(-tau);
-            const double P = sp[jj];
-            const double c = T * oma * P;
-            int slot = 0;
-            if (kPooled)
-              slot = pool_off[jj] + (int)((gpre[jj] >> (8 * rw)) & 255u) +
-                     __popcll(gbits[rw * kGW + jj] & rlow);
-            if (MODE == kContrib) {
-              if (!isfinite(c)) bad = true;
-              if (slot < kPool) pool[slot] = c;
-              else atomicAdd(a.partial + spos[jj], c);
-            } else if (MODE == kGSum) {
-              accd += sg[jj] * c;
-            } else {  // kGrad
-              const double gI = sg[jj];
-              rem -= gI * c;  // downstream sum of g*contrib after this pair
-              const double dtau = gI * T * exp(-tau) * P - rem;
-              const double y1 = T * oma, y2 = dtau * wgt;
-              if (slot < kPool) {
-                pool[2 * slot] = y1;
-                pool[2 * slot + 1] = y2;
-              } else {
-                double r[7] = {0, 0, 0, 0, 0, 0, 0};
-                grad_terms(y1, y2, sk[jj], dx, dy, sa0[jj], sa1[jj], sa2[jj], r);
-                r[0] *= gI;
-                double* rec = a.partial + (int64_t)spos[jj] * 8;
-#pragma unroll
-                for (int k = 0; k < 7; ++k) atomicAdd(rec + k, r[k]);
-              }
-            }
-            S += tau;
+          for (int w = 0; w < 8; ++w) {
+            const int c = __popc(rows[w * kRays + tid] & range_mask(w, j0, j1));
+            if (w < 4) pre_lo |= (uint32_t)cnt_r << (8 * w);
+            else pre_hi |= (uint32_t)cnt_r << (8 * (w - 4));
+            cnt_r += c;
           }
         }
-      }
-      if (kPooled) {
+        wpre[tid] = pre_lo;
+        wpre[kRays + tid] = pre_hi;
+        int total;
+        const int roff = block_scan(cnt_r, scan_tmp, total);
+        ray_off[tid] = roff;
         __syncthreads();
-        if (have) {
-          // reduce this Gaussian's pooled pairs in ascending cell order
-          double r[7] = {0, 0, 0, 0, 0, 0, 0};
-          int k = off;
+        // ---- P2: Gaussian-parallel weights into the flat slots
+        const bool mine = have && tid >= j0 && tid < j1;
+        if (mine) {
+          const int jw = tid >> 5;
+          const uint32_t below = ((1u << lane) - 1u) & range_mask(jw, j0, j1);
+          const uint32_t pshift = 8 * (jw & 3);
+          const uint32_t* wp = wpre + (jw < 4 ? 0 : kRays);
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
-            uint64_t m = gm[w];
-            while (m && k < kPool) {
+            uint64_t m = lm[w];
+            while (m) {
               const int b = __ffsll((long long)m) - 1;
               m &= m - 1;
-              if (MODE == kContrib) {
-                r[0] += pool[k];
-              } else {
-                const int c = w * 64 + b;
-                const double dx = dsub((double)(tx * kTile + (c & 15)), su[tid]);
-                const double dy = dsub((double)(ty * kTile + (c >> 4)), sv[tid]);
-                grad_terms(pool[2 * k], pool[2 * k + 1], sk[tid], dx, dy, sa0[tid], sa1[tid], sa2[tid], r);
-              }
-              ++k;
-            }
-          }
-          if (MODE == kContrib) {
-            if (off + cnt > kPool) atomicAdd(a.partial + pos, r[0]);
-            else a.partial[pos] = r[0];
-          } else {
-            r[0] *= sg[tid];
-            double* rec = a.partial + (int64_t)pos * 8;
-            if (off + cnt > kPool) {
-#pragma unroll
-              for (int q = 0; q < 7; ++q) atomicAdd(rec + q, r[q]);
-            } else {
-              reinterpret_cast<double4*>(rec)[0] = make_double4(r[0], r[1], r[2], r[3]);
-              reinterpret_cast<double4*>(rec)[1] = make_double4(r[4], r[5], r[6], 0.0);
+              const int r = w * 64 + b;
+              const int p = ray_off[r] + (int)((wp[r] >> pshift) & 255u) + __popc(rows[jw * kRays + r] & below);
+              const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
+              const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
+              const double wgt = exp(-quadform(sa0[tid], sa1[tid], sa2[tid], dx, dy));
+              if (MODE == kSum) fw[p] = sk[tid] * wgt;
+              else if (MODE == kSplat) fw[p] = wgt * sg[tid];
+              else fw[p] = wgt;
+              if (Cfg::kJ) fj[p] = (uint8_t)tid;
             }
           }
         }
+        __syncthreads();
+        // ---- P3: ray-serial, additions only
+        if (cnt_r > 0) {
+          const int p0 = roff, p1 = roff + cnt_r;
+          if (MODE == kSum) {
+            for (int p = p0; p < p1; ++p) {
+              S += fw[p];
+              if (S > a.s_stop) { alive = false; break; }
+            }
+          } else if (MODE == kSplat) {
+            for (int p = p0; p < p1; ++p) accd += fw[p];
+          } else {
+            int p = p0;
+            for (; p < p1; ++p) {
+              if (!(S < a.s_stop)) break;
+              fs[p] = S;
+              S += sk[fj[p]] * fw[p];
+            }
+            for (; p < p1; ++p) fs[p] = __longlong_as_double(0x7ff0000000000000ll);  // dead: T = 0
+            alive = S < a.s_stop;
+          }
+        }
+        if (Cfg::kS) {
+          __syncthreads();
+          // ---- P4: flat pair-parallel transmittance and contributions
+          for (int p = tid; p < total; p += kRays) {
+            const int j = fj[p];
+            const double wgt = fw[p];
+            const double tau = sk[j] * wgt;
+            const double T = exp(-fs[p]);
+            const double oma = -expm1(-tau);
+            const double c = T * oma * sp[j];
+            if (MODE == kContrib) {
+              fs[p] = c;
+              if (!isfinite(c)) bad = true;
+            } else if (MODE == kGSum) {
+              fs[p] = sg[j] * c;
+            } else {
+              const double gI = sg[j];
+              fs[p] = gI * c;
+              fx[p] = gI * T * exp(-tau) * sp[j];
+              fy[p] = T * oma;
+            }
+          }
+          __syncthreads();
+          // ---- P5: ray-serial sums of g*contrib (backward)
+          if (MODE == kGSum) {
+            for (int p = roff; p < roff + cnt_r; ++p) accd += fs[p];
+          } else if (MODE == kGrad) {
+            for (int p = roff; p < roff + cnt_r; ++p) {
+              rem -= fs[p];
+              fs[p] = rem;  // downstream sum after this pair
+            }
+          }
+          if (MODE == kGrad) __syncthreads();
+          // ---- P7: Gaussian-parallel reduction in cell order
+          if ((MODE == kContrib || MODE == kGrad) && mine) {
+            const int jw = tid >> 5;
+            const uint32_t below = ((1u << lane) - 1u) & range_mask(jw, j0, j1);
+            const uint32_t pshift = 8 * (jw & 3);
+            const uint32_t* wp = wpre + (jw < 4 ? 0 : kRays);
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              uint64_t m = lm[w];
+              while (m) {
+                const int b = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                const int r = w * 64 + b;
+                const int p = ray_off[r] + (int)((wp[r] >> pshift) & 255u) + __popc(rows[jw * kRays + r] & below);
+                if (MODE == kContrib) {
+                  racc[0] += fs[p];
+                } else {
+                  const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
+                  const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
+                  const double y2 = (fx[p] - fs[p]) * fw[p];
+                  grad_terms(fy[p], y2, sk[tid], dx, dy, sa0[tid], sa1[tid], sa2[tid], racc);
+                }
+              }
+            }
+          }
+        }
+        __syncthreads();
+        j0 = j1;
+      }
+      if (MODE == kContrib && have) a.partial[pos] = racc[0];
+      if (MODE == kGrad && have) {
+        double4* rec = reinterpret_cast<double4*>(a.partial + (int64_t)pos * 8);
+        rec[0] = make_double4(racc[0] * sg[tid], racc[1], racc[2], racc[3]);
+        rec[1] = make_double4(racc[4], racc[5], racc[6], 0.0);
       }
     }
     // every Gaussian of the segment owns a record: zero the ones past an early exit
-    if (kPooled) {
+    if (MODE == kContrib || MODE == kGrad) {
       for (int i = cs + tid; i < end; i += kChunk) {
         const int p = a.pair_pos[i];
         if (MODE == kContrib) a.partial[p] = 0.0;
@@ -391,12 +456,12 @@ __global__ void __launch_bounds__(256) k_reduce_intensity(const int32_t* pair_st
 }
 
 template <int MODE>
-static int walk_grid(int max_items, size_t smem) {
+static int walk_grid(int max_items) {
   static int per_sm = 0;
   static int sms = 0;
   if (per_sm == 0) {
-    if (smem > 0)
-      cudaFuncSetAttribute(k_walk<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = WalkCfg<MODE>::kSmem;
+    cudaFuncSetAttribute(k_walk<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_walk<MODE>, 256, smem);
     per_sm = b > 0 ? b : 1;
@@ -409,10 +474,9 @@ static int walk_grid(int max_items, size_t smem) {
 
 template <int MODE>
 static int launch_walk(const WalkArgs& a, int max_items, cudaStream_t st) {
-  constexpr size_t smem = MODE == kGrad ? 2 * kPool * sizeof(double)
-                                        : (MODE == kContrib ? kPool * sizeof(double) : 0);
   if (cudaMemsetAsync(a.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
-  k_walk<MODE><<<walk_grid<MODE>(max_items, smem), 256, smem, st>>>(a);
+  const int grid = walk_grid<MODE>(max_items);
+  k_walk<MODE><<<grid, 256, WalkCfg<MODE>::kSmem, st>>>(a);
   note_launch();
   return check_launch();
 }
