@@ -110,6 +110,18 @@ typedef struct sdgr_projection {
   double* look;          /* (n,4) unit look dir xyz, distance (geometry.py:308-313) */
 } sdgr_projection;
 
+/* Packed per-(tile, Gaussian) record, one per sorted pair of the computation
+ * plane, so the ordered tile walks read their inputs coalesced (80 B). */
+typedef struct sdgr_pair_rec {
+  double u, v;              /* computation-plane center              */
+  double a00, a01, a11;     /* inverse covariance                    */
+  double kappa, phase;      /* ke_fwd + ke_bwd, max(0, P~)           */
+  uint64_t cell_mask;       /* 8x8 member window at (bbox.x0, bbox.y0) */
+  int16_t x0, x1, y0, y1;   /* clipped cell bbox                      */
+  int32_t pos;              /* pre-sort position (partial-record index) */
+  int32_t prim;             /* scene index                           */
+} sdgr_pair_rec;
+
 /* (tile, Gaussian) binning of one plane: the per-tile key lists.
  * Pairs are emitted per Gaussian in list order (rank order on the computation
  * plane, index order on the imaging plane) at "pre-sort positions"; Gaussian g
@@ -134,6 +146,8 @@ typedef struct sdgr_tiles {
   int32_t* items;       /* (max_items,4) tile, start, end, first item of tile */
   int32_t* tile_first;  /* (n_tiles) index of each tile's first work item     */
   int32_t* n_items;     /* (4) device: [0] work items, [1] overflow flag, [2] walk counter */
+  sdgr_pair_rec* pair_rec; /* (n_pairs) packed per-pair records in sorted order
+                              (computation plane; filled by sdgr_bin_pairs)   */
 } sdgr_tiles;
 
 /* Scene gradients (backward.SceneGradients, backward.py:25-50), float32. */
@@ -192,10 +206,10 @@ int sdgr_composite_forward(const sdgr_view* view, const sdgr_projection* proj,
                            double* seg_sum, double* seg_base, double* partial_I,
                            double* intensity, int32_t* status, void* stream);
 /* splat_image (forward.py:227-240): image (n_rg, n_az) FP64 overwritten.
- * part: (max_items*256) FP64 scratch. */
+ * Gaussian-parallel with deterministic fixed-point (2^-32) accumulation, so it
+ * needs no imaging-plane lists.  scratch: n_rg*n_az*8 bytes. */
 int sdgr_splat(const sdgr_view* view, const sdgr_projection* proj,
-               const sdgr_tiles* img, const double* intensity, double* part,
-               double* image, void* stream);
+               const double* intensity, void* scratch, double* image, void* stream);
 
 /* ------------------------------------------------ backward (K8-K10) ------ */
 /* grad_image_stage (backward.py:86-104).  dL_dS: (n_rg, n_az) FP64.

@@ -59,8 +59,11 @@ class TilesDesc(C.Structure):
         ("pre_prim", _p), ("pair_start", _p), ("tile_range", _p),
         ("seg_len", C.c_int32), ("max_items", C.c_int32), ("device_count", C.c_int32), ("pad_", C.c_int32),
         ("items", _p), ("tile_first", _p),
-        ("n_items", _p),
+        ("n_items", _p), ("pair_rec", _p),
     ]
+
+
+PAIR_REC_BYTES = 80  # sizeof(sdgr_pair_rec)
 
 
 class GradsDesc(C.Structure):
@@ -83,7 +86,7 @@ SIGNATURES = [
                                  C.POINTER(TilesDesc), _p, C.c_size_t, _p]),
     ("sdgr_composite_forward", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc),
                                          C.c_double, _p, _p, _p, _p, _p, _p]),
-    ("sdgr_splat", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc), _p, _p, _p, _p]),
+    ("sdgr_splat", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), _p, _p, _p, _p]),
     ("sdgr_grad_image", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), _p, _p, _p, _p]),
     ("sdgr_grad_intensity", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc),
                                       C.c_double, _p, _p, _p, _p, _p, _p]),

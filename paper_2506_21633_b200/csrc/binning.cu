@@ -443,10 +443,30 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, int64
 }
 
 // scene index of each sorted pair: pair_prim[i] = pre_prim[pair_pos[i]]
+// ... and, for the computation plane, the packed record the tile walks read
+// coalesced instead of gathering from the N-sized projection records.
 __global__ void __launch_bounds__(256) k_gather_prim(const int32_t* pos, const int32_t* pre, int64_t n_cap,
-                                                     const int32_t* n_dev, int32_t* prim) {
+                                                     const int32_t* n_dev, int32_t* prim,
+                                                     sdgr_plane pl, const double* kappa,
+                                                     const double* phase, sdgr_pair_rec* rec) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < eff_count(n_cap, n_dev)) prim[i] = pre[pos[i]];
+  if (i >= eff_count(n_cap, n_dev)) return;
+  const int32_t p = pos[i];
+  const int32_t g = pre[p];
+  prim[i] = g;
+  if (!rec) return;
+  const double2 uv = reinterpret_cast<const double2*>(pl.uv)[g];
+  const double4 A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
+  const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
+  double4* r = reinterpret_cast<double4*>(rec + i);
+  r[0] = make_double4(uv.x, uv.y, A.x, A.y);
+  r[1] = make_double4(A.z, kappa[g], phase[g], __longlong_as_double((long long)pl.cell_mask[g]));
+  int4 tail;
+  tail.x = (int)(unsigned short)bb.x | ((int)bb.y << 16);
+  tail.y = (int)(unsigned short)bb.z | ((int)bb.w << 16);
+  tail.z = p;
+  tail.w = g;
+  reinterpret_cast<int4*>(rec + i)[4] = tail;
 }
 
 // depth-segment work items: each tile list is cut into segments of at most
@@ -518,7 +538,8 @@ int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, con
     k_tile_ranges<<<(unsigned)((tl.n_tiles + 255) / 256), 256, 0, st>>>(tl.pair_tile, np, n_dev,
                                                                         tl.n_tiles, tl.tile_range);
     k_gather_prim<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(tl.pair_pos, tl.pre_prim, np, n_dev,
-                                                                tl.pair_prim);
+                                                                tl.pair_prim, pl, proj.kappa, proj.phase,
+                                                                tl.plane == 0 ? tl.pair_rec : nullptr);
     note_launch(2);
   } else {
     k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,

@@ -22,8 +22,8 @@ int launch_emit_and_sort(const sdgr_projection&, const sdgr_view&, const int32_t
                          sdgr_tiles&, void*, size_t, cudaStream_t);
 int launch_composite_forward(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, double,
                              double*, double*, double*, double*, int32_t*, cudaStream_t);
-int launch_splat(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, const double*, double*,
-                 double*, cudaStream_t);
+int launch_splat(const sdgr_view&, const sdgr_projection&, const double*, double*, double*,
+                 cudaStream_t);
 int launch_grad_image(const sdgr_view&, const sdgr_projection&, const double*, const double*, double*,
                       cudaStream_t);
 int launch_grad_intensity(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, double,
@@ -112,19 +112,18 @@ int sdgr_composite_forward(const sdgr_view* view, const sdgr_projection* proj, c
   if (!view_ok(view) || !proj || !tiles_ok(comp) || comp->plane != 0 || !intensity || !status ||
       !comp->pair_start)
     return SDGR_ERR_INVALID;
-  if (comp->n_pairs > 0 && (!seg_sum || !seg_base || !partial_I || !comp->pair_pos))
+  if (comp->n_pairs > 0 && (!seg_sum || !seg_base || !partial_I || !comp->pair_pos || !comp->pair_rec))
     return SDGR_ERR_INVALID;
   if (std::isnan(s_stop)) return SDGR_ERR_INVALID;
   return launch_composite_forward(*view, *proj, *comp, s_stop, seg_sum, seg_base, partial_I, intensity,
                                   status, static_cast<cudaStream_t>(stream));
 }
 
-int sdgr_splat(const sdgr_view* view, const sdgr_projection* proj, const sdgr_tiles* img,
-               const double* intensity, double* part, double* image, void* stream) {
-  if (!view_ok(view) || !proj || !tiles_ok(img) || img->plane != 1 || !intensity || !image)
-    return SDGR_ERR_INVALID;
-  if (img->n_pairs > 0 && !part) return SDGR_ERR_INVALID;
-  return launch_splat(*view, *proj, *img, intensity, part, image, static_cast<cudaStream_t>(stream));
+int sdgr_splat(const sdgr_view* view, const sdgr_projection* proj, const double* intensity, void* scratch,
+               double* image, void* stream) {
+  if (!view_ok(view) || !proj || !intensity || !image || !scratch) return SDGR_ERR_INVALID;
+  return launch_splat(*view, *proj, intensity, static_cast<double*>(scratch), image,
+                      static_cast<cudaStream_t>(stream));
 }
 
 int sdgr_grad_image(const sdgr_view* view, const sdgr_projection* proj, const double* intensity,
@@ -137,7 +136,7 @@ int sdgr_grad_intensity(const sdgr_view* view, const sdgr_projection* proj, cons
                         double s_stop, const double* seg_base, const double* dL_dI, double* seg_g,
                         double* seg_d, double* partial_g, void* stream) {
   if (!view_ok(view) || !proj || !tiles_ok(comp) || comp->plane != 0 || !dL_dI) return SDGR_ERR_INVALID;
-  if (comp->n_pairs > 0 && (!seg_base || !seg_g || !seg_d || !partial_g || !comp->pair_pos))
+  if (comp->n_pairs > 0 && (!seg_base || !seg_g || !seg_d || !partial_g || !comp->pair_rec))
     return SDGR_ERR_INVALID;
   if (std::isnan(s_stop)) return SDGR_ERR_INVALID;
   return launch_grad_intensity(*view, *proj, *comp, s_stop, seg_base, dL_dI, seg_g, seg_d, partial_g,

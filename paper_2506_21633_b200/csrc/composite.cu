@@ -1,35 +1,39 @@
-// composite.cu — K6/K7/K9: the tile walks.
+// composite.cu — K6/K7/K9: compositing on the computation plane and the
+// imaging-plane splat.
 //
-// A work item is one depth segment (<= seg_len Gaussians) of one 16x16 tile
-// list.  A persistent CTA of 256 threads pulls items from an atomic counter.
-// Thread r owns ray (cell / pixel) r of the tile for the order-dependent
-// steps; thread j owns Gaussian j of the current chunk of 256.
-//
-// Per chunk:
-//   P0  thread j stages Gaussian j and derives its 256-bit in-tile member
-//       mask from the 8x8 cell window K1 stored (the exact FP64 membership is
-//       reused, never recomputed); bits go into a cell-major 256x256 bitmap.
-//   P1  thread r counts its ray's live members; a block scan lays every
+// Order-INdependent sums run as streaming kernels with deterministic
+// fixed-point accumulation (integer adds are associative, so the result does
+// not depend on thread timing):
+//   k_segsum   per depth segment of a tile, the optical depth each ray
+//              accumulates (sum of tau), into shared u32 hi/lo counters;
+//   k_splat    image[p] = sum_g w I_g, Gaussian-parallel, global u64 REDs.
+// Order-DEpendent passes are tile walks.  A work item is one depth segment
+// (<= seg_len Gaussians) of one 16x16 tile list; a persistent CTA of 256
+// threads pulls items from an atomic counter.  Thread r owns ray r of the tile
+// for the order-dependent steps; thread j owns Gaussian j of the chunk:
+//   P0  thread j loads the packed record of pair j (coalesced) and derives its
+//       256-bit in-tile member mask from the 8x8 cell window K1 stored (the
+//       exact FP64 membership is reused); bits go into a cell-major bitmap.
+//   P1  thread r counts its ray's live members; a block scan lays every live
 //       (ray, member) pair out in a flat shared array in ray-major,
-//       depth-minor order -- exactly the per-ray walk order of the reference.
-//   P2  thread j evaluates w = exp(-q) for each of its member cells (pair-
-//       parallel, full warps) into the pair's flat slot.
-//   P3  thread r runs the order-dependent part over its own slots: only
-//       additions (log-transmittance prefix, early ray termination).
+//       depth-minor order -- exactly the reference's per-ray walk order.
+//   P2  thread j evaluates w = exp(-q) for its live member cells (pair-
+//       parallel) into the pair's flat slot.
+//   P3  thread r: log-transmittance prefix and early termination (adds only).
 //   P4  flat pair-parallel pass: T = e^-S, 1 - e^-tau, contributions.
-//   P5  thread r: downstream suffix sums (backward only; additions).
+//   P5  thread r: downstream suffix sums (backward only; adds only).
 //   P7  thread j reduces its own pairs in cell order into ONE partial record
 //       per (tile, Gaussian) pair, indexed by the pair's pre-sort position:
-//       no atomics, fixed summation order => deterministic results.
-// If a chunk has more live pairs than the flat array holds it is processed
-// in sub-chunks of consecutive Gaussians (ray state carries over).
+//       no atomics, fixed order => deterministic.
+// A chunk whose live pairs exceed the flat array is processed in sub-chunks
+// of consecutive Gaussians (ray state carries over).
 //
 // Modes (reference stage they replace):
-//   kSum     segment optical-depth sums          (forward.py:182-187, cumsum)
-//   kContrib per-pair contributions -> I_g        (forward.py:188-192)
-//   kSplat   image = sum_g w I_g per pixel        (forward.py:227-240)
-//   kGSum    segment sums of g*contrib            (backward.py:129-139)
-//   kGrad    reverse-recurrence gradients         (backward.py:122-148)
+//   k_segsum  segment optical-depth sums        (forward.py:182-187, cumsum)
+//   kContrib  per-pair contributions -> I_g      (forward.py:188-192)
+//   k_splat   image = sum_g w I_g                (forward.py:227-240)
+//   kGSum     segment sums of g*contrib          (backward.py:129-139)
+//   kGrad     reverse-recurrence gradients       (backward.py:122-148)
 // Depth segments are stitched with per-ray exclusive prefix (forward) /
 // suffix (backward) scans over a tile's items, in FP64.
 //
@@ -40,69 +44,73 @@
 
 namespace sdgr {
 
-enum WalkMode { kSum = 0, kContrib = 1, kSplat = 2, kGSum = 3, kGrad = 4 };
+enum WalkMode { kContrib = 1, kGSum = 3, kGrad = 4 };
+
+// fixed point: value * 2^32 in a u64 (values are >= 0)
+constexpr double kFix = 4294967296.0;
+constexpr double kFixInv = 1.0 / 4294967296.0;
+constexpr double kFixMax = 1.0e5;  // per-term clamp: keeps 8192-term sums far from 2^32
 
 template <int MODE>
 struct WalkCfg {
-  static constexpr int kCap = MODE == kGrad ? 2048 : 4096;            // flat pair slots
-  static constexpr bool kS = MODE == kContrib || MODE == kGSum || MODE == kGrad;
-  static constexpr bool kJ = kS;                                       // slot -> Gaussian
+  static constexpr int kCap = MODE == kGrad ? 2048 : 4096;  // flat pair slots
   static constexpr bool kXY = MODE == kGrad;
-  static constexpr size_t kSmem = kCap * (8 + (kS ? 8 : 0) + (kXY ? 16 : 0) + (kJ ? 1 : 0));
+  static constexpr size_t kSmem = kCap * (8 + 8 + (kXY ? 16 : 0) + 1);
 };
 
 struct WalkArgs {
-  sdgr_plane pl;
   int n_cols, n_rows, tiles_x;
   double cutoff;
-  const int32_t* pair_prim;
-  const int32_t* pair_pos;
+  const sdgr_pair_rec* rec;
   const int32_t* items;
   const int32_t* n_items;
   uint32_t* counter;
-  const double* kappa;
-  const double* phase;
-  const double* gvec;      // kSplat: intensity; kGSum/kGrad: dL/dI
+  const double* gvec;      // kGSum/kGrad: dL/dI
   double s_stop;
   const double* seg_base;  // exclusive prefix of optical depth per (item, ray)
   const double* seg_g;     // kGrad: this segment's sum of g*contrib
   const double* seg_d;     // kGrad: downstream (later segments) sum of g*contrib
-  double* seg_out;         // kSum: seg sums; kSplat: partial pixels; kGSum: seg_g
+  double* seg_out;         // kGSum: seg_g
   double* partial;         // kContrib: (n_pairs); kGrad: (n_pairs, 8)
   int32_t* status;
 };
 
 // 256-bit in-tile member mask of one Gaussian (bit = local cell (iv&15)*16+(iu&15)).
-__device__ __forceinline__ void member_mask(short4 bb, uint64_t cm, double2 uv, double4 A, int tx,
-                                            int ty, double cutoff, uint64_t m[4]) {
+// Small footprints: the 8x8 window rows are shifted into place (no per-bit
+// loop).  Large footprints: exact FP64 test of the bbox cells in the tile.
+__device__ __forceinline__ void member_mask(const sdgr_pair_rec& r, int tx, int ty, double cutoff,
+                                            uint64_t m[4]) {
   m[0] = m[1] = m[2] = m[3] = 0;
-  if ((bb.y - bb.x) < 8 && (bb.w - bb.z) < 8) {
-    while (cm) {
-      const int b = __ffsll((long long)cm) - 1;
-      cm &= cm - 1;
-      const int iu = bb.x + (b & 7), iv = bb.z + (b >> 3);
-      if ((iu >> 4) == tx && (iv >> 4) == ty) {
-        const int c = ((iv & 15) << 4) | (iu & 15);
-        const uint64_t bit = 1ull << (c & 63);
+  const int x0 = r.x0, x1 = r.x1, y0 = r.y0, y1 = r.y1;
+  if (x0 > x1 || y0 > y1) return;
+  if ((x1 - x0) < 8 && (y1 - y0) < 8) {
+    const uint64_t cm = r.cell_mask;
+    const int c0 = x0 - tx * kTile, r0 = y0 - ty * kTile;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) m[w] |= (c >> 6) == w ? bit : 0ull;
-      }
+    for (int k = 0; k < 8; ++k) {
+      const int rr = r0 + k;
+      const uint32_t byte = (uint32_t)(cm >> (8 * k)) & 0xffu;
+      if (rr < 0 || rr > 15 || byte == 0) continue;
+      const uint32_t bits = (c0 >= 0 ? (byte << c0) : (byte >> (-c0))) & 0xffffu;
+      const uint64_t v = (uint64_t)bits << ((rr & 3) * 16);
+      const int w = rr >> 2;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) m[q] |= (w == q) ? v : 0ull;
     }
     return;
   }
-  // large footprint: exact FP64 test of the bbox cells inside this tile
   const bool dense = !isfinite(cutoff);
-  const double cut2 = dmul(cutoff, cutoff), a01x2 = dmul(2.0, A.y);
-  const int cx0 = max((int)bb.x, tx * kTile), cx1 = min((int)bb.y, tx * kTile + kTile - 1);
-  const int cy0 = max((int)bb.z, ty * kTile), cy1 = min((int)bb.w, ty * kTile + kTile - 1);
+  const double cut2 = dmul(cutoff, cutoff), a01x2 = dmul(2.0, r.a01);
+  const int cx0 = max(x0, tx * kTile), cx1 = min(x1, tx * kTile + kTile - 1);
+  const int cy0 = max(y0, ty * kTile), cy1 = min(y1, ty * kTile + kTile - 1);
   for (int iv = cy0; iv <= cy1; ++iv) {
-    const double dy = dsub((double)iv, uv.y);
-    const double t3 = dmul(A.z, dmul(dy, dy));
+    const double dy = dsub((double)iv, r.v);
+    const double t3 = dmul(r.a11, dmul(dy, dy));
     for (int iu = cx0; iu <= cx1; ++iu) {
       bool member = dense;
       if (!dense) {
-        const double dx = dsub((double)iu, uv.x);
-        const double q = dadd(dadd(dmul(A.x, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
+        const double dx = dsub((double)iu, r.u);
+        const double q = dadd(dadd(dmul(r.a00, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
         member = q <= cut2;
       }
       if (member) {
@@ -113,6 +121,19 @@ __device__ __forceinline__ void member_mask(short4 bb, uint64_t cm, double2 uv, 
       }
     }
   }
+}
+
+__device__ __forceinline__ sdgr_pair_rec load_rec(const sdgr_pair_rec* p) {
+  sdgr_pair_rec r;
+  const double2* s = reinterpret_cast<const double2*>(p);
+  const double2 a0 = __ldg(s), a1 = __ldg(s + 1), b0 = __ldg(s + 2), b1 = __ldg(s + 3);
+  const int4 t = __ldg(reinterpret_cast<const int4*>(p) + 4);
+  r.u = a0.x; r.v = a0.y; r.a00 = a1.x; r.a01 = a1.y;
+  r.a11 = b0.x; r.kappa = b0.y; r.phase = b1.x; r.cell_mask = (uint64_t)__double_as_longlong(b1.y);
+  r.x0 = (int16_t)(t.x & 0xffff); r.x1 = (int16_t)(t.x >> 16);
+  r.y0 = (int16_t)(t.y & 0xffff); r.y1 = (int16_t)(t.y >> 16);
+  r.pos = t.z; r.prim = t.w;
+  return r;
 }
 
 // exclusive block scan (256 threads); also returns the block total
@@ -160,6 +181,100 @@ __device__ __forceinline__ void grad_terms(double y1, double y2, double kap, dou
   r[6] += -2.0 * dq * (a01 * dx + a11 * dy);
 }
 
+// ============================================================ pass A ==========
+__device__ __forceinline__ void fix_add(uint32_t* lo, uint32_t* hi, double v) {
+  const uint64_t f = __double2ull_rn(fmin(v, kFixMax) * kFix);
+  const uint32_t l = (uint32_t)f;
+  uint32_t h = (uint32_t)(f >> 32);
+  if (l) {
+    const uint32_t old = atomicAdd(lo, l);
+    h += (old + l) < old;  // carry
+  }
+  if (h) atomicAdd(hi, h);
+}
+
+__global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const int32_t* items,
+                                                const int32_t* n_items_p, uint32_t* counter, int tiles_x,
+                                                double cutoff, double* seg_sum) {
+  __shared__ uint32_t lo[kRays], hi[kRays];
+  __shared__ int item_s;
+  const int tid = threadIdx.x;
+  const int n_items = *n_items_p;
+  while (true) {
+    __syncthreads();
+    if (tid == 0) item_s = (int)atomicAdd(counter, 1u);
+    lo[tid] = 0u;
+    hi[tid] = 0u;
+    __syncthreads();
+    const int item = item_s;
+    if (item >= n_items) return;
+    const int4 it = reinterpret_cast<const int4*>(items)[item];
+    const int tx = it.x % tiles_x, ty = it.x / tiles_x;
+    for (int i = it.y + tid; i < it.z; i += kRays) {
+      const sdgr_pair_rec r = load_rec(rec + i);
+      uint64_t m[4];
+      member_mask(r, tx, ty, cutoff, m);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint64_t bits = m[w];
+        while (bits) {
+          const int b = __ffsll((long long)bits) - 1;
+          bits &= bits - 1;
+          const int c = w * 64 + b;
+          const double dx = dsub((double)(tx * kTile + (c & 15)), r.u);
+          const double dy = dsub((double)(ty * kTile + (c >> 4)), r.v);
+          fix_add(lo + c, hi + c, r.kappa * exp(-quadform(r.a00, r.a01, r.a11, dx, dy)));
+        }
+      }
+    }
+    __syncthreads();
+    seg_sum[(int64_t)item * kRays + tid] = ((double)hi[tid] * kFix + (double)lo[tid]) * kFixInv;
+  }
+}
+
+// ============================================================ splat ===========
+// One thread per Gaussian; its member pixels (imaging-plane cell window K1
+// stored) receive w * I_g through global u64 fixed-point REDs.
+__global__ void __launch_bounds__(256) k_splat(sdgr_view view, sdgr_plane pl, const uint8_t* flags,
+                                               const double* intensity, int64_t n,
+                                               unsigned long long* acc) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n || !(flags[g] & SDGR_FLAG_VISIBLE)) return;
+  const double I = intensity[g];
+  if (I == 0.0) return;
+  const double2 uv = reinterpret_cast<const double2*>(pl.uv)[g];
+  const double4 A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
+  const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
+  if (bb.x > bb.y || bb.z > bb.w) return;
+  auto add = [&](int iu, int iv, double q) {
+    const double v = exp(-q) * I;
+    atomicAdd(acc + (int64_t)iv * view.n_az + iu, (unsigned long long)__double2ull_rn(fmin(v, kFixMax) * kFix));
+  };
+  if ((bb.y - bb.x) < 8 && (bb.w - bb.z) < 8) {
+    uint64_t cm = pl.cell_mask[g];
+    while (cm) {
+      const int b = __ffsll((long long)cm) - 1;
+      cm &= cm - 1;
+      const int iu = bb.x + (b & 7), iv = bb.z + (b >> 3);
+      add(iu, iv, quadform(A.x, A.y, A.z, dsub((double)iu, uv.x), dsub((double)iv, uv.y)));
+    }
+    return;
+  }
+  const bool dense = !isfinite(view.cutoff);
+  const double cut2 = dmul(view.cutoff, view.cutoff);
+  for (int iv = bb.z; iv <= bb.w; ++iv)
+    for (int iu = bb.x; iu <= bb.y; ++iu) {
+      const double q = quadform(A.x, A.y, A.z, dsub((double)iu, uv.x), dsub((double)iv, uv.y));
+      if (dense || q <= cut2) add(iu, iv, q);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_splat_finish(const unsigned long long* acc, int64_t n, double* image) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) image[i] = (double)acc[i] * kFixInv;
+}
+
+// ============================================================ tile walks ======
 template <int MODE>
 __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
   using Cfg = WalkCfg<MODE>;
@@ -174,9 +289,9 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
   __shared__ int32_t base_s;
   __shared__ int item_s;
   extern __shared__ double dyn[];
-  double* fw = dyn;                                         // w (kSum: tau, kSplat: w*I)
+  double* fw = dyn;                                         // w
   double* fs = fw + kCap;                                   // S / contrib / g*contrib / D
-  double* fx = fs + (Cfg::kS ? kCap : 0);                   // kGrad: g*T*a*P
+  double* fx = fs + kCap;                                   // kGrad: g*T*a*P
   double* fy = fx + (Cfg::kXY ? kCap : 0);                  // kGrad: T*(1-a)
   uint8_t* fj = reinterpret_cast<uint8_t*>(fy + (Cfg::kXY ? kCap : 0));
 
@@ -194,34 +309,29 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
     const int iu = tx * kTile + (tid & 15), iv = ty * kTile + (tid >> 4);
     const bool valid = iu < a.n_cols && iv < a.n_rows;
     const int64_t slot_ray = (int64_t)item * kRays + tid;
-    double S = 0.0, accd = 0.0, rem = 0.0;
-    if (Cfg::kS) S = a.seg_base[slot_ray];
+    double S = a.seg_base[slot_ray], accd = 0.0, rem = 0.0;
     if (MODE == kGrad) rem = a.seg_d[slot_ray] + a.seg_g[slot_ray];
-    bool alive = valid && (MODE == kSplat || S < a.s_stop);
+    bool alive = valid && S < a.s_stop;
     bool bad = false;
 
     int cs = start;
     for (; cs < end; cs += kChunk) {
       if (!__syncthreads_or(alive)) break;
-      // ---- P0: stage Gaussian j = tid, build its member mask, scatter bits
+      // ---- P0: stage pair j = tid, build its member mask, scatter bits
 #pragma unroll
       for (int w = 0; w < 8; ++w) rows[w * kRays + tid] = 0u;
-      const int idx = cs + tid;
       const int nG = min(kChunk, end - cs);
       const bool have = tid < nG;
       uint64_t gm[4] = {0, 0, 0, 0};
       int pos = 0;
       if (have) {
-        const int g = a.pair_prim[idx];
-        const double2 uv = reinterpret_cast<const double2*>(a.pl.uv)[g];
-        const double4 A = reinterpret_cast<const double4*>(a.pl.inv_cov)[g];
-        const short4 bb = reinterpret_cast<const short4*>(a.pl.bbox)[g];
-        member_mask(bb, a.pl.cell_mask[g], uv, A, tx, ty, a.cutoff, gm);
-        su[tid] = uv.x; sv[tid] = uv.y;
-        sa0[tid] = A.x; sa1[tid] = A.y; sa2[tid] = A.z;
-        if (MODE != kSplat) { sk[tid] = a.kappa[g]; sp[tid] = a.phase[g]; }
-        if (MODE == kSplat || MODE == kGSum || MODE == kGrad) sg[tid] = a.gvec[g];
-        if (MODE == kContrib || MODE == kGrad) pos = a.pair_pos[idx];
+        const sdgr_pair_rec r = load_rec(a.rec + cs + tid);
+        member_mask(r, tx, ty, a.cutoff, gm);
+        su[tid] = r.u; sv[tid] = r.v;
+        sa0[tid] = r.a00; sa1[tid] = r.a01; sa2[tid] = r.a11;
+        sk[tid] = r.kappa; sp[tid] = r.phase;
+        if (MODE != kContrib) sg[tid] = a.gvec[r.prim];
+        pos = r.pos;
       }
       __syncthreads();
       {
@@ -253,6 +363,7 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
                               : 0;
         int tot_g;
         const int excl_g = block_scan(cnt_g, scan_tmp, tot_g);
+        if (tot_g == 0) break;  // no live pair left in this chunk
         if (tid == j0) base_s = excl_g;
         __syncthreads();
         const bool fits = have && tid >= j0 && (excl_g + cnt_g - base_s) <= kCap;
@@ -277,11 +388,11 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
         __syncthreads();
         // ---- P2: Gaussian-parallel weights into the flat slots
         const bool mine = have && tid >= j0 && tid < j1;
+        const int jw = tid >> 5;
+        const uint32_t below = ((1u << lane) - 1u) & range_mask(jw, j0, j1);
+        const uint32_t pshift = 8 * (jw & 3);
+        const uint32_t* wp = wpre + (jw < 4 ? 0 : kRays);
         if (mine) {
-          const int jw = tid >> 5;
-          const uint32_t below = ((1u << lane) - 1u) & range_mask(jw, j0, j1);
-          const uint32_t pshift = 8 * (jw & 3);
-          const uint32_t* wp = wpre + (jw < 4 ? 0 : kRays);
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
             uint64_t m = lm[w];
@@ -292,91 +403,73 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
               const int p = ray_off[r] + (int)((wp[r] >> pshift) & 255u) + __popc(rows[jw * kRays + r] & below);
               const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
               const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
-              const double wgt = exp(-quadform(sa0[tid], sa1[tid], sa2[tid], dx, dy));
-              if (MODE == kSum) fw[p] = sk[tid] * wgt;
-              else if (MODE == kSplat) fw[p] = wgt * sg[tid];
-              else fw[p] = wgt;
-              if (Cfg::kJ) fj[p] = (uint8_t)tid;
+              fw[p] = exp(-quadform(sa0[tid], sa1[tid], sa2[tid], dx, dy));
+              fj[p] = (uint8_t)tid;
             }
           }
         }
         __syncthreads();
-        // ---- P3: ray-serial, additions only
+        // ---- P3: ray-serial log-transmittance prefix (additions only)
         if (cnt_r > 0) {
-          const int p0 = roff, p1 = roff + cnt_r;
-          if (MODE == kSum) {
-            for (int p = p0; p < p1; ++p) {
-              S += fw[p];
-              if (S > a.s_stop) { alive = false; break; }
-            }
-          } else if (MODE == kSplat) {
-            for (int p = p0; p < p1; ++p) accd += fw[p];
+          const int p1 = roff + cnt_r;
+          int p = roff;
+          for (; p < p1; ++p) {
+            if (!(S < a.s_stop)) break;
+            fs[p] = S;
+            S += sk[fj[p]] * fw[p];
+          }
+          for (; p < p1; ++p) fs[p] = __longlong_as_double(0x7ff0000000000000ll);  // dead: T = 0
+          alive = S < a.s_stop;
+        }
+        __syncthreads();
+        // ---- P4: flat pair-parallel transmittance and contributions
+        for (int p = tid; p < total; p += kRays) {
+          const int j = fj[p];
+          const double wgt = fw[p];
+          const double tau = sk[j] * wgt;
+          const double T = exp(-fs[p]);
+          const double oma = -expm1(-tau);
+          const double c = T * oma * sp[j];
+          if (MODE == kContrib) {
+            fs[p] = c;
+            if (!isfinite(c)) bad = true;
+          } else if (MODE == kGSum) {
+            fs[p] = sg[j] * c;
           } else {
-            int p = p0;
-            for (; p < p1; ++p) {
-              if (!(S < a.s_stop)) break;
-              fs[p] = S;
-              S += sk[fj[p]] * fw[p];
-            }
-            for (; p < p1; ++p) fs[p] = __longlong_as_double(0x7ff0000000000000ll);  // dead: T = 0
-            alive = S < a.s_stop;
+            const double gI = sg[j];
+            fs[p] = gI * c;
+            fx[p] = gI * T * exp(-tau) * sp[j];
+            fy[p] = T * oma;
           }
         }
-        if (Cfg::kS) {
-          __syncthreads();
-          // ---- P4: flat pair-parallel transmittance and contributions
-          for (int p = tid; p < total; p += kRays) {
-            const int j = fj[p];
-            const double wgt = fw[p];
-            const double tau = sk[j] * wgt;
-            const double T = exp(-fs[p]);
-            const double oma = -expm1(-tau);
-            const double c = T * oma * sp[j];
-            if (MODE == kContrib) {
-              fs[p] = c;
-              if (!isfinite(c)) bad = true;
-            } else if (MODE == kGSum) {
-              fs[p] = sg[j] * c;
-            } else {
-              const double gI = sg[j];
-              fs[p] = gI * c;
-              fx[p] = gI * T * exp(-tau) * sp[j];
-              fy[p] = T * oma;
-            }
+        __syncthreads();
+        // ---- P5: ray-serial sums of g*contrib (backward)
+        if (MODE == kGSum) {
+          for (int p = roff; p < roff + cnt_r; ++p) accd += fs[p];
+        } else if (MODE == kGrad) {
+          for (int p = roff; p < roff + cnt_r; ++p) {
+            rem -= fs[p];
+            fs[p] = rem;  // downstream sum after this pair
           }
           __syncthreads();
-          // ---- P5: ray-serial sums of g*contrib (backward)
-          if (MODE == kGSum) {
-            for (int p = roff; p < roff + cnt_r; ++p) accd += fs[p];
-          } else if (MODE == kGrad) {
-            for (int p = roff; p < roff + cnt_r; ++p) {
-              rem -= fs[p];
-              fs[p] = rem;  // downstream sum after this pair
-            }
-          }
-          if (MODE == kGrad) __syncthreads();
-          // ---- P7: Gaussian-parallel reduction in cell order
-          if ((MODE == kContrib || MODE == kGrad) && mine) {
-            const int jw = tid >> 5;
-            const uint32_t below = ((1u << lane) - 1u) & range_mask(jw, j0, j1);
-            const uint32_t pshift = 8 * (jw & 3);
-            const uint32_t* wp = wpre + (jw < 4 ? 0 : kRays);
+        }
+        // ---- P7: Gaussian-parallel reduction in cell order
+        if (MODE != kGSum && mine) {
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              uint64_t m = lm[w];
-              while (m) {
-                const int b = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                const int r = w * 64 + b;
-                const int p = ray_off[r] + (int)((wp[r] >> pshift) & 255u) + __popc(rows[jw * kRays + r] & below);
-                if (MODE == kContrib) {
-                  racc[0] += fs[p];
-                } else {
-                  const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
-                  const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
-                  const double y2 = (fx[p] - fs[p]) * fw[p];
-                  grad_terms(fy[p], y2, sk[tid], dx, dy, sa0[tid], sa1[tid], sa2[tid], racc);
-                }
+          for (int w = 0; w < 4; ++w) {
+            uint64_t m = lm[w];
+            while (m) {
+              const int b = __ffsll((long long)m) - 1;
+              m &= m - 1;
+              const int r = w * 64 + b;
+              const int p = ray_off[r] + (int)((wp[r] >> pshift) & 255u) + __popc(rows[jw * kRays + r] & below);
+              if (MODE == kContrib) {
+                racc[0] += fs[p];
+              } else {
+                const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
+                const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
+                const double y2 = (fx[p] - fs[p]) * fw[p];
+                grad_terms(fy[p], y2, sk[tid], dx, dy, sa0[tid], sa1[tid], sa2[tid], racc);
               }
             }
           }
@@ -392,9 +485,9 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
       }
     }
     // every Gaussian of the segment owns a record: zero the ones past an early exit
-    if (MODE == kContrib || MODE == kGrad) {
+    if (MODE != kGSum) {
       for (int i = cs + tid; i < end; i += kChunk) {
-        const int p = a.pair_pos[i];
+        const int p = a.rec[i].pos;
         if (MODE == kContrib) a.partial[p] = 0.0;
         else {
           double4* rec = reinterpret_cast<double4*>(a.partial + (int64_t)p * 8);
@@ -403,8 +496,7 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
         }
       }
     }
-    if (MODE == kSum) a.seg_out[slot_ray] = S;
-    if (MODE == kSplat || MODE == kGSum) a.seg_out[slot_ray] = accd;
+    if (MODE == kGSum) a.seg_out[slot_ray] = accd;
     if (MODE == kContrib && __syncthreads_or(bad) && tid == 0) atomicOr(a.status + SDGR_STATUS_NONFINITE, 1);
   }
 }
@@ -428,22 +520,6 @@ __global__ void __launch_bounds__(256) k_seg_scan(const int32_t* range, const in
   }
 }
 
-// image[pixel] = sum over the tile's segment partials, in item order.
-__global__ void __launch_bounds__(256) k_splat_reduce(const int32_t* range, const int32_t* tile_first,
-                                                      int seg_len, int tiles_x, int n_az, int n_rg,
-                                                      const double* part, double* image) {
-  const int t = blockIdx.x;
-  const int iu = (t % tiles_x) * kTile + (threadIdx.x & 15);
-  const int iv = (t / tiles_x) * kTile + (threadIdx.x >> 4);
-  if (iu >= n_az || iv >= n_rg) return;
-  const int cnt = range[2 * t + 1] - range[2 * t];
-  const int nseg = (cnt + seg_len - 1) / seg_len;
-  double s = 0.0;
-  const int64_t first = nseg ? tile_first[t] : 0;
-  for (int k = 0; k < nseg; ++k) s += part[(first + k) * kRays + threadIdx.x];
-  image[(int64_t)iv * n_az + iu] = s;
-}
-
 // intensity[g] = sum of its per-tile partials, in pre-sort (tile-id) order.
 __global__ void __launch_bounds__(256) k_reduce_intensity(const int32_t* pair_start, const int32_t* n_tiles,
                                                           const double* partial, int64_t n, double* out) {
@@ -455,46 +531,47 @@ __global__ void __launch_bounds__(256) k_reduce_intensity(const int32_t* pair_st
   out[g] = acc;
 }
 
+static int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
 template <int MODE>
 static int walk_grid(int max_items) {
   static int per_sm = 0;
-  static int sms = 0;
   if (per_sm == 0) {
     const size_t smem = WalkCfg<MODE>::kSmem;
     cudaFuncSetAttribute(k_walk<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_walk<MODE>, 256, smem);
     per_sm = b > 0 ? b : 1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  return max(1, min(max_items, sms * per_sm));
+  return max(1, min(max_items, sm_count() * per_sm));
 }
 
 template <int MODE>
 static int launch_walk(const WalkArgs& a, int max_items, cudaStream_t st) {
   if (cudaMemsetAsync(a.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
-  const int grid = walk_grid<MODE>(max_items);
-  k_walk<MODE><<<grid, 256, WalkCfg<MODE>::kSmem, st>>>(a);
+  k_walk<MODE><<<walk_grid<MODE>(max_items), 256, WalkCfg<MODE>::kSmem, st>>>(a);
   note_launch();
   return check_launch();
 }
 
-static WalkArgs base_args(const sdgr_view& v, const sdgr_projection& p, const sdgr_tiles& t) {
+static WalkArgs base_args(const sdgr_view& v, const sdgr_tiles& t) {
   WalkArgs a{};
-  a.pl = t.plane == 0 ? p.comp : p.img;
-  a.n_cols = t.plane == 0 ? v.n_u : v.n_az;
-  a.n_rows = t.plane == 0 ? v.n_v : v.n_rg;
+  a.n_cols = v.n_u;
+  a.n_rows = v.n_v;
   a.tiles_x = t.tiles_x;
   a.cutoff = v.cutoff;
-  a.pair_prim = t.pair_prim;
-  a.pair_pos = t.pair_pos;
+  a.rec = t.pair_rec;
   a.items = t.items;
   a.n_items = t.n_items;
   a.counter = reinterpret_cast<uint32_t*>(t.n_items + 2);
-  a.kappa = p.kappa;
-  a.phase = p.phase;
   return a;
 }
 
@@ -502,18 +579,20 @@ int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const
                              double s_stop, double* seg_sum, double* seg_base, double* partial_I,
                              double* intensity, int32_t* status, cudaStream_t st) {
   if (t.n_pairs > 0) {
-    WalkArgs a = base_args(v, p, t);
-    a.s_stop = s_stop;
-    a.seg_out = seg_sum;
-    int rc = launch_walk<kSum>(a, t.max_items, st);
-    if (rc) return rc;
+    uint32_t* counter = reinterpret_cast<uint32_t*>(t.n_items + 2);
+    if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
+    static int per_sm = 0;
+    if (per_sm == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_segsum, 256, 0);
+    k_segsum<<<max(1, min(t.max_items, sm_count() * max(per_sm, 1))), 256, 0, st>>>(
+        t.pair_rec, t.items, t.n_items, counter, t.tiles_x, v.cutoff, seg_sum);
     k_seg_scan<false><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_sum, seg_base);
-    note_launch();
+    note_launch(2);
+    WalkArgs a = base_args(v, t);
+    a.s_stop = s_stop;
     a.seg_base = seg_base;
-    a.seg_out = nullptr;
     a.partial = partial_I;
     a.status = status;
-    rc = launch_walk<kContrib>(a, t.max_items, st);
+    const int rc = launch_walk<kContrib>(a, t.max_items, st);
     if (rc) return rc;
   }
   k_reduce_intensity<<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(t.pair_start, p.comp.n_tiles, partial_I,
@@ -522,18 +601,15 @@ int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const
   return check_launch();
 }
 
-int launch_splat(const sdgr_view& v, const sdgr_projection& p, const sdgr_tiles& t,
-                 const double* intensity, double* part, double* image, cudaStream_t st) {
-  if (t.n_pairs > 0) {
-    WalkArgs a = base_args(v, p, t);
-    a.gvec = intensity;
-    a.seg_out = part;
-    int rc = launch_walk<kSplat>(a, t.max_items, st);
-    if (rc) return rc;
-  }
-  k_splat_reduce<<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, t.tiles_x, v.n_az,
-                                            v.n_rg, part, image);
-  note_launch();
+// image: (n_rg, n_az) FP64; part: scratch of >= n_rg*n_az u64 (8-byte) slots.
+int launch_splat(const sdgr_view& v, const sdgr_projection& p, const double* intensity, double* part,
+                 double* image, cudaStream_t st) {
+  const int64_t npix = (int64_t)v.n_az * v.n_rg;
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(part);
+  if (cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * npix, st) != cudaSuccess) return SDGR_ERR_CUDA;
+  k_splat<<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(v, p.img, p.flags, intensity, p.n, acc);
+  k_splat_finish<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(acc, npix, image);
+  note_launch(2);
   return check_launch();
 }
 
@@ -541,7 +617,7 @@ int launch_grad_intensity(const sdgr_view& v, const sdgr_projection& p, const sd
                           double s_stop, const double* seg_base, const double* dL_dI, double* seg_g,
                           double* seg_d, double* partial_g, cudaStream_t st) {
   if (t.n_pairs == 0) return SDGR_OK;
-  WalkArgs a = base_args(v, p, t);
+  WalkArgs a = base_args(v, t);
   a.s_stop = s_stop;
   a.seg_base = seg_base;
   a.gvec = dL_dI;

@@ -123,9 +123,10 @@ class MultiViewStep:
         ws_need = self.lib.sdgr_workspace_bytes(n, max(cap_pairs.values()))
         self.ws = _empty((ws_need,), torch.uint8, dev)
         self.ws_bytes = ws_need
-        for pl in (0, 1):
+        # only the computation plane is binned: the splat is Gaussian-parallel
+        for pl in (0,):
             cap = cap_pairs[pl]
-            nu, nv = (v.n_u, v.n_v) if pl == 0 else (v.n_az, v.n_rg)
+            nu, nv = v.n_u, v.n_v
             tx, ty = -(-nu // TILE), -(-nv // TILE)
             seg = _seg_len(cap)
             max_items = -(-cap // seg) + tx * ty
@@ -137,19 +138,20 @@ class MultiViewStep:
                 n_items=torch.zeros((4,), dtype=torch.int32, device=dev),
                 seg_a=_empty((max_items * 256,), torch.float64, dev),
                 seg_b=_empty((max_items * 256,), torch.float64, dev),
+                seg_c=_empty((max_items * 256,), torch.float64, dev),
+                partial_I=_empty((cap,), torch.float64, dev),
+                partial_g=_empty((cap, 8), torch.float64, dev),
+                pair_rec=_empty((cap, _lib.PAIR_REC_BYTES), torch.uint8, dev),
             )
-            if pl == 0:
-                t["partial_I"] = _empty((cap,), torch.float64, dev)
-                t["partial_g"] = _empty((cap, 8), torch.float64, dev)
-                t["seg_c"] = _empty((max_items * 256,), torch.float64, dev)
             d = _lib.TilesDesc()
             d.plane, d.tiles_x, d.tiles_y, d.n_tiles = pl, tx, ty, tx * ty
             d.n_pairs = cap
             for k in ("pair_tile", "pair_pos", "pair_prim", "pre_prim", "pair_start", "tile_range", "items",
-                      "tile_first", "n_items"):
+                      "tile_first", "n_items", "pair_rec"):
                 setattr(d, k, ptr(t[k]))
             d.seg_len, d.max_items, d.device_count = seg, max_items, 1
             self.planes[pl] = _PlaneBufs(offsets=_empty((n + 1,), torch.int32, dev), tiles=d, t=t)
+        self.splat_scratch = _empty((v.n_rg * v.n_az,), torch.int64, dev)
         self.cap = dict(cap_pairs)
 
     def calibrate(self):
@@ -177,8 +179,8 @@ class MultiViewStep:
     # -- one view -----------------------------------------------------------
     def _view(self, v, dlds: torch.Tensor, ev=None):
         lib, st, pd = self.lib, _stream(), C.byref(self.pd)
-        P0, P1 = self.planes[0], self.planes[1]
-        t0, t1 = P0.t, P1.t
+        P0 = self.planes[0]
+        t0 = P0.t
 
         def mark(i):
             if ev is not None:
@@ -188,18 +190,17 @@ class MultiViewStep:
         mark(1)
         _check(lib.sdgr_depth_order(pd, ptr(self.order), ptr(self.ws), self.ws_bytes, st), "sdgr_depth_order")
         mark(2)
-        for pl, P in ((0, P0), (1, P1)):
-            _check(lib.sdgr_count_pairs(pd, pl, ptr(self.order) if pl == 0 else None, ptr(P.offsets),
-                                        ptr(self.ws), self.ws_bytes, st), "sdgr_count_pairs")
-            _check(lib.sdgr_bin_pairs(pd, C.byref(v), ptr(self.order) if pl == 0 else None, ptr(P.offsets),
-                                      C.byref(P.tiles), ptr(self.ws), self.ws_bytes, st), "sdgr_bin_pairs")
+        _check(lib.sdgr_count_pairs(pd, 0, ptr(self.order), ptr(P0.offsets), ptr(self.ws), self.ws_bytes, st),
+               "sdgr_count_pairs")
+        _check(lib.sdgr_bin_pairs(pd, C.byref(v), ptr(self.order), ptr(P0.offsets), C.byref(P0.tiles),
+                                  ptr(self.ws), self.ws_bytes, st), "sdgr_bin_pairs")
         mark(3)
         _check(lib.sdgr_composite_forward(C.byref(v), pd, C.byref(P0.tiles), self.s_stop, ptr(t0["seg_a"]),
                                           ptr(t0["seg_b"]), ptr(t0["partial_I"]), ptr(self.intensity),
                                           ptr(self.status), st), "sdgr_composite_forward")
         mark(4)
-        _check(lib.sdgr_splat(C.byref(v), pd, C.byref(P1.tiles), ptr(self.intensity), ptr(t1["seg_a"]),
-                              ptr(self.image), st), "sdgr_splat")
+        _check(lib.sdgr_splat(C.byref(v), pd, ptr(self.intensity), ptr(self.splat_scratch), ptr(self.image), st),
+               "sdgr_splat")
         mark(5)
         _check(lib.sdgr_grad_image(C.byref(v), pd, ptr(self.intensity), ptr(dlds), ptr(self.acc_img), st),
                "sdgr_grad_image")
@@ -246,9 +247,9 @@ class MultiViewStep:
 
     def check(self):
         """One host read per step: capacity overflow and non-finite status."""
-        flags = torch.stack([self.planes[0].t["n_items"][1], self.planes[1].t["n_items"][1], self.status[0]])
-        ov0, ov1, bad = flags.cpu().tolist()
-        if ov0 or ov1:
+        flags = torch.stack([self.planes[0].t["n_items"][1], self.status[0]])
+        ov0, bad = flags.cpu().tolist()
+        if ov0:
             raise OverflowError("pair capacity exceeded; recalibrate")
         if bad:
             raise NumericalError("non-finite intensity in a multi-view step")

@@ -271,6 +271,7 @@ class TileLists:
     items: torch.Tensor
     tile_first: torch.Tensor
     n_items: torch.Tensor
+    pair_rec: torch.Tensor | None = None
     _desc: object = field(default=None, repr=False)
 
     @property
@@ -286,6 +287,7 @@ class TileLists:
             d.pre_prim, d.pair_start, d.tile_range = ptr(self.pre_prim), ptr(self.pair_start), ptr(self.tile_range)
             d.seg_len, d.max_items = self.seg_len, self.max_items
             d.items, d.tile_first, d.n_items = ptr(self.items), ptr(self.tile_first), ptr(self.n_items)
+            d.pair_rec = ptr(self.pair_rec)
             self._desc = d
         return self._desc
 
@@ -350,6 +352,7 @@ class _Binner:
                 items=_empty((max_items, 4), torch.int32, dev),
                 tile_first=_empty((tx * ty,), torch.int32, dev),
                 n_items=torch.zeros((4,), dtype=torch.int32, device=dev),
+                pair_rec=(_empty((max(total, 1), _lib.PAIR_REC_BYTES), torch.uint8, dev) if pl == 0 else None),
             )
             _check(lib.sdgr_bin_pairs(C.byref(p._desc), C.byref(p.view), ptr(order) if pl == 0 else None,
                                       ptr(offsets[pl]), C.byref(tl.desc()), ptr(ws), ws_bytes, st),
@@ -457,16 +460,16 @@ def _first_bad_primitive(proj: Projection) -> int:
 
 def splat_image(intensities: IntensityBuffer, projection: Projection, config=None,
                 pairs: TileLists | None = None) -> torch.Tensor:
-    """forward.splat_image (forward.py:227-240): (n_range, n_azimuth) float64."""
-    if pairs is None:
-        pairs = build_splat_lists(projection, config)
+    """forward.splat_image (forward.py:227-240): (n_range, n_azimuth) float64.
+
+    Gaussian-parallel with deterministic fixed-point accumulation; the
+    imaging-plane tile lists (``pairs``) are not needed and are ignored."""
     v = projection.view
     dev = projection.flags.device
     image = _empty((v.n_rg, v.n_az), torch.float64, dev)
-    part = _empty((max(pairs.max_items, 1) * 256,), torch.float64, dev)
-    _check(_lib.lib().sdgr_splat(C.byref(v), C.byref(projection._desc), C.byref(pairs.desc()),
-                                 ptr(intensities.intensity_n), ptr(part), ptr(image), _stream()),
-           "sdgr_splat")
+    scratch = _empty((v.n_rg * v.n_az,), torch.int64, dev)
+    _check(_lib.lib().sdgr_splat(C.byref(v), C.byref(projection._desc), ptr(intensities.intensity_n),
+                                 ptr(scratch), ptr(image), _stream()), "sdgr_splat")
     return image
 
 
