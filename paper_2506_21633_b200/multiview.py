@@ -38,6 +38,27 @@ def shard_views(configs, rank: int, world: int):
     return [c for i, c in enumerate(configs) if i % world == rank]
 
 
+GRAD_GROUPS = (3, 4, 3, 16, 2, 1)  # positions, rotations, log_scales, sh_coeffs, ke_raw, uv_grad_norm
+
+
+def grad_views(flat: torch.Tensor, n: int) -> SceneGradients:
+    """SceneGradients whose fields are SoA views into one (30 n,) float32
+    buffer; the last n words hold the int32 visible counts."""
+    parts, o = [], 0
+    for w in GRAD_GROUPS:
+        parts.append(flat[o:o + w * n].view(n, w) if w > 1 else flat[o:o + n])
+        o += w * n
+    return SceneGradients(*parts, flat[o:o + n].view(torch.int32))
+
+
+def allreduce_grads(flat: torch.Tensor, n: int, group=None) -> None:
+    """One-step gradient exchange: sum the float gradients and the int32
+    visible counts over all ranks (NCCL on GPU, gloo on CPU)."""
+    import torch.distributed as dist
+    dist.all_reduce(flat[: 29 * n], group=group)
+    dist.all_reduce(flat[29 * n: 30 * n].view(torch.int32), group=group)
+
+
 @dataclass
 class _PlaneBufs:
     offsets: torch.Tensor
@@ -104,17 +125,10 @@ class MultiViewStep:
 
     # -- buffers ------------------------------------------------------------
     def _grad_views(self) -> SceneGradients:
-        n = self.n
-        # SoA views into one (30, n)-shaped storage keep each group contiguous
-        self.flat_soa = torch.zeros((GRAD_WIDTH * n,), dtype=torch.float32, device=self.dev)
-        s = self.flat_soa
-        o = 0
-        parts = []
-        for w in (3, 4, 3, 16, 2, 1):
-            parts.append(s[o:o + w * n].view(n, w) if w > 1 else s[o:o + n])
-            o += w * n
-        vis = s[o:o + n].view(torch.int32)
-        return SceneGradients(*parts, vis)
+        # SoA views into one flat buffer keep each group contiguous and make
+        # the all-reduce one call
+        self.flat_soa = torch.zeros((GRAD_WIDTH * self.n,), dtype=torch.float32, device=self.dev)
+        return grad_views(self.flat_soa, self.n)
 
     def _alloc_planes(self, cap_pairs: dict):
         n, dev = self.n, self.dev
@@ -239,11 +253,7 @@ class MultiViewStep:
         return self.grads
 
     def allreduce(self):
-        import torch.distributed as dist
-        n = self.n
-        fl = self.flat_soa[: 29 * n]
-        dist.all_reduce(fl, group=self.group)
-        dist.all_reduce(self.flat_soa[29 * n:].view(torch.int32), group=self.group)
+        allreduce_grads(self.flat_soa, self.n, self.group)
 
     def check(self):
         """One host read per step: capacity overflow and non-finite status."""
