@@ -40,7 +40,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "SAR views/sec fwd+bwd (1M Gaussians, 512² px) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "views/s"
-RSS_PER_ORACLE_PROC = 7.5e9   # bytes, oracle fwd+bwd at 1M Gaussians / 512^2
+RSS_PER_ORACLE_PROC = 6.0e9   # bytes, oracle fwd+bwd at 1M Gaussians / 512^2 (measured 4.9 GB peak)
 
 
 def parse():
@@ -130,6 +130,12 @@ _CPU_SCENE = None
 _CPU_CFGS = None
 
 
+def _oracle_warm(_):
+    from oracle import sdgr_oracle as O
+    O.oracle_exp(0.0)   # imports + C library load, no rendering
+    return 0
+
+
 def _oracle_view(i):
     from oracle import sdgr_oracle as O
     cfg = _CPU_CFGS[i % len(_CPU_CFGS)]
@@ -160,7 +166,7 @@ def cpu_run(scene, cfgs, procs: int, views: int):
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     ctx = mp.get_context("fork")
     with ctx.Pool(procs) as pool:
-        pool.map(_oracle_view, range(min(procs, 2)))   # warm the workers (imports, C lib)
+        pool.map(_oracle_warm, range(procs))   # warm the workers (imports, C lib)
         t0 = time.perf_counter()
         pool.map(_oracle_view, range(views), chunksize=1)
         return time.perf_counter() - t0
