@@ -108,7 +108,26 @@ typedef struct sdgr_projection {
   /* optional accessors (NULL to skip) */
   double* ke_act;        /* (n,2) softplus(ke_raw)          */
   double* look;          /* (n,4) unit look dir xyz, distance (geometry.py:308-313) */
+  unsigned long long* member_pairs; /* (2) member (cell, Gaussian) pairs T_c, T_i; optional */
 } sdgr_projection;
+
+/* Live-pair replay log, written by sdgr_composite_forward and consumed by
+ * sdgr_grad_intensity: for every live (ray, Gaussian) pair of the computation
+ * plane -- in each ray's walk order -- the log-transmittance before the pair
+ * and its footprint weight, grouped by walk sub-chunk.  The backward then
+ * touches only live pairs (no re-binning, no membership, no weights). */
+typedef struct sdgr_replay {
+  int64_t capacity;      /* pair slots; T_c (member_pairs[0]) always suffices */
+  double* S;             /* (capacity) log-transmittance before the pair   */
+  double* w;             /* (capacity) footprint weight exp(-q)            */
+  uint8_t* j;            /* (capacity) Gaussian index within its chunk      */
+  uint8_t* r;            /* (capacity) ray index within its tile            */
+  int32_t desc_per_item; /* descriptor slots per work item                  */
+  int32_t pad_;
+  int32_t* desc;         /* (max_items*desc_per_item, 4): offset, count, chunk start, j0 | j1 << 16 */
+  int32_t* desc_count;   /* (max_items) descriptors written per item        */
+  unsigned long long* cursor; /* (2) device cursor [0] and overflow flag [1]; zeroed by the forward */
+} sdgr_replay;
 
 /* Packed per-(tile, Gaussian) record, one per sorted pair of the computation
  * plane, so the ordered tile walks read their inputs coalesced (80 B). */
@@ -200,11 +219,13 @@ int sdgr_bin_pairs(const sdgr_projection* proj, const sdgr_view* view,
  * partial_I: (n_pairs) FP64 per-(tile, Gaussian) partial intensities.
  * intensity: (n) FP64, overwritten.  s_stop: rays stop once their
  * log-transmittance exceeds it (+inf = never, the reference's behaviour).
- * status: int32[4]; [0] != 0 if any contribution was non-finite. */
+ * status: int32[4]; [0] != 0 if any contribution was non-finite.
+ * replay: optional (NULL = none) live-pair log for sdgr_grad_intensity. */
 int sdgr_composite_forward(const sdgr_view* view, const sdgr_projection* proj,
                            const sdgr_tiles* comp, double s_stop,
                            double* seg_sum, double* seg_base, double* partial_I,
-                           double* intensity, int32_t* status, void* stream);
+                           double* intensity, int32_t* status, sdgr_replay* replay,
+                           void* stream);
 /* splat_image (forward.py:227-240): image (n_rg, n_az) FP64 overwritten.
  * Gaussian-parallel with deterministic fixed-point (2^-32) accumulation, so it
  * needs no imaging-plane lists.  scratch: n_rg*n_az*8 bytes. */
@@ -221,12 +242,13 @@ int sdgr_grad_image(const sdgr_view* view, const sdgr_projection* proj,
 /* grad_intensity_stage (backward.py:107-148).  dL_dI = acc_img row 0.
  * partial_g: (n_pairs, 8) FP64 per-(tile, Gaussian) partials of dL/dP,
  * dL/dkappa, dL/dA(3), dL/duv(2) on the computation plane.
- * seg_g / seg_d: (max_items*256) FP64 scratch. */
+ * seg_g / seg_d: (max_items*256) FP64 scratch.
+ * replay: the log the forward wrote (NULL = re-walk the tile lists). */
 int sdgr_grad_intensity(const sdgr_view* view, const sdgr_projection* proj,
                         const sdgr_tiles* comp, double s_stop,
                         const double* seg_base, const double* dL_dI,
                         double* seg_g, double* seg_d, double* partial_g,
-                        void* stream);
+                        const sdgr_replay* replay, void* stream);
 /* grad_geometry_stage + grad_sh_stage + the final scatter (backward.py:171-290).
  * Reduces partial_g per Gaussian (fixed order) and chains to parameters.
  * accumulate = 0 overwrites `out`, 1 adds into it (multi-view steps). */

@@ -48,7 +48,14 @@ class ProjectionDesc(C.Structure):
     _fields_ = [
         ("n", C.c_int64), ("comp", Plane), ("img", Plane),
         ("depth_key", _p), ("kappa", _p), ("phase", _p), ("phase_raw", _p),
-        ("flags", _p), ("counters", _p), ("ke_act", _p), ("look", _p),
+        ("flags", _p), ("counters", _p), ("ke_act", _p), ("look", _p), ("member_pairs", _p),
+    ]
+
+
+class ReplayDesc(C.Structure):
+    _fields_ = [
+        ("capacity", C.c_int64), ("S", _p), ("w", _p), ("j", _p), ("r", _p),
+        ("desc_per_item", C.c_int32), ("pad_", C.c_int32), ("desc", _p), ("desc_count", _p), ("cursor", _p),
     ]
 
 
@@ -85,11 +92,11 @@ SIGNATURES = [
     ("sdgr_bin_pairs", C.c_int, [C.POINTER(ProjectionDesc), C.POINTER(View), _p, _p,
                                  C.POINTER(TilesDesc), _p, C.c_size_t, _p]),
     ("sdgr_composite_forward", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc),
-                                         C.c_double, _p, _p, _p, _p, _p, _p]),
+                                         C.c_double, _p, _p, _p, _p, _p, C.POINTER(ReplayDesc), _p]),
     ("sdgr_splat", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), _p, _p, _p, _p]),
     ("sdgr_grad_image", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), _p, _p, _p, _p]),
     ("sdgr_grad_intensity", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc),
-                                      C.c_double, _p, _p, _p, _p, _p, _p]),
+                                      C.c_double, _p, _p, _p, _p, _p, C.POINTER(ReplayDesc), _p]),
     ("sdgr_grad_geometry", C.c_int, [C.POINTER(SceneDesc), C.POINTER(View), C.POINTER(ProjectionDesc),
                                      C.POINTER(TilesDesc), _p, _p, C.POINTER(GradsDesc), C.c_int, _p]),
 ]

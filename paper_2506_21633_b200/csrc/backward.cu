@@ -133,11 +133,25 @@ __global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view 
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = sc.n;
   if (g >= n) return;
-  float res[30];
-#pragma unroll
-  for (int k = 0; k < 30; ++k) res[k] = 0.f;
+  // outputs are written as soon as they are known (no local staging array)
+  auto put = [&](float* base, int64_t i, double v) {
+    base[i] = accumulate ? base[i] + (float)v : (float)v;
+  };
   const bool vis = proj.flags[g] & SDGR_FLAG_VISIBLE;
-  if (vis) {
+  if (!vis) {
+    if (!accumulate) {
+      for (int k = 0; k < 3; ++k) out.positions[3 * g + k] = 0.f;
+      for (int k = 0; k < 4; ++k) out.rotations[4 * g + k] = 0.f;
+      for (int k = 0; k < 3; ++k) out.log_scales[3 * g + k] = 0.f;
+      for (int k = 0; k < 16; ++k) out.sh_coeffs[16 * g + k] = 0.f;
+      out.ke_raw[2 * g] = 0.f;
+      out.ke_raw[2 * g + 1] = 0.f;
+      out.uv_grad_norm[g] = 0.f;
+      out.visible[g] = 0;
+    }
+    return;
+  }
+  {
     // plane-space gradients
     const double4 Ac = reinterpret_cast<const double4*>(proj.comp.inv_cov)[g];
     const double4 Ai = reinterpret_cast<const double4*>(proj.img.inv_cov)[g];
@@ -213,11 +227,12 @@ __global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view 
     const double dqz = 2.0 * (-2 * z * dR[0] - w * dR[1] + x * dR[2] + w * dR[3] - 2 * z * dR[4] + y * dR[5] +
                               x * dR[6] + y * dR[7]);
     const double dot = dqw * w + dqx * x + dqy * y + dqz * z;
-    res[3] = (float)((dqw - dot * w) / nrm);
-    res[4] = (float)((dqx - dot * x) / nrm);
-    res[5] = (float)((dqy - dot * y) / nrm);
-    res[6] = (float)((dqz - dot * z) / nrm);
-    res[7] = (float)dls[0]; res[8] = (float)dls[1]; res[9] = (float)dls[2];
+    put(out.rotations, 4 * g + 0, (dqw - dot * w) / nrm);
+    put(out.rotations, 4 * g + 1, (dqx - dot * x) / nrm);
+    put(out.rotations, 4 * g + 2, (dqy - dot * y) / nrm);
+    put(out.rotations, 4 * g + 3, (dqz - dot * z) / nrm);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) put(out.log_scales, 3 * g + j, dls[j]);
     // position: both affine plane projections + phase look direction
     double dpos[3];
 #pragma unroll
@@ -239,33 +254,21 @@ __global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view 
       dpos[0] += dP * (gP[0] - proj_d * d0) / dist;
       dpos[1] += dP * (gP[1] - proj_d * d1) / dist;
       dpos[2] += dP * (gP[2] - proj_d * d2) / dist;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) res[10 + k] = (float)(dP * basis[k]);
     }
-    res[0] = (float)dpos[0]; res[1] = (float)dpos[1]; res[2] = (float)dpos[2];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) put(out.sh_coeffs, 16 * g + k, active ? dP * basis[k] : 0.0);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) put(out.positions, 3 * g + k, dpos[k]);
     // softplus' = sigmoid (scene.py:36-39)
     const double k0 = ldv<T>(sc.ke_raw, 2 * g), k1 = ldv<T>(sc.ke_raw, 2 * g + 1);
-    res[26] = (float)(dk * 0.5 * (1.0 + tanh(0.5 * k0)));
-    res[27] = (float)(dk * 0.5 * (1.0 + tanh(0.5 * k1)));
+    put(out.ke_raw, 2 * g, dk * 0.5 * (1.0 + tanh(0.5 * k0)));
+    put(out.ke_raw, 2 * g + 1, dk * 0.5 * (1.0 + tanh(0.5 * k1)));
     // densification statistic in NDC units (backward.py:285-289)
     const double gx = duc[0] * (view.n_u / 2.0) + dui[0] * (view.n_az / 2.0);
     const double gy = duc[1] * (view.n_v / 2.0) + dui[1] * (view.n_rg / 2.0);
-    res[28] = (float)sqrt(gx * gx + gy * gy);
+    put(out.uv_grad_norm, g, sqrt(gx * gx + gy * gy));
   }
-  float* dst[5] = {out.positions, out.rotations, out.log_scales, out.sh_coeffs, out.ke_raw};
-  const int width[5] = {3, 4, 3, 16, 2};
-  int o = 0;
-#pragma unroll
-  for (int grp = 0; grp < 5; ++grp) {
-#pragma unroll
-    for (int k = 0; k < width[grp]; ++k) {
-      float* pp = dst[grp] + width[grp] * g + k;
-      *pp = accumulate ? *pp + res[o + k] : res[o + k];
-    }
-    o += width[grp];
-  }
-  out.uv_grad_norm[g] = accumulate ? out.uv_grad_norm[g] + res[28] : res[28];
-  out.visible[g] = accumulate ? out.visible[g] + (int)vis : (int)vis;
+  out.visible[g] = accumulate ? out.visible[g] + 1 : 1;
 }
 
 int launch_grad_image(const sdgr_view& v, const sdgr_projection& p, const double* intensity,

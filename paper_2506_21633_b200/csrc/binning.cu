@@ -13,15 +13,18 @@
 //
 // The radix sort is a single-pass-per-digit "onesweep" design: one upfront
 // histogram kernel for all digits, then per 8-bit digit one kernel that ranks
-// its 4096-key tile with warp match-ranking, resolves its global offset by
-// decoupled look-back, and scatters through shared memory.
+// its 2048-key tile with warp match-ranking, resolves its global offset by
+// decoupled look-back (4 predecessors per step: with a whole 1M-key pass
+// resident in one wave, a one-at-a-time look-back chain dominated -- see
+// profiles/ROUND1.md), and scatters through shared memory.  A chain-free
+// three-kernel pass (count / scan / scatter) was measured slower (41 vs 24 us).
 #include "common.cuh"
 
 namespace sdgr {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortIpt = 16;
-constexpr int kSortTile = kSortThreads * kSortIpt;  // 4096
+constexpr int kSortIpt = 8;
+constexpr int kSortTile = kSortThreads * kSortIpt;  // 2048
 constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kCountMask = (1u << 30) - 1;
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -149,14 +152,22 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   // decoupled look-back for this digit
   uint32_t prefix = 0;
   if (bid > 0) {
+    // 4-wide window: the four predecessor statuses are loaded together, so
+    // a chain of aggregate-only blocks costs 1/4 of the dependent loads
     int64_t j = bid - 1;
-    while (true) {
-      const uint32_t s = vstat[j * 256 + t];
-      const uint32_t f = s & ~kCountMask;
-      if (f == 0) continue;
-      prefix += s & kCountMask;
-      if (f == kFlagP) break;
-      --j;
+    bool done = false;
+    while (!done) {
+      uint32_t s[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s[k] = (j - k >= 0) ? (uint32_t)vstat[(j - k) * 256 + t] : (uint32_t)(2u << 30);
+      int k = 0;
+      for (; k < 4; ++k) {
+        const uint32_t f = s[k] & ~kCountMask;
+        if (f == 0) break;               // not published yet: retry from here
+        prefix += s[k] & kCountMask;
+        if (f == kFlagP) { done = true; break; }
+      }
+      if (!done) j -= k;
     }
     vstat[(int64_t)bid * 256 + t] = kFlagP | (prefix + total);
   }
@@ -264,6 +275,7 @@ template int radix_sort<uint32_t>(const uint32_t*, const uint32_t*, uint32_t*, u
 template size_t radix_ws_bytes<uint64_t>(int64_t, int);
 template size_t radix_ws_bytes<uint32_t>(int64_t, int);
 
+// --------------------------------------------------------------- scan ------
 // --------------------------------------------------------------- scan ------
 // Exclusive scan of v(i) = ntiles[order ? order[i] : i] into out[0..n],
 // out[n] = total.  Three phases: tile sums, scan of sums, tile rescans.

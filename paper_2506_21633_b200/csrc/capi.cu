@@ -21,13 +21,19 @@ size_t binning_ws_bytes(int64_t, int64_t);
 int launch_emit_and_sort(const sdgr_projection&, const sdgr_view&, const int32_t*, const int32_t*,
                          sdgr_tiles&, void*, size_t, cudaStream_t);
 int launch_composite_forward(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, double,
-                             double*, double*, double*, double*, int32_t*, cudaStream_t);
+                             double*, double*, double*, double*, int32_t*, const sdgr_replay*, cudaStream_t);
 int launch_splat(const sdgr_view&, const sdgr_projection&, const double*, double*, double*,
                  cudaStream_t);
 int launch_grad_image(const sdgr_view&, const sdgr_projection&, const double*, const double*, double*,
                       cudaStream_t);
 int launch_grad_intensity(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, double,
-                          const double*, const double*, double*, double*, double*, cudaStream_t);
+                          const double*, const double*, double*, double*, double*, const sdgr_replay*,
+                          cudaStream_t);
+
+static bool replay_ok(const sdgr_replay* r) {
+  return !r || (r->S && r->w && r->j && r->r && r->desc && r->desc_count && r->cursor && r->capacity > 0 &&
+                r->desc_per_item > 0);
+}
 int launch_grad_geometry(const sdgr_scene&, const sdgr_view&, const sdgr_projection&, const sdgr_tiles&,
                          const double*, const double*, const sdgr_grads&, int, cudaStream_t);
 
@@ -108,15 +114,15 @@ int sdgr_bin_pairs(const sdgr_projection* proj, const sdgr_view* view, const int
 
 int sdgr_composite_forward(const sdgr_view* view, const sdgr_projection* proj, const sdgr_tiles* comp,
                            double s_stop, double* seg_sum, double* seg_base, double* partial_I,
-                           double* intensity, int32_t* status, void* stream) {
+                           double* intensity, int32_t* status, sdgr_replay* replay, void* stream) {
   if (!view_ok(view) || !proj || !tiles_ok(comp) || comp->plane != 0 || !intensity || !status ||
-      !comp->pair_start)
+      !comp->pair_start || !replay_ok(replay))
     return SDGR_ERR_INVALID;
   if (comp->n_pairs > 0 && (!seg_sum || !seg_base || !partial_I || !comp->pair_pos || !comp->pair_rec))
     return SDGR_ERR_INVALID;
   if (std::isnan(s_stop)) return SDGR_ERR_INVALID;
   return launch_composite_forward(*view, *proj, *comp, s_stop, seg_sum, seg_base, partial_I, intensity,
-                                  status, static_cast<cudaStream_t>(stream));
+                                  status, replay, static_cast<cudaStream_t>(stream));
 }
 
 int sdgr_splat(const sdgr_view* view, const sdgr_projection* proj, const double* intensity, void* scratch,
@@ -134,12 +140,13 @@ int sdgr_grad_image(const sdgr_view* view, const sdgr_projection* proj, const do
 
 int sdgr_grad_intensity(const sdgr_view* view, const sdgr_projection* proj, const sdgr_tiles* comp,
                         double s_stop, const double* seg_base, const double* dL_dI, double* seg_g,
-                        double* seg_d, double* partial_g, void* stream) {
-  if (!view_ok(view) || !proj || !tiles_ok(comp) || comp->plane != 0 || !dL_dI) return SDGR_ERR_INVALID;
+                        double* seg_d, double* partial_g, const sdgr_replay* replay, void* stream) {
+  if (!view_ok(view) || !proj || !tiles_ok(comp) || comp->plane != 0 || !dL_dI || !replay_ok(replay))
+    return SDGR_ERR_INVALID;
   if (comp->n_pairs > 0 && (!seg_base || !seg_g || !seg_d || !partial_g || !comp->pair_rec))
     return SDGR_ERR_INVALID;
   if (std::isnan(s_stop)) return SDGR_ERR_INVALID;
-  return launch_grad_intensity(*view, *proj, *comp, s_stop, seg_base, dL_dI, seg_g, seg_d, partial_g,
+  return launch_grad_intensity(*view, *proj, *comp, s_stop, seg_base, dL_dI, seg_g, seg_d, partial_g, replay,
                                static_cast<cudaStream_t>(stream));
 }
 

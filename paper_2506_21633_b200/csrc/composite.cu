@@ -53,10 +53,11 @@ constexpr double kFixMax = 1.0e5;  // per-term clamp: keeps 8192-term sums far f
 
 template <int MODE>
 struct WalkCfg {
-  static constexpr int kCap = MODE == kGrad ? 2048 : 4096;  // flat pair slots
+  static constexpr int kCap = MODE == kGSum ? 4096 : 2048;  // flat pair slots
   static constexpr bool kXY = MODE == kGrad;
-  static constexpr size_t kSmem = kCap * (8 + 8 + (kXY ? 16 : 0) + 1);
+  static constexpr size_t kSmem = kCap * (8 + 8 + (kXY ? 16 : 0) + 2);
 };
+constexpr int kReplayCap = 2048;  // == WalkCfg<kContrib>::kCap: one descriptor fits the replay
 
 struct WalkArgs {
   int n_cols, n_rows, tiles_x;
@@ -73,6 +74,8 @@ struct WalkArgs {
   double* seg_out;         // kGSum: seg_g
   double* partial;         // kContrib: (n_pairs); kGrad: (n_pairs, 8)
   int32_t* status;
+  sdgr_replay rp;          // kContrib: live-pair log to write (rp.S == nullptr: none)
+  int item_base;           // unused (0)
 };
 
 // 256-bit in-tile member mask of one Gaussian (bit = local cell (iv&15)*16+(iu&15)).
@@ -294,6 +297,9 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
   double* fx = fs + kCap;                                   // kGrad: g*T*a*P
   double* fy = fx + (Cfg::kXY ? kCap : 0);                  // kGrad: T*(1-a)
   uint8_t* fj = reinterpret_cast<uint8_t*>(fy + (Cfg::kXY ? kCap : 0));
+  uint8_t* fr = fj + kCap;                                  // ray of each slot (replay log)
+  __shared__ long long rp_off;
+  const bool record = MODE == kContrib && a.rp.S != nullptr;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_items = *a.n_items;
@@ -313,6 +319,7 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
     if (MODE == kGrad) rem = a.seg_d[slot_ray] + a.seg_g[slot_ray];
     bool alive = valid && S < a.s_stop;
     bool bad = false;
+    int n_desc = 0;
 
     int cs = start;
     for (; cs < end; cs += kChunk) {
@@ -420,12 +427,35 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
           }
           for (; p < p1; ++p) fs[p] = __longlong_as_double(0x7ff0000000000000ll);  // dead: T = 0
           alive = S < a.s_stop;
+          if (record)
+            for (int q = roff; q < p1; ++q) fr[q] = (uint8_t)tid;
         }
+        if (record && tid == 0) {
+          const unsigned long long o = atomicAdd(a.rp.cursor, (unsigned long long)total);
+          const bool fits = o + (unsigned long long)total <= (unsigned long long)a.rp.capacity &&
+                            n_desc < a.rp.desc_per_item;
+          rp_off = fits ? (long long)o : -1ll;
+          if (fits) {
+            int4 d;
+            d.x = (int)o; d.y = total; d.z = cs; d.w = j0 | (j1 << 16);
+            reinterpret_cast<int4*>(a.rp.desc)[(int64_t)item * a.rp.desc_per_item + n_desc] = d;
+          } else {
+            a.rp.cursor[1] = 1ull;  // overflow: the host must re-walk
+          }
+        }
+        if (record) ++n_desc;
         __syncthreads();
         // ---- P4: flat pair-parallel transmittance and contributions
+        const long long lo = record ? rp_off : -1ll;
         for (int p = tid; p < total; p += kRays) {
           const int j = fj[p];
           const double wgt = fw[p];
+          if (lo >= 0) {
+            a.rp.S[lo + p] = fs[p];
+            a.rp.w[lo + p] = wgt;
+            a.rp.j[lo + p] = (uint8_t)j;
+            a.rp.r[lo + p] = fr[p];
+          }
           const double tau = sk[j] * wgt;
           const double T = exp(-fs[p]);
           const double oma = -expm1(-tau);
@@ -497,7 +527,161 @@ __global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
       }
     }
     if (MODE == kGSum) a.seg_out[slot_ray] = accd;
+    if (record && tid == 0) a.rp.desc_count[item] = min(n_desc, a.rp.desc_per_item);
     if (MODE == kContrib && __syncthreads_or(bad) && tid == 0) atomicOr(a.status + SDGR_STATUS_NONFINITE, 1);
+  }
+}
+
+// ============================================================ replay ==========
+// Backward over the live-pair log the forward walk wrote: per work item, its
+// sub-chunk descriptors in walk order; per descriptor the live pairs in
+// ray-major, depth-minor order with S_before and w.  No binning, membership
+// or weight work is repeated, and only live pairs are touched.
+//   kGSum: per (item, ray) sum of g * contrib          (backward.py:129-139)
+//   kGrad: reverse-recurrence terms, reduced per Gaussian in ray order into
+//          one partial record per (tile, Gaussian)      (backward.py:122-148)
+struct ReplayArgs {
+  sdgr_replay rp;
+  const sdgr_pair_rec* rec;
+  const int32_t* items;
+  const int32_t* n_items;
+  uint32_t* counter;
+  int tiles_x;
+  const double* gvec;     // dL/dI
+  const double* seg_g;    // kGrad
+  const double* seg_d;    // kGrad
+  double* seg_out;        // kGSum
+  double* partial;        // kGrad: (n_pairs, 8), zeroed beforehand
+};
+
+template <int MODE>
+struct ReplayCfg {
+  static constexpr size_t kSmem = kReplayCap * (MODE == kGrad ? 4 * 8 + 2 : 3 * 8 + 2);
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_replay(ReplayArgs a) {
+  constexpr bool kG = MODE == kGrad;
+  __shared__ int32_t run_s[kRays], run_e[kRays];
+  __shared__ double sk[kChunk], sp[kChunk], sg[kChunk];
+  __shared__ double su[kG ? kChunk : 1], sv[kG ? kChunk : 1], sa0[kG ? kChunk : 1], sa1[kG ? kChunk : 1],
+      sa2[kG ? kChunk : 1];
+  __shared__ uint32_t rows[kG ? 8 * kRays : 1];   // rows[w*256 + r]: Gaussians of ray r
+  __shared__ uint32_t jm[kG ? 8 * kChunk : 1];    // jm[w*256 + j]: rays of Gaussian j
+  __shared__ int item_s;
+  extern __shared__ double dyn[];
+  double* fS = dyn;                 // S_before, then (kGrad) g*T*a*P
+  double* fW = fS + kReplayCap;     // w
+  double* fG = fW + kReplayCap;     // g*contrib, then (kGrad) downstream sum D
+  double* fY = fG + kReplayCap;     // kGrad: T*(1-a)
+  uint8_t* fj = reinterpret_cast<uint8_t*>(fG + (kG ? 2 : 1) * kReplayCap);
+  uint8_t* fr = fj + kReplayCap;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int n_items = *a.n_items;
+  while (true) {
+    __syncthreads();
+    if (tid == 0) item_s = (int)atomicAdd(a.counter, 1u);
+    __syncthreads();
+    const int item = item_s;
+    if (item >= n_items) return;
+    const int tile = reinterpret_cast<const int4*>(a.items)[item].x;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int64_t slot_ray = (int64_t)item * kRays + tid;
+    double accd = 0.0, rem = 0.0;
+    if (kG) rem = a.seg_d[slot_ray] + a.seg_g[slot_ray];
+    const int nd = a.rp.desc_count[item];
+    for (int k = 0; k < nd; ++k) {
+      const int4 d = reinterpret_cast<const int4*>(a.rp.desc)[(int64_t)item * a.rp.desc_per_item + k];
+      const int64_t off = d.x;
+      const int n = d.y, cs = d.z, j0 = d.w & 0xffff, j1 = d.w >> 16;
+      __syncthreads();
+      // stage the descriptor's Gaussians and load its pairs
+      int pos = -1;
+      if (tid >= j0 && tid < j1) {
+        const sdgr_pair_rec r = load_rec(a.rec + cs + tid);
+        sk[tid] = r.kappa;
+        sp[tid] = r.phase;
+        sg[tid] = a.gvec[r.prim];
+        if (kG) {
+          su[tid] = r.u; sv[tid] = r.v;
+          sa0[tid] = r.a00; sa1[tid] = r.a01; sa2[tid] = r.a11;
+          pos = r.pos;
+        }
+      }
+      run_s[tid] = 0;
+      run_e[tid] = 0;
+      if (kG) {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) { rows[w * kRays + tid] = 0u; jm[w * kChunk + tid] = 0u; }
+      }
+      for (int p = tid; p < n; p += kRays) {
+        fS[p] = a.rp.S[off + p];
+        fW[p] = a.rp.w[off + p];
+        fj[p] = a.rp.j[off + p];
+        fr[p] = a.rp.r[off + p];
+      }
+      __syncthreads();
+      // ray runs (pairs are ray-major) and, for kGrad, the two membership bitmaps
+      for (int p = tid; p < n; p += kRays) {
+        const int r = fr[p];
+        if (p == 0 || fr[p - 1] != r) run_s[r] = p;
+        if (p == n - 1 || fr[p + 1] != r) run_e[r] = p + 1;
+        if (kG) {
+          const int j = fj[p];
+          atomicOr(rows + (j >> 5) * kRays + r, 1u << (j & 31));
+          atomicOr(jm + (r >> 5) * kChunk + j, 1u << (r & 31));
+        }
+      }
+      // pair-parallel transmittance and contributions
+      for (int p = tid; p < n; p += kRays) {
+        const int j = fj[p];
+        const double tau = sk[j] * fW[p];
+        const double T = exp(-fS[p]);
+        const double oma = -expm1(-tau);
+        const double gI = sg[j];
+        fG[p] = gI * (T * oma * sp[j]);
+        if (kG) {
+          fS[p] = gI * T * exp(-tau) * sp[j];
+          fY[p] = T * oma;
+        }
+      }
+      __syncthreads();
+      // ray-serial sums (additions only)
+      if (!kG) {
+        for (int p = run_s[tid]; p < run_e[tid]; ++p) accd += fG[p];
+      } else {
+        for (int p = run_s[tid]; p < run_e[tid]; ++p) {
+          rem -= fG[p];
+          fG[p] = rem;  // downstream sum after this pair
+        }
+        __syncthreads();
+        // per-Gaussian reduction over its rays in ascending order
+        if (tid >= j0 && tid < j1) {
+          double racc[7] = {0, 0, 0, 0, 0, 0, 0};
+          const int jw = tid >> 5;
+          const uint32_t below = (1u << lane) - 1u;
+#pragma unroll 1
+          for (int w = 0; w < 8; ++w) {
+            uint32_t m = jm[w * kChunk + tid];
+            while (m) {
+              const int b = __ffs(m) - 1;
+              m &= m - 1;
+              const int r = w * 32 + b;
+              int idx = __popc(rows[jw * kRays + r] & below);
+              for (int q = 0; q < jw; ++q) idx += __popc(rows[q * kRays + r]);
+              const int p = run_s[r] + idx;
+              const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
+              const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
+              grad_terms(fY[p], (fS[p] - fG[p]) * fW[p], sk[tid], dx, dy, sa0[tid], sa1[tid], sa2[tid], racc);
+            }
+          }
+          double4* recp = reinterpret_cast<double4*>(a.partial + (int64_t)pos * 8);
+          recp[0] = make_double4(racc[0] * sg[tid], racc[1], racc[2], racc[3]);
+          recp[1] = make_double4(racc[4], racc[5], racc[6], 0.0);
+        }
+      }
+    }
+    if (!kG) a.seg_out[slot_ray] = accd;
   }
 }
 
@@ -577,7 +761,9 @@ static WalkArgs base_args(const sdgr_view& v, const sdgr_tiles& t) {
 
 int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const sdgr_tiles& t,
                              double s_stop, double* seg_sum, double* seg_base, double* partial_I,
-                             double* intensity, int32_t* status, cudaStream_t st) {
+                             double* intensity, int32_t* status, const sdgr_replay* rp, cudaStream_t st) {
+  if (rp && cudaMemsetAsync(rp->cursor, 0, 2 * sizeof(unsigned long long), st) != cudaSuccess)
+    return SDGR_ERR_CUDA;
   if (t.n_pairs > 0) {
     uint32_t* counter = reinterpret_cast<uint32_t*>(t.n_items + 2);
     if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
@@ -592,6 +778,7 @@ int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const
     a.seg_base = seg_base;
     a.partial = partial_I;
     a.status = status;
+    if (rp) a.rp = *rp;
     const int rc = launch_walk<kContrib>(a, t.max_items, st);
     if (rc) return rc;
   }
@@ -615,8 +802,43 @@ int launch_splat(const sdgr_view& v, const sdgr_projection& p, const double* int
 
 int launch_grad_intensity(const sdgr_view& v, const sdgr_projection& p, const sdgr_tiles& t,
                           double s_stop, const double* seg_base, const double* dL_dI, double* seg_g,
-                          double* seg_d, double* partial_g, cudaStream_t st) {
+                          double* seg_d, double* partial_g, const sdgr_replay* rp, cudaStream_t st) {
   if (t.n_pairs == 0) return SDGR_OK;
+  if (rp) {
+    // replay the forward's live-pair log
+    ReplayArgs r{};
+    r.rp = *rp;
+    r.rec = t.pair_rec;
+    r.items = t.items;
+    r.n_items = t.n_items;
+    r.counter = reinterpret_cast<uint32_t*>(t.n_items + 2);
+    r.tiles_x = t.tiles_x;
+    r.gvec = dL_dI;
+    r.seg_out = seg_g;
+    static int per_sm[2] = {0, 0};
+    if (per_sm[0] == 0) {
+      cudaFuncSetAttribute(k_replay<kGSum>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ReplayCfg<kGSum>::kSmem);
+      cudaFuncSetAttribute(k_replay<kGrad>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ReplayCfg<kGrad>::kSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], k_replay<kGSum>, 256, ReplayCfg<kGSum>::kSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], k_replay<kGrad>, 256, ReplayCfg<kGrad>::kSmem);
+    }
+    if (cudaMemsetAsync(r.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
+    k_replay<kGSum><<<max(1, min(t.max_items, sm_count() * max(per_sm[0], 1))), 256, ReplayCfg<kGSum>::kSmem, st>>>(r);
+    k_seg_scan<true><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_g, seg_d);
+    note_launch(2);
+    if (cudaMemsetAsync(partial_g, 0, sizeof(double) * 8 * (size_t)t.n_pairs, st) != cudaSuccess ||
+        cudaMemsetAsync(r.counter, 0, sizeof(uint32_t), st) != cudaSuccess)
+      return SDGR_ERR_CUDA;
+    r.seg_out = nullptr;
+    r.seg_g = seg_g;
+    r.seg_d = seg_d;
+    r.partial = partial_g;
+    k_replay<kGrad><<<max(1, min(t.max_items, sm_count() * max(per_sm[1], 1))), 256, ReplayCfg<kGrad>::kSmem, st>>>(r);
+    note_launch();
+    return check_launch();
+  }
   WalkArgs a = base_args(v, t);
   a.s_stop = s_stop;
   a.seg_base = seg_base;

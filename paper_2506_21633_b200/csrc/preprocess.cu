@@ -42,7 +42,9 @@ __device__ __forceinline__ double ld(const T* p, int64_t i) { return (double)__l
 
 // Footprint of one plane: inverse covariance, clipped bbox, member masks.
 // Writes the plane records for Gaussian g.  (forward.py:33-42, 60-109)
-__device__ void plane_footprint(const sdgr_plane& pl, int64_t g, double u, double v,
+// Returns an upper bound of the Gaussian's member cells on this plane (exact
+// for footprints inside the 8x8 window, the bbox area otherwise).
+__device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double v,
                                 double c00, double c01, double c11, int nu, int nv,
                                 double cutoff, bool dense) {
   // invert_cov2d (forward.py:33-42)
@@ -82,12 +84,18 @@ __device__ void plane_footprint(const sdgr_plane& pl, int64_t g, double u, doubl
         for (int iu = x0; iu <= x1; ++iu) {
           const double dx = dsub((double)iu, u);
           const double q = dadd(dadd(dmul(a00, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
-          if (dense || q <= cut2) {
-            cmask |= 1ull << ((iv - y0) * 8 + (iu - x0));
-            tmask |= 1ull << (((iv >> 4) - ty0) * 8 + ((iu >> 4) - tx0));
-          }
+          if (dense || q <= cut2) cmask |= 1ull << ((iv - y0) * 8 + (iu - x0));
         }
       }
+      // member tiles of the (<= 2x2 tile) window from the cell bits: split the
+      // window's columns / rows at the tile boundary
+      const int csplit = min(8, kTile - (x0 & 15)), rsplit = min(8, kTile - (y0 & 15));
+      const uint64_t col0 = 0x0101010101010101ull * ((1ull << csplit) - 1ull);
+      const uint64_t row0 = rsplit >= 8 ? ~0ull : ((1ull << (8 * rsplit)) - 1ull);
+      if (cmask & col0 & row0) tmask |= 1ull;
+      if (cmask & ~col0 & row0) tmask |= 1ull << 1;
+      if (cmask & col0 & ~row0) tmask |= 1ull << 8;
+      if (cmask & ~col0 & ~row0) tmask |= 1ull << 9;
       ntiles = __popcll(tmask);
     } else if (dense) {
       ntiles = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
@@ -123,6 +131,9 @@ __device__ void plane_footprint(const sdgr_plane& pl, int64_t g, double u, doubl
   pl.cell_mask[g] = cmask;
   pl.tile_mask[g] = tmask;
   pl.n_tiles[g] = ntiles;
+  if (x0 > x1 || y0 > y1) return 0;
+  if ((x1 - x0) < 8 && (y1 - y0) < 8) return __popcll(cmask);
+  return (x1 - x0 + 1) * (y1 - y0 + 1);
 }
 
 __device__ void plane_empty(const sdgr_plane& pl, int64_t g) {
@@ -137,6 +148,7 @@ __global__ void __launch_bounds__(256) k_project(sdgr_scene scene, sdgr_view vie
                                                  sdgr_projection proj) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int n_vis = 0, n_skip = 0, n_cull = 0;
+  unsigned long long m_comp = 0, m_img = 0;
   if (g < scene.n) {
     const T* P = static_cast<const T*>(scene.positions);
     const T* Q = static_cast<const T*>(scene.rotations);
@@ -234,8 +246,8 @@ __global__ void __launch_bounds__(256) k_project(sdgr_scene scene, sdgr_view vie
     proj.flags[g] = (uint8_t)((vis ? SDGR_FLAG_VISIBLE : 0) | (!ok ? SDGR_FLAG_SKIPPED : 0) |
                               ((ok && !inside) ? SDGR_FLAG_CULLED : 0));
     if (vis) {
-      plane_footprint(proj.comp, g, uc, vc, cc00, cc01, cc11, view.n_u, view.n_v, view.cutoff, dense);
-      plane_footprint(proj.img, g, ui, vi, ci00, ci01, ci11, view.n_az, view.n_rg, view.cutoff, dense);
+      m_comp = plane_footprint(proj.comp, g, uc, vc, cc00, cc01, cc11, view.n_u, view.n_v, view.cutoff, dense);
+      m_img = plane_footprint(proj.img, g, ui, vi, ci00, ci01, ci11, view.n_az, view.n_rg, view.cutoff, dense);
       proj.depth_key[g] = depth_key(depth);
       // phase function and extinction (geometry.py:308-317)
       const double r0 = p0 - view.cam[0], r1 = p1 - view.cam[1], r2 = p2 - view.cam[2];
@@ -278,12 +290,27 @@ __global__ void __launch_bounds__(256) k_project(sdgr_scene scene, sdgr_view vie
     if (n_skip) atomicAdd(proj.counters + 1, n_skip);
     if (n_cull) atomicAdd(proj.counters + 2, n_cull);
   }
+  if (proj.member_pairs) {
+    // warp-aggregated member-pair counts (replay-log capacity)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      m_comp += __shfl_down_sync(0xffffffffu, m_comp, off);
+      m_img += __shfl_down_sync(0xffffffffu, m_img, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (m_comp) atomicAdd(proj.member_pairs + 0, m_comp);
+      if (m_img) atomicAdd(proj.member_pairs + 1, m_img);
+    }
+  }
 }
 
 int launch_project(const sdgr_scene& scene, const sdgr_view& view, sdgr_projection& proj,
                    cudaStream_t stream) {
   if (scene.n <= 0) return SDGR_ERR_INVALID;
   if (cudaMemsetAsync(proj.counters, 0, 4 * sizeof(int32_t), stream) != cudaSuccess)
+    return SDGR_ERR_CUDA;
+  if (proj.member_pairs &&
+      cudaMemsetAsync(proj.member_pairs, 0, 2 * sizeof(unsigned long long), stream) != cudaSuccess)
     return SDGR_ERR_CUDA;
   const int threads = 256;
   const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);

@@ -26,7 +26,7 @@ from . import _lib
 from ._lib import ptr
 from .errors import NumericalError
 from .radar import view_constants
-from .rasterizer import (DEFAULT_COV_REG, DEFAULT_CUTOFF, S_STOP, SceneGradients, TILE, _check, _empty,
+from .rasterizer import (DEFAULT_COV_REG, DEFAULT_CUTOFF, S_STOP, ReplayLog, SceneGradients, TILE, _check, _empty,
                          _scene_desc, _seg_len, _stream)
 from .scene import DeviceScene
 
@@ -111,6 +111,8 @@ class MultiViewStep:
         self.pd.phase_raw, self.pd.flags, self.pd.counters = ptr(self.phase_raw), ptr(self.flags), ptr(self.counters)
         self.pd.ke_act = None
         self.pd.look = None
+        self.member_pairs = torch.zeros((2,), dtype=torch.int64, device=dev)
+        self.pd.member_pairs = ptr(self.member_pairs)
         self.order = _empty((n,), torch.int32, dev)
         self.intensity = _empty((n,), torch.float64, dev)
         self.image = _empty(self.img_shape, torch.float64, dev)
@@ -166,6 +168,10 @@ class MultiViewStep:
             d.seg_len, d.max_items, d.device_count = seg, max_items, 1
             self.planes[pl] = _PlaneBufs(offsets=_empty((n + 1,), torch.int32, dev), tiles=d, t=t)
         self.splat_scratch = _empty((v.n_rg * v.n_az,), torch.int64, dev)
+        # live-pair log: member pairs bound every view's live pairs
+        d0 = self.planes[0].tiles
+        self.replay = ReplayLog(int(getattr(self, "calib_tc", cap_pairs[0] * 16) * self.headroom),
+                                d0.max_items, d0.seg_len, dev)
         self.cap = dict(cap_pairs)
 
     def calibrate(self):
@@ -183,7 +189,10 @@ class MultiViewStep:
             for pl in (0, 1):
                 _check(self.lib.sdgr_count_pairs(C.byref(self.pd), pl, ptr(self.order) if pl == 0 else None,
                                                  ptr(off[pl]), ptr(ws), ws_bytes, st), "sdgr_count_pairs")
-            tot = torch.stack([off[0][self.n], off[1][self.n]]).cpu().tolist()
+            tot = torch.cat([torch.stack([off[0][self.n], off[1][self.n]]).to(torch.int64),
+                             self.member_pairs]).cpu().tolist()
+            self.calib_tc = max(getattr(self, "calib_tc", 0), tot[2])
+            tot = tot[:2]
             mx = {0: max(mx[0], tot[0]), 1: max(mx[1], tot[1])}
             self.calib_t16.append(tot)
         self.calib_t16_mean = {pl: float(np.mean([t[pl] for t in self.calib_t16])) for pl in (0, 1)}
@@ -211,7 +220,8 @@ class MultiViewStep:
         mark(3)
         _check(lib.sdgr_composite_forward(C.byref(v), pd, C.byref(P0.tiles), self.s_stop, ptr(t0["seg_a"]),
                                           ptr(t0["seg_b"]), ptr(t0["partial_I"]), ptr(self.intensity),
-                                          ptr(self.status), st), "sdgr_composite_forward")
+                                          ptr(self.status), C.byref(self.replay.desc_c), st),
+               "sdgr_composite_forward")
         mark(4)
         _check(lib.sdgr_splat(C.byref(v), pd, ptr(self.intensity), ptr(self.splat_scratch), ptr(self.image), st),
                "sdgr_splat")
@@ -222,7 +232,8 @@ class MultiViewStep:
         # seg_b holds the forward's exclusive prefixes; seg_a is reused as scratch
         _check(lib.sdgr_grad_intensity(C.byref(v), pd, C.byref(P0.tiles), self.s_stop, ptr(t0["seg_b"]),
                                        ptr(self.acc_img[0]), ptr(t0["seg_a"]), ptr(t0["seg_c"]),
-                                       ptr(t0["partial_g"]), st), "sdgr_grad_intensity")
+                                       ptr(t0["partial_g"]), C.byref(self.replay.desc_c), st),
+               "sdgr_grad_intensity")
         mark(7)
         _check(lib.sdgr_grad_geometry(C.byref(self.sd), C.byref(v), pd, C.byref(P0.tiles), ptr(self.acc_img),
                                       ptr(t0["partial_g"]), C.byref(self.gd), 1, st), "sdgr_grad_geometry")
@@ -257,9 +268,10 @@ class MultiViewStep:
 
     def check(self):
         """One host read per step: capacity overflow and non-finite status."""
-        flags = torch.stack([self.planes[0].t["n_items"][1], self.status[0]])
-        ov0, bad = flags.cpu().tolist()
-        if ov0:
+        flags = torch.stack([self.planes[0].t["n_items"][1].to(torch.int64), self.status[0].to(torch.int64),
+                             self.replay.cursor[1]])
+        ov0, bad, ov_replay = flags.cpu().tolist()
+        if ov0 or ov_replay:
             raise OverflowError("pair capacity exceeded; recalibrate")
         if bad:
             raise NumericalError("non-finite intensity in a multi-view step")

@@ -115,6 +115,7 @@ class Projection:
         self.phase_raw = _empty((n,), torch.float64, device)
         self.flags = _empty((n,), torch.uint8, device)
         self.counters = torch.zeros((4,), dtype=torch.int32, device=device)
+        self.member_pairs = torch.zeros((2,), dtype=torch.int64, device=device)
         self.ke_act = _empty((n, 2), torch.float64, device) if accessors else None
         self.look = _empty((n, 4), torch.float64, device) if accessors else None
         self._vis_idx = None
@@ -128,6 +129,7 @@ class Projection:
         d.depth_key, d.kappa, d.phase, d.phase_raw = (
             ptr(self.depth_key), ptr(self.kappa), ptr(self.phase_f), ptr(self.phase_raw))
         d.flags, d.counters, d.ke_act, d.look = ptr(self.flags), ptr(self.counters), ptr(self.ke_act), ptr(self.look)
+        d.member_pairs = ptr(self.member_pairs)
         return d
 
     # -- reference-shaped accessors (compacted to the K visible rows) -------
@@ -272,6 +274,7 @@ class TileLists:
     tile_first: torch.Tensor
     n_items: torch.Tensor
     pair_rec: torch.Tensor | None = None
+    member_pairs: int | None = None   # member (cell, Gaussian) pairs of the plane (upper bound)
     _desc: object = field(default=None, repr=False)
 
     @property
@@ -329,7 +332,9 @@ class _Binner:
             _check(lib.sdgr_count_pairs(C.byref(p._desc), pl, ptr(order) if pl == 0 else None, ptr(off),
                                         ptr(ws), ws_bytes, st), "sdgr_count_pairs")
             offsets[pl] = off
-        totals = torch.stack([offsets[pl][n] for pl in planes]).cpu().tolist()
+        host = torch.cat([torch.stack([offsets[pl][n] for pl in planes]).to(torch.int64), p.member_pairs]).cpu()
+        totals = host[: len(planes)].tolist()
+        self.member_pairs = host[len(planes):].tolist()
         max_pairs = max(max(totals), 1)
         ws_bytes = lib.sdgr_workspace_bytes(n, max_pairs)
         ws = _empty((ws_bytes,), torch.uint8, dev)
@@ -357,6 +362,7 @@ class _Binner:
             _check(lib.sdgr_bin_pairs(C.byref(p._desc), C.byref(p.view), ptr(order) if pl == 0 else None,
                                       ptr(offsets[pl]), C.byref(tl.desc()), ptr(ws), ws_bytes, st),
                    "sdgr_bin_pairs")
+            tl.member_pairs = int(self.member_pairs[pl])
             out[pl] = tl
         self.order = order
         return out
@@ -386,6 +392,7 @@ class IntensityBuffer:
     status: torch.Tensor
     s_stop: float
     indices: torch.Tensor | None = None
+    replay: "ReplayLog | None" = None
 
     @property
     def intensity(self) -> torch.Tensor:
@@ -393,8 +400,33 @@ class IntensityBuffer:
         return self.intensity_n if self.indices is None else self.intensity_n[self.indices]
 
 
+class ReplayLog:
+    """Buffers of the live-pair log (sdgr_replay, include/sdgr.h): written by
+    the forward walk, replayed by the backward so it touches live pairs only."""
+
+    def __init__(self, capacity: int, max_items: int, seg_len: int, device):
+        cap = int(max(capacity, 1))
+        self.capacity = cap
+        self.desc_per_item = 40 * max(1, -(-seg_len // 256))
+        self.S = _empty((cap,), torch.float64, device)
+        self.w = _empty((cap,), torch.float64, device)
+        self.j = _empty((cap,), torch.uint8, device)
+        self.r = _empty((cap,), torch.uint8, device)
+        self.desc = _empty((max(max_items, 1) * self.desc_per_item, 4), torch.int32, device)
+        self.desc_count = torch.zeros((max(max_items, 1),), dtype=torch.int32, device=device)
+        self.cursor = torch.zeros((2,), dtype=torch.int64, device=device)
+        d = _lib.ReplayDesc()
+        d.capacity, d.desc_per_item = cap, self.desc_per_item
+        d.S, d.w, d.j, d.r = ptr(self.S), ptr(self.w), ptr(self.j), ptr(self.r)
+        d.desc, d.desc_count, d.cursor = ptr(self.desc), ptr(self.desc_count), ptr(self.cursor)
+        self.desc_c = d
+
+    def overflowed(self) -> bool:
+        return bool(self.cursor[1].item())
+
+
 def compute_intensities(rays: TileLists, projection: Projection, s_stop: float = S_STOP,
-                        check: bool = True) -> IntensityBuffer:
+                        check: bool = True, replay: bool = True) -> IntensityBuffer:
     """forward.compute_intensities (forward.py:178-199) on the device."""
     dev = projection.flags.device
     n = projection.n_scene
@@ -407,9 +439,12 @@ def compute_intensities(rays: TileLists, projection: Projection, s_stop: float =
         status=torch.zeros((4,), dtype=torch.int32, device=dev),
         s_stop=float(s_stop),
     )
+    if replay and rays.member_pairs is not None:
+        buf.replay = ReplayLog(rays.member_pairs, rays.max_items, rays.seg_len, dev)
     _check(_lib.lib().sdgr_composite_forward(
         C.byref(projection.view), C.byref(projection._desc), C.byref(rays.desc()), float(s_stop),
-        ptr(buf.seg_sum), ptr(buf.seg_base), ptr(buf.partial), ptr(buf.intensity_n), ptr(buf.status), _stream()),
+        ptr(buf.seg_sum), ptr(buf.seg_base), ptr(buf.partial), ptr(buf.intensity_n), ptr(buf.status),
+        C.byref(buf.replay.desc_c) if buf.replay else None, _stream()),
         "sdgr_composite_forward")
     if check:
         _raise_if_nonfinite(buf, projection, rays)
@@ -566,7 +601,7 @@ def grad_image_stage(fwd: ForwardResult, dL_dS: torch.Tensor) -> torch.Tensor:
     return acc
 
 
-def grad_intensity_stage(fwd: ForwardResult, dL_dI: torch.Tensor) -> torch.Tensor:
+def grad_intensity_stage(fwd: ForwardResult, dL_dI: torch.Tensor, use_replay: bool = True) -> torch.Tensor:
     """backward.grad_intensity_stage (backward.py:107-148): per-(tile, Gaussian)
     partials (T16, 8) float64 = [dL/dP, dL/dkappa, dL/dA00, dL/dA01, dL/dA11,
     dL/du, dL/dv, 0] on the computation plane, indexed by pre-sort position."""
@@ -576,9 +611,11 @@ def grad_intensity_stage(fwd: ForwardResult, dL_dI: torch.Tensor) -> torch.Tenso
     cap = max(rays.max_items, 1) * 256
     seg_g = _empty((cap,), torch.float64, dev)
     seg_d = _empty((cap,), torch.float64, dev)
+    rp = buf.replay if (use_replay and buf.replay is not None and not buf.replay.overflowed()) else None
     _check(_lib.lib().sdgr_grad_intensity(C.byref(p.view), C.byref(p._desc), C.byref(rays.desc()),
                                           buf.s_stop, ptr(buf.seg_base), ptr(dL_dI), ptr(seg_g), ptr(seg_d),
-                                          ptr(partial), _stream()), "sdgr_grad_intensity")
+                                          ptr(partial), C.byref(rp.desc_c) if rp else None, _stream()),
+           "sdgr_grad_intensity")
     return partial
 
 
@@ -604,8 +641,11 @@ def _as_device_grad(dL_dS, fwd: ForwardResult) -> torch.Tensor:
 
 
 def backward(fwd: ForwardResult, dL_dS, out: SceneGradients | None = None, accumulate: bool = False,
-             validate: bool = True) -> SceneGradients:
-    """Full backward from an image gradient (backward.py:243-290)."""
+             validate: bool = True, use_replay: bool = True) -> SceneGradients:
+    """Full backward from an image gradient (backward.py:243-290).
+
+    use_replay=False re-walks the tile lists instead of replaying the forward's
+    live-pair log (both are parity-tested; the replay is the fast path)."""
     shape = tuple(dL_dS.shape)
     img_shape = (fwd.projection.view.n_rg, fwd.projection.view.n_az)
     if shape != img_shape:
@@ -616,7 +656,7 @@ def backward(fwd: ForwardResult, dL_dS, out: SceneGradients | None = None, accum
     if validate and not bool(torch.isfinite(g).all().item()):
         raise InvalidParameterError("dL_dS contains non-finite values")
     acc_img = grad_image_stage(fwd, g)
-    partial = grad_intensity_stage(fwd, acc_img[0])
+    partial = grad_intensity_stage(fwd, acc_img[0], use_replay=use_replay)
     grads = grad_geometry_stage(fwd, acc_img, partial, out=out, accumulate=accumulate)
     return grads.to_numpy() if fwd.host and out is None else grads
 
