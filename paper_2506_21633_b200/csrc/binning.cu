@@ -566,8 +566,9 @@ int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, con
 }
 
 size_t binning_ws_bytes(int64_t n, int64_t max_pairs) {
-  // depth sort: sorted keys + radix scratch (8 passes of 64-bit keys)
-  const size_t depth = align_up(sizeof(uint64_t) * (size_t)n) + radix_ws_bytes<uint64_t>(n, 8);
+  // depth sort: range + 32-bit keys (2 arrays) + radix scratch (4 passes of 32-bit keys)
+  const size_t depth = align_up(16) + 2 * align_up(sizeof(uint32_t) * (size_t)n) +
+                       radix_ws_bytes<uint32_t>(n, 4);
   // pair sort: keys + radix scratch (up to 2 passes of 32-bit keys)
   const size_t pairs = align_up(sizeof(uint32_t) * (size_t)max_pairs) +
                        radix_ws_bytes<uint32_t>(max_pairs, 2);
@@ -575,14 +576,103 @@ size_t binning_ws_bytes(int64_t n, int64_t max_pairs) {
   return std::max(std::max(depth, pairs), scan) + 4096;
 }
 
+// ------------------------------------------------------ depth order --------
+// Exact stable (FP64 depth, index) order with a 32-bit radix sort:
+//   1. min / max of the visible depth keys;
+//   2. k32 = floor((d - dmin) * (2^32 - 2) / (dmax - dmin)): monotone
+//      non-decreasing in d (every FP64 step is monotone), invisible = ~0u;
+//   3. stable 4-pass radix sort of k32 (ties keep index order);
+//   4. runs of equal k32 (depths closer than (dmax-dmin)/2^32) are re-sorted
+//      by the full 64-bit key, index as tie-break -- exactly np.lexsort's
+//      (depth, index) order (forward.py:147), at half the passes of a 64-bit sort.
+__device__ __forceinline__ double key_to_depth(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+__global__ void __launch_bounds__(256) k_key_range(const uint64_t* key, int64_t n, unsigned long long* range) {
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = key[i];
+    if (k != ~0ull) {
+      lo = k < lo ? k : lo;
+      hi = k > hi ? k : hi;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long a = __shfl_down_sync(0xffffffffu, lo, off);
+    const unsigned long long b = __shfl_down_sync(0xffffffffu, hi, off);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(range, lo);
+    atomicMax(range + 1, hi);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_key32(const uint64_t* key, int64_t n, const unsigned long long* range,
+                                               uint32_t* k32) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t k = key[i];
+  if (k == ~0ull) { k32[i] = 0xffffffffu; return; }
+  const double dmin = key_to_depth(range[0]), dmax = key_to_depth(range[1]);
+  const double span = dsub(dmax, dmin);
+  double q = 0.0;
+  if (span > 0.0) q = dmul(dsub(key_to_depth(k), dmin), 4294967294.0 / span);
+  k32[i] = (uint32_t)fmin(fmax(q, 0.0), 4294967294.0);
+}
+
+// one thread per run of equal k32 (runs are rare and short); stable by index
+__global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s, const uint64_t* key, int64_t n,
+                                                  int32_t* order) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t k = k32s[i];
+  if (k == 0xffffffffu) return;                       // invisible tail: order irrelevant
+  if (i > 0 && k32s[i - 1] == k) return;               // not a run start
+  if (i + 1 >= n || k32s[i + 1] != k) return;          // run of length 1
+  int64_t e = i + 1;
+  while (e < n && k32s[e] == k) ++e;
+  for (int64_t a = i + 1; a < e; ++a) {                // insertion sort by (key, index)
+    const int32_t g = order[a];
+    const uint64_t kg = key[g];
+    int64_t b = a - 1;
+    while (b >= i) {
+      const int32_t h = order[b];
+      const uint64_t kh = key[h];
+      if (kh < kg || (kh == kg && h < g)) break;
+      order[b + 1] = h;
+      --b;
+    }
+    order[b + 1] = g;
+  }
+}
+
 int launch_depth_order(const sdgr_projection& proj, int32_t* order, void* ws, size_t ws_bytes,
                        cudaStream_t st) {
   const int64_t n = proj.n;
-  uint64_t* ksorted = static_cast<uint64_t*>(ws);
-  const size_t used = align_up(sizeof(uint64_t) * (size_t)n);
+  char* p = static_cast<char*>(ws);
+  unsigned long long* range = reinterpret_cast<unsigned long long*>(p); p += align_up(16);
+  uint32_t* k32 = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)n);
+  uint32_t* k32s = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)n);
+  const size_t used = (size_t)(p - static_cast<char*>(ws));
   if (used > ws_bytes) return SDGR_ERR_CAPACITY;
-  return radix_sort<uint64_t>(proj.depth_key, nullptr, ksorted, reinterpret_cast<uint32_t*>(order), n,
-                              nullptr, 0, 64, static_cast<char*>(ws) + used, ws_bytes - used, st);
+  if (cudaMemsetAsync(range, 0xff, sizeof(unsigned long long), st) != cudaSuccess ||
+      cudaMemsetAsync(range + 1, 0, sizeof(unsigned long long), st) != cudaSuccess)
+    return SDGR_ERR_CUDA;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  k_key_range<<<std::min<unsigned>(blocks, 148 * 8), 256, 0, st>>>(proj.depth_key, n, range);
+  k_key32<<<blocks, 256, 0, st>>>(proj.depth_key, n, range, k32);
+  note_launch(2);
+  const int rc = radix_sort<uint32_t>(k32, nullptr, k32s, reinterpret_cast<uint32_t*>(order), n, nullptr, 0,
+                                      32, p, ws_bytes - used, st);
+  if (rc != SDGR_OK) return rc;
+  k_fix_runs<<<blocks, 256, 0, st>>>(k32s, proj.depth_key, n, order);
+  note_launch();
+  return check_launch();
 }
 
 }  // namespace sdgr

@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(256) k_splat_finish(const unsigned long long* 
 
 // ============================================================ tile walks ======
 template <int MODE>
-__global__ void __launch_bounds__(256) k_walk(WalkArgs a) {
+__global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
   using Cfg = WalkCfg<MODE>;
   constexpr int kCap = Cfg::kCap;
   __shared__ uint32_t rows[8 * kRays];   // rows[w*256 + r]: bit (j&31) of word w = Gaussian j covers ray r
@@ -560,7 +560,7 @@ struct ReplayCfg {
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(256) k_replay(ReplayArgs a) {
+__global__ void __launch_bounds__(256, 3) k_replay(ReplayArgs a) {
   constexpr bool kG = MODE == kGrad;
   __shared__ int32_t run_s[kRays], run_e[kRays];
   __shared__ double sk[kChunk], sp[kChunk], sg[kChunk];

@@ -243,3 +243,21 @@ def test_multiview_step_equals_sum_of_views():
     for k in ref:
         assert_close(getattr(got, k).double().cpu().numpy(), ref[k].cpu().numpy(), atol=1e-5, rtol=1e-5, what=k)
     assert torch.equal(got.visible.cpu(), vis.cpu())
+
+
+def test_depth_ties_and_near_ties_vs_oracle():
+    """Exact (depth, index) order with duplicated positions (ties -> index
+    order) and positions 1e-12 m apart (runs of equal 32-bit depth keys)."""
+    rng = np.random.default_rng(31)
+    base = targets.random_scene(rng, 300, spread=2.0, scale_low=0.2, scale_high=0.5)
+    reps = [base]
+    for eps in (0.0, 1e-12, -3e-12):
+        s = base.copy()
+        s.positions = s.positions + eps
+        reps.append(s)
+    scene = targets.concatenate(reps)
+    perm = rng.permutation(len(scene))
+    scene = sdgr.Scene(*(getattr(scene, g)[perm] for g in GROUPS))
+    cfg = sdgr.RadarConfig(azimuth_deg=15.0, elevation_deg=45.0, altitude_m=2.0, range_res_m=0.25,
+                           azimuth_res_m=0.25, n_range=48, n_azimuth=48)
+    _oracle_compare(scene, cfg, 3.0, seed=31)
