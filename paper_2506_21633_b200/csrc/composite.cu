@@ -75,7 +75,7 @@ struct WalkArgs {
   double* partial;         // kContrib: (n_pairs); kGrad: (n_pairs, 8)
   int32_t* status;
   sdgr_replay rp;          // kContrib: live-pair log to write (rp.S == nullptr: none)
-  int item_base;           // unused (0)
+  int seg_filter;          // 0: all items, 1: first segment of each tile only, 2: later segments only
 };
 
 // 256-bit in-tile member mask of one Gaussian (bit = local cell (iv&15)*16+(iu&15)).
@@ -310,12 +310,13 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
     const int item = item_s;
     if (item >= n_items) return;
     const int4 it = reinterpret_cast<const int4*>(a.items)[item];
+    if ((a.seg_filter == 1 && item != it.w) || (a.seg_filter == 2 && item == it.w)) continue;
     const int tile = it.x, start = it.y, end = it.z;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     const int iu = tx * kTile + (tid & 15), iv = ty * kTile + (tid >> 4);
     const bool valid = iu < a.n_cols && iv < a.n_rows;
     const int64_t slot_ray = (int64_t)item * kRays + tid;
-    double S = a.seg_base[slot_ray], accd = 0.0, rem = 0.0;
+    double S = a.seg_base ? a.seg_base[slot_ray] : 0.0, accd = 0.0, rem = 0.0;
     if (MODE == kGrad) rem = a.seg_d[slot_ray] + a.seg_g[slot_ray];
     bool alive = valid && S < a.s_stop;
     bool bad = false;
@@ -324,9 +325,14 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
     int cs = start;
     for (; cs < end; cs += kChunk) {
       if (!__syncthreads_or(alive)) break;
-      // ---- P0: stage pair j = tid, build its member mask, scatter bits
+      // ---- P0: stage pair j = tid, member mask restricted to live rays,
+      //      skip the chunk outright when no Gaussian touches a live ray
 #pragma unroll
       for (int w = 0; w < 8; ++w) rows[w * kRays + tid] = 0u;
+      {
+        const uint32_t ab0 = __ballot_sync(0xffffffffu, alive);
+        if (lane == 0) alive_bits[warp] = ab0;
+      }
       const int nG = min(kChunk, end - cs);
       const bool have = tid < nG;
       uint64_t gm[4] = {0, 0, 0, 0};
@@ -341,6 +347,18 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
         pos = r.pos;
       }
       __syncthreads();
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        gm[w] &= ((uint64_t)alive_bits[2 * w] | ((uint64_t)alive_bits[2 * w + 1] << 32));
+      if (!__syncthreads_or(have && (gm[0] | gm[1] | gm[2] | gm[3]))) {
+        if (have && MODE == kContrib) a.partial[pos] = 0.0;
+        if (have && MODE == kGrad) {
+          double4* rec = reinterpret_cast<double4*>(a.partial + (int64_t)pos * 8);
+          rec[0] = make_double4(0, 0, 0, 0);
+          rec[1] = make_double4(0, 0, 0, 0);
+        }
+        continue;
+      }
       {
         const uint32_t bit = 1u << lane;
         uint32_t* col = rows + warp * kRays;
@@ -527,6 +545,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
       }
     }
     if (MODE == kGSum) a.seg_out[slot_ray] = accd;
+    if (MODE == kContrib && a.seg_out) a.seg_out[slot_ray] = S;  // first segment: S after it
     if (record && tid == 0) a.rp.desc_count[item] = min(n_desc, a.rp.desc_per_item);
     if (MODE == kContrib && __syncthreads_or(bad) && tid == 0) atomicOr(a.status + SDGR_STATUS_NONFINITE, 1);
   }
@@ -765,6 +784,10 @@ int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const
   if (rp && cudaMemsetAsync(rp->cursor, 0, 2 * sizeof(unsigned long long), st) != cudaSuccess)
     return SDGR_ERR_CUDA;
   if (t.n_pairs > 0) {
+    // Pass A: per-(segment, ray) optical depth, then the per-ray exclusive
+    // prefix over the tile's segments, then the walk.  (A two-phase variant
+    // -- first segments walked exactly, pass A only on rays still alive --
+    // measured slower: the first phase runs at one CTA per tile.)
     uint32_t* counter = reinterpret_cast<uint32_t*>(t.n_items + 2);
     if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
     static int per_sm = 0;
