@@ -185,34 +185,24 @@ __device__ __forceinline__ void grad_terms(double y1, double y2, double kap, dou
 }
 
 // ============================================================ pass A ==========
-__device__ __forceinline__ void fix_add(uint32_t* lo, uint32_t* hi, double v) {
-  const uint64_t f = __double2ull_rn(fmin(v, kFixMax) * kFix);
-  const uint32_t l = (uint32_t)f;
-  uint32_t h = (uint32_t)(f >> 32);
-  if (l) {
-    const uint32_t old = atomicAdd(lo, l);
-    h += (old + l) < old;  // carry
-  }
-  if (h) atomicAdd(hi, h);
-}
-
+// Per (segment, ray) fixed-point sums of tau, accumulated with fire-and-forget
+// global RED.ADD.U64 (native; integer adds commute, so the sums are exact and
+// deterministic); the segment scan converts them back to FP64.
 __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const int32_t* items,
                                                 const int32_t* n_items_p, uint32_t* counter, int tiles_x,
-                                                double cutoff, double* seg_sum) {
-  __shared__ uint32_t lo[kRays], hi[kRays];
+                                                double cutoff, unsigned long long* seg_fx) {
   __shared__ int item_s;
   const int tid = threadIdx.x;
   const int n_items = *n_items_p;
   while (true) {
     __syncthreads();
     if (tid == 0) item_s = (int)atomicAdd(counter, 1u);
-    lo[tid] = 0u;
-    hi[tid] = 0u;
     __syncthreads();
     const int item = item_s;
     if (item >= n_items) return;
     const int4 it = reinterpret_cast<const int4*>(items)[item];
     const int tx = it.x % tiles_x, ty = it.x / tiles_x;
+    unsigned long long* acc = seg_fx + (int64_t)item * kRays;
     for (int i = it.y + tid; i < it.z; i += kRays) {
       const sdgr_pair_rec r = load_rec(rec + i);
       uint64_t m[4];
@@ -226,12 +216,11 @@ __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const 
           const int c = w * 64 + b;
           const double dx = dsub((double)(tx * kTile + (c & 15)), r.u);
           const double dy = dsub((double)(ty * kTile + (c >> 4)), r.v);
-          fix_add(lo + c, hi + c, r.kappa * exp(-quadform(r.a00, r.a01, r.a11, dx, dy)));
+          const double tau = r.kappa * exp(-quadform(r.a00, r.a01, r.a11, dx, dy));
+          atomicAdd(acc + c, (unsigned long long)__double2ull_rn(fmin(tau, kFixMax) * kFix));
         }
       }
     }
-    __syncthreads();
-    seg_sum[(int64_t)item * kRays + tid] = ((double)hi[tid] * kFix + (double)lo[tid]) * kFixInv;
   }
 }
 
@@ -706,7 +695,7 @@ __global__ void __launch_bounds__(256, 3) k_replay(ReplayArgs a) {
 
 // Per-ray exclusive prefix (forward) or suffix (backward) over a tile's
 // segment items.  One CTA per tile, thread = ray.
-template <bool kSuffix>
+template <bool kSuffix, bool kFixIn = false>
 __global__ void __launch_bounds__(256) k_seg_scan(const int32_t* range, const int32_t* tile_first,
                                                   int seg_len, const double* in, double* out) {
   const int t = blockIdx.x;
@@ -717,7 +706,7 @@ __global__ void __launch_bounds__(256) k_seg_scan(const int32_t* range, const in
   double run = 0.0;
   for (int k = 0; k < nseg; ++k) {
     const int64_t s = (first + (kSuffix ? nseg - 1 - k : k)) * kRays + threadIdx.x;
-    const double v = in[s];
+    const double v = kFixIn ? (double)reinterpret_cast<const unsigned long long*>(in)[s] * kFixInv : in[s];
     out[s] = run;
     run += v;
   }
@@ -789,12 +778,16 @@ int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const
     // -- first segments walked exactly, pass A only on rays still alive --
     // measured slower: the first phase runs at one CTA per tile.)
     uint32_t* counter = reinterpret_cast<uint32_t*>(t.n_items + 2);
+    // seg_sum is reused as u64 fixed-point counters (same 8-byte slots).
+    unsigned long long* seg_fx = reinterpret_cast<unsigned long long*>(seg_sum);
     if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
+    if (cudaMemsetAsync(seg_fx, 0, (size_t)t.max_items * kRays * sizeof(unsigned long long), st) != cudaSuccess)
+      return SDGR_ERR_CUDA;
     static int per_sm = 0;
     if (per_sm == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_segsum, 256, 0);
     k_segsum<<<max(1, min(t.max_items, sm_count() * max(per_sm, 1))), 256, 0, st>>>(
-        t.pair_rec, t.items, t.n_items, counter, t.tiles_x, v.cutoff, seg_sum);
-    k_seg_scan<false><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_sum, seg_base);
+        t.pair_rec, t.items, t.n_items, counter, t.tiles_x, v.cutoff, seg_fx);
+    k_seg_scan<false, true><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_sum, seg_base);
     note_launch(2);
     WalkArgs a = base_args(v, t);
     a.s_stop = s_stop;
