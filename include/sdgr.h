@@ -126,7 +126,8 @@ typedef struct sdgr_replay {
   int32_t pad_;
   int32_t* desc;         /* (max_items*desc_per_item, 4): offset, count, chunk start, j0 | j1 << 16 */
   int32_t* desc_count;   /* (max_items) descriptors written per item        */
-  unsigned long long* cursor; /* (2) device cursor [0] and overflow flag [1]; zeroed by the forward */
+  unsigned long long* cursor; /* (2) device cursor [0], zeroed by the forward, and a
+                                 sticky overflow flag [1] the caller zeroes */
 } sdgr_replay;
 
 /* Packed per-(tile, Gaussian) record, one per sorted pair of the computation

@@ -242,7 +242,7 @@ int radix_sort(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64
   if (cudaMemsetAsync(hist, 0, (size_t)((char*)status - (char*)hist) + status_bytes, st) !=
       cudaSuccess)
     return SDGR_ERR_CUDA;
-  const int hist_blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  const int hist_blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 2);  // fewer global bin REDs
   k_radix_hist<K><<<hist_blocks, 256, 0, st>>>(kin, n, n_dev, begin_bit, npass, hist);
   k_radix_hist_scan<<<npass, 256, 0, st>>>(hist, base);
   note_launch(2);
@@ -606,7 +606,16 @@ __global__ void __launch_bounds__(256) k_key_range(const uint64_t* key, int64_t 
     lo = a < lo ? a : lo;
     hi = b > hi ? b : hi;
   }
-  if ((threadIdx.x & 31) == 0) {
+  // one RED pair per block: same-address atomics serialise at L2
+  __shared__ unsigned long long s_lo[8], s_hi[8];
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { s_lo[warp] = lo; s_hi[warp] = hi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      lo = s_lo[w] < lo ? s_lo[w] : lo;
+      hi = s_hi[w] > hi ? s_hi[w] : hi;
+    }
     atomicMin(range, lo);
     atomicMax(range + 1, hi);
   }
@@ -664,7 +673,7 @@ int launch_depth_order(const sdgr_projection& proj, int32_t* order, void* ws, si
       cudaMemsetAsync(range + 1, 0, sizeof(unsigned long long), st) != cudaSuccess)
     return SDGR_ERR_CUDA;
   const unsigned blocks = (unsigned)((n + 255) / 256);
-  k_key_range<<<std::min<unsigned>(blocks, 148 * 8), 256, 0, st>>>(proj.depth_key, n, range);
+  k_key_range<<<std::min<unsigned>(blocks, 148 * 2), 256, 0, st>>>(proj.depth_key, n, range);
   k_key32<<<blocks, 256, 0, st>>>(proj.depth_key, n, range, k32);
   note_launch(2);
   const int rc = radix_sort<uint32_t>(k32, nullptr, k32s, reinterpret_cast<uint32_t*>(order), n, nullptr, 0,

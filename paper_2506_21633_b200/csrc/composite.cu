@@ -5,7 +5,7 @@
 // fixed-point accumulation (integer adds are associative, so the result does
 // not depend on thread timing):
 //   k_segsum   per depth segment of a tile, the optical depth each ray
-//              accumulates (sum of tau), into shared u32 hi/lo counters;
+//              accumulates (sum of tau), global u64 fixed-point REDs;
 //   k_splat    image[p] = sum_g w I_g, Gaussian-parallel, global u64 REDs.
 // Order-DEpendent passes are tile walks.  A work item is one depth segment
 // (<= seg_len Gaussians) of one 16x16 tile list; a persistent CTA of 256
@@ -188,11 +188,54 @@ __device__ __forceinline__ void grad_terms(double y1, double y2, double kap, dou
 // Per (segment, ray) fixed-point sums of tau, accumulated with fire-and-forget
 // global RED.ADD.U64 (native; integer adds commute, so the sums are exact and
 // deterministic); the segment scan converts them back to FP64.
+//
+// Work is flattened per warp: the 32 lanes' member masks are laid end to end
+// (warp scan of their popcounts) and each round of the loop hands one member
+// (Gaussian, cell) to every lane, so the exp/RED work runs at full SIMT width
+// whatever the per-Gaussian member counts are.
+
+// position of the k-th (0-based) set bit of x; k < popc(x)
+__device__ __forceinline__ int nth_bit64(uint64_t x, int k) {
+  int pos = 0;
+  uint32_t w = (uint32_t)x;
+  int c = __popc(w);
+  if (k >= c) { k -= c; w = (uint32_t)(x >> 32); pos = 32; }
+  c = __popc(w & 0xffffu); if (k >= c) { k -= c; w >>= 16; pos += 16; }
+  c = __popc(w & 0xffu);   if (k >= c) { k -= c; w >>= 8; pos += 8; }
+  c = __popc(w & 0xfu);    if (k >= c) { k -= c; w >>= 4; pos += 4; }
+  c = __popc(w & 0x3u);    if (k >= c) { k -= c; w >>= 2; pos += 2; }
+  if (k >= (int)(w & 1u)) pos += 1;
+  return pos;
+}
+
+// cell of the k-th member of a 256-bit mask held as 4 words in shared memory
+__device__ __forceinline__ int nth_member(const uint64_t* m, int stride, int k) {
+  uint64_t x = m[0];
+  int base = 0, c = __popcll(x);
+  if (k >= c) { k -= c; x = m[stride]; base = 64; c = __popcll(x);
+    if (k >= c) { k -= c; x = m[2 * stride]; base = 128; c = __popcll(x);
+      if (k >= c) { k -= c; x = m[3 * stride]; base = 192; } } }
+  return base + nth_bit64(x, k);
+}
+
+// owner lane of flat member k: the last lane whose exclusive offset is <= k
+__device__ __forceinline__ int flat_owner(int excl, int k) {
+  int o = 0;
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1) {
+    const int e = __shfl_sync(0xffffffffu, excl, o + step);
+    if (e <= k) o += step;
+  }
+  return o;
+}
+
 __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const int32_t* items,
                                                 const int32_t* n_items_p, uint32_t* counter, int tiles_x,
                                                 double cutoff, unsigned long long* seg_fx) {
   __shared__ int item_s;
-  const int tid = threadIdx.x;
+  __shared__ double s_u[kRays], s_v[kRays], s_a0[kRays], s_a1[kRays], s_a2[kRays], s_k[kRays];
+  __shared__ uint64_t s_m[4 * kRays];
+  const int tid = threadIdx.x, lane = tid & 31, wbase = tid & ~31;
   const int n_items = *n_items_p;
   while (true) {
     __syncthreads();
@@ -203,23 +246,40 @@ __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const 
     const int4 it = reinterpret_cast<const int4*>(items)[item];
     const int tx = it.x % tiles_x, ty = it.x / tiles_x;
     unsigned long long* acc = seg_fx + (int64_t)item * kRays;
-    for (int i = it.y + tid; i < it.z; i += kRays) {
-      const sdgr_pair_rec r = load_rec(rec + i);
-      uint64_t m[4];
-      member_mask(r, tx, ty, cutoff, m);
+    for (int i0 = it.y; i0 < it.z; i0 += kRays) {
+      uint64_t m[4] = {0, 0, 0, 0};
+      if (i0 + tid < it.z) {
+        const sdgr_pair_rec r = load_rec(rec + i0 + tid);
+        member_mask(r, tx, ty, cutoff, m);
+        s_u[tid] = r.u; s_v[tid] = r.v;
+        s_a0[tid] = r.a00; s_a1[tid] = r.a01; s_a2[tid] = r.a11; s_k[tid] = r.kappa;
+      }
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        uint64_t bits = m[w];
-        while (bits) {
-          const int b = __ffsll((long long)bits) - 1;
-          bits &= bits - 1;
-          const int c = w * 64 + b;
-          const double dx = dsub((double)(tx * kTile + (c & 15)), r.u);
-          const double dy = dsub((double)(ty * kTile + (c >> 4)), r.v);
-          const double tau = r.kappa * exp(-quadform(r.a00, r.a01, r.a11, dx, dy));
+      for (int w = 0; w < 4; ++w) s_m[w * kRays + tid] = m[w];
+      const int cnt = __popcll(m[0]) + __popcll(m[1]) + __popcll(m[2]) + __popcll(m[3]);
+      int incl = cnt;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+      }
+      const int excl = incl - cnt;
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      __syncwarp();
+      for (int b = 0; b < tot; b += 32) {
+        const int k = b + lane;
+        const int o = flat_owner(excl, k);
+        const int eo = __shfl_sync(0xffffffffu, excl, o);
+        if (k < tot) {
+          const int j = wbase + o;
+          const int c = nth_member(s_m + j, kRays, k - eo);
+          const double dx = dsub((double)(tx * kTile + (c & 15)), s_u[j]);
+          const double dy = dsub((double)(ty * kTile + (c >> 4)), s_v[j]);
+          const double tau = s_k[j] * exp(-quadform(s_a0[j], s_a1[j], s_a2[j], dx, dy));
           atomicAdd(acc + c, (unsigned long long)__double2ull_rn(fmin(tau, kFixMax) * kFix));
         }
       }
+      __syncwarp();
     }
   }
 }
@@ -417,22 +477,35 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
               const int p = ray_off[r] + (int)((wp[r] >> pshift) & 255u) + __popc(rows[jw * kRays + r] & below);
               const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
               const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
-              fw[p] = exp(-quadform(sa0[tid], sa1[tid], sa2[tid], dx, dy));
+              const double wgt = exp(-quadform(sa0[tid], sa1[tid], sa2[tid], dx, dy));
+              fw[p] = wgt;
+              fs[p] = dmul(sk[tid], wgt);  // tau, replaced by S_before in P3
               fj[p] = (uint8_t)tid;
             }
           }
         }
         __syncthreads();
-        // ---- P3: ray-serial log-transmittance prefix (additions only)
+        // ---- P3: ray-serial log-transmittance prefix (additions only); the
+        //      tau loads are issued 4 ahead of the dependent add chain
         if (cnt_r > 0) {
+          const double kInf = __longlong_as_double(0x7ff0000000000000ll);
           const int p1 = roff + cnt_r;
           int p = roff;
-          for (; p < p1; ++p) {
-            if (!(S < a.s_stop)) break;
-            fs[p] = S;
-            S += sk[fj[p]] * fw[p];
+          while (p < p1 && S < a.s_stop) {
+            double t4[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) t4[k] = p + k < p1 ? fs[p + k] : 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (p + k < p1) {
+                const bool live = S < a.s_stop;
+                fs[p + k] = live ? S : kInf;  // dead: T = 0
+                if (live) S = dadd(S, t4[k]);
+              }
+            }
+            p += 4;
           }
-          for (; p < p1; ++p) fs[p] = __longlong_as_double(0x7ff0000000000000ll);  // dead: T = 0
+          for (; p < p1; ++p) fs[p] = kInf;
           alive = S < a.s_stop;
           if (record)
             for (int q = roff; q < p1; ++q) fr[q] = (uint8_t)tid;
@@ -770,7 +843,7 @@ static WalkArgs base_args(const sdgr_view& v, const sdgr_tiles& t) {
 int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const sdgr_tiles& t,
                              double s_stop, double* seg_sum, double* seg_base, double* partial_I,
                              double* intensity, int32_t* status, const sdgr_replay* rp, cudaStream_t st) {
-  if (rp && cudaMemsetAsync(rp->cursor, 0, 2 * sizeof(unsigned long long), st) != cudaSuccess)
+  if (rp && cudaMemsetAsync(rp->cursor, 0, sizeof(unsigned long long), st) != cudaSuccess)  // [1] is sticky
     return SDGR_ERR_CUDA;
   if (t.n_pairs > 0) {
     // Pass A: per-(segment, ray) optical depth, then the per-ray exclusive

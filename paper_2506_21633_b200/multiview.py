@@ -250,6 +250,7 @@ class MultiViewStep:
         self.status.zero_()
         for P in self.planes.values():
             P.t["n_items"].zero_()   # sticky overflow flags: one check per step
+        self.replay.cursor.zero_()
         evs = []
         for i, v in enumerate(self.views):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)] if timing else None

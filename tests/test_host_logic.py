@@ -72,7 +72,7 @@ def test_segment_length_heuristic():
     from paper_2506_21633_b200.rasterizer import _seg_len
 
     assert _seg_len(0) == 256 and _seg_len(1000) == 256
-    assert _seg_len(1_310_000) % 256 == 0 and 1024 <= _seg_len(1_310_000) <= 4096
+    assert _seg_len(1_310_000) % 256 == 0 and 256 <= _seg_len(1_310_000) <= 1024
     assert _seg_len(10**9) == 8192
 
 
