@@ -194,39 +194,23 @@ __device__ __forceinline__ void grad_terms(double y1, double y2, double kap, dou
 // (Gaussian, cell) to every lane, so the exp/RED work runs at full SIMT width
 // whatever the per-Gaussian member counts are.
 
-// position of the k-th (0-based) set bit of x; k < popc(x)
-__device__ __forceinline__ int nth_bit64(uint64_t x, int k) {
-  int pos = 0;
-  uint32_t w = (uint32_t)x;
-  int c = __popc(w);
-  if (k >= c) { k -= c; w = (uint32_t)(x >> 32); pos = 32; }
-  c = __popc(w & 0xffffu); if (k >= c) { k -= c; w >>= 16; pos += 16; }
-  c = __popc(w & 0xffu);   if (k >= c) { k -= c; w >>= 8; pos += 8; }
-  c = __popc(w & 0xfu);    if (k >= c) { k -= c; w >>= 4; pos += 4; }
-  c = __popc(w & 0x3u);    if (k >= c) { k -= c; w >>= 2; pos += 2; }
-  if (k >= (int)(w & 1u)) pos += 1;
-  return pos;
-}
+// Member lists: each lane appends its (lane, cell) entries at its exclusive
+// offset into a per-warp window of kList slots; windows repeat until the
+// warp's total is covered (a lane keeps its not-yet-written bits).
+constexpr int kList = 512;
 
-// cell of the k-th member of a 256-bit mask held as 4 words in shared memory
-__device__ __forceinline__ int nth_member(const uint64_t* m, int stride, int k) {
-  uint64_t x = m[0];
-  int base = 0, c = __popcll(x);
-  if (k >= c) { k -= c; x = m[stride]; base = 64; c = __popcll(x);
-    if (k >= c) { k -= c; x = m[2 * stride]; base = 128; c = __popcll(x);
-      if (k >= c) { k -= c; x = m[3 * stride]; base = 192; } } }
-  return base + nth_bit64(x, k);
-}
-
-// owner lane of flat member k: the last lane whose exclusive offset is <= k
-__device__ __forceinline__ int flat_owner(int excl, int k) {
-  int o = 0;
+__device__ __forceinline__ void fill_window(uint64_t mr[4], int& nx, int lim, int lane, uint16_t* list, int B) {
 #pragma unroll
-  for (int step = 16; step > 0; step >>= 1) {
-    const int e = __shfl_sync(0xffffffffu, excl, o + step);
-    if (e <= k) o += step;
+  for (int w = 0; w < 4; ++w) {
+    uint64_t x = mr[w];
+    while (x && nx < lim) {
+      const int b = __ffsll((long long)x) - 1;
+      x &= x - 1;
+      list[nx - B] = (uint16_t)((lane << 8) | (w * 64 + b));
+      ++nx;
+    }
+    mr[w] = x;
   }
-  return o;
 }
 
 __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const int32_t* items,
@@ -234,8 +218,9 @@ __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const 
                                                 double cutoff, unsigned long long* seg_fx) {
   __shared__ int item_s;
   __shared__ double s_u[kRays], s_v[kRays], s_a0[kRays], s_a1[kRays], s_a2[kRays], s_k[kRays];
-  __shared__ uint64_t s_m[4 * kRays];
+  __shared__ uint16_t s_list[8 * kList];
   const int tid = threadIdx.x, lane = tid & 31, wbase = tid & ~31;
+  uint16_t* list = s_list + (tid >> 5) * kList;
   const int n_items = *n_items_p;
   while (true) {
     __syncthreads();
@@ -254,8 +239,6 @@ __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const 
         s_u[tid] = r.u; s_v[tid] = r.v;
         s_a0[tid] = r.a00; s_a1[tid] = r.a01; s_a2[tid] = r.a11; s_k[tid] = r.kappa;
       }
-#pragma unroll
-      for (int w = 0; w < 4; ++w) s_m[w * kRays + tid] = m[w];
       const int cnt = __popcll(m[0]) + __popcll(m[1]) + __popcll(m[2]) + __popcll(m[3]);
       int incl = cnt;
 #pragma unroll
@@ -263,23 +246,22 @@ __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const 
         const int y = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += y;
       }
-      const int excl = incl - cnt;
+      int nx = incl - cnt;
       const int tot = __shfl_sync(0xffffffffu, incl, 31);
-      __syncwarp();
-      for (int b = 0; b < tot; b += 32) {
-        const int k = b + lane;
-        const int o = flat_owner(excl, k);
-        const int eo = __shfl_sync(0xffffffffu, excl, o);
-        if (k < tot) {
-          const int j = wbase + o;
-          const int c = nth_member(s_m + j, kRays, k - eo);
+      for (int B = 0; B < tot; B += kList) {
+        const int lim = min(tot, B + kList);
+        fill_window(m, nx, lim, lane, list, B);
+        __syncwarp();
+        for (int k = B + lane; k < lim; k += 32) {
+          const int e = list[k - B];
+          const int j = wbase + (e >> 8), c = e & 255;
           const double dx = dsub((double)(tx * kTile + (c & 15)), s_u[j]);
           const double dy = dsub((double)(ty * kTile + (c >> 4)), s_v[j]);
           const double tau = s_k[j] * exp(-quadform(s_a0[j], s_a1[j], s_a2[j], dx, dy));
           atomicAdd(acc + c, (unsigned long long)__double2ull_rn(fmin(tau, kFixMax) * kFix));
         }
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
 }
@@ -459,6 +441,9 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
         int total;
         const int roff = block_scan(cnt_r, scan_tmp, total);
         ray_off[tid] = roff;
+        // replay space for this sub-chunk: the atomic's round trip overlaps P2/P3
+        unsigned long long rp_o = 0;
+        if (record && tid == 0) rp_o = atomicAdd(a.rp.cursor, (unsigned long long)total);
         __syncthreads();
         // ---- P2: Gaussian-parallel weights into the flat slots
         const bool mine = have && tid >= j0 && tid < j1;
@@ -511,7 +496,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
             for (int q = roff; q < p1; ++q) fr[q] = (uint8_t)tid;
         }
         if (record && tid == 0) {
-          const unsigned long long o = atomicAdd(a.rp.cursor, (unsigned long long)total);
+          const unsigned long long o = rp_o;
           const bool fits = o + (unsigned long long)total <= (unsigned long long)a.rp.capacity &&
                             n_desc < a.rp.desc_per_item;
           rp_off = fits ? (long long)o : -1ll;
@@ -769,19 +754,35 @@ __global__ void __launch_bounds__(256, 3) k_replay(ReplayArgs a) {
 // Per-ray exclusive prefix (forward) or suffix (backward) over a tile's
 // segment items.  One CTA per tile, thread = ray.
 template <bool kSuffix, bool kFixIn = false>
-__global__ void __launch_bounds__(256) k_seg_scan(const int32_t* range, const int32_t* tile_first,
-                                                  int seg_len, const double* in, double* out) {
+__global__ void __launch_bounds__(256) k_seg_scan(const int32_t* __restrict__ range,
+                                                  const int32_t* __restrict__ tile_first, int seg_len,
+                                                  const double* __restrict__ in, double* __restrict__ out) {
   const int t = blockIdx.x;
   const int cnt = range[2 * t + 1] - range[2 * t];
   const int nseg = (cnt + seg_len - 1) / seg_len;
   if (nseg == 0) return;
   const int64_t first = tile_first[t];
   double run = 0.0;
-  for (int k = 0; k < nseg; ++k) {
-    const int64_t s = (first + (kSuffix ? nseg - 1 - k : k)) * kRays + threadIdx.x;
-    const double v = kFixIn ? (double)reinterpret_cast<const unsigned long long*>(in)[s] * kFixInv : in[s];
-    out[s] = run;
-    run += v;
+  // loads of 8 segments are issued before the dependent adds
+  for (int k0 = 0; k0 < nseg; k0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + u;
+      v[u] = 0.0;
+      if (k < nseg) {
+        const int64_t s = (first + (kSuffix ? nseg - 1 - k : k)) * kRays + threadIdx.x;
+        v[u] = kFixIn ? (double)reinterpret_cast<const unsigned long long*>(in)[s] * kFixInv : in[s];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + u;
+      if (k < nseg) {
+        out[(first + (kSuffix ? nseg - 1 - k : k)) * kRays + threadIdx.x] = run;
+        run += v[u];
+      }
+    }
   }
 }
 
