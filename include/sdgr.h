@@ -34,6 +34,7 @@ extern "C" {
 #define SDGR_TILE 16          /* tile edge in cells / pixels (16x16 = 256 rays) */
 #define SDGR_TILE_RAYS 256
 #define SDGR_MAX_PLANE 32767  /* plane dims must fit int16 bboxes */
+#define SDGR_MAX_BATCH 8      /* views per sdgr_grad_geometry_batch call */
 
 typedef enum sdgr_status {
   SDGR_OK = 0,
@@ -257,6 +258,17 @@ int sdgr_grad_geometry(const sdgr_scene* scene, const sdgr_view* view,
                        const sdgr_projection* proj, const sdgr_tiles* comp,
                        const double* acc_img, const double* partial_g,
                        sdgr_grads* out, int accumulate, void* stream);
+/* sdgr_grad_geometry over n_views (1..SDGR_MAX_BATCH) views of one scene in
+ * one pass: arrays of length n_views, element k describing view k exactly as
+ * the single-view call does.  The per-view terms are summed in FP64 before
+ * the (linear) covariance chain and the single read-modify-write of `out`,
+ * so a batch equals the sum of its views up to rounding.  Multi-view steps
+ * (optimize.py:395-425 accumulation) use it to pay the scene loads and the
+ * gradient update once per batch. */
+int sdgr_grad_geometry_batch(const sdgr_scene* scene, int n_views, const sdgr_view* views,
+                             const sdgr_projection* projs, const sdgr_tiles* comps,
+                             const double* const* acc_imgs, const double* const* partial_gs,
+                             sdgr_grads* out, int accumulate, void* stream);
 
 #ifdef __cplusplus
 }

@@ -16,6 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libsdgr.so"
 OK, ERR_INVALID, ERR_NUMERICAL, ERR_STATE, ERR_CUDA, ERR_CAPACITY = range(6)
 FLAG_VISIBLE, FLAG_SKIPPED, FLAG_CULLED = 1, 2, 4
 TILE = 16
+MAX_BATCH = 8
 
 _p = C.c_void_p
 
@@ -99,6 +100,9 @@ SIGNATURES = [
                                       C.c_double, _p, _p, _p, _p, _p, C.POINTER(ReplayDesc), _p]),
     ("sdgr_grad_geometry", C.c_int, [C.POINTER(SceneDesc), C.POINTER(View), C.POINTER(ProjectionDesc),
                                      C.POINTER(TilesDesc), _p, _p, C.POINTER(GradsDesc), C.c_int, _p]),
+    ("sdgr_grad_geometry_batch", C.c_int, [C.POINTER(SceneDesc), C.c_int, C.POINTER(View),
+                                           C.POINTER(ProjectionDesc), C.POINTER(TilesDesc), C.POINTER(_p),
+                                           C.POINTER(_p), C.POINTER(GradsDesc), C.c_int, _p]),
 ]
 
 

@@ -125,20 +125,41 @@ __device__ __forceinline__ void inverse_chain(double a, double b, double c, doub
   d[3] = -(p10 * b + p11 * c);
 }
 
+// Per-view inputs of the geometry epilogue.  A launch covers up to
+// SDGR_MAX_BATCH views: every view-independent factor (scene loads, the
+// covariance factorisation, the gradient read-modify-write) is paid once per
+// batch, and the view terms are summed in FP64 registers.  All view terms of
+// the covariance chain are linear in G3 = mc^T dSc mc + mi^T dSi mi, so the
+// chain runs once on the summed G3.
+struct GeoView {
+  double mc[6], mi[6], cam[3];
+  double half_u, half_v, half_az, half_rg;
+  const uint8_t* flags;
+  const double* inv_c;
+  const double* inv_i;
+  const int32_t* n_tiles;
+  const double* phase_raw;
+  const int32_t* pair_start;
+  const double* acc;      // (6, n) imaging-plane sums
+  const double* partial;  // (n_pairs, 8) computation-plane partial records
+};
+struct GeoBatch {
+  int n_views;
+  GeoView v[SDGR_MAX_BATCH];
+};
+
 template <typename T>
-__global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view view,
-                                                       sdgr_projection proj, const int32_t* pair_start,
-                                                       const double* acc_img, const double* partial,
+__global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, const __grid_constant__ GeoBatch B,
                                                        sdgr_grads out, int accumulate) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = sc.n;
   if (g >= n) return;
-  // outputs are written as soon as they are known (no local staging array)
   auto put = [&](float* base, int64_t i, double v) {
     base[i] = accumulate ? base[i] + (float)v : (float)v;
   };
-  const bool vis = proj.flags[g] & SDGR_FLAG_VISIBLE;
-  if (!vis) {
+  int n_vis = 0;
+  for (int k = 0; k < B.n_views; ++k) n_vis += (B.v[k].flags[g] & SDGR_FLAG_VISIBLE) ? 1 : 0;
+  if (n_vis == 0) {
     if (!accumulate) {
       for (int k = 0; k < 3; ++k) out.positions[3 * g + k] = 0.f;
       for (int k = 0; k < 4; ++k) out.rotations[4 * g + k] = 0.f;
@@ -151,16 +172,30 @@ __global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view 
     }
     return;
   }
-  {
+  const double p0 = ldv<T>(sc.positions, 3 * g), p1 = ldv<T>(sc.positions, 3 * g + 1),
+               p2 = ldv<T>(sc.positions, 3 * g + 2);
+  T c[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) c[k] = __ldg(static_cast<const T*>(sc.sh_coeffs) + 16 * g + k);
+  double G3[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double dpos[3] = {0, 0, 0};
+  double dsh[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) dsh[k] = 0.0;
+  double dk = 0.0, uvn = 0.0;
+#pragma unroll 1
+  for (int vi = 0; vi < B.n_views; ++vi) {
+    const GeoView& V = B.v[vi];
+    if (!(V.flags[g] & SDGR_FLAG_VISIBLE)) continue;
     // plane-space gradients
-    const double4 Ac = reinterpret_cast<const double4*>(proj.comp.inv_cov)[g];
-    const double4 Ai = reinterpret_cast<const double4*>(proj.img.inv_cov)[g];
+    const double4 Ac = reinterpret_cast<const double4*>(V.inv_c)[g];
+    const double4 Ai = reinterpret_cast<const double4*>(V.inv_i)[g];
     // computation-plane partials: one record per member tile, fixed order
     double c7[7] = {0, 0, 0, 0, 0, 0, 0};
     {
-      const int s0 = pair_start[g], cnt = proj.comp.n_tiles[g];
+      const int s0 = V.pair_start[g], cnt = V.n_tiles[g];
       for (int k = 0; k < cnt; ++k) {
-        const double4* rec = reinterpret_cast<const double4*>(partial + (int64_t)(s0 + k) * 8);
+        const double4* rec = reinterpret_cast<const double4*>(V.partial + (int64_t)(s0 + k) * 8);
         const double4 r0 = rec[0], r1 = rec[1];
         c7[0] += r0.x; c7[1] += r0.y; c7[2] += r0.z; c7[3] += r0.w;
         c7[4] += r1.x; c7[5] += r1.y; c7[6] += r1.z;
@@ -168,12 +203,12 @@ __global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view 
     }
     double dSc[4], dSi[4];
     inverse_chain(Ac.x, Ac.y, Ac.z, c7[2], c7[3], c7[4], dSc);
-    inverse_chain(Ai.x, Ai.y, Ai.z, acc_img[1 * n + g], acc_img[2 * n + g], acc_img[3 * n + g], dSi);
+    inverse_chain(Ai.x, Ai.y, Ai.z, V.acc[1 * n + g], V.acc[2 * n + g], V.acc[3 * n + g], dSi);
     const double duc[2] = {c7[5], c7[6]};
-    const double dui[2] = {acc_img[4 * n + g], acc_img[5 * n + g]};
-    const double dP = c7[0], dk = c7[1];
-    // G3 = mc^T dSc mc + mi^T dSi mi   (backward.py:191-193)
-    double G3[9];
+    const double dui[2] = {V.acc[4 * n + g], V.acc[5 * n + g]};
+    const double dP = c7[0];
+    dk += c7[1];
+    // G3 += mc^T dSc mc + mi^T dSi mi   (backward.py:191-193)
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -182,93 +217,92 @@ __global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, sdgr_view 
 #pragma unroll
         for (int b = 0; b < 2; ++b)
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
-            s += view.mc[3 * b + a] * dSc[2 * b + c] * view.mc[3 * c + d] +
-                 view.mi[3 * b + a] * dSi[2 * b + c] * view.mi[3 * c + d];
-        G3[3 * a + d] = s;
+          for (int e = 0; e < 2; ++e)
+            s += V.mc[3 * b + a] * dSc[2 * b + e] * V.mc[3 * e + d] +
+                 V.mi[3 * b + a] * dSi[2 * b + e] * V.mi[3 * e + d];
+        G3[3 * a + d] += s;
       }
-    // covariance factor M = R(q) diag(e^s)   (backward.py:195-213)
-    double q[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = ldv<T>(sc.rotations, 4 * g + k);
-    const double nrm = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-    const double w = q[0] / nrm, x = q[1] / nrm, y = q[2] / nrm, z = q[3] / nrm;
-    double Rq[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
-                    2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
-                    2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
-    double s[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) s[j] = exp(ldv<T>(sc.log_scales, 3 * g + j));
-    double M[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) M[3 * i + j] = Rq[3 * i + j] * s[j];
-    double dM[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j)
-        dM[3 * i + j] = 2.0 * (G3[3 * i] * M[j] + G3[3 * i + 1] * M[3 + j] + G3[3 * i + 2] * M[6 + j]);
-    double dls[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) dls[j] = dM[j] * M[j] + dM[3 + j] * M[3 + j] + dM[6 + j] * M[6 + j];
-    double dR[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) dR[3 * i + j] = dM[3 * i + j] * s[j];
-    // dR/dq-hat partials (backward.py:151-168)
-    const double dqw = 2.0 * (-z * dR[1] + y * dR[2] + z * dR[3] - x * dR[5] - y * dR[6] + x * dR[7]);
-    const double dqx = 2.0 * (y * dR[1] + z * dR[2] + y * dR[3] - 2 * x * dR[4] - w * dR[5] + z * dR[6] +
-                              w * dR[7] - 2 * x * dR[8]);
-    const double dqy = 2.0 * (-2 * y * dR[0] + x * dR[1] + w * dR[2] + x * dR[3] + z * dR[5] - w * dR[6] +
-                              z * dR[7] - 2 * y * dR[8]);
-    const double dqz = 2.0 * (-2 * z * dR[0] - w * dR[1] + x * dR[2] + w * dR[3] - 2 * z * dR[4] + y * dR[5] +
-                              x * dR[6] + y * dR[7]);
-    const double dot = dqw * w + dqx * x + dqy * y + dqz * z;
-    put(out.rotations, 4 * g + 0, (dqw - dot * w) / nrm);
-    put(out.rotations, 4 * g + 1, (dqx - dot * x) / nrm);
-    put(out.rotations, 4 * g + 2, (dqy - dot * y) / nrm);
-    put(out.rotations, 4 * g + 3, (dqz - dot * z) / nrm);
-#pragma unroll
-    for (int j = 0; j < 3; ++j) put(out.log_scales, 3 * g + j, dls[j]);
     // position: both affine plane projections + phase look direction
-    double dpos[3];
+    double dp[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      dpos[k] = duc[0] * view.mc[k] + duc[1] * view.mc[3 + k] + dui[0] * view.mi[k] + dui[1] * view.mi[3 + k];
-    const double p0 = ldv<T>(sc.positions, 3 * g), p1 = ldv<T>(sc.positions, 3 * g + 1),
-                 p2 = ldv<T>(sc.positions, 3 * g + 2);
-    const double r0 = p0 - view.cam[0], r1 = p1 - view.cam[1], r2 = p2 - view.cam[2];
+      dp[k] = duc[0] * V.mc[k] + duc[1] * V.mc[3 + k] + dui[0] * V.mi[k] + dui[1] * V.mi[3 + k];
+    const double r0 = p0 - V.cam[0], r1 = p1 - V.cam[1], r2 = p2 - V.cam[2];
     double dist = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
     if (dist == 0.0) dist = 1.0;
     const double d0 = r0 / dist, d1 = r1 / dist, d2 = r2 / dist;
-    double c[16], basis[16], gP[3];
+    if (V.phase_raw[g] > 0.0) {
+      double cd[16], basis[16], gP[3];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) c[k] = ldv<T>(sc.sh_coeffs, 16 * g + k);
-    sh_grad_contract(d0, d1, d2, c, gP, basis);
-    const bool active = proj.phase_raw[g] > 0.0;
-    if (active) {
+      for (int k = 0; k < 16; ++k) cd[k] = (double)c[k];
+      sh_grad_contract(d0, d1, d2, cd, gP, basis);
       const double proj_d = gP[0] * d0 + gP[1] * d1 + gP[2] * d2;
-      dpos[0] += dP * (gP[0] - proj_d * d0) / dist;
-      dpos[1] += dP * (gP[1] - proj_d * d1) / dist;
-      dpos[2] += dP * (gP[2] - proj_d * d2) / dist;
+      dp[0] += dP * (gP[0] - proj_d * d0) / dist;
+      dp[1] += dP * (gP[1] - proj_d * d1) / dist;
+      dp[2] += dP * (gP[2] - proj_d * d2) / dist;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) dsh[k] += dP * basis[k];
     }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) put(out.sh_coeffs, 16 * g + k, active ? dP * basis[k] : 0.0);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) put(out.positions, 3 * g + k, dpos[k]);
-    // softplus' = sigmoid (scene.py:36-39)
-    const double k0 = ldv<T>(sc.ke_raw, 2 * g), k1 = ldv<T>(sc.ke_raw, 2 * g + 1);
-    put(out.ke_raw, 2 * g, dk * 0.5 * (1.0 + tanh(0.5 * k0)));
-    put(out.ke_raw, 2 * g + 1, dk * 0.5 * (1.0 + tanh(0.5 * k1)));
+    for (int k = 0; k < 3; ++k) dpos[k] += dp[k];
     // densification statistic in NDC units (backward.py:285-289)
-    const double gx = duc[0] * (view.n_u / 2.0) + dui[0] * (view.n_az / 2.0);
-    const double gy = duc[1] * (view.n_v / 2.0) + dui[1] * (view.n_rg / 2.0);
-    put(out.uv_grad_norm, g, sqrt(gx * gx + gy * gy));
+    const double gx = duc[0] * V.half_u + dui[0] * V.half_az;
+    const double gy = duc[1] * V.half_v + dui[1] * V.half_rg;
+    uvn += sqrt(gx * gx + gy * gy);
   }
-  out.visible[g] = accumulate ? out.visible[g] + 1 : 1;
+  // covariance factor M = R(q) diag(e^s)   (backward.py:195-213)
+  double q[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) q[k] = ldv<T>(sc.rotations, 4 * g + k);
+  const double nrm = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const double w = q[0] / nrm, x = q[1] / nrm, y = q[2] / nrm, z = q[3] / nrm;
+  const double Rq[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                        2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                        2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+  double s[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) s[j] = exp(ldv<T>(sc.log_scales, 3 * g + j));
+  double M[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) M[3 * i + j] = Rq[3 * i + j] * s[j];
+  double dM[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      dM[3 * i + j] = 2.0 * (G3[3 * i] * M[j] + G3[3 * i + 1] * M[3 + j] + G3[3 * i + 2] * M[6 + j]);
+  double dR[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dR[3 * i + j] = dM[3 * i + j] * s[j];
+  // dR/dq-hat partials (backward.py:151-168)
+  const double dqw = 2.0 * (-z * dR[1] + y * dR[2] + z * dR[3] - x * dR[5] - y * dR[6] + x * dR[7]);
+  const double dqx = 2.0 * (y * dR[1] + z * dR[2] + y * dR[3] - 2 * x * dR[4] - w * dR[5] + z * dR[6] +
+                            w * dR[7] - 2 * x * dR[8]);
+  const double dqy = 2.0 * (-2 * y * dR[0] + x * dR[1] + w * dR[2] + x * dR[3] + z * dR[5] - w * dR[6] +
+                            z * dR[7] - 2 * y * dR[8]);
+  const double dqz = 2.0 * (-2 * z * dR[0] - w * dR[1] + x * dR[2] + w * dR[3] - 2 * z * dR[4] + y * dR[5] +
+                            x * dR[6] + y * dR[7]);
+  const double dot = dqw * w + dqx * x + dqy * y + dqz * z;
+  put(out.rotations, 4 * g + 0, (dqw - dot * w) / nrm);
+  put(out.rotations, 4 * g + 1, (dqx - dot * x) / nrm);
+  put(out.rotations, 4 * g + 2, (dqy - dot * y) / nrm);
+  put(out.rotations, 4 * g + 3, (dqz - dot * z) / nrm);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) put(out.log_scales, 3 * g + j, dM[j] * M[j] + dM[3 + j] * M[3 + j] + dM[6 + j] * M[6 + j]);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) put(out.sh_coeffs, 16 * g + k, dsh[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) put(out.positions, 3 * g + k, dpos[k]);
+  // softplus' = sigmoid (scene.py:36-39)
+  const double k0 = ldv<T>(sc.ke_raw, 2 * g), k1 = ldv<T>(sc.ke_raw, 2 * g + 1);
+  put(out.ke_raw, 2 * g, dk * 0.5 * (1.0 + tanh(0.5 * k0)));
+  put(out.ke_raw, 2 * g + 1, dk * 0.5 * (1.0 + tanh(0.5 * k1)));
+  put(out.uv_grad_norm, g, uvn);
+  out.visible[g] = accumulate ? out.visible[g] + n_vis : n_vis;
 }
 
 int launch_grad_image(const sdgr_view& v, const sdgr_projection& p, const double* intensity,
@@ -278,14 +312,33 @@ int launch_grad_image(const sdgr_view& v, const sdgr_projection& p, const double
   return check_launch();
 }
 
-int launch_grad_geometry(const sdgr_scene& sc, const sdgr_view& v, const sdgr_projection& p,
-                         const sdgr_tiles& comp, const double* acc_img, const double* partial,
-                         const sdgr_grads& out, int accumulate, cudaStream_t st) {
+int launch_grad_geometry(const sdgr_scene& sc, int n_views, const sdgr_view* views,
+                         const sdgr_projection* projs, const sdgr_tiles* comps, const double* const* acc_imgs,
+                         const double* const* partials, const sdgr_grads& out, int accumulate,
+                         cudaStream_t st) {
+  GeoBatch B;
+  B.n_views = n_views;
+  for (int k = 0; k < n_views; ++k) {
+    const sdgr_view& v = views[k];
+    GeoView& G = B.v[k];
+    for (int i = 0; i < 6; ++i) { G.mc[i] = v.mc[i]; G.mi[i] = v.mi[i]; }
+    for (int i = 0; i < 3; ++i) G.cam[i] = v.cam[i];
+    G.half_u = v.n_u / 2.0; G.half_v = v.n_v / 2.0;
+    G.half_az = v.n_az / 2.0; G.half_rg = v.n_rg / 2.0;
+    G.flags = projs[k].flags;
+    G.inv_c = projs[k].comp.inv_cov;
+    G.inv_i = projs[k].img.inv_cov;
+    G.n_tiles = projs[k].comp.n_tiles;
+    G.phase_raw = projs[k].phase_raw;
+    G.pair_start = comps[k].pair_start;
+    G.acc = acc_imgs[k];
+    G.partial = partials[k];
+  }
   const unsigned blocks = (unsigned)((sc.n + 127) / 128);
   if (sc.dtype == 0)
-    k_grad_geometry<float><<<blocks, 128, 0, st>>>(sc, v, p, comp.pair_start, acc_img, partial, out, accumulate);
+    k_grad_geometry<float><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
   else
-    k_grad_geometry<double><<<blocks, 128, 0, st>>>(sc, v, p, comp.pair_start, acc_img, partial, out, accumulate);
+    k_grad_geometry<double><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
   note_launch();
   return check_launch();
 }

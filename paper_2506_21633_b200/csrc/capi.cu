@@ -34,8 +34,8 @@ static bool replay_ok(const sdgr_replay* r) {
   return !r || (r->S && r->w && r->j && r->r && r->desc && r->desc_count && r->cursor && r->capacity > 0 &&
                 r->desc_per_item > 0);
 }
-int launch_grad_geometry(const sdgr_scene&, const sdgr_view&, const sdgr_projection&, const sdgr_tiles&,
-                         const double*, const double*, const sdgr_grads&, int, cudaStream_t);
+int launch_grad_geometry(const sdgr_scene&, int, const sdgr_view*, const sdgr_projection*, const sdgr_tiles*,
+                         const double* const*, const double* const*, const sdgr_grads&, int, cudaStream_t);
 
 static bool view_ok(const sdgr_view* v) {
   if (!v) return false;
@@ -153,12 +153,23 @@ int sdgr_grad_intensity(const sdgr_view* view, const sdgr_projection* proj, cons
 int sdgr_grad_geometry(const sdgr_scene* scene, const sdgr_view* view, const sdgr_projection* proj,
                        const sdgr_tiles* comp, const double* acc_img, const double* partial_g,
                        sdgr_grads* out, int accumulate, void* stream) {
-  if (!scene || !view_ok(view) || !proj || !comp || comp->plane != 0 || !comp->pair_start || !acc_img ||
-      !out)
+  return sdgr_grad_geometry_batch(scene, 1, view, proj, comp, &acc_img, &partial_g, out, accumulate, stream);
+}
+
+int sdgr_grad_geometry_batch(const sdgr_scene* scene, int n_views, const sdgr_view* views,
+                             const sdgr_projection* projs, const sdgr_tiles* comps,
+                             const double* const* acc_imgs, const double* const* partial_gs,
+                             sdgr_grads* out, int accumulate, void* stream) {
+  if (!scene || n_views < 1 || n_views > SDGR_MAX_BATCH || !views || !projs || !comps || !acc_imgs ||
+      !partial_gs || !out)
     return SDGR_ERR_INVALID;
-  if (comp->n_pairs > 0 && !partial_g) return SDGR_ERR_INVALID;
-  if (scene->n != proj->n) return SDGR_ERR_STATE;
-  return launch_grad_geometry(*scene, *view, *proj, *comp, acc_img, partial_g, *out, accumulate,
+  for (int k = 0; k < n_views; ++k) {
+    const sdgr_tiles* c = comps + k;
+    if (!view_ok(views + k) || c->plane != 0 || !c->pair_start || !acc_imgs[k]) return SDGR_ERR_INVALID;
+    if (c->n_pairs > 0 && !partial_gs[k]) return SDGR_ERR_INVALID;
+    if (scene->n != projs[k].n) return SDGR_ERR_STATE;
+  }
+  return launch_grad_geometry(*scene, n_views, views, projs, comps, acc_imgs, partial_gs, *out, accumulate,
                               static_cast<cudaStream_t>(stream));
 }
 

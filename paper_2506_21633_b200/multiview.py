@@ -71,7 +71,7 @@ class MultiViewStep:
 
     def __init__(self, scene: DeviceScene, configs, cov_reg: float = DEFAULT_COV_REG,
                  cutoff: float = DEFAULT_CUTOFF, s_stop: float = S_STOP, headroom: float = 1.3,
-                 group=None):
+                 group=None, geo_batch: int = _lib.MAX_BATCH):
         self.scene = scene
         self.configs = list(configs)
         self.views = [view_constants(c, cov_reg, cutoff) for c in self.configs]
@@ -87,36 +87,20 @@ class MultiViewStep:
         if len(shapes) != 1:
             raise ValueError("all views of a step must share the image size")
         self.img_shape = shapes.pop()
-        # per-view (reused) projection records
-        self.rec = {}
-        for name in ("comp", "img"):
-            self.rec[name] = dict(uv=_empty((n, 2), torch.float64, dev), inv_cov=_empty((n, 4), torch.float64, dev),
-                                  bbox=_empty((n, 4), torch.int16, dev), cell_mask=_empty((n,), torch.int64, dev),
-                                  tile_mask=_empty((n,), torch.int64, dev), n_tiles=_empty((n,), torch.int32, dev))
-        self.depth_key = _empty((n,), torch.int64, dev)
-        self.kappa = _empty((n,), torch.float64, dev)
-        self.phase = _empty((n,), torch.float64, dev)
-        self.phase_raw = _empty((n,), torch.float64, dev)
-        self.flags = _empty((n,), torch.uint8, dev)
+        # geometry epilogue batches: `geo_batch` views' projections, partial
+        # records and imaging-plane sums stay resident until one batched
+        # sdgr_grad_geometry_batch call consumes them
+        self.geo_batch = max(1, min(int(geo_batch), _lib.MAX_BATCH, len(self.views)))
         self.counters = torch.zeros((4,), dtype=torch.int32, device=dev)
-        self.pd = _lib.ProjectionDesc()
-        self.pd.n = n
-        for name in ("comp", "img"):
-            pl = _lib.Plane()
-            r = self.rec[name]
-            pl.uv, pl.inv_cov, pl.cov, pl.bbox = ptr(r["uv"]), ptr(r["inv_cov"]), None, ptr(r["bbox"])
-            pl.cell_mask, pl.tile_mask, pl.n_tiles = ptr(r["cell_mask"]), ptr(r["tile_mask"]), ptr(r["n_tiles"])
-            setattr(self.pd, name, pl)
-        self.pd.depth_key, self.pd.kappa, self.pd.phase = ptr(self.depth_key), ptr(self.kappa), ptr(self.phase)
-        self.pd.phase_raw, self.pd.flags, self.pd.counters = ptr(self.phase_raw), ptr(self.flags), ptr(self.counters)
-        self.pd.ke_act = None
-        self.pd.look = None
         self.member_pairs = torch.zeros((2,), dtype=torch.int64, device=dev)
-        self.pd.member_pairs = ptr(self.member_pairs)
+        self.proj_bufs = [self._projection_bufs() for _ in range(self.geo_batch)]
+        self.pds = [pd for pd, _ in self.proj_bufs]
+        self.pd = self.pds[0]
         self.order = _empty((n,), torch.int32, dev)
         self.intensity = _empty((n,), torch.float64, dev)
         self.image = _empty(self.img_shape, torch.float64, dev)
-        self.acc_img = _empty((6, n), torch.float64, dev)
+        self.acc_imgs = [_empty((6, n), torch.float64, dev) for _ in range(self.geo_batch)]
+        self.acc_img = self.acc_imgs[0]
         self.status = torch.zeros((4,), dtype=torch.int32, device=dev)
         # gradients: one flat float32 buffer so the all-reduce is one call
         self.grads = self._grad_views()
@@ -126,6 +110,30 @@ class MultiViewStep:
         self.stage_events = None
 
     # -- buffers ------------------------------------------------------------
+    def _projection_bufs(self):
+        """One set of per-view projection records (K1 outputs) + its descriptor."""
+        n, dev = self.n, self.dev
+        rec = {}
+        pd = _lib.ProjectionDesc()
+        pd.n = n
+        for name in ("comp", "img"):
+            r = dict(uv=_empty((n, 2), torch.float64, dev), inv_cov=_empty((n, 4), torch.float64, dev),
+                     bbox=_empty((n, 4), torch.int16, dev), cell_mask=_empty((n,), torch.int64, dev),
+                     tile_mask=_empty((n,), torch.int64, dev), n_tiles=_empty((n,), torch.int32, dev))
+            rec[name] = r
+            pl = _lib.Plane()
+            pl.uv, pl.inv_cov, pl.cov, pl.bbox = ptr(r["uv"]), ptr(r["inv_cov"]), None, ptr(r["bbox"])
+            pl.cell_mask, pl.tile_mask, pl.n_tiles = ptr(r["cell_mask"]), ptr(r["tile_mask"]), ptr(r["n_tiles"])
+            setattr(pd, name, pl)
+        for k, dt in (("depth_key", torch.int64), ("kappa", torch.float64), ("phase", torch.float64),
+                      ("phase_raw", torch.float64), ("flags", torch.uint8)):
+            rec[k] = _empty((n,), dt, dev)
+            setattr(pd, k, ptr(rec[k]))
+        pd.counters, pd.member_pairs = ptr(self.counters), ptr(self.member_pairs)
+        pd.ke_act = None
+        pd.look = None
+        return pd, rec
+
     def _grad_views(self) -> SceneGradients:
         # SoA views into one flat buffer keep each group contiguous and make
         # the all-reduce one call
@@ -156,7 +164,6 @@ class MultiViewStep:
                 seg_b=_empty((max_items * 256,), torch.float64, dev),
                 seg_c=_empty((max_items * 256,), torch.float64, dev),
                 partial_I=_empty((cap,), torch.float64, dev),
-                partial_g=_empty((cap, 8), torch.float64, dev),
                 pair_rec=_empty((cap, _lib.PAIR_REC_BYTES), torch.uint8, dev),
             )
             d = _lib.TilesDesc()
@@ -167,6 +174,16 @@ class MultiViewStep:
                 setattr(d, k, ptr(t[k]))
             d.seg_len, d.max_items, d.device_count = seg, max_items, 1
             self.planes[pl] = _PlaneBufs(offsets=_empty((n + 1,), torch.int32, dev), tiles=d, t=t)
+        # per batch slot: pair_start (TilesDesc copy) and the partial records
+        d0, t0 = self.planes[0].tiles, self.planes[0].t
+        self.slot_pair_start = [t0["pair_start"]] + [_empty((n,), torch.int32, dev)
+                                                     for _ in range(self.geo_batch - 1)]
+        self.slot_partial = [_empty((d0.n_pairs, 8), torch.float64, dev) for _ in range(self.geo_batch)]
+        self.slot_tiles = []
+        for k in range(self.geo_batch):
+            dk = _lib.TilesDesc.from_buffer_copy(d0)
+            dk.pair_start = ptr(self.slot_pair_start[k])
+            self.slot_tiles.append(dk)
         self.splat_scratch = _empty((v.n_rg * v.n_az,), torch.int64, dev)
         # live-pair log: member pairs bound every view's live pairs
         d0 = self.planes[0].tiles
@@ -200,10 +217,14 @@ class MultiViewStep:
         return mx
 
     # -- one view -----------------------------------------------------------
-    def _view(self, v, dlds: torch.Tensor, ev=None):
-        lib, st, pd = self.lib, _stream(), C.byref(self.pd)
+    def _view(self, v, dlds: torch.Tensor, slot: int, ev=None):
+        """K1-K9 of one view into batch slot `slot` (the geometry epilogue runs per batch)."""
+        lib, st = self.lib, _stream()
+        pd = C.byref(self.pds[slot])
         P0 = self.planes[0]
         t0 = P0.t
+        tiles = C.byref(self.slot_tiles[slot])
+        acc = self.acc_imgs[slot]
 
         def mark(i):
             if ev is not None:
@@ -215,10 +236,10 @@ class MultiViewStep:
         mark(2)
         _check(lib.sdgr_count_pairs(pd, 0, ptr(self.order), ptr(P0.offsets), ptr(self.ws), self.ws_bytes, st),
                "sdgr_count_pairs")
-        _check(lib.sdgr_bin_pairs(pd, C.byref(v), ptr(self.order), ptr(P0.offsets), C.byref(P0.tiles),
+        _check(lib.sdgr_bin_pairs(pd, C.byref(v), ptr(self.order), ptr(P0.offsets), tiles,
                                   ptr(self.ws), self.ws_bytes, st), "sdgr_bin_pairs")
         mark(3)
-        _check(lib.sdgr_composite_forward(C.byref(v), pd, C.byref(P0.tiles), self.s_stop, ptr(t0["seg_a"]),
+        _check(lib.sdgr_composite_forward(C.byref(v), pd, tiles, self.s_stop, ptr(t0["seg_a"]),
                                           ptr(t0["seg_b"]), ptr(t0["partial_I"]), ptr(self.intensity),
                                           ptr(self.status), C.byref(self.replay.desc_c), st),
                "sdgr_composite_forward")
@@ -226,18 +247,31 @@ class MultiViewStep:
         _check(lib.sdgr_splat(C.byref(v), pd, ptr(self.intensity), ptr(self.splat_scratch), ptr(self.image), st),
                "sdgr_splat")
         mark(5)
-        _check(lib.sdgr_grad_image(C.byref(v), pd, ptr(self.intensity), ptr(dlds), ptr(self.acc_img), st),
+        _check(lib.sdgr_grad_image(C.byref(v), pd, ptr(self.intensity), ptr(dlds), ptr(acc), st),
                "sdgr_grad_image")
         mark(6)
         # seg_b holds the forward's exclusive prefixes; seg_a is reused as scratch
-        _check(lib.sdgr_grad_intensity(C.byref(v), pd, C.byref(P0.tiles), self.s_stop, ptr(t0["seg_b"]),
-                                       ptr(self.acc_img[0]), ptr(t0["seg_a"]), ptr(t0["seg_c"]),
-                                       ptr(t0["partial_g"]), C.byref(self.replay.desc_c), st),
+        _check(lib.sdgr_grad_intensity(C.byref(v), pd, tiles, self.s_stop, ptr(t0["seg_b"]),
+                                       ptr(acc[0]), ptr(t0["seg_a"]), ptr(t0["seg_c"]),
+                                       ptr(self.slot_partial[slot]), C.byref(self.replay.desc_c), st),
                "sdgr_grad_intensity")
         mark(7)
-        _check(lib.sdgr_grad_geometry(C.byref(self.sd), C.byref(v), pd, C.byref(P0.tiles), ptr(self.acc_img),
-                                      ptr(t0["partial_g"]), C.byref(self.gd), 1, st), "sdgr_grad_geometry")
-        mark(8)
+
+    def _geometry(self, views, ev=None):
+        """Batched K10 over the views held in slots 0..len(views)-1."""
+        k = len(views)
+        Views = _lib.View * k
+        Projs = _lib.ProjectionDesc * k
+        Tiles = _lib.TilesDesc * k
+        Ptrs = C.c_void_p * k
+        if ev is not None:
+            ev[0].record()
+        _check(self.lib.sdgr_grad_geometry_batch(
+            C.byref(self.sd), k, Views(*views), Projs(*self.pds[:k]), Tiles(*self.slot_tiles[:k]),
+            Ptrs(*[ptr(a) for a in self.acc_imgs[:k]]), Ptrs(*[ptr(p) for p in self.slot_partial[:k]]),
+            C.byref(self.gd), 1, _stream()), "sdgr_grad_geometry_batch")
+        if ev is not None:
+            ev[1].record()
 
     def run(self, dlds: torch.Tensor, timing: bool = False, check: bool = True):
         """Forward + backward of every view; dlds: (V, H, W) float64 on device.
@@ -251,13 +285,20 @@ class MultiViewStep:
         for P in self.planes.values():
             P.t["n_items"].zero_()   # sticky overflow flags: one check per step
         self.replay.cursor.zero_()
-        evs = []
-        for i, v in enumerate(self.views):
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)] if timing else None
-            self._view(v, dlds[i], ev)
+        evs, gevs = [], []
+        B = self.geo_batch
+        for b0 in range(0, len(self.views), B):
+            batch = self.views[b0:b0 + B]
+            for k, v in enumerate(batch):
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)] if timing else None
+                self._view(v, dlds[b0 + k], k, ev)
+                if timing:
+                    evs.append(ev)
+            gev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timing else None
+            self._geometry(batch, gev)
             if timing:
-                evs.append(ev)
-        self.stage_events = evs
+                gevs.append(gev)
+        self.stage_events = (evs, gevs)
         if self.group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
             self.allreduce()
         if check:
@@ -278,11 +319,15 @@ class MultiViewStep:
             raise NumericalError("non-finite intensity in a multi-view step")
 
     def stage_times_ms(self):
-        """Per-stage device time summed over the last timed run's views."""
+        """Per-stage device time summed over the last timed run's views
+        (grad_geometry: summed over its batched launches)."""
         names = ("project", "depth_sort", "binning", "forward_comp", "splat", "grad_image",
-                 "grad_intensity", "grad_geometry")
-        out = dict.fromkeys(names, 0.0)
-        for ev in self.stage_events or []:
+                 "grad_intensity")
+        out = dict.fromkeys(names + ("grad_geometry",), 0.0)
+        evs, gevs = self.stage_events or ([], [])
+        for ev in evs:
             for i, nm in enumerate(names):
                 out[nm] += ev[i].elapsed_time(ev[i + 1])
+        for ev in gevs:
+            out["grad_geometry"] += ev[0].elapsed_time(ev[1])
         return out

@@ -26,7 +26,7 @@ dl = torch.randn((a.views, 512, 512), device="cuda", dtype=torch.float64)
 step.run(dl)
 rows = []
 for i, v in enumerate(step.views):
-    step._view(v, dl[i])
+    step._view(v, dl[i], 0)
     torch.cuda.synchronize()
     t = step.planes[0].t
     rows.append((int(step.planes[0].offsets[step.n].item()), int(step.member_pairs[0].item()),

@@ -223,14 +223,17 @@ def test_bitwise_determinism():
         assert np.array_equal(getattr(outs[0][1], k), getattr(outs[1][1], k)), k
 
 
-def test_multiview_step_equals_sum_of_views():
+@pytest.mark.parametrize("geo_batch", [1, 2, 8])
+def test_multiview_step_equals_sum_of_views(geo_batch):
+    """Batched geometry epilogue (1, partial and full batches) == the sum of
+    single-view backward passes."""
     from paper_2506_21633_b200.multiview import MultiViewStep
 
     tank = targets.to_float32_exact(targets.composite_target(targets.tank_preset(), [3000, 1500, 500], seed=6))
     cfgs = [sdgr.RadarConfig(azimuth_deg=az, elevation_deg=el, altitude_m=0.5, n_range=96, n_azimuth=96)
             for az, el in ((0.0, 30.0), (90.0, 45.0), (200.0, 60.0))]
     ds = sdgr.DeviceScene.from_host(tank, dtype=torch.float32)
-    step = MultiViewStep(ds, cfgs)
+    step = MultiViewStep(ds, cfgs, geo_batch=geo_batch)
     dl = torch.randn((3, 96, 96), dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(3))
     got = step.run(dl)
     ref = {k: 0.0 for k in GROUPS + ("uv_grad_norm",)}
