@@ -268,39 +268,75 @@ __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const 
 
 // ============================================================ splat ===========
 // One thread per Gaussian; its member pixels (imaging-plane cell window K1
-// stored) receive w * I_g through global u64 fixed-point REDs.
+// stored) receive w * I_g through global u64 fixed-point REDs.  Small
+// footprints (<= 8x8 window) are flattened per warp through a member list
+// (as in pass A) so the exp/RED work runs at full SIMT width; larger
+// footprints are walked by their own thread.
+__device__ __forceinline__ void splat_add(unsigned long long* acc, int n_az, int iu, int iv, double q, double I) {
+  const double v = exp(-q) * I;
+  atomicAdd(acc + (int64_t)iv * n_az + iu, (unsigned long long)__double2ull_rn(fmin(v, kFixMax) * kFix));
+}
+
 __global__ void __launch_bounds__(256) k_splat(sdgr_view view, sdgr_plane pl, const uint8_t* flags,
                                                const double* intensity, int64_t n,
                                                unsigned long long* acc) {
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n || !(flags[g] & SDGR_FLAG_VISIBLE)) return;
-  const double I = intensity[g];
-  if (I == 0.0) return;
-  const double2 uv = reinterpret_cast<const double2*>(pl.uv)[g];
-  const double4 A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
-  const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
-  if (bb.x > bb.y || bb.z > bb.w) return;
-  auto add = [&](int iu, int iv, double q) {
-    const double v = exp(-q) * I;
-    atomicAdd(acc + (int64_t)iv * view.n_az + iu, (unsigned long long)__double2ull_rn(fmin(v, kFixMax) * kFix));
-  };
-  if ((bb.y - bb.x) < 8 && (bb.w - bb.z) < 8) {
-    uint64_t cm = pl.cell_mask[g];
-    while (cm) {
-      const int b = __ffsll((long long)cm) - 1;
-      cm &= cm - 1;
-      const int iu = bb.x + (b & 7), iv = bb.z + (b >> 3);
-      add(iu, iv, quadform(A.x, A.y, A.z, dsub((double)iu, uv.x), dsub((double)iv, uv.y)));
+  __shared__ double s_u[256], s_v[256], s_a0[256], s_a1[256], s_a2[256], s_I[256];
+  __shared__ int32_t s_x[256], s_y[256];
+  __shared__ uint16_t s_list[8 * kList];
+  const int tid = threadIdx.x, lane = tid & 31, wbase = tid & ~31;
+  uint16_t* list = s_list + (tid >> 5) * kList;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + tid;
+  uint64_t m[4] = {0, 0, 0, 0};
+  bool large = false;
+  double2 uv = make_double2(0, 0);
+  double4 A = make_double4(0, 0, 0, 0);
+  short4 bb = make_short4(0, -1, 0, -1);
+  double I = 0.0;
+  if (g < n && (flags[g] & SDGR_FLAG_VISIBLE)) {
+    I = intensity[g];
+    if (I != 0.0) {
+      uv = reinterpret_cast<const double2*>(pl.uv)[g];
+      A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
+      bb = reinterpret_cast<const short4*>(pl.bbox)[g];
+      if (bb.x <= bb.y && bb.z <= bb.w) {
+        if ((bb.y - bb.x) < 8 && (bb.w - bb.z) < 8) m[0] = pl.cell_mask[g];
+        else large = true;
+      }
     }
-    return;
   }
-  const bool dense = !isfinite(view.cutoff);
-  const double cut2 = dmul(view.cutoff, view.cutoff);
-  for (int iv = bb.z; iv <= bb.w; ++iv)
-    for (int iu = bb.x; iu <= bb.y; ++iu) {
-      const double q = quadform(A.x, A.y, A.z, dsub((double)iu, uv.x), dsub((double)iv, uv.y));
-      if (dense || q <= cut2) add(iu, iv, q);
+  s_u[tid] = uv.x; s_v[tid] = uv.y; s_a0[tid] = A.x; s_a1[tid] = A.y; s_a2[tid] = A.z; s_I[tid] = I;
+  s_x[tid] = bb.x; s_y[tid] = bb.z;
+  const int cnt = __popcll(m[0]);
+  int incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  int nx = incl - cnt;
+  const int tot = __shfl_sync(0xffffffffu, incl, 31);
+  for (int B = 0; B < tot; B += kList) {
+    const int lim = min(tot, B + kList);
+    fill_window(m, nx, lim, lane, list, B);
+    __syncwarp();
+    for (int k = B + lane; k < lim; k += 32) {
+      const int e = list[k - B];
+      const int j = wbase + (e >> 8), b = e & 63;
+      const int iu = s_x[j] + (b & 7), iv = s_y[j] + (b >> 3);
+      splat_add(acc, view.n_az, iu, iv,
+                quadform(s_a0[j], s_a1[j], s_a2[j], dsub((double)iu, s_u[j]), dsub((double)iv, s_v[j])), s_I[j]);
     }
+    __syncwarp();
+  }
+  if (large) {
+    const bool dense = !isfinite(view.cutoff);
+    const double cut2 = dmul(view.cutoff, view.cutoff);
+    for (int iv = bb.z; iv <= bb.w; ++iv)
+      for (int iu = bb.x; iu <= bb.y; ++iu) {
+        const double q = quadform(A.x, A.y, A.z, dsub((double)iu, uv.x), dsub((double)iv, uv.y));
+        if (dense || q <= cut2) splat_add(acc, view.n_az, iu, iv, q, I);
+      }
+  }
 }
 
 __global__ void __launch_bounds__(256) k_splat_finish(const unsigned long long* acc, int64_t n, double* image) {
