@@ -653,32 +653,96 @@ struct ReplayArgs {
   const double* seg_g;    // kGrad
   const double* seg_d;    // kGrad
   double* seg_out;        // kGSum
-  double* partial;        // kGrad: (n_pairs, 8), zeroed beforehand
+  double* partial;        // kGrad: (n_pairs, 8), every record written
 };
+
+// Segmented inclusive scan across the block: thread t holds cnt <= 8
+// consecutive log entries (thread t's before thread t+1's), hd[e] marks the first entry of a run.  On return v[e]
+// is the sum of its run up to and including e.  Fixed association order
+// (thread-serial, then warp shuffles, then warps in order): deterministic.
+// One __syncthreads inside; consecutive calls need a barrier between them.
+__device__ __forceinline__ void block_seg_scan8(double (&v)[8], const bool (&hd)[8], int cnt, double* s_agg,
+                                                int* s_flag) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double run = 0.0;
+  int any = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (e < cnt) {
+      if (hd[e]) { run = v[e]; any = 1; } else { run += v[e]; }
+      v[e] = run;
+    }
+  }
+  double a = run;
+  int f = any;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double ao = __shfl_up_sync(0xffffffffu, a, off);
+    const int fo = __shfl_up_sync(0xffffffffu, f, off);
+    if (lane >= off) {
+      if (!f) a = ao + a;
+      f |= fo;
+    }
+  }
+  double ex = __shfl_up_sync(0xffffffffu, a, 1);
+  int exf = __shfl_up_sync(0xffffffffu, f, 1);
+  if (lane == 0) { ex = 0.0; exf = 0; }
+  if (lane == 31) { s_agg[warp] = a; s_flag[warp] = f; }
+  __syncthreads();
+  double wc = 0.0;
+  for (int w = 0; w < warp; ++w) wc = s_flag[w] ? s_agg[w] : wc + s_agg[w];
+  const double carry = exf ? ex : wc + ex;
+  bool open = true;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (e < cnt && open) {
+      if (hd[e]) open = false;
+      else v[e] += carry;
+    }
+  }
+}
 
 template <int MODE>
 struct ReplayCfg {
-  static constexpr size_t kSmem = kReplayCap * (MODE == kGrad ? 4 * 8 + 2 : 3 * 8 + 2);
+  // fS, fW (+ fD) doubles, fj, fr bytes (+ perm u16)
+  static constexpr size_t kSmem = kReplayCap * (MODE == kGrad ? 3 * 8 + 2 + 2 : 2 * 8 + 2);
 };
 
+// Per descriptor (<= kReplayCap log entries of Gaussians [j0, j1) of one chunk):
+//   L  stage the Gaussians and the entries;
+//   B  entry-parallel g*contrib (ceil(n/256) contiguous entries per thread), a block
+//      segmented scan over the ray runs: per-ray sums (kGSum) or the downstream
+//      sum D after each pair (kGrad) -- no ray-serial loops;
+//   C  kGrad: counting sort of the entries into Gaussian-major order (ray
+//      bitmaps per Gaussian), then per warp (32 Gaussians) the gradient terms
+//      of up to 8 contiguous entries per lane, reduced per Gaussian with a warp
+//      segmented scan of the 7-term vectors: one partial record per
+//      (tile, Gaussian) pair, written once.  Pairs of the item no descriptor
+//      covers get zero records here, so partial_g needs no memset.
 template <int MODE>
-__global__ void __launch_bounds__(256, 3) k_replay(ReplayArgs a) {
+__global__ void __launch_bounds__(256, MODE == kGrad ? 2 : 4) k_replay(ReplayArgs a) {
   constexpr bool kG = MODE == kGrad;
-  __shared__ int32_t run_s[kRays], run_e[kRays];
+  constexpr int kCap = kReplayCap;
   __shared__ double sk[kChunk], sp[kChunk], sg[kChunk];
   __shared__ double su[kG ? kChunk : 1], sv[kG ? kChunk : 1], sa0[kG ? kChunk : 1], sa1[kG ? kChunk : 1],
       sa2[kG ? kChunk : 1];
-  __shared__ uint32_t rows[kG ? 8 * kRays : 1];   // rows[w*256 + r]: Gaussians of ray r
-  __shared__ uint32_t jm[kG ? 8 * kChunk : 1];    // jm[w*256 + j]: rays of Gaussian j
+  __shared__ int32_t spos[kG ? kChunk : 1];
+  __shared__ double ray_acc[kRays];                 // kGSum: per-ray sum; kGrad: remaining sum per ray
+  __shared__ uint32_t jm[kG ? 8 * kChunk : 1];      // jm[w*256 + j]: rays of Gaussian j (bit r&31 of word r>>5)
+  __shared__ uint32_t jpre[kG ? 2 * kChunk : 1];    // per Gaussian: byte prefix counts of its jm words
+  __shared__ int32_t gstart[kG ? kChunk + 1 : 1];
+  __shared__ double s_agg[8];
+  __shared__ int s_flag[8];
+  __shared__ int32_t scan_tmp[8];
   __shared__ int item_s;
   extern __shared__ double dyn[];
-  double* fS = dyn;                 // S_before, then (kGrad) g*T*a*P
-  double* fW = fS + kReplayCap;     // w
-  double* fG = fW + kReplayCap;     // g*contrib, then (kGrad) downstream sum D
-  double* fY = fG + kReplayCap;     // kGrad: T*(1-a)
-  uint8_t* fj = reinterpret_cast<uint8_t*>(fG + (kG ? 2 : 1) * kReplayCap);
-  uint8_t* fr = fj + kReplayCap;
-  const int tid = threadIdx.x, lane = tid & 31;
+  double* fS = dyn;                                  // S_before
+  double* fW = fS + kCap;                            // w
+  double* fD = fW + kCap;                            // kGrad: downstream sum after the pair
+  uint16_t* perm = reinterpret_cast<uint16_t*>(fD + (kG ? kCap : 0));  // kGrad: Gaussian-major -> log
+  uint8_t* fj = reinterpret_cast<uint8_t*>(perm + (kG ? kCap : 0));
+  uint8_t* fr = fj + kCap;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_items = *a.n_items;
   while (true) {
     __syncthreads();
@@ -686,19 +750,28 @@ __global__ void __launch_bounds__(256, 3) k_replay(ReplayArgs a) {
     __syncthreads();
     const int item = item_s;
     if (item >= n_items) return;
-    const int tile = reinterpret_cast<const int4*>(a.items)[item].x;
-    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int4 it = reinterpret_cast<const int4*>(a.items)[item];
+    const int tx = it.x % a.tiles_x, ty = it.x / a.tiles_x;
     const int64_t slot_ray = (int64_t)item * kRays + tid;
-    double accd = 0.0, rem = 0.0;
-    if (kG) rem = a.seg_d[slot_ray] + a.seg_g[slot_ray];
+    ray_acc[tid] = kG ? a.seg_d[slot_ray] + a.seg_g[slot_ray] : 0.0;
+    int covered = it.y;  // kGrad: pairs below this have a record
     const int nd = a.rp.desc_count[item];
     for (int k = 0; k < nd; ++k) {
       const int4 d = reinterpret_cast<const int4*>(a.rp.desc)[(int64_t)item * a.rp.desc_per_item + k];
       const int64_t off = d.x;
       const int n = d.y, cs = d.z, j0 = d.w & 0xffff, j1 = d.w >> 16;
       __syncthreads();
-      // stage the descriptor's Gaussians and load its pairs
-      int pos = -1;
+      // ---- L: Gaussians and entries
+      if (kG) {
+        for (int i = covered + tid; i < cs + j0; i += kRays) {
+          double4* rp = reinterpret_cast<double4*>(a.partial + (int64_t)__ldg(&a.rec[i].pos) * 8);
+          rp[0] = make_double4(0, 0, 0, 0);
+          rp[1] = make_double4(0, 0, 0, 0);
+        }
+        covered = cs + j1;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) jm[w * kChunk + tid] = 0u;
+      }
       if (tid >= j0 && tid < j1) {
         const sdgr_pair_rec r = load_rec(a.rec + cs + tid);
         sk[tid] = r.kappa;
@@ -707,14 +780,8 @@ __global__ void __launch_bounds__(256, 3) k_replay(ReplayArgs a) {
         if (kG) {
           su[tid] = r.u; sv[tid] = r.v;
           sa0[tid] = r.a00; sa1[tid] = r.a01; sa2[tid] = r.a11;
-          pos = r.pos;
+          spos[tid] = r.pos;
         }
-      }
-      run_s[tid] = 0;
-      run_e[tid] = 0;
-      if (kG) {
-#pragma unroll
-        for (int w = 0; w < 8; ++w) { rows[w * kRays + tid] = 0u; jm[w * kChunk + tid] = 0u; }
       }
       for (int p = tid; p < n; p += kRays) {
         fS[p] = a.rp.S[off + p];
@@ -723,67 +790,174 @@ __global__ void __launch_bounds__(256, 3) k_replay(ReplayArgs a) {
         fr[p] = a.rp.r[off + p];
       }
       __syncthreads();
-      // ray runs (pairs are ray-major) and, for kGrad, the two membership bitmaps
-      for (int p = tid; p < n; p += kRays) {
-        const int r = fr[p];
-        if (p == 0 || fr[p - 1] != r) run_s[r] = p;
-        if (p == n - 1 || fr[p + 1] != r) run_e[r] = p + 1;
-        if (kG) {
-          const int j = fj[p];
-          atomicOr(rows + (j >> 5) * kRays + r, 1u << (j & 31));
-          atomicOr(jm + (r >> 5) * kChunk + j, 1u << (r & 31));
+      // ---- B: g*contrib per entry, segmented scan over the ray runs
+      // E contiguous entries per thread, E = ceil(n / 256) <= 8: all threads share the work
+      const int E = (n + kRays - 1) / kRays;
+      const int q0 = E * tid;
+      const int cnt = max(0, min(E, n - q0));
+      double v[8];
+      bool hd[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        v[e] = 0.0;
+        hd[e] = true;
+        if (e < cnt) {
+          const int q = q0 + e;
+          const int j = fj[q], r = fr[q];
+          const double tau = sk[j] * fW[q];
+          const double T = exp(-fS[q]);
+          const double oma = -expm1(-tau);
+          v[e] = sg[j] * (T * oma * sp[j]);
+          hd[e] = q == 0 || fr[q - 1] != r;
+          if (kG) atomicOr(jm + (r >> 5) * kChunk + j, 1u << (r & 31));
         }
       }
-      // pair-parallel transmittance and contributions
-      for (int p = tid; p < n; p += kRays) {
-        const int j = fj[p];
-        const double tau = sk[j] * fW[p];
-        const double T = exp(-fS[p]);
-        const double oma = -expm1(-tau);
-        const double gI = sg[j];
-        fG[p] = gI * (T * oma * sp[j]);
-        if (kG) {
-          fS[p] = gI * T * exp(-tau) * sp[j];
-          fY[p] = T * oma;
+      block_seg_scan8(v, hd, cnt, s_agg, s_flag);
+      if (kG) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (e < cnt) fD[q0 + e] = ray_acc[fr[q0 + e]] - v[e];
+        __syncthreads();
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int q = q0 + e;
+        if (e < cnt && (q == n - 1 || fr[q + 1] != fr[q])) {
+          if (kG) ray_acc[fr[q]] -= v[e];
+          else ray_acc[fr[q]] += v[e];
+        }
+      }
+      if (!kG) continue;
+      // ---- C: Gaussian-major order
+      {
+        int c = 0;
+        uint32_t plo = 0, phi = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          if (w < 4) plo |= (uint32_t)c << (8 * w);
+          else phi |= (uint32_t)c << (8 * (w - 4));
+          c += __popc(jm[w * kChunk + tid]);
+        }
+        jpre[tid] = plo;
+        jpre[kChunk + tid] = phi;
+        int tot;
+        const int gs = block_scan(c, scan_tmp, tot);
+        gstart[tid] = gs;
+        if (tid == 0) gstart[kChunk] = tot;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (e < cnt) {
+          const int q = q0 + e;
+          const int j = fj[q], r = fr[q], w = r >> 5;
+          const int rank = (int)((jpre[(w < 4 ? 0 : kChunk) + j] >> (8 * (w & 3))) & 255u) +
+                           __popc(jm[w * kChunk + j] & ((1u << (r & 31)) - 1u));
+          perm[gstart[j] + rank] = (uint16_t)q;
         }
       }
       __syncthreads();
-      // ray-serial sums (additions only)
-      if (!kG) {
-        for (int p = run_s[tid]; p < run_e[tid]; ++p) accd += fG[p];
-      } else {
-        for (int p = run_s[tid]; p < run_e[tid]; ++p) {
-          rem -= fG[p];
-          fG[p] = rem;  // downstream sum after this pair
-        }
-        __syncthreads();
-        // per-Gaussian reduction over its rays in ascending order
-        if (tid >= j0 && tid < j1) {
-          double racc[7] = {0, 0, 0, 0, 0, 0, 0};
-          const int jw = tid >> 5;
-          const uint32_t below = (1u << lane) - 1u;
-#pragma unroll 1
-          for (int w = 0; w < 8; ++w) {
-            uint32_t m = jm[w * kChunk + tid];
-            while (m) {
-              const int b = __ffs(m) - 1;
-              m &= m - 1;
-              const int r = w * 32 + b;
-              int idx = __popc(rows[jw * kRays + r] & below);
-              for (int q = 0; q < jw; ++q) idx += __popc(rows[q * kRays + r]);
-              const int p = run_s[r] + idx;
-              const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
-              const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
-              grad_terms(fY[p], (fS[p] - fG[p]) * fW[p], sk[tid], dx, dy, sa0[tid], sa1[tid], sa2[tid], racc);
-            }
+      // Gaussians of [j0, j1) without live entries still own a (zero) record
+      if (tid >= j0 && tid < j1 && gstart[tid + 1] == gstart[tid]) {
+        double4* rp = reinterpret_cast<double4*>(a.partial + (int64_t)spos[tid] * 8);
+        rp[0] = make_double4(0, 0, 0, 0);
+        rp[1] = make_double4(0, 0, 0, 0);
+      }
+      const int glo = max(32 * warp, j0), ghi = min(32 * warp + 32, j1);
+      if (glo >= ghi) continue;  // warp-uniform
+      const int lo = gstart[glo], hi = gstart[ghi];
+      double carry[7] = {0, 0, 0, 0, 0, 0, 0};
+      for (int R = lo, E7 = 0; R < hi; R += 32 * E7) {
+        E7 = min(8, (hi - R + 31) / 32);  // entries per lane this round
+        const int e0 = R + E7 * lane;
+        const int ec = max(0, min(E7, hi - e0));
+        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+        double first[7];
+        int first_j = -1;       // Gaussian of a leading run that ends inside this lane
+        bool seen_head = false;
+        int any = 0;
+        for (int e = 0; e < ec; ++e) {
+          const int qq = e0 + e;
+          const int p = perm[qq];
+          const int j = fj[p], r = fr[p];
+          const bool head = qq == gstart[j];
+          const bool tail = qq == gstart[j + 1] - 1;
+          if (head) {
+#pragma unroll
+            for (int t = 0; t < 7; ++t) acc[t] = 0.0;
+            seen_head = true;
+            any = 1;
           }
-          double4* recp = reinterpret_cast<double4*>(a.partial + (int64_t)pos * 8);
-          recp[0] = make_double4(racc[0] * sg[tid], racc[1], racc[2], racc[3]);
-          recp[1] = make_double4(racc[4], racc[5], racc[6], 0.0);
+          const double kap = sk[j], wgt = fW[p];
+          const double tau = kap * wgt;
+          const double T = exp(-fS[p]);
+          const double oma = -expm1(-tau);
+          const double x = sg[j] * T * exp(-tau) * sp[j];
+          const double dx = dsub((double)(tx * kTile + (r & 15)), su[j]);
+          const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[j]);
+          grad_terms(T * oma, (x - fD[p]) * wgt, kap, dx, dy, sa0[j], sa1[j], sa2[j], acc);
+          if (tail) {
+            if (seen_head) {
+              double4* rp = reinterpret_cast<double4*>(a.partial + (int64_t)spos[j] * 8);
+              rp[0] = make_double4(acc[0] * sg[j], acc[1], acc[2], acc[3]);
+              rp[1] = make_double4(acc[4], acc[5], acc[6], 0.0);
+            } else {
+#pragma unroll
+              for (int t = 0; t < 7; ++t) first[t] = acc[t];
+              first_j = j;
+            }
+#pragma unroll
+            for (int t = 0; t < 7; ++t) acc[t] = 0.0;
+            seen_head = true;  // later entries of this lane start new runs
+          }
+        }
+        // warp segmented scan of the open-run sums (acc, any): carry into each
+        // lane's leading run
+        double ex[7];
+        int f = any;
+#pragma unroll
+        for (int t = 0; t < 7; ++t) ex[t] = acc[t];
+#pragma unroll
+        for (int offs = 1; offs < 32; offs <<= 1) {
+          const int fo = __shfl_up_sync(0xffffffffu, f, offs);
+#pragma unroll
+          for (int t = 0; t < 7; ++t) {
+            const double ao = __shfl_up_sync(0xffffffffu, ex[t], offs);
+            if (lane >= offs && !f) ex[t] = ao + ex[t];
+          }
+          if (lane >= offs) f |= fo;
+        }
+        // ex/f: inclusive; shift to exclusive and fold in the round carry
+        const int fall = __shfl_sync(0xffffffffu, f, 31);
+        int exf = __shfl_up_sync(0xffffffffu, f, 1);
+        if (lane == 0) exf = 0;
+#pragma unroll
+        for (int t = 0; t < 7; ++t) {
+          const double last = __shfl_sync(0xffffffffu, ex[t], 31);
+          double e = __shfl_up_sync(0xffffffffu, ex[t], 1);
+          if (lane == 0) e = 0.0;
+          const double cin = exf ? e : carry[t] + e;
+          if (first_j >= 0) first[t] += cin;
+          carry[t] = fall ? last : carry[t] + last;
+        }
+        if (first_j >= 0) {
+          double4* rp = reinterpret_cast<double4*>(a.partial + (int64_t)spos[first_j] * 8);
+          rp[0] = make_double4(first[0] * sg[first_j], first[1], first[2], first[3]);
+          rp[1] = make_double4(first[4], first[5], first[6], 0.0);
         }
       }
     }
-    if (!kG) a.seg_out[slot_ray] = accd;
+    if (kG) {
+      // pairs after the last descriptor
+      for (int i = covered + tid; i < it.z; i += kRays) {
+        double4* rp = reinterpret_cast<double4*>(a.partial + (int64_t)__ldg(&a.rec[i].pos) * 8);
+        rp[0] = make_double4(0, 0, 0, 0);
+        rp[1] = make_double4(0, 0, 0, 0);
+      }
+    } else {
+      __syncthreads();
+      a.seg_out[slot_ray] = ray_acc[tid];
+    }
   }
 }
 
@@ -954,9 +1128,8 @@ int launch_grad_intensity(const sdgr_view& v, const sdgr_projection& p, const sd
     k_replay<kGSum><<<max(1, min(t.max_items, sm_count() * max(per_sm[0], 1))), 256, ReplayCfg<kGSum>::kSmem, st>>>(r);
     k_seg_scan<true><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_g, seg_d);
     note_launch(2);
-    if (cudaMemsetAsync(partial_g, 0, sizeof(double) * 8 * (size_t)t.n_pairs, st) != cudaSuccess ||
-        cudaMemsetAsync(r.counter, 0, sizeof(uint32_t), st) != cudaSuccess)
-      return SDGR_ERR_CUDA;
+    // k_replay<kGrad> writes every pair's record (zeros for pairs it skips)
+    if (cudaMemsetAsync(r.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
     r.seg_out = nullptr;
     r.seg_g = seg_g;
     r.seg_d = seg_d;
