@@ -119,7 +119,8 @@ typedef struct sdgr_projection {
  * touches only live pairs (no re-binning, no membership, no weights). */
 typedef struct sdgr_replay {
   int64_t capacity;      /* pair slots; T_c (member_pairs[0]) always suffices */
-  double* S;             /* (capacity) log-transmittance before the pair   */
+  double* y1;            /* (capacity) T (1 - e^-tau): transmittance x opacity */
+  double* t2;            /* (capacity) T e^-tau: transmittance after the pair  */
   double* w;             /* (capacity) footprint weight exp(-q)            */
   uint8_t* j;            /* (capacity) Gaussian index within its chunk      */
   uint8_t* r;            /* (capacity) ray index within its tile            */
@@ -129,6 +130,8 @@ typedef struct sdgr_replay {
   int32_t* desc_count;   /* (max_items) descriptors written per item        */
   unsigned long long* cursor; /* (2) device cursor [0], zeroed by the forward, and a
                                  sticky overflow flag [1] the caller zeroes */
+  double* gpair;         /* (tiles->n_pairs) scratch: dL/dI per sorted pair, written by
+                            the first backward replay pass, read by the second */
 } sdgr_replay;
 
 /* Packed per-(tile, Gaussian) record, one per sorted pair of the computation

@@ -55,8 +55,9 @@ class ProjectionDesc(C.Structure):
 
 class ReplayDesc(C.Structure):
     _fields_ = [
-        ("capacity", C.c_int64), ("S", _p), ("w", _p), ("j", _p), ("r", _p),
+        ("capacity", C.c_int64), ("y1", _p), ("t2", _p), ("w", _p), ("j", _p), ("r", _p),
         ("desc_per_item", C.c_int32), ("pad_", C.c_int32), ("desc", _p), ("desc_count", _p), ("cursor", _p),
+        ("gpair", _p),
     ]
 
 

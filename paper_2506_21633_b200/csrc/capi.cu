@@ -31,7 +31,7 @@ int launch_grad_intensity(const sdgr_view&, const sdgr_projection&, const sdgr_t
                           cudaStream_t);
 
 static bool replay_ok(const sdgr_replay* r) {
-  return !r || (r->S && r->w && r->j && r->r && r->desc && r->desc_count && r->cursor && r->capacity > 0 &&
+  return !r || (r->y1 && r->t2 && r->w && r->j && r->r && r->desc && r->desc_count && r->cursor && r->gpair && r->capacity > 0 &&
                 r->desc_per_item > 0);
 }
 int launch_grad_geometry(const sdgr_scene&, int, const sdgr_view*, const sdgr_projection*, const sdgr_tiles*,

@@ -74,7 +74,7 @@ struct WalkArgs {
   double* seg_out;         // kGSum: seg_g
   double* partial;         // kContrib: (n_pairs); kGrad: (n_pairs, 8)
   int32_t* status;
-  sdgr_replay rp;          // kContrib: live-pair log to write (rp.S == nullptr: none)
+  sdgr_replay rp;          // kContrib: live-pair log to write (rp.y1 == nullptr: none)
   int seg_filter;          // 0: all items, 1: first segment of each tile only, 2: later segments only
 };
 
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
   uint8_t* fj = reinterpret_cast<uint8_t*>(fy + (Cfg::kXY ? kCap : 0));
   uint8_t* fr = fj + kCap;                                  // ray of each slot (replay log)
   __shared__ long long rp_off;
-  const bool record = MODE == kContrib && a.rp.S != nullptr;
+  const bool record = MODE == kContrib && a.rp.y1 != nullptr;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_items = *a.n_items;
@@ -551,15 +551,17 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
         for (int p = tid; p < total; p += kRays) {
           const int j = fj[p];
           const double wgt = fw[p];
+          const double tau = sk[j] * wgt;
+          const double T = exp(-fs[p]);
+          const double oma = -expm1(-tau);
           if (lo >= 0) {
-            a.rp.S[lo + p] = fs[p];
+            // the backward needs only these per live pair: no transcendentals there
+            a.rp.y1[lo + p] = T * oma;
+            a.rp.t2[lo + p] = T * exp(-tau);
             a.rp.w[lo + p] = wgt;
             a.rp.j[lo + p] = (uint8_t)j;
             a.rp.r[lo + p] = fr[p];
           }
-          const double tau = sk[j] * wgt;
-          const double T = exp(-fs[p]);
-          const double oma = -expm1(-tau);
           const double c = T * oma * sp[j];
           if (MODE == kContrib) {
             fs[p] = c;
@@ -637,7 +639,8 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
 // ============================================================ replay ==========
 // Backward over the live-pair log the forward walk wrote: per work item, its
 // sub-chunk descriptors in walk order; per descriptor the live pairs in
-// ray-major, depth-minor order with S_before and w.  No binning, membership
+// ray-major, depth-minor order with y1 = T(1 - e^-tau), t2 = T e^-tau and w
+// (the forward already evaluated every transcendental the backward needs).  No binning, membership
 // or weight work is repeated, and only live pairs are touched.
 //   kGSum: per (item, ray) sum of g * contrib          (backward.py:129-139)
 //   kGrad: reverse-recurrence terms, reduced per Gaussian in ray order into
@@ -704,8 +707,8 @@ __device__ __forceinline__ void block_seg_scan8(double (&v)[8], const bool (&hd)
 
 template <int MODE>
 struct ReplayCfg {
-  // fS, fW (+ fD) doubles, fj, fr bytes (+ perm u16)
-  static constexpr size_t kSmem = kReplayCap * (MODE == kGrad ? 3 * 8 + 2 + 2 : 2 * 8 + 2);
+  // fY (+ fW, fD) doubles, fj, fr bytes (+ perm u16)
+  static constexpr size_t kSmem = kReplayCap * (MODE == kGrad ? 3 * 8 + 2 + 2 : 8 + 2);
 };
 
 // Per descriptor (<= kReplayCap log entries of Gaussians [j0, j1) of one chunk):
@@ -735,10 +738,11 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? 2 : 4) k_replay(ReplayArg
   __shared__ int s_flag[8];
   __shared__ int32_t scan_tmp[8];
   __shared__ int item_s;
+  __shared__ int4 s_desc[kRays];                    // the item's first 256 descriptors
   extern __shared__ double dyn[];
-  double* fS = dyn;                                  // S_before
-  double* fW = fS + kCap;                            // w
-  double* fD = fW + kCap;                            // kGrad: downstream sum after the pair
+  double* fY = dyn;                                  // y1 = T (1 - e^-tau)
+  double* fW = fY + kCap;                            // kGrad: w
+  double* fD = fW + (kG ? kCap : 0);                 // kGrad: x - D (x = g T e^-tau P, D downstream sum)
   uint16_t* perm = reinterpret_cast<uint16_t*>(fD + (kG ? kCap : 0));  // kGrad: Gaussian-major -> log
   uint8_t* fj = reinterpret_cast<uint8_t*>(perm + (kG ? kCap : 0));
   uint8_t* fr = fj + kCap;
@@ -750,17 +754,20 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? 2 : 4) k_replay(ReplayArg
     __syncthreads();
     const int item = item_s;
     if (item >= n_items) return;
+    // item metadata, its descriptors and the per-ray seeds load in parallel
     const int4 it = reinterpret_cast<const int4*>(a.items)[item];
+    const int nd = a.rp.desc_count[item];
+    const int4* descs = reinterpret_cast<const int4*>(a.rp.desc) + (int64_t)item * a.rp.desc_per_item;
+    if (tid < nd) s_desc[tid] = descs[tid];
     const int tx = it.x % a.tiles_x, ty = it.x / a.tiles_x;
     const int64_t slot_ray = (int64_t)item * kRays + tid;
     ray_acc[tid] = kG ? a.seg_d[slot_ray] + a.seg_g[slot_ray] : 0.0;
     int covered = it.y;  // kGrad: pairs below this have a record
-    const int nd = a.rp.desc_count[item];
     for (int k = 0; k < nd; ++k) {
-      const int4 d = reinterpret_cast<const int4*>(a.rp.desc)[(int64_t)item * a.rp.desc_per_item + k];
+      __syncthreads();
+      const int4 d = k < kRays ? s_desc[k] : descs[k];
       const int64_t off = d.x;
       const int n = d.y, cs = d.z, j0 = d.w & 0xffff, j1 = d.w >> 16;
-      __syncthreads();
       // ---- L: Gaussians and entries
       if (kG) {
         for (int i = covered + tid; i < cs + j0; i += kRays) {
@@ -776,7 +783,13 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? 2 : 4) k_replay(ReplayArg
         const sdgr_pair_rec r = load_rec(a.rec + cs + tid);
         sk[tid] = r.kappa;
         sp[tid] = r.phase;
-        sg[tid] = a.gvec[r.prim];
+        if (kG) {
+          sg[tid] = a.rp.gpair[cs + tid];  // written by the kGSum pass: no prim -> dL/dI gather chain
+        } else {
+          const double g = a.gvec[r.prim];
+          sg[tid] = g;
+          a.rp.gpair[cs + tid] = g;
+        }
         if (kG) {
           su[tid] = r.u; sv[tid] = r.v;
           sa0[tid] = r.a00; sa1[tid] = r.a01; sa2[tid] = r.a11;
@@ -784,8 +797,8 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? 2 : 4) k_replay(ReplayArg
         }
       }
       for (int p = tid; p < n; p += kRays) {
-        fS[p] = a.rp.S[off + p];
-        fW[p] = a.rp.w[off + p];
+        fY[p] = a.rp.y1[off + p];
+        if (kG) fW[p] = a.rp.w[off + p];
         fj[p] = a.rp.j[off + p];
         fr[p] = a.rp.r[off + p];
       }
@@ -804,10 +817,8 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? 2 : 4) k_replay(ReplayArg
         if (e < cnt) {
           const int q = q0 + e;
           const int j = fj[q], r = fr[q];
-          const double tau = sk[j] * fW[q];
-          const double T = exp(-fS[q]);
-          const double oma = -expm1(-tau);
-          v[e] = sg[j] * (T * oma * sp[j]);
+          v[e] = sg[j] * (fY[q] * sp[j]);
+          if (kG) fD[q] = sg[j] * a.rp.t2[off + q] * sp[j];  // x, thread-private until P7
           hd[e] = q == 0 || fr[q - 1] != r;
           if (kG) atomicOr(jm + (r >> 5) * kChunk + j, 1u << (r & 31));
         }
@@ -816,7 +827,7 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? 2 : 4) k_replay(ReplayArg
       if (kG) {
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-          if (e < cnt) fD[q0 + e] = ray_acc[fr[q0 + e]] - v[e];
+          if (e < cnt) fD[q0 + e] -= ray_acc[fr[q0 + e]] - v[e];
         __syncthreads();
       }
 #pragma unroll
@@ -888,14 +899,9 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? 2 : 4) k_replay(ReplayArg
             seen_head = true;
             any = 1;
           }
-          const double kap = sk[j], wgt = fW[p];
-          const double tau = kap * wgt;
-          const double T = exp(-fS[p]);
-          const double oma = -expm1(-tau);
-          const double x = sg[j] * T * exp(-tau) * sp[j];
           const double dx = dsub((double)(tx * kTile + (r & 15)), su[j]);
           const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[j]);
-          grad_terms(T * oma, (x - fD[p]) * wgt, kap, dx, dy, sa0[j], sa1[j], sa2[j], acc);
+          grad_terms(fY[p], fD[p] * fW[p], sk[j], dx, dy, sa0[j], sa1[j], sa2[j], acc);
           if (tail) {
             if (seen_head) {
               double4* rp = reinterpret_cast<double4*>(a.partial + (int64_t)spos[j] * 8);

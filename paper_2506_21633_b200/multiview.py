@@ -188,7 +188,7 @@ class MultiViewStep:
         # live-pair log: member pairs bound every view's live pairs
         d0 = self.planes[0].tiles
         self.replay = ReplayLog(int(getattr(self, "calib_tc", cap_pairs[0] * 16) * self.headroom),
-                                d0.max_items, d0.seg_len, dev)
+                                d0.max_items, d0.seg_len, dev, d0.n_pairs)
         self.cap = dict(cap_pairs)
 
     def calibrate(self):

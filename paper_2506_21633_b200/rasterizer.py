@@ -406,21 +406,24 @@ class ReplayLog:
     """Buffers of the live-pair log (sdgr_replay, include/sdgr.h): written by
     the forward walk, replayed by the backward so it touches live pairs only."""
 
-    def __init__(self, capacity: int, max_items: int, seg_len: int, device):
+    def __init__(self, capacity: int, max_items: int, seg_len: int, device, n_pairs: int = 1):
         cap = int(max(capacity, 1))
         self.capacity = cap
         self.desc_per_item = 40 * max(1, -(-seg_len // 256))
-        self.S = _empty((cap,), torch.float64, device)
+        self.y1 = _empty((cap,), torch.float64, device)
+        self.t2 = _empty((cap,), torch.float64, device)
         self.w = _empty((cap,), torch.float64, device)
         self.j = _empty((cap,), torch.uint8, device)
         self.r = _empty((cap,), torch.uint8, device)
         self.desc = _empty((max(max_items, 1) * self.desc_per_item, 4), torch.int32, device)
         self.desc_count = torch.zeros((max(max_items, 1),), dtype=torch.int32, device=device)
         self.cursor = torch.zeros((2,), dtype=torch.int64, device=device)
+        self.gpair = _empty((max(int(n_pairs), 1),), torch.float64, device)
         d = _lib.ReplayDesc()
         d.capacity, d.desc_per_item = cap, self.desc_per_item
-        d.S, d.w, d.j, d.r = ptr(self.S), ptr(self.w), ptr(self.j), ptr(self.r)
+        d.y1, d.t2, d.w, d.j, d.r = ptr(self.y1), ptr(self.t2), ptr(self.w), ptr(self.j), ptr(self.r)
         d.desc, d.desc_count, d.cursor = ptr(self.desc), ptr(self.desc_count), ptr(self.cursor)
+        d.gpair = ptr(self.gpair)
         self.desc_c = d
 
     def overflowed(self) -> bool:
@@ -442,7 +445,7 @@ def compute_intensities(rays: TileLists, projection: Projection, s_stop: float =
         s_stop=float(s_stop),
     )
     if replay and rays.member_pairs is not None:
-        buf.replay = ReplayLog(rays.member_pairs, rays.max_items, rays.seg_len, dev)
+        buf.replay = ReplayLog(rays.member_pairs, rays.max_items, rays.seg_len, dev, rays.n_pairs)
     _check(_lib.lib().sdgr_composite_forward(
         C.byref(projection.view), C.byref(projection._desc), C.byref(rays.desc()), float(s_stop),
         ptr(buf.seg_sum), ptr(buf.seg_base), ptr(buf.partial), ptr(buf.intensity_n), ptr(buf.status),
