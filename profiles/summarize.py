@@ -90,3 +90,33 @@ def source_hot(path, kernel_regex="k_walk", skip=0, top=25):
     for (f, ln), d in sorted(lines.items(), key=lambda x: -x[1]["samples"])[:top]:
         st = ",".join(f"{k}:{v}" for k, v in sorted(d["stalls"].items(), key=lambda x: -x[1])[:3])
         print(f"{100 * d['samples'] / tot:5.1f}% {f}:{ln:<4} {d['src']:<90} [{st}]")
+
+
+def source_inst(path, kernel_regex="k_segsum", skip=0, top=25):
+    """Per-CUDA-line executed warp instructions (where the instruction count goes)."""
+    txt = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass",
+                          "-k", f"regex:{kernel_regex}", "--launch-skip", str(skip), "--launch-count", "1"],
+                         capture_output=True, text=True).stdout
+    rows, fname, hdr = {}, None, None
+    for r in csv.reader(txt.splitlines()):
+        if not r:
+            continue
+        if r[0] == "File Path":
+            fname = r[1].split("/")[-1]
+            continue
+        if r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr is None or len(r) != len(hdr) or not r[0].isdigit():
+            continue
+        i = hdr.index("Instructions Executed")
+        try:
+            v = int(r[i] or 0)
+        except ValueError:
+            continue
+        if v:
+            rows[(fname, int(r[0]))] = (v, r[1].strip()[:90])
+    tot = sum(v for v, _ in rows.values()) or 1
+    print(f"{kernel_regex} launch {skip}: {tot / 1e6:.1f}M warp instructions")
+    for (f, ln), (v, src) in sorted(rows.items(), key=lambda x: -x[1][0])[:top]:
+        print(f"{100 * v / tot:5.1f}% {v / 1e6:7.2f}M {f}:{ln:<4} {src}")
