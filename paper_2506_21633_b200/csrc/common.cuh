@@ -95,4 +95,15 @@ int check_launch();  // returns SDGR_OK or SDGR_ERR_CUDA after a launch
 template <typename T>
 __device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
 
+// SMs of the current device (cached; persistent grids are sized from it)
+inline int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
 }  // namespace sdgr

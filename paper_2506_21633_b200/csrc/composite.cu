@@ -1013,15 +1013,6 @@ __global__ void __launch_bounds__(256) k_reduce_intensity(const int32_t* pair_st
   out[g] = acc;
 }
 
-static int sm_count() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
 
 template <int MODE>
 static int walk_grid(int max_items) {

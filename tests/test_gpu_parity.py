@@ -136,6 +136,30 @@ def test_depth_key_roundtrip():
     assert torch.equal(out.abs(), d.abs())
 
 
+def test_depth_order_api_matches_lexsort():
+    """sdgr_depth_order (kept as a standalone C-ABI utility; the binning no
+    longer needs a global order): visible Gaussians by (depth, index)."""
+    import ctypes as C
+
+    from paper_2506_21633_b200 import _lib
+
+    tank = targets.composite_target(targets.tank_preset(), [4000, 2000, 1000], seed=9)
+    cfg = sdgr.RadarConfig(azimuth_deg=33.0, elevation_deg=50.0, altitude_m=0.5, n_range=96, n_azimuth=96)
+    proj = sdgr.project_all(tank, cfg)
+    n = proj.n_scene
+    lib = _lib.lib()
+    ws_bytes = lib.sdgr_workspace_bytes(n, 1)
+    ws = torch.empty((ws_bytes,), dtype=torch.uint8, device="cuda")
+    order = torch.empty((n,), dtype=torch.int32, device="cuda")
+    assert lib.sdgr_depth_order(C.byref(proj.desc()), order.data_ptr(), ws.data_ptr(), ws_bytes, None) == 0
+    torch.cuda.synchronize()
+    vis = ((proj.flags & _lib.FLAG_VISIBLE) != 0).cpu().numpy()
+    depth = decode_depth(proj.depth_key).cpu().numpy()
+    idx = np.nonzero(vis)[0]
+    want = idx[np.lexsort((idx, depth[idx]))]
+    assert np.array_equal(order.cpu().numpy()[: idx.size], want)
+
+
 def test_empty_and_culled():
     cfg = sdgr.RadarConfig(azimuth_deg=20.0, elevation_deg=40.0, altitude_m=2.0, range_res_m=0.5,
                            azimuth_res_m=0.5, n_range=16, n_azimuth=16)
