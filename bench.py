@@ -14,8 +14,12 @@ per-Gaussian gradients.  Weak scaling: per-GPU work is fixed as N grows.
            over ranks.
 `e2e`    : the same step through the public API from pinned host memory
            (scene + upstream gradients H2D, accumulated gradients D2H).
-`roofline`: HBM roofline of the preprocess + sort + binning kernels with the
-           SURVEY.md §8d algorithmic byte formula.
+`roofline`: the dominant kernel (largest device time in an instrumented
+           step), timed live inside the timed region with CUDA events around
+           each of its launches (sdgr_profile_begin/end); achieved = its
+           algorithmic HBM bytes per launch (kernel_bytes())
+           / mean launch time; traffic = ncu DRAM bytes per launch from
+           profiles/ (committed capture) when present.
 `cpu_baseline`: the oracle port (oracle/sdgr_oracle.py, the reference's
            algorithm restated in NumPy + C) on the host cores, rank 0, N=1.
 `--impl reference`: the reference's CPU path (oracle port; the reference is
@@ -25,7 +29,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -204,15 +207,63 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU side
-def hbm_bytes_per_view(n: int, t16: dict, tiles: dict) -> float:
-    """B_pre + B_rank + B_bin (algorithmic bytes, FP32 params)."""
-    b_pre = 184.0 * n
-    b_rank = 192.0 * n
-    b_bin = 0.0
-    for p in (0, 1):
-        b = math.ceil(math.log2(max(tiles[p], 2))) + math.ceil(math.log2(max(n, 2)))
-        b_bin += t16[p] * (12 + 24 * math.ceil(b / 8) + 8)
-    return b_pre + b_rank + b_bin
+SCENE_B = 12 + 16 + 12 + 64 + 8          # f32 positions, rotations, log_scales, sh_coeffs, ke_raw per Gaussian
+GRAD_RMW_B = 2 * (29 * 4 + 4)            # f32 gradient groups + int32 visible count, read + written
+PROJ_W_B = 2 * (16 + 32 + 8 + 8 + 8 + 4) + 8 * 4 + 1   # K1 outputs per Gaussian (two planes + key/kappa/phase/flags)
+REC_B = 80                               # packed computation-plane pair record
+LOG_B = 8 + 8 + 8 + 1 + 1                # replay log entry: y1, t2, w, j, r
+
+
+def kernel_bytes(kid: int, n: int, t16: float, live: float, items: float, batch: float) -> float:
+    """Algorithmic HBM bytes of ONE launch of kernel `kid`:
+    every input read once and every output written once, per view-level
+    counts n (Gaussians), t16 (computation-plane pairs), live (logged live
+    pairs), items (depth-segment work items); batch = views per geometry launch."""
+    from paper_2506_21633_b200 import _lib as L
+    if kid == L.K_PROJECT:
+        return n * (SCENE_B + PROJ_W_B)
+    if kid == L.K_SEGSUM:
+        return REC_B * t16 + 8 * 256 * items
+    if kid == L.K_WALK:
+        return (REC_B + 8) * t16 + LOG_B * live + 8 * 256 * items
+    if kid == L.K_REPLAY_GSUM:
+        return (8 + 1 + 1) * live + (REC_B + 8 + 8) * t16 + 8 * 256 * items
+    if kid == L.K_REPLAY_GRAD:
+        return LOG_B * live + (REC_B + 8 + 64) * t16 + 2 * 8 * 256 * items
+    if kid == L.K_GEOMETRY:
+        per_view = n * (1 + 32 + 32 + 4 + 4 + 8 + 40) + 64 * t16
+        return n * (SCENE_B + GRAD_RMW_B) + batch * per_view
+    if kid == L.K_SPLAT:
+        return n * (1 + 8 + 16 + 32 + 8 + 8)
+    if kid == L.K_GRAD_IMAGE:
+        return n * (1 + 8 + 16 + 32 + 8 + 8 + 48)
+    if kid == L.K_GATHER:
+        return t16 * (4 + 4 + 80 + 4 + REC_B)
+    if kid == L.K_EMIT:
+        return n * 32 + 8 * t16
+    if kid == L.K_ONESWEEP:   # 6 passes per view: 4 over the N depth keys, 2 over the pairs
+        return 16 * (4 * n + 2 * t16) / 6
+    return float("nan")
+
+
+def _profile(lib):
+    import ctypes as C
+    from paper_2506_21633_b200 import _lib as L
+    ms = (C.c_double * L.PROFILE_KERNELS)()
+    cnt = (C.c_int64 * L.PROFILE_KERNELS)()
+    if lib.sdgr_profile_end(ms, cnt) != 0:
+        raise RuntimeError("sdgr_profile_end failed")
+    return list(ms), list(cnt)
+
+
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture summary."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None, None
+    d = json.loads(p.read_text())
+    e = d.get("kernels", {}).get(kernel)
+    return (e["dram_bytes_per_launch"], d.get("source")) if e else (None, None)
 
 
 def run_sdgr(args):
@@ -248,8 +299,20 @@ def run_sdgr(args):
         if world > 1:
             dist.barrier()
 
+    from paper_2506_21633_b200 import _lib as L
+    lib = L.lib()
     for _ in range(max(args.warmup, 3)):
         step.run(dlds)
+    torch.cuda.synchronize()
+    # one instrumented (untimed) step: per-kernel device time -> the dominant
+    # kernel; per-view live pairs and work items for its byte count
+    lib.sdgr_profile_begin(sum(1 << k for k in L.KERNEL_NAMES))
+    vstats = []
+    step.run(dlds, stats=vstats)
+    prof_ms, prof_cnt = _profile(lib)
+    st = torch.stack(vstats).double().mean(0).tolist()
+    live_pv, items_pv = st[0], st[1]
+    dom = max(L.KERNEL_NAMES, key=lambda k: prof_ms[k])
     torch.cuda.synchronize()
     barrier()
     # ---------------- timed: inputs resident in HBM ----------------
@@ -257,6 +320,7 @@ def run_sdgr(args):
     with ClockSampler(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
         barrier()
+        lib.sdgr_profile_begin(1 << dom)   # events around the dominant kernel's launches only
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for k in range(args.steps):
@@ -264,6 +328,7 @@ def run_sdgr(args):
         e1.record()
         torch.cuda.synchronize()
         barrier()
+        dom_ms, dom_cnt = _profile(lib)
     step.check()
     launches = (sdgr.launch_count() - l0) // args.steps
     ms = e0.elapsed_time(e1) / args.steps
@@ -309,19 +374,25 @@ def run_sdgr(args):
         e2e = {"value": world * V / (float(t.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t.item())}
 
-    # ---------------- roofline (preprocess + sort + binning) ----------------
+    # ---------------- roofline: the dominant kernel ----------------
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    v0 = step.views[0]
-    tiles = {0: -(-v0.n_u // 16) * -(-v0.n_v // 16), 1: -(-v0.n_az // 16) * -(-v0.n_rg // 16)}
-    bpv = hbm_bytes_per_view(args.n, step.calib_t16_mean, tiles)
-    t_hbm_ms = stages["project"] + stages["depth_sort"] + stages["binning"]
-    achieved = bpv * V / (t_hbm_ms / 1e3) / 1e9 if t_hbm_ms > 0 else None
+    t16_pv = step.calib_t16_mean[0]
+    batch = V / -(-V // step.geo_batch)
+    launch_ms = dom_ms[dom] / max(dom_cnt[dom], 1)
+    bpl = kernel_bytes(dom, args.n, t16_pv, live_pv, items_pv, batch)
+    achieved = bpl / (launch_ms / 1e3) / 1e9 if launch_ms > 0 else None
+    traffic, traffic_src = ncu_traffic(L.KERNEL_NAMES[dom])
+    step_ms_all = sum(prof_ms)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None,
-                "kernels": "k_project + radix sorts + count/emit/ranges/items (both planes)",
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
-                "bytes_per_view": bpv}
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": L.KERNEL_NAMES[dom], "bytes_per_launch": bpl, "launch_ms": launch_ms,
+                "launches_per_step": dom_cnt[dom] / args.steps,
+                "share_of_instrumented_kernels": prof_ms[dom] / step_ms_all if step_ms_all else None,
+                "kernel_ms_per_step": {L.KERNEL_NAMES[k]: round(prof_ms[k], 3) for k in L.KERNEL_NAMES},
+                "per_view": {"t16": t16_pv, "live_pairs": live_pv, "items": items_pv},
+                "traffic_source": traffic_src,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6.65 TB/s"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

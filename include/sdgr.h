@@ -190,6 +190,26 @@ int sdgr_version(void);
 const char* sdgr_status_string(int status);
 /* Kernels launched by this library since load (the bench's gpu_launches). */
 uint64_t sdgr_launch_count(void);
+/* Device timing of selected kernels: between sdgr_profile_begin(mask) and
+ * sdgr_profile_end, every launch of a kernel whose bit (1 << SDGR_K_*) is in
+ * mask is bracketed by CUDA events on its launch stream.  sdgr_profile_end
+ * synchronises on the last event and returns per-kernel totals (ms) and
+ * launch counts in arrays of SDGR_PROFILE_KERNELS entries (index = SDGR_K_*).
+ * Used by bench.py to time the dominant kernel inside the timed region. */
+#define SDGR_PROFILE_KERNELS 16
+#define SDGR_K_PROJECT 1      /* K1 k_project                      */
+#define SDGR_K_ONESWEEP 2     /* radix sort passes (depth + tile)  */
+#define SDGR_K_EMIT 3         /* pair emission                     */
+#define SDGR_K_GATHER 4       /* pair record packing               */
+#define SDGR_K_SEGSUM 5       /* forward pass A (segment sums)     */
+#define SDGR_K_WALK 6         /* forward tile walk (contributions) */
+#define SDGR_K_SPLAT 7        /* imaging-plane splat               */
+#define SDGR_K_GRAD_IMAGE 8   /* imaging-plane backward            */
+#define SDGR_K_REPLAY_GSUM 9  /* backward replay, segment sums     */
+#define SDGR_K_REPLAY_GRAD 10 /* backward replay, gradients        */
+#define SDGR_K_GEOMETRY 11    /* per-Gaussian chain rule (batched) */
+int sdgr_profile_begin(uint32_t kernel_mask);
+int sdgr_profile_end(double* ms, int64_t* launches);
 /* Bytes of scratch the binning calls need for n Gaussians / max pairs. */
 size_t sdgr_workspace_bytes(int64_t n, int64_t max_pairs);
 

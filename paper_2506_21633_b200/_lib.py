@@ -17,6 +17,12 @@ OK, ERR_INVALID, ERR_NUMERICAL, ERR_STATE, ERR_CUDA, ERR_CAPACITY = range(6)
 FLAG_VISIBLE, FLAG_SKIPPED, FLAG_CULLED = 1, 2, 4
 TILE = 16
 MAX_BATCH = 8
+PROFILE_KERNELS = 16
+K_PROJECT, K_ONESWEEP, K_EMIT, K_GATHER, K_SEGSUM, K_WALK, K_SPLAT, K_GRAD_IMAGE, K_REPLAY_GSUM, K_REPLAY_GRAD, \
+    K_GEOMETRY = range(1, 12)
+KERNEL_NAMES = {K_PROJECT: "k_project", K_ONESWEEP: "k_onesweep", K_EMIT: "k_emit_pairs", K_GATHER: "k_gather_prim",
+                K_SEGSUM: "k_segsum", K_WALK: "k_walk<kContrib>", K_SPLAT: "k_splat", K_GRAD_IMAGE: "k_grad_image",
+                K_REPLAY_GSUM: "k_replay<kGSum>", K_REPLAY_GRAD: "k_replay<kGrad>", K_GEOMETRY: "k_grad_geometry"}
 
 _p = C.c_void_p
 
@@ -88,6 +94,8 @@ SIGNATURES = [
     ("sdgr_status_string", C.c_char_p, [C.c_int]),
     ("sdgr_launch_count", C.c_uint64, []),
     ("sdgr_workspace_bytes", C.c_size_t, [C.c_int64, C.c_int64]),
+    ("sdgr_profile_begin", C.c_int, [C.c_uint32]),
+    ("sdgr_profile_end", C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     ("sdgr_project", C.c_int, [C.POINTER(SceneDesc), C.POINTER(View), C.POINTER(ProjectionDesc), _p]),
     ("sdgr_depth_order", C.c_int, [C.POINTER(ProjectionDesc), _p, _p, C.c_size_t, _p]),
     ("sdgr_count_pairs", C.c_int, [C.POINTER(ProjectionDesc), C.c_int32, _p, _p, _p, C.c_size_t, _p]),

@@ -307,7 +307,10 @@ __global__ void __launch_bounds__(128) k_grad_geometry(sdgr_scene sc, const __gr
 
 int launch_grad_image(const sdgr_view& v, const sdgr_projection& p, const double* intensity,
                       const double* dLdS, double* acc, cudaStream_t st) {
-  k_grad_image<<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(v, p.img, p.flags, intensity, dLdS, acc, p.n);
+  {
+    KernelTimer kt(SDGR_K_GRAD_IMAGE, st);
+    k_grad_image<<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(v, p.img, p.flags, intensity, dLdS, acc, p.n);
+  }
   note_launch();
   return check_launch();
 }
@@ -335,10 +338,13 @@ int launch_grad_geometry(const sdgr_scene& sc, int n_views, const sdgr_view* vie
     G.partial = partials[k];
   }
   const unsigned blocks = (unsigned)((sc.n + 127) / 128);
-  if (sc.dtype == 0)
-    k_grad_geometry<float><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
-  else
-    k_grad_geometry<double><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
+  {
+    KernelTimer kt(SDGR_K_GEOMETRY, st);
+    if (sc.dtype == 0)
+      k_grad_geometry<float><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
+    else
+      k_grad_geometry<double><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
+  }
   note_launch();
   return check_launch();
 }

@@ -255,12 +255,15 @@ int radix_sort(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64
     K* ko = to_out ? kout : kalt;
     uint32_t* vo = to_out ? vout : valt;
     uint32_t* stat = status + (size_t)pass * nblk * 256;
-    if (pass == 0 && vin == nullptr)
-      k_onesweep<K, true><<<(unsigned)nblk, kSortThreads, smem, st>>>(
-          ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
-    else
-      k_onesweep<K, false><<<(unsigned)nblk, kSortThreads, smem, st>>>(
-          ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
+    {
+      KernelTimer kt(SDGR_K_ONESWEEP, st);
+      if (pass == 0 && vin == nullptr)
+        k_onesweep<K, true><<<(unsigned)nblk, kSortThreads, smem, st>>>(
+            ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
+      else
+        k_onesweep<K, false><<<(unsigned)nblk, kSortThreads, smem, st>>>(
+            ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
+    }
     note_launch();
     ki = ko;
     vi = vo;
@@ -536,9 +539,12 @@ int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, con
     uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * np);
     const size_t used = (size_t)(p - static_cast<char*>(ws));
     if (used > ws_bytes) return SDGR_ERR_CAPACITY;
-    k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,
-                                                              view.cutoff, keys, tl.pre_prim,
-                                                              tl.pair_start, np, overflow);
+    {
+      KernelTimer kt(SDGR_K_EMIT, st);
+      k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,
+                                                                view.cutoff, keys, tl.pre_prim,
+                                                                tl.pair_start, np, overflow);
+    }
     note_launch();
     int bits = 1;
     while ((1 << bits) < tl.n_tiles) ++bits;
@@ -549,9 +555,12 @@ int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, con
     if (rc != SDGR_OK) return rc;
     k_tile_ranges<<<(unsigned)((tl.n_tiles + 255) / 256), 256, 0, st>>>(tl.pair_tile, np, n_dev,
                                                                         tl.n_tiles, tl.tile_range);
-    k_gather_prim<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(tl.pair_pos, tl.pre_prim, np, n_dev,
-                                                                tl.pair_prim, pl, proj.kappa, proj.phase,
-                                                                tl.plane == 0 ? tl.pair_rec : nullptr);
+    {
+      KernelTimer kt(SDGR_K_GATHER, st);
+      k_gather_prim<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(tl.pair_pos, tl.pre_prim, np, n_dev,
+                                                                  tl.pair_prim, pl, proj.kappa, proj.phase,
+                                                                  tl.plane == 0 ? tl.pair_rec : nullptr);
+    }
     note_launch(2);
   } else {
     k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,

@@ -13,6 +13,33 @@ static std::atomic<uint64_t> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 int check_launch() { return cudaPeekAtLastError() == cudaSuccess ? SDGR_OK : SDGR_ERR_CUDA; }
 
+// ---- kernel timing: a pool of event pairs recorded around selected launches
+constexpr int kProfMax = 16384;
+static uint32_t g_prof_mask = 0;
+static cudaEvent_t g_prof_ev[2 * kProfMax];
+static int g_prof_id[kProfMax];
+static int g_prof_created = 0, g_prof_n = 0;
+static bool g_prof_open = false;
+
+void prof_mark(int id, bool begin, cudaStream_t st) {
+  if (!(g_prof_mask & (1u << id))) return;
+  if (begin) {
+    if (g_prof_n >= kProfMax) return;
+    if (g_prof_n >= g_prof_created) {
+      cudaEventCreate(&g_prof_ev[2 * g_prof_n]);
+      cudaEventCreate(&g_prof_ev[2 * g_prof_n + 1]);
+      g_prof_created = g_prof_n + 1;
+    }
+    cudaEventRecord(g_prof_ev[2 * g_prof_n], st);
+    g_prof_id[g_prof_n] = id;
+    g_prof_open = true;
+  } else if (g_prof_open) {
+    cudaEventRecord(g_prof_ev[2 * g_prof_n + 1], st);
+    ++g_prof_n;
+    g_prof_open = false;
+  }
+}
+
 int launch_project(const sdgr_scene&, const sdgr_view&, sdgr_projection&, cudaStream_t);
 int launch_depth_order(const sdgr_projection&, int32_t*, void*, size_t, cudaStream_t);
 int scan_counts(const int32_t*, const int32_t*, int64_t, int32_t*, void*, cudaStream_t);
@@ -73,6 +100,28 @@ const char* sdgr_status_string(int s) {
 }
 
 uint64_t sdgr_launch_count(void) { return g_launches.load(); }
+
+int sdgr_profile_begin(uint32_t kernel_mask) {
+  g_prof_mask = kernel_mask;
+  g_prof_n = 0;
+  g_prof_open = false;
+  return SDGR_OK;
+}
+
+int sdgr_profile_end(double* ms, int64_t* launches) {
+  g_prof_mask = 0;
+  if (!ms || !launches) return SDGR_ERR_INVALID;
+  for (int k = 0; k < SDGR_PROFILE_KERNELS; ++k) { ms[k] = 0.0; launches[k] = 0; }
+  if (g_prof_n > 0 && cudaEventSynchronize(g_prof_ev[2 * g_prof_n - 1]) != cudaSuccess) return SDGR_ERR_CUDA;
+  for (int i = 0; i < g_prof_n; ++i) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, g_prof_ev[2 * i], g_prof_ev[2 * i + 1]) != cudaSuccess) return SDGR_ERR_CUDA;
+    ms[g_prof_id[i]] += t;
+    launches[g_prof_id[i]] += 1;
+  }
+  g_prof_n = 0;
+  return SDGR_OK;
+}
 
 size_t sdgr_workspace_bytes(int64_t n, int64_t max_pairs) {
   return binning_ws_bytes(n < 1 ? 1 : n, max_pairs < 1 ? 1 : max_pairs);

@@ -92,6 +92,16 @@ __device__ __forceinline__ double softplus64(double x) {
 void note_launch(int n = 1);
 int check_launch();  // returns SDGR_OK or SDGR_ERR_CUDA after a launch
 
+// Kernel timing (sdgr_profile_begin/end): events around a launch, only when
+// the kernel's bit is enabled.  Usage: { KernelTimer kt(SDGR_K_WALK, st); k<<<...>>>(...); }
+void prof_mark(int id, bool begin, cudaStream_t st);
+struct KernelTimer {
+  int id;
+  cudaStream_t st;
+  KernelTimer(int i, cudaStream_t s) : id(i), st(s) { prof_mark(id, true, st); }
+  ~KernelTimer() { prof_mark(id, false, st); }
+};
+
 template <typename T>
 __device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
 

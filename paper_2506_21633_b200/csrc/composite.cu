@@ -1030,7 +1030,10 @@ static int walk_grid(int max_items) {
 template <int MODE>
 static int launch_walk(const WalkArgs& a, int max_items, cudaStream_t st) {
   if (cudaMemsetAsync(a.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
-  k_walk<MODE><<<walk_grid<MODE>(max_items), 256, WalkCfg<MODE>::kSmem, st>>>(a);
+  {
+    KernelTimer kt(MODE == kContrib ? SDGR_K_WALK : 0, st);
+    k_walk<MODE><<<walk_grid<MODE>(max_items), 256, WalkCfg<MODE>::kSmem, st>>>(a);
+  }
   note_launch();
   return check_launch();
 }
@@ -1066,8 +1069,11 @@ int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const
       return SDGR_ERR_CUDA;
     static int per_sm = 0;
     if (per_sm == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_segsum, 256, 0);
-    k_segsum<<<max(1, min(t.max_items, sm_count() * max(per_sm, 1))), 256, 0, st>>>(
-        t.pair_rec, t.items, t.n_items, counter, t.tiles_x, v.cutoff, seg_fx);
+    {
+      KernelTimer kt(SDGR_K_SEGSUM, st);
+      k_segsum<<<max(1, min(t.max_items, sm_count() * max(per_sm, 1))), 256, 0, st>>>(
+          t.pair_rec, t.items, t.n_items, counter, t.tiles_x, v.cutoff, seg_fx);
+    }
     k_seg_scan<false, true><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_sum, seg_base);
     note_launch(2);
     WalkArgs a = base_args(v, t);
@@ -1091,7 +1097,10 @@ int launch_splat(const sdgr_view& v, const sdgr_projection& p, const double* int
   const int64_t npix = (int64_t)v.n_az * v.n_rg;
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(part);
   if (cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * npix, st) != cudaSuccess) return SDGR_ERR_CUDA;
-  k_splat<<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(v, p.img, p.flags, intensity, p.n, acc);
+  {
+    KernelTimer kt(SDGR_K_SPLAT, st);
+    k_splat<<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(v, p.img, p.flags, intensity, p.n, acc);
+  }
   k_splat_finish<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(acc, npix, image);
   note_launch(2);
   return check_launch();
@@ -1122,7 +1131,11 @@ int launch_grad_intensity(const sdgr_view& v, const sdgr_projection& p, const sd
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], k_replay<kGrad>, 256, ReplayCfg<kGrad>::kSmem);
     }
     if (cudaMemsetAsync(r.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
-    k_replay<kGSum><<<max(1, min(t.max_items, sm_count() * max(per_sm[0], 1))), 256, ReplayCfg<kGSum>::kSmem, st>>>(r);
+    {
+      KernelTimer kt(SDGR_K_REPLAY_GSUM, st);
+      k_replay<kGSum><<<max(1, min(t.max_items, sm_count() * max(per_sm[0], 1))), 256, ReplayCfg<kGSum>::kSmem,
+                        st>>>(r);
+    }
     k_seg_scan<true><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_g, seg_d);
     note_launch(2);
     // k_replay<kGrad> writes every pair's record (zeros for pairs it skips)
@@ -1131,7 +1144,11 @@ int launch_grad_intensity(const sdgr_view& v, const sdgr_projection& p, const sd
     r.seg_g = seg_g;
     r.seg_d = seg_d;
     r.partial = partial_g;
-    k_replay<kGrad><<<max(1, min(t.max_items, sm_count() * max(per_sm[1], 1))), 256, ReplayCfg<kGrad>::kSmem, st>>>(r);
+    {
+      KernelTimer kt(SDGR_K_REPLAY_GRAD, st);
+      k_replay<kGrad><<<max(1, min(t.max_items, sm_count() * max(per_sm[1], 1))), 256, ReplayCfg<kGrad>::kSmem,
+                        st>>>(r);
+    }
     note_launch();
     return check_launch();
   }

@@ -314,10 +314,13 @@ int launch_project(const sdgr_scene& scene, const sdgr_view& view, sdgr_projecti
     return SDGR_ERR_CUDA;
   const int threads = 256;
   const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
-  if (scene.dtype == 0)
-    k_project<float><<<blocks, threads, 0, stream>>>(scene, view, proj);
-  else
-    k_project<double><<<blocks, threads, 0, stream>>>(scene, view, proj);
+  {
+    KernelTimer kt(SDGR_K_PROJECT, stream);
+    if (scene.dtype == 0)
+      k_project<float><<<blocks, threads, 0, stream>>>(scene, view, proj);
+    else
+      k_project<double><<<blocks, threads, 0, stream>>>(scene, view, proj);
+  }
   note_launch();
   return check_launch();
 }

@@ -273,9 +273,11 @@ class MultiViewStep:
         if ev is not None:
             ev[1].record()
 
-    def run(self, dlds: torch.Tensor, timing: bool = False, check: bool = True):
+    def run(self, dlds: torch.Tensor, timing: bool = False, check: bool = True, stats: list | None = None):
         """Forward + backward of every view; dlds: (V, H, W) float64 on device.
-        Returns the accumulated SceneGradients (all-reduced if distributed)."""
+        Returns the accumulated SceneGradients (all-reduced if distributed).
+        stats: if a list, one device tensor per view is appended holding
+        (live pairs logged by the forward, work items) -- no host sync."""
         if self.cap is None:
             self.calibrate()
         if dlds.shape[0] != len(self.views):
@@ -292,6 +294,9 @@ class MultiViewStep:
             for k, v in enumerate(batch):
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)] if timing else None
                 self._view(v, dlds[b0 + k], k, ev)
+                if stats is not None:
+                    stats.append(torch.stack([self.replay.cursor[0],
+                                              self.planes[0].t["n_items"][0].to(torch.int64)]))
                 if timing:
                     evs.append(ev)
             gev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timing else None
