@@ -16,7 +16,8 @@ NAMES = [("k_walk<1>", "k_walk<kContrib>"), ("k_replay<4>", "k_replay<kGrad>"), 
 
 
 def unit_scale(u):
-    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "msecond": 1e3, "nsecond": 1e-3}.get(u, 1)
+    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3,
+            "nsecond": 1e-3, "ns": 1e-3}.get(u, 1)
 
 
 def main(out, reps):
