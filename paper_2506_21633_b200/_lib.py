@@ -11,7 +11,10 @@ import ctypes as C
 from pathlib import Path
 
 ABI_VERSION = 1
-LIB_PATH = Path(__file__).resolve().parent / "libsdgr.so"
+import os  # noqa: E402
+
+# SDGR_LIB selects a profiling build (e.g. libsdgr_prof.so) of the same ABI
+LIB_PATH = Path(__file__).resolve().parent / os.environ.get("SDGR_LIB", "libsdgr.so")
 
 OK, ERR_INVALID, ERR_NUMERICAL, ERR_STATE, ERR_CUDA, ERR_CAPACITY = range(6)
 FLAG_VISIBLE, FLAG_SKIPPED, FLAG_CULLED = 1, 2, 4

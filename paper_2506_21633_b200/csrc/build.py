@@ -17,11 +17,11 @@ PKG = HERE.parent
 ROOT = PKG.parent
 SOURCES = ["capi.cu", "preprocess.cu", "binning.cu", "composite.cu", "backward.cu"]
 HEADERS = [HERE / "common.cuh", ROOT / "include" / "sdgr.h"]
-LIB = PKG / "libsdgr.so"
+LIB = PKG / os.environ.get("SDGR_LIB_NAME", "libsdgr.so")   # profiling variants: another name
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
-         "-Xptxas", "-warn-spills", "-I", str(ROOT / "include")]
+         "-Xptxas", "-warn-spills", "-I", str(ROOT / "include")] + os.environ.get("SDGR_EXTRA_FLAGS", "").split()
 
 
 def _stale(target: Path, deps) -> bool:
@@ -32,7 +32,7 @@ def _stale(target: Path, deps) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    objdir = PKG / "_build"
+    objdir = PKG / ("_build" + os.environ.get("SDGR_BUILD_SUFFIX", ""))
     objdir.mkdir(exist_ok=True)
     objs = []
     for src in SOURCES:

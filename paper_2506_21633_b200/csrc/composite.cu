@@ -345,8 +345,29 @@ __global__ void __launch_bounds__(256) k_splat_finish(const unsigned long long* 
 }
 
 // ============================================================ tile walks ======
+#ifdef SDGR_WALK_PROFILE
+// phase profile of the walks (profiling builds only, profiles/walk_phases.py):
+// cycles between the barriers that close each phase, by thread 0 of each CTA
+__device__ unsigned long long g_walk_prof[16];
+#define WPROF(k)                                                                    \
+  do {                                                                              \
+    if (threadIdx.x == 0) {                                                         \
+      const long long t_ = clock64();                                               \
+      atomicAdd(&g_walk_prof[k], (unsigned long long)(t_ - t_prev));                \
+      t_prev = t_;                                                                  \
+    }                                                                               \
+  } while (0)
+#else
+#define WPROF(k) \
+  do {           \
+  } while (0)
+#endif
+
 template <int MODE>
 __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
+#ifdef SDGR_WALK_PROFILE
+  long long t_prev = clock64();
+#endif
   using Cfg = WalkCfg<MODE>;
   constexpr int kCap = Cfg::kCap;
   __shared__ uint32_t rows[8 * kRays];   // rows[w*256 + r]: bit (j&31) of word w = Gaussian j covers ray r
@@ -374,6 +395,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
     __syncthreads();
     if (tid == 0) item_s = (int)atomicAdd(a.counter, 1u);
     __syncthreads();
+    WPROF(0);
     const int item = item_s;
     if (item >= n_items) return;
     const int4 it = reinterpret_cast<const int4*>(a.items)[item];
@@ -414,6 +436,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
         pos = r.pos;
       }
       __syncthreads();
+      WPROF(1);
 #pragma unroll
       for (int w = 0; w < 4; ++w)
         gm[w] &= ((uint64_t)alive_bits[2 * w] | ((uint64_t)alive_bits[2 * w + 1] << 32));
@@ -446,6 +469,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
         const uint32_t ab = __ballot_sync(0xffffffffu, alive);
         if (lane == 0) alive_bits[warp] = ab;
         __syncthreads();
+        WPROF(3);
         uint64_t lm[4];
 #pragma unroll
         for (int w = 0; w < 4; ++w)
@@ -460,6 +484,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
         __syncthreads();
         const bool fits = have && tid >= j0 && (excl_g + cnt_g - base_s) <= kCap;
         const int j1 = j0 + __syncthreads_count(fits);
+        WPROF(4);
         // ---- P1: per-ray counts of members in [j0, j1), flat offsets
         int cnt_r = 0;
         uint32_t pre_lo = 0, pre_hi = 0;
@@ -481,6 +506,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
         unsigned long long rp_o = 0;
         if (record && tid == 0) rp_o = atomicAdd(a.rp.cursor, (unsigned long long)total);
         __syncthreads();
+        WPROF(5);
         // ---- P2: Gaussian-parallel weights into the flat slots
         const bool mine = have && tid >= j0 && tid < j1;
         const int jw = tid >> 5;
@@ -506,6 +532,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
           }
         }
         __syncthreads();
+        WPROF(6);
         // ---- P3: ray-serial log-transmittance prefix (additions only); the
         //      tau loads are issued 4 ahead of the dependent add chain
         if (cnt_r > 0) {
@@ -531,6 +558,10 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
           if (record)
             for (int q = roff; q < p1; ++q) fr[q] = (uint8_t)tid;
         }
+#ifdef SDGR_WALK_PROFILE
+        __syncthreads();
+        WPROF(10);
+#endif
         if (record && tid == 0) {
           const unsigned long long o = rp_o;
           const bool fits = o + (unsigned long long)total <= (unsigned long long)a.rp.capacity &&
@@ -546,6 +577,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
         }
         if (record) ++n_desc;
         __syncthreads();
+        WPROF(7);
         // ---- P4: flat pair-parallel transmittance and contributions
         const long long lo = record ? rp_off : -1ll;
         for (int p = tid; p < total; p += kRays) {
@@ -576,6 +608,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
           }
         }
         __syncthreads();
+        WPROF(8);
         // ---- P5: ray-serial sums of g*contrib (backward)
         if (MODE == kGSum) {
           for (int p = roff; p < roff + cnt_r; ++p) accd += fs[p];
@@ -608,6 +641,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
           }
         }
         __syncthreads();
+        WPROF(9);
         j0 = j1;
       }
       if (MODE == kContrib && have) a.partial[pos] = racc[0];
@@ -1169,3 +1203,11 @@ int launch_grad_intensity(const sdgr_view& v, const sdgr_projection& p, const sd
 }
 
 }  // namespace sdgr
+
+#ifdef SDGR_WALK_PROFILE
+extern "C" int sdgr_debug_walk_profile(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, sdgr::g_walk_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 4;
+  unsigned long long z[16] = {};
+  return cudaMemcpyToSymbol(sdgr::g_walk_prof, z, sizeof(z)) == cudaSuccess ? 0 : 4;
+}
+#endif
