@@ -586,14 +586,19 @@ size_t binning_ws_bytes(int64_t n, int64_t max_pairs) {
 }
 
 // ------------------------------------------------------ depth order --------
-// Exact stable (FP64 depth, index) order with a 32-bit radix sort:
+// Exact stable (FP64 depth, index) order with a 24-bit radix sort:
 //   1. min / max of the visible depth keys;
-//   2. k32 = floor((d - dmin) * (2^32 - 2) / (dmax - dmin)): monotone
-//      non-decreasing in d (every FP64 step is monotone), invisible = ~0u;
-//   3. stable 4-pass radix sort of k32 (ties keep index order);
-//   4. runs of equal k32 (depths closer than (dmax-dmin)/2^32) are re-sorted
-//      by the full 64-bit key, index as tie-break -- exactly np.lexsort's
-//      (depth, index) order (forward.py:147), at half the passes of a 64-bit sort.
+//   2. k = floor((d - dmin) * (2^24 - 2) / (dmax - dmin)): monotone
+//      non-decreasing in d (every FP64 step is monotone), invisible = 2^24 - 1;
+//   3. stable 3-pass radix sort of k (ties keep index order);
+//   4. runs of equal k (depths closer than (dmax-dmin)/2^24; ~1.3 keys per
+//      run on c4) are re-sorted by the full 64-bit key, index as tie-break --
+//      exactly np.lexsort's (depth, index) order (forward.py:147), with 3
+//      passes instead of the 8 of a 64-bit sort.
+constexpr int kKeyBits = 24;
+constexpr uint32_t kKeyInvisible = (1u << kKeyBits) - 1u;
+constexpr uint32_t kKeyMax = kKeyInvisible - 1u;
+
 __device__ __forceinline__ double key_to_depth(uint64_t k) {
   const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double((long long)b);
@@ -635,12 +640,12 @@ __global__ void __launch_bounds__(256) k_key32(const uint64_t* key, int64_t n, c
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint64_t k = key[i];
-  if (k == ~0ull) { k32[i] = 0xffffffffu; return; }
+  if (k == ~0ull) { k32[i] = kKeyInvisible; return; }
   const double dmin = key_to_depth(range[0]), dmax = key_to_depth(range[1]);
   const double span = dsub(dmax, dmin);
   double q = 0.0;
-  if (span > 0.0) q = dmul(dsub(key_to_depth(k), dmin), 4294967294.0 / span);
-  k32[i] = (uint32_t)fmin(fmax(q, 0.0), 4294967294.0);
+  if (span > 0.0) q = dmul(dsub(key_to_depth(k), dmin), (double)kKeyMax / span);
+  k32[i] = (uint32_t)fmin(fmax(q, 0.0), (double)kKeyMax);
 }
 
 // one thread per run of equal k32 (runs are rare and short); stable by index
@@ -649,7 +654,7 @@ __global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s, const ui
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t k = k32s[i];
-  if (k == 0xffffffffu) return;                       // invisible tail: order irrelevant
+  if (k == kKeyInvisible) return;                     // invisible tail: order irrelevant
   if (i > 0 && k32s[i - 1] == k) return;               // not a run start
   if (i + 1 >= n || k32s[i + 1] != k) return;          // run of length 1
   int64_t e = i + 1;
@@ -686,7 +691,7 @@ int launch_depth_order(const sdgr_projection& proj, int32_t* order, void* ws, si
   k_key32<<<blocks, 256, 0, st>>>(proj.depth_key, n, range, k32);
   note_launch(2);
   const int rc = radix_sort<uint32_t>(k32, nullptr, k32s, reinterpret_cast<uint32_t*>(order), n, nullptr, 0,
-                                      32, p, ws_bytes - used, st);
+                                      kKeyBits, p, ws_bytes - used, st);
   if (rc != SDGR_OK) return rc;
   k_fix_runs<<<blocks, 256, 0, st>>>(k32s, proj.depth_key, n, order);
   note_launch();
