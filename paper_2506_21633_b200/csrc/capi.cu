@@ -21,6 +21,17 @@ static int g_prof_id[kProfMax];
 static int g_prof_created = 0, g_prof_n = 0;
 static bool g_prof_open = false;
 
+// inside a stream capture the records must be external event nodes (a
+// default-flag record only orders the capture and never fires on replay)
+static void prof_record(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(ev, st);
+}
+
 void prof_mark(int id, bool begin, cudaStream_t st) {
   if (!(g_prof_mask & (1u << id))) return;
   if (begin) {
@@ -30,11 +41,11 @@ void prof_mark(int id, bool begin, cudaStream_t st) {
       cudaEventCreate(&g_prof_ev[2 * g_prof_n + 1]);
       g_prof_created = g_prof_n + 1;
     }
-    cudaEventRecord(g_prof_ev[2 * g_prof_n], st);
+    prof_record(g_prof_ev[2 * g_prof_n], st);
     g_prof_id[g_prof_n] = id;
     g_prof_open = true;
   } else if (g_prof_open) {
-    cudaEventRecord(g_prof_ev[2 * g_prof_n + 1], st);
+    prof_record(g_prof_ev[2 * g_prof_n + 1], st);
     ++g_prof_n;
     g_prof_open = false;
   }

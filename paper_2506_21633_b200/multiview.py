@@ -108,6 +108,8 @@ class MultiViewStep:
         self.cap = None
         self.planes = None
         self.stage_events = None
+        self.graph = None
+        self.graph_launches = 0
 
     # -- buffers ------------------------------------------------------------
     def _projection_bufs(self):
@@ -273,7 +275,8 @@ class MultiViewStep:
         if ev is not None:
             ev[1].record()
 
-    def run(self, dlds: torch.Tensor, timing: bool = False, check: bool = True, stats: list | None = None):
+    def run(self, dlds: torch.Tensor, timing: bool = False, check: bool = True, stats: list | None = None,
+            allreduce: bool = True):
         """Forward + backward of every view; dlds: (V, H, W) float64 on device.
         Returns the accumulated SceneGradients (all-reduced if distributed).
         stats: if a list, one device tensor per view is appended holding
@@ -304,6 +307,35 @@ class MultiViewStep:
             if timing:
                 gevs.append(gev)
         self.stage_events = (evs, gevs)
+        if allreduce and (self.group is not None or
+                          (torch.distributed.is_available() and torch.distributed.is_initialized())):
+            self.allreduce()
+        if check:
+            self.check()
+        return self.grads
+
+    # -- CUDA graph of a whole step -------------------------------------------
+    def capture(self, dlds: torch.Tensor, warm: bool = True):
+        """Record one step (every view's forward + backward; no all-reduce, no
+        host check) as a CUDA graph over static buffers: the scene tensors and
+        `dlds` are read where they live, so callers overwrite them in place and
+        call graph_step().  Kernel launches are replayed without host work or
+        per-launch gaps.  Returns the number of library kernels in the graph."""
+        if self.cap is None:
+            self.calibrate()
+        if warm:
+            self.run(dlds, check=False)   # first-call attributes / occupancy queries happen here
+        torch.cuda.synchronize()
+        n0 = self.lib.sdgr_launch_count()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.run(dlds, check=False, allreduce=False)
+        self.graph_launches = int(self.lib.sdgr_launch_count() - n0)
+        return self.graph_launches
+
+    def graph_step(self, check: bool = False):
+        """One captured step (+ the all-reduce when distributed)."""
+        self.graph.replay()
         if self.group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
             self.allreduce()
         if check:

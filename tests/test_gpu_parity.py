@@ -272,6 +272,30 @@ def test_multiview_step_equals_sum_of_views(geo_batch):
     assert torch.equal(got.visible.cpu(), vis.cpu())
 
 
+def test_multiview_graph_replay_equals_run():
+    """The captured CUDA graph of a step reproduces run() bitwise, and reads
+    its static inputs in place (new dL/dS values are picked up on replay)."""
+    from paper_2506_21633_b200.multiview import MultiViewStep
+
+    tank = targets.to_float32_exact(targets.composite_target(targets.tank_preset(), [3000, 1500, 500], seed=4))
+    cfgs = [sdgr.RadarConfig(azimuth_deg=az, elevation_deg=el, altitude_m=0.5, n_range=96, n_azimuth=96)
+            for az, el in ((10.0, 30.0), (130.0, 60.0), (250.0, 45.0))]
+    ds = sdgr.DeviceScene.from_host(tank, dtype=torch.float32)
+    step = MultiViewStep(ds, cfgs, geo_batch=2)
+    gen = torch.Generator("cuda").manual_seed(5)
+    dl = torch.randn((3, 96, 96), dtype=torch.float64, device="cuda", generator=gen)
+    step.run(dl)
+    want = step.flat_soa.clone()
+    assert step.capture(dl) > 0
+    step.graph_step(check=True)
+    assert torch.equal(step.flat_soa, want)
+    dl.copy_(torch.randn((3, 96, 96), dtype=torch.float64, device="cuda", generator=gen))
+    step.run(dl)
+    want2 = step.flat_soa.clone()
+    step.graph_step(check=True)
+    assert torch.equal(step.flat_soa, want2)
+
+
 def test_depth_ties_and_near_ties_vs_oracle():
     """Exact (depth, index) order with duplicated positions (ties -> index
     order) and positions 1e-12 m apart (runs of equal 32-bit depth keys)."""
