@@ -71,7 +71,7 @@ class MultiViewStep:
 
     def __init__(self, scene: DeviceScene, configs, cov_reg: float = DEFAULT_COV_REG,
                  cutoff: float = DEFAULT_CUTOFF, s_stop: float = S_STOP, headroom: float = 1.3,
-                 group=None, geo_batch: int = _lib.MAX_BATCH):
+                 group=None, geo_batch: int = _lib.MAX_BATCH, lanes: int = 4):
         self.scene = scene
         self.configs = list(configs)
         self.views = [view_constants(c, cov_reg, cutoff) for c in self.configs]
@@ -91,15 +91,19 @@ class MultiViewStep:
         # records and imaging-plane sums stay resident until one batched
         # sdgr_grad_geometry_batch call consumes them
         self.geo_batch = max(1, min(int(geo_batch), _lib.MAX_BATCH, len(self.views)))
-        self.counters = torch.zeros((4,), dtype=torch.int32, device=dev)
-        self.member_pairs = torch.zeros((2,), dtype=torch.int64, device=dev)
-        self.proj_bufs = [self._projection_bufs() for _ in range(self.geo_batch)]
+        # lanes: views alternate between `lanes` streams, each with its own
+        # per-view working buffers, so one view's latency-bound walks overlap
+        # another view's preprocessing; the batch's geometry joins the lanes
+        self.n_lanes = max(1, min(int(lanes), self.geo_batch))
+        self.lanes = [self._lane() for _ in range(self.n_lanes)]
+        self.counters, self.member_pairs = self.lanes[0].counters, self.lanes[0].member_pairs
+        # two slot sets: batch b's geometry overlaps batch b+1's views
+        self.n_slots = 2 * self.geo_batch if len(self.views) > self.geo_batch else self.geo_batch
+        self.proj_bufs = [self._projection_bufs(self._lane_of(k)) for k in range(self.n_slots)]
         self.pds = [pd for pd, _ in self.proj_bufs]
         self.pd = self.pds[0]
-        self.order = _empty((n,), torch.int32, dev)
-        self.intensity = _empty((n,), torch.float64, dev)
-        self.image = _empty(self.img_shape, torch.float64, dev)
-        self.acc_imgs = [_empty((6, n), torch.float64, dev) for _ in range(self.geo_batch)]
+        self.order = self.lanes[0].order
+        self.acc_imgs = [_empty((6, n), torch.float64, dev) for _ in range(self.n_slots)]
         self.acc_img = self.acc_imgs[0]
         self.status = torch.zeros((4,), dtype=torch.int32, device=dev)
         # gradients: one flat float32 buffer so the all-reduce is one call
@@ -112,7 +116,23 @@ class MultiViewStep:
         self.graph_launches = 0
 
     # -- buffers ------------------------------------------------------------
-    def _projection_bufs(self):
+    class _Lane:
+        pass
+
+    def _lane(self):
+        """Stream + per-view working buffers of one lane (pair buffers are
+        added by _alloc_planes once the capacities are known)."""
+        n, dev = self.n, self.dev
+        ln = MultiViewStep._Lane()
+        ln.stream = torch.cuda.Stream(device=dev)
+        ln.counters = torch.zeros((4,), dtype=torch.int32, device=dev)
+        ln.member_pairs = torch.zeros((2,), dtype=torch.int64, device=dev)
+        ln.order = _empty((n,), torch.int32, dev)
+        ln.intensity = _empty((n,), torch.float64, dev)
+        ln.image = _empty(self.img_shape, torch.float64, dev)
+        return ln
+
+    def _projection_bufs(self, lane):
         """One set of per-view projection records (K1 outputs) + its descriptor."""
         n, dev = self.n, self.dev
         rec = {}
@@ -131,7 +151,7 @@ class MultiViewStep:
                       ("phase_raw", torch.float64), ("flags", torch.uint8)):
             rec[k] = _empty((n,), dt, dev)
             setattr(pd, k, ptr(rec[k]))
-        pd.counters, pd.member_pairs = ptr(self.counters), ptr(self.member_pairs)
+        pd.counters, pd.member_pairs = ptr(lane.counters), ptr(lane.member_pairs)
         pd.ke_act = None
         pd.look = None
         return pd, rec
@@ -145,17 +165,16 @@ class MultiViewStep:
     def _alloc_planes(self, cap_pairs: dict):
         n, dev = self.n, self.dev
         v = self.views[0]
-        self.planes = {}
         ws_need = self.lib.sdgr_workspace_bytes(n, max(cap_pairs.values()))
-        self.ws = _empty((ws_need,), torch.uint8, dev)
-        self.ws_bytes = ws_need
+        cap = cap_pairs[0]
+        nu, nv = v.n_u, v.n_v
+        tx, ty = -(-nu // TILE), -(-nv // TILE)
+        seg = _seg_len(cap)
+        max_items = -(-cap // seg) + tx * ty
         # only the computation plane is binned: the splat is Gaussian-parallel
-        for pl in (0,):
-            cap = cap_pairs[pl]
-            nu, nv = v.n_u, v.n_v
-            tx, ty = -(-nu // TILE), -(-nv // TILE)
-            seg = _seg_len(cap)
-            max_items = -(-cap // seg) + tx * ty
+        for ln in self.lanes:
+            ln.ws = _empty((ws_need,), torch.uint8, dev)
+            ln.ws_bytes = ws_need
             t = dict(
                 pair_tile=_empty((cap,), torch.int32, dev), pair_pos=_empty((cap,), torch.int32, dev),
                 pair_prim=_empty((cap,), torch.int32, dev), pre_prim=_empty((cap,), torch.int32, dev),
@@ -169,28 +188,29 @@ class MultiViewStep:
                 pair_rec=_empty((cap, _lib.PAIR_REC_BYTES), torch.uint8, dev),
             )
             d = _lib.TilesDesc()
-            d.plane, d.tiles_x, d.tiles_y, d.n_tiles = pl, tx, ty, tx * ty
+            d.plane, d.tiles_x, d.tiles_y, d.n_tiles = 0, tx, ty, tx * ty
             d.n_pairs = cap
             for k in ("pair_tile", "pair_pos", "pair_prim", "pre_prim", "pair_start", "tile_range", "items",
                       "tile_first", "n_items", "pair_rec"):
                 setattr(d, k, ptr(t[k]))
             d.seg_len, d.max_items, d.device_count = seg, max_items, 1
-            self.planes[pl] = _PlaneBufs(offsets=_empty((n + 1,), torch.int32, dev), tiles=d, t=t)
-        # per batch slot: pair_start (TilesDesc copy) and the partial records
-        d0, t0 = self.planes[0].tiles, self.planes[0].t
-        self.slot_pair_start = [t0["pair_start"]] + [_empty((n,), torch.int32, dev)
-                                                     for _ in range(self.geo_batch - 1)]
-        self.slot_partial = [_empty((d0.n_pairs, 8), torch.float64, dev) for _ in range(self.geo_batch)]
+            ln.plane = _PlaneBufs(offsets=_empty((n + 1,), torch.int32, dev), tiles=d, t=t)
+            ln.splat_scratch = _empty((v.n_rg * v.n_az,), torch.int64, dev)
+            # live-pair log: member pairs bound every view's live pairs
+            ln.replay = ReplayLog(int(getattr(self, "calib_tc", cap * 16) * self.headroom), max_items, seg, dev, cap)
+        ln0 = self.lanes[0]
+        self.planes = {0: ln0.plane}
+        self.ws, self.ws_bytes = ln0.ws, ln0.ws_bytes
+        self.replay = ln0.replay
+        self.intensity, self.image, self.splat_scratch = ln0.intensity, ln0.image, ln0.splat_scratch
+        # per batch slot (lane = slot mod lanes): pair_start and the partial records
+        self.slot_pair_start = [_empty((n,), torch.int32, dev) for _ in range(self.n_slots)]
+        self.slot_partial = [_empty((cap, 8), torch.float64, dev) for _ in range(self.n_slots)]
         self.slot_tiles = []
-        for k in range(self.geo_batch):
-            dk = _lib.TilesDesc.from_buffer_copy(d0)
+        for k in range(self.n_slots):
+            dk = _lib.TilesDesc.from_buffer_copy(self._lane_of(k).plane.tiles)
             dk.pair_start = ptr(self.slot_pair_start[k])
             self.slot_tiles.append(dk)
-        self.splat_scratch = _empty((v.n_rg * v.n_az,), torch.int64, dev)
-        # live-pair log: member pairs bound every view's live pairs
-        d0 = self.planes[0].tiles
-        self.replay = ReplayLog(int(getattr(self, "calib_tc", cap_pairs[0] * 16) * self.headroom),
-                                d0.max_items, d0.seg_len, dev, d0.n_pairs)
         self.cap = dict(cap_pairs)
 
     def calibrate(self):
@@ -220,10 +240,12 @@ class MultiViewStep:
 
     # -- one view -----------------------------------------------------------
     def _view(self, v, dlds: torch.Tensor, slot: int, ev=None):
-        """K1-K9 of one view into batch slot `slot` (the geometry epilogue runs per batch)."""
+        """K1-K9 of one view into batch slot `slot` (the geometry epilogue runs
+        per batch), on the current stream with lane slot % lanes's buffers."""
         lib, st = self.lib, _stream()
+        ln = self._lane_of(slot)
         pd = C.byref(self.pds[slot])
-        P0 = self.planes[0]
+        P0 = ln.plane
         t0 = P0.t
         tiles = C.byref(self.slot_tiles[slot])
         acc = self.acc_imgs[slot]
@@ -234,33 +256,36 @@ class MultiViewStep:
         mark(0)
         _check(lib.sdgr_project(C.byref(self.sd), C.byref(v), pd, st), "sdgr_project")
         mark(1)
-        _check(lib.sdgr_depth_order(pd, ptr(self.order), ptr(self.ws), self.ws_bytes, st), "sdgr_depth_order")
+        _check(lib.sdgr_depth_order(pd, ptr(ln.order), ptr(ln.ws), ln.ws_bytes, st), "sdgr_depth_order")
         mark(2)
-        _check(lib.sdgr_count_pairs(pd, 0, ptr(self.order), ptr(P0.offsets), ptr(self.ws), self.ws_bytes, st),
+        _check(lib.sdgr_count_pairs(pd, 0, ptr(ln.order), ptr(P0.offsets), ptr(ln.ws), ln.ws_bytes, st),
                "sdgr_count_pairs")
-        _check(lib.sdgr_bin_pairs(pd, C.byref(v), ptr(self.order), ptr(P0.offsets), tiles,
-                                  ptr(self.ws), self.ws_bytes, st), "sdgr_bin_pairs")
+        _check(lib.sdgr_bin_pairs(pd, C.byref(v), ptr(ln.order), ptr(P0.offsets), tiles,
+                                  ptr(ln.ws), ln.ws_bytes, st), "sdgr_bin_pairs")
         mark(3)
         _check(lib.sdgr_composite_forward(C.byref(v), pd, tiles, self.s_stop, ptr(t0["seg_a"]),
-                                          ptr(t0["seg_b"]), ptr(t0["partial_I"]), ptr(self.intensity),
-                                          ptr(self.status), C.byref(self.replay.desc_c), st),
+                                          ptr(t0["seg_b"]), ptr(t0["partial_I"]), ptr(ln.intensity),
+                                          ptr(self.status), C.byref(ln.replay.desc_c), st),
                "sdgr_composite_forward")
         mark(4)
-        _check(lib.sdgr_splat(C.byref(v), pd, ptr(self.intensity), ptr(self.splat_scratch), ptr(self.image), st),
+        _check(lib.sdgr_splat(C.byref(v), pd, ptr(ln.intensity), ptr(ln.splat_scratch), ptr(ln.image), st),
                "sdgr_splat")
         mark(5)
-        _check(lib.sdgr_grad_image(C.byref(v), pd, ptr(self.intensity), ptr(dlds), ptr(acc), st),
+        _check(lib.sdgr_grad_image(C.byref(v), pd, ptr(ln.intensity), ptr(dlds), ptr(acc), st),
                "sdgr_grad_image")
         mark(6)
         # seg_b holds the forward's exclusive prefixes; seg_a is reused as scratch
         _check(lib.sdgr_grad_intensity(C.byref(v), pd, tiles, self.s_stop, ptr(t0["seg_b"]),
                                        ptr(acc[0]), ptr(t0["seg_a"]), ptr(t0["seg_c"]),
-                                       ptr(self.slot_partial[slot]), C.byref(self.replay.desc_c), st),
+                                       ptr(self.slot_partial[slot]), C.byref(ln.replay.desc_c), st),
                "sdgr_grad_intensity")
         mark(7)
 
-    def _geometry(self, views, ev=None):
-        """Batched K10 over the views held in slots 0..len(views)-1."""
+    def _lane_of(self, slot: int):
+        return self.lanes[(slot % self.geo_batch) % self.n_lanes]
+
+    def _geometry(self, views, s0: int = 0, ev=None):
+        """Batched K10 over the views held in slots s0..s0+len(views)-1."""
         k = len(views)
         Views = _lib.View * k
         Projs = _lib.ProjectionDesc * k
@@ -269,8 +294,8 @@ class MultiViewStep:
         if ev is not None:
             ev[0].record()
         _check(self.lib.sdgr_grad_geometry_batch(
-            C.byref(self.sd), k, Views(*views), Projs(*self.pds[:k]), Tiles(*self.slot_tiles[:k]),
-            Ptrs(*[ptr(a) for a in self.acc_imgs[:k]]), Ptrs(*[ptr(p) for p in self.slot_partial[:k]]),
+            C.byref(self.sd), k, Views(*views), Projs(*self.pds[s0:s0 + k]), Tiles(*self.slot_tiles[s0:s0 + k]),
+            Ptrs(*[ptr(a) for a in self.acc_imgs[s0:s0 + k]]), Ptrs(*[ptr(p) for p in self.slot_partial[s0:s0 + k]]),
             C.byref(self.gd), 1, _stream()), "sdgr_grad_geometry_batch")
         if ev is not None:
             ev[1].record()
@@ -287,23 +312,40 @@ class MultiViewStep:
             raise ValueError("one upstream image gradient per view")
         self.flat_soa.zero_()
         self.status.zero_()
-        for P in self.planes.values():
-            P.t["n_items"].zero_()   # sticky overflow flags: one check per step
-        self.replay.cursor.zero_()
+        for ln in self.lanes:
+            ln.plane.t["n_items"].zero_()   # sticky overflow flags: one check per step
+            ln.replay.cursor.zero_()
         evs, gevs = [], []
         B = self.geo_batch
-        for b0 in range(0, len(self.views), B):
+        n_sets = self.n_slots // B
+        main = torch.cuda.current_stream()
+        start = torch.cuda.Event()
+        start.record(main)             # lanes start after the zeroing above
+        for ln in self.lanes:
+            ln.stream.wait_event(start)
+        geo_done = [None] * n_sets     # geometry that last read each slot set
+        for bi, b0 in enumerate(range(0, len(self.views), B)):
             batch = self.views[b0:b0 + B]
+            s0 = (bi % n_sets) * B
+            if geo_done[bi % n_sets] is not None:
+                for ln in self.lanes:
+                    ln.stream.wait_event(geo_done[bi % n_sets])
             for k, v in enumerate(batch):
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)] if timing else None
-                self._view(v, dlds[b0 + k], k, ev)
-                if stats is not None:
-                    stats.append(torch.stack([self.replay.cursor[0],
-                                              self.planes[0].t["n_items"][0].to(torch.int64)]))
+                ln = self._lane_of(s0 + k)
+                with torch.cuda.stream(ln.stream):
+                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)] if timing else None
+                    self._view(v, dlds[b0 + k], s0 + k, ev)
+                    if stats is not None:
+                        stats.append(torch.stack([ln.replay.cursor[0], ln.plane.t["n_items"][0].to(torch.int64)]))
                 if timing:
                     evs.append(ev)
+            for ln in self.lanes:      # this batch's views are done (lanes run on)
+                main.wait_stream(ln.stream)
             gev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timing else None
-            self._geometry(batch, gev)
+            self._geometry(batch, s0, gev)
+            done = torch.cuda.Event()
+            done.record(main)
+            geo_done[bi % n_sets] = done
             if timing:
                 gevs.append(gev)
         self.stage_events = (evs, gevs)
@@ -347,9 +389,11 @@ class MultiViewStep:
 
     def check(self):
         """One host read per step: capacity overflow and non-finite status."""
-        flags = torch.stack([self.planes[0].t["n_items"][1].to(torch.int64), self.status[0].to(torch.int64),
-                             self.replay.cursor[1]])
-        ov0, bad, ov_replay = flags.cpu().tolist()
+        flags = torch.stack([self.status[0].to(torch.int64)] +
+                            [ln.plane.t["n_items"][1].to(torch.int64) for ln in self.lanes] +
+                            [ln.replay.cursor[1] for ln in self.lanes])
+        f = flags.cpu().tolist()
+        bad, ov0, ov_replay = f[0], any(f[1:1 + self.n_lanes]), any(f[1 + self.n_lanes:])
         if ov0 or ov_replay:
             raise OverflowError("pair capacity exceeded; recalibrate")
         if bad:
