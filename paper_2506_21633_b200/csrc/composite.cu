@@ -474,33 +474,45 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
 #pragma unroll
         for (int w = 0; w < 4; ++w)
           lm[w] = gm[w] & ((uint64_t)alive_bits[2 * w] | ((uint64_t)alive_bits[2 * w + 1] << 32));
-        const int cnt_g = (have && tid >= j0)
-                              ? __popcll(lm[0]) + __popcll(lm[1]) + __popcll(lm[2]) + __popcll(lm[3])
-                              : 0;
-        int tot_g;
-        const int excl_g = block_scan(cnt_g, scan_tmp, tot_g);
-        if (tot_g == 0) break;  // no live pair left in this chunk
-        if (tid == j0) base_s = excl_g;
-        __syncthreads();
-        const bool fits = have && tid >= j0 && (excl_g + cnt_g - base_s) <= kCap;
-        const int j1 = j0 + __syncthreads_count(fits);
-        WPROF(4);
-        // ---- P1: per-ray counts of members in [j0, j1), flat offsets
+        // ---- P1: per-ray counts of the members in [j0, j1), flat offsets.
+        //      Common case: everything left in the chunk fits the flat array
+        //      (j1 = nG, one scan); otherwise the chunk is cut by Gaussians.
         int cnt_r = 0;
         uint32_t pre_lo = 0, pre_hi = 0;
-        if (alive) {
+        auto ray_counts = [&](int jb) {
+          cnt_r = 0;
+          pre_lo = pre_hi = 0;
+          if (alive) {
 #pragma unroll
-          for (int w = 0; w < 8; ++w) {
-            const int c = __popc(rows[w * kRays + tid] & range_mask(w, j0, j1));
-            if (w < 4) pre_lo |= (uint32_t)cnt_r << (8 * w);
-            else pre_hi |= (uint32_t)cnt_r << (8 * (w - 4));
-            cnt_r += c;
+            for (int w = 0; w < 8; ++w) {
+              const int c = __popc(rows[w * kRays + tid] & range_mask(w, j0, jb));
+              if (w < 4) pre_lo |= (uint32_t)cnt_r << (8 * w);
+              else pre_hi |= (uint32_t)cnt_r << (8 * (w - 4));
+              cnt_r += c;
+            }
           }
+        };
+        int j1 = nG;
+        ray_counts(j1);
+        int total;
+        int roff = block_scan(cnt_r, scan_tmp, total);
+        if (total == 0) break;  // no live pair left in this chunk
+        if (total > kCap) {     // block-uniform
+          const int cnt_g = (have && tid >= j0)
+                                ? __popcll(lm[0]) + __popcll(lm[1]) + __popcll(lm[2]) + __popcll(lm[3])
+                                : 0;
+          int tot_g;
+          const int excl_g = block_scan(cnt_g, scan_tmp, tot_g);
+          if (tid == j0) base_s = excl_g;
+          __syncthreads();
+          const bool fits = have && tid >= j0 && (excl_g + cnt_g - base_s) <= kCap;
+          j1 = j0 + __syncthreads_count(fits);
+          ray_counts(j1);
+          roff = block_scan(cnt_r, scan_tmp, total);
         }
+        WPROF(4);
         wpre[tid] = pre_lo;
         wpre[kRays + tid] = pre_hi;
-        int total;
-        const int roff = block_scan(cnt_r, scan_tmp, total);
         ray_off[tid] = roff;
         // replay space for this sub-chunk: the atomic's round trip overlaps P2/P3
         unsigned long long rp_o = 0;
