@@ -305,20 +305,26 @@ def run_sdgr(args):
     for _ in range(max(args.warmup, 3)):
         step.run(dlds)
     torch.cuda.synchronize()
-    # one instrumented (untimed) step: per-kernel device time -> the dominant
-    # kernel; per-view live pairs and work items for its byte count
+    # one instrumented (untimed) single-stream step: per-kernel device time ->
+    # the dominant kernel; per-view live pairs and work items for its bytes
     lib.sdgr_profile_begin(sum(1 << k for k in L.KERNEL_NAMES))
     vstats = []
-    step.run(dlds, stats=vstats)
+    step.run(dlds, stats=vstats, lanes=1)
     prof_ms, prof_cnt = _profile(lib)
     st = torch.stack(vstats).double().mean(0).tolist()
     live_pv, items_pv = st[0], st[1]
     dom = max(L.KERNEL_NAMES, key=lambda k: prof_ms[k])
-    torch.cuda.synchronize()
-    barrier()
-    # the step is captured once as a CUDA graph (static scene / dL/dS buffers);
-    # event nodes bracket the dominant kernel's launches inside it
+    # roofline timing: a single-stream graph of the step with event nodes
+    # around the dominant kernel's launches.  (In the concurrent step below a
+    # kernel's events also span the time its blocks wait for SM slots held by
+    # other streams' kernels, so they would not be launch durations.)
     lib.sdgr_profile_begin(1 << dom)
+    step.capture(dlds, warm=False, lanes=1)
+    for _ in range(max(args.steps, 3)):
+        step.graph_step()
+    torch.cuda.synchronize()
+    dom_ms, dom_cnt = _profile(lib)   # the last replay's launches of the dominant kernel
+    # the timed step: one CUDA graph, views on `lanes` concurrent streams
     launches = step.capture(dlds, warm=False)
     step.graph_step()
     torch.cuda.synchronize()
@@ -334,7 +340,6 @@ def run_sdgr(args):
         e1.record()
         torch.cuda.synchronize()
         barrier()
-    dom_ms, dom_cnt = _profile(lib)   # the last timed replay's launches of the dominant kernel
     step.check()
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], device="cuda")
@@ -342,7 +347,7 @@ def run_sdgr(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     value = world * V / (ms_max / 1e3)
-    step.run(dlds, timing=True, check=False)   # untimed, graph-free: per-stage breakdown
+    step.run(dlds, timing=True, check=False, lanes=1)   # untimed, graph-free, one stream: stage breakdown
     torch.cuda.synchronize()
     stages = step.stage_times_ms()
 
@@ -396,7 +401,8 @@ def run_sdgr(args):
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": L.KERNEL_NAMES[dom], "bytes_per_launch": bpl, "launch_ms": launch_ms,
                 "launches_per_step": dom_per_step,
-                "timing": "CUDA event nodes around each launch inside the captured step graph (last timed replay)",
+                "timing": "CUDA event nodes around each launch inside a single-stream graph of the step "
+                          "(kernel alone on the GPU; last of the replays)",
                 "share_of_instrumented_kernels": prof_ms[dom] / step_ms_all if step_ms_all else None,
                 "kernel_ms_per_step": {L.KERNEL_NAMES[k]: round(prof_ms[k], 3) for k in L.KERNEL_NAMES},
                 "per_view": {"t16": t16_pv, "live_pairs": live_pv, "items": items_pv},
@@ -414,7 +420,7 @@ def run_sdgr(args):
                    "execution": f"one CUDA graph per step, views on {step.n_lanes} concurrent streams",
                    "t16_per_view": step.calib_t16_mean},
         "roofline": roofline,
-        "stage_ms_per_step": stages,
+        "stage_ms_per_step_single_stream": stages,
         "gpu_launches": int(launches),
         "e2e": e2e,
         "clocks": clk.summary(),

@@ -239,15 +239,17 @@ class MultiViewStep:
         return mx
 
     # -- one view -----------------------------------------------------------
-    def _view(self, v, dlds: torch.Tensor, slot: int, ev=None):
+    def _view(self, v, dlds: torch.Tensor, slot: int, ev=None, ln=None):
         """K1-K9 of one view into batch slot `slot` (the geometry epilogue runs
-        per batch), on the current stream with lane slot % lanes's buffers."""
+        per batch), on the current stream with lane `ln`'s working buffers."""
         lib, st = self.lib, _stream()
-        ln = self._lane_of(slot)
+        ln = ln if ln is not None else self._lane_of(slot)
         pd = C.byref(self.pds[slot])
         P0 = ln.plane
         t0 = P0.t
-        tiles = C.byref(self.slot_tiles[slot])
+        td = _lib.TilesDesc.from_buffer_copy(ln.plane.tiles)   # the lane's pair buffers,
+        td.pair_start = self.slot_tiles[slot].pair_start        # the slot's record slots
+        tiles = C.byref(td)
         acc = self.acc_imgs[slot]
 
         def mark(i):
@@ -281,8 +283,8 @@ class MultiViewStep:
                "sdgr_grad_intensity")
         mark(7)
 
-    def _lane_of(self, slot: int):
-        return self.lanes[(slot % self.geo_batch) % self.n_lanes]
+    def _lane_of(self, slot: int, n_lanes: int | None = None):
+        return self.lanes[(slot % self.geo_batch) % (n_lanes or self.n_lanes)]
 
     def _geometry(self, views, s0: int = 0, ev=None):
         """Batched K10 over the views held in slots s0..s0+len(views)-1."""
@@ -301,11 +303,12 @@ class MultiViewStep:
             ev[1].record()
 
     def run(self, dlds: torch.Tensor, timing: bool = False, check: bool = True, stats: list | None = None,
-            allreduce: bool = True):
+            allreduce: bool = True, lanes: int | None = None):
         """Forward + backward of every view; dlds: (V, H, W) float64 on device.
         Returns the accumulated SceneGradients (all-reduced if distributed).
         stats: if a list, one device tensor per view is appended holding
-        (live pairs logged by the forward, work items) -- no host sync."""
+        (live pairs logged by the forward, work items) -- no host sync.
+        lanes: use only the first `lanes` view streams (default: all)."""
         if self.cap is None:
             self.calibrate()
         if dlds.shape[0] != len(self.views):
@@ -321,31 +324,38 @@ class MultiViewStep:
         main = torch.cuda.current_stream()
         start = torch.cuda.Event()
         start.record(main)             # lanes start after the zeroing above
-        for ln in self.lanes:
+        L = max(1, min(int(lanes or self.n_lanes), self.n_lanes))
+        active = self.lanes[:L]
+        for ln in active:
             ln.stream.wait_event(start)
         geo_done = [None] * n_sets     # geometry that last read each slot set
+        geo_last = None
         for bi, b0 in enumerate(range(0, len(self.views), B)):
             batch = self.views[b0:b0 + B]
             s0 = (bi % n_sets) * B
-            if geo_done[bi % n_sets] is not None:
-                for ln in self.lanes:
-                    ln.stream.wait_event(geo_done[bi % n_sets])
+            # one lane = fully serial (each kernel alone on the GPU: the
+            # single-stream timing mode); otherwise only slot-set reuse waits
+            wait_geo = geo_last if L == 1 else geo_done[bi % n_sets]
+            if wait_geo is not None:
+                for ln in active:
+                    ln.stream.wait_event(wait_geo)
             for k, v in enumerate(batch):
-                ln = self._lane_of(s0 + k)
+                ln = self._lane_of(s0 + k, L)
                 with torch.cuda.stream(ln.stream):
                     ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)] if timing else None
-                    self._view(v, dlds[b0 + k], s0 + k, ev)
+                    self._view(v, dlds[b0 + k], s0 + k, ev, ln)
                     if stats is not None:
                         stats.append(torch.stack([ln.replay.cursor[0], ln.plane.t["n_items"][0].to(torch.int64)]))
                 if timing:
                     evs.append(ev)
-            for ln in self.lanes:      # this batch's views are done (lanes run on)
+            for ln in active:          # this batch's views are done (lanes run on)
                 main.wait_stream(ln.stream)
             gev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timing else None
             self._geometry(batch, s0, gev)
             done = torch.cuda.Event()
             done.record(main)
             geo_done[bi % n_sets] = done
+            geo_last = done
             if timing:
                 gevs.append(gev)
         self.stage_events = (evs, gevs)
@@ -357,7 +367,7 @@ class MultiViewStep:
         return self.grads
 
     # -- CUDA graph of a whole step -------------------------------------------
-    def capture(self, dlds: torch.Tensor, warm: bool = True):
+    def capture(self, dlds: torch.Tensor, warm: bool = True, lanes: int | None = None):
         """Record one step (every view's forward + backward; no all-reduce, no
         host check) as a CUDA graph over static buffers: the scene tensors and
         `dlds` are read where they live, so callers overwrite them in place and
@@ -366,12 +376,12 @@ class MultiViewStep:
         if self.cap is None:
             self.calibrate()
         if warm:
-            self.run(dlds, check=False)   # first-call attributes / occupancy queries happen here
+            self.run(dlds, check=False, lanes=lanes)   # first-call attributes / occupancy queries
         torch.cuda.synchronize()
         n0 = self.lib.sdgr_launch_count()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.run(dlds, check=False, allreduce=False)
+            self.run(dlds, check=False, allreduce=False, lanes=lanes)
         self.graph_launches = int(self.lib.sdgr_launch_count() - n0)
         return self.graph_launches
 
