@@ -293,6 +293,26 @@ int sdgr_grad_geometry_batch(const sdgr_scene* scene, int n_views, const sdgr_vi
                              const double* const* acc_imgs, const double* const* partial_gs,
                              sdgr_grads* out, int accumulate, void* stream);
 
+/* ----------------------------------- training step -- */
+/* optimize.loss (optimize.py:85-102): value = (1-l) mean|S-Y| + l (1 - SSIM(S,Y))
+ * and dL_dS (h, w) FP64, SSIM with its analytic gradient (metrics.py:98-137):
+ * 11x11 separable Gaussian window (sigma 1.5, `kernel11` = its 11 normalised
+ * taps in HOST memory, zero padded), interior mean; images smaller than the
+ * window use one global window.  value: device FP64 scalar.  scratch:
+ * sdgr_loss_scratch_bytes(h, w).  lambda_ssim in [0, 1]. */
+size_t sdgr_loss_scratch_bytes(int h, int w);
+int sdgr_loss(const double* S, const double* Y, int h, int w, double lambda_ssim, double max_val,
+              const double* kernel11, double* value, double* dL_dS, void* scratch, void* stream);
+/* optimize.adam_step (optimize.py:171-207), in place on `scene`; `m` and `v`
+ * are scenes of the same dtype/shape holding the moment buffers; grads are the
+ * FP32 SceneGradients.  lr[5] per group (positions, rotations, log_scales,
+ * sh_coeffs, ke_raw); bc1 = 1 - beta1^step, bc2 = 1 - beta2^step computed by
+ * the caller; displacement_bound <= 0 disables the clamp.  Non-finite
+ * gradient entries are zeroed and added to *n_skipped (device u64). */
+int sdgr_adam_step(sdgr_scene* scene, const sdgr_grads* grads, sdgr_scene* m, sdgr_scene* v,
+                   const double* lr, double beta1, double beta2, double eps, double bc1, double bc2,
+                   double displacement_bound, unsigned long long* n_skipped, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

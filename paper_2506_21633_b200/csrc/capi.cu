@@ -68,6 +68,12 @@ int launch_grad_intensity(const sdgr_view&, const sdgr_projection&, const sdgr_t
                           const double*, const double*, double*, double*, double*, const sdgr_replay*,
                           cudaStream_t);
 
+size_t loss_scratch_bytes(int, int);
+int launch_loss(const double*, const double*, int, int, double, double, const double*, double*, double*, void*,
+                cudaStream_t);
+int launch_adam(const sdgr_scene&, const sdgr_grads&, const sdgr_scene&, const sdgr_scene&, const double*, double,
+                double, double, double, double, double, unsigned long long*, cudaStream_t);
+
 static bool replay_ok(const sdgr_replay* r) {
   return !r || (r->y1 && r->t2 && r->w && r->j && r->r && r->desc && r->desc_count && r->cursor && r->gpair && r->capacity > 0 &&
                 r->desc_per_item > 0);
@@ -231,6 +237,35 @@ int sdgr_grad_geometry_batch(const sdgr_scene* scene, int n_views, const sdgr_vi
   }
   return launch_grad_geometry(*scene, n_views, views, projs, comps, acc_imgs, partial_gs, *out, accumulate,
                               static_cast<cudaStream_t>(stream));
+}
+
+size_t sdgr_loss_scratch_bytes(int h, int w) { return h > 0 && w > 0 ? loss_scratch_bytes(h, w) : 0; }
+
+int sdgr_loss(const double* S, const double* Y, int h, int w, double lambda_ssim, double max_val,
+              const double* kernel11, double* value, double* dL_dS, void* scratch, void* stream) {
+  if (!S || !Y || !value || !dL_dS || !scratch || h < 1 || w < 1) return SDGR_ERR_INVALID;
+  if (!(lambda_ssim >= 0.0 && lambda_ssim <= 1.0) || !(max_val > 0.0)) return SDGR_ERR_INVALID;
+  if (lambda_ssim > 0.0 && h >= 11 && w >= 11 && !kernel11) return SDGR_ERR_INVALID;
+  return launch_loss(S, Y, h, w, lambda_ssim, max_val, kernel11, value, dL_dS, scratch,
+                     static_cast<cudaStream_t>(stream));
+}
+
+static bool scene_ok(const sdgr_scene* s) {
+  return s && s->n >= 1 && (s->dtype == 0 || s->dtype == 1) && s->positions && s->rotations && s->log_scales &&
+         s->sh_coeffs && s->ke_raw;
+}
+
+int sdgr_adam_step(sdgr_scene* scene, const sdgr_grads* grads, sdgr_scene* m, sdgr_scene* v, const double* lr,
+                   double beta1, double beta2, double eps, double bc1, double bc2, double displacement_bound,
+                   unsigned long long* n_skipped, void* stream) {
+  if (!scene_ok(scene) || !scene_ok(m) || !scene_ok(v) || !grads || !lr || !n_skipped) return SDGR_ERR_INVALID;
+  if (m->n != scene->n || v->n != scene->n || m->dtype != scene->dtype || v->dtype != scene->dtype)
+    return SDGR_ERR_STATE;
+  if (!grads->positions || !grads->rotations || !grads->log_scales || !grads->sh_coeffs || !grads->ke_raw)
+    return SDGR_ERR_INVALID;
+  if (!(bc1 > 0.0) || !(bc2 > 0.0)) return SDGR_ERR_INVALID;
+  return launch_adam(*scene, *grads, *m, *v, lr, beta1, beta2, eps, bc1, bc2, displacement_bound, n_skipped,
+                     static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

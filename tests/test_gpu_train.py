@@ -1,0 +1,97 @@
+"""Device loss / SSIM gradient / Adam (csrc/train.cu) vs the reference's own
+outputs (tests/golden/train, made by tests/golden/make_golden_train.py) and the
+oracle restatement (oracle/train_oracle.py)."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import assert_close
+from oracle import train_oracle as T
+
+pytestmark = pytest.mark.gpu
+
+TRAIN = Path(__file__).resolve().parent / "golden" / "train"
+LOSS = sorted(TRAIN.glob("loss_*.npz"))
+ADAM = sorted(TRAIN.glob("adam_*.npz"))
+
+
+@pytest.mark.parametrize("path", LOSS, ids=[p.stem for p in LOSS])
+def test_device_loss_matches_reference(path):
+    from paper_2506_21633_b200 import train
+
+    z = np.load(path)
+    value, grad = train.loss(z["S"], z["Y"], float(z["lam"]), float(z["max_val"]))
+    assert abs(value - float(z["value"])) <= 1e-12 * max(1.0, abs(float(z["value"]))), (value, float(z["value"]))
+    assert_close(grad, z["grad"], atol=1e-15, rtol=1e-10, what="dL/dS")
+
+
+def test_device_loss_stays_on_device_and_is_deterministic():
+    from paper_2506_21633_b200 import train
+
+    g = torch.Generator("cuda").manual_seed(2)
+    S = torch.rand((96, 80), dtype=torch.float64, device="cuda", generator=g)
+    Y = torch.rand((96, 80), dtype=torch.float64, device="cuda", generator=g)
+    buf = train.LossBuffers(96, 80)
+    v1, g1 = train.loss(S, Y, 0.2, 1.0, buffers=buf)
+    v2, g2 = train.loss(S, Y, 0.2, 1.0, buffers=buf)
+    assert v1.is_cuda and g1.is_cuda
+    assert torch.equal(v1, v2) and torch.equal(g1, g2)
+    ov, og = T.loss(S.cpu().numpy(), Y.cpu().numpy(), 0.2, 1.0)
+    assert abs(float(v1) - ov) <= 1e-12
+    assert_close(g1.cpu().numpy(), og, atol=1e-15, rtol=1e-10, what="dL/dS")
+
+
+def _grads(z, k, n):
+    from paper_2506_21633_b200.rasterizer import SceneGradients
+
+    f = lambda g: torch.from_numpy(z[f"g{k}_{g}"].astype(np.float32)).cuda()  # noqa: E731
+    return SceneGradients(f("positions"), f("rotations"), f("log_scales"), f("sh_coeffs"), f("ke_raw"),
+                          torch.zeros(n, dtype=torch.float32, device="cuda"),
+                          torch.ones(n, dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("path", ADAM, ids=[p.stem for p in ADAM])
+def test_device_adam_fp64_matches_reference(path):
+    from paper_2506_21633_b200 import train
+    from paper_2506_21633_b200.scene import DeviceScene
+
+    z = np.load(path)
+    scene = DeviceScene(*(torch.from_numpy(z[f"p0_{g}"].copy()).cuda() for g in T.GROUPS))
+    state = train.AdamState.for_scene(scene)
+    lrs = dict(zip(T.GROUPS, z["lrs"]))
+    bound = float(z["bound"])
+    n = len(scene)
+    for k in range(2):
+        train.adam_step(scene, _grads(z, k, n), state, lrs, None if bound < 0 else bound)
+        for g in T.GROUPS:
+            assert_close(getattr(scene, g).cpu().numpy(), z[f"p{k + 1}_{g}"], atol=0.0, rtol=1e-15, what=g)
+            assert_close(getattr(state.m, g).cpu().numpy(), z[f"m{k + 1}_{g}"], atol=0.0, rtol=1e-15, what=g)
+            assert_close(getattr(state.v, g).cpu().numpy(), z[f"v{k + 1}_{g}"], atol=0.0, rtol=1e-15, what=g)
+    assert state.n_skipped == int(z["n_skipped"])
+
+
+def test_device_adam_fp32_scene_vs_oracle():
+    from paper_2506_21633_b200 import train
+    from paper_2506_21633_b200.scene import DeviceScene
+
+    z = np.load(ADAM[0])
+    p0 = {g: z[f"p0_{g}"].astype(np.float32).astype(np.float64) for g in T.GROUPS}
+    scene = DeviceScene(*(torch.from_numpy(p0[g].astype(np.float32)).cuda() for g in T.GROUPS))
+    state = train.AdamState.for_scene(scene)
+    lrs = dict(zip(T.GROUPS, z["lrs"]))
+    params = {g: p0[g].copy() for g in T.GROUPS}
+    m = {g: np.zeros_like(params[g]) for g in T.GROUPS}
+    v = {g: np.zeros_like(params[g]) for g in T.GROUPS}
+    step = 0
+    for k in range(2):
+        train.adam_step(scene, _grads(z, k, len(scene)), state, lrs)
+        step, _ = T.adam_step(params, {g: z[f"g{k}_{g}"] for g in T.GROUPS}, m, v, step, lrs)
+        # the device keeps FP32 parameters and moments between steps
+        for g in T.GROUPS:
+            params[g] = params[g].astype(np.float32).astype(np.float64)
+            m[g] = m[g].astype(np.float32).astype(np.float64)
+            v[g] = v[g].astype(np.float32).astype(np.float64)
+    for g in T.GROUPS:
+        assert_close(getattr(scene, g).double().cpu().numpy(), params[g], atol=1e-6, rtol=1e-5, what=g)
