@@ -71,7 +71,8 @@ class MultiViewStep:
 
     def __init__(self, scene: DeviceScene, configs, cov_reg: float = DEFAULT_COV_REG,
                  cutoff: float = DEFAULT_CUTOFF, s_stop: float = S_STOP, headroom: float = 1.3,
-                 group=None, geo_batch: int = _lib.MAX_BATCH, lanes: int = 4):
+                 group=None, geo_batch: int = _lib.MAX_BATCH, lanes: int = 4, targets: torch.Tensor | None = None,
+                 lambda_ssim: float = 0.2, max_val: float = 1.0):
         self.scene = scene
         self.configs = list(configs)
         self.views = [view_constants(c, cov_reg, cutoff) for c in self.configs]
@@ -97,6 +98,18 @@ class MultiViewStep:
         self.n_lanes = max(1, min(int(lanes), self.geo_batch))
         self.lanes = [self._lane() for _ in range(self.n_lanes)]
         self.counters, self.member_pairs = self.lanes[0].counters, self.lanes[0].member_pairs
+        # training mode: each view's dL/dS comes from the device loss against
+        # its target image (optimize.loss), written into the run's dlds buffer
+        self.targets = None
+        if targets is not None:
+            if tuple(targets.shape) != (len(self.views),) + self.img_shape:
+                raise ValueError("targets must be (V, n_range, n_azimuth)")
+            from .train import LossBuffers
+            self.targets = targets.to(device=dev, dtype=torch.float64).contiguous()
+            self.lambda_ssim, self.max_val = float(lambda_ssim), float(max_val)
+            self.loss_values = torch.zeros((len(self.views),), dtype=torch.float64, device=dev)
+            for ln in self.lanes:
+                ln.loss = LossBuffers(*self.img_shape, device=dev)
         # two slot sets: batch b's geometry overlaps batch b+1's views
         self.n_slots = 2 * self.geo_batch if len(self.views) > self.geo_batch else self.geo_batch
         self.proj_bufs = [self._projection_bufs(self._lane_of(k)) for k in range(self.n_slots)]
@@ -239,7 +252,7 @@ class MultiViewStep:
         return mx
 
     # -- one view -----------------------------------------------------------
-    def _view(self, v, dlds: torch.Tensor, slot: int, ev=None, ln=None):
+    def _view(self, v, dlds: torch.Tensor, slot: int, ev=None, ln=None, vi: int = 0):
         """K1-K9 of one view into batch slot `slot` (the geometry epilogue runs
         per batch), on the current stream with lane `ln`'s working buffers."""
         lib, st = self.lib, _stream()
@@ -272,6 +285,11 @@ class MultiViewStep:
         mark(4)
         _check(lib.sdgr_splat(C.byref(v), pd, ptr(ln.intensity), ptr(ln.splat_scratch), ptr(ln.image), st),
                "sdgr_splat")
+        if self.targets is not None:   # dL/dS of this view from the device loss
+            h, w = self.img_shape
+            _check(lib.sdgr_loss(ptr(ln.image), ptr(self.targets[vi]), h, w, self.lambda_ssim, self.max_val,
+                                 C.cast(ln.loss.kernel, C.c_void_p), ptr(self.loss_values[vi]), ptr(dlds),
+                                 ptr(ln.loss.scratch), st), "sdgr_loss")
         mark(5)
         _check(lib.sdgr_grad_image(C.byref(v), pd, ptr(ln.intensity), ptr(dlds), ptr(acc), st),
                "sdgr_grad_image")
@@ -343,7 +361,7 @@ class MultiViewStep:
                 ln = self._lane_of(s0 + k, L)
                 with torch.cuda.stream(ln.stream):
                     ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)] if timing else None
-                    self._view(v, dlds[b0 + k], s0 + k, ev, ln)
+                    self._view(v, dlds[b0 + k], s0 + k, ev, ln, vi=b0 + k)
                     if stats is not None:
                         stats.append(torch.stack([ln.replay.cursor[0], ln.plane.t["n_items"][0].to(torch.int64)]))
                 if timing:

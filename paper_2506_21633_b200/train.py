@@ -116,3 +116,37 @@ def adam_step(scene: DeviceScene, grads: SceneGradients, state: AdamState, lrs: 
     _check(_lib.lib().sdgr_adam_step(C.byref(sd), C.byref(gd), C.byref(md), C.byref(vd), lr, float(b1), float(b2),
                                      float(state.eps), bc1, bc2, bound, ptr(state.skipped), _stream()),
            "sdgr_adam_step")
+
+
+class TrainStep:
+    """One optimiser step over a set of views, entirely on the device: for
+    every view render -> loss vs its target -> backward (MultiViewStep with
+    targets), the gradient sum (all-reduced across ranks when distributed),
+    the SH-degree mask, and Adam -- the multi-view form of the body of
+    optimize.train (optimize.py:395-425; one view per step there).  The view
+    work is one CUDA graph per step; Adam is one more kernel."""
+
+    def __init__(self, scene: DeviceScene, configs, targets: torch.Tensor, lambda_ssim: float = 0.2,
+                 max_val: float = 1.0, **kw):
+        from .multiview import MultiViewStep
+        self.scene = scene
+        self.mv = MultiViewStep(scene, configs, targets=targets, lambda_ssim=lambda_ssim, max_val=max_val, **kw)
+        self.dlds = torch.zeros(targets.shape, dtype=torch.float64, device=scene.device)
+        self.state = AdamState.for_scene(scene)
+        self.graph = False
+
+    def __call__(self, lrs: dict, sh_active: int = 16, displacement_bound: float | None = None,
+                 use_graph: bool = True) -> torch.Tensor:
+        """Returns the per-view loss values (device tensor, before the update)."""
+        if use_graph:
+            if not self.graph:
+                self.mv.capture(self.dlds)
+                self.graph = True
+            self.mv.graph_step()
+        else:
+            self.mv.run(self.dlds, check=False)
+        g = self.mv.grads
+        if sh_active < 16:
+            g.sh_coeffs[:, sh_active:] = 0.0   # optimize.py:412-413
+        adam_step(self.scene, g, self.state, lrs, displacement_bound)
+        return self.mv.loss_values

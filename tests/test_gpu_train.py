@@ -95,3 +95,47 @@ def test_device_adam_fp32_scene_vs_oracle():
             v[g] = v[g].astype(np.float32).astype(np.float64)
     for g in T.GROUPS:
         assert_close(getattr(scene, g).double().cpu().numpy(), params[g], atol=1e-6, rtol=1e-5, what=g)
+
+
+def _toy_problem(n_views=3, size=64):
+    import paper_2506_21633_b200 as sdgr
+    from paper_2506_21633_b200 import targets
+    from paper_2506_21633_b200.scene import DeviceScene
+
+    tank = targets.to_float32_exact(targets.composite_target(targets.tank_preset(), [1500, 800, 300], seed=8))
+    cfgs = [sdgr.RadarConfig(azimuth_deg=az, elevation_deg=45.0, altitude_m=0.5, n_range=size, n_azimuth=size)
+            for az in np.linspace(0.0, 240.0, n_views)]
+    truth = DeviceScene.from_host(tank, dtype=torch.float64)
+    tg = torch.stack([torch.as_tensor(sdgr.render(truth, c)).cuda() for c in cfgs]).double()
+    start = DeviceScene.from_host(tank, dtype=torch.float64)
+    g = torch.Generator("cuda").manual_seed(1)
+    start.positions += 0.05 * torch.randn(start.positions.shape, dtype=torch.float64, device="cuda", generator=g)
+    return start, cfgs, tg
+
+
+def test_trainstep_loss_and_dlds_match_standalone_loss():
+    import paper_2506_21633_b200 as sdgr
+    from paper_2506_21633_b200 import train
+
+    scene, cfgs, tg = _toy_problem()
+    ts = train.TrainStep(scene, cfgs, tg, lambda_ssim=0.2, geo_batch=2)
+    ts.mv.run(ts.dlds, check=True)
+    for i, c in enumerate(cfgs):
+        img = torch.as_tensor(sdgr.render(scene, c)).cuda().double()
+        v, gr = train.loss(img, tg[i], 0.2, 1.0)
+        assert abs(float(ts.mv.loss_values[i]) - float(v)) <= 1e-10
+        assert_close(ts.dlds[i].cpu().numpy(), gr.cpu().numpy(), atol=1e-14, rtol=1e-8, what="dL/dS")
+
+
+def test_trainstep_reduces_the_loss():
+    from paper_2506_21633_b200 import train
+
+    scene, cfgs, tg = _toy_problem()
+    ts = train.TrainStep(scene, cfgs, tg, lambda_ssim=0.2, geo_batch=2)
+    lrs = {"positions": 2e-3, "rotations": 1e-3, "log_scales": 5e-3, "sh_coeffs": 2.5e-3, "ke_raw": 5e-2}
+    first = float(ts(lrs).sum())
+    for _ in range(15):
+        last = ts(lrs)
+    ts.mv.check()
+    assert float(last.sum()) < first
+    assert ts.state.step == 16
