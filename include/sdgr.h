@@ -313,6 +313,28 @@ int sdgr_adam_step(sdgr_scene* scene, const sdgr_grads* grads, sdgr_scene* m, sd
                    const double* lr, double beta1, double beta2, double eps, double bc1, double bc2,
                    double displacement_bound, unsigned long long* n_skipped, void* stream);
 
+/* -------------------------------- densification ------ */
+/* optimize.densify_and_prune (optimize.py:251-312) and GradAccumulator
+ * (:217-239) as device passes; the caller gathers rows with the index lists
+ * the flags define, and draws the split samples xi from its own seeded
+ * generator (rng.normal(size=(2 * n_split, 3)), as the reference does). */
+/* norm_sum += uv_grad_norm, pos_sum (n,3) += positions, count += visible for
+ * rows with visible > 0 (visible = views that saw the Gaussian). FP64. */
+int sdgr_accum_update(const sdgr_grads* grads, int64_t n, double* norm_sum, double* pos_sum,
+                      double* count, void* stream);
+/* flags[g] = 2 split (max e^s > cap), 1 clone (mean norm > grad_thr, small,
+ * seen), 0 keep.  small: max e^s <= small_size. */
+int sdgr_densify_flags(const sdgr_scene* scene, const double* norm_sum, const double* count, double cap,
+                       double small_size, double grad_thr, uint8_t* flags, void* stream);
+/* in place on gathered clone rows: positions += -position_lr * pos_sum / max(count, 1) */
+int sdgr_clone_shift(sdgr_scene* clones, const double* pos_sum, const double* count, double position_lr,
+                     void* stream);
+/* in place on gathered child rows (each parent twice): positions += chol(Sigma) xi (xi: (n,3) FP64),
+ * log_scales -= log_shrink */
+int sdgr_split_children(sdgr_scene* children, const double* xi, double log_shrink, void* stream);
+/* survive[g] = DC phase (sh_0 * SH_C0) >= phase_floor and max e^s <= cap */
+int sdgr_prune_flags(const sdgr_scene* scene, double cap, double phase_floor, uint8_t* survive, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

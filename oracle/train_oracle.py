@@ -6,6 +6,7 @@ Follows the reference line by line:
   ssim_with_grad  metrics.py:98-137 (_ssim_kernel :45-49, _ssim_filter :52-55,
                   _ssim_terms :58-76)
   adam_step       optimize.py:171-207
+  densify_and_prune optimize.py:251-312 (covariances: scene.py:49-97)
 Pinned by tests/test_train_oracle.py against tests/golden/train/*.npz, which
 tests/golden/make_golden_train.py produced by running the reference itself.
 The separable filter is restated with explicit zero padding instead of
@@ -142,3 +143,68 @@ def adam_step(params, grads, m, v, step, lrs, displacement_bound=None, b1=0.9, b
         params[g] -= st
     params["rotations"] /= np.linalg.norm(params["rotations"], axis=1, keepdims=True)
     return step, skipped
+
+
+def covariances(rotations, log_scales):
+    # scene.py:49-97 (quats_to_rotation_matrices + covariances_from_arrays)
+    q = rotations / np.linalg.norm(rotations, axis=-1, keepdims=True)
+    w, x, y, z = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
+    R = np.empty((len(q), 3, 3))
+    R[:, 0, 0] = 1 - 2 * (y * y + z * z)
+    R[:, 0, 1] = 2 * (x * y - w * z)
+    R[:, 0, 2] = 2 * (x * z + w * y)
+    R[:, 1, 0] = 2 * (x * y + w * z)
+    R[:, 1, 1] = 1 - 2 * (x * x + z * z)
+    R[:, 1, 2] = 2 * (y * z - w * x)
+    R[:, 2, 0] = 2 * (x * z - w * y)
+    R[:, 2, 1] = 2 * (y * z + w * x)
+    R[:, 2, 2] = 1 - 2 * (x * x + y * y)
+    M = R * np.exp(log_scales)[:, None, :]
+    cov = M @ np.swapaxes(M, -1, -2)
+    return 0.5 * (cov + np.swapaxes(cov, -1, -2))
+
+
+SH_C0 = 0.28209479177387814
+
+
+def densify_and_prune(params, norm_sum, pos_sum, count, cfg, ground_extent, extent, lr, rng, m=None, v=None):
+    """optimize.py:251-312 on dicts of float64 arrays.  cfg = (grad_threshold,
+    max_radius_factor, clone_size_factor, prune_phase_floor, split_scale_shrink).
+    Returns (new params, (n_cloned, n_split, n_pruned, n_after), new m, new v)."""
+    thr, radius_factor, clone_factor, floor, shrink = cfg
+    cap = radius_factor * ground_extent
+    max_scale = np.exp(params["log_scales"]).max(axis=1)
+    split = max_scale > cap
+    small = max_scale <= clone_factor * extent
+    mean_norm = norm_sum / np.maximum(count, 1.0)
+    clone = (mean_norm > thr) & small & ~split & (count > 0)
+    kept = ~split
+    parts = [{g: params[g][kept] for g in GROUPS}]
+    n_clone = int(clone.sum())
+    if n_clone:
+        c = {g: params[g][clone] for g in GROUPS}
+        c["positions"] = c["positions"] + (-lr * (pos_sum / np.maximum(count, 1.0)[:, None])[clone])
+        parts.append(c)
+    n_split = int(split.sum())
+    if n_split:
+        rows = np.repeat(np.flatnonzero(split), 2)
+        ch = {g: params[g][rows] for g in GROUPS}
+        chol = np.linalg.cholesky(covariances(ch["rotations"], ch["log_scales"]))
+        xi = rng.normal(size=(len(rows), 3))
+        ch["positions"] = ch["positions"] + np.einsum("kab,kb->ka", chol, xi)
+        ch["log_scales"] = ch["log_scales"] - np.log(shrink)
+        parts.append(ch)
+    merged = {g: np.concatenate([p[g] for p in parts]) for g in GROUPS}
+    dc_phase = merged["sh_coeffs"][:, 0] * SH_C0
+    oversized = np.exp(merged["log_scales"]).max(axis=1) > cap
+    survive = (dc_phase >= floor) & ~oversized
+    out = {g: merged[g][survive] for g in GROUPS}
+    new_m = new_v = None
+    if m is not None:
+        n_new = n_clone + 2 * n_split
+
+        def reidx(d):
+            return {g: np.concatenate([d[g][kept], np.zeros((n_new,) + d[g].shape[1:])])[survive] for g in GROUPS}
+        new_m, new_v = reidx(m), reidx(v)
+    event = (n_clone, n_split, int((~survive).sum()), int(survive.sum()))
+    return out, event, new_m, new_v

@@ -115,6 +115,11 @@ SIGNATURES = [
     ("sdgr_grad_geometry_batch", C.c_int, [C.POINTER(SceneDesc), C.c_int, C.POINTER(View),
                                            C.POINTER(ProjectionDesc), C.POINTER(TilesDesc), C.POINTER(_p),
                                            C.POINTER(_p), C.POINTER(GradsDesc), C.c_int, _p]),
+    ("sdgr_accum_update", C.c_int, [C.POINTER(GradsDesc), C.c_int64, _p, _p, _p, _p]),
+    ("sdgr_densify_flags", C.c_int, [C.POINTER(SceneDesc), _p, _p, C.c_double, C.c_double, C.c_double, _p, _p]),
+    ("sdgr_clone_shift", C.c_int, [C.POINTER(SceneDesc), _p, _p, C.c_double, _p]),
+    ("sdgr_split_children", C.c_int, [C.POINTER(SceneDesc), _p, C.c_double, _p]),
+    ("sdgr_prune_flags", C.c_int, [C.POINTER(SceneDesc), C.c_double, C.c_double, _p, _p]),
     ("sdgr_loss_scratch_bytes", C.c_size_t, [C.c_int, C.c_int]),
     ("sdgr_loss", C.c_int, [_p, _p, C.c_int, C.c_int, C.c_double, C.c_double, _p, _p, _p, _p, _p]),
     ("sdgr_adam_step", C.c_int, [C.POINTER(SceneDesc), C.POINTER(GradsDesc), C.POINTER(SceneDesc),

@@ -74,6 +74,13 @@ int launch_loss(const double*, const double*, int, int, double, double, const do
 int launch_adam(const sdgr_scene&, const sdgr_grads&, const sdgr_scene&, const sdgr_scene&, const double*, double,
                 double, double, double, double, double, unsigned long long*, cudaStream_t);
 
+int launch_accum_update(const sdgr_grads&, int64_t, double*, double*, double*, cudaStream_t);
+int launch_densify_flags(const sdgr_scene&, const double*, const double*, double, double, double, uint8_t*,
+                         cudaStream_t);
+int launch_clone_shift(const sdgr_scene&, const double*, const double*, double, cudaStream_t);
+int launch_split_children(const sdgr_scene&, const double*, double, cudaStream_t);
+int launch_prune_flags(const sdgr_scene&, double, double, double, uint8_t*, cudaStream_t);
+
 static bool replay_ok(const sdgr_replay* r) {
   return !r || (r->y1 && r->t2 && r->w && r->j && r->r && r->desc && r->desc_count && r->cursor && r->gpair && r->capacity > 0 &&
                 r->desc_per_item > 0);
@@ -266,6 +273,43 @@ int sdgr_adam_step(sdgr_scene* scene, const sdgr_grads* grads, sdgr_scene* m, sd
   if (!(bc1 > 0.0) || !(bc2 > 0.0)) return SDGR_ERR_INVALID;
   return launch_adam(*scene, *grads, *m, *v, lr, beta1, beta2, eps, bc1, bc2, displacement_bound, n_skipped,
                      static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_accum_update(const sdgr_grads* grads, int64_t n, double* norm_sum, double* pos_sum, double* count,
+                      void* stream) {
+  if (!grads || n < 0 || !norm_sum || !pos_sum || !count || !grads->positions || !grads->uv_grad_norm ||
+      !grads->visible)
+    return SDGR_ERR_INVALID;
+  if (n == 0) return SDGR_OK;
+  return launch_accum_update(*grads, n, norm_sum, pos_sum, count, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_densify_flags(const sdgr_scene* scene, const double* norm_sum, const double* count, double cap,
+                       double small_size, double grad_thr, uint8_t* flags, void* stream) {
+  if (!scene_ok(scene) || !norm_sum || !count || !flags) return SDGR_ERR_INVALID;
+  return launch_densify_flags(*scene, norm_sum, count, cap, small_size, grad_thr, flags,
+                              static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_clone_shift(sdgr_scene* clones, const double* pos_sum, const double* count, double position_lr,
+                     void* stream) {
+  if (!clones || clones->n < 0 || !pos_sum || !count) return SDGR_ERR_INVALID;
+  if (clones->n == 0) return SDGR_OK;
+  if (!scene_ok(clones)) return SDGR_ERR_INVALID;
+  return launch_clone_shift(*clones, pos_sum, count, position_lr, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_split_children(sdgr_scene* children, const double* xi, double log_shrink, void* stream) {
+  if (!children || children->n < 0 || !xi) return SDGR_ERR_INVALID;
+  if (children->n == 0) return SDGR_OK;
+  if (!scene_ok(children)) return SDGR_ERR_INVALID;
+  return launch_split_children(*children, xi, log_shrink, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_prune_flags(const sdgr_scene* scene, double cap, double phase_floor, uint8_t* survive, void* stream) {
+  if (!scene_ok(scene) || !survive) return SDGR_ERR_INVALID;
+  return launch_prune_flags(*scene, cap, phase_floor, 0.28209479177387814, survive,
+                            static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -67,12 +67,48 @@ def adam_case(bound):
     return rec
 
 
+def densify_case():
+    """densify_and_prune (optimize.py:251-312) with clones, splits and prunes."""
+    rng = np.random.default_rng(9)
+    scene = random_scene(rng, 300)
+    view = optimize.RadarConfig(azimuth_deg=0.0, elevation_deg=45.0, range_res_m=0.3, n_range=64)  # cap 5.76
+    scene.log_scales[:20] = np.log(rng.uniform(6.0, 9.0, size=(20, 3)))        # oversized -> split
+    scene.log_scales[20:80] = np.log(rng.uniform(0.005, 0.05, size=(60, 3)))   # small -> clone candidates
+    scene.sh_coeffs[280:, 0] = 0.001                                           # weak phase -> pruned
+    n = len(scene)
+    accum = optimize.GradAccumulator.zeros(n)
+    accum.norm_sum[:] = rng.uniform(0.0, 0.02, size=n)
+    accum.pos_sum[:] = rng.normal(0.0, 1.0, size=(n, 3))
+    accum.count[:] = rng.integers(0, 4, size=n).astype(np.float64)
+    state = optimize.AdamState.for_scene(scene)
+    for g in GROUPS:
+        state.m[g][:] = rng.normal(size=state.m[g].shape)
+        state.v[g][:] = rng.uniform(size=state.v[g].shape)
+    cfg = optimize.TrainConfig()
+    rec = {f"in_{g}": getattr(scene, g).copy() for g in GROUPS}
+    rec.update({f"in_m_{g}": state.m[g].copy() for g in GROUPS})
+    rec.update({f"in_v_{g}": state.v[g].copy() for g in GROUPS})
+    rec.update(norm_sum=accum.norm_sum.copy(), pos_sum=accum.pos_sum.copy(), count=accum.count.copy())
+    extent, lr, seed = 10.0, 0.02, 7
+    out, acc2, ev = optimize.densify_and_prune(scene, accum, cfg, view, extent, lr, np.random.default_rng(seed),
+                                               state=state)
+    rec.update({f"out_{g}": getattr(out, g) for g in GROUPS})
+    rec.update({f"out_m_{g}": state.m[g] for g in GROUPS})
+    rec.update({f"out_v_{g}": state.v[g] for g in GROUPS})
+    rec.update(event=np.array([ev.n_cloned, ev.n_split, ev.n_pruned, ev.n_after]), extent=np.float64(extent),
+               lr=np.float64(lr), seed=np.int64(seed), ground_extent=np.float64(view.ground_extent_m),
+               cfg=np.array([cfg.densify_grad_threshold, cfg.max_radius_factor, cfg.clone_size_factor,
+                             cfg.prune_phase_floor, cfg.split_scale_shrink]))
+    return rec
+
+
 def main():
     OUT.mkdir(exist_ok=True)
     for name, d in loss_cases().items():
         np.savez_compressed(OUT / f"loss_{name}.npz", **d)
     np.savez_compressed(OUT / "adam_free.npz", **adam_case(None))
     np.savez_compressed(OUT / "adam_bound.npz", **adam_case(0.004))
+    np.savez_compressed(OUT / "densify.npz", **densify_case())
     print("wrote", sorted(p.name for p in OUT.glob("*.npz")))
 
 

@@ -139,3 +139,50 @@ def test_trainstep_reduces_the_loss():
     ts.mv.check()
     assert float(last.sum()) < first
     assert ts.state.step == 16
+
+
+def test_device_densify_matches_reference():
+    from paper_2506_21633_b200 import densify, train
+    from paper_2506_21633_b200.radar import RadarConfig
+    from paper_2506_21633_b200.scene import DeviceScene
+
+    z = np.load(TRAIN / "densify.npz")
+    scene = DeviceScene(*(torch.from_numpy(z[f"in_{g}"].copy()).cuda() for g in T.GROUPS))
+    state = train.AdamState.for_scene(scene)
+    for g in T.GROUPS:
+        getattr(state.m, g).copy_(torch.from_numpy(z[f"in_m_{g}"]))
+        getattr(state.v, g).copy_(torch.from_numpy(z[f"in_v_{g}"]))
+    acc = densify.GradAccumulator(torch.from_numpy(z["norm_sum"]).cuda(), torch.from_numpy(z["pos_sum"]).cuda(),
+                                  torch.from_numpy(z["count"]).cuda())
+    c = z["cfg"]
+    cfg = densify.DensifyConfig(*map(float, c))
+    view = RadarConfig(azimuth_deg=0.0, elevation_deg=45.0, range_res_m=0.3, n_range=64)
+    assert abs(view.ground_extent_m - float(z["ground_extent"])) == 0.0
+    out, acc2, ev = densify.densify_and_prune(scene, acc, cfg, view, float(z["extent"]), float(z["lr"]),
+                                              np.random.default_rng(int(z["seed"])), state=state)
+    assert (ev.n_cloned, ev.n_split, ev.n_pruned, ev.n_after) == tuple(int(x) for x in z["event"])
+    for g in T.GROUPS:
+        assert_close(getattr(out, g).cpu().numpy(), z[f"out_{g}"], atol=1e-14, rtol=1e-12, what=g)
+        assert np.array_equal(getattr(state.m, g).cpu().numpy(), z[f"out_m_{g}"]), g
+        assert np.array_equal(getattr(state.v, g).cpu().numpy(), z[f"out_v_{g}"]), g
+    assert float(acc2.count.sum()) == 0.0 and acc2.count.shape[0] == ev.n_after
+
+
+def test_device_accumulator_update():
+    from paper_2506_21633_b200 import densify
+    from paper_2506_21633_b200.rasterizer import SceneGradients
+
+    n = 100
+    g = torch.Generator("cuda").manual_seed(3)
+    pos = torch.randn((n, 3), dtype=torch.float32, device="cuda", generator=g)
+    uvn = torch.rand((n,), dtype=torch.float32, device="cuda", generator=g)
+    vis = torch.randint(0, 3, (n,), dtype=torch.int32, device="cuda", generator=g)
+    z = lambda *s: torch.zeros(s, dtype=torch.float32, device="cuda")  # noqa: E731
+    grads = SceneGradients(pos, z(n, 4), z(n, 3), z(n, 16), z(n, 2), uvn, vis)
+    acc = densify.GradAccumulator.zeros(n)
+    acc.update(grads)
+    acc.update(grads)
+    m = (vis > 0).double()
+    assert torch.equal(acc.count, 2 * vis.double())
+    assert torch.allclose(acc.norm_sum, 2 * uvn.double() * m)
+    assert torch.allclose(acc.pos_sum, 2 * pos.double() * m[:, None])

@@ -40,3 +40,17 @@ def test_adam_oracle_matches_reference(path):
             assert np.array_equal(m[g], z[f"m{k + 1}_{g}"]), g
             assert np.array_equal(v[g], z[f"v{k + 1}_{g}"]), g
     assert skipped == int(z["n_skipped"])
+
+
+def test_densify_oracle_matches_reference():
+    z = np.load(TRAIN / "densify.npz")
+    params = {g: z[f"in_{g}"] for g in T.GROUPS}
+    m = {g: z[f"in_m_{g}"] for g in T.GROUPS}
+    v = {g: z[f"in_v_{g}"] for g in T.GROUPS}
+    out, event, nm, nv = T.densify_and_prune(params, z["norm_sum"], z["pos_sum"], z["count"], z["cfg"],
+                                             float(z["ground_extent"]), float(z["extent"]), float(z["lr"]),
+                                             np.random.default_rng(int(z["seed"])), m, v)
+    assert tuple(event) == tuple(z["event"])
+    for g in T.GROUPS:
+        assert np.array_equal(out[g], z[f"out_{g}"]), g
+        assert np.array_equal(nm[g], z[f"out_m_{g}"]) and np.array_equal(nv[g], z[f"out_v_{g}"]), g
