@@ -335,6 +335,16 @@ int sdgr_split_children(sdgr_scene* children, const double* xi, double log_shrin
 /* survive[g] = DC phase (sh_0 * SH_C0) >= phase_floor and max e^s <= cap */
 int sdgr_prune_flags(const sdgr_scene* scene, double cap, double phase_floor, uint8_t* survive, void* stream);
 
+/* ---------------------------- scene checkpoints ---- */
+/* The reference's binary PLY vertex records (ply.py:110-155): per Gaussian 28
+ * little-endian doubles, x y z qw qx qy qz log_scale_xyz sh_0..15 ke_fwd ke_bwd.
+ * pack: scene (f32/f64 SoA) -> out (n * 28 doubles, vertex-major).
+ * unpack: in (n vertices of `stride` doubles) -> scene; col[k] (host, 28
+ * ints) = column of scene property k in a vertex. */
+int sdgr_ply_pack(const sdgr_scene* scene, double* out, void* stream);
+int sdgr_ply_unpack(const double* in, int64_t n, int stride, const int32_t* col, sdgr_scene* scene,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -115,6 +115,8 @@ SIGNATURES = [
     ("sdgr_grad_geometry_batch", C.c_int, [C.POINTER(SceneDesc), C.c_int, C.POINTER(View),
                                            C.POINTER(ProjectionDesc), C.POINTER(TilesDesc), C.POINTER(_p),
                                            C.POINTER(_p), C.POINTER(GradsDesc), C.c_int, _p]),
+    ("sdgr_ply_pack", C.c_int, [C.POINTER(SceneDesc), _p, _p]),
+    ("sdgr_ply_unpack", C.c_int, [_p, C.c_int64, C.c_int, C.POINTER(C.c_int32), C.POINTER(SceneDesc), _p]),
     ("sdgr_accum_update", C.c_int, [C.POINTER(GradsDesc), C.c_int64, _p, _p, _p, _p]),
     ("sdgr_densify_flags", C.c_int, [C.POINTER(SceneDesc), _p, _p, C.c_double, C.c_double, C.c_double, _p, _p]),
     ("sdgr_clone_shift", C.c_int, [C.POINTER(SceneDesc), _p, _p, C.c_double, _p]),

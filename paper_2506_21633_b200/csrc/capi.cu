@@ -81,6 +81,9 @@ int launch_clone_shift(const sdgr_scene&, const double*, const double*, double, 
 int launch_split_children(const sdgr_scene&, const double*, double, cudaStream_t);
 int launch_prune_flags(const sdgr_scene&, double, double, double, uint8_t*, cudaStream_t);
 
+int launch_ply_pack(const sdgr_scene&, double*, cudaStream_t);
+int launch_ply_unpack(const double*, int64_t, int, const int32_t*, const sdgr_scene&, cudaStream_t);
+
 static bool replay_ok(const sdgr_replay* r) {
   return !r || (r->y1 && r->t2 && r->w && r->j && r->r && r->desc && r->desc_count && r->cursor && r->gpair && r->capacity > 0 &&
                 r->desc_per_item > 0);
@@ -310,6 +313,22 @@ int sdgr_prune_flags(const sdgr_scene* scene, double cap, double phase_floor, ui
   if (!scene_ok(scene) || !survive) return SDGR_ERR_INVALID;
   return launch_prune_flags(*scene, cap, phase_floor, 0.28209479177387814, survive,
                             static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_ply_pack(const sdgr_scene* scene, double* out, void* stream) {
+  if (!scene || scene->n < 0 || !out) return SDGR_ERR_INVALID;
+  if (scene->n == 0) return SDGR_OK;
+  if (!scene_ok(scene)) return SDGR_ERR_INVALID;
+  return launch_ply_pack(*scene, out, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_ply_unpack(const double* in, int64_t n, int stride, const int32_t* col, sdgr_scene* scene, void* stream) {
+  if (!scene || !col || n < 0 || stride < 28 || scene->n != n) return SDGR_ERR_INVALID;
+  if (n == 0) return SDGR_OK;
+  if (!in || !scene_ok(scene)) return SDGR_ERR_INVALID;
+  for (int k = 0; k < 28; ++k)
+    if (col[k] < 0 || col[k] >= stride) return SDGR_ERR_INVALID;
+  return launch_ply_unpack(in, n, stride, col, *scene, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"
