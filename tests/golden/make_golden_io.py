@@ -68,3 +68,28 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def make_dataset():
+    """A 3-view dataset written by the reference (imageio.save_image,
+    dataset.save_manifest) and decoded by dataset.load_dataset."""
+    from sarsplat import dataset, imageio
+    d = OUT / "dataset"
+    d.mkdir(exist_ok=True)
+    rng = np.random.default_rng(6)
+    recs = []
+    specs = (("v0.png", "per-image-max", None, "train"), ("v1.pgm", "fixed-max", 2.0, "train"),
+             ("v2.png", "fixed-max", 1.5, "test"))
+    for k, (name, norm, mv, split) in enumerate(specs):
+        img = rng.uniform(0.0, 1.4, size=(24, 20))
+        imageio.save_image(img, d / name, normalization=norm, max_val=mv)
+        recs.append(dataset.ViewRecord(image=name, azimuth_deg=30.0 * k, elevation_deg=45.0, altitude_m=0.5,
+                                       range_res_m=0.3, azimuth_res_m=0.3, split=split, n_range=24, n_azimuth=20))
+    dataset.save_manifest(recs, d / "manifest.jsonl")
+    ds = dataset.load_dataset(d / "manifest.jsonl")
+    np.savez_compressed(OUT / "dataset.npz", images=np.stack([img for _, img in ds.views]),
+                        az=np.array([c.azimuth_deg for c, _ in ds.views]), splits=np.array(ds.splits))
+
+
+if __name__ == "__main__" and "--dataset" in sys.argv:  # run after main(): python make_golden_io.py --dataset
+    make_dataset()

@@ -61,3 +61,15 @@ def test_missing_property_is_rejected(tmp_path):
     (tmp_path / "bad.ply").write_bytes(raw)
     with pytest.raises(InvalidParameterError):
         plyio.load_scene(tmp_path / "bad.ply")
+
+
+def test_load_views_matches_reference_dataset():
+    from paper_2506_21633_b200 import dataset
+
+    z = np.load(IO / "dataset.npz")
+    cfgs, targets, splits = dataset.load_views(IO / "dataset" / "manifest.jsonl")
+    assert np.array_equal(targets.cpu().numpy(), z["images"])      # bit-identical dequantisation
+    assert [c.azimuth_deg for c in cfgs] == list(z["az"])
+    assert splits == list(z["splits"])
+    cfgs_t, t_train, _ = dataset.load_views(IO / "dataset" / "manifest.jsonl", split="train")
+    assert len(cfgs_t) == 2 and np.array_equal(t_train.cpu().numpy(), z["images"][:2])
