@@ -49,7 +49,7 @@ RSS_PER_ORACLE_PROC = 6.0e9   # bytes, oracle fwd+bwd at 1M Gaussians / 512^2 (m
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sdgr", choices=("sdgr", "reference"))
     ap.add_argument("--n", type=int, default=1_000_000)
