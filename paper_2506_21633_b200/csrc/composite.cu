@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
   __shared__ int32_t scan_tmp[8];
   __shared__ int32_t base_s;
   __shared__ int item_s;
+  __shared__ uint16_t wlist[8 * kList];                     // per-warp member lists (P2)
   extern __shared__ double dyn[];
   double* fw = dyn;                                         // w
   double* fs = fw + kCap;                                   // S / contrib / g*contrib / D
@@ -519,28 +520,48 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
         if (record && tid == 0) rp_o = atomicAdd(a.rp.cursor, (unsigned long long)total);
         __syncthreads();
         WPROF(5);
-        // ---- P2: Gaussian-parallel weights into the flat slots
+        // ---- P2: weights into the flat slots.  The warp's (Gaussian, ray)
+        //      members go through a member list so every lane evaluates one
+        //      exp per round whatever the per-Gaussian member counts.
         const bool mine = have && tid >= j0 && tid < j1;
         const int jw = tid >> 5;
-        const uint32_t below = ((1u << lane) - 1u) & range_mask(jw, j0, j1);
+        const uint32_t rmask_w = range_mask(jw, j0, j1);
+        const uint32_t below = ((1u << lane) - 1u) & rmask_w;
         const uint32_t pshift = 8 * (jw & 3);
         const uint32_t* wp = wpre + (jw < 4 ? 0 : kRays);
-        if (mine) {
+        {
+          uint64_t mm[4];
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            uint64_t m = lm[w];
-            while (m) {
-              const int b = __ffsll((long long)m) - 1;
-              m &= m - 1;
-              const int r = w * 64 + b;
-              const int p = ray_off[r] + (int)((wp[r] >> pshift) & 255u) + __popc(rows[jw * kRays + r] & below);
-              const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
-              const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
-              const double wgt = exp(-quadform(sa0[tid], sa1[tid], sa2[tid], dx, dy));
+          for (int w = 0; w < 4; ++w) mm[w] = mine ? lm[w] : 0ull;
+          const int cnt = __popcll(mm[0]) + __popcll(mm[1]) + __popcll(mm[2]) + __popcll(mm[3]);
+          int incl = cnt;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+          }
+          int nx = incl - cnt;
+          const int tot = __shfl_sync(0xffffffffu, incl, 31);
+          uint16_t* list = wlist + jw * kList;
+          for (int B = 0; B < tot; B += kList) {
+            const int lim = min(tot, B + kList);
+            fill_window(mm, nx, lim, lane, list, B);
+            __syncwarp();
+            for (int k = B + lane; k < lim; k += 32) {
+              const int e = list[k - B];
+              const int owner = e >> 8, r = e & 255;
+              const int j = jw * 32 + owner;
+              const uint32_t bl = ((1u << owner) - 1u) & rmask_w;
+              const int p = ray_off[r] + (int)((wp[r] >> pshift) & 255u) + __popc(rows[jw * kRays + r] & bl);
+              const double dx = dsub((double)(tx * kTile + (r & 15)), su[j]);
+              const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[j]);
+              const double wgt = exp(-quadform(sa0[j], sa1[j], sa2[j], dx, dy));
               fw[p] = wgt;
-              fs[p] = dmul(sk[tid], wgt);  // tau, replaced by S_before in P3
-              fj[p] = (uint8_t)tid;
+              fs[p] = dmul(sk[j], wgt);  // tau, replaced by S_before in P3
+              fj[p] = (uint8_t)j;
+              fr[p] = (uint8_t)r;
             }
+            __syncwarp();
           }
         }
         __syncthreads();
@@ -567,8 +588,6 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
           }
           for (; p < p1; ++p) fs[p] = kInf;
           alive = S < a.s_stop;
-          if (record)
-            for (int q = roff; q < p1; ++q) fr[q] = (uint8_t)tid;
         }
 #ifdef SDGR_WALK_PROFILE
         __syncthreads();
