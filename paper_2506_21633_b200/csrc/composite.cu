@@ -616,11 +616,12 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
           const double wgt = fw[p];
           const double tau = sk[j] * wgt;
           const double T = exp(-fs[p]);
-          const double oma = -expm1(-tau);
+          const double em1 = expm1(-tau);
+          const double oma = -em1;
           if (lo >= 0) {
             // the backward needs only these per live pair: no transcendentals there
             a.rp.y1[lo + p] = T * oma;
-            a.rp.t2[lo + p] = T * exp(-tau);
+            a.rp.t2[lo + p] = T * (1.0 + em1);  // T e^-tau
             a.rp.w[lo + p] = wgt;
             a.rp.j[lo + p] = (uint8_t)j;
             a.rp.r[lo + p] = fr[p];
