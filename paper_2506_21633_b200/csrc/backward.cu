@@ -21,7 +21,7 @@ __device__ __forceinline__ double ldv(const void* p, int64_t i) {
   return (double)__ldg(static_cast<const T*>(p) + i);
 }
 
-__global__ void __launch_bounds__(256) k_grad_image(sdgr_view view, sdgr_plane pl, const uint8_t* flags,
+__global__ void __launch_bounds__(256, SDGR_MINB_GRAD_IMAGE) k_grad_image(sdgr_view view, sdgr_plane pl, const uint8_t* flags,
                                                     const double* intensity, const double* dLdS,
                                                     double* acc, int64_t n) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

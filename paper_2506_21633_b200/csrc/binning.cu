@@ -22,8 +22,18 @@
 
 namespace sdgr {
 
+#ifndef SDGR_SORT_IPT
+#define SDGR_SORT_IPT 8
+#endif
+#ifndef SDGR_SORT_MATCH
+#define SDGR_SORT_MATCH 0
+#endif
+#ifndef SDGR_SORT_LB
+#define SDGR_SORT_LB 4
+#endif
 constexpr int kSortThreads = 256;
-constexpr int kSortIpt = 8;
+constexpr int kSortIpt = SDGR_SORT_IPT;
+constexpr int kLookback = SDGR_SORT_LB;  // predecessor statuses loaded per look-back step
 constexpr int kSortTile = kSortThreads * kSortIpt;  // 2048
 constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kCountMask = (1u << 30) - 1;
 
@@ -114,7 +124,19 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 #pragma unroll
   for (int i = 0; i < kSortIpt; ++i) {
     const uint32_t d = dig[i];
+#if SDGR_SORT_MATCH
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
+#else
+    // warp multi-split by ballots (9 bits: 8 digit bits + the invalid flag);
+    // cheaper than MATCH.ANY, which serialises on the MIO pipe
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) {
+      const bool bit = (d >> b) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? bal : ~bal;
+    }
+#endif
     uint32_t before = 0;
     if (d < 256) before = whist[warp][d];
     rank[i] = before + __popc(peers & lt);
@@ -157,11 +179,12 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     int64_t j = bid - 1;
     bool done = false;
     while (!done) {
-      uint32_t s[4];
+      uint32_t s[kLookback];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) s[k] = (j - k >= 0) ? (uint32_t)vstat[(j - k) * 256 + t] : (uint32_t)(2u << 30);
+      for (int k = 0; k < kLookback; ++k)
+        s[k] = (j - k >= 0) ? (uint32_t)vstat[(j - k) * 256 + t] : (uint32_t)(2u << 30);
       int k = 0;
-      for (; k < 4; ++k) {
+      for (; k < kLookback; ++k) {
         const uint32_t f = s[k] & ~kCountMask;
         if (f == 0) break;               // not published yet: retry from here
         prefix += s[k] & kCountMask;

@@ -21,6 +21,18 @@ constexpr int kTile = SDGR_TILE;        // 16
 constexpr int kRays = SDGR_TILE_RAYS;   // 256 rays (cells) per tile
 constexpr int kChunk = 256;             // Gaussians staged per tile-walk chunk
 
+// Minimum resident 256-thread blocks per SM for the Gaussian-parallel FP64
+// kernels: capping registers at 64 (4 blocks, 50% occupancy) hides the FP64
+// dependency latency better than the few spills it costs (k_project
+// 6.5 -> 6.15 ms/step, k_grad_image 2.57 -> 2.42 on the c4 bench; 5 and 6
+// were slower).  Overridable for A/B builds via SDGR_EXTRA_FLAGS.
+#ifndef SDGR_MINB_PROJECT
+#define SDGR_MINB_PROJECT 4
+#endif
+#ifndef SDGR_MINB_GRAD_IMAGE
+#define SDGR_MINB_GRAD_IMAGE 4
+#endif
+
 // ---- explicit-rounding FP64 helpers (no contraction) -----------------------
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }

@@ -144,7 +144,7 @@ __device__ void plane_empty(const sdgr_plane& pl, int64_t g) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_project(sdgr_scene scene, sdgr_view view,
+__global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene scene, sdgr_view view,
                                                  sdgr_projection proj) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int n_vis = 0, n_skip = 0, n_cull = 0;
