@@ -26,7 +26,7 @@ namespace sdgr {
 #define SDGR_SORT_IPT 8
 #endif
 #ifndef SDGR_SORT_MATCH
-#define SDGR_SORT_MATCH 0
+#define SDGR_SORT_MATCH 1  // MATCH.ANY measured ~4% faster than the 9-ballot split here
 #endif
 #ifndef SDGR_SORT_LB
 #define SDGR_SORT_LB 4
