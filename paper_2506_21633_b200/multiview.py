@@ -415,6 +415,20 @@ class MultiViewStep:
     def allreduce(self):
         allreduce_grads(self.flat_soa, self.n, self.group)
 
+    def bind(self, scene: DeviceScene, flat_soa: torch.Tensor | None = None):
+        """Point the step at another scene of the same size (and optionally
+        another flat gradient buffer).  A graph captured afterwards reads and
+        writes those buffers; graphs captured before keep theirs."""
+        if len(scene) != self.n or scene.dtype != self.scene.dtype:
+            raise ValueError("bind: scene must match the step's size and dtype")
+        self.scene, self.sd = scene, _scene_desc(scene)
+        if flat_soa is not None:
+            if flat_soa.shape != self.flat_soa.shape or flat_soa.dtype != torch.float32:
+                raise ValueError("bind: flat gradient buffer shape/dtype mismatch")
+            self.flat_soa = flat_soa
+            self.grads = grad_views(flat_soa, self.n)
+            self.gd = self.grads.desc()
+
     def check(self):
         """One host read per step: capacity overflow and non-finite status."""
         flags = torch.stack([self.status[0].to(torch.int64)] +
@@ -440,3 +454,94 @@ class MultiViewStep:
         for ev in gevs:
             out["grad_geometry"] += ev[0].elapsed_time(ev[1])
         return out
+
+
+class HostStepPipeline:
+    """Steps fed from and returned to pinned host memory, pipelined.
+
+    Each submit() takes one step's inputs in host memory -- the scene arrays
+    and the per-view dL/dS -- and delivers that step's accumulated gradients
+    (the flat (30 n,) float32 SoA of MultiViewStep) back into a host buffer.
+    Two device banks (scene, dL/dS, gradients) alternate: step k+1's uploads
+    run on a copy stream while step k's graph computes, and step k's gradient
+    download overlaps step k+1's compute, so the PCIe copies hide under the
+    kernels.  Every step still moves all of its inputs and its result.
+
+    This is the host-facing shape of the reference's loop: per step the host
+    hands over parameters and upstream gradients and reads the parameter
+    gradients back (optimize.py:395-425 around render/backward).
+    """
+
+    def __init__(self, step: MultiViewStep, dl_dtype=torch.float32):
+        if step.cap is None:
+            step.calibrate()
+        self.step = step
+        dev, n = step.dev, step.n
+        V = len(step.views)
+        shape = (V,) + step.img_shape
+        base_scene, base_flat = step.scene, step.flat_soa
+        self.banks = []
+        for b in range(2):
+            scene = base_scene if b == 0 else DeviceScene(*(a.clone() for a in base_scene.arrays()))  # valid warm-up input
+            flat = base_flat if b == 0 else torch.zeros_like(base_flat)
+            dl_in = torch.empty(shape, dtype=dl_dtype, device=dev)
+            dl64 = dl_in if dl_dtype == torch.float64 else torch.empty(shape, dtype=torch.float64, device=dev)
+            self.banks.append(dict(scene=scene, flat=flat, dl_in=dl_in, dl64=dl64, graph=None,
+                                   uploaded=torch.cuda.Event(), computed=torch.cuda.Event(),
+                                   downloaded=torch.cuda.Event(), used=False))
+        self.up = torch.cuda.Stream(device=dev)
+        self.down = torch.cuda.Stream(device=dev)
+        self.k = 0
+        self.launches = 0
+        for bk in self.banks:
+            step.bind(bk["scene"], bk["flat"])
+            step.run(bk["dl64"].zero_(), check=False, allreduce=False)   # warm: attributes, occupancy queries
+            torch.cuda.synchronize()
+            n0 = step.lib.sdgr_launch_count()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                if bk["dl64"] is not bk["dl_in"]:
+                    bk["dl64"].copy_(bk["dl_in"])
+                step.run(bk["dl64"], check=False, allreduce=False)
+            bk["graph"] = g
+            self.launches = int(step.lib.sdgr_launch_count() - n0)
+        step.bind(base_scene, base_flat)
+
+    def submit(self, host_scene: dict, host_dl: torch.Tensor, host_out: torch.Tensor):
+        """Queue one step.  host_scene: {group: pinned tensor} for positions,
+        rotations, log_scales, sh_coeffs, ke_raw; host_dl: pinned (V, H, W);
+        host_out: pinned float32 (30 n,) receiving the gradients.  Returns an
+        event that completes when host_out holds this step's result."""
+        bk = self.banks[self.k % 2]
+        self.k += 1
+        main = torch.cuda.current_stream()
+        with torch.cuda.stream(self.up):
+            if bk["used"]:
+                self.up.wait_event(bk["computed"])      # the bank's previous graph has read its inputs
+            for g, dst in zip(("positions", "rotations", "log_scales", "sh_coeffs", "ke_raw"),
+                              bk["scene"].arrays()):
+                dst.copy_(host_scene[g], non_blocking=True)
+            bk["dl_in"].copy_(host_dl, non_blocking=True)
+            bk["uploaded"].record(self.up)
+        main.wait_event(bk["uploaded"])
+        if bk["used"]:
+            main.wait_event(bk["downloaded"])            # its previous gradients have left the device
+        bk["graph"].replay()
+        if self.step.group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
+            allreduce_grads(bk["flat"], self.step.n, self.step.group)
+        bk["computed"].record(main)
+        with torch.cuda.stream(self.down):
+            self.down.wait_event(bk["computed"])
+            host_out.copy_(bk["flat"], non_blocking=True)
+            bk["downloaded"].record(self.down)
+        bk["used"] = True
+        done = torch.cuda.Event()
+        done.record(self.down)
+        return done
+
+    def drain(self):
+        """Make the current stream wait for every queued download."""
+        torch.cuda.current_stream().wait_stream(self.down)
+
+    def check(self):
+        self.step.check()

@@ -296,6 +296,61 @@ def test_multiview_graph_replay_equals_run():
     assert torch.equal(step.flat_soa, want2)
 
 
+def test_host_pipeline_equals_run():
+    """HostStepPipeline (two banks, overlapped H2D / D2H) returns, for each
+    submitted step, exactly run()'s gradients for that step's host inputs."""
+    from paper_2506_21633_b200.multiview import HostStepPipeline, MultiViewStep
+
+    tank = targets.to_float32_exact(targets.composite_target(targets.tank_preset(), [3000, 1500, 500], seed=4))
+    cfgs = [sdgr.RadarConfig(azimuth_deg=az, elevation_deg=el, altitude_m=0.5, n_range=96, n_azimuth=96)
+            for az, el in ((10.0, 30.0), (130.0, 60.0), (250.0, 45.0))]
+    ds = sdgr.DeviceScene.from_host(tank, dtype=torch.float32)
+    step = MultiViewStep(ds, cfgs, geo_batch=2)
+    pipe = HostStepPipeline(step, dl_dtype=torch.float32)
+    g = torch.Generator().manual_seed(3)
+    groups = ("positions", "rotations", "log_scales", "sh_coeffs", "ke_raw")
+    inputs, outs, wants = [], [], []
+    for k in range(4):   # perturbed scenes so every step's result differs
+        sc = {nm: (getattr(ds, nm).cpu() + (1e-3 * k if nm == "positions" else 0.0)).pin_memory() for nm in groups}
+        dl = torch.randn((3, 96, 96), generator=g, dtype=torch.float32).pin_memory()
+        inputs.append((sc, dl))
+        outs.append(torch.empty(step.flat_soa.shape, dtype=torch.float32).pin_memory())
+    for k, (sc, dl) in enumerate(inputs):
+        pipe.submit(sc, dl, outs[k])
+    pipe.drain()
+    torch.cuda.synchronize()
+    pipe.check()
+    for k, (sc, dl) in enumerate(inputs):
+        for nm in groups:
+            getattr(ds, nm).copy_(sc[nm])
+        step.run(dl.cuda().double())
+        assert torch.equal(outs[k], step.flat_soa.cpu()), k
+
+
+def test_multiview_capacity_overflow_is_detected():
+    """Pair buffers are sized by calibration; a scene that later needs more
+    pairs (grown footprints) must raise OverflowError from check(), never
+    write past the buffers, and recalibration must recover the exact result."""
+    from paper_2506_21633_b200.multiview import MultiViewStep
+
+    tank = targets.to_float32_exact(targets.composite_target(targets.tank_preset(), [3000, 1500, 500], seed=4))
+    cfgs = [sdgr.RadarConfig(azimuth_deg=az, elevation_deg=45.0, altitude_m=0.5, n_range=96, n_azimuth=96)
+            for az in (10.0, 130.0)]
+    ds = sdgr.DeviceScene.from_host(tank, dtype=torch.float32)
+    step = MultiViewStep(ds, cfgs, geo_batch=2, headroom=1.0)
+    dl = torch.randn((2, 96, 96), dtype=torch.float64, device="cuda",
+                     generator=torch.Generator("cuda").manual_seed(2))
+    step.run(dl)
+    ds.log_scales.add_(1.5)          # ~4.5x larger footprints: far more pairs than calibrated
+    with pytest.raises(OverflowError):
+        step.run(dl)
+    torch.cuda.synchronize()         # no illegal address
+    step.calibrate()
+    got = step.run(dl)
+    ref = MultiViewStep(ds, cfgs, geo_batch=2).run(dl)
+    assert torch.equal(got.positions, ref.positions) and torch.equal(got.visible, ref.visible)
+
+
 def test_depth_ties_and_near_ties_vs_oracle():
     """Exact (depth, index) order with duplicated positions (ties -> index
     order) and positions 1e-12 m apart (runs of equal 32-bit depth keys)."""
