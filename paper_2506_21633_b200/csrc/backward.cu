@@ -142,6 +142,7 @@ struct GeoView {
   const int32_t* pair_start;
   const double* acc;      // (6, n) imaging-plane sums
   const double* partial;  // (n_pairs, 8) computation-plane partial records
+  int64_t cap;            // n_pairs: records beyond it were never written (overflowed step)
 };
 struct GeoBatch {
   int n_views;
@@ -195,7 +196,9 @@ __global__ void __launch_bounds__(128, 5) k_grad_geometry(sdgr_scene sc, const _
     // computation-plane partials: one record per member tile, fixed order
     double c7[7] = {0, 0, 0, 0, 0, 0, 0};
     {
-      const int s0 = V.pair_start[g], cnt = V.n_tiles[g];
+      const int s0 = V.pair_start[g];
+      const int64_t room = V.cap - s0 > 0 ? V.cap - s0 : 0;   // overflowed step: stay in bounds
+      const int cnt = V.n_tiles[g] < room ? V.n_tiles[g] : (int)room;
       for (int k = 0; k < cnt; ++k) {
         const double4* rec = reinterpret_cast<const double4*>(V.partial + (int64_t)(s0 + k) * 8);
         const double4 r0 = rec[0], r1 = rec[1];
@@ -338,6 +341,7 @@ int launch_grad_geometry(const sdgr_scene& sc, int n_views, const sdgr_view* vie
     G.pair_start = comps[k].pair_start;
     G.acc = acc_imgs[k];
     G.partial = partials[k];
+    G.cap = comps[k].n_pairs;
   }
   const unsigned blocks = (unsigned)((sc.n + 127) / 128);
   {

@@ -416,10 +416,11 @@ __global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t
   int64_t o = offsets[i];
   pair_start[g] = (int32_t)o;
   if (cnt == 0) return;
-  if (o + cnt > cap) {  // caller's pair buffers are too small: flag, emit nothing
-    *overflow = 1;
-    return;
-  }
+  // caller's pair buffers too small: flag it and emit only the pairs that fit,
+  // so every slot below the capacity still holds a real (tile, Gaussian) pair
+  // and the (discarded) rest of the step stays in bounds
+  if (o + cnt > cap) *overflow = 1;
+  if (o >= cap) return;
   const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
   const int tx0 = bb.x >> 4, tx1 = bb.y >> 4, ty0 = bb.z >> 4, ty1 = bb.w >> 4;
   if ((tx1 - tx0) < 8 && (ty1 - ty0) < 8) {
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t
       const int tx = tx0 + (b & 7), ty = ty0 + (b >> 3);
       keys[o] = (uint32_t)(ty * tiles_x + tx);
       vals[o] = g;
-      ++o;
+      if (++o >= cap) return;
     }
     return;
   }
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t
       if (hit) {
         keys[o] = (uint32_t)(ty * tiles_x + tx);
         vals[o] = g;
-        ++o;
+        if (++o >= cap) return;
       }
     }
 }

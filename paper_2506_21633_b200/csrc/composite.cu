@@ -606,11 +606,11 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
             a.rp.cursor[1] = 1ull;  // overflow: the host must re-walk
           }
         }
-        if (record) ++n_desc;
         __syncthreads();
         WPROF(7);
         // ---- P4: flat pair-parallel transmittance and contributions
         const long long lo = record ? rp_off : -1ll;
+        if (lo >= 0) ++n_desc;  // count only descriptors actually written (log overflow)
         for (int p = tid; p < total; p += kRays) {
           const int j = fj[p];
           const double wgt = fw[p];
@@ -1070,10 +1070,13 @@ __global__ void __launch_bounds__(256) k_seg_scan(const int32_t* __restrict__ ra
 
 // intensity[g] = sum of its per-tile partials, in pre-sort (tile-id) order.
 __global__ void __launch_bounds__(256) k_reduce_intensity(const int32_t* pair_start, const int32_t* n_tiles,
-                                                          const double* partial, int64_t n, double* out) {
+                                                          const double* partial, int64_t n, int64_t cap,
+                                                          double* out) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n) return;
-  const int s = pair_start[g], c = n_tiles[g];
+  const int s = pair_start[g];
+  const int64_t room = cap - s > 0 ? cap - s : 0;   // capacity overflow: stay in bounds
+  const int c = n_tiles[g] < room ? n_tiles[g] : (int)room;
   double acc = 0.0;
   for (int k = 0; k < c; ++k) acc += partial[s + k];
   out[g] = acc;
@@ -1152,7 +1155,7 @@ int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const
     if (rc) return rc;
   }
   k_reduce_intensity<<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(t.pair_start, p.comp.n_tiles, partial_I,
-                                                                     p.n, intensity);
+                                                                     p.n, t.n_pairs, intensity);
   note_launch();
   return check_launch();
 }
