@@ -29,6 +29,9 @@ constexpr int kChunk = 256;             // Gaussians staged per tile-walk chunk
 #ifndef SDGR_MINB_PROJECT
 #define SDGR_MINB_PROJECT 4
 #endif
+#ifndef SDGR_MINB_REPLAY_GRAD
+#define SDGR_MINB_REPLAY_GRAD 2
+#endif
 #ifndef SDGR_MINB_GRAD_IMAGE
 #define SDGR_MINB_GRAD_IMAGE 4
 #endif

@@ -789,7 +789,7 @@ struct ReplayCfg {
 //      (tile, Gaussian) pair, written once.  Pairs of the item no descriptor
 //      covers get zero records here, so partial_g needs no memset.
 template <int MODE>
-__global__ void __launch_bounds__(256, MODE == kGrad ? 2 : 4) k_replay(ReplayArgs a) {
+__global__ void __launch_bounds__(256, MODE == kGrad ? SDGR_MINB_REPLAY_GRAD : 4) k_replay(ReplayArgs a) {
   constexpr bool kG = MODE == kGrad;
   constexpr int kCap = kReplayCap;
   __shared__ double sk[kChunk], sp[kChunk], sg[kChunk];
@@ -862,11 +862,27 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? 2 : 4) k_replay(ReplayArg
           spos[tid] = r.pos;
         }
       }
-      for (int p = tid; p < n; p += kRays) {
-        fY[p] = a.rp.y1[off + p];
-        if (kG) fW[p] = a.rp.w[off + p];
-        fj[p] = a.rp.j[off + p];
-        fr[p] = a.rp.r[off + p];
+      // log entries: two rows of loads in flight per thread; kGrad also
+      // stages t2 here (into fD) so stage B reads no global memory
+      for (int p = tid; p < n; p += 2 * kRays) {
+        const int p2 = p + kRays;
+        const bool two = p2 < n;
+        const double y_a = a.rp.y1[off + p];
+        const double y_b = two ? a.rp.y1[off + p2] : 0.0;
+        double w_a = 0.0, w_b = 0.0, t_a = 0.0, t_b = 0.0;
+        if (kG) {
+          w_a = a.rp.w[off + p];
+          t_a = a.rp.t2[off + p];
+          if (two) { w_b = a.rp.w[off + p2]; t_b = a.rp.t2[off + p2]; }
+        }
+        const uint8_t j_a = a.rp.j[off + p], r_a = a.rp.r[off + p];
+        const uint8_t j_b = two ? a.rp.j[off + p2] : 0, r_b = two ? a.rp.r[off + p2] : 0;
+        fY[p] = y_a; fj[p] = j_a; fr[p] = r_a;
+        if (kG) { fW[p] = w_a; fD[p] = t_a; }
+        if (two) {
+          fY[p2] = y_b; fj[p2] = j_b; fr[p2] = r_b;
+          if (kG) { fW[p2] = w_b; fD[p2] = t_b; }
+        }
       }
       __syncthreads();
       // ---- B: g*contrib per entry, segmented scan over the ray runs
@@ -884,7 +900,7 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? 2 : 4) k_replay(ReplayArg
           const int q = q0 + e;
           const int j = fj[q], r = fr[q];
           v[e] = sg[j] * (fY[q] * sp[j]);
-          if (kG) fD[q] = sg[j] * a.rp.t2[off + q] * sp[j];  // x, thread-private until P7
+          if (kG) fD[q] = sg[j] * fD[q] * sp[j];  // x (fD held t2), thread-private until P7
           hd[e] = q == 0 || fr[q - 1] != r;
           if (kG) atomicOr(jm + (r >> 5) * kChunk + j, 1u << (r & 31));
         }
