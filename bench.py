@@ -253,6 +253,34 @@ def kernel_bytes(kid: int, n: int, t16: float, live: float, items: float, batch:
     return float("nan")
 
 
+def preprocess_sort_roofline(n: int, step, stages: dict, views: int, peak: float) -> dict:
+    """North-star target: preprocess + sort at >= 50 % of HBM
+    roofline.  Algorithmic bytes per view by the survey's formula:
+    B_pre = 184 N, B_rank = 192 N, B_bin = sum over planes of
+    T16_p (12 + 24 ceil(b_p / 8) + 8), b_p = ceil(log2 tiles_p) + ceil(log2 N);
+    time = the single-stream device time of the project + depth_sort +
+    binning stages (each kernel alone on the GPU).  This design bins only the
+    computation plane (the splat is Gaussian-parallel), so the formula's
+    imaging-plane term is work it never does; `frac_comp_plane_only` drops it."""
+    import math
+    v0 = step.views[0]
+    lg_n = math.ceil(math.log2(max(n, 2)))
+    tiles = {0: -(-v0.n_u // 16) * -(-v0.n_v // 16), 1: -(-v0.n_az // 16) * -(-v0.n_rg // 16)}
+    b_bin = {}
+    for pl in (0, 1):
+        bits = math.ceil(math.log2(max(tiles[pl], 2))) + lg_n
+        b_bin[pl] = step.calib_t16_mean[pl] * (12 + 24 * math.ceil(bits / 8) + 8)
+    b_pre, b_rank = 184.0 * n, 192.0 * n
+    ms = (stages["project"] + stages["depth_sort"] + stages["binning"]) / views
+    full = b_pre + b_rank + b_bin[0] + b_bin[1]
+    comp = b_pre + b_rank + b_bin[0]
+    return {"ms_per_view": ms, "bytes_per_view": full, "achieved_gbs": full / (ms / 1e3) / 1e9,
+            "peak_gbs": peak, "frac": full / (ms / 1e3) / 1e9 / peak,
+            "frac_comp_plane_only": comp / (ms / 1e3) / 1e9 / peak,
+            "stages": ["project", "depth_sort", "binning"], "target_frac": 0.5,
+            "formula": "SURVEY.md §8d: 184N + 192N + sum_p T16_p (12 + 24 ceil(b_p/8) + 8)"}
+
+
 def _profile(lib):
     import ctypes as C
     from paper_2506_21633_b200 import _lib as L
@@ -426,6 +454,7 @@ def run_sdgr(args):
                    "t16_per_view": step.calib_t16_mean},
         "roofline": roofline,
         "stage_ms_per_step_single_stream": stages,
+        "preprocess_sort_roofline": preprocess_sort_roofline(args.n, step, stages, V, peak),
         "gpu_launches": int(launches),
         "e2e": e2e,
         "clocks": clk.summary(),

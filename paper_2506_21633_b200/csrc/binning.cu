@@ -69,27 +69,12 @@ __global__ void __launch_bounds__(256) k_radix_hist(const K* __restrict__ keys, 
   }
 }
 
-// exclusive scan of each 256-bin digit histogram; one block per pass
-__global__ void k_radix_hist_scan(const uint32_t* __restrict__ hist, uint32_t* __restrict__ base) {
-  __shared__ uint32_t s[256];
-  const int p = blockIdx.x, t = threadIdx.x;
-  s[t] = hist[p * 256 + t];
-  __syncthreads();
-  for (int off = 1; off < 256; off <<= 1) {
-    const uint32_t v = t >= off ? s[t - off] : 0u;
-    __syncthreads();
-    s[t] += v;
-    __syncthreads();
-  }
-  base[p * 256 + t] = s[t] - hist[p * 256 + t];
-}
-
 // ------------------------------------------------------------- onesweep ----
 template <typename K, bool kIota>
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n_cap, const int32_t* n_dev, int shift,
-    const uint32_t* __restrict__ base, uint32_t* status, uint32_t* counter) {
+    const uint32_t* __restrict__ ghist, uint32_t* status, uint32_t* counter) {
   const int64_t n = eff_count(n_cap, n_dev);
   extern __shared__ __align__(16) unsigned char dyn[];
   K* skeys = reinterpret_cast<K*>(dyn);
@@ -97,7 +82,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   __shared__ uint32_t whist[kSortThreads / 32][256];
   __shared__ uint32_t dstart[256];
   __shared__ int64_t goff[256];
-  __shared__ uint32_t scan_tmp[8];
+  __shared__ uint32_t scan_tmp[16];
   __shared__ int bid_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -158,18 +143,22 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   volatile uint32_t* vstat = status;
   if (bid == 0) vstat[t] = kFlagP | total;
   else vstat[(int64_t)bid * 256 + t] = kFlagA | total;
-  // block-local exclusive scan of totals over digits
-  uint32_t x = total;
+  // block-local exclusive scans over digits: this tile's totals, and the
+  // pass's global digit histogram (-> the digit's global base offset)
+  const uint32_t h = ghist[t];
+  uint32_t x = total, xh = h;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
-    if (lane >= off) x += y;
+    const uint32_t yh = __shfl_up_sync(0xffffffffu, xh, off);
+    if (lane >= off) { x += y; xh += yh; }
   }
-  if (lane == 31) scan_tmp[warp] = x;
+  if (lane == 31) { scan_tmp[warp] = x; scan_tmp[8 + warp] = xh; }
   __syncthreads();
-  uint32_t wpre = 0;
-  for (int w = 0; w < warp; ++w) wpre += scan_tmp[w];
+  uint32_t wpre = 0, wpreh = 0;
+  for (int w = 0; w < warp; ++w) { wpre += scan_tmp[w]; wpreh += scan_tmp[8 + w]; }
   const uint32_t excl = wpre + x - total;
+  const uint32_t gbase = wpreh + xh - h;
   dstart[t] = excl;
   // decoupled look-back for this digit
   uint32_t prefix = 0;
@@ -194,7 +183,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     }
     vstat[(int64_t)bid * 256 + t] = kFlagP | (prefix + total);
   }
-  goff[t] = (int64_t)base[t] + prefix - excl;
+  goff[t] = (int64_t)gbase + prefix - excl;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortIpt; ++i) {
@@ -222,7 +211,6 @@ size_t radix_ws_bytes(int64_t n, int npass) {
   const int64_t nblk = (n + kSortTile - 1) / kSortTile;
   size_t b = 0;
   b += align_up(sizeof(uint32_t) * 8 * 256);                  // hist
-  b += align_up(sizeof(uint32_t) * 8 * 256);                  // base
   b += align_up(sizeof(uint32_t) * 8);                        // counters
   b += align_up(sizeof(uint32_t) * (size_t)npass * nblk * 256);  // status
   b += align_up(sizeof(K) * (size_t)n);                       // alt keys
@@ -254,21 +242,19 @@ int radix_sort(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64
   const int64_t nblk = (n + kSortTile - 1) / kSortTile;
   char* p = static_cast<char*>(ws);
   uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * 8 * 256);
-  uint32_t* base = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * 8 * 256);
   uint32_t* ctr = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * 8);
   uint32_t* status = reinterpret_cast<uint32_t*>(p);
   const size_t status_bytes = sizeof(uint32_t) * (size_t)npass * nblk * 256;
   p += align_up(status_bytes);
   K* kalt = reinterpret_cast<K*>(p); p += align_up(sizeof(K) * (size_t)n);
   uint32_t* valt = reinterpret_cast<uint32_t*>(p);
-  // hist, base, counters and status are contiguous: one memset
+  // hist, counters and status are contiguous: one memset
   if (cudaMemsetAsync(hist, 0, (size_t)((char*)status - (char*)hist) + status_bytes, st) !=
       cudaSuccess)
     return SDGR_ERR_CUDA;
   const int hist_blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 2);  // fewer global bin REDs
   k_radix_hist<K><<<hist_blocks, 256, 0, st>>>(kin, n, n_dev, begin_bit, npass, hist);
-  k_radix_hist_scan<<<npass, 256, 0, st>>>(hist, base);
-  note_launch(2);
+  note_launch();
   const size_t smem = (sizeof(K) + 4) * kSortTile;
   const K* ki = kin;
   const uint32_t* vi = vin;
@@ -282,10 +268,10 @@ int radix_sort(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64
       KernelTimer kt(SDGR_K_ONESWEEP, st);
       if (pass == 0 && vin == nullptr)
         k_onesweep<K, true><<<(unsigned)nblk, kSortThreads, smem, st>>>(
-            ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
+            ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, hist + pass * 256, stat, ctr + pass);
       else
         k_onesweep<K, false><<<(unsigned)nblk, kSortThreads, smem, st>>>(
-            ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, base + pass * 256, stat, ctr + pass);
+            ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, hist + pass * 256, stat, ctr + pass);
     }
     note_launch();
     ki = ko;
@@ -461,35 +447,23 @@ __global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t
     }
 }
 
-// CSR tile ranges from the sorted keys: range[t] = [lower_bound(t),
-// lower_bound(t+1)); empty tiles get [s, s] like a CSR offsets array.
-__device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* k, int64_t n, uint32_t v) {
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (k[mid] < v) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* keys, int64_t n_cap,
-                                                     const int32_t* n_dev, int n_tiles, int32_t* range) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_tiles) return;
-  const int64_t n = eff_count(n_cap, n_dev);
-  range[2 * t] = (int32_t)lower_bound_u32(keys, n, (uint32_t)t);
-  range[2 * t + 1] = (int32_t)lower_bound_u32(keys, n, (uint32_t)t + 1u);
-}
-
 // scene index of each sorted pair: pair_prim[i] = pre_prim[pair_pos[i]]
 // ... and, for the computation plane, the packed record the tile walks read
 // coalesced instead of gathering from the N-sized projection records.
+// Also the CSR tile ranges of the non-empty tiles, from the run boundaries of
+// the sorted tile ids (range was preset to -1; k_make_items fills the empty
+// tiles' [s, s]).
 __global__ void __launch_bounds__(256) k_gather_prim(const int32_t* pos, const int32_t* pre, int64_t n_cap,
                                                      const int32_t* n_dev, int32_t* prim,
                                                      sdgr_plane pl, const double* kappa,
-                                                     const double* phase, sdgr_pair_rec* rec) {
+                                                     const double* phase, sdgr_pair_rec* rec,
+                                                     const uint32_t* keys, int32_t* range) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= eff_count(n_cap, n_dev)) return;
+  const int64_t n = eff_count(n_cap, n_dev);
+  if (i >= n) return;
+  const uint32_t t = keys[i];
+  if (i == 0 || keys[i - 1] != t) range[2 * t] = (int32_t)i;
+  if (i == n - 1 || keys[i + 1] != t) range[2 * t + 1] = (int32_t)(i + 1);
   const int32_t p = pos[i];
   const int32_t g = pre[p];
   prim[i] = g;
@@ -510,11 +484,39 @@ __global__ void __launch_bounds__(256) k_gather_prim(const int32_t* pos, const i
 
 // depth-segment work items: each tile list is cut into segments of at most
 // seg_len Gaussians; items are tile-major, segment-minor.
-__global__ void __launch_bounds__(1024) k_make_items(const int32_t* range, int n_tiles, int seg_len,
+__global__ void __launch_bounds__(1024) k_make_items(int32_t* range, int n_tiles, int seg_len,
                                                      int max_items, int32_t* items,
                                                      int32_t* tile_first, int32_t* n_items,
-                                                     int32_t* overflow) {
+                                                     int32_t* overflow, int64_t n_cap, const int32_t* n_dev) {
   __shared__ int32_t tmp[32];
+  // empty tiles (range still -1): [s, s] with s = start of the next non-empty
+  // tile, or the pair count -- a suffix min over tiles, chunks last to first
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t after = (int32_t)eff_count(n_cap, n_dev);
+    const int n_chunks = (n_tiles + 1023) / 1024;
+    for (int c = n_chunks - 1; c >= 0; --c) {
+      const int t = c * 1024 + (1023 - (int)threadIdx.x);   // thread 0 = last tile of the chunk
+      const int32_t s0 = t < n_tiles ? range[2 * t] : -1;
+      int32_t m = s0 < 0 ? INT32_MAX : s0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int32_t o = __shfl_up_sync(0xffffffffu, m, off);
+        if (lane >= off) m = min(m, o);
+      }
+      if (lane == 31) tmp[warp] = m;
+      __syncthreads();
+      int32_t pre = after;
+      for (int w = 0; w < warp; ++w) pre = min(pre, tmp[w]);
+      m = min(m, pre);
+      if (t < n_tiles && s0 < 0) { range[2 * t] = m; range[2 * t + 1] = m; }
+      int32_t all = after;
+      for (int w = 0; w < 32; ++w) all = min(all, tmp[w]);
+      __syncthreads();
+      after = all;
+    }
+    __syncthreads();
+  }
   int32_t carry = 0;
   for (int t0 = 0; t0 < n_tiles; t0 += 1024) {
     const int t = t0 + threadIdx.x;
@@ -553,7 +555,7 @@ int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, con
   const int64_t n = proj.n, np = tl.n_pairs;  // np: exact count, or capacity with a device count
   // device-side pair count = offsets[n] (the scan's total) when capacity mode is on
   const int32_t* n_dev = tl.device_count ? offsets + n : nullptr;
-  if (cudaMemsetAsync(tl.tile_range, 0, sizeof(int32_t) * 2 * (size_t)tl.n_tiles, st) != cudaSuccess)
+  if (cudaMemsetAsync(tl.tile_range, 0xff, sizeof(int32_t) * 2 * (size_t)tl.n_tiles, st) != cudaSuccess)
     return SDGR_ERR_CUDA;
   // n_items[0] is written by k_make_items; n_items[1] (overflow) is sticky
   // until the caller clears it, so one check can cover many views.
@@ -577,15 +579,14 @@ int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, con
                                         reinterpret_cast<uint32_t*>(tl.pair_pos), np, n_dev, 0, bits,
                                         p, ws_bytes - used, st);
     if (rc != SDGR_OK) return rc;
-    k_tile_ranges<<<(unsigned)((tl.n_tiles + 255) / 256), 256, 0, st>>>(tl.pair_tile, np, n_dev,
-                                                                        tl.n_tiles, tl.tile_range);
     {
       KernelTimer kt(SDGR_K_GATHER, st);
       k_gather_prim<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(tl.pair_pos, tl.pre_prim, np, n_dev,
                                                                   tl.pair_prim, pl, proj.kappa, proj.phase,
-                                                                  tl.plane == 0 ? tl.pair_rec : nullptr);
+                                                                  tl.plane == 0 ? tl.pair_rec : nullptr,
+                                                                  tl.pair_tile, tl.tile_range);
     }
-    note_launch(2);
+    note_launch();
   } else {
     k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,
                                                               view.cutoff, nullptr, nullptr,
@@ -593,7 +594,7 @@ int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, con
     note_launch();
   }
   k_make_items<<<1, 1024, 0, st>>>(tl.tile_range, tl.n_tiles, tl.seg_len, tl.max_items, tl.items,
-                                   tl.tile_first, tl.n_items, overflow);
+                                   tl.tile_first, tl.n_items, overflow, np, n_dev);
   note_launch();
   return check_launch();
 }
