@@ -34,7 +34,7 @@ extern "C" {
 #define SDGR_TILE 16          /* tile edge in cells / pixels (16x16 = 256 rays) */
 #define SDGR_TILE_RAYS 256
 #define SDGR_MAX_PLANE 32767  /* plane dims must fit int16 bboxes */
-#define SDGR_MAX_BATCH 8      /* views per sdgr_grad_geometry_batch call */
+#define SDGR_MAX_BATCH 8      /* views per batched call (*_batch) */
 
 typedef enum sdgr_status {
   SDGR_OK = 0,
@@ -212,18 +212,31 @@ int sdgr_profile_begin(uint32_t kernel_mask);
 int sdgr_profile_end(double* ms, int64_t* launches);
 /* Bytes of scratch the binning calls need for n Gaussians / max pairs. */
 size_t sdgr_workspace_bytes(int64_t n, int64_t max_pairs);
+/* ... and the batched calls for n_views (1..SDGR_MAX_BATCH) views (0 if n_views is out of range). */
+size_t sdgr_batch_workspace_bytes(int64_t n, int64_t max_pairs, int n_views);
 
 /* ------------------------------------------------ preprocess (K1) -------- */
 /* geometry.project_all (geometry.py:233-340) + the footprint bbox / member
  * tests of forward._footprint_pairs (forward.py:60-109) for both planes. */
 int sdgr_project(const sdgr_scene* scene, const sdgr_view* view,
                  sdgr_projection* proj, void* stream);
+/* sdgr_project for n_views (1..SDGR_MAX_BATCH) views of one scene in one
+ * launch: views[k] -> projs[k], each exactly as the single-view call.  The
+ * parameters are read once and their view-independent half (normalised
+ * quaternion, R(q), e^s, Sigma = M M^T, softplus extinctions) is computed once
+ * per Gaussian for the whole batch (a multi-view step's preprocessing). */
+int sdgr_project_batch(const sdgr_scene* scene, int n_views, const sdgr_view* views,
+                       sdgr_projection* projs, void* stream);
 
 /* --------------------------------------------------- binning (K2-K5) ----- */
 /* Stable sort of the visible Gaussians by (depth, index): order[rank] = g.
  * The depth half of np.lexsort((prim, depth, cell)) (forward.py:147). */
 int sdgr_depth_order(const sdgr_projection* proj, int32_t* order,
                      void* ws, size_t ws_bytes, void* stream);
+/* sdgr_depth_order for n_views projections of one scene (orders[k] <- projs[k]),
+ * every radix pass one launch over all views.  ws: sdgr_batch_workspace_bytes. */
+int sdgr_depth_order_batch(int n_views, const sdgr_projection* projs, int32_t* const* orders,
+                           void* ws, size_t ws_bytes, void* stream);
 /* offsets[i] = exclusive prefix of member-tile counts in rank order (plane 0,
  * `order` given) or scene order (plane 1, order == NULL); offsets has n+1
  * entries, offsets[n] = T16 for the plane. */
@@ -236,6 +249,13 @@ int sdgr_count_pairs(const sdgr_projection* proj, int32_t plane,
 int sdgr_bin_pairs(const sdgr_projection* proj, const sdgr_view* view,
                    const int32_t* order, const int32_t* offsets,
                    sdgr_tiles* tiles, void* ws, size_t ws_bytes, void* stream);
+/* sdgr_count_pairs + sdgr_bin_pairs of one plane for n_views views, each
+ * stage one launch over all views: orders[k] (plane 0) / NULL (plane 1),
+ * offsets[k] (n+1, written), tiles[k] (same tile grid, capacity and
+ * device_count for every view).  ws: sdgr_batch_workspace_bytes. */
+int sdgr_bin_batch(int n_views, const sdgr_projection* projs, const sdgr_view* views, int32_t plane,
+                   const int32_t* const* orders, int32_t* const* offsets, sdgr_tiles* tiles,
+                   void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------- forward (K6, K7) ------ */
 /* compute_intensities (forward.py:178-199): per-ray emission-absorption walk.

@@ -104,6 +104,13 @@ SIGNATURES = [
     ("sdgr_count_pairs", C.c_int, [C.POINTER(ProjectionDesc), C.c_int32, _p, _p, _p, C.c_size_t, _p]),
     ("sdgr_bin_pairs", C.c_int, [C.POINTER(ProjectionDesc), C.POINTER(View), _p, _p,
                                  C.POINTER(TilesDesc), _p, C.c_size_t, _p]),
+    ("sdgr_batch_workspace_bytes", C.c_size_t, [C.c_int64, C.c_int64, C.c_int]),
+    ("sdgr_project_batch", C.c_int, [C.POINTER(SceneDesc), C.c_int, C.POINTER(View), C.POINTER(ProjectionDesc),
+                                     _p]),
+    ("sdgr_depth_order_batch", C.c_int, [C.c_int, C.POINTER(ProjectionDesc), C.POINTER(_p), _p, C.c_size_t,
+                                         _p]),
+    ("sdgr_bin_batch", C.c_int, [C.c_int, C.POINTER(ProjectionDesc), C.POINTER(View), C.c_int32,
+                                 C.POINTER(_p), C.POINTER(_p), C.POINTER(TilesDesc), _p, C.c_size_t, _p]),
     ("sdgr_composite_forward", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), C.POINTER(TilesDesc),
                                          C.c_double, _p, _p, _p, _p, _p, C.POINTER(ReplayDesc), _p]),
     ("sdgr_splat", C.c_int, [C.POINTER(View), C.POINTER(ProjectionDesc), _p, _p, _p, _p]),

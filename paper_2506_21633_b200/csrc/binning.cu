@@ -11,13 +11,21 @@
 // so each tile's list is ordered by (depth, index) / index, bit-exactly the
 // order the reference walks each ray.
 //
-// The radix sort is a single-pass-per-digit "onesweep" design: one upfront
-// histogram kernel for all digits, then per 8-bit digit one kernel that ranks
-// its 2048-key tile with warp match-ranking, resolves its global offset by
-// decoupled look-back (4 predecessors per step: with a whole 1M-key pass
-// resident in one wave, a one-at-a-time look-back chain dominated -- see
-// profiles/ROUND1.md), and scatters through shared memory.  A chain-free
-// three-kernel pass (count / scan / scatter) was measured slower (41 vs 24 us).
+// Every stage is batched over up to SDGR_MAX_BATCH views of one scene: one
+// launch covers all views (per-view pointers travel in the kernel parameter
+// block, the view is blockIdx.y or part of the flattened block id).  A 1M-key
+// sort or a 1M-entry scan is far too small to fill 148 SMs on its own -- the
+// single-view passes were look-back- and launch-latency bound (profiles/) --
+// so batching the views is what turns these stages bandwidth-shaped.  The
+// single-view entry points are batches of one.
+//
+// The radix sort is a single-pass-per-digit "onesweep" design: the digit
+// histograms come from the kernel that produces the keys (fused), then per
+// 8-bit digit one kernel ranks its 2048-key tile with warp match-ranking,
+// resolves its global offset by decoupled look-back (4 predecessors per step)
+// and scatters through shared memory.  Blocks take their (view, tile) from
+// one atomic ticket, views interleaved, so each view's look-back chain only
+// ever waits on blocks that already started.
 #include "common.cuh"
 
 namespace sdgr {
@@ -31,15 +39,17 @@ namespace sdgr {
 #ifndef SDGR_SORT_LB
 #define SDGR_SORT_LB 4
 #endif
+constexpr int kMaxBatch = SDGR_MAX_BATCH;
 constexpr int kSortThreads = 256;
 constexpr int kSortIpt = SDGR_SORT_IPT;
 constexpr int kLookback = SDGR_SORT_LB;  // predecessor statuses loaded per look-back step
 constexpr int kSortTile = kSortThreads * kSortIpt;  // 2048
+constexpr int kMaxPass = 3;                          // 24-bit keys at most (depth keys, <= 16M tiles)
+constexpr int kHistStride = kMaxPass * 256;          // per-view digit histogram words
 constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kCountMask = (1u << 30) - 1;
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-// ------------------------------------------------------------ histogram ----
 // Item counts may live on the device (n_dev != NULL): the host passes a
 // capacity n and the kernels use min(*n_dev, n), so the whole binning chain
 // runs without a host round trip (and can be graph-captured).
@@ -49,36 +59,30 @@ __device__ __forceinline__ int64_t eff_count(int64_t n, const int32_t* n_dev) {
   return d < n ? d : n;
 }
 
-template <typename K>
-__global__ void __launch_bounds__(256) k_radix_hist(const K* __restrict__ keys, int64_t n_cap,
-                                                    const int32_t* n_dev, int begin_bit, int npass,
-                                                    uint32_t* __restrict__ hist) {
-  __shared__ uint32_t sh[8][256];
-  const int64_t n = eff_count(n_cap, n_dev);
-  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
-  __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const K k = keys[i];
-    for (int p = 0; p < npass; ++p) atomicAdd(&sh[p][(uint32_t)(k >> (begin_bit + 8 * p)) & 255u], 1u);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) {
-    const uint32_t c = (&sh[0][0])[i];
-    if (c) atomicAdd(hist + i, c);
-  }
+// blocks per view for grid-stride kernels that flush a block histogram:
+// ~2 blocks per SM over the whole batch
+static unsigned stride_blocks(int64_t n, int nv) {
+  const int64_t want = std::max<int64_t>(1, (int64_t)sm_count() * 2 / nv);
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, want));
 }
 
 // ------------------------------------------------------------- onesweep ----
-template <typename K, bool kIota>
+// Per-view key / value arrays of one pass.
+struct SortIO {
+  const uint32_t* kin[kMaxBatch];
+  const uint32_t* vin[kMaxBatch];   // unused when the pass is an iota pass
+  uint32_t* kout[kMaxBatch];
+  uint32_t* vout[kMaxBatch];
+  const int32_t* n_dev[kMaxBatch];  // device counts (NULL: n_cap)
+};
+
+template <bool kIota>
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(
-    const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
-    uint32_t* __restrict__ vout, int64_t n_cap, const int32_t* n_dev, int shift,
-    const uint32_t* __restrict__ ghist, uint32_t* status, uint32_t* counter) {
-  const int64_t n = eff_count(n_cap, n_dev);
+    const __grid_constant__ SortIO io, int nv, int64_t n_cap, int64_t nblk, int shift, int pass,
+    const uint32_t* __restrict__ ghist_all, uint32_t* status_all, uint32_t* counter) {
   extern __shared__ __align__(16) unsigned char dyn[];
-  K* skeys = reinterpret_cast<K*>(dyn);
-  uint32_t* svals = reinterpret_cast<uint32_t*>(dyn + sizeof(K) * kSortTile);
+  uint32_t* skeys = reinterpret_cast<uint32_t*>(dyn);
+  uint32_t* svals = reinterpret_cast<uint32_t*>(dyn + sizeof(uint32_t) * kSortTile);
   __shared__ uint32_t whist[kSortThreads / 32][256];
   __shared__ uint32_t dstart[256];
   __shared__ int64_t goff[256];
@@ -89,12 +93,20 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   if (tid == 0) bid_s = (int)atomicAdd(counter, 1u);
   for (int i = tid; i < (kSortThreads / 32) * 256; i += kSortThreads) (&whist[0][0])[i] = 0;
   __syncthreads();
-  const int bid = bid_s;
+  const int view = bid_s % nv;
+  const int bid = bid_s / nv;
+  const int64_t n = eff_count(n_cap, io.n_dev[view]);
   const int64_t tile0 = (int64_t)bid * kSortTile;
   if (tile0 >= n && bid > 0) return;  // beyond the device count: nobody waits on us
+  const uint32_t* __restrict__ kin = io.kin[view];
+  const uint32_t* __restrict__ vin = io.vin[view];
+  uint32_t* __restrict__ kout = io.kout[view];
+  uint32_t* __restrict__ vout = io.vout[view];
+  const uint32_t* ghist = ghist_all + (size_t)view * kHistStride + pass * 256;
+  uint32_t* status = status_all + (size_t)view * nblk * 256;
   const uint32_t lt = (1u << lane) - 1u;
 
-  K keys[kSortIpt];
+  uint32_t keys[kSortIpt];
   uint32_t vals[kSortIpt];
   uint32_t rank[kSortIpt];
   uint32_t dig[kSortIpt];
@@ -102,9 +114,9 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   for (int i = 0; i < kSortIpt; ++i) {
     const int64_t idx = tile0 + warp * (32 * kSortIpt) + i * 32 + lane;
     const bool valid = idx < n;
-    keys[i] = valid ? kin[idx] : K(0);
+    keys[i] = valid ? kin[idx] : 0u;
     vals[i] = valid ? (kIota ? (uint32_t)idx : vin[idx]) : 0u;
-    dig[i] = valid ? ((uint32_t)(keys[i] >> shift) & 255u) : 256u;
+    dig[i] = valid ? ((keys[i] >> shift) & 255u) : 256u;
   }
 #pragma unroll
   for (int i = 0; i < kSortIpt; ++i) {
@@ -112,8 +124,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 #if SDGR_SORT_MATCH
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
 #else
-    // warp multi-split by ballots (9 bits: 8 digit bits + the invalid flag);
-    // cheaper than MATCH.ANY, which serialises on the MIO pipe
+    // warp multi-split by ballots (9 bits: 8 digit bits + the invalid flag)
     uint32_t peers = 0xffffffffu;
 #pragma unroll
     for (int b = 0; b < 9; ++b) {
@@ -198,108 +209,129 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   const int64_t rem = n - tile0;
   const int cnt = rem < kSortTile ? (int)rem : kSortTile;
   for (int i = tid; i < cnt; i += kSortThreads) {
-    const K k = skeys[i];
-    const uint32_t d = (uint32_t)(k >> shift) & 255u;
+    const uint32_t k = skeys[i];
+    const uint32_t d = (k >> shift) & 255u;
     const int64_t gp = goff[d] + i;
     kout[gp] = k;
     vout[gp] = svals[i];
   }
 }
 
-template <typename K>
-size_t radix_ws_bytes(int64_t n, int npass) {
+// Radix scratch of a batch: digit histograms (filled by the key producer),
+// per-pass tickets, look-back status words, and the ping-pong key / value
+// arrays (view-strided).
+struct RadixWs {
+  uint32_t* hist;    // [nv][kMaxPass][256]
+  uint32_t* ctr;     // [kMaxPass]
+  uint32_t* status;  // [kMaxPass][nv][nblk][256]
+  uint32_t* kalt;    // [nv][n]
+  uint32_t* valt;    // [nv][n]
+  int64_t nblk;
+  size_t zero_bytes; // hist .. end of status (one memset)
+};
+
+static size_t radix_ws_bytes(int64_t n, int nv) {
   const int64_t nblk = (n + kSortTile - 1) / kSortTile;
   size_t b = 0;
-  b += align_up(sizeof(uint32_t) * 8 * 256);                  // hist
-  b += align_up(sizeof(uint32_t) * 8);                        // counters
-  b += align_up(sizeof(uint32_t) * (size_t)npass * nblk * 256);  // status
-  b += align_up(sizeof(K) * (size_t)n);                       // alt keys
-  b += align_up(sizeof(uint32_t) * (size_t)n);                // alt vals
+  b += align_up(sizeof(uint32_t) * (size_t)nv * kHistStride);
+  b += align_up(sizeof(uint32_t) * kMaxPass);
+  b += align_up(sizeof(uint32_t) * (size_t)kMaxPass * nv * nblk * 256);
+  b += 2 * align_up(sizeof(uint32_t) * (size_t)nv * n);
   return b;
 }
 
-template <typename K>
-void set_sort_smem() {
+static RadixWs radix_layout(char*& p, int64_t n, int nv) {
+  RadixWs r;
+  r.nblk = (n + kSortTile - 1) / kSortTile;
+  char* base = p;
+  r.hist = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * kHistStride);
+  r.ctr = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * kMaxPass);
+  r.status = reinterpret_cast<uint32_t*>(p);
+  p += align_up(sizeof(uint32_t) * (size_t)kMaxPass * nv * r.nblk * 256);
+  r.zero_bytes = (size_t)(p - base);
+  r.kalt = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * n);
+  r.valt = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * n);
+  return r;
+}
+
+static void set_sort_smem() {
   static bool done = false;
   if (done) return;
-  const int bytes = (int)((sizeof(K) + 4) * kSortTile);
-  cudaFuncSetAttribute(k_onesweep<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_onesweep<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  const int bytes = (int)(8 * kSortTile);
+  cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   done = true;
 }
 
-// Stable sort of (key, value) by key bits [begin_bit, end_bit).  vin == NULL
-// means values are the input positions.  Output lands in kout/vout.
-template <typename K>
-int radix_sort(const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64_t n,
-               const int32_t* n_dev, int begin_bit, int end_bit, void* ws, size_t ws_bytes,
-               cudaStream_t st) {
-  if (n <= 0) return SDGR_OK;
-  const int npass = (end_bit - begin_bit + 7) / 8;
-  if (npass < 1 || npass > 8) return SDGR_ERR_INVALID;
-  if (ws_bytes < radix_ws_bytes<K>(n, npass)) return SDGR_ERR_CAPACITY;
-  set_sort_smem<K>();
-  const int64_t nblk = (n + kSortTile - 1) / kSortTile;
-  char* p = static_cast<char*>(ws);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * 8 * 256);
-  uint32_t* ctr = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * 8);
-  uint32_t* status = reinterpret_cast<uint32_t*>(p);
-  const size_t status_bytes = sizeof(uint32_t) * (size_t)npass * nblk * 256;
-  p += align_up(status_bytes);
-  K* kalt = reinterpret_cast<K*>(p); p += align_up(sizeof(K) * (size_t)n);
-  uint32_t* valt = reinterpret_cast<uint32_t*>(p);
-  // hist, counters and status are contiguous: one memset
-  if (cudaMemsetAsync(hist, 0, (size_t)((char*)status - (char*)hist) + status_bytes, st) !=
-      cudaSuccess)
-    return SDGR_ERR_CUDA;
-  const int hist_blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 2);  // fewer global bin REDs
-  k_radix_hist<K><<<hist_blocks, 256, 0, st>>>(kin, n, n_dev, begin_bit, npass, hist);
-  note_launch();
-  const size_t smem = (sizeof(K) + 4) * kSortTile;
-  const K* ki = kin;
-  const uint32_t* vi = vin;
+// Stable sort of each view's (key, value) by key bits [0, 8*npass), values =
+// input positions (iota) when `iota`.  The digit histograms must already be
+// in r.hist and the tickets / status words zeroed.  Output lands in
+// io.kout / io.vout.
+static int radix_passes(const SortIO& io, bool iota, int nv, int64_t n_cap, int npass, const RadixWs& r,
+                        cudaStream_t st) {
+  if (npass < 1 || npass > kMaxPass) return SDGR_ERR_INVALID;
+  set_sort_smem();
+  const size_t smem = 8 * kSortTile;
+  SortIO cur = io;
   for (int pass = 0; pass < npass; ++pass) {
     // the last pass must land in kout: alternate so that it does
     const bool to_out = ((npass - 1 - pass) % 2) == 0;
-    K* ko = to_out ? kout : kalt;
-    uint32_t* vo = to_out ? vout : valt;
-    uint32_t* stat = status + (size_t)pass * nblk * 256;
+    for (int v = 0; v < nv; ++v) {
+      cur.kout[v] = to_out ? io.kout[v] : r.kalt + (size_t)v * n_cap;
+      cur.vout[v] = to_out ? io.vout[v] : r.valt + (size_t)v * n_cap;
+    }
+    uint32_t* stat = r.status + (size_t)pass * nv * r.nblk * 256;
+    const unsigned grid = (unsigned)(r.nblk * nv);
     {
       KernelTimer kt(SDGR_K_ONESWEEP, st);
-      if (pass == 0 && vin == nullptr)
-        k_onesweep<K, true><<<(unsigned)nblk, kSortThreads, smem, st>>>(
-            ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, hist + pass * 256, stat, ctr + pass);
+      if (pass == 0 && iota)
+        k_onesweep<true><<<grid, kSortThreads, smem, st>>>(cur, nv, n_cap, r.nblk, 8 * pass, pass, r.hist, stat,
+                                                           r.ctr + pass);
       else
-        k_onesweep<K, false><<<(unsigned)nblk, kSortThreads, smem, st>>>(
-            ki, vi, ko, vo, n, n_dev, begin_bit + 8 * pass, hist + pass * 256, stat, ctr + pass);
+        k_onesweep<false><<<grid, kSortThreads, smem, st>>>(cur, nv, n_cap, r.nblk, 8 * pass, pass, r.hist, stat,
+                                                            r.ctr + pass);
     }
     note_launch();
-    ki = ko;
-    vi = vo;
+    for (int v = 0; v < nv; ++v) {
+      cur.kin[v] = cur.kout[v];
+      cur.vin[v] = cur.vout[v];
+    }
   }
   return check_launch();
 }
 
-template int radix_sort<uint64_t>(const uint64_t*, const uint32_t*, uint64_t*, uint32_t*,
-                                  int64_t, const int32_t*, int, int, void*, size_t, cudaStream_t);
-template int radix_sort<uint32_t>(const uint32_t*, const uint32_t*, uint32_t*, uint32_t*,
-                                  int64_t, const int32_t*, int, int, void*, size_t, cudaStream_t);
-template size_t radix_ws_bytes<uint64_t>(int64_t, int);
-template size_t radix_ws_bytes<uint32_t>(int64_t, int);
-
-// --------------------------------------------------------------- scan ------
-// --------------------------------------------------------------- scan ------
-// Exclusive scan of v(i) = ntiles[order ? order[i] : i] into out[0..n],
-// out[n] = total.  Three phases: tile sums, scan of sums, tile rescans.
-constexpr int kScanTile = 2048;  // 256 threads x 8
-
-struct TileCount {
-  const int32_t* ntiles;
-  const int32_t* order;
-  __device__ __forceinline__ int32_t operator()(int64_t i) const {
-    return ntiles[order ? order[i] : i];
+// block histogram of up to kMaxPass 8-bit digits, flushed to the view's slot
+struct BlockHist {
+  uint32_t (*sh)[256];
+  __device__ void clear() {
+    for (int i = threadIdx.x; i < kMaxPass * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+  }
+  __device__ void add(uint32_t k, int npass) {
+    for (int p = 0; p < npass; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
+  }
+  __device__ void flush(uint32_t* dst, int npass) {
+    for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) {
+      const uint32_t c = (&sh[0][0])[i];
+      if (c) atomicAdd(dst + i, c);
+    }
   }
 };
+
+// --------------------------------------------------------------- scan ------
+// Exclusive scan of v(i) = ntiles[order ? order[i] : i] into out[0..n],
+// out[n] = total, per view.  Three phases: tile sums, scan of sums, rescans.
+constexpr int kScanTile = 2048;  // 256 threads x 8
+
+struct ScanIO {
+  const int32_t* ntiles[kMaxBatch];
+  const int32_t* order[kMaxBatch];
+  int32_t* out[kMaxBatch];
+};
+
+__device__ __forceinline__ int32_t tile_count(const ScanIO& io, int v, int64_t i) {
+  const int32_t* o = io.order[v];
+  return io.ntiles[v][o ? o[i] : i];
+}
 
 __device__ __forceinline__ int32_t block_excl_scan(int32_t x, int32_t* tmp, int32_t& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -321,21 +353,24 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t x, int32_t* tmp, int3
   return pre + s - x;
 }
 
-__global__ void __launch_bounds__(256) k_scan_reduce(TileCount f, int64_t n, int32_t* sums) {
+__global__ void __launch_bounds__(256) k_scan_reduce(const __grid_constant__ ScanIO io, int64_t n, int32_t* sums,
+                                                     int64_t nb) {
   __shared__ int32_t tmp[8];
+  const int v = blockIdx.y;
   const int64_t t0 = (int64_t)blockIdx.x * kScanTile;
   int32_t acc = 0;
   for (int i = 0; i < 8; ++i) {
     const int64_t idx = t0 + i * 256 + threadIdx.x;
-    if (idx < n) acc += f(idx);
+    if (idx < n) acc += tile_count(io, v, idx);
   }
   int32_t total;
   block_excl_scan(acc, tmp, total);
-  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+  if (threadIdx.x == 0) sums[v * nb + blockIdx.x] = total;
 }
 
-__global__ void __launch_bounds__(1024) k_scan_sums(int32_t* sums, int64_t nb) {
+__global__ void __launch_bounds__(1024) k_scan_sums(int32_t* sums_all, int64_t nb) {
   __shared__ int32_t tmp[32];
+  int32_t* sums = sums_all + blockIdx.x * nb;
   int32_t carry = 0;
   for (int64_t b0 = 0; b0 < nb; b0 += 1024) {
     const int64_t i = b0 + threadIdx.x;
@@ -347,20 +382,22 @@ __global__ void __launch_bounds__(1024) k_scan_sums(int32_t* sums, int64_t nb) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_scan_down(TileCount f, int64_t n, const int32_t* sums,
-                                                   int32_t* out) {
+__global__ void __launch_bounds__(256) k_scan_down(const __grid_constant__ ScanIO io, int64_t n,
+                                                   const int32_t* sums, int64_t nb) {
   __shared__ int32_t tmp[8];
+  const int vw = blockIdx.y;
+  int32_t* out = io.out[vw];
   const int64_t t0 = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 8;  // blocked
   int32_t v[8];
   int32_t acc = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int64_t idx = t0 + i;
-    v[i] = idx < n ? f(idx) : 0;
+    v[i] = idx < n ? tile_count(io, vw, idx) : 0;
     acc += v[i];
   }
   int32_t total;
-  int32_t run = sums[blockIdx.x] + block_excl_scan(acc, tmp, total);
+  int32_t run = sums[vw * nb + blockIdx.x] + block_excl_scan(acc, tmp, total);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int64_t idx = t0 + i;
@@ -370,81 +407,107 @@ __global__ void __launch_bounds__(256) k_scan_down(TileCount f, int64_t n, const
   }
 }
 
-size_t scan_ws_bytes(int64_t n) { return align_up(sizeof(int32_t) * ((n + kScanTile - 1) / kScanTile + 1)); }
+static size_t scan_ws_bytes(int64_t n, int nv) {
+  return align_up(sizeof(int32_t) * (size_t)nv * ((n + kScanTile - 1) / kScanTile + 1));
+}
 
-int scan_counts(const int32_t* ntiles, const int32_t* order, int64_t n, int32_t* out, void* ws,
-                cudaStream_t st) {
+static int scan_counts_batch(const ScanIO& io, int nv, int64_t n, void* ws, cudaStream_t st) {
   const int64_t nb = (n + kScanTile - 1) / kScanTile;
   int32_t* sums = static_cast<int32_t*>(ws);
-  TileCount f{ntiles, order};
-  k_scan_reduce<<<(unsigned)nb, 256, 0, st>>>(f, n, sums);
-  k_scan_sums<<<1, 1024, 0, st>>>(sums, nb);
-  k_scan_down<<<(unsigned)nb, 256, 0, st>>>(f, n, sums, out);
+  k_scan_reduce<<<dim3((unsigned)nb, nv), 256, 0, st>>>(io, n, sums, nb);
+  k_scan_sums<<<nv, 1024, 0, st>>>(sums, nb);
+  k_scan_down<<<dim3((unsigned)nb, nv), 256, 0, st>>>(io, n, sums, nb);
   note_launch(3);
   return check_launch();
 }
 
 // --------------------------------------------------------- pair emission ----
-// One thread per list position i (rank for the comp plane, index for the
+// Grid-stride over list positions i (rank for the comp plane, index for the
 // imaging plane): emit the member tiles of Gaussian g = order[i] at
 // offsets[i].  Tiles come from the 8x8 tile window bitmask, or for huge
 // footprints from an exact FP64 re-enumeration (same test as k_project).
-__global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t* order,
-                                                    const int32_t* offsets, int64_t n,
-                                                    int tiles_x, double cutoff,
-                                                    uint32_t* keys, int32_t* vals,
-                                                    int32_t* pair_start, int64_t cap,
-                                                    int32_t* overflow) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int32_t g = order ? order[i] : (int32_t)i;
-  const int32_t cnt = pl.n_tiles[g];
-  int64_t o = offsets[i];
-  pair_start[g] = (int32_t)o;
-  if (cnt == 0) return;
-  // caller's pair buffers too small: flag it and emit only the pairs that fit,
-  // so every slot below the capacity still holds a real (tile, Gaussian) pair
-  // and the (discarded) rest of the step stays in bounds
-  if (o + cnt > cap) *overflow = 1;
-  if (o >= cap) return;
-  const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
-  const int tx0 = bb.x >> 4, tx1 = bb.y >> 4, ty0 = bb.z >> 4, ty1 = bb.w >> 4;
-  if ((tx1 - tx0) < 8 && (ty1 - ty0) < 8) {
-    uint64_t m = pl.tile_mask[g];
-    while (m) {
-      const int b = __ffsll((long long)m) - 1;
-      m &= m - 1;
-      const int tx = tx0 + (b & 7), ty = ty0 + (b >> 3);
-      keys[o] = (uint32_t)(ty * tiles_x + tx);
-      vals[o] = g;
-      if (++o >= cap) return;
-    }
-    return;
+// The tile sort's digit histograms are accumulated on the way.
+struct EmitIO {
+  sdgr_plane pl[kMaxBatch];
+  const int32_t* order[kMaxBatch];
+  const int32_t* offsets[kMaxBatch];
+  uint32_t* keys[kMaxBatch];
+  int32_t* vals[kMaxBatch];
+  int32_t* pair_start[kMaxBatch];
+  int32_t* overflow[kMaxBatch];
+};
+
+__global__ void __launch_bounds__(256) k_emit_pairs(const __grid_constant__ EmitIO io, int64_t n, int tiles_x,
+                                                    double cutoff, int64_t cap, uint32_t* hist, int npass) {
+  __shared__ uint32_t sh[kMaxPass][256];
+  BlockHist bh{sh};
+  if (hist) {
+    bh.clear();
+    __syncthreads();
   }
+  const int v = blockIdx.y;
+  const sdgr_plane& pl = io.pl[v];
+  const int32_t* order = io.order[v];
+  uint32_t* keys = io.keys[v];
+  int32_t* vals = io.vals[v];
   const bool dense = !isfinite(cutoff);
-  const double2 uv = reinterpret_cast<const double2*>(pl.uv)[g];
-  const double4 A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
-  const double cut2 = dmul(cutoff, cutoff), a01x2 = dmul(2.0, A.y);
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) {
-      bool hit = dense;
-      const int cx0 = max((int)bb.x, tx * kTile), cx1 = min((int)bb.y, tx * kTile + kTile - 1);
-      const int cy0 = max((int)bb.z, ty * kTile), cy1 = min((int)bb.w, ty * kTile + kTile - 1);
-      for (int iv = cy0; iv <= cy1 && !hit; ++iv) {
-        const double dy = dsub((double)iv, uv.y);
-        const double t3 = dmul(A.z, dmul(dy, dy));
-        for (int iu = cx0; iu <= cx1; ++iu) {
-          const double dx = dsub((double)iu, uv.x);
-          const double q = dadd(dadd(dmul(A.x, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
-          if (q <= cut2) { hit = true; break; }
+  const double cut2 = dmul(cutoff, cutoff);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t g = order ? order[i] : (int32_t)i;
+    const int32_t cnt = pl.n_tiles[g];
+    int64_t o = io.offsets[v][i];
+    io.pair_start[v][g] = (int32_t)o;
+    if (cnt == 0) continue;
+    // caller's pair buffers too small: flag it and emit only the pairs that fit,
+    // so every slot below the capacity still holds a real (tile, Gaussian) pair
+    // and the (discarded) rest of the step stays in bounds
+    if (o + cnt > cap) *io.overflow[v] = 1;
+    if (o >= cap || !keys) continue;
+    const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
+    const int tx0 = bb.x >> 4, tx1 = bb.y >> 4, ty0 = bb.z >> 4, ty1 = bb.w >> 4;
+    if ((tx1 - tx0) < 8 && (ty1 - ty0) < 8) {
+      uint64_t m = pl.tile_mask[g];
+      while (m && o < cap) {
+        const int b = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        const uint32_t t = (uint32_t)((ty0 + (b >> 3)) * tiles_x + tx0 + (b & 7));
+        keys[o] = t;
+        vals[o] = g;
+        ++o;
+        if (hist) bh.add(t, npass);
+      }
+      continue;
+    }
+    const double2 uv = reinterpret_cast<const double2*>(pl.uv)[g];
+    const double4 A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
+    const double a01x2 = dmul(2.0, A.y);
+    for (int ty = ty0; ty <= ty1 && o < cap; ++ty)
+      for (int tx = tx0; tx <= tx1 && o < cap; ++tx) {
+        bool hit = dense;
+        const int cx0 = max((int)bb.x, tx * kTile), cx1 = min((int)bb.y, tx * kTile + kTile - 1);
+        const int cy0 = max((int)bb.z, ty * kTile), cy1 = min((int)bb.w, ty * kTile + kTile - 1);
+        for (int iv = cy0; iv <= cy1 && !hit; ++iv) {
+          const double dy = dsub((double)iv, uv.y);
+          const double t3 = dmul(A.z, dmul(dy, dy));
+          for (int iu = cx0; iu <= cx1; ++iu) {
+            const double dx = dsub((double)iu, uv.x);
+            const double q = dadd(dadd(dmul(A.x, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
+            if (q <= cut2) { hit = true; break; }
+          }
+        }
+        if (hit) {
+          const uint32_t t = (uint32_t)(ty * tiles_x + tx);
+          keys[o] = t;
+          vals[o] = g;
+          ++o;
+          if (hist) bh.add(t, npass);
         }
       }
-      if (hit) {
-        keys[o] = (uint32_t)(ty * tiles_x + tx);
-        vals[o] = g;
-        if (++o >= cap) return;
-      }
-    }
+  }
+  if (hist) {
+    __syncthreads();
+    bh.flush(hist + (size_t)v * kHistStride, npass);
+  }
 }
 
 // scene index of each sorted pair: pair_prim[i] = pre_prim[pair_pos[i]]
@@ -453,27 +516,43 @@ __global__ void __launch_bounds__(256) k_emit_pairs(sdgr_plane pl, const int32_t
 // Also the CSR tile ranges of the non-empty tiles, from the run boundaries of
 // the sorted tile ids (range was preset to -1; k_make_items fills the empty
 // tiles' [s, s]).
-__global__ void __launch_bounds__(256) k_gather_prim(const int32_t* pos, const int32_t* pre, int64_t n_cap,
-                                                     const int32_t* n_dev, int32_t* prim,
-                                                     sdgr_plane pl, const double* kappa,
-                                                     const double* phase, sdgr_pair_rec* rec,
-                                                     const uint32_t* keys, int32_t* range) {
+struct GatherIO {
+  const int32_t* pos[kMaxBatch];
+  const int32_t* pre[kMaxBatch];
+  const int32_t* n_dev[kMaxBatch];
+  int32_t* prim[kMaxBatch];
+  const double* uv[kMaxBatch];
+  const double* inv_cov[kMaxBatch];
+  const int16_t* bbox[kMaxBatch];
+  const uint64_t* cell_mask[kMaxBatch];
+  const double* kappa[kMaxBatch];
+  const double* phase[kMaxBatch];
+  sdgr_pair_rec* rec[kMaxBatch];
+  const uint32_t* keys[kMaxBatch];
+  int32_t* range[kMaxBatch];
+};
+
+__global__ void __launch_bounds__(256) k_gather_prim(const __grid_constant__ GatherIO io, int64_t n_cap) {
+  const int v = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n = eff_count(n_cap, n_dev);
+  const int64_t n = eff_count(n_cap, io.n_dev[v]);
   if (i >= n) return;
+  const uint32_t* keys = io.keys[v];
+  int32_t* range = io.range[v];
   const uint32_t t = keys[i];
   if (i == 0 || keys[i - 1] != t) range[2 * t] = (int32_t)i;
   if (i == n - 1 || keys[i + 1] != t) range[2 * t + 1] = (int32_t)(i + 1);
-  const int32_t p = pos[i];
-  const int32_t g = pre[p];
-  prim[i] = g;
+  const int32_t p = io.pos[v][i];
+  const int32_t g = io.pre[v][p];
+  io.prim[v][i] = g;
+  sdgr_pair_rec* rec = io.rec[v];
   if (!rec) return;
-  const double2 uv = reinterpret_cast<const double2*>(pl.uv)[g];
-  const double4 A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
-  const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
+  const double2 uv = reinterpret_cast<const double2*>(io.uv[v])[g];
+  const double4 A = reinterpret_cast<const double4*>(io.inv_cov[v])[g];
+  const short4 bb = reinterpret_cast<const short4*>(io.bbox[v])[g];
   double4* r = reinterpret_cast<double4*>(rec + i);
   r[0] = make_double4(uv.x, uv.y, A.x, A.y);
-  r[1] = make_double4(A.z, kappa[g], phase[g], __longlong_as_double((long long)pl.cell_mask[g]));
+  r[1] = make_double4(A.z, io.kappa[v][g], io.phase[v][g], __longlong_as_double((long long)io.cell_mask[v][g]));
   int4 tail;
   tail.x = (int)(unsigned short)bb.x | ((int)bb.y << 16);
   tail.y = (int)(unsigned short)bb.z | ((int)bb.w << 16);
@@ -483,17 +562,32 @@ __global__ void __launch_bounds__(256) k_gather_prim(const int32_t* pos, const i
 }
 
 // depth-segment work items: each tile list is cut into segments of at most
-// seg_len Gaussians; items are tile-major, segment-minor.
-__global__ void __launch_bounds__(1024) k_make_items(int32_t* range, int n_tiles, int seg_len,
-                                                     int max_items, int32_t* items,
-                                                     int32_t* tile_first, int32_t* n_items,
-                                                     int32_t* overflow, int64_t n_cap, const int32_t* n_dev) {
+// seg_len Gaussians; items are tile-major, segment-minor.  One block per view.
+struct ItemsIO {
+  int32_t* range[kMaxBatch];
+  int32_t* items[kMaxBatch];
+  int32_t* tile_first[kMaxBatch];
+  int32_t* n_items[kMaxBatch];
+  const int32_t* n_dev[kMaxBatch];
+};
+
+__global__ void __launch_bounds__(1024) k_range_init(const __grid_constant__ ItemsIO io, int n_tiles) {
+  int32_t* range = io.range[blockIdx.y];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n_tiles; i += gridDim.x * blockDim.x) range[i] = -1;
+}
+
+__global__ void __launch_bounds__(1024) k_make_items(const __grid_constant__ ItemsIO io, int n_tiles, int seg_len,
+                                                     int max_items, int64_t n_cap) {
   __shared__ int32_t tmp[32];
+  const int v = blockIdx.x;
+  int32_t* range = io.range[v];
+  int32_t* items = io.items[v];
+  int32_t* tile_first = io.tile_first[v];
   // empty tiles (range still -1): [s, s] with s = start of the next non-empty
   // tile, or the pair count -- a suffix min over tiles, chunks last to first
   {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int32_t after = (int32_t)eff_count(n_cap, n_dev);
+    int32_t after = (int32_t)eff_count(n_cap, io.n_dev[v]);
     const int n_chunks = (n_tiles + 1023) / 1024;
     for (int c = n_chunks - 1; c >= 0; --c) {
       const int t = c * 1024 + (1023 - (int)threadIdx.x);   // thread 0 = last tile of the chunk
@@ -543,71 +637,129 @@ __global__ void __launch_bounds__(1024) k_make_items(int32_t* range, int n_tiles
     carry += total;
   }
   if (threadIdx.x == 0) {
-    *n_items = carry < max_items ? carry : max_items;
-    if (carry > max_items) *overflow = 1;
+    io.n_items[v][0] = carry < max_items ? carry : max_items;
+    if (carry > max_items) io.n_items[v][1] = 1;
   }
 }
 
-int launch_emit_and_sort(const sdgr_projection& proj, const sdgr_view& view, const int32_t* order,
-                         const int32_t* offsets, sdgr_tiles& tl, void* ws, size_t ws_bytes,
-                         cudaStream_t st) {
-  const sdgr_plane& pl = tl.plane == 0 ? proj.comp : proj.img;
-  const int64_t n = proj.n, np = tl.n_pairs;  // np: exact count, or capacity with a device count
-  // device-side pair count = offsets[n] (the scan's total) when capacity mode is on
-  const int32_t* n_dev = tl.device_count ? offsets + n : nullptr;
-  if (cudaMemsetAsync(tl.tile_range, 0xff, sizeof(int32_t) * 2 * (size_t)tl.n_tiles, st) != cudaSuccess)
-    return SDGR_ERR_CUDA;
-  // n_items[0] is written by k_make_items; n_items[1] (overflow) is sticky
-  // until the caller clears it, so one check can cover many views.
-  int32_t* overflow = tl.n_items + 1;
-  if (np > 0) {
-    char* p = static_cast<char*>(ws);
-    uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * np);
-    const size_t used = (size_t)(p - static_cast<char*>(ws));
-    if (used > ws_bytes) return SDGR_ERR_CAPACITY;
-    {
-      KernelTimer kt(SDGR_K_EMIT, st);
-      k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,
-                                                                view.cutoff, keys, tl.pre_prim,
-                                                                tl.pair_start, np, overflow);
+// Workspace of a binning batch (plane lists of nv views, pair capacity cap).
+static size_t bin_ws_bytes(int64_t n, int64_t cap, int nv) {
+  return scan_ws_bytes(n, nv) + align_up(sizeof(uint32_t) * (size_t)nv * cap) + radix_ws_bytes(cap, nv);
+}
+
+// Count + emit + tile sort + gather + work items for nv views of one plane.
+// offsets[v]: (n+1) caller arrays receiving the per-view pair offsets.
+int launch_bin_batch(int nv, const sdgr_projection* projs, const sdgr_view* views, int plane,
+                     const int32_t* const* orders, int32_t* const* offsets, sdgr_tiles* tls, bool count,
+                     void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (nv < 1 || nv > kMaxBatch) return SDGR_ERR_INVALID;
+  const int64_t n = projs[0].n, cap = tls[0].n_pairs;
+  const sdgr_tiles& t0 = tls[0];
+  for (int v = 1; v < nv; ++v)
+    if (projs[v].n != n || tls[v].n_pairs != cap || tls[v].n_tiles != t0.n_tiles ||
+        tls[v].tiles_x != t0.tiles_x || tls[v].device_count != t0.device_count || tls[v].plane != t0.plane)
+      return SDGR_ERR_INVALID;
+  if (ws_bytes < bin_ws_bytes(n, std::max<int64_t>(cap, 1), nv)) return SDGR_ERR_CAPACITY;
+  char* p = static_cast<char*>(ws);
+  void* scan_ws = p; p += scan_ws_bytes(n, nv);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * std::max<int64_t>(cap, 1));
+  const RadixWs r = radix_layout(p, std::max<int64_t>(cap, 1), nv);
+
+  if (count) {
+    ScanIO sio;
+    for (int v = 0; v < nv; ++v) {
+      const sdgr_plane& pl = plane == 0 ? projs[v].comp : projs[v].img;
+      sio.ntiles[v] = pl.n_tiles;
+      sio.order[v] = orders ? orders[v] : nullptr;
+      sio.out[v] = offsets[v];
     }
-    note_launch();
-    int bits = 1;
-    while ((1 << bits) < tl.n_tiles) ++bits;
-    // stable by tile; values = pre-sort positions (iota)
-    const int rc = radix_sort<uint32_t>(keys, nullptr, tl.pair_tile,
-                                        reinterpret_cast<uint32_t*>(tl.pair_pos), np, n_dev, 0, bits,
-                                        p, ws_bytes - used, st);
+    const int rc = scan_counts_batch(sio, nv, n, scan_ws, st);
     if (rc != SDGR_OK) return rc;
+  }
+  ItemsIO iio;
+  for (int v = 0; v < nv; ++v) {
+    iio.range[v] = tls[v].tile_range;
+    iio.items[v] = tls[v].items;
+    iio.tile_first[v] = tls[v].tile_first;
+    iio.n_items[v] = tls[v].n_items;
+    // device-side pair count = offsets[n] (the scan's total) in capacity mode
+    iio.n_dev[v] = tls[v].device_count ? offsets[v] + n : nullptr;
+  }
+  k_range_init<<<dim3((unsigned)std::min(8, (2 * t0.n_tiles + 1023) / 1024), nv), 1024, 0, st>>>(iio, t0.n_tiles);
+  note_launch();
+  int bits = 1;
+  while ((1 << bits) < t0.n_tiles) ++bits;
+  const int npass = (bits + 7) / 8;
+  if (npass > kMaxPass) return SDGR_ERR_INVALID;
+  if (cap > 0 && cudaMemsetAsync(r.hist, 0, r.zero_bytes, st) != cudaSuccess) return SDGR_ERR_CUDA;
+  EmitIO eio;
+  for (int v = 0; v < nv; ++v) {
+    eio.pl[v] = plane == 0 ? projs[v].comp : projs[v].img;
+    eio.order[v] = orders ? orders[v] : nullptr;
+    eio.offsets[v] = offsets[v];
+    eio.keys[v] = cap > 0 ? keys + (size_t)v * cap : nullptr;
+    eio.vals[v] = tls[v].pre_prim;
+    eio.pair_start[v] = tls[v].pair_start;
+    eio.overflow[v] = tls[v].n_items + 1;  // sticky until the caller clears it
+  }
+  {
+    KernelTimer kt(SDGR_K_EMIT, st);
+    k_emit_pairs<<<dim3(stride_blocks(n, nv), nv), 256, 0, st>>>(eio, n, t0.tiles_x, views[0].cutoff, cap,
+                                                                 cap > 0 ? r.hist : nullptr, npass);
+  }
+  note_launch();
+  if (cap > 0) {
+    SortIO sio;
+    for (int v = 0; v < nv; ++v) {
+      sio.kin[v] = keys + (size_t)v * cap;
+      sio.vin[v] = nullptr;
+      sio.kout[v] = tls[v].pair_tile;
+      sio.vout[v] = reinterpret_cast<uint32_t*>(tls[v].pair_pos);
+      sio.n_dev[v] = iio.n_dev[v];
+    }
+    // stable by tile; values = pre-sort positions (iota)
+    int rc = radix_passes(sio, true, nv, cap, npass, r, st);
+    if (rc != SDGR_OK) return rc;
+    GatherIO gio;
+    for (int v = 0; v < nv; ++v) {
+      const sdgr_plane& pl = plane == 0 ? projs[v].comp : projs[v].img;
+      gio.pos[v] = tls[v].pair_pos;
+      gio.pre[v] = tls[v].pre_prim;
+      gio.n_dev[v] = iio.n_dev[v];
+      gio.prim[v] = tls[v].pair_prim;
+      gio.uv[v] = pl.uv;
+      gio.inv_cov[v] = pl.inv_cov;
+      gio.bbox[v] = pl.bbox;
+      gio.cell_mask[v] = pl.cell_mask;
+      gio.kappa[v] = projs[v].kappa;
+      gio.phase[v] = projs[v].phase;
+      gio.rec[v] = plane == 0 ? tls[v].pair_rec : nullptr;
+      gio.keys[v] = tls[v].pair_tile;
+      gio.range[v] = tls[v].tile_range;
+    }
     {
       KernelTimer kt(SDGR_K_GATHER, st);
-      k_gather_prim<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(tl.pair_pos, tl.pre_prim, np, n_dev,
-                                                                  tl.pair_prim, pl, proj.kappa, proj.phase,
-                                                                  tl.plane == 0 ? tl.pair_rec : nullptr,
-                                                                  tl.pair_tile, tl.tile_range);
+      k_gather_prim<<<dim3((unsigned)((cap + 255) / 256), nv), 256, 0, st>>>(gio, cap);
     }
     note_launch();
-  } else {
-    k_emit_pairs<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl, order, offsets, n, tl.tiles_x,
-                                                              view.cutoff, nullptr, nullptr,
-                                                              tl.pair_start, 0, overflow);
-    note_launch();
   }
-  k_make_items<<<1, 1024, 0, st>>>(tl.tile_range, tl.n_tiles, tl.seg_len, tl.max_items, tl.items,
-                                   tl.tile_first, tl.n_items, overflow, np, n_dev);
+  k_make_items<<<nv, 1024, 0, st>>>(iio, t0.n_tiles, t0.seg_len, t0.max_items, cap);
   note_launch();
   return check_launch();
 }
 
-size_t binning_ws_bytes(int64_t n, int64_t max_pairs) {
-  // depth sort: range + 32-bit keys (2 arrays) + radix scratch (4 passes of 32-bit keys)
-  const size_t depth = align_up(16) + 2 * align_up(sizeof(uint32_t) * (size_t)n) +
-                       radix_ws_bytes<uint32_t>(n, 4);
-  // pair sort: keys + radix scratch (up to 2 passes of 32-bit keys)
-  const size_t pairs = align_up(sizeof(uint32_t) * (size_t)max_pairs) +
-                       radix_ws_bytes<uint32_t>(max_pairs, 2);
-  const size_t scan = scan_ws_bytes(n);
-  return std::max(std::max(depth, pairs), scan) + 4096;
+// Counting alone (sdgr_count_pairs): offsets per view.
+int launch_count_batch(int nv, const int32_t* const* ntiles, const int32_t* const* orders, int64_t n,
+                       int32_t* const* offsets, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (nv < 1 || nv > kMaxBatch) return SDGR_ERR_INVALID;
+  if (ws_bytes < scan_ws_bytes(n, nv)) return SDGR_ERR_CAPACITY;
+  ScanIO sio;
+  for (int v = 0; v < nv; ++v) {
+    sio.ntiles[v] = ntiles[v];
+    sio.order[v] = orders ? orders[v] : nullptr;
+    sio.out[v] = offsets[v];
+  }
+  return scan_counts_batch(sio, nv, n, ws, st);
 }
 
 // ------------------------------------------------------ depth order --------
@@ -624,12 +776,22 @@ constexpr int kKeyBits = 24;
 constexpr uint32_t kKeyInvisible = (1u << kKeyBits) - 1u;
 constexpr uint32_t kKeyMax = kKeyInvisible - 1u;
 
+struct DepthIO {
+  const uint64_t* key[kMaxBatch];
+  int32_t* order[kMaxBatch];
+};
+
 __device__ __forceinline__ double key_to_depth(uint64_t k) {
   const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double((long long)b);
 }
 
-__global__ void __launch_bounds__(256) k_key_range(const uint64_t* key, int64_t n, unsigned long long* range) {
+// range[2v] = min visible key, range[2v+1] = ~max visible key (both by
+// atomicMin so one 0xff memset initialises them)
+__global__ void __launch_bounds__(256) k_key_range(const __grid_constant__ DepthIO io, int64_t n,
+                                                   unsigned long long* range_all) {
+  const int v = blockIdx.y;
+  const uint64_t* key = io.key[v];
   unsigned long long lo = ~0ull, hi = 0ull;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t k = key[i];
@@ -655,33 +817,53 @@ __global__ void __launch_bounds__(256) k_key_range(const uint64_t* key, int64_t 
       lo = s_lo[w] < lo ? s_lo[w] : lo;
       hi = s_hi[w] > hi ? s_hi[w] : hi;
     }
-    atomicMin(range, lo);
-    atomicMax(range + 1, hi);
+    atomicMin(range_all + 2 * v, lo);
+    atomicMin(range_all + 2 * v + 1, ~hi);
   }
 }
 
-__global__ void __launch_bounds__(256) k_key32(const uint64_t* key, int64_t n, const unsigned long long* range,
-                                               uint32_t* k32) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint64_t k = key[i];
-  if (k == ~0ull) { k32[i] = kKeyInvisible; return; }
-  const double dmin = key_to_depth(range[0]), dmax = key_to_depth(range[1]);
+// 24-bit keys + their three digit histograms
+__global__ void __launch_bounds__(256) k_key32(const __grid_constant__ DepthIO io, int64_t n,
+                                               const unsigned long long* range_all, uint32_t* k32_all,
+                                               uint32_t* hist) {
+  __shared__ uint32_t sh[kMaxPass][256];
+  BlockHist bh{sh};
+  bh.clear();
+  __syncthreads();
+  const int v = blockIdx.y;
+  const uint64_t* key = io.key[v];
+  uint32_t* k32 = k32_all + (size_t)v * n;
+  const double dmin = key_to_depth(range_all[2 * v]), dmax = key_to_depth(~range_all[2 * v + 1]);
   const double span = dsub(dmax, dmin);
-  double q = 0.0;
-  if (span > 0.0) q = dmul(dsub(key_to_depth(k), dmin), (double)kKeyMax / span);
-  k32[i] = (uint32_t)fmin(fmax(q, 0.0), (double)kKeyMax);
+  const double scale = span > 0.0 ? (double)kKeyMax / span : 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = key[i];
+    uint32_t q32 = kKeyInvisible;
+    if (k != ~0ull) {
+      double q = 0.0;
+      if (span > 0.0) q = dmul(dsub(key_to_depth(k), dmin), scale);
+      q32 = (uint32_t)fmin(fmax(q, 0.0), (double)kKeyMax);
+    }
+    k32[i] = q32;
+    bh.add(q32, kMaxPass);
+  }
+  __syncthreads();
+  bh.flush(hist + (size_t)v * kHistStride, kMaxPass);
 }
 
 // one thread per run of equal k32 (runs are rare and short); stable by index
-__global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s, const uint64_t* key, int64_t n,
-                                                  int32_t* order) {
+__global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s_all, const __grid_constant__ DepthIO io,
+                                                  int64_t n) {
+  const int v = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const uint32_t* k32s = k32s_all + (size_t)v * n;
   const uint32_t k = k32s[i];
   if (k == kKeyInvisible) return;                     // invisible tail: order irrelevant
   if (i > 0 && k32s[i - 1] == k) return;               // not a run start
   if (i + 1 >= n || k32s[i + 1] != k) return;          // run of length 1
+  const uint64_t* key = io.key[v];
+  int32_t* order = io.order[v];
   int64_t e = i + 1;
   while (e < n && k32s[e] == k) ++e;
   for (int64_t a = i + 1; a < e; ++a) {                // insertion sort by (key, index)
@@ -699,28 +881,51 @@ __global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s, const ui
   }
 }
 
-int launch_depth_order(const sdgr_projection& proj, int32_t* order, void* ws, size_t ws_bytes,
-                       cudaStream_t st) {
-  const int64_t n = proj.n;
+static size_t depth_ws_bytes(int64_t n, int nv) {
+  return align_up(16 * (size_t)nv) + 2 * align_up(sizeof(uint32_t) * (size_t)nv * n) + radix_ws_bytes(n, nv);
+}
+
+int launch_depth_order_batch(int nv, const sdgr_projection* projs, int32_t* const* orders, void* ws,
+                             size_t ws_bytes, cudaStream_t st) {
+  if (nv < 1 || nv > kMaxBatch) return SDGR_ERR_INVALID;
+  const int64_t n = projs[0].n;
+  for (int v = 1; v < nv; ++v)
+    if (projs[v].n != n) return SDGR_ERR_INVALID;
+  if (ws_bytes < depth_ws_bytes(n, nv)) return SDGR_ERR_CAPACITY;
   char* p = static_cast<char*>(ws);
-  unsigned long long* range = reinterpret_cast<unsigned long long*>(p); p += align_up(16);
-  uint32_t* k32 = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)n);
-  uint32_t* k32s = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)n);
-  const size_t used = (size_t)(p - static_cast<char*>(ws));
-  if (used > ws_bytes) return SDGR_ERR_CAPACITY;
-  if (cudaMemsetAsync(range, 0xff, sizeof(unsigned long long), st) != cudaSuccess ||
-      cudaMemsetAsync(range + 1, 0, sizeof(unsigned long long), st) != cudaSuccess)
+  unsigned long long* range = reinterpret_cast<unsigned long long*>(p); p += align_up(16 * (size_t)nv);
+  uint32_t* k32 = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * n);
+  uint32_t* k32s = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * n);
+  const RadixWs r = radix_layout(p, n, nv);
+  DepthIO dio;
+  for (int v = 0; v < nv; ++v) {
+    dio.key[v] = projs[v].depth_key;
+    dio.order[v] = orders[v];
+  }
+  if (cudaMemsetAsync(range, 0xff, 16 * (size_t)nv, st) != cudaSuccess ||
+      cudaMemsetAsync(r.hist, 0, r.zero_bytes, st) != cudaSuccess)
     return SDGR_ERR_CUDA;
-  const unsigned blocks = (unsigned)((n + 255) / 256);
-  k_key_range<<<std::min<unsigned>(blocks, 148 * 2), 256, 0, st>>>(proj.depth_key, n, range);
-  k_key32<<<blocks, 256, 0, st>>>(proj.depth_key, n, range, k32);
+  const unsigned sb = stride_blocks(n, nv);
+  k_key_range<<<dim3(sb, nv), 256, 0, st>>>(dio, n, range);
+  k_key32<<<dim3(sb, nv), 256, 0, st>>>(dio, n, range, k32, r.hist);
   note_launch(2);
-  const int rc = radix_sort<uint32_t>(k32, nullptr, k32s, reinterpret_cast<uint32_t*>(order), n, nullptr, 0,
-                                      kKeyBits, p, ws_bytes - used, st);
+  SortIO sio;
+  for (int v = 0; v < nv; ++v) {
+    sio.kin[v] = k32 + (size_t)v * n;
+    sio.vin[v] = nullptr;
+    sio.kout[v] = k32s + (size_t)v * n;
+    sio.vout[v] = reinterpret_cast<uint32_t*>(orders[v]);
+    sio.n_dev[v] = nullptr;
+  }
+  const int rc = radix_passes(sio, true, nv, n, kMaxPass, r, st);
   if (rc != SDGR_OK) return rc;
-  k_fix_runs<<<blocks, 256, 0, st>>>(k32s, proj.depth_key, n, order);
+  k_fix_runs<<<dim3((unsigned)((n + 255) / 256), nv), 256, 0, st>>>(k32s, dio, n);
   note_launch();
   return check_launch();
+}
+
+size_t batch_ws_bytes(int64_t n, int64_t max_pairs, int nv) {
+  return std::max(depth_ws_bytes(n, nv), bin_ws_bytes(n, max_pairs, nv)) + 4096;
 }
 
 }  // namespace sdgr

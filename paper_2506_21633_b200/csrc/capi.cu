@@ -51,13 +51,13 @@ void prof_mark(int id, bool begin, cudaStream_t st) {
   }
 }
 
-int launch_project(const sdgr_scene&, const sdgr_view&, sdgr_projection&, cudaStream_t);
-int launch_depth_order(const sdgr_projection&, int32_t*, void*, size_t, cudaStream_t);
-int scan_counts(const int32_t*, const int32_t*, int64_t, int32_t*, void*, cudaStream_t);
-size_t scan_ws_bytes(int64_t);
-size_t binning_ws_bytes(int64_t, int64_t);
-int launch_emit_and_sort(const sdgr_projection&, const sdgr_view&, const int32_t*, const int32_t*,
-                         sdgr_tiles&, void*, size_t, cudaStream_t);
+int launch_project(const sdgr_scene&, int, const sdgr_view*, sdgr_projection*, cudaStream_t);
+int launch_depth_order_batch(int, const sdgr_projection*, int32_t* const*, void*, size_t, cudaStream_t);
+int launch_count_batch(int, const int32_t* const*, const int32_t* const*, int64_t, int32_t* const*, void*, size_t,
+                       cudaStream_t);
+int launch_bin_batch(int, const sdgr_projection*, const sdgr_view*, int, const int32_t* const*, int32_t* const*,
+                     sdgr_tiles*, bool, void*, size_t, cudaStream_t);
+size_t batch_ws_bytes(int64_t, int64_t, int);
 int launch_composite_forward(const sdgr_view&, const sdgr_projection&, const sdgr_tiles&, double,
                              double*, double*, double*, double*, int32_t*, const sdgr_replay*, cudaStream_t);
 int launch_splat(const sdgr_view&, const sdgr_projection&, const double*, double*, double*,
@@ -151,41 +151,83 @@ int sdgr_profile_end(double* ms, int64_t* launches) {
 }
 
 size_t sdgr_workspace_bytes(int64_t n, int64_t max_pairs) {
-  return binning_ws_bytes(n < 1 ? 1 : n, max_pairs < 1 ? 1 : max_pairs);
+  return sdgr_batch_workspace_bytes(n, max_pairs, 1);
+}
+
+size_t sdgr_batch_workspace_bytes(int64_t n, int64_t max_pairs, int n_views) {
+  if (n_views < 1 || n_views > SDGR_MAX_BATCH) return 0;
+  return batch_ws_bytes(n < 1 ? 1 : n, max_pairs < 1 ? 1 : max_pairs, n_views);
 }
 
 int sdgr_project(const sdgr_scene* scene, const sdgr_view* view, sdgr_projection* proj, void* stream) {
-  if (!scene || !proj || !view_ok(view)) return SDGR_ERR_INVALID;
-  if (scene->n < 1 || proj->n != scene->n) return SDGR_ERR_INVALID;
-  if (scene->dtype != 0 && scene->dtype != 1) return SDGR_ERR_INVALID;
-  return launch_project(*scene, *view, *proj, static_cast<cudaStream_t>(stream));
+  return sdgr_project_batch(scene, 1, view, proj, stream);
+}
+
+int sdgr_project_batch(const sdgr_scene* scene, int n_views, const sdgr_view* views, sdgr_projection* projs,
+                       void* stream) {
+  if (!scene || !projs || !views || n_views < 1 || n_views > SDGR_MAX_BATCH) return SDGR_ERR_INVALID;
+  if (scene->n < 1 || (scene->dtype != 0 && scene->dtype != 1)) return SDGR_ERR_INVALID;
+  for (int k = 0; k < n_views; ++k)
+    if (!view_ok(views + k) || projs[k].n != scene->n) return SDGR_ERR_INVALID;
+  return launch_project(*scene, n_views, views, projs, static_cast<cudaStream_t>(stream));
 }
 
 int sdgr_depth_order(const sdgr_projection* proj, int32_t* order, void* ws, size_t ws_bytes,
                      void* stream) {
-  if (!proj || !order || !ws || proj->n < 1) return SDGR_ERR_INVALID;
-  return launch_depth_order(*proj, order, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+  return sdgr_depth_order_batch(1, proj, &order, ws, ws_bytes, stream);
+}
+
+int sdgr_depth_order_batch(int n_views, const sdgr_projection* projs, int32_t* const* orders, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (n_views < 1 || n_views > SDGR_MAX_BATCH || !projs || !orders || !ws) return SDGR_ERR_INVALID;
+  for (int k = 0; k < n_views; ++k)
+    if (!orders[k] || projs[k].n < 1 || projs[k].n != projs[0].n) return SDGR_ERR_INVALID;
+  return launch_depth_order_batch(n_views, projs, orders, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int sdgr_count_pairs(const sdgr_projection* proj, int32_t plane, const int32_t* order,
                      int32_t* offsets, void* ws, size_t ws_bytes, void* stream) {
   if (!proj || !offsets || !ws || proj->n < 1 || (plane != 0 && plane != 1)) return SDGR_ERR_INVALID;
-  if (ws_bytes < scan_ws_bytes(proj->n)) return SDGR_ERR_CAPACITY;
   const sdgr_plane& pl = plane == 0 ? proj->comp : proj->img;
-  return scan_counts(pl.n_tiles, order, proj->n, offsets, ws, static_cast<cudaStream_t>(stream));
+  const int32_t* nt = pl.n_tiles;
+  return launch_count_batch(1, &nt, &order, proj->n, &offsets, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+static bool bin_args_ok(const sdgr_projection* proj, const sdgr_view* view, const int32_t* order,
+                        const int32_t* offsets, const sdgr_tiles* tiles) {
+  if (!proj || !view_ok(view) || !offsets || !tiles_ok(tiles)) return false;
+  if (tiles->plane == 0 && !order) return false;
+  if (!tiles->pair_start) return false;
+  if (tiles->n_pairs > 0 && (!tiles->pair_tile || !tiles->pair_prim || !tiles->pair_pos || !tiles->pre_prim))
+    return false;
+  return true;
 }
 
 int sdgr_bin_pairs(const sdgr_projection* proj, const sdgr_view* view, const int32_t* order,
                    const int32_t* offsets, sdgr_tiles* tiles, void* ws, size_t ws_bytes,
                    void* stream) {
-  if (!proj || !view_ok(view) || !offsets || !tiles_ok(tiles) || !ws) return SDGR_ERR_INVALID;
-  if (tiles->plane == 0 && !order) return SDGR_ERR_INVALID;
-  if (!tiles->pair_start) return SDGR_ERR_INVALID;
-  if (tiles->n_pairs > 0 && (!tiles->pair_tile || !tiles->pair_prim || !tiles->pair_pos || !tiles->pre_prim))
-    return SDGR_ERR_INVALID;
+  if (!ws || !bin_args_ok(proj, view, order, offsets, tiles)) return SDGR_ERR_INVALID;
   if (tiles->n_pairs > 0x7fffffffLL) return SDGR_ERR_CAPACITY;
-  return launch_emit_and_sort(*proj, *view, tiles->plane == 0 ? order : nullptr, offsets, *tiles, ws,
-                              ws_bytes, static_cast<cudaStream_t>(stream));
+  const int32_t* ord = tiles->plane == 0 ? order : nullptr;
+  int32_t* off = const_cast<int32_t*>(offsets);  // read only: counting is off
+  return launch_bin_batch(1, proj, view, tiles->plane, &ord, &off, tiles, false, ws, ws_bytes,
+                          static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_bin_batch(int n_views, const sdgr_projection* projs, const sdgr_view* views, int32_t plane,
+                   const int32_t* const* orders, int32_t* const* offsets, sdgr_tiles* tiles, void* ws,
+                   size_t ws_bytes, void* stream) {
+  if (n_views < 1 || n_views > SDGR_MAX_BATCH || !projs || !views || !offsets || !tiles || !ws ||
+      (plane != 0 && plane != 1) || (plane == 0 && !orders))
+    return SDGR_ERR_INVALID;
+  for (int k = 0; k < n_views; ++k) {
+    if (tiles[k].plane != plane || !bin_args_ok(projs + k, views + k, orders ? orders[k] : nullptr, offsets[k],
+                                                tiles + k))
+      return SDGR_ERR_INVALID;
+    if (tiles[k].n_pairs > 0x7fffffffLL) return SDGR_ERR_CAPACITY;
+  }
+  return launch_bin_batch(n_views, projs, views, plane, plane == 0 ? orders : nullptr, offsets, tiles, true, ws,
+                          ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int sdgr_composite_forward(const sdgr_view* view, const sdgr_projection* proj, const sdgr_tiles* comp,

@@ -78,14 +78,17 @@ __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double
     const double cut2 = dmul(cutoff, cutoff);
     if (small) {
       const double a01x2 = dmul(2.0, a01);
+      const int ncol = x1 - x0 + 1;
       for (int iv = y0; iv <= y1; ++iv) {
         const double dy = dsub((double)iv, v);
         const double t3 = dmul(a11, dmul(dy, dy));
-        for (int iu = x0; iu <= x1; ++iu) {
-          const double dx = dsub((double)iu, u);
+        uint32_t row = 0;   // this row's member bits (32-bit shifts, one 64-bit merge per row)
+        for (int c = 0; c < ncol; ++c) {
+          const double dx = dsub((double)(x0 + c), u);
           const double q = dadd(dadd(dmul(a00, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
-          if (dense || q <= cut2) cmask |= 1ull << ((iv - y0) * 8 + (iu - x0));
+          row |= (uint32_t)(dense || q <= cut2) << c;
         }
+        cmask |= (uint64_t)row << (8 * (iv - y0));
       }
       // member tiles of the (<= 2x2 tile) window from the cell bits: split the
       // window's columns / rows at the tile boundary
@@ -143,33 +146,32 @@ __device__ void plane_empty(const sdgr_plane& pl, int64_t g) {
   pl.n_tiles[g] = 0;
 }
 
+// View batch of K1: per-view constants and outputs, passed by value (the
+// kernel parameter space holds up to SDGR_MAX_BATCH views).
+struct ProjBatch {
+  sdgr_view view[SDGR_MAX_BATCH];
+  sdgr_projection proj[SDGR_MAX_BATCH];
+  int nv;
+};
+
+// One thread per Gaussian, looping over the batch's views: the parameters
+// are read once and the view-independent half of project_all -- quaternion
+// normalisation, R(q), e^s, Sigma = M M^T (scene.py:49-97) and the softplus
+// extinctions (geometry.py:317) -- is computed once per batch instead of once
+// per view.  Per view: x_r, plane coordinates, the two covariance sandwiches,
+// skip/cull, footprints, depth key and the SH phase (geometry.py:249-317).
 template <typename T>
-__global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene scene, sdgr_view view,
-                                                 sdgr_projection proj) {
+__global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene scene, const __grid_constant__ ProjBatch B) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int n_vis = 0, n_skip = 0, n_cull = 0;
-  unsigned long long m_comp = 0, m_img = 0;
-  if (g < scene.n) {
-    const T* P = static_cast<const T*>(scene.positions);
+  const bool live = g < scene.n;
+  const T* P = static_cast<const T*>(scene.positions);
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+  double C00 = 0.0, C01 = 0.0, C02 = 0.0, C11 = 0.0, C12 = 0.0, C22 = 0.0;
+  double kf = 0.0, kb = 0.0;
+  if (live) {
     const T* Q = static_cast<const T*>(scene.rotations);
     const T* L = static_cast<const T*>(scene.log_scales);
-    const double p0 = ld(P, 3 * g), p1 = ld(P, 3 * g + 1), p2 = ld(P, 3 * g + 2);
-    const double* R = view.R;
-    // x_r = positions @ R.T + T  (geometry.py:249; OpenBLAS FMA chain)
-    double xr[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-      xr[i] = dadd(dfma(p2, R[3 * i + 2], dfma(p1, R[3 * i + 1], dmul(p0, R[3 * i]))), view.T[i]);
-    // plane coordinates (geometry.py:78-105) and ndc_to_pixel (:73-75)
-    const double undc = ddiv(dmul(2.0, xr[0]), view.den_u);
-    const double vcndc = ddiv(dmul(2.0, xr[1]), view.den_v);
-    const double vindc = dsub(ddiv(dmul(2.0, xr[2]), view.den_v), view.off_vi);
-    const double uc = dsub(dmul(dmul(dadd(undc, 1.0), 0.5), (double)view.n_u), 0.5);
-    const double vc = dsub(dmul(dmul(dadd(vcndc, 1.0), 0.5), (double)view.n_v), 0.5);
-    const double ui = dsub(dmul(dmul(dadd(undc, 1.0), 0.5), (double)view.n_az), 0.5);
-    const double vi = dsub(dmul(dmul(dadd(vindc, 1.0), 0.5), (double)view.n_rg), 0.5);
-    const double depth = xr[2];
-
+    p0 = ld(P, 3 * g); p1 = ld(P, 3 * g + 1); p2 = ld(P, 3 * g + 2);
     // covariance R(q) diag(e^s)^2 R(q)^T  (scene.py:49-97)
     double q[4];
 #pragma unroll
@@ -195,133 +197,167 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
     for (int i = 0; i < 3; ++i)
 #pragma unroll
       for (int j = 0; j < 3; ++j) M[3 * i + j] = dmul(Rq[3 * i + j], s[j]);
-    double C[9];
+    // Sigma_ij = fma(M_i2, M_j2, fma(M_i1, M_j1, M_i0 M_j0)): symmetric bit for bit
+    auto cij = [&](int i, int j) {
+      return dfma(M[3 * i + 2], M[3 * j + 2], dfma(M[3 * i + 1], M[3 * j + 1], dmul(M[3 * i], M[3 * j])));
+    };
+    C00 = cij(0, 0); C01 = cij(0, 1); C02 = cij(0, 2);
+    C11 = cij(1, 1); C12 = cij(1, 2); C22 = cij(2, 2);
+    const T* K = static_cast<const T*>(scene.ke_raw);
+    kf = softplus64(ld(K, 2 * g));
+    kb = softplus64(ld(K, 2 * g + 1));
+  }
+  const double Cm[9] = {C00, C01, C02, C01, C11, C12, C02, C12, C22};
+
+  for (int k = 0; k < B.nv; ++k) {
+    const sdgr_view& view = B.view[k];
+    const sdgr_projection& proj = B.proj[k];
+    int n_vis = 0, n_skip = 0, n_cull = 0;
+    unsigned long long m_comp = 0, m_img = 0;
+    if (live) {
+      const double* R = view.R;
+      // x_r = positions @ R.T + T  (geometry.py:249; OpenBLAS FMA chain)
+      double xr[3];
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
+      for (int i = 0; i < 3; ++i)
+        xr[i] = dadd(dfma(p2, R[3 * i + 2], dfma(p1, R[3 * i + 1], dmul(p0, R[3 * i]))), view.T[i]);
+      // plane coordinates (geometry.py:78-105) and ndc_to_pixel (:73-75)
+      const double undc = ddiv(dmul(2.0, xr[0]), view.den_u);
+      const double vcndc = ddiv(dmul(2.0, xr[1]), view.den_v);
+      const double vindc = dsub(ddiv(dmul(2.0, xr[2]), view.den_v), view.off_vi);
+      const double uc = dsub(dmul(dmul(dadd(undc, 1.0), 0.5), (double)view.n_u), 0.5);
+      const double vc = dsub(dmul(dmul(dadd(vcndc, 1.0), 0.5), (double)view.n_v), 0.5);
+      const double ui = dsub(dmul(dmul(dadd(undc, 1.0), 0.5), (double)view.n_az), 0.5);
+      const double vi = dsub(dmul(dmul(dadd(vindc, 1.0), 0.5), (double)view.n_rg), 0.5);
+      const double depth = xr[2];
+
+      // sandwich mc C mc^T (geometry.py:269-278): sequential over (b, c)
+      double cc[4], ci[4];
 #pragma unroll
-      for (int j = 0; j < 3; ++j)
-        C[3 * i + j] = dfma(M[3 * i + 2], M[3 * j + 2],
-                            dfma(M[3 * i + 1], M[3 * j + 1], dmul(M[3 * i], M[3 * j])));
-    // sandwich mc C mc^T (geometry.py:269-278): sequential over (b, c)
-    double cc[4], ci[4];
+      for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+        for (int d = 0; d < 2; ++d) {
+          double accc = 0.0, acci = 0.0;
 #pragma unroll
-      for (int d = 0; d < 2; ++d) {
-        double accc = 0.0, acci = 0.0;
-        bool first = true;
+          for (int b = 0; b < 3; ++b)
 #pragma unroll
-        for (int b = 0; b < 3; ++b)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const double tc = dmul(dmul(view.mc[3 * a + b], C[3 * b + c]), view.mc[3 * d + c]);
-            const double ti = dmul(dmul(view.mi[3 * a + b], C[3 * b + c]), view.mi[3 * d + c]);
-            accc = first ? tc : dadd(accc, tc);
-            acci = first ? ti : dadd(acci, ti);
-            first = false;
-          }
-        cc[2 * a + d] = accc;
-        ci[2 * a + d] = acci;
+            for (int c = 0; c < 3; ++c) {
+              const double tc = dmul(dmul(view.mc[3 * a + b], Cm[3 * b + c]), view.mc[3 * d + c]);
+              const double ti = dmul(dmul(view.mi[3 * a + b], Cm[3 * b + c]), view.mi[3 * d + c]);
+              accc = (b == 0 && c == 0) ? tc : dadd(accc, tc);
+              acci = (b == 0 && c == 0) ? ti : dadd(acci, ti);
+            }
+          cc[2 * a + d] = accc;
+          ci[2 * a + d] = acci;
+        }
+      const double cc00 = dadd(cc[0], view.cov_reg), cc11 = dadd(cc[3], view.cov_reg);
+      const double cc01 = dmul(0.5, dadd(cc[1], cc[2]));
+      const double ci00 = dadd(ci[0], view.cov_reg), ci11 = dadd(ci[3], view.cov_reg);
+      const double ci01 = dmul(0.5, dadd(ci[1], ci[2]));
+      const double detc = dsub(dmul(cc00, cc11), dmul(cc01, cc01));
+      const double deti = dsub(dmul(ci00, ci11), dmul(ci01, ci01));
+      const bool finite = isfinite(uc) && isfinite(vc) && isfinite(ui) && isfinite(vi) &&
+                          isfinite(depth) && isfinite(detc) && isfinite(deti);
+      const bool ok = finite && detc > 0.0 && deti > 0.0;
+      const bool dense = !isfinite(view.cutoff);
+      bool inside = true;
+      if (!dense) {
+        // frustum cull (geometry.py:293-305)
+        const double ru = dmul(view.cutoff, dsqrt(np_max0(cc00)));
+        const double rv = dmul(view.cutoff, dsqrt(np_max0(cc11)));
+        inside = (dadd(uc, ru) >= 0.0) && (dsub(uc, ru) <= (double)view.n_u - 1.0) &&
+                 (dadd(vc, rv) >= 0.0) && (dsub(vc, rv) <= (double)view.n_v - 1.0);
       }
-    const double cc00 = dadd(cc[0], view.cov_reg), cc11 = dadd(cc[3], view.cov_reg);
-    const double cc01 = dmul(0.5, dadd(cc[1], cc[2]));
-    const double ci00 = dadd(ci[0], view.cov_reg), ci11 = dadd(ci[3], view.cov_reg);
-    const double ci01 = dmul(0.5, dadd(ci[1], ci[2]));
-    const double detc = dsub(dmul(cc00, cc11), dmul(cc01, cc01));
-    const double deti = dsub(dmul(ci00, ci11), dmul(ci01, ci01));
-    const bool finite = isfinite(uc) && isfinite(vc) && isfinite(ui) && isfinite(vi) &&
-                        isfinite(depth) && isfinite(detc) && isfinite(deti);
-    const bool ok = finite && detc > 0.0 && deti > 0.0;
-    const bool dense = !isfinite(view.cutoff);
-    bool inside = true;
-    if (!dense) {
-      // frustum cull (geometry.py:293-305)
-      const double ru = dmul(view.cutoff, dsqrt(np_max0(cc00)));
-      const double rv = dmul(view.cutoff, dsqrt(np_max0(cc11)));
-      inside = (dadd(uc, ru) >= 0.0) && (dsub(uc, ru) <= (double)view.n_u - 1.0) &&
-               (dadd(vc, rv) >= 0.0) && (dsub(vc, rv) <= (double)view.n_v - 1.0);
-    }
-    const bool vis = ok && inside;
-    n_vis = vis; n_skip = !ok; n_cull = ok && !inside;
-    proj.flags[g] = (uint8_t)((vis ? SDGR_FLAG_VISIBLE : 0) | (!ok ? SDGR_FLAG_SKIPPED : 0) |
-                              ((ok && !inside) ? SDGR_FLAG_CULLED : 0));
-    if (vis) {
-      m_comp = plane_footprint(proj.comp, g, uc, vc, cc00, cc01, cc11, view.n_u, view.n_v, view.cutoff, dense);
-      m_img = plane_footprint(proj.img, g, ui, vi, ci00, ci01, ci11, view.n_az, view.n_rg, view.cutoff, dense);
-      proj.depth_key[g] = depth_key(depth);
-      // phase function and extinction (geometry.py:308-317)
-      const double r0 = p0 - view.cam[0], r1 = p1 - view.cam[1], r2 = p2 - view.cam[2];
-      double dist = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
-      if (dist == 0.0) dist = 1.0;
-      const double d0 = r0 / dist, d1 = r1 / dist, d2 = r2 / dist;
-      double b[16];
-      sh_basis(d0, d1, d2, b);
-      const T* S = static_cast<const T*>(scene.sh_coeffs);
-      double praw = 0.0;
+      const bool vis = ok && inside;
+      n_vis = vis; n_skip = !ok; n_cull = ok && !inside;
+      proj.flags[g] = (uint8_t)((vis ? SDGR_FLAG_VISIBLE : 0) | (!ok ? SDGR_FLAG_SKIPPED : 0) |
+                                ((ok && !inside) ? SDGR_FLAG_CULLED : 0));
+      if (vis) {
+        m_comp = plane_footprint(proj.comp, g, uc, vc, cc00, cc01, cc11, view.n_u, view.n_v, view.cutoff, dense);
+        m_img = plane_footprint(proj.img, g, ui, vi, ci00, ci01, ci11, view.n_az, view.n_rg, view.cutoff, dense);
+        proj.depth_key[g] = depth_key(depth);
+        // phase function and extinction (geometry.py:308-317)
+        const double r0 = p0 - view.cam[0], r1 = p1 - view.cam[1], r2 = p2 - view.cam[2];
+        double dist = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
+        if (dist == 0.0) dist = 1.0;
+        const double d0 = r0 / dist, d1 = r1 / dist, d2 = r2 / dist;
+        double b[16];
+        sh_basis(d0, d1, d2, b);
+        const T* S = static_cast<const T*>(scene.sh_coeffs);
+        double praw = 0.0;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) praw += b[k] * ld(S, 16 * g + k);
-      const T* K = static_cast<const T*>(scene.ke_raw);
-      const double kf = softplus64(ld(K, 2 * g)), kb = softplus64(ld(K, 2 * g + 1));
-      proj.kappa[g] = kf + kb;
-      proj.phase[g] = (praw == praw) ? fmax(praw, 0.0) : praw;  // NaN propagates (np.maximum)
-      proj.phase_raw[g] = praw;
-      if (proj.ke_act) reinterpret_cast<double2*>(proj.ke_act)[g] = make_double2(kf, kb);
-      if (proj.look) reinterpret_cast<double4*>(proj.look)[g] = make_double4(d0, d1, d2, dist);
-    } else {
-      plane_empty(proj.comp, g);
-      plane_empty(proj.img, g);
-      proj.depth_key[g] = ~0ull;
-      proj.kappa[g] = 0.0;
-      proj.phase[g] = 0.0;
-      proj.phase_raw[g] = 0.0;
-      // accessor arrays keep the raw projection for non-visible rows too
-      reinterpret_cast<double2*>(proj.comp.uv)[g] = make_double2(uc, vc);
-      reinterpret_cast<double2*>(proj.img.uv)[g] = make_double2(ui, vi);
-      if (proj.comp.cov) reinterpret_cast<double4*>(proj.comp.cov)[g] = make_double4(cc00, cc01, cc11, 0.0);
-      if (proj.img.cov) reinterpret_cast<double4*>(proj.img.cov)[g] = make_double4(ci00, ci01, ci11, 0.0);
+        for (int j = 0; j < 16; ++j) praw += b[j] * ld(S, 16 * g + j);
+        proj.kappa[g] = kf + kb;
+        proj.phase[g] = (praw == praw) ? fmax(praw, 0.0) : praw;  // NaN propagates (np.maximum)
+        proj.phase_raw[g] = praw;
+        if (proj.ke_act) reinterpret_cast<double2*>(proj.ke_act)[g] = make_double2(kf, kb);
+        if (proj.look) reinterpret_cast<double4*>(proj.look)[g] = make_double4(d0, d1, d2, dist);
+      } else {
+        plane_empty(proj.comp, g);
+        plane_empty(proj.img, g);
+        proj.depth_key[g] = ~0ull;
+        proj.kappa[g] = 0.0;
+        proj.phase[g] = 0.0;
+        proj.phase_raw[g] = 0.0;
+        // accessor arrays keep the raw projection for non-visible rows too
+        reinterpret_cast<double2*>(proj.comp.uv)[g] = make_double2(uc, vc);
+        reinterpret_cast<double2*>(proj.img.uv)[g] = make_double2(ui, vi);
+        if (proj.comp.cov) reinterpret_cast<double4*>(proj.comp.cov)[g] = make_double4(cc00, cc01, cc11, 0.0);
+        if (proj.img.cov) reinterpret_cast<double4*>(proj.img.cov)[g] = make_double4(ci00, ci01, ci11, 0.0);
+      }
     }
-  }
-  // block-aggregated counters
-  n_vis = __syncthreads_count(n_vis);
-  n_skip = __syncthreads_count(n_skip);
-  n_cull = __syncthreads_count(n_cull);
-  if (threadIdx.x == 0) {
-    if (n_vis) atomicAdd(proj.counters + 0, n_vis);
-    if (n_skip) atomicAdd(proj.counters + 1, n_skip);
-    if (n_cull) atomicAdd(proj.counters + 2, n_cull);
-  }
-  if (proj.member_pairs) {
-    // warp-aggregated member-pair counts (replay-log capacity)
+    // block-aggregated counters
+    n_vis = __syncthreads_count(n_vis);
+    n_skip = __syncthreads_count(n_skip);
+    n_cull = __syncthreads_count(n_cull);
+    if (threadIdx.x == 0) {
+      if (n_vis) atomicAdd(proj.counters + 0, n_vis);
+      if (n_skip) atomicAdd(proj.counters + 1, n_skip);
+      if (n_cull) atomicAdd(proj.counters + 2, n_cull);
+    }
+    if (proj.member_pairs) {
+      // warp-aggregated member-pair counts (replay-log capacity)
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      m_comp += __shfl_down_sync(0xffffffffu, m_comp, off);
-      m_img += __shfl_down_sync(0xffffffffu, m_img, off);
-    }
-    if ((threadIdx.x & 31) == 0) {
-      if (m_comp) atomicAdd(proj.member_pairs + 0, m_comp);
-      if (m_img) atomicAdd(proj.member_pairs + 1, m_img);
+      for (int off = 16; off > 0; off >>= 1) {
+        m_comp += __shfl_down_sync(0xffffffffu, m_comp, off);
+        m_img += __shfl_down_sync(0xffffffffu, m_img, off);
+      }
+      if ((threadIdx.x & 31) == 0) {
+        if (m_comp) atomicAdd(proj.member_pairs + 0, m_comp);
+        if (m_img) atomicAdd(proj.member_pairs + 1, m_img);
+      }
     }
   }
 }
 
-int launch_project(const sdgr_scene& scene, const sdgr_view& view, sdgr_projection& proj,
+// zero every view's counters (one launch instead of 2 memsets per view)
+__global__ void k_project_init(const __grid_constant__ ProjBatch B) {
+  const int k = threadIdx.x >> 2, i = threadIdx.x & 3;
+  if (k >= B.nv) return;
+  B.proj[k].counters[i] = 0;
+  if (i < 2 && B.proj[k].member_pairs) B.proj[k].member_pairs[i] = 0ull;
+}
+
+int launch_project(const sdgr_scene& scene, int nv, const sdgr_view* views, sdgr_projection* projs,
                    cudaStream_t stream) {
-  if (scene.n <= 0) return SDGR_ERR_INVALID;
-  if (cudaMemsetAsync(proj.counters, 0, 4 * sizeof(int32_t), stream) != cudaSuccess)
-    return SDGR_ERR_CUDA;
-  if (proj.member_pairs &&
-      cudaMemsetAsync(proj.member_pairs, 0, 2 * sizeof(unsigned long long), stream) != cudaSuccess)
-    return SDGR_ERR_CUDA;
+  if (scene.n <= 0 || nv < 1 || nv > SDGR_MAX_BATCH) return SDGR_ERR_INVALID;
+  ProjBatch B;
+  B.nv = nv;
+  for (int k = 0; k < nv; ++k) {
+    B.view[k] = views[k];
+    B.proj[k] = projs[k];
+  }
+  k_project_init<<<1, 4 * SDGR_MAX_BATCH, 0, stream>>>(B);
   const int threads = 256;
   const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
   {
     KernelTimer kt(SDGR_K_PROJECT, stream);
     if (scene.dtype == 0)
-      k_project<float><<<blocks, threads, 0, stream>>>(scene, view, proj);
+      k_project<float><<<blocks, threads, 0, stream>>>(scene, B);
     else
-      k_project<double><<<blocks, threads, 0, stream>>>(scene, view, proj);
+      k_project<double><<<blocks, threads, 0, stream>>>(scene, B);
   }
-  note_launch();
+  note_launch(2);
   return check_launch();
 }
 

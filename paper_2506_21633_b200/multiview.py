@@ -97,7 +97,9 @@ class MultiViewStep:
         # another view's preprocessing; the batch's geometry joins the lanes
         self.n_lanes = max(1, min(int(lanes), self.geo_batch))
         self.lanes = [self._lane() for _ in range(self.n_lanes)]
-        self.counters, self.member_pairs = self.lanes[0].counters, self.lanes[0].member_pairs
+        # the batched preprocessing (K1-K5 of a whole batch) runs on its own
+        # stream, one batch ahead of the lanes' walks
+        self.pre_stream = torch.cuda.Stream(device=dev)
         # training mode: each view's dL/dS comes from the device loss against
         # its target image (optimize.loss), written into the run's dlds buffer
         self.targets = None
@@ -112,10 +114,11 @@ class MultiViewStep:
                 ln.loss = LossBuffers(*self.img_shape, device=dev)
         # two slot sets: batch b's geometry overlaps batch b+1's views
         self.n_slots = 2 * self.geo_batch if len(self.views) > self.geo_batch else self.geo_batch
-        self.proj_bufs = [self._projection_bufs(self._lane_of(k)) for k in range(self.n_slots)]
+        self.proj_bufs = [self._projection_bufs() for k in range(self.n_slots)]
         self.pds = [pd for pd, _ in self.proj_bufs]
         self.pd = self.pds[0]
-        self.order = self.lanes[0].order
+        self.counters, self.member_pairs = self.proj_bufs[0][1]["counters"], self.proj_bufs[0][1]["member_pairs"]
+        self.order = _empty((n,), torch.int32, dev)
         self.acc_imgs = [_empty((6, n), torch.float64, dev) for _ in range(self.n_slots)]
         self.acc_img = self.acc_imgs[0]
         self.status = torch.zeros((4,), dtype=torch.int32, device=dev)
@@ -138,14 +141,11 @@ class MultiViewStep:
         n, dev = self.n, self.dev
         ln = MultiViewStep._Lane()
         ln.stream = torch.cuda.Stream(device=dev)
-        ln.counters = torch.zeros((4,), dtype=torch.int32, device=dev)
-        ln.member_pairs = torch.zeros((2,), dtype=torch.int64, device=dev)
-        ln.order = _empty((n,), torch.int32, dev)
         ln.intensity = _empty((n,), torch.float64, dev)
         ln.image = _empty(self.img_shape, torch.float64, dev)
         return ln
 
-    def _projection_bufs(self, lane):
+    def _projection_bufs(self):
         """One set of per-view projection records (K1 outputs) + its descriptor."""
         n, dev = self.n, self.dev
         rec = {}
@@ -164,7 +164,9 @@ class MultiViewStep:
                       ("phase_raw", torch.float64), ("flags", torch.uint8)):
             rec[k] = _empty((n,), dt, dev)
             setattr(pd, k, ptr(rec[k]))
-        pd.counters, pd.member_pairs = ptr(lane.counters), ptr(lane.member_pairs)
+        rec["counters"] = torch.zeros((4,), dtype=torch.int32, device=dev)
+        rec["member_pairs"] = torch.zeros((2,), dtype=torch.int64, device=dev)
+        pd.counters, pd.member_pairs = ptr(rec["counters"]), ptr(rec["member_pairs"])
         pd.ke_act = None
         pd.look = None
         return pd, rec
@@ -178,26 +180,23 @@ class MultiViewStep:
     def _alloc_planes(self, cap_pairs: dict):
         n, dev = self.n, self.dev
         v = self.views[0]
-        ws_need = self.lib.sdgr_workspace_bytes(n, max(cap_pairs.values()))
         cap = cap_pairs[0]
         nu, nv = v.n_u, v.n_v
         tx, ty = -(-nu // TILE), -(-nv // TILE)
         seg = _seg_len(cap)
         max_items = -(-cap // seg) + tx * ty
-        # only the computation plane is binned: the splat is Gaussian-parallel
-        for ln in self.lanes:
-            ln.ws = _empty((ws_need,), torch.uint8, dev)
-            ln.ws_bytes = ws_need
+        # per slot: the binning outputs a view's walks and geometry read (the
+        # batched preprocessing of batch b+1 fills one slot set while batch b's
+        # lanes walk the other); only the computation plane is binned -- the
+        # splat is Gaussian-parallel
+        self.slot_t, self.slot_tiles, self.slot_order, self.slot_offsets = [], [], [], []
+        for _ in range(self.n_slots):
             t = dict(
                 pair_tile=_empty((cap,), torch.int32, dev), pair_pos=_empty((cap,), torch.int32, dev),
                 pair_prim=_empty((cap,), torch.int32, dev), pre_prim=_empty((cap,), torch.int32, dev),
                 pair_start=_empty((n,), torch.int32, dev), tile_range=_empty((tx * ty, 2), torch.int32, dev),
                 items=_empty((max_items, 4), torch.int32, dev), tile_first=_empty((tx * ty,), torch.int32, dev),
                 n_items=torch.zeros((4,), dtype=torch.int32, device=dev),
-                seg_a=_empty((max_items * 256,), torch.float64, dev),
-                seg_b=_empty((max_items * 256,), torch.float64, dev),
-                seg_c=_empty((max_items * 256,), torch.float64, dev),
-                partial_I=_empty((cap,), torch.float64, dev),
                 pair_rec=_empty((cap, _lib.PAIR_REC_BYTES), torch.uint8, dev),
             )
             d = _lib.TilesDesc()
@@ -207,23 +206,28 @@ class MultiViewStep:
                       "tile_first", "n_items", "pair_rec"):
                 setattr(d, k, ptr(t[k]))
             d.seg_len, d.max_items, d.device_count = seg, max_items, 1
-            ln.plane = _PlaneBufs(offsets=_empty((n + 1,), torch.int32, dev), tiles=d, t=t)
+            self.slot_t.append(t)
+            self.slot_tiles.append(d)
+            self.slot_order.append(_empty((n,), torch.int32, dev))
+            self.slot_offsets.append(_empty((n + 1,), torch.int32, dev))
+        # one batch workspace: the preprocessing runs on one stream
+        self.ws_bytes = self.lib.sdgr_batch_workspace_bytes(n, cap, self.geo_batch)
+        self.ws = _empty((self.ws_bytes,), torch.uint8, dev)
+        # per lane: the walks' scratch (segment sums, partial intensities, replay log)
+        for ln in self.lanes:
+            ln.t = dict(
+                seg_a=_empty((max_items * 256,), torch.float64, dev),
+                seg_b=_empty((max_items * 256,), torch.float64, dev),
+                seg_c=_empty((max_items * 256,), torch.float64, dev),
+                partial_I=_empty((cap,), torch.float64, dev),
+            )
             ln.splat_scratch = _empty((v.n_rg * v.n_az,), torch.int64, dev)
             # live-pair log: member pairs bound every view's live pairs
             ln.replay = ReplayLog(int(getattr(self, "calib_tc", cap * 16) * self.headroom), max_items, seg, dev, cap)
         ln0 = self.lanes[0]
-        self.planes = {0: ln0.plane}
-        self.ws, self.ws_bytes = ln0.ws, ln0.ws_bytes
         self.replay = ln0.replay
         self.intensity, self.image, self.splat_scratch = ln0.intensity, ln0.image, ln0.splat_scratch
-        # per batch slot (lane = slot mod lanes): pair_start and the partial records
-        self.slot_pair_start = [_empty((n,), torch.int32, dev) for _ in range(self.n_slots)]
         self.slot_partial = [_empty((cap, 8), torch.float64, dev) for _ in range(self.n_slots)]
-        self.slot_tiles = []
-        for k in range(self.n_slots):
-            dk = _lib.TilesDesc.from_buffer_copy(self._lane_of(k).plane.tiles)
-            dk.pair_start = ptr(self.slot_pair_start[k])
-            self.slot_tiles.append(dk)
         self.cap = dict(cap_pairs)
 
     def calibrate(self):
@@ -252,37 +256,48 @@ class MultiViewStep:
         return mx
 
     # -- one view -----------------------------------------------------------
+    def _preprocess(self, views, s0: int, ev=None):
+        """K1-K5 of a batch of views into slots s0..s0+len(views)-1, each stage
+        one launch over the whole batch (sdgr_*_batch), on the current stream."""
+        lib, st, k = self.lib, _stream(), len(views)
+        Views, Projs, Tiles, Ptrs = _lib.View * k, _lib.ProjectionDesc * k, _lib.TilesDesc * k, C.c_void_p * k
+        vs, pds = Views(*views), Projs(*self.pds[s0:s0 + k])
+        orders = Ptrs(*[ptr(o) for o in self.slot_order[s0:s0 + k]])
+        offsets = Ptrs(*[ptr(o) for o in self.slot_offsets[s0:s0 + k]])
+        tiles = Tiles(*self.slot_tiles[s0:s0 + k])
+
+        def mark(i):
+            if ev is not None:
+                ev[i].record()
+        mark(0)
+        _check(lib.sdgr_project_batch(C.byref(self.sd), k, vs, pds, st), "sdgr_project_batch")
+        mark(1)
+        _check(lib.sdgr_depth_order_batch(k, pds, orders, ptr(self.ws), self.ws_bytes, st), "sdgr_depth_order_batch")
+        mark(2)
+        _check(lib.sdgr_bin_batch(k, pds, vs, 0, orders, offsets, tiles, ptr(self.ws), self.ws_bytes, st),
+               "sdgr_bin_batch")
+        mark(3)
+
     def _view(self, v, dlds: torch.Tensor, slot: int, ev=None, ln=None, vi: int = 0):
-        """K1-K9 of one view into batch slot `slot` (the geometry epilogue runs
-        per batch), on the current stream with lane `ln`'s working buffers."""
+        """K6-K9 of one view held in batch slot `slot` (preprocessed by
+        _preprocess; the geometry epilogue runs per batch), on the current
+        stream with lane `ln`'s walk scratch."""
         lib, st = self.lib, _stream()
         ln = ln if ln is not None else self._lane_of(slot)
         pd = C.byref(self.pds[slot])
-        P0 = ln.plane
-        t0 = P0.t
-        td = _lib.TilesDesc.from_buffer_copy(ln.plane.tiles)   # the lane's pair buffers,
-        td.pair_start = self.slot_tiles[slot].pair_start        # the slot's record slots
-        tiles = C.byref(td)
+        t0 = ln.t
+        tiles = C.byref(self.slot_tiles[slot])
         acc = self.acc_imgs[slot]
 
         def mark(i):
             if ev is not None:
                 ev[i].record()
         mark(0)
-        _check(lib.sdgr_project(C.byref(self.sd), C.byref(v), pd, st), "sdgr_project")
-        mark(1)
-        _check(lib.sdgr_depth_order(pd, ptr(ln.order), ptr(ln.ws), ln.ws_bytes, st), "sdgr_depth_order")
-        mark(2)
-        _check(lib.sdgr_count_pairs(pd, 0, ptr(ln.order), ptr(P0.offsets), ptr(ln.ws), ln.ws_bytes, st),
-               "sdgr_count_pairs")
-        _check(lib.sdgr_bin_pairs(pd, C.byref(v), ptr(ln.order), ptr(P0.offsets), tiles,
-                                  ptr(ln.ws), ln.ws_bytes, st), "sdgr_bin_pairs")
-        mark(3)
         _check(lib.sdgr_composite_forward(C.byref(v), pd, tiles, self.s_stop, ptr(t0["seg_a"]),
                                           ptr(t0["seg_b"]), ptr(t0["partial_I"]), ptr(ln.intensity),
                                           ptr(self.status), C.byref(ln.replay.desc_c), st),
                "sdgr_composite_forward")
-        mark(4)
+        mark(1)
         _check(lib.sdgr_splat(C.byref(v), pd, ptr(ln.intensity), ptr(ln.splat_scratch), ptr(ln.image), st),
                "sdgr_splat")
         if self.targets is not None:   # dL/dS of this view from the device loss
@@ -290,16 +305,16 @@ class MultiViewStep:
             _check(lib.sdgr_loss(ptr(ln.image), ptr(self.targets[vi]), h, w, self.lambda_ssim, self.max_val,
                                  C.cast(ln.loss.kernel, C.c_void_p), ptr(self.loss_values[vi]), ptr(dlds),
                                  ptr(ln.loss.scratch), st), "sdgr_loss")
-        mark(5)
+        mark(2)
         _check(lib.sdgr_grad_image(C.byref(v), pd, ptr(ln.intensity), ptr(dlds), ptr(acc), st),
                "sdgr_grad_image")
-        mark(6)
+        mark(3)
         # seg_b holds the forward's exclusive prefixes; seg_a is reused as scratch
         _check(lib.sdgr_grad_intensity(C.byref(v), pd, tiles, self.s_stop, ptr(t0["seg_b"]),
                                        ptr(acc[0]), ptr(t0["seg_a"]), ptr(t0["seg_c"]),
                                        ptr(self.slot_partial[slot]), C.byref(ln.replay.desc_c), st),
                "sdgr_grad_intensity")
-        mark(7)
+        mark(4)
 
     def _lane_of(self, slot: int, n_lanes: int | None = None):
         return self.lanes[(slot % self.geo_batch) % (n_lanes or self.n_lanes)]
@@ -333,10 +348,11 @@ class MultiViewStep:
             raise ValueError("one upstream image gradient per view")
         self.flat_soa.zero_()
         self.status.zero_()
+        for t in self.slot_t:
+            t["n_items"].zero_()        # sticky overflow flags: one check per step
         for ln in self.lanes:
-            ln.plane.t["n_items"].zero_()   # sticky overflow flags: one check per step
             ln.replay.cursor.zero_()
-        evs, gevs = [], []
+        evs, pevs, gevs = [], [], []
         B = self.geo_batch
         n_sets = self.n_slots // B
         main = torch.cuda.current_stream()
@@ -344,26 +360,36 @@ class MultiViewStep:
         start.record(main)             # lanes start after the zeroing above
         L = max(1, min(int(lanes or self.n_lanes), self.n_lanes))
         active = self.lanes[:L]
-        for ln in active:
-            ln.stream.wait_event(start)
+        # one lane = fully serial (each kernel alone on the GPU: the
+        # single-stream timing mode), preprocessing included
+        pre = active[0].stream if L == 1 else self.pre_stream
+        for s_ in set([pre] + [ln.stream for ln in active]):
+            s_.wait_event(start)
         geo_done = [None] * n_sets     # geometry that last read each slot set
         geo_last = None
         for bi, b0 in enumerate(range(0, len(self.views), B)):
             batch = self.views[b0:b0 + B]
             s0 = (bi % n_sets) * B
-            # one lane = fully serial (each kernel alone on the GPU: the
-            # single-stream timing mode); otherwise only slot-set reuse waits
             wait_geo = geo_last if L == 1 else geo_done[bi % n_sets]
             if wait_geo is not None:
-                for ln in active:
-                    ln.stream.wait_event(wait_geo)
+                pre.wait_event(wait_geo)   # the slot set's previous geometry has read it
+            with torch.cuda.stream(pre):
+                pev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timing else None
+                self._preprocess(batch, s0, pev)
+                ready = torch.cuda.Event()
+                ready.record(pre)
+            if timing:
+                pevs.append(pev)
+            for ln in active:
+                ln.stream.wait_event(ready)
             for k, v in enumerate(batch):
                 ln = self._lane_of(s0 + k, L)
                 with torch.cuda.stream(ln.stream):
-                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)] if timing else None
+                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if timing else None
                     self._view(v, dlds[b0 + k], s0 + k, ev, ln, vi=b0 + k)
                     if stats is not None:
-                        stats.append(torch.stack([ln.replay.cursor[0], ln.plane.t["n_items"][0].to(torch.int64)]))
+                        stats.append(torch.stack([ln.replay.cursor[0],
+                                                  self.slot_t[s0 + k]["n_items"][0].to(torch.int64)]))
                 if timing:
                     evs.append(ev)
             for ln in active:          # this batch's views are done (lanes run on)
@@ -376,7 +402,8 @@ class MultiViewStep:
             geo_last = done
             if timing:
                 gevs.append(gev)
-        self.stage_events = (evs, gevs)
+        main.wait_stream(pre)
+        self.stage_events = (evs, pevs, gevs)
         if allreduce and (self.group is not None or
                           (torch.distributed.is_available() and torch.distributed.is_initialized())):
             self.allreduce()
@@ -432,10 +459,10 @@ class MultiViewStep:
     def check(self):
         """One host read per step: capacity overflow and non-finite status."""
         flags = torch.stack([self.status[0].to(torch.int64)] +
-                            [ln.plane.t["n_items"][1].to(torch.int64) for ln in self.lanes] +
+                            [t["n_items"][1].to(torch.int64) for t in self.slot_t] +
                             [ln.replay.cursor[1] for ln in self.lanes])
         f = flags.cpu().tolist()
-        bad, ov0, ov_replay = f[0], any(f[1:1 + self.n_lanes]), any(f[1 + self.n_lanes:])
+        bad, ov0, ov_replay = f[0], any(f[1:1 + self.n_slots]), any(f[1 + self.n_slots:])
         if ov0 or ov_replay:
             raise OverflowError("pair capacity exceeded; recalibrate")
         if bad:
@@ -443,11 +470,15 @@ class MultiViewStep:
 
     def stage_times_ms(self):
         """Per-stage device time summed over the last timed run's views
-        (grad_geometry: summed over its batched launches)."""
-        names = ("project", "depth_sort", "binning", "forward_comp", "splat", "grad_image",
-                 "grad_intensity")
-        out = dict.fromkeys(names + ("grad_geometry",), 0.0)
-        evs, gevs = self.stage_events or ([], [])
+        (project / depth_sort / binning: the batched launches; grad_geometry:
+        summed over its batched launches)."""
+        pre_names = ("project", "depth_sort", "binning")
+        names = ("forward_comp", "splat", "grad_image", "grad_intensity")
+        out = dict.fromkeys(pre_names + names + ("grad_geometry",), 0.0)
+        evs, pevs, gevs = self.stage_events or ([], [], [])
+        for ev in pevs:
+            for i, nm in enumerate(pre_names):
+                out[nm] += ev[i].elapsed_time(ev[i + 1])
         for ev in evs:
             for i, nm in enumerate(names):
                 out[nm] += ev[i].elapsed_time(ev[i + 1])

@@ -26,10 +26,11 @@ dl = torch.randn((a.views, 512, 512), device="cuda", dtype=torch.float64)
 step.run(dl)
 rows = []
 for i, v in enumerate(step.views):
+    step._preprocess([v], 0)
     step._view(v, dl[i], 0)
     torch.cuda.synchronize()
-    t = step.planes[0].t
-    rows.append((int(step.planes[0].offsets[step.n].item()), int(step.member_pairs[0].item()),
+    t = step.slot_t[0]
+    rows.append((int(step.slot_offsets[0][step.n].item()), int(step.member_pairs[0].item()),
                  int(step.member_pairs[1].item()), int(step.replay.cursor[0].item()), int(t["n_items"][0].item())))
 n = len(rows)
 mean = [sum(r[k] for r in rows) / n for k in range(5)]
