@@ -93,6 +93,9 @@ typedef struct sdgr_plane {
   uint64_t* cell_mask;  /* (n) members in the 8x8 cell window at (x0,y0), bit = (iv-y0)*8+(iu-x0) */
   uint64_t* tile_mask;  /* (n) member tiles in the 8x8 tile window at (x0/16,y0/16) */
   int32_t* n_tiles;     /* (n) number of 16x16 tiles holding >= 1 member cell */
+  double* packed;       /* (n,8) optional, computation plane only (NULL = skip): per visible
+                           Gaussian u, v, a00, a01, a11, kappa, phase, cell_mask (bits) in one
+                           64-byte row, so the pair-record gather reads 2 sectors, not 6 */
 } sdgr_plane;
 
 /* Output of sdgr_project (geometry.Projection, geometry.py:185-230). */

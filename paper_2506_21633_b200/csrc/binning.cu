@@ -61,8 +61,8 @@ __device__ __forceinline__ int64_t eff_count(int64_t n, const int32_t* n_dev) {
 
 // blocks per view for grid-stride kernels that flush a block histogram:
 // ~2 blocks per SM over the whole batch
-static unsigned stride_blocks(int64_t n, int nv) {
-  const int64_t want = std::max<int64_t>(1, (int64_t)sm_count() * 2 / nv);
+static unsigned stride_blocks(int64_t n, int nv, int per_sm = 2) {
+  const int64_t want = std::max<int64_t>(1, (int64_t)sm_count() * per_sm / nv);
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, want));
 }
 
@@ -527,11 +527,15 @@ struct GatherIO {
   const uint64_t* cell_mask[kMaxBatch];
   const double* kappa[kMaxBatch];
   const double* phase[kMaxBatch];
+  const double* packed[kMaxBatch];
   sdgr_pair_rec* rec[kMaxBatch];
   const uint32_t* keys[kMaxBatch];
   int32_t* range[kMaxBatch];
 };
 
+// One thread per sorted pair.  With the computation plane's packed 64-byte
+// per-Gaussian rows (sdgr_plane.packed) a pair's record is 2 sectors + the
+// bbox instead of 6 scattered SoA sectors.
 __global__ void __launch_bounds__(256) k_gather_prim(const __grid_constant__ GatherIO io, int64_t n_cap) {
   const int v = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -547,12 +551,19 @@ __global__ void __launch_bounds__(256) k_gather_prim(const __grid_constant__ Gat
   io.prim[v][i] = g;
   sdgr_pair_rec* rec = io.rec[v];
   if (!rec) return;
-  const double2 uv = reinterpret_cast<const double2*>(io.uv[v])[g];
-  const double4 A = reinterpret_cast<const double4*>(io.inv_cov[v])[g];
-  const short4 bb = reinterpret_cast<const short4*>(io.bbox[v])[g];
   double4* r = reinterpret_cast<double4*>(rec + i);
-  r[0] = make_double4(uv.x, uv.y, A.x, A.y);
-  r[1] = make_double4(A.z, io.kappa[v][g], io.phase[v][g], __longlong_as_double((long long)io.cell_mask[v][g]));
+  const short4 bb = reinterpret_cast<const short4*>(io.bbox[v])[g];
+  if (io.packed[v]) {
+    const double4* pk = reinterpret_cast<const double4*>(io.packed[v]) + 2 * g;
+    const double4 r0 = pk[0], r1 = pk[1];
+    r[0] = r0;
+    r[1] = r1;
+  } else {
+    const double2 uv = reinterpret_cast<const double2*>(io.uv[v])[g];
+    const double4 A = reinterpret_cast<const double4*>(io.inv_cov[v])[g];
+    r[0] = make_double4(uv.x, uv.y, A.x, A.y);
+    r[1] = make_double4(A.z, io.kappa[v][g], io.phase[v][g], __longlong_as_double((long long)io.cell_mask[v][g]));
+  }
   int4 tail;
   tail.x = (int)(unsigned short)bb.x | ((int)bb.y << 16);
   tail.y = (int)(unsigned short)bb.z | ((int)bb.w << 16);
@@ -704,7 +715,7 @@ int launch_bin_batch(int nv, const sdgr_projection* projs, const sdgr_view* view
   }
   {
     KernelTimer kt(SDGR_K_EMIT, st);
-    k_emit_pairs<<<dim3(stride_blocks(n, nv), nv), 256, 0, st>>>(eio, n, t0.tiles_x, views[0].cutoff, cap,
+    k_emit_pairs<<<dim3(stride_blocks(n, nv, 8), nv), 256, 0, st>>>(eio, n, t0.tiles_x, views[0].cutoff, cap,
                                                                  cap > 0 ? r.hist : nullptr, npass);
   }
   note_launch();
@@ -733,6 +744,7 @@ int launch_bin_batch(int nv, const sdgr_projection* projs, const sdgr_view* view
       gio.cell_mask[v] = pl.cell_mask;
       gio.kappa[v] = projs[v].kappa;
       gio.phase[v] = projs[v].phase;
+      gio.packed[v] = plane == 0 ? pl.packed : nullptr;
       gio.rec[v] = plane == 0 ? tls[v].pair_rec : nullptr;
       gio.keys[v] = tls[v].pair_tile;
       gio.range[v] = tls[v].tile_range;
@@ -787,19 +799,34 @@ __device__ __forceinline__ double key_to_depth(uint64_t k) {
 }
 
 // range[2v] = min visible key, range[2v+1] = ~max visible key (both by
-// atomicMin so one 0xff memset initialises them)
+// atomicMin so one 0xff memset initialises them).  Each thread reads
+// kKeyIpt keys (pairs of 16-byte loads, block-strided) before reducing.
+constexpr int kKeyIpt = 16;
+
 __global__ void __launch_bounds__(256) k_key_range(const __grid_constant__ DepthIO io, int64_t n,
                                                    unsigned long long* range_all) {
   const int v = blockIdx.y;
   const uint64_t* key = io.key[v];
   unsigned long long lo = ~0ull, hi = 0ull;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = key[i];
-    if (k != ~0ull) {
-      lo = k < lo ? k : lo;
-      hi = k > hi ? k : hi;
+  const int64_t b0 = (int64_t)blockIdx.x * 256 * kKeyIpt;
+  uint64_t k[kKeyIpt];
+#pragma unroll
+  for (int j = 0; j < kKeyIpt / 2; ++j) {
+    const int64_t i = b0 + 2 * (j * 256 + threadIdx.x);
+    if (i + 1 < n) {
+      const ulonglong2 kk = reinterpret_cast<const ulonglong2*>(key + i)[0];
+      k[2 * j] = kk.x; k[2 * j + 1] = kk.y;
+    } else {
+      k[2 * j] = i < n ? key[i] : ~0ull;
+      k[2 * j + 1] = ~0ull;
     }
   }
+#pragma unroll
+  for (int j = 0; j < kKeyIpt; ++j)
+    if (k[j] != ~0ull) {
+      lo = k[j] < lo ? k[j] : lo;
+      hi = k[j] > hi ? k[j] : hi;
+    }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     const unsigned long long a = __shfl_down_sync(0xffffffffu, lo, off);
@@ -817,47 +844,72 @@ __global__ void __launch_bounds__(256) k_key_range(const __grid_constant__ Depth
       lo = s_lo[w] < lo ? s_lo[w] : lo;
       hi = s_hi[w] > hi ? s_hi[w] : hi;
     }
-    atomicMin(range_all + 2 * v, lo);
-    atomicMin(range_all + 2 * v + 1, ~hi);
+    if (lo != ~0ull) atomicMin(range_all + 2 * v, lo);
+    if (hi != 0ull) atomicMin(range_all + 2 * v + 1, ~hi);
   }
 }
 
 // 24-bit keys + their three digit histograms
-__global__ void __launch_bounds__(256) k_key32(const __grid_constant__ DepthIO io, int64_t n,
+__global__ void __launch_bounds__(256) k_key32(const __grid_constant__ DepthIO io, int64_t n, int64_t ks,
                                                const unsigned long long* range_all, uint32_t* k32_all,
                                                uint32_t* hist) {
   __shared__ uint32_t sh[kMaxPass][256];
   BlockHist bh{sh};
   bh.clear();
-  __syncthreads();
   const int v = blockIdx.y;
   const uint64_t* key = io.key[v];
-  uint32_t* k32 = k32_all + (size_t)v * n;
+  uint32_t* k32 = k32_all + (size_t)v * ks;
   const double dmin = key_to_depth(range_all[2 * v]), dmax = key_to_depth(~range_all[2 * v + 1]);
   const double span = dsub(dmax, dmin);
   const double scale = span > 0.0 ? (double)kKeyMax / span : 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = key[i];
-    uint32_t q32 = kKeyInvisible;
-    if (k != ~0ull) {
-      double q = 0.0;
-      if (span > 0.0) q = dmul(dsub(key_to_depth(k), dmin), scale);
-      q32 = (uint32_t)fmin(fmax(q, 0.0), (double)kKeyMax);
+  const int64_t b0 = (int64_t)blockIdx.x * 256 * kKeyIpt;
+  uint64_t k[kKeyIpt];
+#pragma unroll
+  for (int j = 0; j < kKeyIpt / 2; ++j) {
+    const int64_t i = b0 + 2 * (j * 256 + threadIdx.x);
+    if (i + 1 < n) {
+      const ulonglong2 kk = reinterpret_cast<const ulonglong2*>(key + i)[0];
+      k[2 * j] = kk.x; k[2 * j + 1] = kk.y;
+    } else {
+      k[2 * j] = i < n ? key[i] : ~0ull;
+      k[2 * j + 1] = ~0ull;
     }
-    k32[i] = q32;
-    bh.add(q32, kMaxPass);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kKeyIpt / 2; ++j) {
+    const int64_t i = b0 + 2 * (j * 256 + threadIdx.x);
+    uint32_t q2[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      uint32_t q32 = kKeyInvisible;
+      if (k[2 * j + e] != ~0ull) {
+        double q = 0.0;
+        if (span > 0.0) q = dmul(dsub(key_to_depth(k[2 * j + e]), dmin), scale);
+        q32 = (uint32_t)fmin(fmax(q, 0.0), (double)kKeyMax);
+      }
+      q2[e] = q32;
+    }
+    if (i + 1 < n) {
+      reinterpret_cast<uint2*>(k32 + i)[0] = make_uint2(q2[0], q2[1]);
+      bh.add(q2[0], kMaxPass);
+      bh.add(q2[1], kMaxPass);
+    } else if (i < n) {
+      k32[i] = q2[0];
+      bh.add(q2[0], kMaxPass);
+    }
   }
   __syncthreads();
   bh.flush(hist + (size_t)v * kHistStride, kMaxPass);
 }
 
 // one thread per run of equal k32 (runs are rare and short); stable by index
-__global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s_all, const __grid_constant__ DepthIO io,
-                                                  int64_t n) {
+__global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s_all, int64_t ks,
+                                                  const __grid_constant__ DepthIO io, int64_t n) {
   const int v = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint32_t* k32s = k32s_all + (size_t)v * n;
+  const uint32_t* k32s = k32s_all + (size_t)v * ks;
   const uint32_t k = k32s[i];
   if (k == kKeyInvisible) return;                     // invisible tail: order irrelevant
   if (i > 0 && k32s[i - 1] == k) return;               // not a run start
@@ -881,8 +933,12 @@ __global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s_all, cons
   }
 }
 
+// per-view stride of the 24-bit key arrays (keeps uint2 stores aligned)
+static int64_t key_stride(int64_t n) { return (n + 63) & ~int64_t(63); }
+
 static size_t depth_ws_bytes(int64_t n, int nv) {
-  return align_up(16 * (size_t)nv) + 2 * align_up(sizeof(uint32_t) * (size_t)nv * n) + radix_ws_bytes(n, nv);
+  return align_up(16 * (size_t)nv) + 2 * align_up(sizeof(uint32_t) * (size_t)nv * key_stride(n)) +
+         radix_ws_bytes(n, nv);
 }
 
 int launch_depth_order_batch(int nv, const sdgr_projection* projs, int32_t* const* orders, void* ws,
@@ -894,32 +950,34 @@ int launch_depth_order_batch(int nv, const sdgr_projection* projs, int32_t* cons
   if (ws_bytes < depth_ws_bytes(n, nv)) return SDGR_ERR_CAPACITY;
   char* p = static_cast<char*>(ws);
   unsigned long long* range = reinterpret_cast<unsigned long long*>(p); p += align_up(16 * (size_t)nv);
-  uint32_t* k32 = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * n);
-  uint32_t* k32s = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * n);
+  const int64_t ks = key_stride(n);
+  uint32_t* k32 = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * ks);
+  uint32_t* k32s = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * ks);
   const RadixWs r = radix_layout(p, n, nv);
   DepthIO dio;
   for (int v = 0; v < nv; ++v) {
+    if (reinterpret_cast<uintptr_t>(projs[v].depth_key) & 15) return SDGR_ERR_INVALID;  // 16-byte loads
     dio.key[v] = projs[v].depth_key;
     dio.order[v] = orders[v];
   }
   if (cudaMemsetAsync(range, 0xff, 16 * (size_t)nv, st) != cudaSuccess ||
       cudaMemsetAsync(r.hist, 0, r.zero_bytes, st) != cudaSuccess)
     return SDGR_ERR_CUDA;
-  const unsigned sb = stride_blocks(n, nv);
-  k_key_range<<<dim3(sb, nv), 256, 0, st>>>(dio, n, range);
-  k_key32<<<dim3(sb, nv), 256, 0, st>>>(dio, n, range, k32, r.hist);
+  const unsigned kb = (unsigned)((n + 256 * kKeyIpt - 1) / (256 * kKeyIpt));
+  k_key_range<<<dim3(kb, nv), 256, 0, st>>>(dio, n, range);
+  k_key32<<<dim3(kb, nv), 256, 0, st>>>(dio, n, ks, range, k32, r.hist);
   note_launch(2);
   SortIO sio;
   for (int v = 0; v < nv; ++v) {
-    sio.kin[v] = k32 + (size_t)v * n;
+    sio.kin[v] = k32 + (size_t)v * ks;
     sio.vin[v] = nullptr;
-    sio.kout[v] = k32s + (size_t)v * n;
+    sio.kout[v] = k32s + (size_t)v * ks;
     sio.vout[v] = reinterpret_cast<uint32_t*>(orders[v]);
     sio.n_dev[v] = nullptr;
   }
   const int rc = radix_passes(sio, true, nv, n, kMaxPass, r, st);
   if (rc != SDGR_OK) return rc;
-  k_fix_runs<<<dim3((unsigned)((n + 255) / 256), nv), 256, 0, st>>>(k32s, dio, n);
+  k_fix_runs<<<dim3((unsigned)((n + 255) / 256), nv), 256, 0, st>>>(k32s, ks, dio, n);
   note_launch();
   return check_launch();
 }

@@ -27,7 +27,7 @@ constexpr int kChunk = 256;             // Gaussians staged per tile-walk chunk
 // 6.5 -> 6.15 ms/step, k_grad_image 2.57 -> 2.42 on the c4 bench; 5 and 6
 // were slower).  Overridable for A/B builds via SDGR_EXTRA_FLAGS.
 #ifndef SDGR_MINB_PROJECT
-#define SDGR_MINB_PROJECT 2
+#define SDGR_MINB_PROJECT 4
 #endif
 #ifndef SDGR_MINB_REPLAY_GRAD
 #define SDGR_MINB_REPLAY_GRAD 2

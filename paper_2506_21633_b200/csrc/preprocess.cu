@@ -46,10 +46,11 @@ __device__ __forceinline__ double ld(const T* p, int64_t i) { return (double)__l
 // for footprints inside the 8x8 window, the bbox area otherwise).
 __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double v,
                                 double c00, double c01, double c11, int nu, int nv,
-                                double cutoff, bool dense) {
+                                double cutoff, bool dense, double4& rec_out) {
   // invert_cov2d (forward.py:33-42)
   double det = dsub(dmul(c00, c11), dmul(c01, c01));
   double a00 = ddiv(c11, det), a01 = ddiv(-c01, det), a11 = ddiv(c00, det);
+  rec_out = make_double4(a00, a01, a11, 0.0);
   reinterpret_cast<double2*>(pl.uv)[g] = make_double2(u, v);
   reinterpret_cast<double4*>(pl.inv_cov)[g] = make_double4(a00, a01, a11, 0.0);
   if (pl.cov) reinterpret_cast<double4*>(pl.cov)[g] = make_double4(c00, c01, c11, 0.0);
@@ -132,6 +133,7 @@ __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double
   }
   reinterpret_cast<short4*>(pl.bbox)[g] = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
   pl.cell_mask[g] = cmask;
+  rec_out.w = __longlong_as_double((long long)cmask);
   pl.tile_mask[g] = tmask;
   pl.n_tiles[g] = ntiles;
   if (x0 > x1 || y0 > y1) return 0;
@@ -273,8 +275,9 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
       proj.flags[g] = (uint8_t)((vis ? SDGR_FLAG_VISIBLE : 0) | (!ok ? SDGR_FLAG_SKIPPED : 0) |
                                 ((ok && !inside) ? SDGR_FLAG_CULLED : 0));
       if (vis) {
-        m_comp = plane_footprint(proj.comp, g, uc, vc, cc00, cc01, cc11, view.n_u, view.n_v, view.cutoff, dense);
-        m_img = plane_footprint(proj.img, g, ui, vi, ci00, ci01, ci11, view.n_az, view.n_rg, view.cutoff, dense);
+        double4 rc, ri;
+        m_comp = plane_footprint(proj.comp, g, uc, vc, cc00, cc01, cc11, view.n_u, view.n_v, view.cutoff, dense, rc);
+        m_img = plane_footprint(proj.img, g, ui, vi, ci00, ci01, ci11, view.n_az, view.n_rg, view.cutoff, dense, ri);
         proj.depth_key[g] = depth_key(depth);
         // phase function and extinction (geometry.py:308-317)
         const double r0 = p0 - view.cam[0], r1 = p1 - view.cam[1], r2 = p2 - view.cam[2];
@@ -287,8 +290,14 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
         double praw = 0.0;
 #pragma unroll
         for (int j = 0; j < 16; ++j) praw += b[j] * ld(S, 16 * g + j);
+        const double ph = (praw == praw) ? fmax(praw, 0.0) : praw;  // NaN propagates (np.maximum)
         proj.kappa[g] = kf + kb;
-        proj.phase[g] = (praw == praw) ? fmax(praw, 0.0) : praw;  // NaN propagates (np.maximum)
+        proj.phase[g] = ph;
+        if (proj.comp.packed) {
+          double4* pk = reinterpret_cast<double4*>(proj.comp.packed) + 2 * g;
+          pk[0] = make_double4(uc, vc, rc.x, rc.y);
+          pk[1] = make_double4(rc.z, kf + kb, ph, rc.w);
+        }
         proj.phase_raw[g] = praw;
         if (proj.ke_act) reinterpret_cast<double2*>(proj.ke_act)[g] = make_double2(kf, kb);
         if (proj.look) reinterpret_cast<double4*>(proj.look)[g] = make_double4(d0, d1, d2, dist);

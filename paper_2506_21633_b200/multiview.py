@@ -159,6 +159,9 @@ class MultiViewStep:
             pl = _lib.Plane()
             pl.uv, pl.inv_cov, pl.cov, pl.bbox = ptr(r["uv"]), ptr(r["inv_cov"]), None, ptr(r["bbox"])
             pl.cell_mask, pl.tile_mask, pl.n_tiles = ptr(r["cell_mask"]), ptr(r["tile_mask"]), ptr(r["n_tiles"])
+            if name == "comp":   # 64-byte rows the pair-record gather reads
+                r["packed"] = _empty((n, 8), torch.float64, dev)
+                pl.packed = ptr(r["packed"])
             setattr(pd, name, pl)
         for k, dt in (("depth_key", torch.int64), ("kappa", torch.float64), ("phase", torch.float64),
                       ("phase_raw", torch.float64), ("flags", torch.uint8)):

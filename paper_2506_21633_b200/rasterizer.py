@@ -87,6 +87,7 @@ class _PlaneRecords:
         self.cell_mask = _empty((n,), torch.int64, device)
         self.tile_mask = _empty((n,), torch.int64, device)
         self.n_tiles = _empty((n,), torch.int32, device)
+        self.packed = None   # gather rows: multi-view steps only
 
     def desc(self) -> _lib.Plane:
         p = _lib.Plane()
