@@ -96,6 +96,9 @@ typedef struct sdgr_plane {
   double* packed;       /* (n,8) optional, computation plane only (NULL = skip): per visible
                            Gaussian u, v, a00, a01, a11, kappa, phase, cell_mask (bits) in one
                            64-byte row, so the pair-record gather reads 2 sectors, not 6 */
+  uint64_t* emit;       /* (n,2) optional (NULL = skip): bbox (4 x int16) and tile_mask in one
+                           16-byte row per Gaussian, for the fused count + emit pass of
+                           sdgr_bin_batch (1 random sector per Gaussian instead of 4) */
 } sdgr_plane;
 
 /* Output of sdgr_project (geometry.Projection, geometry.py:185-230). */

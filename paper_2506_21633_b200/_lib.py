@@ -50,7 +50,7 @@ class SceneDesc(C.Structure):
 class Plane(C.Structure):
     _fields_ = [
         ("uv", _p), ("inv_cov", _p), ("cov", _p), ("bbox", _p),
-        ("cell_mask", _p), ("tile_mask", _p), ("n_tiles", _p), ("packed", _p),
+        ("cell_mask", _p), ("tile_mask", _p), ("n_tiles", _p), ("packed", _p), ("emit", _p),
     ]
 
 

@@ -118,26 +118,34 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     vals[i] = valid ? (kIota ? (uint32_t)idx : vin[idx]) : 0u;
     dig[i] = valid ? ((keys[i] >> shift) & 255u) : 256u;
   }
+  // peer masks of all items first: the MATCH latencies overlap instead of
+  // each one sitting in front of the per-warp counter update chain
+  uint32_t peers[kSortIpt];
 #pragma unroll
   for (int i = 0; i < kSortIpt; ++i) {
     const uint32_t d = dig[i];
 #if SDGR_SORT_MATCH
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    peers[i] = __match_any_sync(0xffffffffu, d);
 #else
     // warp multi-split by ballots (9 bits: 8 digit bits + the invalid flag)
-    uint32_t peers = 0xffffffffu;
+    uint32_t pm = 0xffffffffu;
 #pragma unroll
     for (int b = 0; b < 9; ++b) {
       const bool bit = (d >> b) & 1u;
       const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-      peers &= bit ? bal : ~bal;
+      pm &= bit ? bal : ~bal;
     }
+    peers[i] = pm;
 #endif
+  }
+#pragma unroll
+  for (int i = 0; i < kSortIpt; ++i) {
+    const uint32_t d = dig[i];
     uint32_t before = 0;
     if (d < 256) before = whist[warp][d];
-    rank[i] = before + __popc(peers & lt);
+    rank[i] = before + __popc(peers[i] & lt);
     __syncwarp();
-    if (d < 256 && lane == __ffs(peers) - 1) whist[warp][d] = before + __popc(peers);
+    if (d < 256 && lane == __ffs(peers[i]) - 1) whist[warp][d] = before + __popc(peers[i]);
     __syncwarp();
   }
   __syncthreads();
@@ -510,6 +518,170 @@ __global__ void __launch_bounds__(256) k_emit_pairs(const __grid_constant__ Emit
   }
 }
 
+// Fused count + emit (the batched multi-view path): one pass over the list
+// positions does what k_scan_reduce / k_scan_sums / k_scan_down + k_emit_pairs
+// do, reading each Gaussian's 16-byte emit row (bbox | tile_mask,
+// sdgr_plane.emit) once.  Block = 2048 consecutive list positions; its pair
+// offset comes from a single-value decoupled look-back (warp-wide window) over
+// the view's earlier blocks, blocks ticketed like the onesweep passes.
+constexpr int kEmitIpt = 8;
+constexpr int kEmitTile = 256 * kEmitIpt;
+constexpr unsigned long long kSFlagA = 1ull << 62, kSFlagP = 2ull << 62, kSValue = (1ull << 62) - 1;
+
+struct FusedEmitIO {
+  const ulonglong2* erow[kMaxBatch];
+  const int32_t* ntiles[kMaxBatch];
+  const double* uv[kMaxBatch];
+  const double* inv_cov[kMaxBatch];
+  const int32_t* order[kMaxBatch];
+  int32_t* offsets[kMaxBatch];
+  uint32_t* keys[kMaxBatch];
+  int32_t* vals[kMaxBatch];
+  int32_t* pair_start[kMaxBatch];
+  int32_t* overflow[kMaxBatch];
+};
+
+__global__ void __launch_bounds__(256) k_count_emit(const __grid_constant__ FusedEmitIO io, int nv, int64_t n,
+                                                    int64_t nblk, int tiles_x, double cutoff, int64_t cap,
+                                                    uint32_t* hist, int npass, unsigned long long* status_all,
+                                                    uint32_t* ticket) {
+  __shared__ uint32_t sh[kMaxPass][256];
+  __shared__ int32_t scnt[kEmitTile];
+  __shared__ int32_t wtmp[8];
+  __shared__ int bid_s;
+  __shared__ long long base_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  BlockHist bh{sh};
+  bh.clear();
+  if (tid == 0) bid_s = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int v = bid_s % nv;
+  const int64_t bid = bid_s / nv;
+  const int64_t tile0 = bid * kEmitTile;
+  const int32_t* order = io.order[v];
+  const ulonglong2* erow = io.erow[v];
+  int32_t g[kEmitIpt], cnt[kEmitIpt];
+  ulonglong2 row[kEmitIpt];
+#pragma unroll
+  for (int k = 0; k < kEmitIpt; ++k) {
+    const int64_t r = tile0 + k * 256 + tid;
+    g[k] = r < n ? (order ? order[r] : (int32_t)r) : -1;
+  }
+#pragma unroll
+  for (int k = 0; k < kEmitIpt; ++k) row[k] = g[k] >= 0 ? erow[g[k]] : make_ulonglong2(0x0000000100000001ull, 0ull);
+#pragma unroll
+  for (int k = 0; k < kEmitIpt; ++k) {
+    const short4 bb = *reinterpret_cast<const short4*>(&row[k].x);
+    const bool tsmall = ((bb.y >> 4) - (bb.x >> 4)) < 8 && ((bb.w >> 4) - (bb.z >> 4)) < 8;
+    cnt[k] = bb.x > bb.y ? 0 : (tsmall ? __popcll(row[k].y) : io.ntiles[v][g[k]]);
+    scnt[k * 256 + tid] = cnt[k];
+  }
+  __syncthreads();
+  // exclusive scan over the tile in list order: thread t owns 8 consecutive slots
+  int32_t loc[kEmitIpt], sum = 0;
+#pragma unroll
+  for (int j = 0; j < kEmitIpt; ++j) {
+    loc[j] = sum;
+    sum += scnt[tid * kEmitIpt + j];
+  }
+  int32_t total;
+  const int32_t texcl = block_excl_scan(sum, wtmp, total);
+#pragma unroll
+  for (int j = 0; j < kEmitIpt; ++j) scnt[tid * kEmitIpt + j] = texcl + loc[j];
+  // tile prefix: decoupled look-back over the view's earlier tiles
+  if (warp == 0) {
+    volatile unsigned long long* status = status_all + (size_t)v * nblk;
+    unsigned long long prefix = 0;
+    if (bid == 0) {
+      if (lane == 0) status[0] = kSFlagP | (unsigned long long)total;
+    } else {
+      if (lane == 0) status[bid] = kSFlagA | (unsigned long long)total;
+      int64_t j = bid - 1;
+      while (true) {
+        const int64_t idx = j - lane;
+        const unsigned long long s = idx >= 0 ? (unsigned long long)status[idx] : (unsigned long long)(2ull << 62);
+        const unsigned long long f = s & ~kSValue;
+        const uint32_t pm = __ballot_sync(0xffffffffu, f == kSFlagP);
+        const uint32_t nr = __ballot_sync(0xffffffffu, f == 0);
+        const int fp = pm ? __ffs(pm) - 1 : 31;            // nearest inclusive prefix (or the window end)
+        const uint32_t upto = fp == 31 ? 0xffffffffu : ((2u << fp) - 1u);
+        if (nr & upto) continue;                           // a nearer tile has not published yet
+        unsigned long long val = lane <= fp ? (s & kSValue) : 0ull;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) val += __shfl_down_sync(0xffffffffu, val, off);
+        prefix += __shfl_sync(0xffffffffu, val, 0);
+        if (pm) break;
+        j -= 32;
+      }
+      if (lane == 0) status[bid] = kSFlagP | (prefix + (unsigned long long)total);
+    }
+    if (lane == 0) base_s = (long long)prefix;
+  }
+  __syncthreads();
+  const int64_t base = base_s;
+  if (tid == 0 && tile0 + kEmitTile >= n) io.offsets[v][n] = (int32_t)(base + total);  // T16 (device count)
+  uint32_t* keys = io.keys[v];
+  int32_t* vals = io.vals[v];
+  const bool dense = !isfinite(cutoff);
+  const double cut2 = dmul(cutoff, cutoff);
+#pragma unroll
+  for (int k = 0; k < kEmitIpt; ++k) {
+    const int64_t r = tile0 + k * 256 + tid;
+    if (r >= n) break;
+    int64_t o = base + scnt[k * 256 + tid];
+    io.offsets[v][r] = (int32_t)o;
+    io.pair_start[v][g[k]] = (int32_t)o;
+    const int32_t c = cnt[k];
+    if (c == 0) continue;
+    if (o + c > cap) *io.overflow[v] = 1;
+    if (o >= cap || !keys) continue;
+    const short4 bb = *reinterpret_cast<const short4*>(&row[k].x);
+    const int tx0 = bb.x >> 4, tx1 = bb.y >> 4, ty0 = bb.z >> 4, ty1 = bb.w >> 4;
+    if ((tx1 - tx0) < 8 && (ty1 - ty0) < 8) {
+      uint64_t m = row[k].y;
+      while (m && o < cap) {
+        const int b = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        const uint32_t t = (uint32_t)((ty0 + (b >> 3)) * tiles_x + tx0 + (b & 7));
+        keys[o] = t;
+        vals[o] = g[k];
+        ++o;
+        if (hist) bh.add(t, npass);
+      }
+      continue;
+    }
+    const double2 uv = reinterpret_cast<const double2*>(io.uv[v])[g[k]];
+    const double4 A = reinterpret_cast<const double4*>(io.inv_cov[v])[g[k]];
+    const double a01x2 = dmul(2.0, A.y);
+    for (int ty = ty0; ty <= ty1 && o < cap; ++ty)
+      for (int tx = tx0; tx <= tx1 && o < cap; ++tx) {
+        bool hit = dense;
+        const int cx0 = max((int)bb.x, tx * kTile), cx1 = min((int)bb.y, tx * kTile + kTile - 1);
+        const int cy0 = max((int)bb.z, ty * kTile), cy1 = min((int)bb.w, ty * kTile + kTile - 1);
+        for (int iv = cy0; iv <= cy1 && !hit; ++iv) {
+          const double dy = dsub((double)iv, uv.y);
+          const double t3 = dmul(A.z, dmul(dy, dy));
+          for (int iu = cx0; iu <= cx1; ++iu) {
+            const double dx = dsub((double)iu, uv.x);
+            const double q = dadd(dadd(dmul(A.x, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
+            if (q <= cut2) { hit = true; break; }
+          }
+        }
+        if (hit) {
+          const uint32_t t = (uint32_t)(ty * tiles_x + tx);
+          keys[o] = t;
+          vals[o] = g[k];
+          ++o;
+          if (hist) bh.add(t, npass);
+        }
+      }
+  }
+  if (hist) {
+    __syncthreads();
+    bh.flush(hist + (size_t)v * kHistStride, npass);
+  }
+}
+
 // scene index of each sorted pair: pair_prim[i] = pre_prim[pair_pos[i]]
 // ... and, for the computation plane, the packed record the tile walks read
 // coalesced instead of gathering from the N-sized projection records.
@@ -540,35 +712,42 @@ __global__ void __launch_bounds__(256) k_gather_prim(const __grid_constant__ Gat
   const int v = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = eff_count(n_cap, io.n_dev[v]);
-  if (i >= n) return;
+  if ((int64_t)blockIdx.x * blockDim.x >= n) return;   // whole block beyond the count
+  const bool live = i < n;
+  const int64_t ii = live ? i : n - 1;                   // dead lanes redo the last pair, store nothing
   const uint32_t* keys = io.keys[v];
   int32_t* range = io.range[v];
-  const uint32_t t = keys[i];
-  if (i == 0 || keys[i - 1] != t) range[2 * t] = (int32_t)i;
-  if (i == n - 1 || keys[i + 1] != t) range[2 * t + 1] = (int32_t)(i + 1);
-  const int32_t p = io.pos[v][i];
+  const uint32_t t = keys[ii];
+  if (live) {
+    if (i == 0 || keys[i - 1] != t) range[2 * t] = (int32_t)i;
+    if (i == n - 1 || keys[i + 1] != t) range[2 * t + 1] = (int32_t)(i + 1);
+  }
+  const int32_t p = io.pos[v][ii];
   const int32_t g = io.pre[v][p];
-  io.prim[v][i] = g;
+  if (live) io.prim[v][i] = g;
   sdgr_pair_rec* rec = io.rec[v];
   if (!rec) return;
-  double4* r = reinterpret_cast<double4*>(rec + i);
   const short4 bb = reinterpret_cast<const short4*>(io.bbox[v])[g];
+  double4 r0, r1;
   if (io.packed[v]) {
     const double4* pk = reinterpret_cast<const double4*>(io.packed[v]) + 2 * g;
-    const double4 r0 = pk[0], r1 = pk[1];
-    r[0] = r0;
-    r[1] = r1;
+    r0 = pk[0];
+    r1 = pk[1];
   } else {
     const double2 uv = reinterpret_cast<const double2*>(io.uv[v])[g];
     const double4 A = reinterpret_cast<const double4*>(io.inv_cov[v])[g];
-    r[0] = make_double4(uv.x, uv.y, A.x, A.y);
-    r[1] = make_double4(A.z, io.kappa[v][g], io.phase[v][g], __longlong_as_double((long long)io.cell_mask[v][g]));
+    r0 = make_double4(uv.x, uv.y, A.x, A.y);
+    r1 = make_double4(A.z, io.kappa[v][g], io.phase[v][g], __longlong_as_double((long long)io.cell_mask[v][g]));
   }
   int4 tail;
   tail.x = (int)(unsigned short)bb.x | ((int)bb.y << 16);
   tail.y = (int)(unsigned short)bb.z | ((int)bb.w << 16);
   tail.z = p;
   tail.w = g;
+  if (!live) return;
+  double4* r = reinterpret_cast<double4*>(rec + i);
+  r[0] = r0;
+  r[1] = r1;
   reinterpret_cast<int4*>(rec + i)[4] = tail;
 }
 
@@ -654,8 +833,13 @@ __global__ void __launch_bounds__(1024) k_make_items(const __grid_constant__ Ite
 }
 
 // Workspace of a binning batch (plane lists of nv views, pair capacity cap).
+static size_t fused_ws_bytes(int64_t n, int nv) {
+  return align_up(sizeof(uint32_t)) + align_up(8 * (size_t)nv * ((n + kEmitTile - 1) / kEmitTile));
+}
+
 static size_t bin_ws_bytes(int64_t n, int64_t cap, int nv) {
-  return scan_ws_bytes(n, nv) + align_up(sizeof(uint32_t) * (size_t)nv * cap) + radix_ws_bytes(cap, nv);
+  return std::max(scan_ws_bytes(n, nv), fused_ws_bytes(n, nv)) + align_up(sizeof(uint32_t) * (size_t)nv * cap) +
+         radix_ws_bytes(cap, nv);
 }
 
 // Count + emit + tile sort + gather + work items for nv views of one plane.
@@ -672,11 +856,14 @@ int launch_bin_batch(int nv, const sdgr_projection* projs, const sdgr_view* view
       return SDGR_ERR_INVALID;
   if (ws_bytes < bin_ws_bytes(n, std::max<int64_t>(cap, 1), nv)) return SDGR_ERR_CAPACITY;
   char* p = static_cast<char*>(ws);
-  void* scan_ws = p; p += scan_ws_bytes(n, nv);
+  void* scan_ws = p; p += std::max(scan_ws_bytes(n, nv), fused_ws_bytes(n, nv));
   uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * std::max<int64_t>(cap, 1));
   const RadixWs r = radix_layout(p, std::max<int64_t>(cap, 1), nv);
 
-  if (count) {
+  // fused count + emit when every view has emit rows (multi-view steps)
+  bool fused = count;
+  for (int v = 0; v < nv; ++v) fused = fused && (plane == 0 ? projs[v].comp.emit : projs[v].img.emit) != nullptr;
+  if (count && !fused) {
     ScanIO sio;
     for (int v = 0; v < nv; ++v) {
       const sdgr_plane& pl = plane == 0 ? projs[v].comp : projs[v].img;
@@ -713,7 +900,32 @@ int launch_bin_batch(int nv, const sdgr_projection* projs, const sdgr_view* view
     eio.pair_start[v] = tls[v].pair_start;
     eio.overflow[v] = tls[v].n_items + 1;  // sticky until the caller clears it
   }
-  {
+  if (fused) {
+    FusedEmitIO fio;
+    for (int v = 0; v < nv; ++v) {
+      const sdgr_plane& pl = plane == 0 ? projs[v].comp : projs[v].img;
+      fio.erow[v] = reinterpret_cast<const ulonglong2*>(pl.emit);
+      fio.ntiles[v] = pl.n_tiles;
+      fio.uv[v] = pl.uv;
+      fio.inv_cov[v] = pl.inv_cov;
+      fio.order[v] = eio.order[v];
+      fio.offsets[v] = offsets[v];
+      fio.keys[v] = eio.keys[v];
+      fio.vals[v] = eio.vals[v];
+      fio.pair_start[v] = eio.pair_start[v];
+      fio.overflow[v] = eio.overflow[v];
+    }
+    const int64_t nblk = (n + kEmitTile - 1) / kEmitTile;
+    uint32_t* ticket = static_cast<uint32_t*>(scan_ws);
+    unsigned long long* status =
+        reinterpret_cast<unsigned long long*>(static_cast<char*>(scan_ws) + align_up(sizeof(uint32_t)));
+    if (cudaMemsetAsync(scan_ws, 0, fused_ws_bytes(n, nv), st) != cudaSuccess) return SDGR_ERR_CUDA;
+    {
+      KernelTimer kt(SDGR_K_EMIT, st);
+      k_count_emit<<<(unsigned)(nblk * nv), 256, 0, st>>>(fio, nv, n, nblk, t0.tiles_x, views[0].cutoff, cap,
+                                                           cap > 0 ? r.hist : nullptr, npass, status, ticket);
+    }
+  } else {
     KernelTimer kt(SDGR_K_EMIT, st);
     k_emit_pairs<<<dim3(stride_blocks(n, nv, 8), nv), 256, 0, st>>>(eio, n, t0.tiles_x, views[0].cutoff, cap,
                                                                  cap > 0 ? r.hist : nullptr, npass);

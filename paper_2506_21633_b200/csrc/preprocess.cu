@@ -40,6 +40,12 @@ __device__ __forceinline__ void sh_basis(double x, double y, double z, double* b
 template <typename T>
 __device__ __forceinline__ double ld(const T* p, int64_t i) { return (double)__ldg(p + i); }
 
+// bbox as the short4 bit pattern (x0, x1, y0, y1) in one u64 (sdgr_plane.emit)
+__device__ __forceinline__ unsigned long long emit_bbox(int x0, int x1, int y0, int y1) {
+  return (unsigned long long)(uint16_t)x0 | ((unsigned long long)(uint16_t)x1 << 16) |
+         ((unsigned long long)(uint16_t)y0 << 32) | ((unsigned long long)(uint16_t)y1 << 48);
+}
+
 // Footprint of one plane: inverse covariance, clipped bbox, member masks.
 // Writes the plane records for Gaussian g.  (forward.py:33-42, 60-109)
 // Returns an upper bound of the Gaussian's member cells on this plane (exact
@@ -80,16 +86,21 @@ __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double
     if (small) {
       const double a01x2 = dmul(2.0, a01);
       const int ncol = x1 - x0 + 1;
-      for (int iv = y0; iv <= y1; ++iv) {
-        const double dy = dsub((double)iv, v);
+      // cell centres as exact FP64 integers stepped by 1.0 (no int->double
+      // conversion per cell; (double)(x0 + c) has the same bits)
+      const double fx0 = (double)x0;
+      double fy = (double)y0;
+      for (int r = 0; r <= y1 - y0; ++r, fy += 1.0) {
+        const double dy = dsub(fy, v);
         const double t3 = dmul(a11, dmul(dy, dy));
         uint32_t row = 0;   // this row's member bits (32-bit shifts, one 64-bit merge per row)
-        for (int c = 0; c < ncol; ++c) {
-          const double dx = dsub((double)(x0 + c), u);
+        double fx = fx0;
+        for (int c = 0; c < ncol; ++c, fx += 1.0) {
+          const double dx = dsub(fx, u);
           const double q = dadd(dadd(dmul(a00, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
           row |= (uint32_t)(dense || q <= cut2) << c;
         }
-        cmask |= (uint64_t)row << (8 * (iv - y0));
+        cmask |= (uint64_t)row << (8 * r);
       }
       // member tiles of the (<= 2x2 tile) window from the cell bits: split the
       // window's columns / rows at the tile boundary
@@ -135,6 +146,9 @@ __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double
   pl.cell_mask[g] = cmask;
   rec_out.w = __longlong_as_double((long long)cmask);
   pl.tile_mask[g] = tmask;
+  if (pl.emit)
+    reinterpret_cast<ulonglong2*>(pl.emit)[g] =
+        make_ulonglong2(emit_bbox(x0, x1, y0, y1), (unsigned long long)tmask);
   pl.n_tiles[g] = ntiles;
   if (x0 > x1 || y0 > y1) return 0;
   if ((x1 - x0) < 8 && (y1 - y0) < 8) return __popcll(cmask);
@@ -143,6 +157,7 @@ __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double
 
 __device__ void plane_empty(const sdgr_plane& pl, int64_t g) {
   reinterpret_cast<short4*>(pl.bbox)[g] = make_short4(1, 0, 1, 0);
+  if (pl.emit) reinterpret_cast<ulonglong2*>(pl.emit)[g] = make_ulonglong2(emit_bbox(1, 0, 1, 0), 0ull);
   pl.cell_mask[g] = 0;
   pl.tile_mask[g] = 0;
   pl.n_tiles[g] = 0;
@@ -209,7 +224,18 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
     kf = softplus64(ld(K, 2 * g));
     kb = softplus64(ld(K, 2 * g + 1));
   }
-  const double Cm[9] = {C00, C01, C02, C01, C11, C12, C02, C12, C22};
+  // view-independent state lives in shared memory across the view loop (keeps
+  // the per-view FP64 chain inside 64 registers without spills); per-view
+  // counters are block accumulators flushed once at the end
+  __shared__ double s_state[11][256];
+  __shared__ unsigned long long s_cnt[SDGR_MAX_BATCH][5];
+  {
+    const double st[11] = {p0, p1, p2, C00, C01, C02, C11, C12, C22, kf, kb};
+#pragma unroll
+    for (int j = 0; j < 11; ++j) s_state[j][threadIdx.x] = st[j];
+    for (int i = threadIdx.x; i < SDGR_MAX_BATCH * 5; i += blockDim.x) (&s_cnt[0][0])[i] = 0ull;
+  }
+  __syncthreads();
 
   for (int k = 0; k < B.nv; ++k) {
     const sdgr_view& view = B.view[k];
@@ -217,6 +243,10 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
     int n_vis = 0, n_skip = 0, n_cull = 0;
     unsigned long long m_comp = 0, m_img = 0;
     if (live) {
+      const double p0 = s_state[0][threadIdx.x], p1 = s_state[1][threadIdx.x], p2 = s_state[2][threadIdx.x];
+      const double Cm[9] = {s_state[3][threadIdx.x], s_state[4][threadIdx.x], s_state[5][threadIdx.x],
+                            s_state[4][threadIdx.x], s_state[6][threadIdx.x], s_state[7][threadIdx.x],
+                            s_state[5][threadIdx.x], s_state[7][threadIdx.x], s_state[8][threadIdx.x]};
       const double* R = view.R;
       // x_r = positions @ R.T + T  (geometry.py:249; OpenBLAS FMA chain)
       double xr[3];
@@ -291,15 +321,16 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
 #pragma unroll
         for (int j = 0; j < 16; ++j) praw += b[j] * ld(S, 16 * g + j);
         const double ph = (praw == praw) ? fmax(praw, 0.0) : praw;  // NaN propagates (np.maximum)
-        proj.kappa[g] = kf + kb;
+        const double kfv = s_state[9][threadIdx.x], kbv = s_state[10][threadIdx.x], kappa_g = kfv + kbv;
+        proj.kappa[g] = kappa_g;
         proj.phase[g] = ph;
         if (proj.comp.packed) {
           double4* pk = reinterpret_cast<double4*>(proj.comp.packed) + 2 * g;
           pk[0] = make_double4(uc, vc, rc.x, rc.y);
-          pk[1] = make_double4(rc.z, kf + kb, ph, rc.w);
+          pk[1] = make_double4(rc.z, kappa_g, ph, rc.w);
         }
         proj.phase_raw[g] = praw;
-        if (proj.ke_act) reinterpret_cast<double2*>(proj.ke_act)[g] = make_double2(kf, kb);
+        if (proj.ke_act) reinterpret_cast<double2*>(proj.ke_act)[g] = make_double2(kfv, kbv);
         if (proj.look) reinterpret_cast<double4*>(proj.look)[g] = make_double4(d0, d1, d2, dist);
       } else {
         plane_empty(proj.comp, g);
@@ -315,26 +346,30 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
         if (proj.img.cov) reinterpret_cast<double4*>(proj.img.cov)[g] = make_double4(ci00, ci01, ci11, 0.0);
       }
     }
-    // block-aggregated counters
-    n_vis = __syncthreads_count(n_vis);
-    n_skip = __syncthreads_count(n_skip);
-    n_cull = __syncthreads_count(n_cull);
-    if (threadIdx.x == 0) {
-      if (n_vis) atomicAdd(proj.counters + 0, n_vis);
-      if (n_skip) atomicAdd(proj.counters + 1, n_skip);
-      if (n_cull) atomicAdd(proj.counters + 2, n_cull);
-    }
-    if (proj.member_pairs) {
-      // warp-aggregated member-pair counts (replay-log capacity)
+    // warp-aggregated into the block's shared counters (no block barrier per view)
+    const int cv = __popc(__ballot_sync(0xffffffffu, n_vis)), cs = __popc(__ballot_sync(0xffffffffu, n_skip)),
+              cc = __popc(__ballot_sync(0xffffffffu, n_cull));
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        m_comp += __shfl_down_sync(0xffffffffu, m_comp, off);
-        m_img += __shfl_down_sync(0xffffffffu, m_img, off);
-      }
-      if ((threadIdx.x & 31) == 0) {
-        if (m_comp) atomicAdd(proj.member_pairs + 0, m_comp);
-        if (m_img) atomicAdd(proj.member_pairs + 1, m_img);
-      }
+    for (int off = 16; off > 0; off >>= 1) {
+      m_comp += __shfl_down_sync(0xffffffffu, m_comp, off);
+      m_img += __shfl_down_sync(0xffffffffu, m_img, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (cv) atomicAdd(&s_cnt[k][0], (unsigned long long)cv);
+      if (cs) atomicAdd(&s_cnt[k][1], (unsigned long long)cs);
+      if (cc) atomicAdd(&s_cnt[k][2], (unsigned long long)cc);
+      if (m_comp) atomicAdd(&s_cnt[k][3], m_comp);
+      if (m_img) atomicAdd(&s_cnt[k][4], m_img);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 5 * B.nv) {
+    const int k = threadIdx.x / 5, j = threadIdx.x % 5;
+    const unsigned long long c = s_cnt[k][j];
+    const sdgr_projection& proj = B.proj[k];
+    if (c) {
+      if (j < 3) atomicAdd(proj.counters + j, (int)c);
+      else if (proj.member_pairs) atomicAdd(proj.member_pairs + (j - 3), c);
     }
   }
 }

@@ -162,6 +162,8 @@ class MultiViewStep:
             if name == "comp":   # 64-byte rows the pair-record gather reads
                 r["packed"] = _empty((n, 8), torch.float64, dev)
                 pl.packed = ptr(r["packed"])
+                r["emit"] = _empty((n, 2), torch.int64, dev)
+                pl.emit = ptr(r["emit"])
             setattr(pd, name, pl)
         for k, dt in (("depth_key", torch.int64), ("kappa", torch.float64), ("phase", torch.float64),
                       ("phase_raw", torch.float64), ("flags", torch.uint8)):

@@ -88,6 +88,7 @@ class _PlaneRecords:
         self.tile_mask = _empty((n,), torch.int64, device)
         self.n_tiles = _empty((n,), torch.int32, device)
         self.packed = None   # gather rows: multi-view steps only
+        self.emit = None     # fused count + emit rows: multi-view steps only
 
     def desc(self) -> _lib.Plane:
         p = _lib.Plane()
