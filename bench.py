@@ -216,7 +216,7 @@ def run_reference(args):
 # ----------------------------------------------------------------------------- GPU side
 SCENE_B = 12 + 16 + 12 + 64 + 8          # f32 positions, rotations, log_scales, sh_coeffs, ke_raw per Gaussian
 GRAD_RMW_B = 2 * (29 * 4 + 4)            # f32 gradient groups + int32 visible count, read + written
-PROJ_W_B = 2 * (16 + 32 + 8 + 8 + 8 + 4) + 8 * 4 + 1   # K1 outputs per Gaussian (two planes + key/kappa/phase/flags)
+PROJ_W_B = 2 * (16 + 32 + 8 + 8 + 8 + 4) + 8 * 4 + 1 + 64 + 16   # K1 outputs per Gaussian: two planes, key/kappa/phase/flags, packed + emit rows
 REC_B = 80                               # packed computation-plane pair record
 LOG_B = 8 + 8 + 8 + 1 + 1                # replay log entry: y1, t2, w, j, r
 
@@ -225,10 +225,11 @@ def kernel_bytes(kid: int, n: int, t16: float, live: float, items: float, batch:
     """Algorithmic HBM bytes of ONE launch of kernel `kid`:
     every input read once and every output written once, per view-level
     counts n (Gaussians), t16 (computation-plane pairs), live (logged live
-    pairs), items (depth-segment work items); batch = views per geometry launch."""
+    pairs), items (depth-segment work items); batch = views per batched
+    launch (K1, binning and the geometry epilogue run once per batch)."""
     from paper_2506_21633_b200 import _lib as L
-    if kid == L.K_PROJECT:
-        return n * (SCENE_B + PROJ_W_B)
+    if kid == L.K_PROJECT:     # parameters read once per batch, records written per view
+        return n * SCENE_B + batch * n * PROJ_W_B
     if kid == L.K_SEGSUM:
         return REC_B * t16 + 8 * 256 * items
     if kid == L.K_WALK:
@@ -244,12 +245,12 @@ def kernel_bytes(kid: int, n: int, t16: float, live: float, items: float, batch:
         return n * (1 + 8 + 16 + 32 + 8 + 8)
     if kid == L.K_GRAD_IMAGE:
         return n * (1 + 8 + 16 + 32 + 8 + 8 + 48)
-    if kid == L.K_GATHER:
-        return t16 * (4 + 4 + 80 + 4 + REC_B)
-    if kid == L.K_EMIT:
-        return n * 32 + 8 * t16
-    if kid == L.K_ONESWEEP:   # 6 passes per view: 4 over the N depth keys, 2 over the pairs
-        return 16 * (4 * n + 2 * t16) / 6
+    if kid == L.K_GATHER:      # pos, pre, packed row + bbox, tile id read; record + prim written
+        return batch * t16 * (4 + 4 + 64 + 8 + 4 + REC_B + 4)
+    if kid == L.K_EMIT:        # order + 16 B emit row read, offsets / pair_start / key / value written
+        return batch * (n * (4 + 16 + 4 + 4) + 8 * t16)
+    if kid == L.K_ONESWEEP:    # 5 passes per batch: 3 over the N depth keys, 2 over the pairs (key + value r+w)
+        return batch * 16 * (3 * n + 2 * t16) / 5
     return float("nan")
 
 
