@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=0)
-    ap.add_argument("--lanes", type=int, default=4, help="concurrent view streams per GPU")
+    ap.add_argument("--lanes", type=int, default=8, help="concurrent view streams per GPU")
     return ap.parse_args()
 
 
@@ -451,7 +451,7 @@ def run_sdgr(args):
                    "views_per_rank": V, "gaussians": args.n, "image": [args.size, args.size],
                    "param_dtype": args.param_dtype, "parallelism": f"view-sharded dp{world}",
                    "s_stop": step.s_stop, "l2": "inputs larger than L2 (112 MB params + ~0.3 GB/view records)",
-                   "execution": f"one CUDA graph per step, views on {step.n_lanes} concurrent streams",
+                   "execution": f"one CUDA graph per step; K1-K5 batched per {step.geo_batch} views on a preprocessing stream, the views on {step.n_lanes} concurrent streams",
                    "t16_per_view": step.calib_t16_mean},
         "roofline": roofline,
         "stage_ms_per_step_single_stream": stages,

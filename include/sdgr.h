@@ -205,7 +205,7 @@ uint64_t sdgr_launch_count(void);
 #define SDGR_PROFILE_KERNELS 16
 #define SDGR_K_PROJECT 1      /* K1 k_project                      */
 #define SDGR_K_ONESWEEP 2     /* radix sort passes (depth + tile)  */
-#define SDGR_K_EMIT 3         /* pair emission                     */
+#define SDGR_K_EMIT 3         /* pair emission (fused count + emit in batches) */
 #define SDGR_K_GATHER 4       /* pair record packing               */
 #define SDGR_K_SEGSUM 5       /* forward pass A (segment sums)     */
 #define SDGR_K_WALK 6         /* forward tile walk (contributions) */

@@ -23,7 +23,7 @@ MAX_BATCH = 8
 PROFILE_KERNELS = 16
 K_PROJECT, K_ONESWEEP, K_EMIT, K_GATHER, K_SEGSUM, K_WALK, K_SPLAT, K_GRAD_IMAGE, K_REPLAY_GSUM, K_REPLAY_GRAD, \
     K_GEOMETRY = range(1, 12)
-KERNEL_NAMES = {K_PROJECT: "k_project", K_ONESWEEP: "k_onesweep", K_EMIT: "k_emit_pairs", K_GATHER: "k_gather_prim",
+KERNEL_NAMES = {K_PROJECT: "k_project", K_ONESWEEP: "k_onesweep", K_EMIT: "k_count_emit", K_GATHER: "k_gather_prim",
                 K_SEGSUM: "k_segsum", K_WALK: "k_walk<kContrib>", K_SPLAT: "k_splat", K_GRAD_IMAGE: "k_grad_image",
                 K_REPLAY_GSUM: "k_replay<kGSum>", K_REPLAY_GRAD: "k_replay<kGrad>", K_GEOMETRY: "k_grad_geometry"}
 

@@ -177,14 +177,15 @@ __global__ void __launch_bounds__(128, 5) k_grad_geometry(sdgr_scene sc, const _
   }
   const double p0 = ldv<T>(sc.positions, 3 * g), p1 = ldv<T>(sc.positions, 3 * g + 1),
                p2 = ldv<T>(sc.positions, 3 * g + 2);
-  T c[16];
+  // the 16 SH-gradient accumulators live in this thread's shared-memory
+  // column (only touched when the phase gate is open) and the SH coefficients
+  // are re-read from L1 per view: keeps the view loop's state in registers
+  __shared__ double s_dsh[16][128];
+  const T* csh = static_cast<const T*>(sc.sh_coeffs) + 16 * g;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) c[k] = __ldg(static_cast<const T*>(sc.sh_coeffs) + 16 * g + k);
+  for (int k = 0; k < 16; ++k) s_dsh[k][threadIdx.x] = 0.0;
   double G3[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   double dpos[3] = {0, 0, 0};
-  double dsh[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) dsh[k] = 0.0;
   double dk = 0.0, uvn = 0.0;
 #pragma unroll 1
   for (int vi = 0; vi < B.n_views; ++vi) {
@@ -239,14 +240,14 @@ __global__ void __launch_bounds__(128, 5) k_grad_geometry(sdgr_scene sc, const _
     if (V.phase_raw[g] > 0.0) {
       double cd[16], basis[16], gP[3];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) cd[k] = (double)c[k];
+      for (int k = 0; k < 16; ++k) cd[k] = (double)__ldg(csh + k);
       sh_grad_contract(d0, d1, d2, cd, gP, basis);
       const double proj_d = gP[0] * d0 + gP[1] * d1 + gP[2] * d2;
       dp[0] += dP * (gP[0] - proj_d * d0) / dist;
       dp[1] += dP * (gP[1] - proj_d * d1) / dist;
       dp[2] += dP * (gP[2] - proj_d * d2) / dist;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) dsh[k] += dP * basis[k];
+      for (int k = 0; k < 16; ++k) s_dsh[k][threadIdx.x] += dP * basis[k];
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) dpos[k] += dp[k];
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(128, 5) k_grad_geometry(sdgr_scene sc, const _
 #pragma unroll
   for (int j = 0; j < 3; ++j) put(out.log_scales, 3 * g + j, dM[j] * M[j] + dM[3 + j] * M[3 + j] + dM[6 + j] * M[6 + j]);
 #pragma unroll
-  for (int k = 0; k < 16; ++k) put(out.sh_coeffs, 16 * g + k, dsh[k]);
+  for (int k = 0; k < 16; ++k) put(out.sh_coeffs, 16 * g + k, s_dsh[k][threadIdx.x]);
 #pragma unroll
   for (int k = 0; k < 3; ++k) put(out.positions, 3 * g + k, dpos[k]);
   // softplus' = sigmoid (scene.py:36-39)

@@ -71,7 +71,7 @@ class MultiViewStep:
 
     def __init__(self, scene: DeviceScene, configs, cov_reg: float = DEFAULT_COV_REG,
                  cutoff: float = DEFAULT_CUTOFF, s_stop: float = S_STOP, headroom: float = 1.3,
-                 group=None, geo_batch: int = _lib.MAX_BATCH, lanes: int = 4, targets: torch.Tensor | None = None,
+                 group=None, geo_batch: int = _lib.MAX_BATCH, lanes: int = 8, targets: torch.Tensor | None = None,
                  lambda_ssim: float = 0.2, max_val: float = 1.0):
         self.scene = scene
         self.configs = list(configs)

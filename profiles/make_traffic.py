@@ -12,7 +12,7 @@ import sys
 NAMES = [("k_walk<1>", "k_walk<kContrib>"), ("k_replay<4>", "k_replay<kGrad>"), ("k_replay<3>", "k_replay<kGSum>"),
          ("k_grad_geometry", "k_grad_geometry"), ("k_project", "k_project"), ("k_segsum", "k_segsum"),
          ("k_splat_finish", None), ("k_splat", "k_splat"), ("k_grad_image", "k_grad_image"),
-         ("k_gather_prim", "k_gather_prim"), ("k_emit_pairs", "k_emit_pairs"), ("k_onesweep", "k_onesweep")]
+         ("k_gather_prim", "k_gather_prim"), ("k_count_emit", "k_count_emit"), ("k_onesweep", "k_onesweep")]
 
 
 def unit_scale(u):
