@@ -84,7 +84,9 @@ typedef struct sdgr_scene {
   const void* ke_raw;     /* (n,2) softplus pre-activations */
 } sdgr_scene;
 
-/* One projection plane's footprint records (N-sized). */
+/* One projection plane's footprint records (N-sized).  With both `packed` and
+ * `emit` given (multi-view steps), uv, bbox, cell_mask and tile_mask may be
+ * NULL: sdgr_project then skips them and the binning reads the rows. */
 typedef struct sdgr_plane {
   double* uv;           /* (n,2) pixel-space center                          */
   double* inv_cov;      /* (n,4) a00, a01, a11, 0  (forward.py:33-42)        */
@@ -107,8 +109,8 @@ typedef struct sdgr_projection {
   sdgr_plane comp;       /* computation plane (n_u x n_v)   */
   sdgr_plane img;        /* imaging plane (n_az x n_rg)     */
   uint64_t* depth_key;   /* (n) order-preserving FP64 depth key; UINT64_MAX if not visible */
-  double* kappa;         /* (n) ke_fwd + ke_bwd (geometry.py:317, Projection.ke_sum) */
-  double* phase;         /* (n) max(0, P~)                  (geometry.py:316) */
+  double* kappa;         /* (n) ke_fwd + ke_bwd (geometry.py:317, Projection.ke_sum); NULL if comp.packed */
+  double* phase;         /* (n) max(0, P~)                  (geometry.py:316); NULL if comp.packed */
   double* phase_raw;     /* (n) P~ (backward clamp gate)    (geometry.py:315) */
   uint8_t* flags;        /* (n) SDGR_FLAG_* */
   int32_t* counters;     /* (4) [0] visible, [1] skipped, [2] culled; zeroed by sdgr_project */

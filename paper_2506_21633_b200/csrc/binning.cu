@@ -526,10 +526,11 @@ constexpr unsigned long long kSFlagA = 1ull << 62, kSFlagP = 2ull << 62, kSValue
 struct FusedEmitIO {
   const ulonglong2* erow[kMaxBatch];
   const int32_t* ntiles[kMaxBatch];
-  const double* uv[kMaxBatch];
+  const double* uv[kMaxBatch];      // centre of Gaussian g at uv[uv_stride * g]
   const double* inv_cov[kMaxBatch];
   const int32_t* order[kMaxBatch];
   int32_t* offsets[kMaxBatch];
+  int uv_stride[kMaxBatch];         // 2: SoA uv, 8: packed rows
   uint32_t* keys[kMaxBatch];
   int32_t* vals[kMaxBatch];
   int32_t* pair_start[kMaxBatch];
@@ -645,7 +646,7 @@ __global__ void __launch_bounds__(256) k_count_emit(const __grid_constant__ Fuse
       }
       continue;
     }
-    const double2 uv = reinterpret_cast<const double2*>(io.uv[v])[g[k]];
+    const double2 uv = *reinterpret_cast<const double2*>(io.uv[v] + (int64_t)io.uv_stride[v] * g[k]);
     const double4 A = reinterpret_cast<const double4*>(io.inv_cov[v])[g[k]];
     const double a01x2 = dmul(2.0, A.y);
     for (int ty = ty0; ty <= ty1 && o < cap; ++ty)
@@ -695,6 +696,7 @@ struct GatherIO {
   const double* kappa[kMaxBatch];
   const double* phase[kMaxBatch];
   const double* packed[kMaxBatch];
+  const ulonglong2* erow[kMaxBatch];  // bbox source when the SoA bbox is absent
   sdgr_pair_rec* rec[kMaxBatch];
   const uint32_t* keys[kMaxBatch];
   int32_t* range[kMaxBatch];
@@ -722,7 +724,8 @@ __global__ void __launch_bounds__(256) k_gather_prim(const __grid_constant__ Gat
   if (live) io.prim[v][i] = g;
   sdgr_pair_rec* rec = io.rec[v];
   if (!rec) return;
-  const short4 bb = reinterpret_cast<const short4*>(io.bbox[v])[g];
+  const short4 bb = io.bbox[v] ? reinterpret_cast<const short4*>(io.bbox[v])[g]
+                               : *reinterpret_cast<const short4*>(&io.erow[v][g].x);
   double4 r0, r1;
   if (io.packed[v]) {
     const double4* pk = reinterpret_cast<const double4*>(io.packed[v]) + 2 * g;
@@ -901,7 +904,8 @@ int launch_bin_batch(int nv, const sdgr_projection* projs, const sdgr_view* view
       const sdgr_plane& pl = plane == 0 ? projs[v].comp : projs[v].img;
       fio.erow[v] = reinterpret_cast<const ulonglong2*>(pl.emit);
       fio.ntiles[v] = pl.n_tiles;
-      fio.uv[v] = pl.uv;
+      fio.uv[v] = pl.uv ? pl.uv : pl.packed;
+      fio.uv_stride[v] = pl.uv ? 2 : 8;
       fio.inv_cov[v] = pl.inv_cov;
       fio.order[v] = eio.order[v];
       fio.offsets[v] = offsets[v];
@@ -952,6 +956,7 @@ int launch_bin_batch(int nv, const sdgr_projection* projs, const sdgr_view* view
       gio.kappa[v] = projs[v].kappa;
       gio.phase[v] = projs[v].phase;
       gio.packed[v] = plane == 0 ? pl.packed : nullptr;
+      gio.erow[v] = reinterpret_cast<const ulonglong2*>(pl.emit);
       gio.rec[v] = plane == 0 ? tls[v].pair_rec : nullptr;
       gio.keys[v] = tls[v].pair_tile;
       gio.range[v] = tls[v].tile_range;

@@ -50,21 +50,23 @@ __device__ __forceinline__ unsigned long long emit_bbox(int x0, int x1, int y0, 
 // Writes the plane records for Gaussian g.  (forward.py:33-42, 60-109)
 // Returns an upper bound of the Gaussian's member cells on this plane (exact
 // for footprints inside the 8x8 window, the bbox area otherwise).
+// ru, rv = cutoff * sqrt(max(c00, 0)), cutoff * sqrt(max(c11, 0)) (forward.py:74-75),
+// computed by the caller (the computation plane's are the cull's).
+// SoA outputs other than inv_cov / n_tiles may be NULL (multi-view steps read
+// the packed / emit rows instead).
 __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double v,
-                                double c00, double c01, double c11, int nu, int nv,
+                                double c00, double c01, double c11, double ru, double rv, int nu, int nv,
                                 double cutoff, bool dense, double4& rec_out) {
   // invert_cov2d (forward.py:33-42)
   double det = dsub(dmul(c00, c11), dmul(c01, c01));
   double a00 = ddiv(c11, det), a01 = ddiv(-c01, det), a11 = ddiv(c00, det);
   rec_out = make_double4(a00, a01, a11, 0.0);
-  reinterpret_cast<double2*>(pl.uv)[g] = make_double2(u, v);
+  if (pl.uv) reinterpret_cast<double2*>(pl.uv)[g] = make_double2(u, v);
   reinterpret_cast<double4*>(pl.inv_cov)[g] = make_double4(a00, a01, a11, 0.0);
   if (pl.cov) reinterpret_cast<double4*>(pl.cov)[g] = make_double4(c00, c01, c11, 0.0);
 
   int x0, x1, y0, y1;
   if (!dense) {
-    double ru = dmul(cutoff, dsqrt(np_max0(c00)));
-    double rv = dmul(cutoff, dsqrt(np_max0(c11)));
     double fx0 = fmax(ceil(dsub(u, ru)), 0.0);
     double fx1 = fmin(floor(dadd(u, ru)), (double)nu - 1.0);
     double fy0 = fmax(ceil(dsub(v, rv)), 0.0);
@@ -142,10 +144,10 @@ __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double
       }
     }
   }
-  reinterpret_cast<short4*>(pl.bbox)[g] = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
-  pl.cell_mask[g] = cmask;
+  if (pl.bbox) reinterpret_cast<short4*>(pl.bbox)[g] = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
+  if (pl.cell_mask) pl.cell_mask[g] = cmask;
   rec_out.w = __longlong_as_double((long long)cmask);
-  pl.tile_mask[g] = tmask;
+  if (pl.tile_mask) pl.tile_mask[g] = tmask;
   if (pl.emit)
     reinterpret_cast<ulonglong2*>(pl.emit)[g] =
         make_ulonglong2(emit_bbox(x0, x1, y0, y1), (unsigned long long)tmask);
@@ -156,10 +158,10 @@ __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double
 }
 
 __device__ void plane_empty(const sdgr_plane& pl, int64_t g) {
-  reinterpret_cast<short4*>(pl.bbox)[g] = make_short4(1, 0, 1, 0);
+  if (pl.bbox) reinterpret_cast<short4*>(pl.bbox)[g] = make_short4(1, 0, 1, 0);
   if (pl.emit) reinterpret_cast<ulonglong2*>(pl.emit)[g] = make_ulonglong2(emit_bbox(1, 0, 1, 0), 0ull);
-  pl.cell_mask[g] = 0;
-  pl.tile_mask[g] = 0;
+  if (pl.cell_mask) pl.cell_mask[g] = 0;
+  if (pl.tile_mask) pl.tile_mask[g] = 0;
   pl.n_tiles[g] = 0;
 }
 
@@ -293,10 +295,11 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
       const bool ok = finite && detc > 0.0 && deti > 0.0;
       const bool dense = !isfinite(view.cutoff);
       bool inside = true;
+      double ru = 0.0, rv = 0.0;
       if (!dense) {
-        // frustum cull (geometry.py:293-305)
-        const double ru = dmul(view.cutoff, dsqrt(np_max0(cc00)));
-        const double rv = dmul(view.cutoff, dsqrt(np_max0(cc11)));
+        // frustum cull (geometry.py:293-305); the radii are the footprint's too
+        ru = dmul(view.cutoff, dsqrt(np_max0(cc00)));
+        rv = dmul(view.cutoff, dsqrt(np_max0(cc11)));
         inside = (dadd(uc, ru) >= 0.0) && (dsub(uc, ru) <= (double)view.n_u - 1.0) &&
                  (dadd(vc, rv) >= 0.0) && (dsub(vc, rv) <= (double)view.n_v - 1.0);
       }
@@ -306,14 +309,19 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
                                 ((ok && !inside) ? SDGR_FLAG_CULLED : 0));
       if (vis) {
         double4 rc, ri;
-        m_comp = plane_footprint(proj.comp, g, uc, vc, cc00, cc01, cc11, view.n_u, view.n_v, view.cutoff, dense, rc);
-        m_img = plane_footprint(proj.img, g, ui, vi, ci00, ci01, ci11, view.n_az, view.n_rg, view.cutoff, dense, ri);
+        m_comp = plane_footprint(proj.comp, g, uc, vc, cc00, cc01, cc11, ru, rv, view.n_u, view.n_v, view.cutoff,
+                                 dense, rc);
+        const double rui = dense ? 0.0 : dmul(view.cutoff, dsqrt(np_max0(ci00)));
+        const double rvi = dense ? 0.0 : dmul(view.cutoff, dsqrt(np_max0(ci11)));
+        m_img = plane_footprint(proj.img, g, ui, vi, ci00, ci01, ci11, rui, rvi, view.n_az, view.n_rg, view.cutoff,
+                                dense, ri);
         proj.depth_key[g] = depth_key(depth);
         // phase function and extinction (geometry.py:308-317)
         const double r0 = p0 - view.cam[0], r1 = p1 - view.cam[1], r2 = p2 - view.cam[2];
         double dist = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
         if (dist == 0.0) dist = 1.0;
-        const double d0 = r0 / dist, d1 = r1 / dist, d2 = r2 / dist;
+        const double idist = 1.0 / dist;   // (not a key: one division instead of three)
+        const double d0 = r0 * idist, d1 = r1 * idist, d2 = r2 * idist;
         double b[16];
         sh_basis(d0, d1, d2, b);
         const T* S = static_cast<const T*>(scene.sh_coeffs);
@@ -322,8 +330,8 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
         for (int j = 0; j < 16; ++j) praw += b[j] * ld(S, 16 * g + j);
         const double ph = (praw == praw) ? fmax(praw, 0.0) : praw;  // NaN propagates (np.maximum)
         const double kfv = s_state[9][threadIdx.x], kbv = s_state[10][threadIdx.x], kappa_g = kfv + kbv;
-        proj.kappa[g] = kappa_g;
-        proj.phase[g] = ph;
+        if (proj.kappa) proj.kappa[g] = kappa_g;
+        if (proj.phase) proj.phase[g] = ph;
         if (proj.comp.packed) {
           double4* pk = reinterpret_cast<double4*>(proj.comp.packed) + 2 * g;
           pk[0] = make_double4(uc, vc, rc.x, rc.y);
@@ -336,12 +344,12 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
         plane_empty(proj.comp, g);
         plane_empty(proj.img, g);
         proj.depth_key[g] = ~0ull;
-        proj.kappa[g] = 0.0;
-        proj.phase[g] = 0.0;
+        if (proj.kappa) proj.kappa[g] = 0.0;
+        if (proj.phase) proj.phase[g] = 0.0;
         proj.phase_raw[g] = 0.0;
         // accessor arrays keep the raw projection for non-visible rows too
-        reinterpret_cast<double2*>(proj.comp.uv)[g] = make_double2(uc, vc);
-        reinterpret_cast<double2*>(proj.img.uv)[g] = make_double2(ui, vi);
+        if (proj.comp.uv) reinterpret_cast<double2*>(proj.comp.uv)[g] = make_double2(uc, vc);
+        if (proj.img.uv) reinterpret_cast<double2*>(proj.img.uv)[g] = make_double2(ui, vi);
         if (proj.comp.cov) reinterpret_cast<double4*>(proj.comp.cov)[g] = make_double4(cc00, cc01, cc11, 0.0);
         if (proj.img.cov) reinterpret_cast<double4*>(proj.img.cov)[g] = make_double4(ci00, ci01, ci11, 0.0);
       }

@@ -159,16 +159,20 @@ class MultiViewStep:
             pl = _lib.Plane()
             pl.uv, pl.inv_cov, pl.cov, pl.bbox = ptr(r["uv"]), ptr(r["inv_cov"]), None, ptr(r["bbox"])
             pl.cell_mask, pl.tile_mask, pl.n_tiles = ptr(r["cell_mask"]), ptr(r["tile_mask"]), ptr(r["n_tiles"])
-            if name == "comp":   # 64-byte rows the pair-record gather reads
+            if name == "comp":
+                # 64-byte rows the pair-record gather reads, 16-byte rows the
+                # fused count + emit reads; the SoA copies they replace are
+                # not written (nothing in a multi-view step reads them)
                 r["packed"] = _empty((n, 8), torch.float64, dev)
                 pl.packed = ptr(r["packed"])
                 r["emit"] = _empty((n, 2), torch.int64, dev)
                 pl.emit = ptr(r["emit"])
+                pl.uv = pl.bbox = pl.cell_mask = pl.tile_mask = None
             setattr(pd, name, pl)
-        for k, dt in (("depth_key", torch.int64), ("kappa", torch.float64), ("phase", torch.float64),
-                      ("phase_raw", torch.float64), ("flags", torch.uint8)):
+        for k, dt in (("depth_key", torch.int64), ("phase_raw", torch.float64), ("flags", torch.uint8)):
             rec[k] = _empty((n,), dt, dev)
             setattr(pd, k, ptr(rec[k]))
+        pd.kappa = pd.phase = None   # carried by the packed rows
         rec["counters"] = torch.zeros((4,), dtype=torch.int32, device=dev)
         rec["member_pairs"] = torch.zeros((2,), dtype=torch.int64, device=dev)
         pd.counters, pd.member_pairs = ptr(rec["counters"]), ptr(rec["member_pairs"])
