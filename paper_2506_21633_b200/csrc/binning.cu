@@ -537,7 +537,10 @@ struct FusedEmitIO {
   int32_t* overflow[kMaxBatch];
 };
 
-__global__ void __launch_bounds__(256) k_count_emit(const __grid_constant__ FusedEmitIO io, int nv, int64_t n,
+#ifndef SDGR_EMIT_MINB
+#define SDGR_EMIT_MINB 2
+#endif
+__global__ void __launch_bounds__(256, SDGR_EMIT_MINB) k_count_emit(const __grid_constant__ FusedEmitIO io, int nv, int64_t n,
                                                     int64_t nblk, int tiles_x, double cutoff, int64_t cap,
                                                     uint32_t* hist, int npass, unsigned long long* status_all,
                                                     uint32_t* ticket) {
@@ -1115,57 +1118,69 @@ __global__ void __launch_bounds__(256) k_key32(const __grid_constant__ DepthIO i
   bh.flush(hist + (size_t)v * kHistStride, kMaxPass);
 }
 
-// one thread per run of equal k32 (runs are rare and short); stable by index
+// Runs of equal k32 (rare and short): each warp finds the run starts among its
+// 32 keys (neighbours by shuffle), then resolves its runs one at a time with
+// all 32 lanes -- lane t holds entry t of the run and computes its rank under
+// (64-bit key, index) by comparing against every other entry.  Runs longer
+// than 32 fall back to lane 0's in-place insertion sort.
 __global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s_all, int64_t ks,
                                                   const __grid_constant__ DepthIO io, int64_t n) {
   const int v = blockIdx.y;
+  const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
   const uint32_t* k32s = k32s_all + (size_t)v * ks;
-  const uint32_t k = k32s[i];
-  if (k == kKeyInvisible) return;                     // invisible tail: order irrelevant
-  if (i > 0 && k32s[i - 1] == k) return;               // not a run start
-  if (i + 1 >= n || k32s[i + 1] != k) return;          // run of length 1
+  const uint32_t k = i < n ? k32s[i] : kKeyInvisible;
+  uint32_t prev = __shfl_up_sync(0xffffffffu, k, 1), next = __shfl_down_sync(0xffffffffu, k, 1);
+  if (lane == 0) prev = (i > 0 && i - 1 < n) ? k32s[i - 1] : kKeyInvisible;
+  if (lane == 31) next = i + 1 < n ? k32s[i + 1] : kKeyInvisible;
+  // the invisible tail's order is irrelevant
+  const bool start = i < n && k != kKeyInvisible && prev != k && next == k;
+  uint32_t starts = __ballot_sync(0xffffffffu, start);
+  if (!starts) return;
   const uint64_t* key = io.key[v];
   int32_t* order = io.order[v];
-  int64_t e = i + 1;
-  while (e < n && k32s[e] == k) ++e;
-  constexpr int kRunLocal = 32;
-  if (e - i <= kRunLocal) {
-    // short run: all (key, index) loads issued together, sorted in local
-    // memory, written back once (no chain of dependent global loads)
-    const int L = (int)(e - i);
-    uint64_t kk[kRunLocal];
-    int32_t gg[kRunLocal];
-    for (int a = 0; a < L; ++a) gg[a] = order[i + a];
-    for (int a = 0; a < L; ++a) kk[a] = key[gg[a]];
-    for (int a = 1; a < L; ++a) {
-      const uint64_t kg = kk[a];
-      const int32_t g = gg[a];
-      int b = a - 1;
-      while (b >= 0 && (kk[b] > kg || (kk[b] == kg && gg[b] > g))) {
-        kk[b + 1] = kk[b];
-        gg[b + 1] = gg[b];
-        --b;
+  while (starts) {
+    const int src = __ffs(starts) - 1;
+    starts &= starts - 1;
+    const int64_t i0 = __shfl_sync(0xffffffffu, i, src);
+    const uint32_t kv = __shfl_sync(0xffffffffu, k, src);
+    const int64_t j = i0 + lane;
+    const bool in = j < n && k32s[j] == kv;
+    const uint32_t inb = __ballot_sync(0xffffffffu, in);
+    if (inb == 0xffffffffu) {
+      // longer than a warp: serial in-place insertion sort by (key, index)
+      if (lane == 0) {
+        int64_t e = i0 + 32;
+        while (e < n && k32s[e] == kv) ++e;
+        for (int64_t a = i0 + 1; a < e; ++a) {
+          const int32_t g = order[a];
+          const uint64_t kg = key[g];
+          int64_t b = a - 1;
+          while (b >= i0) {
+            const int32_t h = order[b];
+            const uint64_t kh = key[h];
+            if (kh < kg || (kh == kg && h < g)) break;
+            order[b + 1] = h;
+            --b;
+          }
+          order[b + 1] = g;
+        }
       }
-      kk[b + 1] = kg;
-      gg[b + 1] = g;
+      __syncwarp();
+      continue;
     }
-    for (int a = 0; a < L; ++a) order[i + a] = gg[a];
-    return;
-  }
-  for (int64_t a = i + 1; a < e; ++a) {                // insertion sort by (key, index)
-    const int32_t g = order[a];
-    const uint64_t kg = key[g];
-    int64_t b = a - 1;
-    while (b >= i) {
-      const int32_t h = order[b];
-      const uint64_t kh = key[h];
-      if (kh < kg || (kh == kg && h < g)) break;
-      order[b + 1] = h;
-      --b;
+    const int L = __ffs(~inb) - 1;   // run length (>= 2)
+    const int32_t g = lane < L ? order[i0 + lane] : 0;
+    const uint64_t kg = lane < L ? key[g] : ~0ull;
+    int rank = 0;
+    for (int t = 0; t < L; ++t) {
+      const int32_t gt = __shfl_sync(0xffffffffu, g, t);
+      const uint64_t kt = __shfl_sync(0xffffffffu, kg, t);
+      rank += (kt < kg || (kt == kg && gt < g)) ? 1 : 0;
     }
-    order[b + 1] = g;
+    __syncwarp();
+    if (lane < L) order[i0 + rank] = g;
+    __syncwarp();
   }
 }
 
