@@ -373,6 +373,24 @@ int sdgr_ply_pack(const sdgr_scene* scene, double* out, void* stream);
 int sdgr_ply_unpack(const double* in, int64_t n, int stride, const int32_t* col, sdgr_scene* scene,
                     void* stream);
 
+/* ------------------------------ point-cloud evaluation -- */
+/* metrics.chamfer / precision_recall_f1 / dbscan_inlier_mask (metrics.py:140-183)
+ * on a uniform grid of dims[0] x dims[1] x dims[2] cells (<= 2^24) of edge h
+ * with corner lo (host arrays).  Points are (n,3) FP64 device arrays.
+ * ws: sdgr_grid_workspace_bytes(n of the gridded set, cells). */
+size_t sdgr_grid_workspace_bytes(int64_t n, int64_t n_cells);
+/* d2[i] = squared distance from query i to its nearest reference point (the
+ * cKDTree query of metrics.py:150-151, 159-160), exact, FP64. */
+int sdgr_nn_sqdist(const double* ref, int64_t n_ref, const double* query, int64_t n_query,
+                   const double* lo, double h, const int32_t* dims, double* d2,
+                   void* ws, size_t ws_bytes, void* stream);
+/* DBSCAN (sklearn semantics, metrics.py:165-177): root[i] = the smallest core
+ * index of point i's cluster (core: >= min_pts points within eps, itself
+ * included; border points join the cluster the reference's index-order
+ * expansion reaches first), -1 for noise.  Requires h >= eps. */
+int sdgr_dbscan(const double* pts, int64_t n, const double* lo, double h, const int32_t* dims,
+                double eps, int32_t min_pts, int32_t* root, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

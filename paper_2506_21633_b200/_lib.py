@@ -122,6 +122,11 @@ SIGNATURES = [
     ("sdgr_grad_geometry_batch", C.c_int, [C.POINTER(SceneDesc), C.c_int, C.POINTER(View),
                                            C.POINTER(ProjectionDesc), C.POINTER(TilesDesc), C.POINTER(_p),
                                            C.POINTER(_p), C.POINTER(GradsDesc), C.c_int, _p]),
+    ("sdgr_grid_workspace_bytes", C.c_size_t, [C.c_int64, C.c_int64]),
+    ("sdgr_nn_sqdist", C.c_int, [_p, C.c_int64, _p, C.c_int64, C.POINTER(C.c_double), C.c_double,
+                                 C.POINTER(C.c_int32), _p, _p, C.c_size_t, _p]),
+    ("sdgr_dbscan", C.c_int, [_p, C.c_int64, C.POINTER(C.c_double), C.c_double, C.POINTER(C.c_int32),
+                              C.c_double, C.c_int32, _p, _p, C.c_size_t, _p]),
     ("sdgr_ply_pack", C.c_int, [C.POINTER(SceneDesc), _p, _p]),
     ("sdgr_ply_unpack", C.c_int, [_p, C.c_int64, C.c_int, C.POINTER(C.c_int32), C.POINTER(SceneDesc), _p]),
     ("sdgr_accum_update", C.c_int, [C.POINTER(GradsDesc), C.c_int64, _p, _p, _p, _p]),

@@ -1233,6 +1233,43 @@ int launch_depth_order_batch(int nv, const sdgr_projection* projs, int32_t* cons
   return check_launch();
 }
 
+// ------------------------------------------------- generic key sort --------
+// Stable sort of n 32-bit keys (bits [0, bits)) with their input positions:
+// keys_out ascending, perm_out[i] = input index.  Used by the evaluation grid
+// (eval.cu).
+__global__ void __launch_bounds__(256) k_key_hist(const uint32_t* keys, int64_t n, int npass, uint32_t* hist) {
+  __shared__ uint32_t sh[kMaxPass][256];
+  BlockHist bh{sh};
+  bh.clear();
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bh.add(keys[i], npass);
+  __syncthreads();
+  bh.flush(hist, npass);
+}
+
+size_t sort_u32_ws_bytes(int64_t n) { return radix_ws_bytes(n < 1 ? 1 : n, 1) + 4096; }
+
+int sort_u32(const uint32_t* keys, int64_t n, int bits, uint32_t* keys_out, uint32_t* perm_out, void* ws,
+             size_t ws_bytes, cudaStream_t st) {
+  if (n <= 0) return SDGR_OK;
+  const int npass = (bits + 7) / 8;
+  if (npass < 1 || npass > kMaxPass) return SDGR_ERR_INVALID;
+  if (ws_bytes < sort_u32_ws_bytes(n)) return SDGR_ERR_CAPACITY;
+  char* p = static_cast<char*>(ws);
+  const RadixWs r = radix_layout(p, n, 1);
+  if (cudaMemsetAsync(r.hist, 0, r.zero_bytes, st) != cudaSuccess) return SDGR_ERR_CUDA;
+  k_key_hist<<<stride_blocks(n, 1, 2), 256, 0, st>>>(keys, n, npass, r.hist);
+  note_launch();
+  SortIO io;
+  io.kin[0] = keys;
+  io.vin[0] = nullptr;
+  io.kout[0] = keys_out;
+  io.vout[0] = perm_out;
+  io.n_dev[0] = nullptr;
+  return radix_passes(io, true, 1, n, npass, r, st);
+}
+
 size_t batch_ws_bytes(int64_t n, int64_t max_pairs, int nv) {
   return std::max(depth_ws_bytes(n, nv), bin_ws_bytes(n, max_pairs, nv)) + 4096;
 }
