@@ -45,6 +45,16 @@
 namespace sdgr {
 
 enum WalkMode { kContrib = 1, kGSum = 3, kGrad = 4 };
+// Persistent walk grids: SDGR_WALK_GRID_DIV = 1 fills every SM's resident
+// CTA slots with one view's walk; > 1 leaves room for the walks of views on
+// other streams to run alongside (A/B knob for the multi-view step).
+#ifndef SDGR_WALK_GRID_DIV
+#define SDGR_WALK_GRID_DIV 1
+#endif
+static int persistent_grid(int per_sm) {
+  return std::max(1, sm_count() * std::max(per_sm, 1) / SDGR_WALK_GRID_DIV);
+}
+
 
 // fixed point: value * 2^32 in a u64 (values are >= 0)
 constexpr double kFix = 4294967296.0;
@@ -1109,7 +1119,7 @@ static int walk_grid(int max_items) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_walk<MODE>, 256, smem);
     per_sm = b > 0 ? b : 1;
   }
-  return max(1, min(max_items, sm_count() * per_sm));
+  return max(1, min(max_items, persistent_grid(per_sm)));
 }
 
 template <int MODE>
@@ -1156,7 +1166,7 @@ int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const
     if (per_sm == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_segsum, 256, 0);
     {
       KernelTimer kt(SDGR_K_SEGSUM, st);
-      k_segsum<<<max(1, min(t.max_items, sm_count() * max(per_sm, 1))), 256, 0, st>>>(
+      k_segsum<<<max(1, min(t.max_items, persistent_grid(per_sm))), 256, 0, st>>>(
           t.pair_rec, t.items, t.n_items, counter, t.tiles_x, v.cutoff, seg_fx);
     }
     k_seg_scan<false, true><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_sum, seg_base);
@@ -1218,7 +1228,7 @@ int launch_grad_intensity(const sdgr_view& v, const sdgr_projection& p, const sd
     if (cudaMemsetAsync(r.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
     {
       KernelTimer kt(SDGR_K_REPLAY_GSUM, st);
-      k_replay<kGSum><<<max(1, min(t.max_items, sm_count() * max(per_sm[0], 1))), 256, ReplayCfg<kGSum>::kSmem,
+      k_replay<kGSum><<<max(1, min(t.max_items, persistent_grid(per_sm[0]))), 256, ReplayCfg<kGSum>::kSmem,
                         st>>>(r);
     }
     k_seg_scan<true><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_g, seg_d);
@@ -1231,7 +1241,7 @@ int launch_grad_intensity(const sdgr_view& v, const sdgr_projection& p, const sd
     r.partial = partial_g;
     {
       KernelTimer kt(SDGR_K_REPLAY_GRAD, st);
-      k_replay<kGrad><<<max(1, min(t.max_items, sm_count() * max(per_sm[1], 1))), 256, ReplayCfg<kGrad>::kSmem,
+      k_replay<kGrad><<<max(1, min(t.max_items, persistent_grid(per_sm[1]))), 256, ReplayCfg<kGrad>::kSmem,
                         st>>>(r);
     }
     note_launch();
