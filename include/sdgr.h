@@ -108,7 +108,8 @@ typedef struct sdgr_projection {
   int64_t n;
   sdgr_plane comp;       /* computation plane (n_u x n_v)   */
   sdgr_plane img;        /* imaging plane (n_az x n_rg)     */
-  uint64_t* depth_key;   /* (n) order-preserving FP64 depth key; UINT64_MAX if not visible */
+  uint64_t* depth_key;   /* (n) order-preserving FP64 depth key; UINT64_MAX if not visible;
+                            16-byte aligned (sdgr_depth_order* read it in 16-byte loads) */
   double* kappa;         /* (n) ke_fwd + ke_bwd (geometry.py:317, Projection.ke_sum); NULL if comp.packed */
   double* phase;         /* (n) max(0, P~)                  (geometry.py:316); NULL if comp.packed */
   double* phase_raw;     /* (n) P~ (backward clamp gate)    (geometry.py:315) */

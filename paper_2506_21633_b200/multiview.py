@@ -152,22 +152,22 @@ class MultiViewStep:
         pd = _lib.ProjectionDesc()
         pd.n = n
         for name in ("comp", "img"):
-            r = dict(uv=_empty((n, 2), torch.float64, dev), inv_cov=_empty((n, 4), torch.float64, dev),
-                     bbox=_empty((n, 4), torch.int16, dev), cell_mask=_empty((n,), torch.int64, dev),
-                     tile_mask=_empty((n,), torch.int64, dev), n_tiles=_empty((n,), torch.int32, dev))
-            rec[name] = r
             pl = _lib.Plane()
-            pl.uv, pl.inv_cov, pl.cov, pl.bbox = ptr(r["uv"]), ptr(r["inv_cov"]), None, ptr(r["bbox"])
-            pl.cell_mask, pl.tile_mask, pl.n_tiles = ptr(r["cell_mask"]), ptr(r["tile_mask"]), ptr(r["n_tiles"])
+            r = dict(inv_cov=_empty((n, 4), torch.float64, dev), n_tiles=_empty((n,), torch.int32, dev))
             if name == "comp":
                 # 64-byte rows the pair-record gather reads, 16-byte rows the
-                # fused count + emit reads; the SoA copies they replace are
-                # not written (nothing in a multi-view step reads them)
+                # fused count + emit reads; the SoA uv / bbox / masks they
+                # replace are neither allocated nor written
                 r["packed"] = _empty((n, 8), torch.float64, dev)
-                pl.packed = ptr(r["packed"])
                 r["emit"] = _empty((n, 2), torch.int64, dev)
-                pl.emit = ptr(r["emit"])
-                pl.uv = pl.bbox = pl.cell_mask = pl.tile_mask = None
+                pl.packed, pl.emit = ptr(r["packed"]), ptr(r["emit"])
+            else:
+                r.update(uv=_empty((n, 2), torch.float64, dev), bbox=_empty((n, 4), torch.int16, dev),
+                         cell_mask=_empty((n,), torch.int64, dev), tile_mask=_empty((n,), torch.int64, dev))
+                pl.uv, pl.bbox = ptr(r["uv"]), ptr(r["bbox"])
+                pl.cell_mask, pl.tile_mask = ptr(r["cell_mask"]), ptr(r["tile_mask"])
+            pl.inv_cov, pl.n_tiles, pl.cov = ptr(r["inv_cov"]), ptr(r["n_tiles"]), None
+            rec[name] = r
             setattr(pd, name, pl)
         for k, dt in (("depth_key", torch.int64), ("phase_raw", torch.float64), ("flags", torch.uint8)):
             rec[k] = _empty((n,), dt, dev)
