@@ -402,3 +402,35 @@ def test_batched_preprocessing_equals_single_views(n_views):
             ni = int(t["n_items"][0].item())
             assert ni == int(tl.n_items[0].item())
             assert torch.equal(t["items"][:ni].cpu(), tl.items[:ni].cpu()), f"view {k}: work items"
+
+
+@pytest.mark.parametrize("cutoff", [3.0, math.inf], ids=["cut", "dense"])
+def test_batched_preprocessing_small_scenes(cutoff):
+    """Batched vs single-view binning on gradcheck-sized scenes, including the
+    dense all-pairs mode (cutoff = inf, reference forward.py:80-84) and
+    Gaussians larger than the 8x8 windows (exact re-enumeration paths)."""
+    from paper_2506_21633_b200.multiview import MultiViewStep
+
+    rng = np.random.default_rng(4)
+    n = 300
+    host = sdgr.Scene(positions=rng.uniform(-4, 4, size=(n, 3)),
+                      rotations=rng.normal(size=(n, 4)),
+                      log_scales=rng.uniform(np.log(0.05), np.log(2.5), size=(n, 3)),
+                      sh_coeffs=np.column_stack([rng.uniform(1, 3, n), rng.normal(0, 0.1, (n, 15))]),
+                      ke_raw=rng.uniform(-0.5, 1.0, size=(n, 2)))
+    host = targets.to_float32_exact(host)
+    cfgs = [sdgr.RadarConfig(azimuth_deg=az, elevation_deg=45.0, altitude_m=0.5, n_range=40, n_azimuth=40)
+            for az in (0.0, 70.0, 140.0, 250.0)]
+    ds = sdgr.DeviceScene.from_host(host, dtype=torch.float32)
+    step = MultiViewStep(ds, cfgs, geo_batch=4, cutoff=cutoff)
+    step.calibrate()
+    step._preprocess(step.views, 0)
+    torch.cuda.synchronize()
+    for k, c in enumerate(cfgs):
+        tl = sdgr.render_forward(ds, c, cutoff=cutoff).rays
+        m = tl.n_pairs
+        t = step.slot_t[k]
+        assert int(step.slot_offsets[k][step.n].item()) == m
+        assert torch.equal(t["pair_prim"][:m].cpu(), tl.pair_prim[:m].cpu()), f"view {k}: key lists"
+        assert torch.equal(t["tile_range"].cpu(), tl.tile_range.cpu()), f"view {k}: tile ranges"
+        assert torch.equal(t["pair_rec"][:m].cpu(), tl.pair_rec[:m].cpu()), f"view {k}: pair records"
