@@ -17,6 +17,7 @@ step; on overflow the step is recalibrated and re-run.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -30,6 +31,7 @@ from .rasterizer import (DEFAULT_COV_REG, DEFAULT_CUTOFF, S_STOP, ReplayLog, Sce
                          _scene_desc, _seg_len, _stream)
 from .scene import DeviceScene
 
+MULTIVIEW_SEG_LEN = 2048  # depth-segment floor for concurrent multi-view steps
 GRAD_WIDTH = 30  # 3 + 4 + 3 + 16 + 2 + uv_grad_norm + (visible as int32 view)
 
 
@@ -192,7 +194,11 @@ class MultiViewStep:
         cap = cap_pairs[0]
         nu, nv = v.n_u, v.n_v
         tx, ty = -(-nu // TILE), -(-nv // TILE)
-        seg = _seg_len(cap)
+        # depth segments: a lone view wants ~32 per SM so its walk has no tail
+        # (_seg_len); with 8 views in flight the tails overlap, and longer
+        # segments mean fewer pass-A items and segment scans: 2048 measured
+        # +3 % views/s at c4 over 512 (profiles/ROUND1.md)
+        seg = _seg_len(cap) if os.environ.get("SDGR_SEG_LEN") else max(_seg_len(cap), MULTIVIEW_SEG_LEN)
         max_items = -(-cap // seg) + tx * ty
         # per slot: the binning outputs a view's walks and geometry read (the
         # batched preprocessing of batch b+1 fills one slot set while batch b's

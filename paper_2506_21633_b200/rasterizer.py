@@ -22,6 +22,7 @@ tensors (float32).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 
@@ -308,6 +309,8 @@ class TileLists:
 
 
 def _seg_len(n_pairs: int) -> int:
+    if os.environ.get("SDGR_SEG_LEN"):          # A/B override (profiling)
+        return int(min(max(int(os.environ["SDGR_SEG_LEN"]), 256), 8192)) // 256 * 256
     seg = -(-n_pairs // SMS_TARGET_ITEMS)
     seg = -(-seg // 256) * 256
     return int(min(max(seg, 256), 8192))
