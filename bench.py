@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=0)
     ap.add_argument("--lanes", type=int, default=8, help="concurrent view streams per GPU")
+    ap.add_argument("--geo-batch", type=int, default=None, help="views per batched launch (default: the build's max)")
     return ap.parse_args()
 
 
@@ -324,7 +325,7 @@ def run_sdgr(args):
     V = len(mine)
     scene = sdgr.DeviceScene.from_host(host_scene, dtype=pdt)
     kw = {} if args.s_stop is None else {"s_stop": args.s_stop}
-    step = MultiViewStep(scene, mine, lanes=args.lanes, **kw)
+    step = MultiViewStep(scene, mine, lanes=args.lanes, geo_batch=args.geo_batch, **kw)
     totals = []
     mx = step.calibrate()
     g = torch.Generator(device="cpu").manual_seed(1234 + rank)

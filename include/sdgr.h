@@ -34,7 +34,9 @@ extern "C" {
 #define SDGR_TILE 16          /* tile edge in cells / pixels (16x16 = 256 rays) */
 #define SDGR_TILE_RAYS 256
 #define SDGR_MAX_PLANE 32767  /* plane dims must fit int16 bboxes */
-#define SDGR_MAX_BATCH 8      /* views per batched call (*_batch) */
+#ifndef SDGR_MAX_BATCH
+#define SDGR_MAX_BATCH 16     /* views per batched call (*_batch); sdgr_max_batch() reports the build's */
+#endif
 
 typedef enum sdgr_status {
   SDGR_OK = 0,
@@ -199,6 +201,8 @@ int sdgr_version(void);
 const char* sdgr_status_string(int status);
 /* Kernels launched by this library since load (the bench's gpu_launches). */
 uint64_t sdgr_launch_count(void);
+/* SDGR_MAX_BATCH of this build (views per *_batch call). */
+int sdgr_max_batch(void);
 /* Device timing of selected kernels: between sdgr_profile_begin(mask) and
  * sdgr_profile_end, every launch of a kernel whose bit (1 << SDGR_K_*) is in
  * mask is bracketed by CUDA events on its launch stream.  sdgr_profile_end

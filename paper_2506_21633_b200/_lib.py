@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / os.environ.get("SDGR_LIB", "libsdgr
 OK, ERR_INVALID, ERR_NUMERICAL, ERR_STATE, ERR_CUDA, ERR_CAPACITY = range(6)
 FLAG_VISIBLE, FLAG_SKIPPED, FLAG_CULLED = 1, 2, 4
 TILE = 16
-MAX_BATCH = 8
+MAX_BATCH = 16  # default build's SDGR_MAX_BATCH; lib().sdgr_max_batch() is authoritative
 PROFILE_KERNELS = 16
 K_PROJECT, K_ONESWEEP, K_EMIT, K_GATHER, K_SEGSUM, K_WALK, K_SPLAT, K_GRAD_IMAGE, K_REPLAY_GSUM, K_REPLAY_GRAD, \
     K_GEOMETRY = range(1, 12)
@@ -96,6 +96,7 @@ SIGNATURES = [
     ("sdgr_version", C.c_int, []),
     ("sdgr_status_string", C.c_char_p, [C.c_int]),
     ("sdgr_launch_count", C.c_uint64, []),
+    ("sdgr_max_batch", C.c_int, []),
     ("sdgr_workspace_bytes", C.c_size_t, [C.c_int64, C.c_int64]),
     ("sdgr_profile_begin", C.c_int, [C.c_uint32]),
     ("sdgr_profile_end", C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64)]),

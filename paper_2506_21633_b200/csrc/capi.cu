@@ -128,6 +128,8 @@ const char* sdgr_status_string(int s) {
 
 uint64_t sdgr_launch_count(void) { return g_launches.load(); }
 
+int sdgr_max_batch(void) { return SDGR_MAX_BATCH; }
+
 int sdgr_profile_begin(uint32_t kernel_mask) {
   g_prof_mask = kernel_mask;
   g_prof_n = 0;

@@ -73,7 +73,7 @@ class MultiViewStep:
 
     def __init__(self, scene: DeviceScene, configs, cov_reg: float = DEFAULT_COV_REG,
                  cutoff: float = DEFAULT_CUTOFF, s_stop: float = S_STOP, headroom: float = 1.3,
-                 group=None, geo_batch: int = _lib.MAX_BATCH, lanes: int = 8, targets: torch.Tensor | None = None,
+                 group=None, geo_batch: int | None = None, lanes: int = 8, targets: torch.Tensor | None = None,
                  lambda_ssim: float = 0.2, max_val: float = 1.0):
         self.scene = scene
         self.configs = list(configs)
@@ -93,7 +93,8 @@ class MultiViewStep:
         # geometry epilogue batches: `geo_batch` views' projections, partial
         # records and imaging-plane sums stay resident until one batched
         # sdgr_grad_geometry_batch call consumes them
-        self.geo_batch = max(1, min(int(geo_batch), _lib.MAX_BATCH, len(self.views)))
+        max_batch = int(self.lib.sdgr_max_batch())
+        self.geo_batch = max(1, min(int(geo_batch or max_batch), max_batch, len(self.views)))
         # lanes: views alternate between `lanes` streams, each with its own
         # per-view working buffers, so one view's latency-bound walks overlap
         # another view's preprocessing; the batch's geometry joins the lanes

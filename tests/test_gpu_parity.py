@@ -369,7 +369,7 @@ def test_depth_ties_and_near_ties_vs_oracle():
     _oracle_compare(scene, cfg, 3.0, seed=31)
 
 
-@pytest.mark.parametrize("n_views", [1, 3, 8])
+@pytest.mark.parametrize("n_views", [1, 3, 8, 16])
 def test_batched_preprocessing_equals_single_views(n_views):
     """sdgr_project_batch + sdgr_depth_order_batch + sdgr_bin_batch (one launch
     per stage over the batch, packed / emit rows, fused count + emit) produce
@@ -378,11 +378,11 @@ def test_batched_preprocessing_equals_single_views(n_views):
     from paper_2506_21633_b200.multiview import MultiViewStep
 
     tank = targets.to_float32_exact(targets.composite_target(targets.tank_preset(), [6000, 3000, 1000], seed=8))
-    angles = [(az, el) for el in (30.0, 45.0, 60.0) for az in (0.0, 50.0, 130.0)][:n_views]
+    angles = [(az, el) for el in (30.0, 45.0, 60.0) for az in (0.0, 50.0, 130.0, 200.0, 290.0, 340.0)][:n_views]
     cfgs = [sdgr.RadarConfig(azimuth_deg=az, elevation_deg=el, altitude_m=0.5, n_range=128, n_azimuth=128)
             for az, el in angles]
     ds = sdgr.DeviceScene.from_host(tank, dtype=torch.float32)
-    step = MultiViewStep(ds, cfgs, geo_batch=8)
+    step = MultiViewStep(ds, cfgs)
     step.calibrate()
     step._preprocess(step.views, 0)
     torch.cuda.synchronize()
