@@ -239,6 +239,10 @@ __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const 
     const int item = item_s;
     if (item >= n_items) return;
     const int4 it = reinterpret_cast<const int4*>(items)[item];
+    // a tile's last segment: its optical depth is no later segment's prefix
+    // (the scan is exclusive), so pass A skips it -- for a single-segment
+    // tile, the whole tile
+    if (item + 1 >= n_items || items[4 * (item + 1)] != it.x) continue;
     const int tx = it.x % tiles_x, ty = it.x / tiles_x;
     unsigned long long* acc = seg_fx + (int64_t)item * kRays;
     for (int i0 = it.y; i0 < it.z; i0 += kRays) {
