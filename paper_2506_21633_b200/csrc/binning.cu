@@ -1118,77 +1118,63 @@ __global__ void __launch_bounds__(256) k_key32(const __grid_constant__ DepthIO i
   bh.flush(hist + (size_t)v * kHistStride, kMaxPass);
 }
 
-// Runs of equal k32 (rare and short): each warp finds the run starts among its
-// 32 keys (neighbours by shuffle), then resolves its runs one at a time with
-// all 32 lanes -- lane t holds entry t of the run and computes its rank under
-// (64-bit key, index) by comparing against every other entry.  Runs longer
-// than 32 fall back to lane 0's in-place insertion sort.
-__global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s_all, int64_t ks,
+// Runs of equal k32 (~10 % of the keys on c4, at most a handful long): the
+// last radix pass wrote its order to `tmp`; one thread per position copies it
+// to `order`, except that a member of a run of L <= kRunPar entries computes
+// its rank under (64-bit key, index) against the L - 1 others (independent,
+// L1-resident loads) and lands at run start + rank.  Longer runs fall back
+// to one thread's insertion sort.  No thread waits on another.
+constexpr int kRunPar = 64;
+
+__global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s_all, const uint32_t* tmp_all, int64_t ks,
                                                   const __grid_constant__ DepthIO io, int64_t n) {
   const int v = blockIdx.y;
-  const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
   const uint32_t* k32s = k32s_all + (size_t)v * ks;
-  const uint32_t k = i < n ? k32s[i] : kKeyInvisible;
-  uint32_t prev = __shfl_up_sync(0xffffffffu, k, 1), next = __shfl_down_sync(0xffffffffu, k, 1);
-  if (lane == 0) prev = (i > 0 && i - 1 < n) ? k32s[i - 1] : kKeyInvisible;
-  if (lane == 31) next = i + 1 < n ? k32s[i + 1] : kKeyInvisible;
-  // the invisible tail's order is irrelevant
-  const bool start = i < n && k != kKeyInvisible && prev != k && next == k;
-  uint32_t starts = __ballot_sync(0xffffffffu, start);
-  if (!starts) return;
-  const uint64_t* key = io.key[v];
+  const uint32_t* tmp = tmp_all + (size_t)v * ks;
   int32_t* order = io.order[v];
-  while (starts) {
-    const int src = __ffs(starts) - 1;
-    starts &= starts - 1;
-    const int64_t i0 = __shfl_sync(0xffffffffu, i, src);
-    const uint32_t kv = __shfl_sync(0xffffffffu, k, src);
-    const int64_t j = i0 + lane;
-    const bool in = j < n && k32s[j] == kv;
-    const uint32_t inb = __ballot_sync(0xffffffffu, in);
-    if (inb == 0xffffffffu) {
-      // longer than a warp: serial in-place insertion sort by (key, index)
-      if (lane == 0) {
-        int64_t e = i0 + 32;
-        while (e < n && k32s[e] == kv) ++e;
-        for (int64_t a = i0 + 1; a < e; ++a) {
-          const int32_t g = order[a];
-          const uint64_t kg = key[g];
-          int64_t b = a - 1;
-          while (b >= i0) {
-            const int32_t h = order[b];
-            const uint64_t kh = key[h];
-            if (kh < kg || (kh == kg && h < g)) break;
-            order[b + 1] = h;
-            --b;
-          }
-          order[b + 1] = g;
-        }
+  const uint32_t k = k32s[i];
+  const int32_t g = (int32_t)tmp[i];
+  if (k == kKeyInvisible) { order[i] = g; return; }   // invisible tail: order irrelevant
+  int64_t s = i, e = i + 1;
+  while (s > 0 && k32s[s - 1] == k) --s;
+  while (e < n && k32s[e] == k) ++e;
+  if (e - s == 1) { order[i] = g; return; }
+  const uint64_t* key = io.key[v];
+  if (e - s > kRunPar) {
+    if (i != s) return;
+    for (int64_t a = s; a < e; ++a) order[a] = (int32_t)tmp[a];
+    for (int64_t a = s + 1; a < e; ++a) {              // insertion sort by (key, index)
+      const int32_t ga = order[a];
+      const uint64_t kga = key[ga];
+      int64_t b = a - 1;
+      while (b >= s) {
+        const int32_t h = order[b];
+        const uint64_t kh = key[h];
+        if (kh < kga || (kh == kga && h < ga)) break;
+        order[b + 1] = h;
+        --b;
       }
-      __syncwarp();
-      continue;
+      order[b + 1] = ga;
     }
-    const int L = __ffs(~inb) - 1;   // run length (>= 2)
-    const int32_t g = lane < L ? order[i0 + lane] : 0;
-    const uint64_t kg = lane < L ? key[g] : ~0ull;
-    int rank = 0;
-    for (int t = 0; t < L; ++t) {
-      const int32_t gt = __shfl_sync(0xffffffffu, g, t);
-      const uint64_t kt = __shfl_sync(0xffffffffu, kg, t);
-      rank += (kt < kg || (kt == kg && gt < g)) ? 1 : 0;
-    }
-    __syncwarp();
-    if (lane < L) order[i0 + rank] = g;
-    __syncwarp();
+    return;
   }
+  const uint64_t kg = key[g];
+  int rank = 0;
+  for (int64_t j = s; j < e; ++j) {
+    const int32_t h = (int32_t)tmp[j];
+    const uint64_t kh = key[h];
+    rank += (j != i && (kh < kg || (kh == kg && h < g))) ? 1 : 0;
+  }
+  order[s + rank] = g;
 }
 
 // per-view stride of the 24-bit key arrays (keeps uint2 stores aligned)
 static int64_t key_stride(int64_t n) { return (n + 63) & ~int64_t(63); }
 
 static size_t depth_ws_bytes(int64_t n, int nv) {
-  return align_up(16 * (size_t)nv) + 2 * align_up(sizeof(uint32_t) * (size_t)nv * key_stride(n)) +
+  return align_up(16 * (size_t)nv) + 3 * align_up(sizeof(uint32_t) * (size_t)nv * key_stride(n)) +
          radix_ws_bytes(n, nv);
 }
 
@@ -1204,6 +1190,7 @@ int launch_depth_order_batch(int nv, const sdgr_projection* projs, int32_t* cons
   const int64_t ks = key_stride(n);
   uint32_t* k32 = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * ks);
   uint32_t* k32s = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * ks);
+  uint32_t* tmp = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * ks);
   const RadixWs r = radix_layout(p, n, nv);
   DepthIO dio;
   for (int v = 0; v < nv; ++v) {
@@ -1223,12 +1210,12 @@ int launch_depth_order_batch(int nv, const sdgr_projection* projs, int32_t* cons
     sio.kin[v] = k32 + (size_t)v * ks;
     sio.vin[v] = nullptr;
     sio.kout[v] = k32s + (size_t)v * ks;
-    sio.vout[v] = reinterpret_cast<uint32_t*>(orders[v]);
+    sio.vout[v] = tmp + (size_t)v * ks;   // k_fix_runs moves it to orders[v]
     sio.n_dev[v] = nullptr;
   }
   const int rc = radix_passes(sio, true, nv, n, kMaxPass, r, st);
   if (rc != SDGR_OK) return rc;
-  k_fix_runs<<<dim3((unsigned)((n + 255) / 256), nv), 256, 0, st>>>(k32s, ks, dio, n);
+  k_fix_runs<<<dim3((unsigned)((n + 255) / 256), nv), 256, 0, st>>>(k32s, tmp, ks, dio, n);
   note_launch();
   return check_launch();
 }
