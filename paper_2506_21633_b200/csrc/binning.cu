@@ -519,7 +519,10 @@ __global__ void __launch_bounds__(256) k_emit_pairs(const __grid_constant__ Emit
 // sdgr_plane.emit) once.  Block = 2048 consecutive list positions; its pair
 // offset comes from a single-value decoupled look-back (warp-wide window) over
 // the view's earlier blocks, blocks ticketed like the onesweep passes.
-constexpr int kEmitIpt = 8;
+#ifndef SDGR_EMIT_IPT
+#define SDGR_EMIT_IPT 4
+#endif
+constexpr int kEmitIpt = SDGR_EMIT_IPT;
 constexpr int kEmitTile = 256 * kEmitIpt;
 constexpr unsigned long long kSFlagA = 1ull << 62, kSFlagP = 2ull << 62, kSValue = (1ull << 62) - 1;
 
@@ -538,7 +541,7 @@ struct FusedEmitIO {
 };
 
 #ifndef SDGR_EMIT_MINB
-#define SDGR_EMIT_MINB 2
+#define SDGR_EMIT_MINB 3
 #endif
 __global__ void __launch_bounds__(256, SDGR_EMIT_MINB) k_count_emit(const __grid_constant__ FusedEmitIO io, int nv, int64_t n,
                                                     int64_t nblk, int tiles_x, double cutoff, int64_t cap,
