@@ -85,7 +85,6 @@ struct WalkArgs {
   double* partial;         // kContrib: (n_pairs); kGrad: (n_pairs, 8)
   int32_t* status;
   sdgr_replay rp;          // kContrib: live-pair log to write (rp.y1 == nullptr: none)
-  int seg_filter;          // 0: all items, 1: first segment of each tile only, 2: later segments only
 };
 
 // 256-bit in-tile member mask of one Gaussian (bit = local cell (iv&15)*16+(iu&15)).
@@ -414,7 +413,6 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
     const int item = item_s;
     if (item >= n_items) return;
     const int4 it = reinterpret_cast<const int4*>(a.items)[item];
-    if ((a.seg_filter == 1 && item != it.w) || (a.seg_filter == 2 && item == it.w)) continue;
     const int tile = it.x, start = it.y, end = it.z;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     const int iu = tx * kTile + (tid & 15), iv = ty * kTile + (tid >> 4);

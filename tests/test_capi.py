@@ -82,3 +82,45 @@ def test_struct_layouts_match_c(tmp_path):
         for f, _ in py._fields_:
             assert int(out[f"{cname}.{f}"]) == getattr(py, f).offset, f"{cname}.{f}"
     assert int(out["sdgr_pair_rec"]) == _lib.PAIR_REC_BYTES
+
+
+def test_batch_entry_points_validate_without_device(lib):
+    from paper_2506_21633_b200 import _lib
+    mb = lib.sdgr_max_batch()
+    assert mb == _lib.MAX_BATCH == 16
+    # workspace sizing: 0 outside 1..max_batch, growing with the batch
+    assert lib.sdgr_batch_workspace_bytes(1_000_000, 1_500_000, 0) == 0
+    assert lib.sdgr_batch_workspace_bytes(1_000_000, 1_500_000, mb + 1) == 0
+    w1 = lib.sdgr_batch_workspace_bytes(1_000_000, 1_500_000, 1)
+    assert w1 == lib.sdgr_workspace_bytes(1_000_000, 1_500_000)
+    assert lib.sdgr_batch_workspace_bytes(1_000_000, 1_500_000, mb) > 8 * w1
+    sd = _lib.SceneDesc()
+    views = (_lib.View * (mb + 1))()
+    projs = (_lib.ProjectionDesc * (mb + 1))()
+    tiles = (_lib.TilesDesc * (mb + 1))()
+    ptrs = (C.c_void_p * (mb + 1))()
+    for k in (0, mb + 1):   # batch size out of range
+        assert lib.sdgr_project_batch(C.byref(sd), k, views, projs, None) == _lib.ERR_INVALID
+        assert lib.sdgr_depth_order_batch(k, projs, ptrs, None, 0, None) == _lib.ERR_INVALID
+        assert lib.sdgr_bin_batch(k, projs, views, 0, ptrs, ptrs, tiles, None, 0, None) == _lib.ERR_INVALID
+        assert lib.sdgr_grad_geometry_batch(C.byref(sd), k, views, projs, tiles, ptrs, ptrs,
+                                            C.byref(_lib.GradsDesc()), 1, None) == _lib.ERR_INVALID
+    # NULL orders / unset views inside a valid batch size
+    assert lib.sdgr_depth_order_batch(2, projs, None, None, 0, None) == _lib.ERR_INVALID
+    assert lib.sdgr_bin_batch(2, projs, views, 0, None, ptrs, tiles, None, 0, None) == _lib.ERR_INVALID
+    assert lib.sdgr_project_batch(C.byref(sd), 2, views, projs, None) == _lib.ERR_INVALID
+
+
+def test_eval_entry_points_validate_without_device(lib):
+    from paper_2506_21633_b200 import _lib
+    lo = (C.c_double * 3)(0.0, 0.0, 0.0)
+    dims = (C.c_int32 * 3)(4, 4, 4)
+    bad_dims = (C.c_int32 * 3)(4096, 4096, 4096)   # > 2^24 cells
+    assert lib.sdgr_grid_workspace_bytes(1000, 64) > 0
+    one = C.c_void_p(1)
+    assert lib.sdgr_nn_sqdist(one, 10, one, 10, lo, 0.0, dims, one, one, 1 << 30, None) == _lib.ERR_INVALID
+    assert lib.sdgr_nn_sqdist(one, 10, one, 10, lo, 1.0, bad_dims, one, one, 1 << 30, None) == _lib.ERR_INVALID
+    assert lib.sdgr_nn_sqdist(one, 10, one, 10, lo, 1.0, dims, one, one, 16, None) == _lib.ERR_CAPACITY
+    # DBSCAN needs cells at least eps wide and min_pts >= 1
+    assert lib.sdgr_dbscan(one, 10, lo, 0.5, dims, 1.0, 3, one, one, 1 << 30, None) == _lib.ERR_INVALID
+    assert lib.sdgr_dbscan(one, 10, lo, 1.0, dims, 1.0, 0, one, one, 1 << 30, None) == _lib.ERR_INVALID
