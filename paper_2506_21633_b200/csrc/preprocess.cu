@@ -230,6 +230,19 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
   // the per-view FP64 chain inside 64 registers without spills); per-view
   // counters are block accumulators flushed once at the end
   __shared__ double s_state[11][256];
+  // FP32 scenes: the block's SH coefficients, staged once with coalesced
+  // loads (read every view; otherwise 16 strided global loads per view per
+  // Gaussian).  FP64 scenes read them from global (the FP64 copy would not
+  // fit next to s_state).
+  constexpr bool kStageSh = sizeof(T) == 4;
+  __shared__ float s_sh[16][256];
+  const T* S = static_cast<const T*>(scene.sh_coeffs);
+  if (kStageSh) {
+    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t lim = (scene.n - g0) * 16;   // valid coefficients of this block
+    for (int e = threadIdx.x; e < 16 * 256; e += blockDim.x)
+      s_sh[e & 15][e >> 4] = e < lim ? (float)__ldg(S + g0 * 16 + e) : 0.f;
+  }
   __shared__ unsigned long long s_cnt[SDGR_MAX_BATCH][5];
   {
     const double st[11] = {p0, p1, p2, C00, C01, C02, C11, C12, C22, kf, kb};
@@ -324,10 +337,10 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
         const double d0 = r0 * idist, d1 = r1 * idist, d2 = r2 * idist;
         double b[16];
         sh_basis(d0, d1, d2, b);
-        const T* S = static_cast<const T*>(scene.sh_coeffs);
         double praw = 0.0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) praw += b[j] * ld(S, 16 * g + j);
+        for (int j = 0; j < 16; ++j)
+          praw += b[j] * (kStageSh ? (double)s_sh[j][threadIdx.x] : ld(S, 16 * g + j));
         const double ph = (praw == praw) ? fmax(praw, 0.0) : praw;  // NaN propagates (np.maximum)
         const double kfv = s_state[9][threadIdx.x], kbv = s_state[10][threadIdx.x], kappa_g = kfv + kbv;
         if (proj.kappa) proj.kappa[g] = kappa_g;
