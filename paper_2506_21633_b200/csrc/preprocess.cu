@@ -243,12 +243,13 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
     for (int e = threadIdx.x; e < 16 * 256; e += blockDim.x)
       s_sh[e & 15][e >> 4] = e < lim ? (float)__ldg(S + g0 * 16 + e) : 0.f;
   }
-  __shared__ unsigned long long s_cnt[SDGR_MAX_BATCH][5];
+  // per-warp counter slots (plain stores; 64-bit shared atomics are CAS loops)
+  __shared__ unsigned long long s_cnt[SDGR_MAX_BATCH][5][8];
   {
     const double st[11] = {p0, p1, p2, C00, C01, C02, C11, C12, C22, kf, kb};
 #pragma unroll
     for (int j = 0; j < 11; ++j) s_state[j][threadIdx.x] = st[j];
-    for (int i = threadIdx.x; i < SDGR_MAX_BATCH * 5; i += blockDim.x) (&s_cnt[0][0])[i] = 0ull;
+    for (int i = threadIdx.x; i < SDGR_MAX_BATCH * 5 * 8; i += blockDim.x) (&s_cnt[0][0][0])[i] = 0ull;
   }
   __syncthreads();
 
@@ -376,17 +377,20 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
       m_img += __shfl_down_sync(0xffffffffu, m_img, off);
     }
     if ((threadIdx.x & 31) == 0) {
-      if (cv) atomicAdd(&s_cnt[k][0], (unsigned long long)cv);
-      if (cs) atomicAdd(&s_cnt[k][1], (unsigned long long)cs);
-      if (cc) atomicAdd(&s_cnt[k][2], (unsigned long long)cc);
-      if (m_comp) atomicAdd(&s_cnt[k][3], m_comp);
-      if (m_img) atomicAdd(&s_cnt[k][4], m_img);
+      const int w = threadIdx.x >> 5;
+      s_cnt[k][0][w] = (unsigned long long)cv;
+      s_cnt[k][1][w] = (unsigned long long)cs;
+      s_cnt[k][2][w] = (unsigned long long)cc;
+      s_cnt[k][3][w] = m_comp;
+      s_cnt[k][4][w] = m_img;
     }
   }
   __syncthreads();
   if (threadIdx.x < 5 * B.nv) {
     const int k = threadIdx.x / 5, j = threadIdx.x % 5;
-    const unsigned long long c = s_cnt[k][j];
+    unsigned long long c = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) c += s_cnt[k][j][w];
     const sdgr_projection& proj = B.proj[k];
     if (c) {
       if (j < 3) atomicAdd(proj.counters + j, (int)c);
