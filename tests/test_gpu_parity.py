@@ -434,3 +434,35 @@ def test_batched_preprocessing_small_scenes(cutoff):
         assert torch.equal(t["pair_prim"][:m].cpu(), tl.pair_prim[:m].cpu()), f"view {k}: key lists"
         assert torch.equal(t["tile_range"].cpu(), tl.tile_range.cpu()), f"view {k}: tile ranges"
         assert torch.equal(t["pair_rec"][:m].cpu(), tl.pair_rec[:m].cpu()), f"view {k}: pair records"
+
+
+def test_multiview_batch_with_a_view_that_sees_nothing():
+    """A batch where one view culls every Gaussian (zero pairs: empty sort,
+    empty tile lists, no work items) next to normal views: the step still
+    equals the sum of the single-view passes, and the empty view adds nothing."""
+    from paper_2506_21633_b200.multiview import MultiViewStep
+
+    tank = targets.composite_target(targets.tank_preset(), [2000, 1000, 500], seed=2)
+    tank.positions[:, 0] += 30.0                          # the target sits 30 m off the scene origin
+    tank = targets.to_float32_exact(tank)
+    wide = dict(range_res_m=1.5, azimuth_res_m=1.5, n_range=96, n_azimuth=96)     # 144 m frames: see it
+    narrow = dict(range_res_m=0.2, azimuth_res_m=0.2, n_range=96, n_azimuth=96)   # 19 m frame: culls all
+    cfgs = [sdgr.RadarConfig(azimuth_deg=30.0, elevation_deg=45.0, altitude_m=0.5, **wide),
+            sdgr.RadarConfig(azimuth_deg=0.0, elevation_deg=45.0, altitude_m=0.5, **narrow),
+            sdgr.RadarConfig(azimuth_deg=250.0, elevation_deg=60.0, altitude_m=0.5, **wide)]
+    ds = sdgr.DeviceScene.from_host(tank, dtype=torch.float32)
+    empty = sdgr.render_forward(ds, cfgs[1])
+    assert empty.rays.n_pairs == 0 and not bool(empty.projection.visible.any())
+    step = MultiViewStep(ds, cfgs)
+    dl = torch.randn((3, 96, 96), dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    got = step.run(dl)
+    ref = {k: 0.0 for k in GROUPS + ("uv_grad_norm",)}
+    vis = 0
+    for i, c in enumerate(cfgs):
+        g = sdgr.backward(sdgr.render_forward(ds, c), dl[i])
+        for k in ref:
+            ref[k] = ref[k] + getattr(g, k).double()
+        vis = vis + g.visible
+    for k in ref:
+        assert_close(getattr(got, k).double().cpu().numpy(), ref[k].cpu().numpy(), atol=1e-5, rtol=1e-5, what=k)
+    assert torch.equal(got.visible.cpu(), vis.cpu())
