@@ -332,12 +332,22 @@ __global__ void __launch_bounds__(256) k_splat(sdgr_view view, sdgr_plane pl, co
     const int lim = min(tot, B + kList);
     fill_window(m, nx, lim, lane, list, B);
     __syncwarp();
-    for (int k = B + lane; k < lim; k += 32) {
-      const int e = list[k - B];
-      const int j = wbase + (e >> 8), b = e & 63;
-      const int iu = s_x[j] + (b & 7), iv = s_y[j] + (b >> 3);
-      splat_add(acc, view.n_az, iu, iv,
-                quadform(s_a0[j], s_a1[j], s_a2[j], dsub((double)iu, s_u[j]), dsub((double)iv, s_v[j])), s_I[j]);
+    for (int k0 = B; k0 < lim; k0 += 32) {
+      const int k = k0 + lane;
+      const bool on = k < lim;
+      int64_t pix = 0;
+      unsigned long long val = 0ull;
+      if (on) {
+        const int e = list[k - B];
+        const int j = wbase + (e >> 8), b = e & 63;
+        const int iu = s_x[j] + (b & 7), iv = s_y[j] + (b >> 3);
+        const double q = quadform(s_a0[j], s_a1[j], s_a2[j], dsub((double)iu, s_u[j]), dsub((double)iv, s_v[j]));
+        pix = (int64_t)iv * view.n_az + iu;
+        val = (unsigned long long)__double2ull_rn(fmin(exp(-q) * s_I[j], kFixMax) * kFix);
+      }
+      // (combining a round's same-pixel terms with MATCH.ANY before the RED
+      // was measured slower: 4.0 -> 6.5 ms/step, only ~17 % of the REDs merge)
+      if (on) atomicAdd(acc + pix, val);
     }
     __syncwarp();
   }
