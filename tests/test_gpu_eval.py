@@ -114,3 +114,20 @@ def test_large_cloud_throughput_sanity(ev):
     np.testing.assert_allclose(d2[sub], E.nn_sqdist(rec[sub], ref), rtol=1e-13, atol=0)
     labels = ev.dbscan_labels(rec[:200_000], 0.1, 5)
     assert labels.shape[0] == 200_000
+
+
+def test_dbscan_tank_scene_matches_sklearn(ev):
+    """The reference's own use (acceptance criterion 8, test_acceptance.py:227):
+    dbscan_filter(scene.positions, eps=0.3, min_pts=5) on a generated tank,
+    labels identical to sklearn's DBSCAN (the reference's implementation)."""
+    sklearn = pytest.importorskip("sklearn.cluster")
+    from paper_2506_21633_b200 import targets
+
+    scene = targets.composite_target(targets.tank_preset(), [12000, 6000, 2000], seed=4)
+    pts = np.vstack([scene.positions, np.random.default_rng(1).uniform(-15, 15, size=(500, 3))])
+    for eps, mp in ((0.3, 5), (0.15, 8)):
+        want = sklearn.DBSCAN(eps=eps, min_samples=mp).fit(pts).labels_
+        got = ev.dbscan_labels(pts, eps, mp).cpu().numpy()
+        np.testing.assert_array_equal(got, want)
+        np.testing.assert_array_equal(ev.dbscan_inlier_mask(pts, eps, mp, keep_largest=True),
+                                      want == np.argmax(np.bincount(want[want >= 0])))
