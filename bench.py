@@ -52,9 +52,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sdgr", choices=("sdgr", "reference"))
-    ap.add_argument("--n", type=int, default=1_000_000)
-    ap.add_argument("--size", type=int, default=512)
-    ap.add_argument("--views-per-rank", type=int, default=45)
+    ap.add_argument("--workload", default="c4", choices=tuple(WORKLOADS),
+                    help="SURVEY.md §8d configuration (default c4, the metric's configuration)")
+    ap.add_argument("--n", type=int, default=None, help="override the workload's Gaussian count")
+    ap.add_argument("--size", type=int, default=None, help="override the workload's image size")
+    ap.add_argument("--sigma", type=float, default=None, help="isotropic Gaussian scale in m (c5 sweep)")
+    ap.add_argument("--views-per-rank", type=int, default=None)
+    ap.add_argument("--dropin-views", type=int, default=6,
+                    help="views timed through render_forward + backward with host arrays (0 = skip)")
     ap.add_argument("--param-dtype", default="f32", choices=("f32", "f64"))
     ap.add_argument("--s-stop", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -62,23 +67,65 @@ def parse():
     ap.add_argument("--cpu-procs", type=int, default=0)
     ap.add_argument("--lanes", type=int, default=8, help="concurrent view streams per GPU")
     ap.add_argument("--geo-batch", type=int, default=None, help="views per batched launch (default: the build's max)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    w = WORKLOADS[a.workload]
+    a.n = a.n or w["n"]
+    a.size = a.size or w["size"]
+    a.views_per_rank = a.views_per_rank or w["views_per_rank"]
+    return a
 
 
-def view_list(size: int):
+# SURVEY.md §8d configurations (BASELINE.json configs[1..4]); the metric is quoted on c4
+WORKLOADS = {
+    "c2": dict(n=100_000, size=256, views_per_rank=36, scene="tank", az=range(0, 360, 10), el=(45.0,),
+               label="single vehicle (tank_preset), {n} Gaussians, {size}x{size}, az 0:360:10 x el 45"),
+    "c3": dict(n=300_000, size=256, views_per_rank=72, scene="tank", az=range(0, 360, 15), el=(15.0, 45.0, 75.0),
+               label="single vehicle (tank_preset), {n} Gaussians, {size}x{size}, az 0:360:15 x el 15/45/75"),
+    "c4": dict(n=1_000_000, size=512, views_per_rank=45, scene="grid", az=range(0, 360, 3), el=(30.0, 45.0, 60.0),
+               label="16-tank grid (20 m pitch), {n} Gaussians, {size}x{size}, az 0:360:3 x el 30/45/60"),
+    "c5": dict(n=1_000_000, size=512, views_per_rank=8, scene="grid", az=range(0, 360, 45), el=(45.0,),
+               label="backward stress: 16-tank grid, {n} Gaussians, isotropic sigma {sigma} m, {size}x{size}, el 45"),
+}
+
+
+def workload_label(args) -> str:
+    return f"{args.workload}: " + WORKLOADS[args.workload]["label"].format(n=args.n, size=args.size,
+                                                                          sigma=args.sigma)
+
+
+def view_list(size: int, workload: str = "c4"):
     from paper_2506_21633_b200.radar import RadarConfig
+    w = WORKLOADS[workload]
     out = []
-    for az in range(0, 360, 3):
-        for el in (30.0, 45.0, 60.0):
+    for az in w["az"]:
+        for el in w["el"]:
             out.append(RadarConfig(azimuth_deg=float(az), elevation_deg=el, altitude_m=0.5, range_res_m=0.3,
                                    azimuth_res_m=0.3, n_range=size, n_azimuth=size))
     return out
 
 
-def make_scene(n: int):
+def make_scene(n: int, workload: str = "c4", sigma: float | None = None):
     from paper_2506_21633_b200 import targets
+    if WORKLOADS[workload]["scene"] == "tank":   # budgets 0.6 / 0.3 / 0.1 as SURVEY §8d c2 / c3
+        b = [int(round(0.6 * n)), int(round(0.3 * n))]
+        scene = targets.composite_target(targets.tank_preset(), b + [n - sum(b)], seed=3)
+    else:
+        scene = targets.tank_grid(n_total=n)
+    if sigma is not None:
+        scene.log_scales[:] = np.log(sigma)
     # float32-exact so the float32 device scene and the FP64 oracle see the same Gaussians
-    return targets.to_float32_exact(targets.tank_grid(n_total=n))
+    return targets.to_float32_exact(scene)
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -183,8 +230,8 @@ def run_reference(args):
         return
     from oracle import sdgr_oracle
     sdgr_oracle.build()
-    scene = make_scene(args.n)
-    cfgs = view_list(args.size)
+    scene = make_scene(args.n, args.workload, args.sigma)
+    cfgs = view_list(args.size, args.workload)
     procs = cpu_procs(args.cpu_procs)
     # warm-up: one-time costs only (fork, imports, page-in) on a small sample
     from paper_2506_21633_b200 import targets
@@ -204,10 +251,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "c4: 16-tank grid, 1M Gaussians, 512x512, 360 views (az 0:360:3 x el 30/45/60)",
+        "config": {"workload": workload_label(args),
                    "views_per_step": procs, "gaussians": args.n, "image": [args.size, args.size]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": f"{procs} c4 views per step, one per forked process "
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "cpu": cpu_model(),
+                         "sample": f"{procs} {args.workload} views per step, one per forked process "
                                    "(oracle/sdgr_oracle.py: NumPy + C key chain, OPENBLAS_NUM_THREADS=1)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -216,7 +263,7 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- GPU side
 SCENE_B = 12 + 16 + 12 + 64 + 8          # f32 positions, rotations, log_scales, sh_coeffs, ke_raw per Gaussian
-GRAD_RMW_B = 2 * (29 * 4 + 4)            # f32 gradient groups + int32 visible count, read + written
+GRAD_RMW_B = 2 * (29 * 4 + 4)            # f32 gradient groups + f32 visible count, read + written
 PROJ_W_B = 2 * (16 + 32 + 8 + 8 + 8 + 4) + 8 * 4 + 1 + 64 + 16   # K1 outputs per Gaussian: two planes, key/kappa/phase/flags, packed + emit rows
 REC_B = 80                               # packed computation-plane pair record
 LOG_B = 8 + 8 + 8 + 1 + 1                # replay log entry: y1, t2, w, j, r
@@ -303,6 +350,60 @@ def ncu_traffic(kernel: str):
     return (e["dram_bytes_per_launch"], d.get("source")) if e else (None, None)
 
 
+def dropin_rate(sdgr, host_scene, cfgs, views: int, world: int, rank: int) -> dict:
+    """Views/s of the reference-shaped call sequence -- one view per call, as
+    the reference's optimize.train does (optimize.py:396-411):
+    fwd = render_forward(numpy FP64 scene, config); grads = backward(fwd,
+    numpy dL/dS) -> numpy FP64 SceneGradients.  Every call uploads the FP64
+    scene and downloads FP64 gradients (pageable numpy memory), so the rate
+    is bounded by those PCIe copies; `copy_bound` times the same bytes as
+    bare torch copies for comparison."""
+    import torch
+    import torch.distributed as dist
+    rng = np.random.default_rng(7 + rank)
+    size = (cfgs[0].n_range, cfgs[0].n_azimuth)
+    dls = [rng.normal(size=size) for _ in range(views)]
+    g = sdgr.backward(sdgr.render_forward(host_scene, cfgs[0]), dls[0])   # warm (first-call attributes)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    t0 = time.perf_counter()
+    for i in range(views):
+        fwd = sdgr.render_forward(host_scene, cfgs[i % len(cfgs)])
+        g = sdgr.backward(fwd, dls[i])
+    e1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1) / views
+    # the bytes every call moves: FP64 scene + dL/dS up; image, FP64 gradients + visible down
+    up = [getattr(host_scene, k) for k in ("positions", "rotations", "log_scales", "sh_coeffs", "ke_raw")] + [dls[0]]
+    down = list(g.param_arrays()) + [g.uv_grad_norm, g.visible, np.zeros(size)]
+    h2d = sum(a.nbytes for a in up)
+    d2h = sum(a.nbytes for a in down)
+    dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in up]
+    back = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in down]
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for _ in range(3):
+        for a, d in zip(up, dev):
+            d.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+        for b in back:
+            b.cpu().numpy()
+    c1.record()
+    torch.cuda.synchronize()
+    copy_ms = c0.elapsed_time(c1) / 3
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": world / (ms / 1e3), "unit": UNIT, "ms_per_view": ms, "wall_ms_per_view": 1e3 * wall / views,
+            "views_timed": views, "h2d_bytes_per_view": int(h2d), "d2h_bytes_per_view": int(d2h),
+            "copy_bound": {"ms_per_view": copy_ms, "views_per_s": world / (copy_ms / 1e3),
+                           "what": "the same H2D + D2H bytes as bare torch copies from/to pageable numpy"},
+            "call": "render_forward(numpy scene, cfg) + backward(fwd, numpy dL/dS) -> numpy FP64 gradients"}
+
+
 def run_sdgr(args):
     import torch
     import torch.distributed as dist
@@ -317,8 +418,8 @@ def run_sdgr(args):
     from paper_2506_21633_b200.multiview import MultiViewStep
 
     pdt = torch.float32 if args.param_dtype == "f32" else torch.float64
-    host_scene = make_scene(args.n)
-    cfgs_all = view_list(args.size)
+    host_scene = make_scene(args.n, args.workload, args.sigma)
+    cfgs_all = view_list(args.size, args.workload)
     # rank r takes views r, r+W, ... and the first views_per_rank of them
     mine = [c for i, c in enumerate(cfgs_all) if i % world == rank]
     mine = (mine * (1 + args.views_per_rank // max(len(mine), 1)))[: args.views_per_rank]
@@ -421,6 +522,11 @@ def run_sdgr(args):
                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t.item()),
                "pipeline": "two device banks: step k's H2D/D2H overlap the neighbouring steps' compute"}
 
+    # ---------------- e2e through the reference-shaped drop-in ----------------
+    dropin = None
+    if args.dropin_views > 0:
+        dropin = dropin_rate(sdgr, host_scene, mine, args.dropin_views, world, rank)
+
     # ---------------- roofline: the dominant kernel ----------------
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -448,7 +554,7 @@ def run_sdgr(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "c4: 16-tank grid, 1M Gaussians, 512x512, 360 views (az 0:360:3 x el 30/45/60)",
+        "config": {"workload": workload_label(args),
                    "views_per_rank": V, "gaussians": args.n, "image": [args.size, args.size],
                    "param_dtype": args.param_dtype, "parallelism": f"view-sharded dp{world}",
                    "s_stop": step.s_stop, "l2": "inputs larger than L2 (112 MB params + ~0.3 GB/view records)",
@@ -459,14 +565,16 @@ def run_sdgr(args):
         "preprocess_sort_roofline": preprocess_sort_roofline(args.n, step, stages, V, peak),
         "gpu_launches": int(launches),
         "e2e": e2e,
+        "e2e_dropin": dropin,
         "clocks": clk.summary(),
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         procs = cpu_procs(args.cpu_procs)
         wall = cpu_run(host_scene, cfgs_all, procs, procs)
         line["cpu_baseline"] = {"value": procs / wall, "unit": UNIT, "cores": procs, "kind": "port",
-                                "sample": f"{procs} c4 views (1M Gaussians, 512x512), one per forked process, "
-                                          f"{wall:.1f} s wall"}
+                                "cpu": cpu_model(),
+                                "sample": f"{procs} {args.workload} views ({args.n} Gaussians, {args.size}x{args.size}),"
+                                          f" one per forked process, {wall:.1f} s wall"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

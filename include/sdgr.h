@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SDGR_ABI_VERSION 1
+#define SDGR_ABI_VERSION 2
 #define SDGR_TILE 16          /* tile edge in cells / pixels (16x16 = 256 rays) */
 #define SDGR_TILE_RAYS 256
 #define SDGR_MAX_PLANE 32767  /* plane dims must fit int16 bboxes */
@@ -185,15 +185,22 @@ typedef struct sdgr_tiles {
                               (computation plane; filled by sdgr_bin_pairs)   */
 } sdgr_tiles;
 
-/* Scene gradients (backward.SceneGradients, backward.py:25-50), float32. */
+/* Scene gradients (backward.SceneGradients, backward.py:25-50).
+ * dtype selects the element type of every gradient array: 0 = float32
+ * (device training steps), 1 = float64 (host callers: the reference returns
+ * FP64).  visible_dtype: 0 = int32 view counts, 1 = counts stored in `dtype`
+ * (exact below 2^24 in float32), so a flat multi-view gradient buffer is
+ * summed across ranks by ONE all-reduce. */
 typedef struct sdgr_grads {
-  float* positions;     /* (n,3)  */
-  float* rotations;     /* (n,4)  */
-  float* log_scales;    /* (n,3)  */
-  float* sh_coeffs;     /* (n,16) */
-  float* ke_raw;        /* (n,2)  */
-  float* uv_grad_norm;  /* (n)    */
-  int32_t* visible;     /* (n) 1 if visible (accumulate mode: count of views) */
+  int32_t dtype;
+  int32_t visible_dtype;
+  void* positions;      /* (n,3)  */
+  void* rotations;      /* (n,4)  */
+  void* log_scales;     /* (n,3)  */
+  void* sh_coeffs;      /* (n,16) */
+  void* ke_raw;         /* (n,2)  */
+  void* uv_grad_norm;   /* (n)    */
+  void* visible;        /* (n) 1 if visible (accumulate mode: count of views) */
 } sdgr_grads;
 
 /* ---------------------------------------------------------------- misc -- */
@@ -341,10 +348,15 @@ int sdgr_loss(const double* S, const double* Y, int h, int w, double lambda_ssim
  * FP32 SceneGradients.  lr[5] per group (positions, rotations, log_scales,
  * sh_coeffs, ke_raw); bc1 = 1 - beta1^step, bc2 = 1 - beta2^step computed by
  * the caller; displacement_bound <= 0 disables the clamp.  Non-finite
- * gradient entries are zeroed and added to *n_skipped (device u64). */
+ * gradient entries are zeroed and added to *n_skipped (device u64).  grads
+ * must be float32 (dtype 0).  guard: optional device int32; when it is
+ * non-zero at run time the whole update is skipped (a multi-view step whose
+ * pair buffers overflowed produced truncated gradients -- MultiViewStep's
+ * overflow word -- so the step can be recalibrated and re-run exactly). */
 int sdgr_adam_step(sdgr_scene* scene, const sdgr_grads* grads, sdgr_scene* m, sdgr_scene* v,
                    const double* lr, double beta1, double beta2, double eps, double bc1, double bc2,
-                   double displacement_bound, unsigned long long* n_skipped, void* stream);
+                   double displacement_bound, unsigned long long* n_skipped, const int32_t* guard,
+                   void* stream);
 
 /* -------------------------------- densification ------ */
 /* optimize.densify_and_prune (optimize.py:251-312) and GradAccumulator
@@ -352,7 +364,8 @@ int sdgr_adam_step(sdgr_scene* scene, const sdgr_grads* grads, sdgr_scene* m, sd
  * the flags define, and draws the split samples xi from its own seeded
  * generator (rng.normal(size=(2 * n_split, 3)), as the reference does). */
 /* norm_sum += uv_grad_norm, pos_sum (n,3) += positions, count += visible for
- * rows with visible > 0 (visible = views that saw the Gaussian). FP64. */
+ * rows with visible > 0 (visible = views that saw the Gaussian). FP64 sums;
+ * grads float32 (dtype 0), visible int32 or float32 counts. */
 int sdgr_accum_update(const sdgr_grads* grads, int64_t n, double* norm_sum, double* pos_sum,
                       double* count, void* stream);
 /* flags[g] = 2 split (max e^s > cap), 1 clone (mean norm > grad_thr, small,

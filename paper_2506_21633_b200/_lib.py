@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 import os  # noqa: E402
 
 # SDGR_LIB selects a profiling build (e.g. libsdgr_prof.so) of the same ABI
@@ -86,6 +86,7 @@ PAIR_REC_BYTES = 80  # sizeof(sdgr_pair_rec)
 
 class GradsDesc(C.Structure):
     _fields_ = [
+        ("dtype", C.c_int32), ("visible_dtype", C.c_int32),
         ("positions", _p), ("rotations", _p), ("log_scales", _p), ("sh_coeffs", _p),
         ("ke_raw", _p), ("uv_grad_norm", _p), ("visible", _p),
     ]
@@ -139,7 +140,7 @@ SIGNATURES = [
     ("sdgr_loss", C.c_int, [_p, _p, C.c_int, C.c_int, C.c_double, C.c_double, _p, _p, _p, _p, _p]),
     ("sdgr_adam_step", C.c_int, [C.POINTER(SceneDesc), C.POINTER(GradsDesc), C.POINTER(SceneDesc),
                                  C.POINTER(SceneDesc), C.POINTER(C.c_double), C.c_double, C.c_double,
-                                 C.c_double, C.c_double, C.c_double, C.c_double, _p, _p]),
+                                 C.c_double, C.c_double, C.c_double, C.c_double, _p, _p, _p]),
 ]
 
 

@@ -151,27 +151,36 @@ struct GeoBatch {
 
 // 5 CTAs/SM: the extra latency hiding beats the register spills it costs
 // (measured 5.7 -> 5.0 ms/step on the c4 batch).
-template <typename T>
+// T: scene parameter type; OT: gradient element type (sdgr_grads.dtype).
+template <typename T, typename OT>
 __global__ void __launch_bounds__(128, 5) k_grad_geometry(sdgr_scene sc, const __grid_constant__ GeoBatch B,
                                                        sdgr_grads out, int accumulate) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = sc.n;
   if (g >= n) return;
-  auto put = [&](float* base, int64_t i, double v) {
-    base[i] = accumulate ? base[i] + (float)v : (float)v;
+  auto put = [&](void* base_, int64_t i, double v) {
+    OT* base = static_cast<OT*>(base_);
+    base[i] = accumulate ? base[i] + (OT)v : (OT)v;
+  };
+  auto put_visible = [&](int n_vis) {
+    if (out.visible_dtype) put(out.visible, g, (double)n_vis);
+    else {
+      int32_t* vis = static_cast<int32_t*>(out.visible);
+      vis[g] = accumulate ? vis[g] + n_vis : n_vis;
+    }
   };
   int n_vis = 0;
   for (int k = 0; k < B.n_views; ++k) n_vis += (B.v[k].flags[g] & SDGR_FLAG_VISIBLE) ? 1 : 0;
   if (n_vis == 0) {
     if (!accumulate) {
-      for (int k = 0; k < 3; ++k) out.positions[3 * g + k] = 0.f;
-      for (int k = 0; k < 4; ++k) out.rotations[4 * g + k] = 0.f;
-      for (int k = 0; k < 3; ++k) out.log_scales[3 * g + k] = 0.f;
-      for (int k = 0; k < 16; ++k) out.sh_coeffs[16 * g + k] = 0.f;
-      out.ke_raw[2 * g] = 0.f;
-      out.ke_raw[2 * g + 1] = 0.f;
-      out.uv_grad_norm[g] = 0.f;
-      out.visible[g] = 0;
+      for (int k = 0; k < 3; ++k) put(out.positions, 3 * g + k, 0.0);
+      for (int k = 0; k < 4; ++k) put(out.rotations, 4 * g + k, 0.0);
+      for (int k = 0; k < 3; ++k) put(out.log_scales, 3 * g + k, 0.0);
+      for (int k = 0; k < 16; ++k) put(out.sh_coeffs, 16 * g + k, 0.0);
+      put(out.ke_raw, 2 * g, 0.0);
+      put(out.ke_raw, 2 * g + 1, 0.0);
+      put(out.uv_grad_norm, g, 0.0);
+      put_visible(0);
     }
     return;
   }
@@ -308,7 +317,7 @@ __global__ void __launch_bounds__(128, 5) k_grad_geometry(sdgr_scene sc, const _
   put(out.ke_raw, 2 * g, dk * 0.5 * (1.0 + tanh(0.5 * k0)));
   put(out.ke_raw, 2 * g + 1, dk * 0.5 * (1.0 + tanh(0.5 * k1)));
   put(out.uv_grad_norm, g, uvn);
-  out.visible[g] = accumulate ? out.visible[g] + n_vis : n_vis;
+  put_visible(n_vis);
 }
 
 int launch_grad_image(const sdgr_view& v, const sdgr_projection& p, const double* intensity,
@@ -347,10 +356,14 @@ int launch_grad_geometry(const sdgr_scene& sc, int n_views, const sdgr_view* vie
   const unsigned blocks = (unsigned)((sc.n + 127) / 128);
   {
     KernelTimer kt(SDGR_K_GEOMETRY, st);
-    if (sc.dtype == 0)
-      k_grad_geometry<float><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
+    if (sc.dtype == 0 && out.dtype == 0)
+      k_grad_geometry<float, float><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
+    else if (sc.dtype == 0)
+      k_grad_geometry<float, double><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
+    else if (out.dtype == 0)
+      k_grad_geometry<double, float><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
     else
-      k_grad_geometry<double><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
+      k_grad_geometry<double, double><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
   }
   note_launch();
   return check_launch();

@@ -72,7 +72,7 @@ size_t loss_scratch_bytes(int, int);
 int launch_loss(const double*, const double*, int, int, double, double, const double*, double*, double*, void*,
                 cudaStream_t);
 int launch_adam(const sdgr_scene&, const sdgr_grads&, const sdgr_scene&, const sdgr_scene&, const double*, double,
-                double, double, double, double, double, unsigned long long*, cudaStream_t);
+                double, double, double, double, double, unsigned long long*, const int32_t*, cudaStream_t);
 
 int launch_accum_update(const sdgr_grads&, int64_t, double*, double*, double*, cudaStream_t);
 int launch_densify_flags(const sdgr_scene&, const double*, const double*, double, double, double, uint8_t*,
@@ -311,21 +311,22 @@ static bool scene_ok(const sdgr_scene* s) {
 
 int sdgr_adam_step(sdgr_scene* scene, const sdgr_grads* grads, sdgr_scene* m, sdgr_scene* v, const double* lr,
                    double beta1, double beta2, double eps, double bc1, double bc2, double displacement_bound,
-                   unsigned long long* n_skipped, void* stream) {
+                   unsigned long long* n_skipped, const int32_t* guard, void* stream) {
   if (!scene_ok(scene) || !scene_ok(m) || !scene_ok(v) || !grads || !lr || !n_skipped) return SDGR_ERR_INVALID;
+  if (grads->dtype != 0) return SDGR_ERR_INVALID;
   if (m->n != scene->n || v->n != scene->n || m->dtype != scene->dtype || v->dtype != scene->dtype)
     return SDGR_ERR_STATE;
   if (!grads->positions || !grads->rotations || !grads->log_scales || !grads->sh_coeffs || !grads->ke_raw)
     return SDGR_ERR_INVALID;
   if (!(bc1 > 0.0) || !(bc2 > 0.0)) return SDGR_ERR_INVALID;
   return launch_adam(*scene, *grads, *m, *v, lr, beta1, beta2, eps, bc1, bc2, displacement_bound, n_skipped,
-                     static_cast<cudaStream_t>(stream));
+                     guard, static_cast<cudaStream_t>(stream));
 }
 
 int sdgr_accum_update(const sdgr_grads* grads, int64_t n, double* norm_sum, double* pos_sum, double* count,
                       void* stream) {
   if (!grads || n < 0 || !norm_sum || !pos_sum || !count || !grads->positions || !grads->uv_grad_norm ||
-      !grads->visible)
+      !grads->visible || grads->dtype != 0)
     return SDGR_ERR_INVALID;
   if (n == 0) return SDGR_OK;
   return launch_accum_update(*grads, n, norm_sum, pos_sum, count, static_cast<cudaStream_t>(stream));

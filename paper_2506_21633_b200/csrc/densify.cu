@@ -25,10 +25,12 @@ __global__ void __launch_bounds__(256) k_accum_update(sdgr_grads gr, int64_t n, 
                                                       double* __restrict__ pos_sum, double* __restrict__ count) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n) return;
-  const int vis = gr.visible[g];  // views in which g was visible (1 per single-view backward)
+  // views in which g was visible (1 per single-view backward)
+  const int vis = gr.visible_dtype ? (int)static_cast<const float*>(gr.visible)[g]
+                                   : static_cast<const int32_t*>(gr.visible)[g];
   if (vis <= 0) return;
-  norm_sum[g] += (double)gr.uv_grad_norm[g];
-  for (int k = 0; k < 3; ++k) pos_sum[3 * g + k] += (double)gr.positions[3 * g + k];
+  norm_sum[g] += (double)static_cast<const float*>(gr.uv_grad_norm)[g];
+  for (int k = 0; k < 3; ++k) pos_sum[3 * g + k] += (double)static_cast<const float*>(gr.positions)[3 * g + k];
   count[g] += (double)vis;
 }
 

@@ -270,9 +270,9 @@ struct AdamArgs {
 };
 
 template <typename T>
-__device__ __forceinline__ double adam_one(T* param, T* m, T* v, const float* grad, int64_t i, const AdamArgs& A,
+__device__ __forceinline__ double adam_one(T* param, T* m, T* v, const void* grad_, int64_t i, const AdamArgs& A,
                                            double lr, unsigned long long& bad) {
-  double g = (double)grad[i];
+  double g = (double)static_cast<const float*>(grad_)[i];
   if (!isfinite(g)) {
     ++bad;
     g = 0.0;
@@ -288,9 +288,11 @@ __device__ __forceinline__ double adam_one(T* param, T* m, T* v, const float* gr
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_adam(sdgr_scene sc, sdgr_grads gr, sdgr_scene m, sdgr_scene v,
-                                              AdamArgs A, unsigned long long* n_skipped) {
+                                              AdamArgs A, unsigned long long* n_skipped,
+                                              const int32_t* guard) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long bad = 0;
+  if (guard && *guard) return;  // overflowed step: its gradients are truncated
   if (g < sc.n) {
     // positions: per-row displacement clamp (optimize.py:196-199)
     {
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(256) k_adam(sdgr_scene sc, sdgr_grads gr, sdgr
           dsqrt(dadd(dadd(dadd(dmul(q[0], q[0]), dmul(q[1], q[1])), dmul(q[2], q[2])), dmul(q[3], q[3])));
       for (int k = 0; k < 4; ++k) R[4 * g + k] = (T)ddiv(q[k], nrm);
     }
-    auto group = [&](const void* p, const void* mp, const void* vp, const float* gp, int width, double lr) {
+    auto group = [&](const void* p, const void* mp, const void* vp, const void* gp, int width, double lr) {
       T* P = (T*)(p);
       for (int k = 0; k < width; ++k) {
         const int64_t i = (int64_t)width * g + k;
@@ -339,15 +341,15 @@ __global__ void __launch_bounds__(256) k_adam(sdgr_scene sc, sdgr_grads gr, sdgr
 
 int launch_adam(const sdgr_scene& sc, const sdgr_grads& gr, const sdgr_scene& m, const sdgr_scene& v,
                 const double* lr, double b1, double b2, double eps, double bc1, double bc2, double bound,
-                unsigned long long* n_skipped, cudaStream_t st) {
+                unsigned long long* n_skipped, const int32_t* guard, cudaStream_t st) {
   AdamArgs A;
   for (int k = 0; k < 5; ++k) A.lr[k] = lr[k];
   A.b1 = b1; A.b2 = b2; A.eps = eps; A.bc1 = bc1; A.bc2 = bc2; A.bound = bound;
   const unsigned blocks = (unsigned)((sc.n + 255) / 256);
   if (sc.dtype == 0)
-    k_adam<float><<<blocks, 256, 0, st>>>(sc, gr, m, v, A, n_skipped);
+    k_adam<float><<<blocks, 256, 0, st>>>(sc, gr, m, v, A, n_skipped, guard);
   else
-    k_adam<double><<<blocks, 256, 0, st>>>(sc, gr, m, v, A, n_skipped);
+    k_adam<double><<<blocks, 256, 0, st>>>(sc, gr, m, v, A, n_skipped, guard);
   note_launch();
   return check_launch();
 }

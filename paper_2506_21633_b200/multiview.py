@@ -11,8 +11,11 @@ summing uv_grad_norm and visible counts too.
 Per view the whole chain -- K1 preprocess, K2-K5 binning, K6/K7 forward,
 K8-K10 backward -- is launched with no host round trip: pair buffers use
 capacities cached from a calibration pass and the exact counts stay on the
-device.  Capacity overflow is detected on the device and checked once per
-step; on overflow the step is recalibrated and re-run.
+device.  Capacity overflow is detected on the device and folded into one
+overflow word per step (`MultiViewStep.overflow`): check() raises
+OverflowError from it, and TrainStep recalibrates and re-runs the step (its
+Adam update is guarded by the same word on the device, so an overflowed step
+never moves the parameters).
 """
 from __future__ import annotations
 
@@ -25,14 +28,14 @@ import torch
 
 from . import _lib
 from ._lib import ptr
-from .errors import NumericalError
+from .errors import NumericalError, StateError
 from .radar import view_constants
 from .rasterizer import (DEFAULT_COV_REG, DEFAULT_CUTOFF, S_STOP, ReplayLog, SceneGradients, TILE, _check, _empty,
                          _scene_desc, _seg_len, _stream)
 from .scene import DeviceScene
 
 MULTIVIEW_SEG_LEN = 2048  # depth-segment floor for concurrent multi-view steps
-GRAD_WIDTH = 30  # 3 + 4 + 3 + 16 + 2 + uv_grad_norm + (visible as int32 view)
+GRAD_WIDTH = 30  # 3 + 4 + 3 + 16 + 2 + uv_grad_norm + visible count (float32, exact below 2^24)
 
 
 def shard_views(configs, rank: int, world: int):
@@ -45,20 +48,21 @@ GRAD_GROUPS = (3, 4, 3, 16, 2, 1)  # positions, rotations, log_scales, sh_coeffs
 
 def grad_views(flat: torch.Tensor, n: int) -> SceneGradients:
     """SceneGradients whose fields are SoA views into one (30 n,) float32
-    buffer; the last n words hold the int32 visible counts."""
+    buffer; the last n words hold the visible counts as float32 (integers
+    below 2^24 are exact, so summing them in float32 is exact)."""
     parts, o = [], 0
     for w in GRAD_GROUPS:
         parts.append(flat[o:o + w * n].view(n, w) if w > 1 else flat[o:o + n])
         o += w * n
-    return SceneGradients(*parts, flat[o:o + n].view(torch.int32))
+    return SceneGradients(*parts, flat[o:o + n])
 
 
 def allreduce_grads(flat: torch.Tensor, n: int, group=None) -> None:
-    """One-step gradient exchange: sum the float gradients and the int32
-    visible counts over all ranks (NCCL on GPU, gloo on CPU)."""
+    """One-step gradient exchange: ONE all-reduce (sum) of the flat float32
+    buffer -- every gradient group, uv_grad_norm and the visible counts --
+    over all ranks (NCCL on GPU, gloo on CPU): 120 B per Gaussian."""
     import torch.distributed as dist
-    dist.all_reduce(flat[: 29 * n], group=group)
-    dist.all_reduce(flat[29 * n: 30 * n].view(torch.int32), group=group)
+    dist.all_reduce(flat[: GRAD_WIDTH * n], group=group)
 
 
 @dataclass
@@ -89,6 +93,10 @@ class MultiViewStep:
         shapes = {(v.n_rg, v.n_az) for v in self.views}
         if len(shapes) != 1:
             raise ValueError("all views of a step must share the image size")
+        # the slot buffers (tile grid, ranges, work items, splat scratch) are
+        # sized from views[0]: every view must have the same ray grid
+        if len({(v.n_u, v.n_v) for v in self.views}) != 1:
+            raise ValueError("all views of a step must share the computation-plane ray grid")
         self.img_shape = shapes.pop()
         # geometry epilogue batches: `geo_batch` views' projections, partial
         # records and imaging-plane sums stay resident until one batched
@@ -125,6 +133,10 @@ class MultiViewStep:
         self.acc_imgs = [_empty((6, n), torch.float64, dev) for _ in range(self.n_slots)]
         self.acc_img = self.acc_imgs[0]
         self.status = torch.zeros((4,), dtype=torch.int32, device=dev)
+        # one device word per step: != 0 when any pair / replay buffer overflowed
+        # (the step's gradients are then truncated); guards the Adam update
+        self.overflow = torch.zeros((), dtype=torch.int32, device=dev)
+        self.generation = 0   # bumped by every (re)allocation: captured graphs are stale
         # gradients: one flat float32 buffer so the all-reduce is one call
         self.grads = self._grad_views()
         self.gd = self.grads.desc()
@@ -245,6 +257,9 @@ class MultiViewStep:
         self.intensity, self.image, self.splat_scratch = ln0.intensity, ln0.image, ln0.splat_scratch
         self.slot_partial = [_empty((cap, 8), torch.float64, dev) for _ in range(self.n_slots)]
         self.cap = dict(cap_pairs)
+        # graphs captured before point at the freed buffers
+        self.graph = None
+        self.generation += 1
 
     def calibrate(self):
         """Measure the pair counts of every view (host syncs) and size buffers."""
@@ -419,6 +434,9 @@ class MultiViewStep:
             if timing:
                 gevs.append(gev)
         main.wait_stream(pre)
+        # fold every overflow flag into one word (device ops: graph-capturable)
+        flags = [t["n_items"][1] for t in self.slot_t] + [ln.replay.cursor[1].to(torch.int32) for ln in self.lanes]
+        torch.amax(torch.stack(flags), dim=0, out=self.overflow)
         self.stage_events = (evs, pevs, gevs)
         if allreduce and (self.group is not None or
                           (torch.distributed.is_available() and torch.distributed.is_initialized())):
@@ -448,6 +466,8 @@ class MultiViewStep:
 
     def graph_step(self, check: bool = False):
         """One captured step (+ the all-reduce when distributed)."""
+        if self.graph is None:
+            raise StateError("no captured graph (calibrate() reallocates the buffers): call capture() again")
         self.graph.replay()
         if self.group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
             self.allreduce()
@@ -474,12 +494,8 @@ class MultiViewStep:
 
     def check(self):
         """One host read per step: capacity overflow and non-finite status."""
-        flags = torch.stack([self.status[0].to(torch.int64)] +
-                            [t["n_items"][1].to(torch.int64) for t in self.slot_t] +
-                            [ln.replay.cursor[1] for ln in self.lanes])
-        f = flags.cpu().tolist()
-        bad, ov0, ov_replay = f[0], any(f[1:1 + self.n_slots]), any(f[1 + self.n_slots:])
-        if ov0 or ov_replay:
+        bad, ov = torch.stack([self.status[0], self.overflow]).cpu().tolist()
+        if ov:
             raise OverflowError("pair capacity exceeded; recalibrate")
         if bad:
             raise NumericalError("non-finite intensity in a multi-view step")
@@ -553,12 +569,15 @@ class HostStepPipeline:
             bk["graph"] = g
             self.launches = int(step.lib.sdgr_launch_count() - n0)
         step.bind(base_scene, base_flat)
+        self.generation = step.generation
 
     def submit(self, host_scene: dict, host_dl: torch.Tensor, host_out: torch.Tensor):
         """Queue one step.  host_scene: {group: pinned tensor} for positions,
         rotations, log_scales, sh_coeffs, ke_raw; host_dl: pinned (V, H, W);
         host_out: pinned float32 (30 n,) receiving the gradients.  Returns an
         event that completes when host_out holds this step's result."""
+        if self.step.generation != self.generation:
+            raise StateError("the step was recalibrated after this pipeline captured it; build a new pipeline")
         bk = self.banks[self.k % 2]
         self.k += 1
         main = torch.cuda.current_stream()

@@ -259,6 +259,9 @@ class TileLists:
     plane 0 (computation): each tile's Gaussians in (depth, index) order --
     the per-ray order of forward.build_ray_lists (forward.py:138-155);
     plane 1 (imaging): index order (forward._build_splat_pairs :213-224).
+
+    Buffers hold `capacity` pairs.  With a cached capacity (device_count) the
+    exact pair count stays on the device (`count_dev`) until n_pairs is read.
     """
 
     plane: int
@@ -266,7 +269,7 @@ class TileLists:
     n_v: int
     tiles_x: int
     tiles_y: int
-    n_pairs: int
+    capacity: int
     pair_tile: torch.Tensor
     pair_pos: torch.Tensor
     pair_prim: torch.Tensor
@@ -279,8 +282,16 @@ class TileLists:
     tile_first: torch.Tensor
     n_items: torch.Tensor
     pair_rec: torch.Tensor | None = None
-    member_pairs: int | None = None   # member (cell, Gaussian) pairs of the plane (upper bound)
+    member_pairs: int | None = None   # member (cell, Gaussian) pairs of the plane (capacity bound)
+    count_dev: torch.Tensor | None = None   # device_count mode: offsets[n] on the device
+    _n_host: int | None = None
     _desc: object = field(default=None, repr=False)
+
+    @property
+    def n_pairs(self) -> int:
+        if self._n_host is None:
+            self._n_host = int(self.count_dev.item())
+        return self._n_host
 
     @property
     def n_tiles(self) -> int:
@@ -290,7 +301,8 @@ class TileLists:
         if self._desc is None:
             d = _lib.TilesDesc()
             d.plane, d.tiles_x, d.tiles_y, d.n_tiles = self.plane, self.tiles_x, self.tiles_y, self.n_tiles
-            d.n_pairs = self.n_pairs
+            d.n_pairs = self.capacity
+            d.device_count = 0 if self.count_dev is None else 1
             d.pair_tile, d.pair_pos, d.pair_prim = ptr(self.pair_tile), ptr(self.pair_pos), ptr(self.pair_prim)
             d.pre_prim, d.pair_start, d.tile_range = ptr(self.pre_prim), ptr(self.pair_start), ptr(self.tile_range)
             d.seg_len, d.max_items = self.seg_len, self.max_items
@@ -316,24 +328,64 @@ def _seg_len(n_pairs: int) -> int:
     return int(min(max(seg, 256), 8192))
 
 
+# Pair capacities per (N, ray grid, image, cutoff, plane) from the last exact
+# binning: later calls of the same shape allocate from them and keep the pair
+# counts on the device (no host round trip inside render_forward).  A call
+# whose counts outgrow them is detected on the device and re-binned exactly.
+_CAPS: dict = {}
+CAP_HEADROOM = 1.25
+
+
 class _Binner:
-    """Runs K2-K5 for both planes with one host read of the pair totals."""
+    """Runs K2-K5 for the requested planes."""
 
     def __init__(self, proj: Projection):
         self.proj = proj
         self.lib = _lib.lib()
         self.dev = proj.flags.device
 
-    def run(self, planes=(0, 1)):
+    def _key(self, pl):
+        v = self.proj.view
+        return (self.proj.n_scene, v.n_u, v.n_v, v.n_az, v.n_rg, float(v.cutoff), pl)
+
+    def _lists(self, pl, cap, count_dev=None):
+        p, dev, n = self.proj, self.dev, self.proj.n_scene
+        v = p.view
+        nu, nv = (v.n_u, v.n_v) if pl == 0 else (v.n_az, v.n_rg)
+        tx, ty = -(-nu // TILE), -(-nv // TILE)
+        seg = _seg_len(cap)
+        max_items = -(-cap // seg) + tx * ty
+        c = max(int(cap), 1)
+        return TileLists(
+            plane=pl, n_u=nu, n_v=nv, tiles_x=tx, tiles_y=ty, capacity=int(cap),
+            pair_tile=_empty((c,), torch.int32, dev), pair_pos=_empty((c,), torch.int32, dev),
+            pair_prim=_empty((c,), torch.int32, dev), pre_prim=_empty((c,), torch.int32, dev),
+            pair_start=_empty((n,), torch.int32, dev), tile_range=_empty((tx * ty, 2), torch.int32, dev),
+            seg_len=seg, max_items=max_items, items=_empty((max_items, 4), torch.int32, dev),
+            tile_first=_empty((tx * ty,), torch.int32, dev),
+            n_items=torch.zeros((4,), dtype=torch.int32, device=dev),
+            pair_rec=(_empty((c, _lib.PAIR_REC_BYTES), torch.uint8, dev) if pl == 0 else None),
+            count_dev=count_dev, _n_host=None if count_dev is not None else int(cap))
+
+    def run(self, planes=(0, 1), exact: bool = False):
+        if not exact and all(self._key(pl) in _CAPS for pl in planes):
+            return self._run_cached(planes)
+        return self._run_exact(planes)
+
+    def _depth_order(self, ws, ws_bytes, st):
+        order = _empty((self.proj.n_scene,), torch.int32, self.dev)
+        _check(self.lib.sdgr_depth_order(C.byref(self.proj._desc), ptr(order), ptr(ws), ws_bytes, st),
+               "sdgr_depth_order")
+        return order
+
+    def _run_exact(self, planes):
+        """Counts first, one host read of the totals, then exactly sized lists."""
         p, lib, st, dev = self.proj, self.lib, _stream(), self.dev
         n = p.n_scene
         ws_bytes = lib.sdgr_workspace_bytes(n, 1)
         ws = _empty((ws_bytes,), torch.uint8, dev)
-        order = None
+        order = self._depth_order(ws, ws_bytes, st) if 0 in planes else None
         offsets = {}
-        if 0 in planes:
-            order = _empty((n,), torch.int32, dev)
-            _check(lib.sdgr_depth_order(C.byref(p._desc), ptr(order), ptr(ws), ws_bytes, st), "sdgr_depth_order")
         for pl in planes:
             off = _empty((n + 1,), torch.int32, dev)
             _check(lib.sdgr_count_pairs(C.byref(p._desc), pl, ptr(order) if pl == 0 else None, ptr(off),
@@ -341,35 +393,40 @@ class _Binner:
             offsets[pl] = off
         host = torch.cat([torch.stack([offsets[pl][n] for pl in planes]).to(torch.int64), p.member_pairs]).cpu()
         totals = host[: len(planes)].tolist()
-        self.member_pairs = host[len(planes):].tolist()
-        max_pairs = max(max(totals), 1)
-        ws_bytes = lib.sdgr_workspace_bytes(n, max_pairs)
+        member = host[len(planes):].tolist()
+        ws_bytes = lib.sdgr_workspace_bytes(n, max(max(totals), 1))
         ws = _empty((ws_bytes,), torch.uint8, dev)
         out = {}
         for pl, total in zip(planes, totals):
-            v = p.view
-            nu, nv = (v.n_u, v.n_v) if pl == 0 else (v.n_az, v.n_rg)
-            tx, ty = -(-nu // TILE), -(-nv // TILE)
-            seg = _seg_len(total)
-            max_items = -(-total // seg) + tx * ty
-            tl = TileLists(
-                plane=pl, n_u=nu, n_v=nv, tiles_x=tx, tiles_y=ty, n_pairs=int(total),
-                pair_tile=_empty((max(total, 1),), torch.int32, dev),
-                pair_pos=_empty((max(total, 1),), torch.int32, dev),
-                pair_prim=_empty((max(total, 1),), torch.int32, dev),
-                pre_prim=_empty((max(total, 1),), torch.int32, dev),
-                pair_start=_empty((n,), torch.int32, dev),
-                tile_range=_empty((tx * ty, 2), torch.int32, dev),
-                seg_len=seg, max_items=max_items,
-                items=_empty((max_items, 4), torch.int32, dev),
-                tile_first=_empty((tx * ty,), torch.int32, dev),
-                n_items=torch.zeros((4,), dtype=torch.int32, device=dev),
-                pair_rec=(_empty((max(total, 1), _lib.PAIR_REC_BYTES), torch.uint8, dev) if pl == 0 else None),
-            )
+            tl = self._lists(pl, int(total))
             _check(lib.sdgr_bin_pairs(C.byref(p._desc), C.byref(p.view), ptr(order) if pl == 0 else None,
                                       ptr(offsets[pl]), C.byref(tl.desc()), ptr(ws), ws_bytes, st),
                    "sdgr_bin_pairs")
-            tl.member_pairs = int(self.member_pairs[pl])
+            tl.member_pairs = int(member[pl])
+            _CAPS[self._key(pl)] = (int(total * CAP_HEADROOM) + 1024, int(member[pl] * CAP_HEADROOM) + 1024)
+            out[pl] = tl
+        self.order = order
+        return out
+
+    def _run_cached(self, planes):
+        """Cached capacities: depth order + fused count/emit/sort per plane
+        (sdgr_bin_batch of one view), counts left on the device."""
+        p, lib, st, dev = self.proj, self.lib, _stream(), self.dev
+        n = p.n_scene
+        caps = {pl: _CAPS[self._key(pl)] for pl in planes}
+        ws_bytes = lib.sdgr_batch_workspace_bytes(n, max(c for c, _ in caps.values()), 1)
+        ws = _empty((ws_bytes,), torch.uint8, dev)
+        order = self._depth_order(ws, ws_bytes, st) if 0 in planes else None
+        out = {}
+        for pl in planes:
+            off = _empty((n + 1,), torch.int32, dev)
+            tl = self._lists(pl, caps[pl][0], count_dev=off[n])
+            tl.member_pairs = caps[pl][1]
+            tls = (_lib.TilesDesc * 1)(tl.desc())
+            orders = (C.c_void_p * 1)(ptr(order) if pl == 0 else None)
+            offs = (C.c_void_p * 1)(ptr(off))
+            _check(lib.sdgr_bin_batch(1, C.byref(p._desc), C.byref(p.view), pl, orders if pl == 0 else None,
+                                      offs, tls, ptr(ws), ws_bytes, st), "sdgr_bin_batch")
             out[pl] = tl
         self.order = order
         return out
@@ -398,13 +455,18 @@ class IntensityBuffer:
     partial: torch.Tensor
     status: torch.Tensor
     s_stop: float
-    indices: torch.Tensor | None = None
+    projection: "Projection | None" = None   # set when the reference's compacted views are wanted
     replay: "ReplayLog | None" = None
+    replay_ok: bool | None = None            # host copy of "the log did not overflow" (one status read)
+
+    @property
+    def indices(self):
+        return None if self.projection is None else self.projection.indices
 
     @property
     def intensity(self) -> torch.Tensor:
         """(K,) compacted like the reference's IntensityBuffer.intensity."""
-        return self.intensity_n if self.indices is None else self.intensity_n[self.indices]
+        return self.intensity_n if self.projection is None else self.intensity_n[self.projection.indices]
 
 
 class ReplayLog:
@@ -437,7 +499,9 @@ class ReplayLog:
 
 def compute_intensities(rays: TileLists, projection: Projection, s_stop: float = S_STOP,
                         check: bool = True, replay: bool = True) -> IntensityBuffer:
-    """forward.compute_intensities (forward.py:178-199) on the device."""
+    """forward.compute_intensities (forward.py:178-199) on the device.
+    check=True reads the status once and raises NumericalError like the
+    reference (forward.py:192-196)."""
     dev = projection.flags.device
     n = projection.n_scene
     cap = max(rays.max_items, 1) * 256
@@ -445,26 +509,48 @@ def compute_intensities(rays: TileLists, projection: Projection, s_stop: float =
         intensity_n=_empty((n,), torch.float64, dev),
         seg_sum=_empty((cap,), torch.float64, dev),
         seg_base=_empty((cap,), torch.float64, dev),
-        partial=_empty((max(rays.n_pairs, 1),), torch.float64, dev),
+        partial=_empty((max(rays.capacity, 1),), torch.float64, dev),
         status=torch.zeros((4,), dtype=torch.int32, device=dev),
         s_stop=float(s_stop),
     )
     if replay and rays.member_pairs is not None:
-        buf.replay = ReplayLog(rays.member_pairs, rays.max_items, rays.seg_len, dev, rays.n_pairs)
+        buf.replay = ReplayLog(rays.member_pairs, rays.max_items, rays.seg_len, dev, rays.capacity)
     _check(_lib.lib().sdgr_composite_forward(
         C.byref(projection.view), C.byref(projection._desc), C.byref(rays.desc()), float(s_stop),
         ptr(buf.seg_sum), ptr(buf.seg_base), ptr(buf.partial), ptr(buf.intensity_n), ptr(buf.status),
         C.byref(buf.replay.desc_c) if buf.replay else None, _stream()),
         "sdgr_composite_forward")
     if check:
-        _raise_if_nonfinite(buf, projection, rays)
+        ov, bad = _forward_status(buf, projection, [rays])
+        if ov:
+            raise OverflowError("pair capacity exceeded")
+        if bad:
+            raise NumericalError(f"non-finite intensity at primitive {_first_bad_primitive(projection)}")
     return buf
 
 
-def _raise_if_nonfinite(buf: IntensityBuffer, proj: Projection, rays: TileLists) -> None:
-    if int(buf.status[0].item()) == 0 and bool(torch.isfinite(buf.intensity_n).all().item()):
-        return
-    raise NumericalError(f"non-finite intensity at primitive {_first_bad_primitive(proj)}")
+def _forward_status(buf: IntensityBuffer, proj: Projection, lists) -> tuple[bool, bool]:
+    """ONE host read per forward: (binning overflow, non-finite intensity);
+    also records whether the replay log overflowed.  A Gaussian with a
+    non-finite phase or extinction poisons every member pair it has in the
+    reference, even behind an opaque ray (forward.py:188-196), so besides
+    the walk's own flag a visible Gaussian with non-finite P or kappa counts
+    when it has a member cell (checked on the error path only)."""
+    words = [buf.status[0].to(torch.int64), (~torch.isfinite(buf.intensity_n)).any().to(torch.int64)]
+    if proj.phase_f is not None and proj.kappa is not None:
+        words.append((proj.visible & ~(torch.isfinite(proj.phase_f) & torch.isfinite(proj.kappa))).any()
+                     .to(torch.int64))
+    else:
+        words.append(torch.zeros((), dtype=torch.int64, device=buf.status.device))
+    words += [tl.n_items[1].to(torch.int64) for tl in lists]
+    if buf.replay is not None:
+        words.append(buf.replay.cursor[1])
+    f = torch.stack(words).cpu().tolist()
+    if buf.replay is not None:
+        buf.replay_ok = not f.pop()
+    ov = any(f[3:])
+    bad = bool(f[0] or f[1]) or (bool(f[2]) and _first_bad_primitive(proj) >= 0)
+    return ov, bad
 
 
 def _first_bad_primitive(proj: Projection) -> int:
@@ -518,39 +604,59 @@ def splat_image(intensities: IntensityBuffer, projection: Projection, config=Non
     return image
 
 
-@dataclass
 class ForwardResult:
-    """A rendered image plus every buffer the backward pass needs (forward.py:243-253)."""
+    """A rendered image plus every buffer the backward pass needs (forward.py:243-253).
 
-    scene: object
-    device_scene: DeviceScene
-    config: object
-    projection: Projection
-    rays: TileLists
-    intensities: IntensityBuffer
-    splat: TileLists
-    image_t: torch.Tensor
-    host: bool = False
+    The imaging-plane tile lists (`splat`) are built on first access: the
+    splat and its backward are Gaussian-parallel and never read them."""
+
+    def __init__(self, scene, device_scene, config, projection, rays, intensities, image_t, host=False,
+                 splat=None):
+        self.scene, self.device_scene, self.config = scene, device_scene, config
+        self.projection, self.rays, self.intensities = projection, rays, intensities
+        self.image_t, self.host = image_t, host
+        self._splat = splat
+        self._image_host = None
+
+    @property
+    def splat(self) -> TileLists:
+        if self._splat is None:
+            self._splat = _Binner(self.projection).run((1,), exact=True)[1]
+        return self._splat
 
     @property
     def image(self):
-        return self.image_t.cpu().numpy() if self.host else self.image_t
+        if not self.host:
+            return self.image_t
+        if self._image_host is None:
+            self._image_host = self.image_t.cpu().numpy()
+        return self._image_host
 
 
 def render_forward(scene, config, cov_reg: float = DEFAULT_COV_REG, cutoff: float = DEFAULT_CUTOFF,
                    s_stop: float = S_STOP, accessors: bool = True) -> ForwardResult:
-    """Render and retain the buffers for backward (forward.py:256-273)."""
+    """Render and retain the buffers for backward (forward.py:256-273).
+
+    One host round trip per call (the status word: non-finite intensity,
+    capacity overflow); pair buffers are sized from the capacities of the
+    last call of the same shape.  Host scenes get the image as numpy FP64."""
     if len(scene) == 0:
         raise NumericalError("cannot retain buffers for an empty scene")
     ds, host = as_device_scene(scene)
     proj = _project(ds, config, cov_reg, cutoff, accessors)
-    binner = _Binner(proj)
-    lists = binner.run((0, 1))
-    buf = compute_intensities(lists[0], proj, s_stop=s_stop)
-    image = splat_image(buf, proj, config, pairs=lists[1])
-    buf.indices = proj.indices if accessors else None
-    return ForwardResult(scene=scene, device_scene=ds, config=config, projection=proj, rays=lists[0],
-                         intensities=buf, splat=lists[1], image_t=image, host=host)
+    for exact in (False, True):
+        rays = _Binner(proj).run((0,), exact=exact)[0]
+        buf = compute_intensities(rays, proj, s_stop=s_stop, check=False)
+        image = splat_image(buf, proj, config)
+        ov, bad = _forward_status(buf, proj, [rays])
+        if not ov:
+            break
+        _CAPS.pop(_Binner(proj)._key(0), None)   # grown footprints: re-bin with exact counts
+    if bad:
+        raise NumericalError(f"non-finite intensity at primitive {_first_bad_primitive(proj)}")
+    buf.projection = proj if accessors else None
+    return ForwardResult(scene=scene, device_scene=ds, config=config, projection=proj, rays=rays,
+                         intensities=buf, image_t=image, host=host)
 
 
 def render(scene, config, cov_reg: float = DEFAULT_COV_REG, cutoff: float = DEFAULT_CUTOFF,
@@ -583,13 +689,21 @@ class SceneGradients:
         return (self.positions, self.rotations, self.log_scales, self.sh_coeffs, self.ke_raw)
 
     @classmethod
-    def zeros_device(cls, n: int, device) -> "SceneGradients":
-        z = lambda *s: torch.zeros(s, dtype=torch.float32, device=device)  # noqa: E731
+    def zeros_device(cls, n: int, device, dtype=torch.float32) -> "SceneGradients":
+        z = lambda *s: torch.zeros(s, dtype=dtype, device=device)  # noqa: E731
         return cls(z(n, 3), z(n, 4), z(n, 3), z(n, 16), z(n, 2), z(n),
                    torch.zeros((n,), dtype=torch.int32, device=device))
 
     def desc(self) -> _lib.GradsDesc:
+        arrays = self.param_arrays() + (self.uv_grad_norm,)
+        dt = arrays[0].dtype
+        if dt not in (torch.float32, torch.float64) or any(a.dtype != dt or not a.is_contiguous() for a in arrays):
+            raise InvalidParameterError("gradient arrays must be contiguous and share float32 or float64")
+        if self.visible.dtype not in (torch.int32, dt):
+            raise InvalidParameterError("visible counts must be int32 or the gradient dtype")
         d = _lib.GradsDesc()
+        d.dtype = 0 if dt == torch.float32 else 1
+        d.visible_dtype = 0 if self.visible.dtype == torch.int32 else 1
         d.positions, d.rotations, d.log_scales = ptr(self.positions), ptr(self.rotations), ptr(self.log_scales)
         d.sh_coeffs, d.ke_raw = ptr(self.sh_coeffs), ptr(self.ke_raw)
         d.uv_grad_norm, d.visible = ptr(self.uv_grad_norm), ptr(self.visible)
@@ -617,11 +731,12 @@ def grad_intensity_stage(fwd: ForwardResult, dL_dI: torch.Tensor, use_replay: bo
     dL/du, dL/dv, 0] on the computation plane, indexed by pre-sort position."""
     p, rays, buf = fwd.projection, fwd.rays, fwd.intensities
     dev = p.flags.device
-    partial = _empty((max(rays.n_pairs, 1), 8), torch.float64, dev)
+    partial = _empty((max(rays.capacity, 1), 8), torch.float64, dev)
     cap = max(rays.max_items, 1) * 256
     seg_g = _empty((cap,), torch.float64, dev)
     seg_d = _empty((cap,), torch.float64, dev)
-    rp = buf.replay if (use_replay and buf.replay is not None and not buf.replay.overflowed()) else None
+    ok = buf.replay_ok if buf.replay_ok is not None else (buf.replay is not None and not buf.replay.overflowed())
+    rp = buf.replay if (use_replay and buf.replay is not None and ok) else None
     _check(_lib.lib().sdgr_grad_intensity(C.byref(p.view), C.byref(p._desc), C.byref(rays.desc()),
                                           buf.s_stop, ptr(buf.seg_base), ptr(dL_dI), ptr(seg_g), ptr(seg_d),
                                           ptr(partial), C.byref(rp.desc_c) if rp else None, _stream()),
@@ -631,10 +746,13 @@ def grad_intensity_stage(fwd: ForwardResult, dL_dI: torch.Tensor, use_replay: bo
 
 def grad_geometry_stage(fwd: ForwardResult, acc_img: torch.Tensor, partial_comp: torch.Tensor,
                         out: SceneGradients | None = None, accumulate: bool = False) -> SceneGradients:
-    """grad_geometry_stage + grad_sh_stage + final scatter (backward.py:171-290)."""
+    """grad_geometry_stage + grad_sh_stage + final scatter (backward.py:171-290).
+    Host (FP64) callers get FP64 gradients like the reference; device callers
+    float32 unless they pass `out`."""
     p = fwd.projection
     if out is None:
-        out = SceneGradients.zeros_device(p.n_scene, p.flags.device)
+        out = SceneGradients.zeros_device(p.n_scene, p.flags.device,
+                                          dtype=torch.float64 if fwd.host else torch.float32)
     sd = _scene_desc(fwd.device_scene)
     gd = out.desc()
     _check(_lib.lib().sdgr_grad_geometry(C.byref(sd), C.byref(p.view), C.byref(p._desc),
@@ -662,9 +780,13 @@ def backward(fwd: ForwardResult, dL_dS, out: SceneGradients | None = None, accum
         raise StateError(f"image gradient shape {shape} does not match forward {img_shape}")
     if fwd.projection.n_scene != len(fwd.scene):
         raise StateError("scene changed since the forward pass; buffers are stale")
+    if validate:
+        # host arrays are checked on the host (no device round trip)
+        ok = (bool(np.all(np.isfinite(dL_dS))) if not isinstance(dL_dS, torch.Tensor)
+              else bool(torch.isfinite(dL_dS).all().item()))
+        if not ok:
+            raise InvalidParameterError("dL_dS contains non-finite values")
     g = _as_device_grad(dL_dS, fwd)
-    if validate and not bool(torch.isfinite(g).all().item()):
-        raise InvalidParameterError("dL_dS contains non-finite values")
     acc_img = grad_image_stage(fwd, g)
     partial = grad_intensity_stage(fwd, acc_img[0], use_replay=use_replay)
     grads = grad_geometry_stage(fwd, acc_img, partial, out=out, accumulate=accumulate)

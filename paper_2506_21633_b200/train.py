@@ -100,11 +100,13 @@ class AdamState:
 
 
 def adam_step(scene: DeviceScene, grads: SceneGradients, state: AdamState, lrs: dict,
-              displacement_bound: float | None = None) -> None:
+              displacement_bound: float | None = None, guard: torch.Tensor | None = None) -> None:
     """optimize.adam_step (optimize.py:171-207), in place on the device scene.
 
     grads: device SceneGradients (float32, e.g. MultiViewStep.grads).  The
-    bias corrections use the host step count (as the reference does)."""
+    bias corrections use the host step count (as the reference does).
+    guard: optional device int32 scalar; the kernel skips the whole update
+    when it is non-zero (MultiViewStep.overflow)."""
     state.step += 1
     b1, b2 = state.beta1, state.beta2
     bc1 = 1.0 - b1 ** state.step
@@ -114,7 +116,8 @@ def adam_step(scene: DeviceScene, grads: SceneGradients, state: AdamState, lrs: 
     gd = grads.desc()
     bound = float(displacement_bound) if displacement_bound is not None else -1.0
     _check(_lib.lib().sdgr_adam_step(C.byref(sd), C.byref(gd), C.byref(md), C.byref(vd), lr, float(b1), float(b2),
-                                     float(state.eps), bc1, bc2, bound, ptr(state.skipped), _stream()),
+                                     float(state.eps), bc1, bc2, bound, ptr(state.skipped),
+                                     ptr(guard) if guard is not None else None, _stream()),
            "sdgr_adam_step")
 
 
@@ -133,20 +136,43 @@ class TrainStep:
         self.mv = MultiViewStep(scene, configs, targets=targets, lambda_ssim=lambda_ssim, max_val=max_val, **kw)
         self.dlds = torch.zeros(targets.shape, dtype=torch.float64, device=scene.device)
         self.state = AdamState.for_scene(scene)
-        self.graph = False
+        self.graph_generation = -1
 
     def __call__(self, lrs: dict, sh_active: int = 16, displacement_bound: float | None = None,
-                 use_graph: bool = True) -> torch.Tensor:
-        """Returns the per-view loss values (device tensor, before the update)."""
+                 use_graph: bool = True, check: bool = True) -> torch.Tensor:
+        """Returns the per-view loss values (device tensor, before the update).
+
+        The Adam kernel is guarded on the device by the step's overflow word,
+        so a step whose pair buffers overflowed (footprints grew past the
+        calibrated capacity) never moves the parameters.  With check=True
+        (one host read per step) such a step is recalibrated -- which also
+        drops the stale graph -- and re-run on the unchanged scene, so the
+        update applied is exactly the one a large enough buffer gives."""
+        for attempt in range(3):
+            self._step(lrs, sh_active, displacement_bound, use_graph)
+            if not check:
+                break
+            bad, ov = torch.stack([self.mv.status[0], self.mv.overflow]).cpu().tolist()
+            if not ov:
+                if bad:
+                    from .errors import NumericalError
+                    raise NumericalError("non-finite intensity in a training step")
+                break
+            self.state.step -= 1          # the guarded update did not happen
+            self.mv.calibrate()           # larger buffers; drops the captured graph
+        else:
+            raise OverflowError("pair capacity still exceeded after recalibration")
+        return self.mv.loss_values
+
+    def _step(self, lrs, sh_active, displacement_bound, use_graph):
         if use_graph:
-            if not self.graph:
+            if self.mv.graph is None or self.graph_generation != self.mv.generation:
                 self.mv.capture(self.dlds)
-                self.graph = True
+                self.graph_generation = self.mv.generation
             self.mv.graph_step()
         else:
             self.mv.run(self.dlds, check=False)
         g = self.mv.grads
         if sh_active < 16:
             g.sh_coeffs[:, sh_active:] = 0.0   # optimize.py:412-413
-        adam_step(self.scene, g, self.state, lrs, displacement_bound)
-        return self.mv.loss_values
+        adam_step(self.scene, g, self.state, lrs, displacement_bound, guard=self.mv.overflow)

@@ -41,7 +41,8 @@ def test_bindings_cover_header():
 
 
 def test_host_only_calls(lib):
-    assert lib.sdgr_version() == 1
+    from paper_2506_21633_b200 import _lib
+    assert lib.sdgr_version() == _lib.ABI_VERSION == 2
     assert lib.sdgr_status_string(1).decode() == "invalid parameter"
     assert lib.sdgr_workspace_bytes(1_000_000, 2_000_000) > 20 * 2**20
     assert isinstance(lib.sdgr_launch_count(), int)

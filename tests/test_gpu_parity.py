@@ -247,10 +247,30 @@ def test_bitwise_determinism():
         assert np.array_equal(getattr(outs[0][1], k), getattr(outs[1][1], k)), k
 
 
+def oracle_sum(scene, cfgs, dl, cutoff=3.0):
+    """Sum over views of the oracle's gradients (FP64) and visible counts:
+    the multi-view parity definition of SURVEY.md §8e."""
+    ref = {k: 0.0 for k in GROUPS + ("uv_grad_norm",)}
+    vis = 0
+    for i, c in enumerate(cfgs):
+        fo = O.render_forward(scene, c, cutoff=cutoff, exp="device")
+        go = O.backward(fo, dl[i].cpu().numpy())
+        for k in ref:
+            ref[k] = ref[k] + go[k]
+        vis = vis + go["visible"].astype(np.int64)
+    return ref, vis
+
+
+def check_step_vs_oracle(got, ref, vis):
+    for k in ref:
+        assert_close(getattr(got, k).double().cpu().numpy(), ref[k], what=k)   # north-star tolerance
+    assert np.array_equal(got.visible.cpu().numpy().astype(np.int64), vis)
+
+
 @pytest.mark.parametrize("geo_batch", [1, 2, 8])
 def test_multiview_step_equals_sum_of_views(geo_batch):
-    """Batched geometry epilogue (1, partial and full batches) == the sum of
-    single-view backward passes."""
+    """Batched geometry epilogue (1, partial and full batches) == the oracle's
+    sum of single-view backward passes."""
     from paper_2506_21633_b200.multiview import MultiViewStep
 
     tank = targets.to_float32_exact(targets.composite_target(targets.tank_preset(), [3000, 1500, 500], seed=6))
@@ -260,16 +280,7 @@ def test_multiview_step_equals_sum_of_views(geo_batch):
     step = MultiViewStep(ds, cfgs, geo_batch=geo_batch)
     dl = torch.randn((3, 96, 96), dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(3))
     got = step.run(dl)
-    ref = {k: 0.0 for k in GROUPS + ("uv_grad_norm",)}
-    vis = 0
-    for i, c in enumerate(cfgs):
-        g = sdgr.backward(sdgr.render_forward(ds, c), dl[i])
-        for k in ref:
-            ref[k] = ref[k] + getattr(g, k).double()
-        vis = vis + g.visible
-    for k in ref:
-        assert_close(getattr(got, k).double().cpu().numpy(), ref[k].cpu().numpy(), atol=1e-5, rtol=1e-5, what=k)
-    assert torch.equal(got.visible.cpu(), vis.cpu())
+    check_step_vs_oracle(got, *oracle_sum(tank, cfgs, dl))
 
 
 def test_multiview_graph_replay_equals_run():
@@ -349,6 +360,7 @@ def test_multiview_capacity_overflow_is_detected():
     got = step.run(dl)
     ref = MultiViewStep(ds, cfgs, geo_batch=2).run(dl)
     assert torch.equal(got.positions, ref.positions) and torch.equal(got.visible, ref.visible)
+    assert step.graph is None   # calibrate() dropped any graph captured on the old buffers
 
 
 def test_depth_ties_and_near_ties_vs_oracle():
@@ -456,13 +468,35 @@ def test_multiview_batch_with_a_view_that_sees_nothing():
     step = MultiViewStep(ds, cfgs)
     dl = torch.randn((3, 96, 96), dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
     got = step.run(dl)
-    ref = {k: 0.0 for k in GROUPS + ("uv_grad_norm",)}
-    vis = 0
-    for i, c in enumerate(cfgs):
-        g = sdgr.backward(sdgr.render_forward(ds, c), dl[i])
-        for k in ref:
-            ref[k] = ref[k] + getattr(g, k).double()
-        vis = vis + g.visible
-    for k in ref:
-        assert_close(getattr(got, k).double().cpu().numpy(), ref[k].cpu().numpy(), atol=1e-5, rtol=1e-5, what=k)
-    assert torch.equal(got.visible.cpu(), vis.cpu())
+    check_step_vs_oracle(got, *oracle_sum(tank, cfgs, dl))
+
+
+def test_multiview_rejects_mixed_ray_grids():
+    """Slot buffers are sized from the first view: a step whose views differ
+    in the computation-plane grid (ray_grid) is refused up front."""
+    from paper_2506_21633_b200.multiview import MultiViewStep
+
+    tank = targets.composite_target(targets.tank_preset(), [300, 150, 50], seed=2)
+    ds = sdgr.DeviceScene.from_host(tank, dtype=torch.float32)
+    cfgs = [sdgr.RadarConfig(azimuth_deg=0.0, elevation_deg=45.0, altitude_m=0.5, n_range=64, n_azimuth=64),
+            sdgr.RadarConfig(azimuth_deg=90.0, elevation_deg=45.0, altitude_m=0.5, n_range=64, n_azimuth=64,
+                             ray_grid=(96, 80))]
+    with pytest.raises(ValueError, match="ray grid"):
+        MultiViewStep(ds, cfgs)
+
+
+def test_host_callers_get_float64_gradients():
+    """render_forward(host scene) + backward return FP64 numpy gradients, like
+    the reference (backward.py:25-50); device callers get float32 tensors."""
+    scene = targets.random_scene(np.random.default_rng(8), 20)
+    cfg = sdgr.RadarConfig(azimuth_deg=20.0, elevation_deg=40.0, altitude_m=2.0, range_res_m=0.5,
+                           azimuth_res_m=0.5, n_range=24, n_azimuth=24)
+    g = sdgr.backward(sdgr.render_forward(scene, cfg), np.ones((24, 24)))
+    assert all(a.dtype == np.float64 for a in g.param_arrays()) and g.visible.dtype == bool
+    fo = O.render_forward(scene, cfg, exp="device")
+    go = O.backward(fo, np.ones((24, 24)))
+    for k in GROUPS:   # FP64 all the way: far inside the north-star tolerance
+        assert_close(getattr(g, k), go[k], atol=1e-12, rtol=1e-9, what=k)
+    ds = sdgr.DeviceScene.from_host(scene, dtype=torch.float32)
+    gd = sdgr.backward(sdgr.render_forward(ds, cfg), torch.ones((24, 24), device="cuda"))
+    assert gd.positions.dtype == torch.float32 and gd.positions.is_cuda

@@ -145,6 +145,39 @@ def test_trainstep_reduces_the_loss():
     assert ts.state.step == 16
 
 
+def test_trainstep_overflow_recalibrates_and_reruns():
+    """a step whose footprints outgrow the calibrated pair / replay
+    capacity must not apply truncated gradients.  The device guard skips Adam,
+    the step recalibrates (dropping the stale graph) and re-runs, and the
+    update equals that of a step calibrated on the grown scene from the start."""
+    from paper_2506_21633_b200 import train
+    from paper_2506_21633_b200.scene import DeviceScene
+
+    scene, cfgs, tg = _toy_problem()
+    lrs = {"positions": 2e-3, "rotations": 1e-3, "log_scales": 5e-3, "sh_coeffs": 2.5e-3, "ke_raw": 5e-2}
+    ts = train.TrainStep(scene, cfgs, tg, lambda_ssim=0.2, geo_batch=2, headroom=1.0)
+    ts.mv.calibrate()                        # capacities of the original footprints
+    ts.mv.capture(ts.dlds)                   # and a graph on those buffers
+    ts.graph_generation = gen = ts.mv.generation
+    scene.log_scales.add_(1.5)               # ~4.5x larger footprints than calibrated
+    twin = DeviceScene(*(a.clone() for a in scene.arrays()))
+    ts(lrs)                                  # overflows, recalibrates, re-runs
+    assert ts.mv.generation > gen and ts.state.step == 1
+    ref = train.TrainStep(twin, cfgs, tg, lambda_ssim=0.2, geo_batch=2)
+    ref(lrs)
+    for x, y in zip(scene.arrays(), twin.arrays()):
+        assert torch.equal(x, y)
+    with pytest.raises(OverflowError):       # without the check the guard still holds
+        small = DeviceScene(*(a.clone() for a in twin.arrays()))
+        t2 = train.TrainStep(small, cfgs, tg, lambda_ssim=0.2, geo_batch=2, headroom=1.0)
+        t2.mv.calibrate()
+        small.log_scales.add_(1.5)
+        before = [a.clone() for a in small.arrays()]
+        t2(lrs, check=False)
+        assert all(torch.equal(x, y) for x, y in zip(small.arrays(), before))   # Adam skipped on device
+        t2.mv.check()
+
+
 def test_device_densify_matches_reference():
     from paper_2506_21633_b200 import densify, train
     from paper_2506_21633_b200.radar import RadarConfig
