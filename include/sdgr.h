@@ -292,8 +292,10 @@ int sdgr_composite_forward(const sdgr_view* view, const sdgr_projection* proj,
                            double* intensity, int32_t* status, sdgr_replay* replay,
                            void* stream);
 /* splat_image (forward.py:227-240): image (n_rg, n_az) FP64 overwritten.
- * Gaussian-parallel with deterministic fixed-point (2^-32) accumulation, so it
- * needs no imaging-plane lists.  scratch: n_rg*n_az*8 bytes. */
+ * Gaussian-parallel with deterministic fixed-point accumulation (u64 sums of
+ * w I * 2^(47-e), 2^e > the view's largest intensity: absolute precision
+ * 2^-47 of the brightest Gaussian, bitwise reproducible), so it needs no
+ * imaging-plane lists.  scratch: (n_rg*n_az + 1) * 8 bytes. */
 int sdgr_splat(const sdgr_view* view, const sdgr_projection* proj,
                const double* intensity, void* scratch, double* image, void* stream);
 
@@ -332,6 +334,53 @@ int sdgr_grad_geometry_batch(const sdgr_scene* scene, int n_views, const sdgr_vi
                              const sdgr_projection* projs, const sdgr_tiles* comps,
                              const double* const* acc_imgs, const double* const* partial_gs,
                              sdgr_grads* out, int accumulate, void* stream);
+
+/* ------------------------ reference-shaped stage outputs (accessors) ---- */
+/* The fused path above keeps per-Gaussian and per-(tile, Gaussian) state.
+ * These calls expose what the reference's stage functions return, for
+ * callers and tests that use the stage API (tests/test_forward.py,
+ * tests/test_backward.py drive those functions directly). */
+/* forward._footprint_pairs + build_ray_lists / _build_splat_pairs
+ * (forward.py:60-155, 213-224): the member (cell, Gaussian) pairs of one
+ * plane in the reference's order -- cell-major, then (depth, index) on the
+ * computation plane, index on the imaging plane -- from the plane's tile
+ * lists.  Needs the projection's SoA records (uv, inv_cov, bbox, cell_mask).
+ * Call 1 (prim == NULL): offsets (n_cells + 1, int64) <- CSR of the member
+ * counts per cell (n_cells = n_u*n_v or n_az*n_rg, cell = iv*width + iu).
+ * Call 2: prim (scene index), delta (dx, dy), q and w = exp(-q) of the
+ * offsets[n_cells] pairs. */
+int sdgr_cell_pairs(const sdgr_projection* proj, const sdgr_view* view, const sdgr_tiles* tiles,
+                    int64_t* offsets, int32_t* prim, double* delta, double* q, double* w, void* stream);
+/* compute_intensities' per-pair buffers (forward.py:167-199) over the
+ * computation-plane pairs of sdgr_cell_pairs: tau, trans, absorb, contrib
+ * (each ray's exclusive log-transmittance prefix in list order).  Needs
+ * proj->kappa and proj->phase. */
+int sdgr_cell_intensities(const sdgr_projection* proj, int64_t n_cells, const int64_t* offsets,
+                          const int32_t* prim, const double* w, double* tau, double* trans,
+                          double* absorb, double* contrib, void* stream);
+/* grad_image_stage's per-pair dL/dbeta = dL/dS[pixel] * I[prim] (backward.py:99). */
+int sdgr_splat_pair_grads(int64_t n_pairs, const int32_t* pair_pixel, const int32_t* pair_prim,
+                          const double* dL_dS, const double* intensity, double* dL_dbeta, void* stream);
+/* Per-Gaussian plane-space gradients, (8, n) FP64 rows:
+ * plane 0 from sdgr_grad_intensity's partial_g: dL/dP, dL/dkappa,
+ *   dL/dSigma_c (2x2 row-major), dL/du, dL/dv (grad_intensity_stage, backward.py:107-148);
+ * plane 1 from sdgr_grad_image's acc_img: dL/dI, 0, dL/dSigma_i, dL/du, dL/dv
+ *   (grad_image_stage, backward.py:86-104).  comp: the plane-0 tiles (NULL for plane 1). */
+int sdgr_stage_grads(const sdgr_projection* proj, int32_t plane, const sdgr_tiles* comp,
+                     const double* src, double* out, void* stream);
+/* grad_geometry_stage + grad_sh_stage + the scatter (backward.py:171-290)
+ * from caller-given plane-space gradients ex (14, n) FP64 rows:
+ * dSigma_c (4), dSigma_i (4), duv_c (2), duv_i (2), dP, dkappa.  out overwritten. */
+int sdgr_grad_geometry_explicit(const sdgr_scene* scene, const sdgr_view* view, const sdgr_projection* proj,
+                                const double* ex, sdgr_grads* out, void* stream);
+/* A projection given in plane space (the reference tests' hand-assembled
+ * Projection, tests/test_forward.py:43-59): n rows, all visible; per plane
+ * uv (n,2) and covariance (n,3: c00, c01, c11), depth (n), phase_raw (n,
+ * P before the clamp), kappa (n) -> the records sdgr_project would write for
+ * the same plane-space values (footprints, depth keys, packed rows). */
+int sdgr_project_planes(const sdgr_view* view, int64_t n, const double* uv_comp, const double* uv_img,
+                        const double* depth, const double* cov_comp, const double* cov_img,
+                        const double* phase_raw, const double* kappa, sdgr_projection* proj, void* stream);
 
 /* ----------------------------------- training step -- */
 /* optimize.loss (optimize.py:85-102): value = (1-l) mean|S-Y| + l (1 - SSIM(S,Y))

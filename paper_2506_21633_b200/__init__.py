@@ -21,7 +21,8 @@ __version__ = "0.1.0"
 _LAZY = {
     "render", "render_forward", "backward", "project_all", "build_ray_lists", "build_splat_lists",
     "compute_intensities", "splat_image", "grad_image_stage", "grad_intensity_stage",
-    "grad_geometry_stage", "ForwardResult", "SceneGradients", "Projection", "TileLists",
+    "grad_geometry_stage", "grad_sh_stage", "forward_from_projection", "ForwardResult", "SceneGradients",
+    "Projection", "TileLists", "image_stage_sums", "intensity_stage_partials", "geometry_stage_fused",
     "IntensityBuffer", "launch_count", "S_STOP", "DEFAULT_COV_REG", "DEFAULT_CUTOFF",
 }
 

@@ -138,6 +138,15 @@ SIGNATURES = [
     ("sdgr_prune_flags", C.c_int, [C.POINTER(SceneDesc), C.c_double, C.c_double, _p, _p]),
     ("sdgr_loss_scratch_bytes", C.c_size_t, [C.c_int, C.c_int]),
     ("sdgr_loss", C.c_int, [_p, _p, C.c_int, C.c_int, C.c_double, C.c_double, _p, _p, _p, _p, _p]),
+    ("sdgr_cell_pairs", C.c_int, [C.POINTER(ProjectionDesc), C.POINTER(View), C.POINTER(TilesDesc), _p, _p, _p,
+                                  _p, _p, _p]),
+    ("sdgr_cell_intensities", C.c_int, [C.POINTER(ProjectionDesc), C.c_int64, _p, _p, _p, _p, _p, _p, _p, _p]),
+    ("sdgr_splat_pair_grads", C.c_int, [C.c_int64, _p, _p, _p, _p, _p, _p]),
+    ("sdgr_stage_grads", C.c_int, [C.POINTER(ProjectionDesc), C.c_int32, C.POINTER(TilesDesc), _p, _p, _p]),
+    ("sdgr_grad_geometry_explicit", C.c_int, [C.POINTER(SceneDesc), C.POINTER(View), C.POINTER(ProjectionDesc),
+                                              _p, C.POINTER(GradsDesc), _p]),
+    ("sdgr_project_planes", C.c_int, [C.POINTER(View), C.c_int64, _p, _p, _p, _p, _p, _p, _p,
+                                      C.POINTER(ProjectionDesc), _p]),
     ("sdgr_adam_step", C.c_int, [C.POINTER(SceneDesc), C.POINTER(GradsDesc), C.POINTER(SceneDesc),
                                  C.POINTER(SceneDesc), C.POINTER(C.c_double), C.c_double, C.c_double,
                                  C.c_double, C.c_double, C.c_double, C.c_double, _p, _p, _p]),

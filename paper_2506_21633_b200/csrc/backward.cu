@@ -143,6 +143,8 @@ struct GeoView {
   const double* acc;      // (6, n) imaging-plane sums
   const double* partial;  // (n_pairs, 8) computation-plane partial records
   int64_t cap;            // n_pairs: records beyond it were never written (overflowed step)
+  const double* ex;       // explicit plane-space gradients (14, n) or NULL: dSigma_c (4), dSigma_i (4),
+                          // duv_c (2), duv_i (2), dP, dkappa (grad_geometry_stage's arguments)
 };
 struct GeoBatch {
   int n_views;
@@ -200,29 +202,39 @@ __global__ void __launch_bounds__(128, 5) k_grad_geometry(sdgr_scene sc, const _
   for (int vi = 0; vi < B.n_views; ++vi) {
     const GeoView& V = B.v[vi];
     if (!(V.flags[g] & SDGR_FLAG_VISIBLE)) continue;
-    // plane-space gradients
-    const double4 Ac = reinterpret_cast<const double4*>(V.inv_c)[g];
-    const double4 Ai = reinterpret_cast<const double4*>(V.inv_i)[g];
-    // computation-plane partials: one record per member tile, fixed order
-    double c7[7] = {0, 0, 0, 0, 0, 0, 0};
-    {
-      const int s0 = V.pair_start[g];
-      const int64_t room = V.cap - s0 > 0 ? V.cap - s0 : 0;   // overflowed step: stay in bounds
-      const int cnt = V.n_tiles[g] < room ? V.n_tiles[g] : (int)room;
-      for (int k = 0; k < cnt; ++k) {
-        const double4* rec = reinterpret_cast<const double4*>(V.partial + (int64_t)(s0 + k) * 8);
-        const double4 r0 = rec[0], r1 = rec[1];
-        c7[0] += r0.x; c7[1] += r0.y; c7[2] += r0.z; c7[3] += r0.w;
-        c7[4] += r1.x; c7[5] += r1.y; c7[6] += r1.z;
+    double dSc[4], dSi[4], duc[2], dui[2], dP;
+    if (V.ex) {
+      // plane-space gradients given by the caller (backward.py:171-240 arguments)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { dSc[i] = V.ex[i * n + g]; dSi[i] = V.ex[(4 + i) * n + g]; }
+      duc[0] = V.ex[8 * n + g]; duc[1] = V.ex[9 * n + g];
+      dui[0] = V.ex[10 * n + g]; dui[1] = V.ex[11 * n + g];
+      dP = V.ex[12 * n + g];
+      dk += V.ex[13 * n + g];
+    } else {
+      // plane-space gradients
+      const double4 Ac = reinterpret_cast<const double4*>(V.inv_c)[g];
+      const double4 Ai = reinterpret_cast<const double4*>(V.inv_i)[g];
+      // computation-plane partials: one record per member tile, fixed order
+      double c7[7] = {0, 0, 0, 0, 0, 0, 0};
+      {
+        const int s0 = V.pair_start[g];
+        const int64_t room = V.cap - s0 > 0 ? V.cap - s0 : 0;   // overflowed step: stay in bounds
+        const int cnt = V.n_tiles[g] < room ? V.n_tiles[g] : (int)room;
+        for (int k = 0; k < cnt; ++k) {
+          const double4* rec = reinterpret_cast<const double4*>(V.partial + (int64_t)(s0 + k) * 8);
+          const double4 r0 = rec[0], r1 = rec[1];
+          c7[0] += r0.x; c7[1] += r0.y; c7[2] += r0.z; c7[3] += r0.w;
+          c7[4] += r1.x; c7[5] += r1.y; c7[6] += r1.z;
+        }
       }
+      inverse_chain(Ac.x, Ac.y, Ac.z, c7[2], c7[3], c7[4], dSc);
+      inverse_chain(Ai.x, Ai.y, Ai.z, V.acc[1 * n + g], V.acc[2 * n + g], V.acc[3 * n + g], dSi);
+      duc[0] = c7[5]; duc[1] = c7[6];
+      dui[0] = V.acc[4 * n + g]; dui[1] = V.acc[5 * n + g];
+      dP = c7[0];
+      dk += c7[1];
     }
-    double dSc[4], dSi[4];
-    inverse_chain(Ac.x, Ac.y, Ac.z, c7[2], c7[3], c7[4], dSc);
-    inverse_chain(Ai.x, Ai.y, Ai.z, V.acc[1 * n + g], V.acc[2 * n + g], V.acc[3 * n + g], dSi);
-    const double duc[2] = {c7[5], c7[6]};
-    const double dui[2] = {V.acc[4 * n + g], V.acc[5 * n + g]};
-    const double dP = c7[0];
-    dk += c7[1];
     // G3 += mc^T dSc mc + mi^T dSi mi   (backward.py:191-193)
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -330,6 +342,33 @@ int launch_grad_image(const sdgr_view& v, const sdgr_projection& p, const double
   return check_launch();
 }
 
+static void launch_geometry_batch(const sdgr_scene& sc, const GeoBatch& B, const sdgr_grads& out, int accumulate,
+                                  cudaStream_t st);
+
+int launch_grad_geometry_explicit(const sdgr_scene& sc, const sdgr_view& v, const sdgr_projection& p,
+                                  const double* ex, const sdgr_grads& out, cudaStream_t st) {
+  GeoBatch B;
+  B.n_views = 1;
+  GeoView& G = B.v[0];
+  for (int i = 0; i < 6; ++i) { G.mc[i] = v.mc[i]; G.mi[i] = v.mi[i]; }
+  for (int i = 0; i < 3; ++i) G.cam[i] = v.cam[i];
+  G.half_u = v.n_u / 2.0; G.half_v = v.n_v / 2.0;
+  G.half_az = v.n_az / 2.0; G.half_rg = v.n_rg / 2.0;
+  G.flags = p.flags;
+  G.inv_c = p.comp.inv_cov;
+  G.inv_i = p.img.inv_cov;
+  G.n_tiles = nullptr;
+  G.phase_raw = p.phase_raw;
+  G.pair_start = nullptr;
+  G.acc = nullptr;
+  G.partial = nullptr;
+  G.cap = 0;
+  G.ex = ex;
+  launch_geometry_batch(sc, B, out, 0, st);
+  note_launch();
+  return check_launch();
+}
+
 int launch_grad_geometry(const sdgr_scene& sc, int n_views, const sdgr_view* views,
                          const sdgr_projection* projs, const sdgr_tiles* comps, const double* const* acc_imgs,
                          const double* const* partials, const sdgr_grads& out, int accumulate,
@@ -352,10 +391,20 @@ int launch_grad_geometry(const sdgr_scene& sc, int n_views, const sdgr_view* vie
     G.acc = acc_imgs[k];
     G.partial = partials[k];
     G.cap = comps[k].n_pairs;
+    G.ex = nullptr;
   }
-  const unsigned blocks = (unsigned)((sc.n + 127) / 128);
   {
     KernelTimer kt(SDGR_K_GEOMETRY, st);
+    launch_geometry_batch(sc, B, out, accumulate, st);
+  }
+  note_launch();
+  return check_launch();
+}
+
+static void launch_geometry_batch(const sdgr_scene& sc, const GeoBatch& B, const sdgr_grads& out, int accumulate,
+                                  cudaStream_t st) {
+  const unsigned blocks = (unsigned)((sc.n + 127) / 128);
+  {
     if (sc.dtype == 0 && out.dtype == 0)
       k_grad_geometry<float, float><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
     else if (sc.dtype == 0)
@@ -365,8 +414,6 @@ int launch_grad_geometry(const sdgr_scene& sc, int n_views, const sdgr_view* vie
     else
       k_grad_geometry<double, double><<<blocks, 128, 0, st>>>(sc, B, out, accumulate);
   }
-  note_launch();
-  return check_launch();
 }
 
 }  // namespace sdgr

@@ -15,7 +15,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 PKG = HERE.parent
 ROOT = PKG.parent
-SOURCES = ["capi.cu", "preprocess.cu", "binning.cu", "composite.cu", "backward.cu", "train.cu", "densify.cu", "plyio.cu", "eval.cu"]
+SOURCES = ["capi.cu", "preprocess.cu", "binning.cu", "composite.cu", "backward.cu", "train.cu", "densify.cu", "plyio.cu", "eval.cu", "stages.cu"]
 HEADERS = [HERE / "common.cuh", ROOT / "include" / "sdgr.h"]
 LIB = PKG / os.environ.get("SDGR_LIB_NAME", "libsdgr.so")   # profiling variants: another name
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -75,6 +75,17 @@ int launch_adam(const sdgr_scene&, const sdgr_grads&, const sdgr_scene&, const s
                 double, double, double, double, double, unsigned long long*, const int32_t*, cudaStream_t);
 
 int launch_accum_update(const sdgr_grads&, int64_t, double*, double*, double*, cudaStream_t);
+int launch_cell_pairs(const sdgr_projection&, const sdgr_view&, const sdgr_tiles&, int64_t*, int32_t*, double*,
+                      double*, double*, cudaStream_t);
+int launch_cell_intensities(const sdgr_projection&, int64_t, const int64_t*, const int32_t*, const double*, double*,
+                            double*, double*, double*, cudaStream_t);
+int launch_splat_pair_grads(int64_t, const int32_t*, const int32_t*, const double*, const double*, double*,
+                            cudaStream_t);
+int launch_stage_grads(const sdgr_projection&, int, const sdgr_tiles*, const double*, double*, cudaStream_t);
+int launch_grad_geometry_explicit(const sdgr_scene&, const sdgr_view&, const sdgr_projection&, const double*,
+                                  const sdgr_grads&, cudaStream_t);
+int launch_project_planes(const sdgr_view&, int64_t, const double*, const double*, const double*, const double*,
+                          const double*, const double*, const double*, const sdgr_projection&, cudaStream_t);
 int launch_densify_flags(const sdgr_scene&, const double*, const double*, double, double, double, uint8_t*,
                          cudaStream_t);
 int launch_clone_shift(const sdgr_scene&, const double*, const double*, double, cudaStream_t);
@@ -291,6 +302,59 @@ int sdgr_grad_geometry_batch(const sdgr_scene* scene, int n_views, const sdgr_vi
   }
   return launch_grad_geometry(*scene, n_views, views, projs, comps, acc_imgs, partial_gs, *out, accumulate,
                               static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_cell_pairs(const sdgr_projection* proj, const sdgr_view* view, const sdgr_tiles* tiles,
+                    int64_t* offsets, int32_t* prim, double* delta, double* q, double* w, void* stream) {
+  if (!proj || !view_ok(view) || !tiles || !offsets || (tiles->plane != 0 && tiles->plane != 1)) return SDGR_ERR_INVALID;
+  if (!tiles->pair_prim || !tiles->tile_range || tiles->n_tiles < 1) return SDGR_ERR_INVALID;
+  const sdgr_plane& pl = tiles->plane == 0 ? proj->comp : proj->img;
+  if (!pl.uv || !pl.inv_cov || !pl.bbox || !pl.cell_mask) return SDGR_ERR_INVALID;   // needs the SoA records
+  if (prim && (!delta || !q || !w)) return SDGR_ERR_INVALID;
+  return launch_cell_pairs(*proj, *view, *tiles, offsets, prim, delta, q, w, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_cell_intensities(const sdgr_projection* proj, int64_t n_cells, const int64_t* offsets, const int32_t* prim,
+                          const double* w, double* tau, double* trans, double* absorb, double* contrib,
+                          void* stream) {
+  if (!proj || !proj->kappa || !proj->phase || n_cells < 0 || !offsets || !tau || !trans || !absorb || !contrib)
+    return SDGR_ERR_INVALID;
+  if (n_cells == 0) return SDGR_OK;
+  if (!prim || !w) return SDGR_ERR_INVALID;
+  return launch_cell_intensities(*proj, n_cells, offsets, prim, w, tau, trans, absorb, contrib,
+                                 static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_splat_pair_grads(int64_t n_pairs, const int32_t* pair_pixel, const int32_t* pair_prim, const double* dL_dS,
+                          const double* intensity, double* dL_dbeta, void* stream) {
+  if (n_pairs < 0) return SDGR_ERR_INVALID;
+  if (n_pairs > 0 && (!pair_pixel || !pair_prim || !dL_dS || !intensity || !dL_dbeta)) return SDGR_ERR_INVALID;
+  return launch_splat_pair_grads(n_pairs, pair_pixel, pair_prim, dL_dS, intensity, dL_dbeta,
+                                 static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_stage_grads(const sdgr_projection* proj, int32_t plane, const sdgr_tiles* comp, const double* src,
+                     double* out, void* stream) {
+  if (!proj || proj->n < 1 || !src || !out || (plane != 0 && plane != 1)) return SDGR_ERR_INVALID;
+  if (plane == 0 && (!comp || comp->plane != 0 || !comp->pair_start)) return SDGR_ERR_INVALID;
+  return launch_stage_grads(*proj, plane, plane == 0 ? comp : nullptr, src, out, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_grad_geometry_explicit(const sdgr_scene* scene, const sdgr_view* view, const sdgr_projection* proj,
+                                const double* ex, sdgr_grads* out, void* stream) {
+  if (!scene || !view_ok(view) || !proj || !ex || !out) return SDGR_ERR_INVALID;
+  if (scene->n != proj->n) return SDGR_ERR_STATE;
+  return launch_grad_geometry_explicit(*scene, *view, *proj, ex, *out, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_project_planes(const sdgr_view* view, int64_t n, const double* uv_comp, const double* uv_img,
+                        const double* depth, const double* cov_comp, const double* cov_img, const double* phase_raw,
+                        const double* kappa, sdgr_projection* proj, void* stream) {
+  if (!view_ok(view) || n < 1 || !uv_comp || !uv_img || !depth || !cov_comp || !cov_img || !phase_raw || !kappa ||
+      !proj || proj->n != n)
+    return SDGR_ERR_INVALID;
+  return launch_project_planes(*view, n, uv_comp, uv_img, depth, cov_comp, cov_img, phase_raw, kappa, *proj,
+                               static_cast<cudaStream_t>(stream));
 }
 
 size_t sdgr_loss_scratch_bytes(int h, int w) { return h > 0 && w > 0 ? loss_scratch_bytes(h, w) : 0; }

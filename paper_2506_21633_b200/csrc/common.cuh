@@ -97,6 +97,58 @@ __device__ __forceinline__ double quadform(double a00, double a01, double a11,
   return dadd(dadd(t1, t2), t3);
 }
 
+// 256-bit in-tile member mask of one Gaussian (bit = local cell (iv&15)*16+(iu&15)).
+// Small footprints: the 8x8 window rows are shifted into place (no per-bit
+// loop).  Large footprints: exact FP64 test of the bbox cells in the tile.
+__device__ __forceinline__ void member_mask(double u, double v, double a00, double a01, double a11,
+                                            uint64_t cell_mask, int x0, int x1, int y0, int y1, int tx, int ty,
+                                            double cutoff, uint64_t m[4]) {
+  m[0] = m[1] = m[2] = m[3] = 0;
+  if (x0 > x1 || y0 > y1) return;
+  if ((x1 - x0) < 8 && (y1 - y0) < 8) {
+    const uint64_t cm = cell_mask;
+    const int c0 = x0 - tx * kTile, r0 = y0 - ty * kTile;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int rr = r0 + k;
+      const uint32_t byte = (uint32_t)(cm >> (8 * k)) & 0xffu;
+      if (rr < 0 || rr > 15 || byte == 0) continue;
+      const uint32_t bits = (c0 >= 0 ? (byte << c0) : (byte >> (-c0))) & 0xffffu;
+      const uint64_t v = (uint64_t)bits << ((rr & 3) * 16);
+      const int w = rr >> 2;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) m[q] |= (w == q) ? v : 0ull;
+    }
+    return;
+  }
+  const bool dense = !isfinite(cutoff);
+  const double cut2 = dmul(cutoff, cutoff), a01x2 = dmul(2.0, a01);
+  const int cx0 = max(x0, tx * kTile), cx1 = min(x1, tx * kTile + kTile - 1);
+  const int cy0 = max(y0, ty * kTile), cy1 = min(y1, ty * kTile + kTile - 1);
+  for (int iv = cy0; iv <= cy1; ++iv) {
+    const double dy = dsub((double)iv, v);
+    const double t3 = dmul(a11, dmul(dy, dy));
+    for (int iu = cx0; iu <= cx1; ++iu) {
+      bool member = dense;
+      if (!dense) {
+        const double dx = dsub((double)iu, u);
+        const double q = dadd(dadd(dmul(a00, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
+        member = q <= cut2;
+      }
+      if (member) {
+        const int c = ((iv & 15) << 4) | (iu & 15);
+        const uint64_t bit = 1ull << (c & 63);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) m[w] |= (c >> 6) == w ? bit : 0ull;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void member_mask(const sdgr_pair_rec& r, int tx, int ty, double cutoff, uint64_t m[4]) {
+  member_mask(r.u, r.v, r.a00, r.a01, r.a11, r.cell_mask, r.x0, r.x1, r.y0, r.y1, tx, ty, cutoff, m);
+}
+
 __device__ __forceinline__ double softplus64(double x) {
   // np.logaddexp(0, x) = max(x,0) + log1p(exp(-|x|))  (scene.py:22-25)
   if (!(x == x)) return x;

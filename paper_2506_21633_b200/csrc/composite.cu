@@ -87,54 +87,6 @@ struct WalkArgs {
   sdgr_replay rp;          // kContrib: live-pair log to write (rp.y1 == nullptr: none)
 };
 
-// 256-bit in-tile member mask of one Gaussian (bit = local cell (iv&15)*16+(iu&15)).
-// Small footprints: the 8x8 window rows are shifted into place (no per-bit
-// loop).  Large footprints: exact FP64 test of the bbox cells in the tile.
-__device__ __forceinline__ void member_mask(const sdgr_pair_rec& r, int tx, int ty, double cutoff,
-                                            uint64_t m[4]) {
-  m[0] = m[1] = m[2] = m[3] = 0;
-  const int x0 = r.x0, x1 = r.x1, y0 = r.y0, y1 = r.y1;
-  if (x0 > x1 || y0 > y1) return;
-  if ((x1 - x0) < 8 && (y1 - y0) < 8) {
-    const uint64_t cm = r.cell_mask;
-    const int c0 = x0 - tx * kTile, r0 = y0 - ty * kTile;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int rr = r0 + k;
-      const uint32_t byte = (uint32_t)(cm >> (8 * k)) & 0xffu;
-      if (rr < 0 || rr > 15 || byte == 0) continue;
-      const uint32_t bits = (c0 >= 0 ? (byte << c0) : (byte >> (-c0))) & 0xffffu;
-      const uint64_t v = (uint64_t)bits << ((rr & 3) * 16);
-      const int w = rr >> 2;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) m[q] |= (w == q) ? v : 0ull;
-    }
-    return;
-  }
-  const bool dense = !isfinite(cutoff);
-  const double cut2 = dmul(cutoff, cutoff), a01x2 = dmul(2.0, r.a01);
-  const int cx0 = max(x0, tx * kTile), cx1 = min(x1, tx * kTile + kTile - 1);
-  const int cy0 = max(y0, ty * kTile), cy1 = min(y1, ty * kTile + kTile - 1);
-  for (int iv = cy0; iv <= cy1; ++iv) {
-    const double dy = dsub((double)iv, r.v);
-    const double t3 = dmul(r.a11, dmul(dy, dy));
-    for (int iu = cx0; iu <= cx1; ++iu) {
-      bool member = dense;
-      if (!dense) {
-        const double dx = dsub((double)iu, r.u);
-        const double q = dadd(dadd(dmul(r.a00, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
-        member = q <= cut2;
-      }
-      if (member) {
-        const int c = ((iv & 15) << 4) | (iu & 15);
-        const uint64_t bit = 1ull << (c & 63);
-#pragma unroll
-        for (int w = 0; w < 4; ++w) m[w] |= (c >> 6) == w ? bit : 0ull;
-      }
-    }
-  }
-}
-
 __device__ __forceinline__ sdgr_pair_rec load_rec(const sdgr_pair_rec* p) {
   sdgr_pair_rec r;
   const double2* s = reinterpret_cast<const double2*>(p);
@@ -285,14 +237,50 @@ __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const 
 // footprints (<= 8x8 window) are flattened per warp through a member list
 // (as in pass A) so the exp/RED work runs at full SIMT width; larger
 // footprints are walked by their own thread.
-__device__ __forceinline__ void splat_add(unsigned long long* acc, int n_az, int iu, int iv, double q, double I) {
-  const double v = exp(-q) * I;
-  atomicAdd(acc + (int64_t)iv * n_az + iu, (unsigned long long)__double2ull_rn(fmin(v, kFixMax) * kFix));
+// Splat fixed point: per view, value * 2^(47 - e) with 2^e > max_g I_g, so
+// every term w I <= I_max maps below 2^47 and a pixel can take 2^16 terms at
+// the maximum before the u64 sum could wrap; the absolute precision is
+// 2^-47 I_max (~7e-15 relative to the brightest Gaussian), whatever the
+// scene's brightness.  Integer adds are associative: the image is bitwise
+// deterministic.  Non-finite terms saturate at 2^47 (the forward's status
+// word has already flagged them).
+constexpr double kSplatTop = 140737488355328.0;   // 2^47
+
+__device__ __forceinline__ double splat_scale(const unsigned long long* max_bits) {
+  const double M = __longlong_as_double((long long)*max_bits);
+  if (!(M > 0.0) || !isfinite(M)) return 1.0;
+  int e;
+  frexp(M, &e);                 // M < 2^e
+  return ldexp(1.0, 47 - e);
+}
+
+__device__ __forceinline__ unsigned long long splat_fix(double v, double scale) {
+  return (unsigned long long)__double2ull_rn(fmin(v * scale, kSplatTop));
+}
+
+__device__ __forceinline__ void splat_add(unsigned long long* acc, int n_az, int iu, int iv, double q, double I,
+                                          double scale) {
+  atomicAdd(acc + (int64_t)iv * n_az + iu, splat_fix(exp(-q) * I, scale));
+}
+
+// max_g I_g over visible Gaussians as u64 bits (I >= 0: the bit order is the value order)
+__global__ void __launch_bounds__(256) k_max_intensity(const uint8_t* flags, const double* intensity, int64_t n,
+                                                       unsigned long long* max_bits) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long b = 0ull;
+  if (g < n && (flags[g] & SDGR_FLAG_VISIBLE)) {
+    const double I = intensity[g];
+    b = (I > 0.0 && isfinite(I)) ? (unsigned long long)__double_as_longlong(I) : 0ull;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) b = max(b, __shfl_down_sync(0xffffffffu, b, off));
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(max_bits, b);
 }
 
 __global__ void __launch_bounds__(256) k_splat(sdgr_view view, sdgr_plane pl, const uint8_t* flags,
                                                const double* intensity, int64_t n,
-                                               unsigned long long* acc) {
+                                               unsigned long long* acc, const unsigned long long* max_bits) {
+  const double scale = splat_scale(max_bits);
   __shared__ double s_u[256], s_v[256], s_a0[256], s_a1[256], s_a2[256], s_I[256];
   __shared__ int32_t s_x[256], s_y[256];
   __shared__ uint16_t s_list[8 * kList];
@@ -343,7 +331,7 @@ __global__ void __launch_bounds__(256) k_splat(sdgr_view view, sdgr_plane pl, co
         const int iu = s_x[j] + (b & 7), iv = s_y[j] + (b >> 3);
         const double q = quadform(s_a0[j], s_a1[j], s_a2[j], dsub((double)iu, s_u[j]), dsub((double)iv, s_v[j]));
         pix = (int64_t)iv * view.n_az + iu;
-        val = (unsigned long long)__double2ull_rn(fmin(exp(-q) * s_I[j], kFixMax) * kFix);
+        val = splat_fix(exp(-q) * s_I[j], scale);
       }
       // (combining a round's same-pixel terms with MATCH.ANY before the RED
       // was measured slower: 4.0 -> 6.5 ms/step, only ~17 % of the REDs merge)
@@ -357,14 +345,15 @@ __global__ void __launch_bounds__(256) k_splat(sdgr_view view, sdgr_plane pl, co
     for (int iv = bb.z; iv <= bb.w; ++iv)
       for (int iu = bb.x; iu <= bb.y; ++iu) {
         const double q = quadform(A.x, A.y, A.z, dsub((double)iu, uv.x), dsub((double)iv, uv.y));
-        if (dense || q <= cut2) splat_add(acc, view.n_az, iu, iv, q, I);
+        if (dense || q <= cut2) splat_add(acc, view.n_az, iu, iv, q, I, scale);
       }
   }
 }
 
 __global__ void __launch_bounds__(256) k_splat_finish(const unsigned long long* acc, int64_t n, double* image) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) image[i] = (double)acc[i] * kFixInv;
+  const double inv = 1.0 / splat_scale(acc + n);
+  if (i < n) image[i] = (double)acc[i] * inv;
 }
 
 // ============================================================ tile walks ======
@@ -1198,18 +1187,21 @@ int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const
   return check_launch();
 }
 
-// image: (n_rg, n_az) FP64; part: scratch of >= n_rg*n_az u64 (8-byte) slots.
+// image: (n_rg, n_az) FP64; part: scratch of >= n_rg*n_az + 1 u64 (8-byte)
+// slots (the pixel sums, then the view's max intensity).
 int launch_splat(const sdgr_view& v, const sdgr_projection& p, const double* intensity, double* part,
                  double* image, cudaStream_t st) {
   const int64_t npix = (int64_t)v.n_az * v.n_rg;
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(part);
-  if (cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * npix, st) != cudaSuccess) return SDGR_ERR_CUDA;
+  if (cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * (npix + 1), st) != cudaSuccess) return SDGR_ERR_CUDA;
+  const unsigned gb = (unsigned)((p.n + 255) / 256);
+  k_max_intensity<<<gb, 256, 0, st>>>(p.flags, intensity, p.n, acc + npix);
   {
     KernelTimer kt(SDGR_K_SPLAT, st);
-    k_splat<<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(v, p.img, p.flags, intensity, p.n, acc);
+    k_splat<<<gb, 256, 0, st>>>(v, p.img, p.flags, intensity, p.n, acc, acc + npix);
   }
   k_splat_finish<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(acc, npix, image);
-  note_launch(2);
+  note_launch(3);
   return check_launch();
 }
 

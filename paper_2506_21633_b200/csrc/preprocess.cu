@@ -407,6 +407,74 @@ __global__ void k_project_init(const __grid_constant__ ProjBatch B) {
   if (i < 2 && B.proj[k].member_pairs) B.proj[k].member_pairs[i] = 0ull;
 }
 
+// Records of a projection given in plane space (the reference tests'
+// hand-assembled Projection, tests/test_forward.py:43-59): every row is
+// visible; footprints, depth keys and packed rows exactly as k_project would
+// write them for the same plane-space values.
+__global__ void __launch_bounds__(256) k_project_planes(sdgr_view view, int64_t n, const double* __restrict__ uv_c,
+                                                        const double* __restrict__ uv_i,
+                                                        const double* __restrict__ depth,
+                                                        const double* __restrict__ cov_c,
+                                                        const double* __restrict__ cov_i,
+                                                        const double* __restrict__ praw,
+                                                        const double* __restrict__ kappa, sdgr_projection proj) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long mc = 0, mi = 0;
+  if (g < n) {
+    const bool dense = !isfinite(view.cutoff);
+    const double c00 = cov_c[3 * g], c01 = cov_c[3 * g + 1], c11 = cov_c[3 * g + 2];
+    const double i00 = cov_i[3 * g], i01 = cov_i[3 * g + 1], i11 = cov_i[3 * g + 2];
+    const double ru = dense ? 0.0 : dmul(view.cutoff, dsqrt(np_max0(c00)));
+    const double rv = dense ? 0.0 : dmul(view.cutoff, dsqrt(np_max0(c11)));
+    const double rui = dense ? 0.0 : dmul(view.cutoff, dsqrt(np_max0(i00)));
+    const double rvi = dense ? 0.0 : dmul(view.cutoff, dsqrt(np_max0(i11)));
+    double4 rc, ri;
+    mc = plane_footprint(proj.comp, g, uv_c[2 * g], uv_c[2 * g + 1], c00, c01, c11, ru, rv, view.n_u, view.n_v,
+                         view.cutoff, dense, rc);
+    mi = plane_footprint(proj.img, g, uv_i[2 * g], uv_i[2 * g + 1], i00, i01, i11, rui, rvi, view.n_az, view.n_rg,
+                         view.cutoff, dense, ri);
+    proj.flags[g] = SDGR_FLAG_VISIBLE;
+    proj.depth_key[g] = depth_key(depth[g]);
+    const double pr = praw[g];
+    const double ph = (pr == pr) ? fmax(pr, 0.0) : pr;
+    if (proj.kappa) proj.kappa[g] = kappa[g];
+    if (proj.phase) proj.phase[g] = ph;
+    proj.phase_raw[g] = pr;
+    if (proj.comp.packed) {
+      double4* pk = reinterpret_cast<double4*>(proj.comp.packed) + 2 * g;
+      pk[0] = make_double4(uv_c[2 * g], uv_c[2 * g + 1], rc.x, rc.y);
+      pk[1] = make_double4(rc.z, kappa[g], ph, rc.w);
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mc += __shfl_down_sync(0xffffffffu, mc, off);
+    mi += __shfl_down_sync(0xffffffffu, mi, off);
+  }
+  const int nv = __popc(__ballot_sync(0xffffffffu, g < n));
+  if ((threadIdx.x & 31) == 0) {
+    if (nv) atomicAdd(proj.counters, nv);
+    if (proj.member_pairs) {
+      if (mc) atomicAdd(proj.member_pairs, mc);
+      if (mi) atomicAdd(proj.member_pairs + 1, mi);
+    }
+  }
+}
+
+int launch_project_planes(const sdgr_view& view, int64_t n, const double* uv_c, const double* uv_i,
+                          const double* depth, const double* cov_c, const double* cov_i, const double* praw,
+                          const double* kappa, const sdgr_projection& proj, cudaStream_t st) {
+  ProjBatch B;
+  B.nv = 1;
+  B.view[0] = view;
+  B.proj[0] = proj;
+  k_project_init<<<1, 4 * SDGR_MAX_BATCH, 0, st>>>(B);
+  k_project_planes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(view, n, uv_c, uv_i, depth, cov_c, cov_i, praw,
+                                                                kappa, proj);
+  note_launch(2);
+  return check_launch();
+}
+
 int launch_project(const sdgr_scene& scene, int nv, const sdgr_view* views, sdgr_projection* projs,
                    cudaStream_t stream) {
   if (scene.n <= 0 || nv < 1 || nv > SDGR_MAX_BATCH) return SDGR_ERR_INVALID;

@@ -249,7 +249,7 @@ class MultiViewStep:
                 seg_c=_empty((max_items * 256,), torch.float64, dev),
                 partial_I=_empty((cap,), torch.float64, dev),
             )
-            ln.splat_scratch = _empty((v.n_rg * v.n_az,), torch.int64, dev)
+            ln.splat_scratch = _empty((v.n_rg * v.n_az + 1,), torch.int64, dev)
             # live-pair log: member pairs bound every view's live pairs
             ln.replay = ReplayLog(int(getattr(self, "calib_tc", cap * 16) * self.headroom), max_items, seg, dev, cap)
         ln0 = self.lanes[0]

@@ -98,19 +98,26 @@ class _PlaneRecords:
         return p
 
 
+def _as_out(t, host: bool):
+    """Reference-shaped results: numpy for host (numpy) callers, device tensors otherwise."""
+    return t.cpu().numpy() if host else t
+
+
 class Projection:
     """Device projection of one scene into one view (geometry.py:185-230).
 
     Records are N-sized in scene order; the reference's compacted views
     (``indices``, ``uv_comp``, ...) are exposed as properties that gather the
-    visible rows on demand.
+    visible rows on demand -- numpy arrays when the scene came from the host,
+    device tensors otherwise.
     """
 
-    def __init__(self, n: int, device, config, cov_reg: float, cutoff: float, accessors: bool):
+    def __init__(self, n: int, device, config, cov_reg: float, cutoff: float, accessors: bool, host: bool = False):
         self.n_scene = n
         self.config = config
         self.cov_reg = cov_reg
         self.cutoff = cutoff
+        self.host = host
         self.view = view_constants(config, cov_reg, cutoff)
         self.comp = _PlaneRecords(n, device, accessors)
         self.img = _PlaneRecords(n, device, accessors)
@@ -124,6 +131,7 @@ class Projection:
         self.ke_act = _empty((n, 2), torch.float64, device) if accessors else None
         self.look = _empty((n, 4), torch.float64, device) if accessors else None
         self._vis_idx = None
+        self._rows = None
         self._counts = None
 
     def desc(self) -> _lib.ProjectionDesc:
@@ -137,19 +145,67 @@ class Projection:
         d.member_pairs = ptr(self.member_pairs)
         return d
 
+    @classmethod
+    def from_planes(cls, config, uv_comp, depth, cov_comp=None, uv_img=None, cov_img=None, ke_sum=None,
+                    phase=None, cutoff: float = DEFAULT_CUTOFF, device=None) -> "Projection":
+        """A projection given directly in plane space -- the reference tests'
+        hand-assembled Projection (tests/test_forward.py:43-59: identity
+        covariances, kappa = P = 1 unless given, uv_img = uv_comp) -- with
+        the device records built by sdgr_project_planes, so the binning,
+        compositing and backward stages run on it unchanged."""
+        host = not isinstance(uv_comp, torch.Tensor)
+        dev = device or (uv_comp.device if not host else torch.device("cuda", torch.cuda.current_device()))
+        f64 = lambda x: (x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))  # noqa: E731
+                         ).to(device=dev, dtype=torch.float64).contiguous()
+        uv_c = f64(uv_comp).reshape(-1, 2)
+        k = uv_c.shape[0]
+        if k == 0:
+            raise InvalidParameterError("projection is empty")
+        eye = torch.eye(2, dtype=torch.float64, device=dev).expand(k, 2, 2)
+        cc = f64(cov_comp).reshape(k, 2, 2) if cov_comp is not None else eye
+        ci = f64(cov_img).reshape(k, 2, 2) if cov_img is not None else cc
+        tri = lambda c: torch.stack([c[:, 0, 0], c[:, 0, 1], c[:, 1, 1]], 1).contiguous()  # noqa: E731
+        uv_i = f64(uv_img).reshape(k, 2) if uv_img is not None else uv_c
+        kap = f64(ke_sum).reshape(k) if ke_sum is not None else torch.ones(k, dtype=torch.float64, device=dev)
+        ph = f64(phase).reshape(k) if phase is not None else torch.ones(k, dtype=torch.float64, device=dev)
+        d = f64(depth).reshape(k)
+        proj = cls(k, dev, config, 0.0, cutoff, accessors=True, host=host)
+        proj._desc = proj.desc()
+        keep = (uv_c, uv_i, d, tri(cc), tri(ci), ph, kap)
+        _check(_lib.lib().sdgr_project_planes(C.byref(proj.view), k, *(ptr(t) for t in keep), C.byref(proj._desc),
+                                              _stream()), "sdgr_project_planes")
+        proj._keep = keep
+        proj.ke_act[:, 0] = kap / 2.0
+        proj.ke_act[:, 1] = kap / 2.0
+        proj.look[:] = torch.tensor([0.0, 0.0, 1.0, 1.0], dtype=torch.float64, device=dev)
+        return proj
+
     # -- reference-shaped accessors (compacted to the K visible rows) -------
     @property
     def visible(self) -> torch.Tensor:
         return (self.flags & _lib.FLAG_VISIBLE) != 0
 
     @property
-    def indices(self) -> torch.Tensor:
+    def idx_t(self) -> torch.Tensor:
+        """Visible scene indices (device tensor), ascending."""
         if self._vis_idx is None:
             self._vis_idx = torch.nonzero(self.visible).flatten()
         return self._vis_idx
 
+    @property
+    def row_of(self) -> torch.Tensor:
+        """Scene index -> projection row (device; -1 for invisible rows)."""
+        if self._rows is None:
+            v = self.visible.to(torch.int64)
+            self._rows = torch.where(self.visible, torch.cumsum(v, 0) - 1, torch.full_like(v, -1))
+        return self._rows
+
+    @property
+    def indices(self):
+        return _as_out(self.idx_t, self.host)
+
     def __len__(self) -> int:
-        return int(self.indices.numel())
+        return int(self.idx_t.numel())
 
     def _counts_host(self):
         if self._counts is None:
@@ -164,23 +220,27 @@ class Projection:
     def n_skipped(self) -> int:
         return int(self._counts_host()[1])
 
+    def _k(self, t):
+        return _as_out(t[self.idx_t], self.host)
+
     @property
     def uv_comp(self):
-        return self.comp.uv[self.indices]
+        return self._k(self.comp.uv)
 
     @property
     def uv_img(self):
-        return self.img.uv[self.indices]
+        return self._k(self.img.uv)
 
     @property
     def depth(self):
-        return decode_depth(self.depth_key[self.indices])
+        return _as_out(decode_depth(self.depth_key[self.idx_t]), self.host)
 
     def _cov(self, pl):
         if pl.cov is None:
             raise StateError("projection was built without covariance accessors")
-        c = pl.cov[self.indices]
-        return torch.stack([torch.stack([c[:, 0], c[:, 1]], -1), torch.stack([c[:, 1], c[:, 2]], -1)], -2)
+        c = pl.cov[self.idx_t]
+        return _as_out(torch.stack([torch.stack([c[:, 0], c[:, 1]], -1), torch.stack([c[:, 1], c[:, 2]], -1)], -2),
+                       self.host)
 
     @property
     def cov_comp(self):
@@ -192,31 +252,31 @@ class Projection:
 
     @property
     def phase(self):
-        return self.phase_f[self.indices]
+        return self._k(self.phase_f)
 
     @property
     def phase_unclamped(self):
-        return self.phase_raw[self.indices]
+        return self._k(self.phase_raw)
 
     @property
     def ke_sum(self):
-        return self.kappa[self.indices]
+        return self._k(self.kappa)
 
     @property
     def ke_fwd(self):
-        return self.ke_act[self.indices, 0]
+        return self._k(self.ke_act[:, 0])
 
     @property
     def ke_bwd(self):
-        return self.ke_act[self.indices, 1]
+        return self._k(self.ke_act[:, 1])
 
     @property
     def look_dirs(self):
-        return self.look[self.indices, :3]
+        return self._k(self.look[:, :3])
 
     @property
     def look_dists(self):
-        return self.look[self.indices, 3]
+        return self._k(self.look[:, 3])
 
     @property
     def rotation(self) -> np.ndarray:
@@ -236,12 +296,12 @@ def project_all(scene, config, cov_reg: float = DEFAULT_COV_REG, cutoff: float =
     """geometry.project_all (geometry.py:233-340) on the device."""
     if len(scene) == 0:
         raise InvalidParameterError("scene is empty")
-    ds, _ = as_device_scene(scene)
-    return _project(ds, config, cov_reg, cutoff, accessors)
+    ds, host = as_device_scene(scene)
+    return _project(ds, config, cov_reg, cutoff, accessors, host)
 
 
-def _project(ds: DeviceScene, config, cov_reg, cutoff, accessors) -> Projection:
-    proj = Projection(len(ds), ds.device, config, cov_reg, cutoff, accessors)
+def _project(ds: DeviceScene, config, cov_reg, cutoff, accessors, host: bool = False) -> Projection:
+    proj = Projection(len(ds), ds.device, config, cov_reg, cutoff, accessors, host=host)
     proj._desc = proj.desc()
     sd = _scene_desc(ds)
     _check(_lib.lib().sdgr_project(C.byref(sd), C.byref(proj.view), C.byref(proj._desc), _stream()),
@@ -254,14 +314,22 @@ def _project(ds: DeviceScene, config, cov_reg, cutoff, accessors) -> Projection:
 # ----------------------------------------------------------------------------
 @dataclass
 class TileLists:
-    """Per-16x16-tile key lists of one plane.
+    """Per-16x16-tile key lists of one plane, plus the reference's per-cell
+    pair view of the same plane.
 
-    plane 0 (computation): each tile's Gaussians in (depth, index) order --
-    the per-ray order of forward.build_ray_lists (forward.py:138-155);
-    plane 1 (imaging): index order (forward._build_splat_pairs :213-224).
+    Device key lists (what the kernels walk): `pair_tile` / `tile_prim` /
+    `tile_range` -- per tile, the scene indices with a member cell in the
+    tile, in (depth, index) order on the computation plane (plane 0) and
+    index order on the imaging plane (plane 1).
 
-    Buffers hold `capacity` pairs.  With a cached capacity (device_count) the
-    exact pair count stays on the device (`count_dev`) until n_pairs is read.
+    Reference view (forward.RayLists / SplatPairs, forward.py:112-135,
+    202-210), materialised on first access by sdgr_cell_pairs: `pair_cell`
+    (`pair_pixel`), `pair_prim` (projection rows), `delta`, `q`, `weight`,
+    `offsets`, `cell_list(iu, iv)` and len() = member pairs.
+
+    Buffers hold `capacity` tile pairs.  With a cached capacity
+    (device_count) the exact count stays on the device (`count_dev`) until
+    n_pairs is read.
     """
 
     plane: int
@@ -272,7 +340,7 @@ class TileLists:
     capacity: int
     pair_tile: torch.Tensor
     pair_pos: torch.Tensor
-    pair_prim: torch.Tensor
+    tile_prim: torch.Tensor
     pre_prim: torch.Tensor
     pair_start: torch.Tensor
     tile_range: torch.Tensor
@@ -284,11 +352,14 @@ class TileLists:
     pair_rec: torch.Tensor | None = None
     member_pairs: int | None = None   # member (cell, Gaussian) pairs of the plane (capacity bound)
     count_dev: torch.Tensor | None = None   # device_count mode: offsets[n] on the device
+    projection: "Projection | None" = None
     _n_host: int | None = None
     _desc: object = field(default=None, repr=False)
+    _cells: dict | None = field(default=None, repr=False)
 
     @property
     def n_pairs(self) -> int:
+        """(tile, Gaussian) pairs of the plane."""
         if self._n_host is None:
             self._n_host = int(self.count_dev.item())
         return self._n_host
@@ -303,7 +374,7 @@ class TileLists:
             d.plane, d.tiles_x, d.tiles_y, d.n_tiles = self.plane, self.tiles_x, self.tiles_y, self.n_tiles
             d.n_pairs = self.capacity
             d.device_count = 0 if self.count_dev is None else 1
-            d.pair_tile, d.pair_pos, d.pair_prim = ptr(self.pair_tile), ptr(self.pair_pos), ptr(self.pair_prim)
+            d.pair_tile, d.pair_pos, d.pair_prim = ptr(self.pair_tile), ptr(self.pair_pos), ptr(self.tile_prim)
             d.pre_prim, d.pair_start, d.tile_range = ptr(self.pre_prim), ptr(self.pair_start), ptr(self.tile_range)
             d.seg_len, d.max_items = self.seg_len, self.max_items
             d.items, d.tile_first, d.n_items = ptr(self.items), ptr(self.tile_first), ptr(self.n_items)
@@ -314,10 +385,76 @@ class TileLists:
     def tile_list(self, tx: int, ty: int) -> torch.Tensor:
         t = ty * self.tiles_x + tx
         s, e = self.tile_range[t].tolist()
-        return self.pair_prim[s:e]
+        return self.tile_prim[s:e]
+
+    # -- reference view: member (cell, Gaussian) pairs ---------------------
+    def cells(self) -> dict:
+        """Device arrays of the member pairs in the reference's order:
+        cell, prim (scene index), row (projection row), delta, q, w, offsets."""
+        if self._cells is None:
+            p = self.projection
+            if p is None:
+                raise StateError("tile lists without their projection")
+            lib, st, dev = _lib.lib(), _stream(), self.tile_range.device
+            n_cells = self.n_u * self.n_v
+            off = torch.zeros((n_cells + 1,), dtype=torch.int64, device=dev)
+            desc = self.desc()
+            _check(lib.sdgr_cell_pairs(C.byref(p._desc), C.byref(p.view), C.byref(desc), ptr(off), None, None, None,
+                                       None, st), "sdgr_cell_pairs")
+            t = int(off[-1].item())
+            prim = _empty((max(t, 1),), torch.int32, dev)
+            delta = _empty((max(t, 1), 2), torch.float64, dev)
+            q = _empty((max(t, 1),), torch.float64, dev)
+            w = _empty((max(t, 1),), torch.float64, dev)
+            if t:
+                _check(lib.sdgr_cell_pairs(C.byref(p._desc), C.byref(p.view), C.byref(desc), ptr(off), ptr(prim),
+                                           ptr(delta), ptr(q), ptr(w), st), "sdgr_cell_pairs")
+            cell = torch.repeat_interleave(torch.arange(n_cells, device=dev), off[1:] - off[:-1])
+            prim, delta, q, w = prim[:t], delta[:t], q[:t], w[:t]
+            self._cells = dict(cell=cell, prim=prim, row=p.row_of[prim.long()], delta=delta, q=q, w=w, offsets=off)
+        return self._cells
+
+    def _ref(self, key):
+        host = self.projection.host if self.projection is not None else False
+        return _as_out(self.cells()[key], host)
+
+    @property
+    def pair_cell(self):
+        return self._ref("cell")
+
+    @property
+    def pair_pixel(self):
+        return self._ref("cell")
+
+    @property
+    def pair_prim(self):
+        """Projection rows of the member pairs (RayLists.pair_prim)."""
+        return self._ref("row")
+
+    @property
+    def delta(self):
+        return self._ref("delta")
+
+    @property
+    def q(self):
+        return self._ref("q")
+
+    @property
+    def weight(self):
+        return self._ref("w")
+
+    @property
+    def offsets(self):
+        return self._ref("offsets")
+
+    def cell_list(self, iu: int, iv: int):
+        """Projection rows covering cell (iu, iv), shallow-to-deep (RayLists.cell_list)."""
+        c = self.cells()
+        a, b = c["offsets"][iv * self.n_u + iu: iv * self.n_u + iu + 2].tolist()
+        return _as_out(c["row"][a:b], self.projection.host)
 
     def __len__(self) -> int:
-        return self.n_pairs
+        return int(self.cells()["cell"].numel())
 
 
 def _seg_len(n_pairs: int) -> int:
@@ -359,13 +496,13 @@ class _Binner:
         return TileLists(
             plane=pl, n_u=nu, n_v=nv, tiles_x=tx, tiles_y=ty, capacity=int(cap),
             pair_tile=_empty((c,), torch.int32, dev), pair_pos=_empty((c,), torch.int32, dev),
-            pair_prim=_empty((c,), torch.int32, dev), pre_prim=_empty((c,), torch.int32, dev),
+            tile_prim=_empty((c,), torch.int32, dev), pre_prim=_empty((c,), torch.int32, dev),
             pair_start=_empty((n,), torch.int32, dev), tile_range=_empty((tx * ty, 2), torch.int32, dev),
             seg_len=seg, max_items=max_items, items=_empty((max_items, 4), torch.int32, dev),
             tile_first=_empty((tx * ty,), torch.int32, dev),
             n_items=torch.zeros((4,), dtype=torch.int32, device=dev),
             pair_rec=(_empty((c, _lib.PAIR_REC_BYTES), torch.uint8, dev) if pl == 0 else None),
-            count_dev=count_dev, _n_host=None if count_dev is not None else int(cap))
+            count_dev=count_dev, projection=p, _n_host=None if count_dev is not None else int(cap))
 
     def run(self, planes=(0, 1), exact: bool = False):
         if not exact and all(self._key(pl) in _CAPS for pl in planes):
@@ -447,7 +584,11 @@ def build_splat_lists(projection: Projection, config=None) -> TileLists:
 # ----------------------------------------------------------------------------
 @dataclass
 class IntensityBuffer:
-    """Per-Gaussian intensities (N-sized, scene order) + per-ray segment state."""
+    """Per-Gaussian intensities (N-sized, scene order) + per-ray segment state.
+
+    Reference view (forward.IntensityBuffer, forward.py:167-175): `intensity`
+    (K rows) and the per-member-pair `tau`, `trans`, `absorb`, `contrib` in
+    the RayLists pair order, computed on first access (sdgr_cell_intensities)."""
 
     intensity_n: torch.Tensor
     seg_sum: torch.Tensor
@@ -458,15 +599,51 @@ class IntensityBuffer:
     projection: "Projection | None" = None   # set when the reference's compacted views are wanted
     replay: "ReplayLog | None" = None
     replay_ok: bool | None = None            # host copy of "the log did not overflow" (one status read)
+    rays: "TileLists | None" = None
+    _pairs: dict | None = None
 
     @property
     def indices(self):
         return None if self.projection is None else self.projection.indices
 
     @property
-    def intensity(self) -> torch.Tensor:
+    def intensity(self):
         """(K,) compacted like the reference's IntensityBuffer.intensity."""
-        return self.intensity_n if self.projection is None else self.intensity_n[self.projection.indices]
+        if self.projection is None:
+            return self.intensity_n
+        return _as_out(self.intensity_n[self.projection.idx_t], self.projection.host)
+
+    def _pair(self, key):
+        if self._pairs is None:
+            if self.rays is None or self.projection is None:
+                raise StateError("per-pair buffers need the ray lists and the projection")
+            c = self.rays.cells()
+            t = c["prim"].numel()
+            dev = self.intensity_n.device
+            out = {k: _empty((max(t, 1),), torch.float64, dev) for k in ("tau", "trans", "absorb", "contrib")}
+            p = self.projection
+            _check(_lib.lib().sdgr_cell_intensities(C.byref(p._desc), self.rays.n_u * self.rays.n_v,
+                                                    ptr(c["offsets"]), ptr(c["prim"]), ptr(c["w"]),
+                                                    ptr(out["tau"]), ptr(out["trans"]), ptr(out["absorb"]),
+                                                    ptr(out["contrib"]), _stream()), "sdgr_cell_intensities")
+            self._pairs = {k: v[:t] for k, v in out.items()}
+        return _as_out(self._pairs[key], self.projection.host)
+
+    @property
+    def tau(self):
+        return self._pair("tau")
+
+    @property
+    def trans(self):
+        return self._pair("trans")
+
+    @property
+    def absorb(self):
+        return self._pair("absorb")
+
+    @property
+    def contrib(self):
+        return self._pair("contrib")
 
 
 class ReplayLog:
@@ -512,6 +689,7 @@ def compute_intensities(rays: TileLists, projection: Projection, s_stop: float =
         partial=_empty((max(rays.capacity, 1),), torch.float64, dev),
         status=torch.zeros((4,), dtype=torch.int32, device=dev),
         s_stop=float(s_stop),
+        projection=projection, rays=rays,
     )
     if replay and rays.member_pairs is not None:
         buf.replay = ReplayLog(rays.member_pairs, rays.max_items, rays.seg_len, dev, rays.capacity)
@@ -590,15 +768,20 @@ def _first_bad_primitive(proj: Projection) -> int:
 
 
 def splat_image(intensities: IntensityBuffer, projection: Projection, config=None,
-                pairs: TileLists | None = None) -> torch.Tensor:
-    """forward.splat_image (forward.py:227-240): (n_range, n_azimuth) float64.
+                pairs: TileLists | None = None):
+    """forward.splat_image (forward.py:227-240): (n_range, n_azimuth) float64
+    (numpy for host callers).
 
     Gaussian-parallel with deterministic fixed-point accumulation; the
     imaging-plane tile lists (``pairs``) are not needed and are ignored."""
+    return _as_out(_splat(intensities, projection), projection.host)
+
+
+def _splat(intensities: IntensityBuffer, projection: Projection) -> torch.Tensor:
     v = projection.view
     dev = projection.flags.device
     image = _empty((v.n_rg, v.n_az), torch.float64, dev)
-    scratch = _empty((v.n_rg * v.n_az,), torch.int64, dev)
+    scratch = _empty((v.n_rg * v.n_az + 1,), torch.int64, dev)
     _check(_lib.lib().sdgr_splat(C.byref(v), C.byref(projection._desc), ptr(intensities.intensity_n),
                                  ptr(scratch), ptr(image), _stream()), "sdgr_splat")
     return image
@@ -643,18 +826,19 @@ def render_forward(scene, config, cov_reg: float = DEFAULT_COV_REG, cutoff: floa
     if len(scene) == 0:
         raise NumericalError("cannot retain buffers for an empty scene")
     ds, host = as_device_scene(scene)
-    proj = _project(ds, config, cov_reg, cutoff, accessors)
+    proj = _project(ds, config, cov_reg, cutoff, accessors, host)
     for exact in (False, True):
         rays = _Binner(proj).run((0,), exact=exact)[0]
         buf = compute_intensities(rays, proj, s_stop=s_stop, check=False)
-        image = splat_image(buf, proj, config)
+        image = _splat(buf, proj)
         ov, bad = _forward_status(buf, proj, [rays])
         if not ov:
             break
         _CAPS.pop(_Binner(proj)._key(0), None)   # grown footprints: re-bin with exact counts
     if bad:
         raise NumericalError(f"non-finite intensity at primitive {_first_bad_primitive(proj)}")
-    buf.projection = proj if accessors else None
+    if not accessors:
+        buf.projection = None
     return ForwardResult(scene=scene, device_scene=ds, config=config, projection=proj, rays=rays,
                          intensities=buf, image_t=image, host=host)
 
@@ -715,9 +899,11 @@ class SceneGradients:
                               self.visible.cpu().numpy() > 0)
 
 
-def grad_image_stage(fwd: ForwardResult, dL_dS: torch.Tensor) -> torch.Tensor:
-    """backward.grad_image_stage (backward.py:86-104): acc (6, N) float64 =
-    [dL/dI, dL/dA00, dL/dA01, dL/dA11, dL/du, dL/dv] on the imaging plane."""
+# -- fused device stages (what backward() runs) ------------------------------
+def image_stage_sums(fwd: ForwardResult, dL_dS: torch.Tensor) -> torch.Tensor:
+    """grad_image_stage's per-Gaussian sums, acc (6, N) float64 = [dL/dI,
+    G00, G01, G11, dL/du, dL/dv] on the imaging plane (G: the quadratic-form
+    gradient before the inverse chain)."""
     p = fwd.projection
     acc = _empty((6, p.n_scene), torch.float64, p.flags.device)
     _check(_lib.lib().sdgr_grad_image(C.byref(p.view), C.byref(p._desc), ptr(fwd.intensities.intensity_n),
@@ -725,10 +911,10 @@ def grad_image_stage(fwd: ForwardResult, dL_dS: torch.Tensor) -> torch.Tensor:
     return acc
 
 
-def grad_intensity_stage(fwd: ForwardResult, dL_dI: torch.Tensor, use_replay: bool = True) -> torch.Tensor:
-    """backward.grad_intensity_stage (backward.py:107-148): per-(tile, Gaussian)
-    partials (T16, 8) float64 = [dL/dP, dL/dkappa, dL/dA00, dL/dA01, dL/dA11,
-    dL/du, dL/dv, 0] on the computation plane, indexed by pre-sort position."""
+def intensity_stage_partials(fwd: ForwardResult, dL_dI: torch.Tensor, use_replay: bool = True) -> torch.Tensor:
+    """grad_intensity_stage's per-(tile, Gaussian) partials (T16, 8) float64
+    = [dL/dP, dL/dkappa, G00, G01, G11, dL/du, dL/dv, 0] on the computation
+    plane, indexed by pre-sort position.  dL_dI: (N,) scene order."""
     p, rays, buf = fwd.projection, fwd.rays, fwd.intensities
     dev = p.flags.device
     partial = _empty((max(rays.capacity, 1), 8), torch.float64, dev)
@@ -744,11 +930,11 @@ def grad_intensity_stage(fwd: ForwardResult, dL_dI: torch.Tensor, use_replay: bo
     return partial
 
 
-def grad_geometry_stage(fwd: ForwardResult, acc_img: torch.Tensor, partial_comp: torch.Tensor,
-                        out: SceneGradients | None = None, accumulate: bool = False) -> SceneGradients:
-    """grad_geometry_stage + grad_sh_stage + final scatter (backward.py:171-290).
-    Host (FP64) callers get FP64 gradients like the reference; device callers
-    float32 unless they pass `out`."""
+def geometry_stage_fused(fwd: ForwardResult, acc_img: torch.Tensor, partial_comp: torch.Tensor,
+                         out: SceneGradients | None = None, accumulate: bool = False) -> SceneGradients:
+    """grad_geometry_stage + grad_sh_stage + final scatter (backward.py:171-290)
+    from the fused stage sums.  Host (FP64) callers get FP64 gradients like
+    the reference; device callers float32 unless they pass `out`."""
     p = fwd.projection
     if out is None:
         out = SceneGradients.zeros_device(p.n_scene, p.flags.device,
@@ -759,6 +945,100 @@ def grad_geometry_stage(fwd: ForwardResult, acc_img: torch.Tensor, partial_comp:
                                          C.byref(fwd.rays.desc()), ptr(acc_img), ptr(partial_comp),
                                          C.byref(gd), int(accumulate), _stream()), "sdgr_grad_geometry")
     return out
+
+
+# -- reference-shaped stage functions (backward.py:86-240) ------------------
+def _stage_grads(fwd: ForwardResult, plane: int, src: torch.Tensor) -> torch.Tensor:
+    p = fwd.projection
+    out = _empty((8, p.n_scene), torch.float64, p.flags.device)
+    _check(_lib.lib().sdgr_stage_grads(C.byref(p._desc), plane, C.byref(fwd.rays.desc()) if plane == 0 else None,
+                                       ptr(src), ptr(out), _stream()), "sdgr_stage_grads")
+    return out
+
+
+def _to_n(fwd: ForwardResult, x, width: int | None = None) -> torch.Tensor:
+    """K-row (reference layout) input -> N-row device FP64 in scene order."""
+    p = fwd.projection
+    dev = p.flags.device
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+    t = t.to(device=dev, dtype=torch.float64)
+    shape = (p.n_scene,) + tuple(t.shape[1:])
+    out = torch.zeros(shape, dtype=torch.float64, device=dev)
+    out[p.idx_t] = t
+    return out
+
+
+def grad_image_stage(fwd: ForwardResult, dL_dS):
+    """backward.grad_image_stage (backward.py:86-104): the reference's
+    4-tuple (dL/dI (K,), dL/dbeta (T_i,) per imaging pair in SplatPairs
+    order, dL/dcov_img (K, 2, 2), dL/duv_img (K, 2))."""
+    g = _as_device_grad(dL_dS, fwd)
+    acc = image_stage_sums(fwd, g)
+    st = _stage_grads(fwd, 1, acc)
+    sp = fwd.splat.cells()
+    t = sp["prim"].numel()
+    dbeta = _empty((max(t, 1),), torch.float64, g.device)
+    _check(_lib.lib().sdgr_splat_pair_grads(t, ptr(sp["cell"].to(torch.int32)), ptr(sp["prim"]), ptr(g),
+                                            ptr(fwd.intensities.intensity_n), ptr(dbeta), _stream()),
+           "sdgr_splat_pair_grads")
+    idx, host = fwd.projection.idx_t, fwd.projection.host
+    return tuple(_as_out(a, host) for a in (st[0][idx], dbeta[:t], st[2:6][:, idx].T.reshape(-1, 2, 2),
+                                            st[6:8][:, idx].T))
+
+
+def grad_intensity_stage(fwd: ForwardResult, dL_dI):
+    """backward.grad_intensity_stage (backward.py:107-148): the reference's
+    4-tuple (dL/dP (K,), dL/dke_sum (K,), dL/dcov_comp (K, 2, 2),
+    dL/duv_comp (K, 2)) for a K-row dL/dI."""
+    partial = intensity_stage_partials(fwd, _to_n(fwd, dL_dI))
+    st = _stage_grads(fwd, 0, partial)
+    idx, host = fwd.projection.idx_t, fwd.projection.host
+    return tuple(_as_out(a, host) for a in (st[0][idx], st[1][idx], st[2:6][:, idx].T.reshape(-1, 2, 2),
+                                            st[6:8][:, idx].T))
+
+
+def _explicit_geometry(fwd: ForwardResult, dcov_c=None, dcov_i=None, duv_c=None, duv_i=None, dP=None,
+                       dke=None) -> SceneGradients:
+    p = fwd.projection
+    if fwd.device_scene is None:
+        raise StateError("the geometry stage needs the scene the projection came from")
+    n, dev = p.n_scene, p.flags.device
+    ex = torch.zeros((14, n), dtype=torch.float64, device=dev)
+    if dcov_c is not None:
+        ex[0:4] = _to_n(fwd, np.asarray(dcov_c).reshape(-1, 4) if not isinstance(dcov_c, torch.Tensor)
+                        else dcov_c.reshape(-1, 4)).T
+    if dcov_i is not None:
+        ex[4:8] = _to_n(fwd, np.asarray(dcov_i).reshape(-1, 4) if not isinstance(dcov_i, torch.Tensor)
+                        else dcov_i.reshape(-1, 4)).T
+    if duv_c is not None:
+        ex[8:10] = _to_n(fwd, duv_c).T
+    if duv_i is not None:
+        ex[10:12] = _to_n(fwd, duv_i).T
+    if dP is not None:
+        ex[12] = _to_n(fwd, dP)
+    if dke is not None:
+        ex[13] = _to_n(fwd, dke)
+    out = SceneGradients.zeros_device(n, dev, dtype=torch.float64)
+    _check(_lib.lib().sdgr_grad_geometry_explicit(C.byref(_scene_desc(fwd.device_scene)), C.byref(p.view),
+                                                  C.byref(p._desc), ptr(ex.contiguous()), C.byref(out.desc()),
+                                                  _stream()), "sdgr_grad_geometry_explicit")
+    return out
+
+
+def grad_geometry_stage(fwd: ForwardResult, dL_dcov_comp, dL_dcov_img, dL_duv_comp, dL_duv_img, dL_dP):
+    """backward.grad_geometry_stage (backward.py:171-232): plane-space
+    gradients (K rows) -> (dL/dpos (K, 3), dL/drot (K, 4), dL/dlogs (K, 3))."""
+    g = _explicit_geometry(fwd, dL_dcov_comp, dL_dcov_img, dL_duv_comp, dL_duv_img, dL_dP)
+    idx = fwd.projection.idx_t
+    host = fwd.projection.host
+    return tuple(_as_out(a[idx], host) for a in (g.positions, g.rotations, g.log_scales))
+
+
+def grad_sh_stage(fwd: ForwardResult, dL_dP):
+    """backward.grad_sh_stage (backward.py:235-240): (K, 16) SH-coefficient
+    gradients, zero where the phase clamp is active."""
+    g = _explicit_geometry(fwd, dP=dL_dP)
+    return _as_out(g.sh_coeffs[fwd.projection.idx_t], fwd.projection.host)
 
 
 def _as_device_grad(dL_dS, fwd: ForwardResult) -> torch.Tensor:
@@ -778,7 +1058,7 @@ def backward(fwd: ForwardResult, dL_dS, out: SceneGradients | None = None, accum
     img_shape = (fwd.projection.view.n_rg, fwd.projection.view.n_az)
     if shape != img_shape:
         raise StateError(f"image gradient shape {shape} does not match forward {img_shape}")
-    if fwd.projection.n_scene != len(fwd.scene):
+    if fwd.scene is None or fwd.projection.n_scene != len(fwd.scene):
         raise StateError("scene changed since the forward pass; buffers are stale")
     if validate:
         # host arrays are checked on the host (no device round trip)
@@ -787,10 +1067,22 @@ def backward(fwd: ForwardResult, dL_dS, out: SceneGradients | None = None, accum
         if not ok:
             raise InvalidParameterError("dL_dS contains non-finite values")
     g = _as_device_grad(dL_dS, fwd)
-    acc_img = grad_image_stage(fwd, g)
-    partial = grad_intensity_stage(fwd, acc_img[0], use_replay=use_replay)
-    grads = grad_geometry_stage(fwd, acc_img, partial, out=out, accumulate=accumulate)
+    acc_img = image_stage_sums(fwd, g)
+    partial = intensity_stage_partials(fwd, acc_img[0], use_replay=use_replay)
+    grads = geometry_stage_fused(fwd, acc_img, partial, out=out, accumulate=accumulate)
     return grads.to_numpy() if fwd.host and out is None else grads
+
+
+def forward_from_projection(projection: Projection, s_stop: float = S_STOP, scene=None) -> ForwardResult:
+    """A ForwardResult for a given projection (tests/test_backward.py:18-27
+    builds one from a synthetic Projection): binning, compositing and the
+    splat on the device; the geometry stages need `scene`."""
+    rays = _Binner(projection).run((0,), exact=True)[0]
+    buf = compute_intensities(rays, projection, s_stop=s_stop)
+    image = _splat(buf, projection)
+    ds = None if scene is None else as_device_scene(scene)[0]
+    return ForwardResult(scene=scene, device_scene=ds, config=projection.config, projection=projection, rays=rays,
+                         intensities=buf, image_t=image, host=projection.host)
 
 
 def launch_count() -> int:

@@ -54,6 +54,12 @@ def assert_close(got, ref, atol=ATOL, rtol=RTOL, what=""):
             f"ref {ref.ravel()[i]!r}; max abs err {np.abs(got - ref).max():.3e}")
 
 
+def npa(x):
+    """numpy view of a reference-shaped result (numpy for host callers,
+    a CUDA tensor for device callers)."""
+    return x.detach().cpu().numpy() if hasattr(x, "detach") else np.asarray(x)
+
+
 @pytest.fixture
 def rng():
     return np.random.default_rng(12345)

@@ -24,7 +24,7 @@ intensities and every gradient column within 1e-6 + 1e-4 |ref|, visible exact.
 import numpy as np
 import pytest
 
-from conftest import GROUPS, assert_close
+from conftest import GROUPS, assert_close, npa
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -69,7 +69,7 @@ def check_tiles(tl, fo, plane, what):
     n = tl.n_pairs
     assert n == tt.size, (what, n, tt.size)
     assert np.array_equal(tl.pair_tile[:n].cpu().numpy().astype(np.int64), tt), what
-    assert np.array_equal(tl.pair_prim[:n].cpu().numpy().astype(np.int64), gi), what
+    assert np.array_equal(tl.tile_prim[:n].cpu().numpy().astype(np.int64), gi), what
     assert np.array_equal(tl.tile_range.cpu().numpy().astype(np.int64), rg), what
 
 
@@ -77,11 +77,11 @@ def dropin_vs_oracle(scene, cfg, key, seed):
     fo, dlds, go = oracle_view(scene, key, cfg, seed)
     fwd = sdgr.render_forward(scene, cfg)
     p = fwd.projection
-    assert np.array_equal(p.indices.cpu().numpy(), fo.proj.indices)
+    assert np.array_equal(npa(p.indices), fo.proj.indices)
     assert p.n_culled == fo.proj.n_culled and p.n_skipped == fo.proj.n_skipped
     check_tiles(fwd.rays, fo, 0, f"{key} comp tiles")
     check_tiles(fwd.splat, fo, 1, f"{key} img tiles")
-    assert_close(fwd.intensities.intensity.cpu().numpy(), fo.inten.intensity, what=f"{key} intensity")
+    assert_close(npa(fwd.intensities.intensity), fo.inten.intensity, what=f"{key} intensity")
     assert_close(fwd.image, fo.image, what=f"{key} image")
     g = sdgr.backward(fwd, dlds)
     for k in GROUPS + ("uv_grad_norm",):

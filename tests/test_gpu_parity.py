@@ -10,7 +10,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import GROUPS, assert_close, golden_files, load_golden
+from conftest import GROUPS, assert_close, npa, golden_files, load_golden
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -28,7 +28,7 @@ GOLDEN = golden_files()
 
 def tiles_np(tl):
     n = tl.n_pairs
-    return (tl.pair_tile[:n].cpu().numpy().astype(np.int64), tl.pair_prim[:n].cpu().numpy().astype(np.int64),
+    return (tl.pair_tile[:n].cpu().numpy().astype(np.int64), tl.tile_prim[:n].cpu().numpy().astype(np.int64),
             tl.tile_range.cpu().numpy().astype(np.int64))
 
 
@@ -46,20 +46,20 @@ def test_golden(path, s_stop):
     z, scene, cfg, cutoff = load_golden(path)
     fwd = sdgr.render_forward(scene, cfg, cutoff=cutoff, s_stop=s_stop)
     p = fwd.projection
-    idx = p.indices.cpu().numpy()
+    idx = npa(p.indices)
     assert np.array_equal(idx, z["indices"])
     assert p.n_culled == int(z["n_culled"]) and p.n_skipped == int(z["n_skipped"])
     # FP64 key chain: pixel centers and depth bit-identical to the reference
-    assert np.array_equal(p.uv_comp.cpu().numpy(), z["uv_comp"])
-    assert np.array_equal(p.uv_img.cpu().numpy(), z["uv_img"])
-    assert np.array_equal(p.depth.cpu().numpy(), z["depth"])
+    assert np.array_equal(npa(p.uv_comp), z["uv_comp"])
+    assert np.array_equal(npa(p.uv_img), z["uv_img"])
+    assert np.array_equal(npa(p.depth), z["depth"])
     # covariances: exp(log-scale) is the only non-reference op (<= 1 ulp)
-    assert_close(p.cov_comp.cpu().numpy()[:, [0, 0, 1], [0, 1, 1]], z["cov_comp"], 1e-12, 1e-12, "cov_comp")
-    assert_close(p.cov_img.cpu().numpy()[:, [0, 0, 1], [0, 1, 1]], z["cov_img"], 1e-12, 1e-12, "cov_img")
+    assert_close(npa(p.cov_comp)[:, [0, 0, 1], [0, 1, 1]], z["cov_comp"], 1e-12, 1e-12, "cov_comp")
+    assert_close(npa(p.cov_img)[:, [0, 0, 1], [0, 1, 1]], z["cov_img"], 1e-12, 1e-12, "cov_img")
     # bit-exact per-tile key lists and ranges, both planes
     check_tiles(fwd.rays, z["tiles0_tile"], z["tiles0_prim"], z["tiles0_range"], "comp tiles")
     check_tiles(fwd.splat, z["tiles1_tile"], z["tiles1_prim"], z["tiles1_range"], "img tiles")
-    assert_close(fwd.intensities.intensity.cpu().numpy(), z["intensity"], what="intensity")
+    assert_close(npa(fwd.intensities.intensity), z["intensity"], what="intensity")
     assert_close(fwd.image.cpu().numpy() if hasattr(fwd.image, "cpu") else fwd.image, z["image"], what="image")
     rows = z["grad_rows"]
     for tag, dlds in (("n", z["dLdS"]), ("s", z["image"])):
@@ -80,8 +80,8 @@ def _oracle_compare(scene, cfg, cutoff, s_stop=sdgr.S_STOP, seed=0, device_scene
         check_tiles(tl, tt, gi, rg, f"plane {plane}")
     # FP64 key chain bit-identical to the oracle's device-exp restatement
     p = fwd.projection
-    assert np.array_equal(p.cov_comp.cpu().numpy(), fo.proj.cov_comp)
-    assert np.array_equal(p.depth.cpu().numpy(), fo.proj.depth)
+    assert np.array_equal(npa(p.cov_comp), fo.proj.cov_comp)
+    assert np.array_equal(npa(p.depth), fo.proj.depth)
     rng = np.random.default_rng(seed)
     dlds = rng.normal(size=img.shape)
     go = O.backward(fo, dlds)
@@ -405,7 +405,7 @@ def test_batched_preprocessing_equals_single_views(n_views):
         t = step.slot_t[k]
         assert int(step.slot_offsets[k][step.n].item()) == n, f"view {k}: pair count"
         assert torch.equal(t["pair_tile"][:n].cpu(), tl.pair_tile[:n].cpu()), f"view {k}: tiles"
-        assert torch.equal(t["pair_prim"][:n].cpu(), tl.pair_prim[:n].cpu()), f"view {k}: key lists"
+        assert torch.equal(t["pair_prim"][:n].cpu(), tl.tile_prim[:n].cpu()), f"view {k}: key lists"
         assert torch.equal(t["tile_range"].cpu(), tl.tile_range.cpu()), f"view {k}: tile ranges"
         assert torch.equal(t["pair_start"].cpu(), tl.pair_start.cpu()), f"view {k}: pair starts"
         assert torch.equal(t["pair_rec"][:n].cpu(), tl.pair_rec[:n].cpu()), f"view {k}: pair records"
@@ -443,7 +443,7 @@ def test_batched_preprocessing_small_scenes(cutoff):
         m = tl.n_pairs
         t = step.slot_t[k]
         assert int(step.slot_offsets[k][step.n].item()) == m
-        assert torch.equal(t["pair_prim"][:m].cpu(), tl.pair_prim[:m].cpu()), f"view {k}: key lists"
+        assert torch.equal(t["pair_prim"][:m].cpu(), tl.tile_prim[:m].cpu()), f"view {k}: key lists"
         assert torch.equal(t["tile_range"].cpu(), tl.tile_range.cpu()), f"view {k}: tile ranges"
         assert torch.equal(t["pair_rec"][:m].cpu(), tl.pair_rec[:m].cpu()), f"view {k}: pair records"
 
