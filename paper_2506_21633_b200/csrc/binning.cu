@@ -1121,16 +1121,20 @@ __global__ void __launch_bounds__(256) k_key32(const __grid_constant__ DepthIO i
   bh.flush(hist + (size_t)v * kHistStride, kMaxPass);
 }
 
-// Runs of equal k32 (~10 % of the keys on c4, at most a handful long): the
+// Runs of equal k32 (~10 % of the keys on c4, almost all of length 2-3): the
 // last radix pass wrote its order to `tmp`; one thread per position copies it
 // to `order`, except that a member of a run of L <= kRunPar entries computes
 // its rank under (64-bit key, index) against the L - 1 others (independent,
-// L1-resident loads) and lands at run start + rank.  Longer runs fall back
-// to one thread's insertion sort.  No thread waits on another.
+// L1-resident loads) and lands at run start + rank.  Each thread looks at
+// most kRunPar positions either way, so no run costs more than O(L kRunPar).
+// Longer runs (many equal depths, or one far outlier squeezing the visible
+// depths into few buckets) are listed by their head and sorted by
+// k_sort_long_runs.
 constexpr int kRunPar = 64;
 
 __global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s_all, const uint32_t* tmp_all, int64_t ks,
-                                                  const __grid_constant__ DepthIO io, int64_t n) {
+                                                  const __grid_constant__ DepthIO io, int64_t n,
+                                                  unsigned long long* lr_count, int64_t* lr_start, int64_t lr_cap) {
   const int v = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -1141,28 +1145,19 @@ __global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s_all, cons
   const int32_t g = (int32_t)tmp[i];
   if (k == kKeyInvisible) { order[i] = g; return; }   // invisible tail: order irrelevant
   int64_t s = i, e = i + 1;
-  while (s > 0 && k32s[s - 1] == k) --s;
-  while (e < n && k32s[e] == k) ++e;
-  if (e - s == 1) { order[i] = g; return; }
-  const uint64_t* key = io.key[v];
-  if (e - s > kRunPar) {
-    if (i != s) return;
-    for (int64_t a = s; a < e; ++a) order[a] = (int32_t)tmp[a];
-    for (int64_t a = s + 1; a < e; ++a) {              // insertion sort by (key, index)
-      const int32_t ga = order[a];
-      const uint64_t kga = key[ga];
-      int64_t b = a - 1;
-      while (b >= s) {
-        const int32_t h = order[b];
-        const uint64_t kh = key[h];
-        if (kh < kga || (kh == kga && h < ga)) break;
-        order[b + 1] = h;
-        --b;
-      }
-      order[b + 1] = ga;
+  while (s > 0 && i - s < kRunPar && k32s[s - 1] == k) --s;
+  while (e < n && e - i <= kRunPar && k32s[e] == k) ++e;
+  const bool open_lo = s > 0 && k32s[s - 1] == k, open_hi = e < n && k32s[e] == k;
+  if (open_lo || open_hi || e - s > kRunPar) {       // long run: index order now, sorted later
+    order[i] = g;
+    if (!open_lo && s == i) {
+      const unsigned long long j = atomicAdd(lr_count + v, 1ull);
+      if ((int64_t)j < lr_cap) lr_start[(int64_t)v * lr_cap + (int64_t)j] = i;
     }
     return;
   }
+  if (e - s == 1) { order[i] = g; return; }
+  const uint64_t* key = io.key[v];
   const uint64_t kg = key[g];
   int rank = 0;
   for (int64_t j = s; j < e; ++j) {
@@ -1173,12 +1168,99 @@ __global__ void __launch_bounds__(256) k_fix_runs(const uint32_t* k32s_all, cons
   order[s + rank] = g;
 }
 
+// One CTA per long run (grid-stride over the view's list): a block-serial
+// stable LSD radix sort of the run's scene indices by the 64-bit depth key,
+// one 8-bit pass per key byte that varies within the run (the input is in
+// index order, so equal keys keep index order: (depth, index) exactly).
+// Ping-pong between order[] and `scratch` (the view's free 24-bit key array).
+__global__ void __launch_bounds__(256) k_sort_long_runs(const uint32_t* k32s_all, int64_t ks,
+                                                        const __grid_constant__ DepthIO io, int64_t n,
+                                                        const unsigned long long* lr_count, const int64_t* lr_start,
+                                                        int64_t lr_cap, uint32_t* scratch_all) {
+  __shared__ int32_t base[256];
+  __shared__ unsigned long long s_or[8], s_and[8];
+  const int v = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t* k32s = k32s_all + (size_t)v * ks;
+  int32_t* order = io.order[v];
+  int32_t* scratch = reinterpret_cast<int32_t*>(scratch_all + (size_t)v * ks);
+  const uint64_t* key = io.key[v];
+  const int64_t cnt = min((int64_t)lr_count[v], lr_cap);
+  for (int64_t r = blockIdx.x; r < cnt; r += gridDim.x) {
+    const int64_t s = lr_start[(int64_t)v * lr_cap + r];
+    const uint32_t k = k32s[s];
+    int64_t e = s;
+    while (true) {   // run end: equal keys form a prefix of every 256-wide window
+      const int64_t p = e + tid;
+      const int same = __syncthreads_count(p < n && k32s[p] == k);
+      e += same;
+      if (same < 256) break;
+    }
+    // bits that vary within the run
+    unsigned long long o = 0ull, a = ~0ull;
+    for (int64_t p = s + tid; p < e; p += 256) {
+      const uint64_t kk = key[order[p]];
+      o |= kk;
+      a &= kk;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      o |= __shfl_xor_sync(0xffffffffu, o, off);
+      a &= __shfl_xor_sync(0xffffffffu, a, off);
+    }
+    if (lane == 0) { s_or[warp] = o; s_and[warp] = a; }
+    __syncthreads();
+    unsigned long long vary = 0ull;
+    for (int w = 0; w < 8; ++w) vary |= s_or[w] ^ s_and[w];
+    int32_t* src = order;
+    int32_t* dst = scratch;
+    for (int b = 0; b < 8; ++b) {
+      if (((vary >> (8 * b)) & 255ull) == 0) continue;
+      base[tid] = 0;
+      __syncthreads();
+      for (int64_t p = s + tid; p < e; p += 256) atomicAdd(&base[(key[src[p]] >> (8 * b)) & 255], 1);
+      __syncthreads();
+      if (tid == 0) {   // exclusive scan of the 256 digit counts (offsets from s)
+        int run = 0;
+        for (int d = 0; d < 256; ++d) { const int c = base[d]; base[d] = run; run += c; }
+      }
+      __syncthreads();
+      for (int64_t t0 = s; t0 < e; t0 += 256) {
+        const int64_t p = t0 + tid;
+        const bool ok = p < e;
+        const int32_t gi = ok ? src[p] : 0;
+        const int d = ok ? (int)((key[gi] >> (8 * b)) & 255) : -1;
+        for (int w = 0; w < 8; ++w) {          // warps in order, lanes in order: stable
+          if (warp == w) {
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            const int before = __popc(peers & ((1u << lane) - 1u));
+            const int leader = __ffs(peers) - 1;
+            int b0 = 0;
+            if (ok && lane == leader) b0 = base[d];
+            b0 = __shfl_sync(0xffffffffu, b0, leader);
+            if (ok) dst[s + b0 + before] = gi;
+            __syncwarp();
+            if (ok && lane == leader) base[d] = b0 + __popc(peers);
+          }
+          __syncthreads();
+        }
+      }
+      int32_t* t = src; src = dst; dst = t;
+      __syncthreads();
+    }
+    if (src != order)
+      for (int64_t p = s + tid; p < e; p += 256) order[p] = src[p];
+    __syncthreads();
+  }
+}
+
 // per-view stride of the 24-bit key arrays (keeps uint2 stores aligned)
 static int64_t key_stride(int64_t n) { return (n + 63) & ~int64_t(63); }
 
+static int64_t long_run_cap(int64_t n) { return n / (kRunPar + 1) + 1; }
+
 static size_t depth_ws_bytes(int64_t n, int nv) {
   return align_up(16 * (size_t)nv) + 3 * align_up(sizeof(uint32_t) * (size_t)nv * key_stride(n)) +
-         radix_ws_bytes(n, nv);
+         align_up(8 * (size_t)nv) + align_up(8 * (size_t)nv * long_run_cap(n)) + radix_ws_bytes(n, nv);
 }
 
 int launch_depth_order_batch(int nv, const sdgr_projection* projs, int32_t* const* orders, void* ws,
@@ -1194,6 +1276,9 @@ int launch_depth_order_batch(int nv, const sdgr_projection* projs, int32_t* cons
   uint32_t* k32 = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * ks);
   uint32_t* k32s = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * ks);
   uint32_t* tmp = reinterpret_cast<uint32_t*>(p); p += align_up(sizeof(uint32_t) * (size_t)nv * ks);
+  unsigned long long* lr_count = reinterpret_cast<unsigned long long*>(p); p += align_up(8 * (size_t)nv);
+  const int64_t lr_cap = long_run_cap(n);
+  int64_t* lr_start = reinterpret_cast<int64_t*>(p); p += align_up(8 * (size_t)nv * lr_cap);
   const RadixWs r = radix_layout(p, n, nv);
   DepthIO dio;
   for (int v = 0; v < nv; ++v) {
@@ -1202,6 +1287,7 @@ int launch_depth_order_batch(int nv, const sdgr_projection* projs, int32_t* cons
     dio.order[v] = orders[v];
   }
   if (cudaMemsetAsync(range, 0xff, 16 * (size_t)nv, st) != cudaSuccess ||
+      cudaMemsetAsync(lr_count, 0, 8 * (size_t)nv, st) != cudaSuccess ||
       cudaMemsetAsync(r.hist, 0, r.zero_bytes, st) != cudaSuccess)
     return SDGR_ERR_CUDA;
   const unsigned kb = (unsigned)((n + 256 * kKeyIpt - 1) / (256 * kKeyIpt));
@@ -1218,8 +1304,11 @@ int launch_depth_order_batch(int nv, const sdgr_projection* projs, int32_t* cons
   }
   const int rc = radix_passes(sio, true, nv, n, kMaxPass, r, st);
   if (rc != SDGR_OK) return rc;
-  k_fix_runs<<<dim3((unsigned)((n + 255) / 256), nv), 256, 0, st>>>(k32s, tmp, ks, dio, n);
-  note_launch();
+  k_fix_runs<<<dim3((unsigned)((n + 255) / 256), nv), 256, 0, st>>>(k32s, tmp, ks, dio, n, lr_count, lr_start,
+                                                                      lr_cap);
+  // (normally no long runs: the CTAs read a zero count and exit)
+  k_sort_long_runs<<<dim3(8, nv), 256, 0, st>>>(k32s, ks, dio, n, lr_count, lr_start, lr_cap, k32);
+  note_launch(2);
   return check_launch();
 }
 

@@ -33,7 +33,7 @@ from . import _lib
 from ._lib import ptr
 from .errors import DeviceError, InvalidParameterError, NumericalError, StateError
 from .radar import n_rays, radar_rotation, view_constants
-from .scene import GROUPS, DeviceScene, as_device_scene
+from .scene import GROUPS, DeviceScene, as_device_scene, upload_f64
 
 DEFAULT_COV_REG = 0.3
 DEFAULT_CUTOFF = 3.0
@@ -812,7 +812,10 @@ class ForwardResult:
         if not self.host:
             return self.image_t
         if self._image_host is None:
-            self._image_host = self.image_t.cpu().numpy()
+            h = torch.empty(self.image_t.shape, dtype=self.image_t.dtype, pin_memory=True)
+            h.copy_(self.image_t, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            self._image_host = h.numpy()
         return self._image_host
 
 
@@ -894,9 +897,18 @@ class SceneGradients:
         return d
 
     def to_numpy(self) -> "SceneGradients":
-        f = lambda t: t.double().cpu().numpy()  # noqa: E731
-        return SceneGradients(*(f(a) for a in self.param_arrays()), f(self.uv_grad_norm),
-                              self.visible.cpu().numpy() > 0)
+        """FP64 numpy copies (the reference's SceneGradients layout): one
+        device-to-pinned copy per array on the current stream, one sync; the
+        pinned buffers come from torch's caching host allocator and back the
+        returned arrays."""
+        arrays = [a.double() for a in self.param_arrays()] + [self.uv_grad_norm.double(), self.visible > 0]
+        host = []
+        for a in arrays:
+            h = torch.empty(a.shape, dtype=a.dtype, pin_memory=True)
+            h.copy_(a, non_blocking=True)
+            host.append(h)
+        torch.cuda.current_stream().synchronize()
+        return SceneGradients(*(h.numpy() for h in host))
 
 
 # -- fused device stages (what backward() runs) ------------------------------
@@ -1045,7 +1057,7 @@ def _as_device_grad(dL_dS, fwd: ForwardResult) -> torch.Tensor:
     dev = fwd.projection.flags.device
     if isinstance(dL_dS, torch.Tensor):
         return dL_dS.to(device=dev, dtype=torch.float64).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(dL_dS, dtype=np.float64)).to(dev)
+    return upload_f64(dL_dS, dev)
 
 
 def backward(fwd: ForwardResult, dL_dS, out: SceneGradients | None = None, accumulate: bool = False,

@@ -85,6 +85,37 @@ class DeviceScene:
         return Scene(*(t.detach().double().cpu().numpy() for t in self.arrays()))
 
 
+_POOL = None
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=max(1, min(8, len(os.sched_getaffinity(0)))))
+    return _POOL
+
+
+def upload_f64(a, device) -> torch.Tensor:
+    """Host array -> device FP64 tensor through a pinned staging buffer filled
+    by several threads (numpy's copy releases the GIL), then one async DMA:
+    roughly memory-bandwidth bound instead of the single-threaded pageable
+    copy path.  The staging block returns to torch's caching host allocator
+    once the copy has completed."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    h = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+    src, dst = a.reshape(-1), h.numpy().reshape(-1)
+    n = src.size
+    k = 8 if n >= (1 << 20) else 1
+    cuts = [n * i // k for i in range(k + 1)]
+    if k == 1:
+        np.copyto(dst, src)
+    else:
+        list(_pool().map(lambda i: np.copyto(dst[cuts[i]:cuts[i + 1]], src[cuts[i]:cuts[i + 1]]), range(k)))
+    return h.to(device, non_blocking=True)
+
+
 def as_device_scene(scene, device=None) -> tuple[DeviceScene, bool]:
     """(device scene, was_host).  Host scenes keep float64 on device so the
     FP64 key chain sees the caller's exact values."""
@@ -95,4 +126,6 @@ def as_device_scene(scene, device=None) -> tuple[DeviceScene, bool]:
         dt = pos.dtype if pos.dtype in (torch.float32, torch.float64) else torch.float64
         return DeviceScene(*(getattr(scene, g).reshape(-1, w).to(dt).contiguous() for g, w in GROUPS)), False
     dev = device or torch.device("cuda", torch.cuda.current_device())
-    return DeviceScene.from_host(scene, dtype=torch.float64, device=dev), True
+    if isinstance(pos, torch.Tensor):
+        return DeviceScene.from_host(scene, dtype=torch.float64, device=dev), True
+    return DeviceScene(*(upload_f64(np.reshape(getattr(scene, g), (-1, w)), dev) for g, w in GROUPS)), True

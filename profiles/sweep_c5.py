@@ -1,12 +1,18 @@
 """BASELINE.json configs[4] / SURVEY.md §8d c5: backward-stress sweep.
 
 c4 layout (16 tanks) with N in {10k, 100k, 1M, 4M} Gaussians and isotropic
-scales sigma in {0.03, 0.1, 0.3} m (log_scales overridden), 512x512, el 45°,
-8 views per step (one batch).  For each point: member pairs per Gaussian,
-(tile, Gaussian) pairs, views/s of forward + backward (CUDA events over a
-captured step), and a size-independent check: the step's gradients are
-finite and the visible counts equal the number of views that kept each
-Gaussian.  Points whose member pairs exceed ~1e9 are skipped.
+scales sigma in {0.03, 0.1, 0.3, 1.0} m (log_scales overridden), 512x512,
+el 45°, 8 views per step (one batch).  For each point: member pairs per
+Gaussian, (tile, Gaussian) pairs, views/s of forward + backward (CUDA
+events over a captured step), and size-independent checks: the gradients
+are finite, the visible counts lie in [0, V], two replays of the step are
+bitwise identical (deterministic reductions), and the backward is exactly
+linear -- dL/dS scaled by 2 gives exactly twice every gradient (power-of-two
+scaling commutes with every FP64/FP32 rounding on the backward path; the
+only exception, counted separately, is float32 subnormal output).
+Points whose member pairs exceed ~1e9 are skipped; the 10k
+sigma = 1.0 point is also checked against the oracle in
+tests/test_gpu_headline.py.
 
     python profiles/sweep_c5.py > gpurun_out/c5.json
 """
@@ -30,14 +36,14 @@ cfgs = [c for c in bench.view_list(512) if c.elevation_deg == 45.0][::15][:V]
 rows = []
 for n in (10_000, 100_000, 1_000_000, 4_000_000):
     base = bench.make_scene(n)
-    for sigma in (0.03, 0.1, 0.3):
+    for sigma in (0.03, 0.1, 0.3, 1.0):
         est = 9 * math.pi * (sigma ** 2 / 0.09 + 0.3)          # member cells per Gaussian
         if est * n > 1.0e9:
             rows.append({"n": n, "sigma": sigma, "skipped": f"~{est * n:.2e} member pairs"})
             continue
         base.log_scales[:] = math.log(sigma)
         ds = sdgr.DeviceScene.from_host(base, dtype=torch.float32)
-        lanes = 8 if est * n < 2e8 else 2
+        lanes = 8 if est * n < 2e8 else 2     # lanes hold one view's walk scratch each
         step = MultiViewStep(ds, cfgs, lanes=lanes)
         step.calibrate()
         dl = torch.randn((V, 512, 512), dtype=torch.float64, device="cuda",
@@ -56,13 +62,28 @@ for n in (10_000, 100_000, 1_000_000, 4_000_000):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         step.check()
+        first = step.flat_soa.clone()
+        step.graph_step()
+        deterministic = bool(torch.equal(step.flat_soa, first))
+        dl.mul_(2.0)                       # the graph reads dl in place
+        step.graph_step()
+        a, b = step.flat_soa[: 29 * step.n], 2.0 * first[: 29 * step.n]
+        # float32 subnormal outputs (|g| < 2^-126, deep occluded pairs) round on
+        # a fixed 2^-149 grid, where 2 x round(v) and round(2 v) can differ
+        off = (a != b) & (b.abs() >= 2.0 ** -125)
+        linear = not bool(off.any())
+        n_subnormal_diff = int(((a != b) & ~off).sum())
+        dl.mul_(0.5)
+        step.graph_step()
         g = step.grads
         finite = all(bool(torch.isfinite(getattr(g, k)).all()) for k in
                      ("positions", "rotations", "log_scales", "sh_coeffs", "ke_raw", "uv_grad_norm"))
         vis_ok = bool((g.visible >= 0).all() and (g.visible <= V).all())
         rows.append({"n": n, "sigma": sigma, "member_pairs_per_gaussian": float(step.calib_tc) / n,
                      "t16_per_view": step.calib_t16_mean[0], "lanes": lanes, "ms_per_step": ms,
-                     "views_per_s": V / (ms / 1e3), "grads_finite": finite, "visible_in_range": vis_ok})
+                     "views_per_s": V / (ms / 1e3), "grads_finite": finite, "visible_in_range": vis_ok,
+                     "replay_bitwise_deterministic": deterministic, "backward_exactly_linear": linear,
+                     "subnormal_only_differences": n_subnormal_diff})
         print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
         del step, ds
         torch.cuda.empty_cache()

@@ -138,3 +138,13 @@ def c3_scene():
 def test_c3_dropin_vs_oracle(c3_scene, az, el):
     """Single 300k tank at 256x256: the deepest tile lists."""
     dropin_vs_oracle(c3_scene, c4_config(az, el, size=256), ("c3", az, el), seed=100 + int(el))
+
+
+def test_c5_large_footprints_vs_oracle():
+    """SURVEY §8d c5 at sigma = 1.0 m (~320 member cells per Gaussian): every
+    footprint is wider than the 8x8 cell window, so K1's tile test, the
+    walks' member masks and the splat run their exact FP64 per-cell loops."""
+    scene = targets.tank_grid(10_000)
+    scene.log_scales[:] = np.log(1.0)
+    scene = targets.to_float32_exact(scene)
+    dropin_vs_oracle(scene, c4_config(150.0, 45.0), ("c5", 1.0), seed=5)

@@ -500,3 +500,41 @@ def test_host_callers_get_float64_gradients():
     ds = sdgr.DeviceScene.from_host(scene, dtype=torch.float32)
     gd = sdgr.backward(sdgr.render_forward(ds, cfg), torch.ones((24, 24), device="cuda"))
     assert gd.positions.dtype == torch.float32 and gd.positions.is_cuda
+
+
+@pytest.mark.parametrize("case", ["equal_depths", "depth_outlier"])
+def test_depth_order_long_runs(case):
+    """runs of equal 24-bit depth keys longer than k_fix_runs'
+    per-thread window (many Gaussians at one depth, or one far outlier along
+    the line of sight squeezing every other depth into a few buckets) are
+    sorted by the block-serial radix pass -- exact (depth, index) order, and
+    the full pipeline still matches the oracle."""
+    import ctypes as C
+
+    from paper_2506_21633_b200 import _lib
+    from paper_2506_21633_b200.radar import radar_rotation
+
+    rng = np.random.default_rng(41)
+    base = targets.random_scene(rng, 400, spread=2.0, scale_low=0.2, scale_high=0.5)
+    cfg = sdgr.RadarConfig(azimuth_deg=25.0, elevation_deg=45.0, altitude_m=2.0, range_res_m=0.25,
+                           azimuth_res_m=0.25, n_range=48, n_azimuth=48)
+    R = radar_rotation(cfg.azimuth_deg, cfg.elevation_deg)
+    if case == "equal_depths":
+        # 300 Gaussians share one depth: spread only across the radar's x / y axes
+        t = rng.uniform(-2, 2, size=(300, 2))
+        base.positions[:300] = base.positions[0] + t[:, :1] * R[0] + t[:, 1:] * R[1]
+    else:
+        base.positions[7] = base.positions[7] + 1.0e5 * R[2]   # same pixel, 100 km deeper
+    proj = sdgr.project_all(base, cfg)
+    n = proj.n_scene
+    lib = _lib.lib()
+    ws_bytes = lib.sdgr_workspace_bytes(n, 1)
+    ws = torch.empty((ws_bytes,), dtype=torch.uint8, device="cuda")
+    order = torch.empty((n,), dtype=torch.int32, device="cuda")
+    assert lib.sdgr_depth_order(C.byref(proj.desc()), order.data_ptr(), ws.data_ptr(), ws_bytes, None) == 0
+    vis = ((proj.flags & _lib.FLAG_VISIBLE) != 0).cpu().numpy()
+    depth = decode_depth(proj.depth_key).cpu().numpy()
+    idx = np.nonzero(vis)[0]
+    want = idx[np.lexsort((idx, depth[idx]))]
+    assert np.array_equal(order.cpu().numpy()[: idx.size], want)
+    _oracle_compare(base, cfg, 3.0, seed=41)

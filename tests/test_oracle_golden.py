@@ -97,3 +97,13 @@ def test_forward_known_answers():
     assert it.intensity[0] == pytest.approx(1.0 - np.exp(-1.0), abs=1e-9)
     assert it.intensity[1] == pytest.approx((1.0 - np.exp(-1.0)) * np.exp(-1.0), abs=1e-9)
     del Scene
+
+
+def test_naive_oracle_matches_golden_dense():
+    """The naive loop renderer (render_reference restatement) reproduces the
+    reference's dense-mode goldens (cutoff = inf), like criterion 2."""
+    from oracle import sdgr_oracle as O
+    for path in [p for p in GOLDEN if p.stem.endswith("_dense")]:
+        z, scene, cfg, cutoff = load_golden(path)
+        img = O.render_reference(scene, cfg)
+        assert np.abs(img - z["image"]).max() <= 1e-10 * max(1.0, float(z["image"].max())), path.stem
