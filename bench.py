@@ -341,13 +341,17 @@ def _profile(lib):
 
 
 def ncu_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture summary."""
+    """DRAM bytes per launch of `kernel` and its compute-side counters from
+    the committed ncu capture summary (profiles/ncu_traffic.json)."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
-        return None, None
+        return None, None, None
     d = json.loads(p.read_text())
     e = d.get("kernels", {}).get(kernel)
-    return (e["dram_bytes_per_launch"], d.get("source")) if e else (None, None)
+    return (e["dram_bytes_per_launch"], d.get("source"), e.get("compute")) if e else (None, None, None)
+
+
+COMPOSITING = ("k_segsum", "k_walk<kContrib>", "k_replay<kGSum>", "k_replay<kGrad>")
 
 
 def dropin_rate(sdgr, host_scene, cfgs, views: int, world: int, rank: int) -> dict:
@@ -536,8 +540,20 @@ def run_sdgr(args):
     dom_per_step = dom_cnt[dom]
     bpl = kernel_bytes(dom, args.n, t16_pv, live_pv, items_pv, batch)
     achieved = bpl / (launch_ms / 1e3) / 1e9 if launch_ms > 0 else None
-    traffic, traffic_src = ncu_traffic(L.KERNEL_NAMES[dom])
+    traffic, traffic_src, dom_compute = ncu_traffic(L.KERNEL_NAMES[dom])
     step_ms_all = sum(prof_ms)
+    # compute-side view of the compositing kernels: not HBM-shaped
+    # work -- member / live pairs per second and the ncu pipe utilisation
+    comp_ms = {nm: prof_ms[k] / V for k, nm in L.KERNEL_NAMES.items() if nm in COMPOSITING}
+    compute_roofline = {
+        "what": "compositing is latency / issue bound, not HBM bound: pairs per second and pipe utilisation",
+        "member_pairs_per_view": float(step.calib_tc_mean) if hasattr(step, "calib_tc_mean") else None,
+        "live_pairs_per_view": live_pv,
+        "forward_ms_per_view": comp_ms.get("k_segsum", 0) + comp_ms.get("k_walk<kContrib>", 0),
+        "backward_ms_per_view": comp_ms.get("k_replay<kGSum>", 0) + comp_ms.get("k_replay<kGrad>", 0),
+        "live_pairs_per_s_fwd_bwd": live_pv / ((sum(comp_ms.values())) / 1e3) if sum(comp_ms.values()) else None,
+        "ncu": {nm: ncu_traffic(nm)[2] for nm in COMPOSITING},
+        "fp64_peak_tflops": 37.0, "fp64_peak_source": "B200 datasheet FP64 (vector) -- not measured here"}
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": L.KERNEL_NAMES[dom], "bytes_per_launch": bpl, "launch_ms": launch_ms,
@@ -548,6 +564,7 @@ def run_sdgr(args):
                 "kernel_ms_per_step": {L.KERNEL_NAMES[k]: round(prof_ms[k], 3) for k in L.KERNEL_NAMES},
                 "per_view": {"t16": t16_pv, "live_pairs": live_pv, "items": items_pv},
                 "traffic_source": traffic_src,
+                "compute": dom_compute,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6.65 TB/s"}
 
     line = {
@@ -563,6 +580,7 @@ def run_sdgr(args):
         "roofline": roofline,
         "stage_ms_per_step_single_stream": stages,
         "preprocess_sort_roofline": preprocess_sort_roofline(args.n, step, stages, V, peak),
+        "compute_roofline": compute_roofline,
         "gpu_launches": int(launches),
         "e2e": e2e,
         "e2e_dropin": dropin,

@@ -259,6 +259,7 @@ int sdgr_composite_forward(const sdgr_view* view, const sdgr_projection* proj, c
 int sdgr_splat(const sdgr_view* view, const sdgr_projection* proj, const double* intensity, void* scratch,
                double* image, void* stream) {
   if (!view_ok(view) || !proj || !intensity || !image || !scratch) return SDGR_ERR_INVALID;
+  if (!proj->img.uv || !proj->img.inv_cov || !proj->img.bbox || !proj->img.cell_mask) return SDGR_ERR_INVALID;
   return launch_splat(*view, *proj, intensity, static_cast<double*>(scratch), image,
                       static_cast<cudaStream_t>(stream));
 }

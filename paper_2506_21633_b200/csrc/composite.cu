@@ -263,18 +263,24 @@ __device__ __forceinline__ void splat_add(unsigned long long* acc, int n_az, int
   atomicAdd(acc + (int64_t)iv * n_az + iu, splat_fix(exp(-q) * I, scale));
 }
 
-// max_g I_g over visible Gaussians as u64 bits (I >= 0: the bit order is the value order)
+// max_g I_g over visible Gaussians as u64 bits (I >= 0: the bit order is the
+// value order); grid-stride, one atomic per block
 __global__ void __launch_bounds__(256) k_max_intensity(const uint8_t* flags, const double* intensity, int64_t n,
                                                        unsigned long long* max_bits) {
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ unsigned long long s_max[8];
   unsigned long long b = 0ull;
-  if (g < n && (flags[g] & SDGR_FLAG_VISIBLE)) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
     const double I = intensity[g];
-    b = (I > 0.0 && isfinite(I)) ? (unsigned long long)__double_as_longlong(I) : 0ull;
+    if ((flags[g] & SDGR_FLAG_VISIBLE) && I > 0.0 && isfinite(I)) b = max(b, (unsigned long long)__double_as_longlong(I));
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) b = max(b, __shfl_down_sync(0xffffffffu, b, off));
-  if ((threadIdx.x & 31) == 0 && b) atomicMax(max_bits, b);
+  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) b = max(b, s_max[w]);
+    if (b) atomicMax(max_bits, b);
+  }
 }
 
 __global__ void __launch_bounds__(256) k_splat(sdgr_view view, sdgr_plane pl, const uint8_t* flags,
@@ -1195,7 +1201,8 @@ int launch_splat(const sdgr_view& v, const sdgr_projection& p, const double* int
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(part);
   if (cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * (npix + 1), st) != cudaSuccess) return SDGR_ERR_CUDA;
   const unsigned gb = (unsigned)((p.n + 255) / 256);
-  k_max_intensity<<<gb, 256, 0, st>>>(p.flags, intensity, p.n, acc + npix);
+  k_max_intensity<<<std::min<unsigned>(gb, 2u * (unsigned)sm_count()), 256, 0, st>>>(p.flags, intensity, p.n,
+                                                                                     acc + npix);
   {
     KernelTimer kt(SDGR_K_SPLAT, st);
     k_splat<<<gb, 256, 0, st>>>(v, p.img, p.flags, intensity, p.n, acc, acc + npix);

@@ -57,9 +57,11 @@ __device__ __forceinline__ unsigned long long emit_bbox(int x0, int x1, int y0, 
 __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double v,
                                 double c00, double c01, double c11, double ru, double rv, int nu, int nv,
                                 double cutoff, bool dense, double4& rec_out) {
-  // invert_cov2d (forward.py:33-42)
+  // invert_cov2d (forward.py:33-42): three divisions by det through one
+  // correctly rounded reciprocal (bit-identical to c / det)
   double det = dsub(dmul(c00, c11), dmul(c01, c01));
-  double a00 = ddiv(c11, det), a01 = ddiv(-c01, det), a11 = ddiv(c00, det);
+  const double rdet = __drcp_rn(det);
+  double a00 = ddiv_rcp(c11, det, rdet), a01 = ddiv_rcp(-c01, det, rdet), a11 = ddiv_rcp(c00, det, rdet);
   rec_out = make_double4(a00, a01, a11, 0.0);
   if (pl.uv) reinterpret_cast<double2*>(pl.uv)[g] = make_double2(u, v);
   reinterpret_cast<double4*>(pl.inv_cov)[g] = make_double4(a00, a01, a11, 0.0);
@@ -170,8 +172,36 @@ __device__ void plane_empty(const sdgr_plane& pl, int64_t g) {
 struct ProjBatch {
   sdgr_view view[SDGR_MAX_BATCH];
   sdgr_projection proj[SDGR_MAX_BATCH];
+  double rden_u[SDGR_MAX_BATCH], rden_v[SDGR_MAX_BATCH];   // RN(1 / den), host IEEE divisions
   int nv;
+  int zero_col2;   // every view has mc[0][2] == mi[0][2] == 0 (R[0][2] = 0, geometry.py:41-47)
 };
+
+// One plane's covariance sandwich m Sigma m^T (geometry.py:269-272): per
+// entry (a, d) the sequential sum over (b, c) of (m[a,b] Sigma[b,c]) m[d,c]
+// (np.einsum's order, no FMA).  kZero: row 0 of m has m[0][2] == 0, so the
+// 22 terms with (a = 0, b = 2) or (d = 0, c = 2) are exactly +-0 (Sigma
+// finite) and adding them changes no bit of a non-zero sum -- skipped.
+template <bool kZero>
+__device__ __forceinline__ void sandwich(const double* m, const double* Cm, double* out) {
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      double acc = 0.0;
+      bool first = true;
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (kZero && ((a == 0 && b == 2) || (d == 0 && c == 2))) continue;
+          const double t = dmul(dmul(m[3 * a + b], Cm[3 * b + c]), m[3 * d + c]);
+          acc = first ? t : dadd(acc, t);
+          first = false;
+        }
+      out[2 * a + d] = acc;
+    }
+}
 
 // One thread per Gaussian, looping over the batch's views: the parameters
 // are read once and the view-independent half of project_all -- quaternion
@@ -270,9 +300,9 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
       for (int i = 0; i < 3; ++i)
         xr[i] = dadd(dfma(p2, R[3 * i + 2], dfma(p1, R[3 * i + 1], dmul(p0, R[3 * i]))), view.T[i]);
       // plane coordinates (geometry.py:78-105) and ndc_to_pixel (:73-75)
-      const double undc = ddiv(dmul(2.0, xr[0]), view.den_u);
-      const double vcndc = ddiv(dmul(2.0, xr[1]), view.den_v);
-      const double vindc = dsub(ddiv(dmul(2.0, xr[2]), view.den_v), view.off_vi);
+      const double undc = ddiv_rcp(dmul(2.0, xr[0]), view.den_u, B.rden_u[k]);
+      const double vcndc = ddiv_rcp(dmul(2.0, xr[1]), view.den_v, B.rden_v[k]);
+      const double vindc = dsub(ddiv_rcp(dmul(2.0, xr[2]), view.den_v, B.rden_v[k]), view.off_vi);
       const double uc = dsub(dmul(dmul(dadd(undc, 1.0), 0.5), (double)view.n_u), 0.5);
       const double vc = dsub(dmul(dmul(dadd(vcndc, 1.0), 0.5), (double)view.n_v), 0.5);
       const double ui = dsub(dmul(dmul(dadd(undc, 1.0), 0.5), (double)view.n_az), 0.5);
@@ -281,23 +311,15 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
 
       // sandwich mc C mc^T (geometry.py:269-278): sequential over (b, c)
       double cc[4], ci[4];
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int d = 0; d < 2; ++d) {
-          double accc = 0.0, acci = 0.0;
-#pragma unroll
-          for (int b = 0; b < 3; ++b)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              const double tc = dmul(dmul(view.mc[3 * a + b], Cm[3 * b + c]), view.mc[3 * d + c]);
-              const double ti = dmul(dmul(view.mi[3 * a + b], Cm[3 * b + c]), view.mi[3 * d + c]);
-              accc = (b == 0 && c == 0) ? tc : dadd(accc, tc);
-              acci = (b == 0 && c == 0) ? ti : dadd(acci, ti);
-            }
-          cc[2 * a + d] = accc;
-          ci[2 * a + d] = acci;
-        }
+      const bool sig_fin = isfinite(Cm[0]) && isfinite(Cm[1]) && isfinite(Cm[2]) && isfinite(Cm[4]) &&
+                           isfinite(Cm[5]) && isfinite(Cm[8]);
+      if (B.zero_col2 && sig_fin) {
+        sandwich<true>(view.mc, Cm, cc);
+        sandwich<true>(view.mi, Cm, ci);
+      } else {
+        sandwich<false>(view.mc, Cm, cc);
+        sandwich<false>(view.mi, Cm, ci);
+      }
       const double cc00 = dadd(cc[0], view.cov_reg), cc11 = dadd(cc[3], view.cov_reg);
       const double cc01 = dmul(0.5, dadd(cc[1], cc[2]));
       const double ci00 = dadd(ci[0], view.cov_reg), ci11 = dadd(ci[3], view.cov_reg);
@@ -480,9 +502,13 @@ int launch_project(const sdgr_scene& scene, int nv, const sdgr_view* views, sdgr
   if (scene.n <= 0 || nv < 1 || nv > SDGR_MAX_BATCH) return SDGR_ERR_INVALID;
   ProjBatch B;
   B.nv = nv;
+  B.zero_col2 = 1;
   for (int k = 0; k < nv; ++k) {
     B.view[k] = views[k];
     B.proj[k] = projs[k];
+    B.rden_u[k] = 1.0 / views[k].den_u;   // host IEEE division: RN(1 / den)
+    B.rden_v[k] = 1.0 / views[k].den_v;
+    if (views[k].mc[2] != 0.0 || views[k].mi[2] != 0.0) B.zero_col2 = 0;
   }
   k_project_init<<<1, 4 * SDGR_MAX_BATCH, 0, stream>>>(B);
   const int threads = 256;

@@ -269,6 +269,7 @@ class MultiViewStep:
         ws = _empty((ws_bytes,), torch.uint8, self.dev)
         off = {pl: _empty((self.n + 1,), torch.int32, self.dev) for pl in (0, 1)}
         self.calib_t16 = []
+        self.calib_tc_all = []
         for v in self.views:
             _check(self.lib.sdgr_project(C.byref(self.sd), C.byref(v), C.byref(self.pd), st), "sdgr_project")
             _check(self.lib.sdgr_depth_order(C.byref(self.pd), ptr(self.order), ptr(ws), ws_bytes, st),
@@ -279,10 +280,12 @@ class MultiViewStep:
             tot = torch.cat([torch.stack([off[0][self.n], off[1][self.n]]).to(torch.int64),
                              self.member_pairs]).cpu().tolist()
             self.calib_tc = max(getattr(self, "calib_tc", 0), tot[2])
+            self.calib_tc_all.append(tot[2])
             tot = tot[:2]
             mx = {0: max(mx[0], tot[0]), 1: max(mx[1], tot[1])}
             self.calib_t16.append(tot)
         self.calib_t16_mean = {pl: float(np.mean([t[pl] for t in self.calib_t16])) for pl in (0, 1)}
+        self.calib_tc_mean = float(np.mean(self.calib_tc_all))
         self._alloc_planes({pl: int(mx[pl] * self.headroom) + 1024 for pl in (0, 1)})
         return mx
 

@@ -79,6 +79,11 @@ def dropin_vs_oracle(scene, cfg, key, seed):
     p = fwd.projection
     assert np.array_equal(npa(p.indices), fo.proj.indices)
     assert p.n_culled == fo.proj.n_culled and p.n_skipped == fo.proj.n_skipped
+    # the FP64 key chain on every visible Gaussian: pixel centres and depth
+    # bit-identical to the reference's arithmetic (none of them involves exp)
+    assert np.array_equal(npa(p.uv_comp), fo.proj.uv_comp), key
+    assert np.array_equal(npa(p.uv_img), fo.proj.uv_img), key
+    assert np.array_equal(npa(p.depth), fo.proj.depth), key
     check_tiles(fwd.rays, fo, 0, f"{key} comp tiles")
     check_tiles(fwd.splat, fo, 1, f"{key} img tiles")
     assert_close(npa(fwd.intensities.intensity), fo.inten.intensity, what=f"{key} intensity")
