@@ -230,6 +230,13 @@ int sdgr_max_batch(void);
 #define SDGR_K_GEOMETRY 11    /* per-Gaussian chain rule (batched) */
 int sdgr_profile_begin(uint32_t kernel_mask);
 int sdgr_profile_end(double* ms, int64_t* launches);
+/* Before sdgr_profile_end: the recorded launches as a timeline -- kernel id
+ * (SDGR_K_*) and the begin / end event times (ms) relative to the first
+ * recorded begin, up to cap entries; returns the count (negative status on
+ * error).  Events are stream-ordered markers: begin fires when the launch
+ * stream reaches the kernel, so with concurrent streams [begin, end] is the
+ * span from "ready" to "done". */
+int sdgr_profile_timeline(int cap, int32_t* ids, double* t0_ms, double* t1_ms);
 /* Bytes of scratch the binning calls need for n Gaussians / max pairs. */
 size_t sdgr_workspace_bytes(int64_t n, int64_t max_pairs);
 /* ... and the batched calls for n_views (1..SDGR_MAX_BATCH) views (0 if n_views is out of range). */

@@ -101,6 +101,7 @@ SIGNATURES = [
     ("sdgr_workspace_bytes", C.c_size_t, [C.c_int64, C.c_int64]),
     ("sdgr_profile_begin", C.c_int, [C.c_uint32]),
     ("sdgr_profile_end", C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    ("sdgr_profile_timeline", C.c_int, [C.c_int, _p, _p, _p]),
     ("sdgr_project", C.c_int, [C.POINTER(SceneDesc), C.POINTER(View), C.POINTER(ProjectionDesc), _p]),
     ("sdgr_depth_order", C.c_int, [C.POINTER(ProjectionDesc), _p, _p, C.c_size_t, _p]),
     ("sdgr_count_pairs", C.c_int, [C.POINTER(ProjectionDesc), C.c_int32, _p, _p, _p, C.c_size_t, _p]),

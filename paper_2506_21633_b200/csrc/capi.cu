@@ -163,6 +163,23 @@ int sdgr_profile_end(double* ms, int64_t* launches) {
   return SDGR_OK;
 }
 
+int sdgr_profile_timeline(int cap, int32_t* ids, double* t0_ms, double* t1_ms) {
+  if (cap < 0 || (cap > 0 && (!ids || !t0_ms || !t1_ms))) return -SDGR_ERR_INVALID;
+  if (g_prof_n == 0) return 0;
+  if (cudaEventSynchronize(g_prof_ev[2 * g_prof_n - 1]) != cudaSuccess) return -SDGR_ERR_CUDA;
+  const int n = g_prof_n < cap ? g_prof_n : cap;
+  for (int i = 0; i < n; ++i) {
+    float a = 0.f, b = 0.f;
+    if (cudaEventElapsedTime(&a, g_prof_ev[0], g_prof_ev[2 * i]) != cudaSuccess ||
+        cudaEventElapsedTime(&b, g_prof_ev[0], g_prof_ev[2 * i + 1]) != cudaSuccess)
+      return -SDGR_ERR_CUDA;
+    ids[i] = g_prof_id[i];
+    t0_ms[i] = a;
+    t1_ms[i] = b;
+  }
+  return n;
+}
+
 size_t sdgr_workspace_bytes(int64_t n, int64_t max_pairs) {
   return sdgr_batch_workspace_bytes(n, max_pairs, 1);
 }

@@ -283,6 +283,23 @@ def test_multiview_step_equals_sum_of_views(geo_batch):
     check_step_vs_oracle(got, *oracle_sum(tank, cfgs, dl))
 
 
+def test_multiview_batch_ramp_vs_oracle():
+    """A step whose batches ramp up (2, 6, 2 views with 8-view batches: three
+    batches over both slot sets) equals the oracle's sum over its views."""
+    from paper_2506_21633_b200.multiview import MultiViewStep
+
+    tank = targets.to_float32_exact(targets.composite_target(targets.tank_preset(), [2000, 1000, 500], seed=7))
+    cfgs = [sdgr.RadarConfig(azimuth_deg=float(az), elevation_deg=el, altitude_m=0.5, n_range=80, n_azimuth=80)
+            for az, el in zip(range(0, 360, 36), (30.0, 45.0, 60.0) * 4)]
+    ds = sdgr.DeviceScene.from_host(tank, dtype=torch.float32)
+    step = MultiViewStep(ds, cfgs, geo_batch=8, ramp=2)
+    assert step.batches == [2, 6, 2]
+    dl = torch.randn((len(cfgs), 80, 80), dtype=torch.float64, device="cuda",
+                     generator=torch.Generator("cuda").manual_seed(8))
+    got = step.run(dl)
+    check_step_vs_oracle(got, *oracle_sum(tank, cfgs, dl))
+
+
 def test_multiview_graph_replay_equals_run():
     """The captured CUDA graph of a step reproduces run() bitwise, and reads
     its static inputs in place (new dL/dS values are picked up on replay)."""
