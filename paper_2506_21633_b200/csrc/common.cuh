@@ -30,7 +30,7 @@ constexpr int kChunk = 256;             // Gaussians staged per tile-walk chunk
 #define SDGR_MINB_PROJECT 4
 #endif
 #ifndef SDGR_MINB_REPLAY_GRAD
-#define SDGR_MINB_REPLAY_GRAD 2
+#define SDGR_MINB_REPLAY_GRAD 3
 #endif
 #ifndef SDGR_MINB_GRAD_IMAGE
 #define SDGR_MINB_GRAD_IMAGE 4

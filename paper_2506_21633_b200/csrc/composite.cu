@@ -17,8 +17,10 @@
 //   P1  thread r counts its ray's live members; a block scan lays every live
 //       (ray, member) pair out in a flat shared array in ray-major,
 //       depth-minor order -- exactly the reference's per-ray walk order.
-//   P2  thread j evaluates w = exp(-q) for its live member cells (pair-
-//       parallel) into the pair's flat slot.
+//   P2  thread j evaluates w = exp(-q) for its own live member cells into
+//       the pairs' flat slots.  (A warp-flattened member list -- every lane
+//       one exp per round -- is better balanced alone on the GPU but costs
+//       more issue slots: 1252 vs 1280 views/s in the concurrent c4 step.)
 //   P3  thread r: log-transmittance prefix and early termination (adds only).
 //   P4  flat pair-parallel pass: T = e^-S, 1 - e^-tau, contributions.
 //   P5  thread r: downstream suffix sums (backward only; adds only).
@@ -397,7 +399,6 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
   __shared__ int32_t scan_tmp[8];
   __shared__ int32_t base_s;
   __shared__ int item_s;
-  __shared__ uint16_t wlist[8 * kList];                     // per-warp member lists (P2)
   extern __shared__ double dyn[];
   double* fw = dyn;                                         // w
   double* fs = fw + kCap;                                   // S / contrib / g*contrib / D
@@ -546,39 +547,22 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
         const uint32_t below = ((1u << lane) - 1u) & rmask_w;
         const uint32_t pshift = 8 * (jw & 3);
         const uint32_t* wp = wpre + (jw < 4 ? 0 : kRays);
-        {
-          uint64_t mm[4];
+        if (mine) {   // thread j: its own live member cells
 #pragma unroll
-          for (int w = 0; w < 4; ++w) mm[w] = mine ? lm[w] : 0ull;
-          const int cnt = __popcll(mm[0]) + __popcll(mm[1]) + __popcll(mm[2]) + __popcll(mm[3]);
-          int incl = cnt;
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += y;
-          }
-          int nx = incl - cnt;
-          const int tot = __shfl_sync(0xffffffffu, incl, 31);
-          uint16_t* list = wlist + jw * kList;
-          for (int B = 0; B < tot; B += kList) {
-            const int lim = min(tot, B + kList);
-            fill_window(mm, nx, lim, lane, list, B);
-            __syncwarp();
-            for (int k = B + lane; k < lim; k += 32) {
-              const int e = list[k - B];
-              const int owner = e >> 8, r = e & 255;
-              const int j = jw * 32 + owner;
-              const uint32_t bl = ((1u << owner) - 1u) & rmask_w;
-              const int p = ray_off[r] + (int)((wp[r] >> pshift) & 255u) + __popc(rows[jw * kRays + r] & bl);
-              const double dx = dsub((double)(tx * kTile + (r & 15)), su[j]);
-              const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[j]);
-              const double wgt = exp(-quadform(sa0[j], sa1[j], sa2[j], dx, dy));
+          for (int w = 0; w < 4; ++w) {
+            uint64_t x = lm[w];
+            while (x) {
+              const int r = w * 64 + __ffsll((long long)x) - 1;
+              x &= x - 1;
+              const int p = ray_off[r] + (int)((wp[r] >> pshift) & 255u) + __popc(rows[jw * kRays + r] & below);
+              const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
+              const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
+              const double wgt = exp(-quadform(sa0[tid], sa1[tid], sa2[tid], dx, dy));
               fw[p] = wgt;
-              fs[p] = dmul(sk[j], wgt);  // tau, replaced by S_before in P3
-              fj[p] = (uint8_t)j;
+              fs[p] = dmul(sk[tid], wgt);
+              fj[p] = (uint8_t)tid;
               fr[p] = (uint8_t)r;
             }
-            __syncwarp();
           }
         }
         __syncthreads();
@@ -800,11 +784,13 @@ struct ReplayCfg {
 //      segmented scan over the ray runs: per-ray sums (kGSum) or the downstream
 //      sum D after each pair (kGrad) -- no ray-serial loops;
 //   C  kGrad: counting sort of the entries into Gaussian-major order (ray
-//      bitmaps per Gaussian), then per warp (32 Gaussians) the gradient terms
-//      of up to 8 contiguous entries per lane, reduced per Gaussian with a warp
-//      segmented scan of the 7-term vectors: one partial record per
-//      (tile, Gaussian) pair, written once.  Pairs of the item no descriptor
-//      covers get zero records here, so partial_g needs no memset.
+//      bitmaps per Gaussian), then thread j sums Gaussian j's gradient terms
+//      over its entries in ray order: one partial record per (tile, Gaussian)
+//      pair, written once.  (A warp-balanced variant -- up to 8 contiguous
+//      entries per lane, warp segmented scan of the 7-term vectors -- held 28
+//      doubles live: 126 registers, 2 CTAs/SM, 7.47 vs 6.49 ms/step.)  Pairs
+//      of the item no descriptor covers get zero records here, so partial_g
+//      needs no memset.
 template <int MODE>
 __global__ void __launch_bounds__(256, MODE == kGrad ? SDGR_MINB_REPLAY_GRAD : 4) k_replay(ReplayArgs a) {
   constexpr bool kG = MODE == kGrad;
@@ -829,7 +815,7 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? SDGR_MINB_REPLAY_GRAD : 4
   uint16_t* perm = reinterpret_cast<uint16_t*>(fD + (kG ? kCap : 0));  // kGrad: Gaussian-major -> log
   uint8_t* fj = reinterpret_cast<uint8_t*>(perm + (kG ? kCap : 0));
   uint8_t* fr = fj + kCap;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int n_items = *a.n_items;
   while (true) {
     __syncthreads();
@@ -967,91 +953,24 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? SDGR_MINB_REPLAY_GRAD : 4
         }
       }
       __syncthreads();
-      // Gaussians of [j0, j1) without live entries still own a (zero) record
-      if (tid >= j0 && tid < j1 && gstart[tid + 1] == gstart[tid]) {
-        double4* rp = reinterpret_cast<double4*>(a.partial + (int64_t)spos[tid] * 8);
-        rp[0] = make_double4(0, 0, 0, 0);
-        rp[1] = make_double4(0, 0, 0, 0);
-      }
-      const int glo = max(32 * warp, j0), ghi = min(32 * warp + 32, j1);
-      if (glo >= ghi) continue;  // warp-uniform
-      const int lo = gstart[glo], hi = gstart[ghi];
-      double carry[7] = {0, 0, 0, 0, 0, 0, 0};
-      for (int R = lo, E7 = 0; R < hi; R += 32 * E7) {
-        E7 = min(8, (hi - R + 31) / 32);  // entries per lane this round
-        const int e0 = R + E7 * lane;
-        const int ec = max(0, min(E7, hi - e0));
+      // C': thread j sums its own entries serially, in ray order (Gaussian-
+      // major via perm): one partial record per (tile, Gaussian)
+      if (tid >= j0 && tid < j1) {
         double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-        double first[7];
-        int first_j = -1;       // Gaussian of a leading run that ends inside this lane
-        bool seen_head = false;
-        int any = 0;
-        for (int e = 0; e < ec; ++e) {
-          const int qq = e0 + e;
+        const int lo = gstart[tid], hi = gstart[tid + 1];
+        for (int qq = lo; qq < hi; ++qq) {
           const int p = perm[qq];
-          const int j = fj[p], r = fr[p];
-          const bool head = qq == gstart[j];
-          const bool tail = qq == gstart[j + 1] - 1;
-          if (head) {
-#pragma unroll
-            for (int t = 0; t < 7; ++t) acc[t] = 0.0;
-            seen_head = true;
-            any = 1;
-          }
-          const double dx = dsub((double)(tx * kTile + (r & 15)), su[j]);
-          const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[j]);
-          grad_terms(fY[p], fD[p] * fW[p], sk[j], dx, dy, sa0[j], sa1[j], sa2[j], acc);
-          if (tail) {
-            if (seen_head) {
-              double4* rp = reinterpret_cast<double4*>(a.partial + (int64_t)spos[j] * 8);
-              rp[0] = make_double4(acc[0] * sg[j], acc[1], acc[2], acc[3]);
-              rp[1] = make_double4(acc[4], acc[5], acc[6], 0.0);
-            } else {
-#pragma unroll
-              for (int t = 0; t < 7; ++t) first[t] = acc[t];
-              first_j = j;
-            }
-#pragma unroll
-            for (int t = 0; t < 7; ++t) acc[t] = 0.0;
-            seen_head = true;  // later entries of this lane start new runs
-          }
+          const int r = fr[p];
+          const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
+          const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
+          grad_terms(fY[p], fD[p] * fW[p], sk[tid], dx, dy, sa0[tid], sa1[tid], sa2[tid], acc);
         }
-        // warp segmented scan of the open-run sums (acc, any): carry into each
-        // lane's leading run
-        double ex[7];
-        int f = any;
-#pragma unroll
-        for (int t = 0; t < 7; ++t) ex[t] = acc[t];
-#pragma unroll
-        for (int offs = 1; offs < 32; offs <<= 1) {
-          const int fo = __shfl_up_sync(0xffffffffu, f, offs);
-#pragma unroll
-          for (int t = 0; t < 7; ++t) {
-            const double ao = __shfl_up_sync(0xffffffffu, ex[t], offs);
-            if (lane >= offs && !f) ex[t] = ao + ex[t];
-          }
-          if (lane >= offs) f |= fo;
-        }
-        // ex/f: inclusive; shift to exclusive and fold in the round carry
-        const int fall = __shfl_sync(0xffffffffu, f, 31);
-        int exf = __shfl_up_sync(0xffffffffu, f, 1);
-        if (lane == 0) exf = 0;
-#pragma unroll
-        for (int t = 0; t < 7; ++t) {
-          const double last = __shfl_sync(0xffffffffu, ex[t], 31);
-          double e = __shfl_up_sync(0xffffffffu, ex[t], 1);
-          if (lane == 0) e = 0.0;
-          const double cin = exf ? e : carry[t] + e;
-          if (first_j >= 0) first[t] += cin;
-          carry[t] = fall ? last : carry[t] + last;
-        }
-        if (first_j >= 0) {
-          double4* rp = reinterpret_cast<double4*>(a.partial + (int64_t)spos[first_j] * 8);
-          rp[0] = make_double4(first[0] * sg[first_j], first[1], first[2], first[3]);
-          rp[1] = make_double4(first[4], first[5], first[6], 0.0);
-        }
+        double4* rp = reinterpret_cast<double4*>(a.partial + (int64_t)spos[tid] * 8);
+        rp[0] = make_double4(acc[0] * sg[tid], acc[1], acc[2], acc[3]);
+        rp[1] = make_double4(acc[4], acc[5], acc[6], 0.0);
       }
     }
+
     if (kG) {
       // pairs after the last descriptor
       for (int i = covered + tid; i < it.z; i += kRays) {
