@@ -155,7 +155,7 @@ struct GeoBatch {
 // (measured 5.7 -> 5.0 ms/step on the c4 batch).
 // T: scene parameter type; OT: gradient element type (sdgr_grads.dtype).
 template <typename T, typename OT>
-__global__ void __launch_bounds__(128, 5) k_grad_geometry(sdgr_scene sc, const __grid_constant__ GeoBatch B,
+__global__ void __launch_bounds__(128, SDGR_MINB_GEOMETRY) k_grad_geometry(sdgr_scene sc, const __grid_constant__ GeoBatch B,
                                                        sdgr_grads out, int accumulate) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = sc.n;

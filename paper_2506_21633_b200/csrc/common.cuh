@@ -32,6 +32,9 @@ constexpr int kChunk = 256;             // Gaussians staged per tile-walk chunk
 #ifndef SDGR_MINB_REPLAY_GRAD
 #define SDGR_MINB_REPLAY_GRAD 3
 #endif
+#ifndef SDGR_MINB_GEOMETRY
+#define SDGR_MINB_GEOMETRY 5
+#endif
 #ifndef SDGR_MINB_GRAD_IMAGE
 #define SDGR_MINB_GRAD_IMAGE 4
 #endif

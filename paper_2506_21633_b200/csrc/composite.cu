@@ -364,6 +364,52 @@ __global__ void __launch_bounds__(256) k_splat_finish(const unsigned long long* 
   if (i < n) image[i] = (double)acc[i] * inv;
 }
 
+// Segmented inclusive scan across the block: thread t holds cnt <= 8
+// consecutive log entries (thread t's before thread t+1's), hd[e] marks the first entry of a run.  On return v[e]
+// is the sum of its run up to and including e.  Fixed association order
+// (thread-serial, then warp shuffles, then warps in order): deterministic.
+// One __syncthreads inside; consecutive calls need a barrier between them.
+__device__ __forceinline__ void block_seg_scan8(double (&v)[8], const bool (&hd)[8], int cnt, double* s_agg,
+                                                int* s_flag) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double run = 0.0;
+  int any = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (e < cnt) {
+      if (hd[e]) { run = v[e]; any = 1; } else { run += v[e]; }
+      v[e] = run;
+    }
+  }
+  double a = run;
+  int f = any;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double ao = __shfl_up_sync(0xffffffffu, a, off);
+    const int fo = __shfl_up_sync(0xffffffffu, f, off);
+    if (lane >= off) {
+      if (!f) a = ao + a;
+      f |= fo;
+    }
+  }
+  double ex = __shfl_up_sync(0xffffffffu, a, 1);
+  int exf = __shfl_up_sync(0xffffffffu, f, 1);
+  if (lane == 0) { ex = 0.0; exf = 0; }
+  if (lane == 31) { s_agg[warp] = a; s_flag[warp] = f; }
+  __syncthreads();
+  double wc = 0.0;
+  for (int w = 0; w < warp; ++w) wc = s_flag[w] ? s_agg[w] : wc + s_agg[w];
+  const double carry = exf ? ex : wc + ex;
+  bool open = true;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (e < cnt && open) {
+      if (hd[e]) open = false;
+      else v[e] += carry;
+    }
+  }
+}
+
 // ============================================================ tile walks ======
 #ifdef SDGR_WALK_PROFILE
 // phase profile of the walks (profiling builds only, profiles/walk_phases.py):
@@ -725,52 +771,6 @@ struct ReplayArgs {
   double* seg_out;        // kGSum
   double* partial;        // kGrad: (n_pairs, 8), every record written
 };
-
-// Segmented inclusive scan across the block: thread t holds cnt <= 8
-// consecutive log entries (thread t's before thread t+1's), hd[e] marks the first entry of a run.  On return v[e]
-// is the sum of its run up to and including e.  Fixed association order
-// (thread-serial, then warp shuffles, then warps in order): deterministic.
-// One __syncthreads inside; consecutive calls need a barrier between them.
-__device__ __forceinline__ void block_seg_scan8(double (&v)[8], const bool (&hd)[8], int cnt, double* s_agg,
-                                                int* s_flag) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double run = 0.0;
-  int any = 0;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    if (e < cnt) {
-      if (hd[e]) { run = v[e]; any = 1; } else { run += v[e]; }
-      v[e] = run;
-    }
-  }
-  double a = run;
-  int f = any;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const double ao = __shfl_up_sync(0xffffffffu, a, off);
-    const int fo = __shfl_up_sync(0xffffffffu, f, off);
-    if (lane >= off) {
-      if (!f) a = ao + a;
-      f |= fo;
-    }
-  }
-  double ex = __shfl_up_sync(0xffffffffu, a, 1);
-  int exf = __shfl_up_sync(0xffffffffu, f, 1);
-  if (lane == 0) { ex = 0.0; exf = 0; }
-  if (lane == 31) { s_agg[warp] = a; s_flag[warp] = f; }
-  __syncthreads();
-  double wc = 0.0;
-  for (int w = 0; w < warp; ++w) wc = s_flag[w] ? s_agg[w] : wc + s_agg[w];
-  const double carry = exf ? ex : wc + ex;
-  bool open = true;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    if (e < cnt && open) {
-      if (hd[e]) open = false;
-      else v[e] += carry;
-    }
-  }
-}
 
 template <int MODE>
 struct ReplayCfg {
