@@ -47,19 +47,6 @@ __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a,
 __device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
 
-// a / b correctly rounded from y = RN(1/b) (Markstein: q = RN(a y) is within
-// an ulp of a / b, r = a - b q is exact by FMA, RN(q + r y) = RN(a / b)): one
-// DMUL + two DFMA instead of a full Newton division when the reciprocal is
-// shared.  Outside the safe range (|q| huge or tiny, non-finite) the true
-// division is used (it also gives exact zeros their sign).
-__device__ __forceinline__ double ddiv_rcp(double a, double b, double y) {
-  const double q = __dmul_rn(a, y);
-  const double aq = fabs(q);
-  if (!(aq < 1.0e300 && aq > 1.0e-290)) return __ddiv_rn(a, b);   // zeros, tiny, huge, non-finite
-  const double r = __fma_rn(-q, b, a);
-  return __fma_rn(r, y, q);
-}
-
 // np.maximum(x, 0.0): NaN propagates (fmax would drop it).
 __device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
 

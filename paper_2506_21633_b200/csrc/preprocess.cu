@@ -57,11 +57,9 @@ __device__ __forceinline__ unsigned long long emit_bbox(int x0, int x1, int y0, 
 __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double v,
                                 double c00, double c01, double c11, double ru, double rv, int nu, int nv,
                                 double cutoff, bool dense, double4& rec_out) {
-  // invert_cov2d (forward.py:33-42): three divisions by det through one
-  // correctly rounded reciprocal (bit-identical to c / det)
+  // invert_cov2d (forward.py:33-42)
   double det = dsub(dmul(c00, c11), dmul(c01, c01));
-  const double rdet = __drcp_rn(det);
-  double a00 = ddiv_rcp(c11, det, rdet), a01 = ddiv_rcp(-c01, det, rdet), a11 = ddiv_rcp(c00, det, rdet);
+  double a00 = ddiv(c11, det), a01 = ddiv(-c01, det), a11 = ddiv(c00, det);
   rec_out = make_double4(a00, a01, a11, 0.0);
   if (pl.uv) reinterpret_cast<double2*>(pl.uv)[g] = make_double2(u, v);
   reinterpret_cast<double4*>(pl.inv_cov)[g] = make_double4(a00, a01, a11, 0.0);
@@ -172,7 +170,6 @@ __device__ void plane_empty(const sdgr_plane& pl, int64_t g) {
 struct ProjBatch {
   sdgr_view view[SDGR_MAX_BATCH];
   sdgr_projection proj[SDGR_MAX_BATCH];
-  double rden_u[SDGR_MAX_BATCH], rden_v[SDGR_MAX_BATCH];   // RN(1 / den), host IEEE divisions
   int nv;
   int zero_col2;   // every view has mc[0][2] == mi[0][2] == 0 (R[0][2] = 0, geometry.py:41-47)
 };
@@ -209,7 +206,7 @@ __device__ __forceinline__ void sandwich(const double* m, const double* Cm, doub
 // extinctions (geometry.py:317) -- is computed once per batch instead of once
 // per view.  Per view: x_r, plane coordinates, the two covariance sandwiches,
 // skip/cull, footprints, depth key and the SH phase (geometry.py:249-317).
-template <typename T>
+template <typename T, bool kZero>
 __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene scene, const __grid_constant__ ProjBatch B) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = g < scene.n;
@@ -300,9 +297,9 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
       for (int i = 0; i < 3; ++i)
         xr[i] = dadd(dfma(p2, R[3 * i + 2], dfma(p1, R[3 * i + 1], dmul(p0, R[3 * i]))), view.T[i]);
       // plane coordinates (geometry.py:78-105) and ndc_to_pixel (:73-75)
-      const double undc = ddiv_rcp(dmul(2.0, xr[0]), view.den_u, B.rden_u[k]);
-      const double vcndc = ddiv_rcp(dmul(2.0, xr[1]), view.den_v, B.rden_v[k]);
-      const double vindc = dsub(ddiv_rcp(dmul(2.0, xr[2]), view.den_v, B.rden_v[k]), view.off_vi);
+      const double undc = ddiv(dmul(2.0, xr[0]), view.den_u);
+      const double vcndc = ddiv(dmul(2.0, xr[1]), view.den_v);
+      const double vindc = dsub(ddiv(dmul(2.0, xr[2]), view.den_v), view.off_vi);
       const double uc = dsub(dmul(dmul(dadd(undc, 1.0), 0.5), (double)view.n_u), 0.5);
       const double vc = dsub(dmul(dmul(dadd(vcndc, 1.0), 0.5), (double)view.n_v), 0.5);
       const double ui = dsub(dmul(dmul(dadd(undc, 1.0), 0.5), (double)view.n_az), 0.5);
@@ -311,15 +308,12 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
 
       // sandwich mc C mc^T (geometry.py:269-278): sequential over (b, c)
       double cc[4], ci[4];
-      const bool sig_fin = isfinite(Cm[0]) && isfinite(Cm[1]) && isfinite(Cm[2]) && isfinite(Cm[4]) &&
-                           isfinite(Cm[5]) && isfinite(Cm[8]);
-      if (B.zero_col2 && sig_fin) {
-        sandwich<true>(view.mc, Cm, cc);
-        sandwich<true>(view.mi, Cm, ci);
-      } else {
-        sandwich<false>(view.mc, Cm, cc);
-        sandwich<false>(view.mi, Cm, ci);
-      }
+      // kZero: a non-finite Sigma makes the reference's sandwich non-finite
+      // (0 * inf = NaN in the skipped terms), i.e. the Gaussian is skipped
+      const bool sig_fin = !kZero || (isfinite(Cm[0]) && isfinite(Cm[1]) && isfinite(Cm[2]) &&
+                                      isfinite(Cm[4]) && isfinite(Cm[5]) && isfinite(Cm[8]));
+      sandwich<kZero>(view.mc, Cm, cc);
+      sandwich<kZero>(view.mi, Cm, ci);
       const double cc00 = dadd(cc[0], view.cov_reg), cc11 = dadd(cc[3], view.cov_reg);
       const double cc01 = dmul(0.5, dadd(cc[1], cc[2]));
       const double ci00 = dadd(ci[0], view.cov_reg), ci11 = dadd(ci[3], view.cov_reg);
@@ -328,7 +322,7 @@ __global__ void __launch_bounds__(256, SDGR_MINB_PROJECT) k_project(sdgr_scene s
       const double deti = dsub(dmul(ci00, ci11), dmul(ci01, ci01));
       const bool finite = isfinite(uc) && isfinite(vc) && isfinite(ui) && isfinite(vi) &&
                           isfinite(depth) && isfinite(detc) && isfinite(deti);
-      const bool ok = finite && detc > 0.0 && deti > 0.0;
+      const bool ok = finite && sig_fin && detc > 0.0 && deti > 0.0;
       const bool dense = !isfinite(view.cutoff);
       bool inside = true;
       double ru = 0.0, rv = 0.0;
@@ -506,8 +500,6 @@ int launch_project(const sdgr_scene& scene, int nv, const sdgr_view* views, sdgr
   for (int k = 0; k < nv; ++k) {
     B.view[k] = views[k];
     B.proj[k] = projs[k];
-    B.rden_u[k] = 1.0 / views[k].den_u;   // host IEEE division: RN(1 / den)
-    B.rden_v[k] = 1.0 / views[k].den_v;
     if (views[k].mc[2] != 0.0 || views[k].mi[2] != 0.0) B.zero_col2 = 0;
   }
   k_project_init<<<1, 4 * SDGR_MAX_BATCH, 0, stream>>>(B);
@@ -515,10 +507,14 @@ int launch_project(const sdgr_scene& scene, int nv, const sdgr_view* views, sdgr
   const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
   {
     KernelTimer kt(SDGR_K_PROJECT, stream);
-    if (scene.dtype == 0)
-      k_project<float><<<blocks, threads, 0, stream>>>(scene, B);
+    if (scene.dtype == 0 && B.zero_col2)
+      k_project<float, true><<<blocks, threads, 0, stream>>>(scene, B);
+    else if (scene.dtype == 0)
+      k_project<float, false><<<blocks, threads, 0, stream>>>(scene, B);
+    else if (B.zero_col2)
+      k_project<double, true><<<blocks, threads, 0, stream>>>(scene, B);
     else
-      k_project<double><<<blocks, threads, 0, stream>>>(scene, B);
+      k_project<double, false><<<blocks, threads, 0, stream>>>(scene, B);
   }
   note_launch(2);
   return check_launch();
