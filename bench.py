@@ -67,6 +67,10 @@ def parse():
     ap.add_argument("--cpu-procs", type=int, default=0)
     ap.add_argument("--lanes", type=int, default=8, help="concurrent view streams per GPU")
     ap.add_argument("--geo-batch", type=int, default=None, help="views per batched launch (default: the build's max)")
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
+                    help="gloo + --share-gpu: exercise the N>1 code path with every rank on cuda:0 "
+                         "(a functional check, never a scaling number)")
+    ap.add_argument("--share-gpu", action="store_true", help="all ranks on cuda:0 (functional check only)")
     a = ap.parse_args()
     w = WORKLOADS[a.workload]
     a.n = a.n or w["n"]
@@ -414,10 +418,13 @@ def run_sdgr(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if args.share_gpu else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     import paper_2506_21633_b200 as sdgr
     from paper_2506_21633_b200.multiview import MultiViewStep
 
@@ -593,6 +600,9 @@ def run_sdgr(args):
                                 "cpu": cpu_model(),
                                 "sample": f"{procs} {args.workload} views ({args.n} Gaussians, {args.size}x{args.size}),"
                                           f" one per forked process, {wall:.1f} s wall"}
+    if args.share_gpu:
+        line["functional_check_only"] = (f"{world} ranks shared cuda:0 over {args.dist_backend}: exercises the "
+                                         "multi-rank path, not a scaling measurement")
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

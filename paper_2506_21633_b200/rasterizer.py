@@ -69,6 +69,23 @@ def _empty(shape, dtype, device):
 
 
 def _scene_desc(ds: DeviceScene) -> _lib.SceneDesc:
+    """POD descriptor of a device scene.  The kernels read raw pointers, so the
+    five arrays must share one float dtype and device, be contiguous and have
+    shape (n, w) -- anything else is rejected here."""
+    arrs = ds.arrays()
+    n = len(ds)
+    dt, dev = arrs[0].dtype, arrs[0].device
+    if dt not in (torch.float32, torch.float64):
+        raise InvalidParameterError(f"scene arrays must be float32 or float64, got {dt}")
+    for (g, w), a in zip(GROUPS, arrs):
+        if a.dtype != dt or a.device != dev:
+            raise InvalidParameterError(f"scene.{g}: dtype/device differ from positions ({a.dtype}, {a.device})")
+        if tuple(a.shape) != (n, w):
+            raise InvalidParameterError(f"scene.{g}: shape {tuple(a.shape)} != ({n}, {w})")
+        if not a.is_contiguous():
+            raise InvalidParameterError(f"scene.{g}: not contiguous")
+    if dev.type != "cuda":
+        raise InvalidParameterError("scene arrays must be CUDA tensors")
     d = _lib.SceneDesc()
     d.n = len(ds)
     d.dtype = 0 if ds.dtype == torch.float32 else 1

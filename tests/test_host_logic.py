@@ -124,3 +124,31 @@ def test_package_imports_without_gpu():
     assert sdgr.__version__
     assert callable(sdgr.render) and callable(sdgr.backward)
     assert math.isfinite(sdgr.S_STOP)
+
+
+def test_scene_descriptor_validation():
+    """a DeviceScene with mixed dtypes, wrong shapes or
+    non-contiguous arrays is rejected before any pointer reaches a kernel
+    (CPU tensors are rejected too)."""
+    import pytest
+    import torch
+
+    from paper_2506_21633_b200.errors import InvalidParameterError
+    from paper_2506_21633_b200.rasterizer import _scene_desc
+    from paper_2506_21633_b200.scene import DeviceScene
+
+    def mk(dtypes=(torch.float32,) * 5, n=4):
+        return DeviceScene(*(torch.zeros((n, w), dtype=dt) for w, dt in zip((3, 4, 3, 16, 2), dtypes)))
+
+    with pytest.raises(InvalidParameterError, match="CUDA"):
+        _scene_desc(mk())
+    with pytest.raises(InvalidParameterError, match="dtype"):
+        _scene_desc(mk((torch.float32, torch.float64, torch.float32, torch.float32, torch.float32)))
+    bad = mk()
+    bad.sh_coeffs = torch.zeros((16, 4)).T            # transposed view: right shape, not contiguous
+    with pytest.raises(InvalidParameterError, match="contiguous"):
+        _scene_desc(bad)
+    bad = mk()
+    bad.ke_raw = torch.zeros((4, 3))
+    with pytest.raises(InvalidParameterError, match="shape"):
+        _scene_desc(bad)
