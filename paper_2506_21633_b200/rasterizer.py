@@ -33,7 +33,7 @@ from . import _lib
 from ._lib import ptr
 from .errors import DeviceError, InvalidParameterError, NumericalError, StateError
 from .radar import n_rays, radar_rotation, view_constants
-from .scene import GROUPS, DeviceScene, as_device_scene, upload_f64
+from .scene import GROUPS, DeviceScene, as_device_scene, download, upload_f64
 
 DEFAULT_COV_REG = 0.3
 DEFAULT_CUTOFF = 3.0
@@ -829,10 +829,7 @@ class ForwardResult:
         if not self.host:
             return self.image_t
         if self._image_host is None:
-            h = torch.empty(self.image_t.shape, dtype=self.image_t.dtype, pin_memory=True)
-            h.copy_(self.image_t, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            self._image_host = h.numpy()
+            self._image_host = download([self.image_t])[0]
         return self._image_host
 
 
@@ -914,18 +911,10 @@ class SceneGradients:
         return d
 
     def to_numpy(self) -> "SceneGradients":
-        """FP64 numpy copies (the reference's SceneGradients layout): one
-        device-to-pinned copy per array on the current stream, one sync; the
-        pinned buffers come from torch's caching host allocator and back the
-        returned arrays."""
+        """FP64 numpy copies (the reference's SceneGradients layout), through
+        one reused pinned staging buffer (scene.download)."""
         arrays = [a.double() for a in self.param_arrays()] + [self.uv_grad_norm.double(), self.visible > 0]
-        host = []
-        for a in arrays:
-            h = torch.empty(a.shape, dtype=a.dtype, pin_memory=True)
-            h.copy_(a, non_blocking=True)
-            host.append(h)
-        torch.cuda.current_stream().synchronize()
-        return SceneGradients(*(h.numpy() for h in host))
+        return SceneGradients(*download(arrays))
 
 
 # -- fused device stages (what backward() runs) ------------------------------

@@ -116,6 +116,38 @@ def upload_f64(a, device) -> torch.Tensor:
     return h.to(device, non_blocking=True)
 
 
+_STAGE = {}
+
+
+def download(tensors) -> list:
+    """Device tensors -> fresh numpy arrays through one reused pinned staging
+    buffer (async D2H of every tensor, one sync, then the copy-out split over
+    the thread pool).  The returned arrays are ordinary pageable numpy memory
+    the caller may keep; the staging block is reused by the next call."""
+    sizes = [t.numel() * t.element_size() for t in tensors]
+    total = sum((b + 255) // 256 * 256 for b in sizes)
+    buf = _STAGE.get("d2h")
+    if buf is None or buf.numel() < total:
+        buf = torch.empty((max(total, 1 << 20),), dtype=torch.uint8, pin_memory=True)
+        _STAGE["d2h"] = buf
+    views, o = [], 0
+    for t, b in zip(tensors, sizes):
+        v = buf[o:o + b].view(t.dtype).view(t.shape)
+        v.copy_(t, non_blocking=True)
+        views.append(v)
+        o += (b + 255) // 256 * 256
+    torch.cuda.current_stream().synchronize()
+    out = [np.empty(tuple(t.shape), dtype=v.numpy().dtype) for t, v in zip(tensors, views)]
+    jobs = []
+    for src, dst in zip(views, out):
+        a, d = src.numpy().reshape(-1), dst.reshape(-1)
+        n = a.size
+        k = 8 if n >= (1 << 20) else 1
+        jobs += [(a, d, n * i // k, n * (i + 1) // k) for i in range(k)]
+    list(_pool().map(lambda j: np.copyto(j[1][j[2]:j[3]], j[0][j[2]:j[3]]), jobs))
+    return out
+
+
 def as_device_scene(scene, device=None) -> tuple[DeviceScene, bool]:
     """(device scene, was_host).  Host scenes keep float64 on device so the
     FP64 key chain sees the caller's exact values."""
