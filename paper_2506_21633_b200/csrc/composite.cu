@@ -50,6 +50,13 @@ enum WalkMode { kContrib = 1, kGSum = 3, kGrad = 4 };
 // Persistent walk grids: SDGR_WALK_GRID_DIV = 1 fills every SM's resident
 // CTA slots with one view's walk; > 1 leaves room for the walks of views on
 // other streams to run alongside (A/B knob for the multi-view step).
+#ifndef SDGR_WALK_CAP
+#define SDGR_WALK_CAP 2048
+#endif
+#ifndef SDGR_DESC_CACHE
+#define SDGR_DESC_CACHE 256
+#endif
+constexpr int kDescCache = SDGR_DESC_CACHE;
 #ifndef SDGR_WALK_GRID_DIV
 #define SDGR_WALK_GRID_DIV 1
 #endif
@@ -65,11 +72,11 @@ constexpr double kFixMax = 1.0e5;  // per-term clamp: keeps 8192-term sums far f
 
 template <int MODE>
 struct WalkCfg {
-  static constexpr int kCap = MODE == kGSum ? 4096 : 2048;  // flat pair slots
+  static constexpr int kCap = MODE == kGSum ? 4096 : SDGR_WALK_CAP;  // flat pair slots
   static constexpr bool kXY = MODE == kGrad;
   static constexpr size_t kSmem = kCap * (8 + 8 + (kXY ? 16 : 0) + 2);
 };
-constexpr int kReplayCap = 2048;  // == WalkCfg<kContrib>::kCap: one descriptor fits the replay
+constexpr int kReplayCap = SDGR_WALK_CAP;  // == WalkCfg<kContrib>::kCap: one descriptor fits the replay
 
 struct WalkArgs {
   int n_cols, n_rows, tiles_x;
@@ -807,7 +814,7 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? SDGR_MINB_REPLAY_GRAD : 4
   __shared__ int s_flag[8];
   __shared__ int32_t scan_tmp[8];
   __shared__ int item_s;
-  __shared__ int4 s_desc[kRays];                    // the item's first 256 descriptors
+  __shared__ int4 s_desc[kDescCache];               // the item's first descriptors
   extern __shared__ double dyn[];
   double* fY = dyn;                                  // y1 = T (1 - e^-tau)
   double* fW = fY + kCap;                            // kGrad: w
@@ -827,14 +834,14 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? SDGR_MINB_REPLAY_GRAD : 4
     const int4 it = reinterpret_cast<const int4*>(a.items)[item];
     const int nd = a.rp.desc_count[item];
     const int4* descs = reinterpret_cast<const int4*>(a.rp.desc) + (int64_t)item * a.rp.desc_per_item;
-    if (tid < nd) s_desc[tid] = descs[tid];
+    if (tid < min(nd, kDescCache)) s_desc[tid] = descs[tid];
     const int tx = it.x % a.tiles_x, ty = it.x / a.tiles_x;
     const int64_t slot_ray = (int64_t)item * kRays + tid;
     ray_acc[tid] = kG ? a.seg_d[slot_ray] + a.seg_g[slot_ray] : 0.0;
     int covered = it.y;  // kGrad: pairs below this have a record
     for (int k = 0; k < nd; ++k) {
       __syncthreads();
-      const int4 d = k < kRays ? s_desc[k] : descs[k];
+      const int4 d = k < kDescCache ? s_desc[k] : descs[k];
       const int64_t off = d.x;
       const int n = d.y, cs = d.z, j0 = d.w & 0xffff, j1 = d.w >> 16;
       // ---- L: Gaussians and entries
