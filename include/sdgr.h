@@ -237,6 +237,14 @@ int sdgr_profile_end(double* ms, int64_t* launches);
  * stream reaches the kernel, so with concurrent streams [begin, end] is the
  * span from "ready" to "done". */
 int sdgr_profile_timeline(int cap, int32_t* ids, double* t0_ms, double* t1_ms);
+/* Page-lock a caller's host buffer for direct DMA (cudaHostRegister,
+ * portable) / release it.  The drop-in host path registers scene arrays it
+ * sees again on a later call (the reference's training loop updates them in
+ * place, optimize.py:206) so their uploads skip the staging copy.  Returns
+ * SDGR_OK or -SDGR_ERR_CUDA (e.g. the pages overlap another registration);
+ * a failure never leaves a pending CUDA error behind. */
+int sdgr_host_register(void* ptr, size_t bytes);
+int sdgr_host_unregister(void* ptr);
 /* Bytes of scratch the binning calls need for n Gaussians / max pairs. */
 size_t sdgr_workspace_bytes(int64_t n, int64_t max_pairs);
 /* ... and the batched calls for n_views (1..SDGR_MAX_BATCH) views (0 if n_views is out of range). */

@@ -180,6 +180,24 @@ int sdgr_profile_timeline(int cap, int32_t* ids, double* t0_ms, double* t1_ms) {
   return n;
 }
 
+int sdgr_host_register(void* ptr, size_t bytes) {
+  if (!ptr || bytes == 0) return -SDGR_ERR_INVALID;
+  if (cudaHostRegister(ptr, bytes, cudaHostRegisterPortable) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return -SDGR_ERR_CUDA;
+  }
+  return SDGR_OK;
+}
+
+int sdgr_host_unregister(void* ptr) {
+  if (!ptr) return -SDGR_ERR_INVALID;
+  if (cudaHostUnregister(ptr) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return -SDGR_ERR_CUDA;
+  }
+  return SDGR_OK;
+}
+
 size_t sdgr_workspace_bytes(int64_t n, int64_t max_pairs) {
   return sdgr_batch_workspace_bytes(n, max_pairs, 1);
 }

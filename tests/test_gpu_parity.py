@@ -555,3 +555,68 @@ def test_depth_order_long_runs(case):
     want = idx[np.lexsort((idx, depth[idx]))]
     assert np.array_equal(order.cpu().numpy()[: idx.size], want)
     _oracle_compare(base, cfg, 3.0, seed=41)
+
+
+def test_registered_scene_arrays_track_in_place_updates():
+    """The drop-in path page-locks scene arrays it sees again (scene.upload_f64):
+    the uploads then DMA from the caller's own memory, so an in-place update
+    between calls (the reference's adam_step, optimize.py:206) must be what the
+    next call renders -- identical to rendering a fresh copy (staging path)."""
+    import gc
+
+    from paper_2506_21633_b200 import scene as scene_mod
+
+    tank = targets.composite_target(targets.tank_preset(), [30000, 8000, 2000], seed=3)
+    cfg = sdgr.RadarConfig(azimuth_deg=31.0, elevation_deg=45.0, altitude_m=0.5, n_range=128, n_azimuth=128)
+    g = np.random.default_rng(1).normal(size=(128, 128))
+    rng = np.random.default_rng(2)
+    for call in range(4):
+        fwd = sdgr.render_forward(tank, cfg)
+        got = (fwd.image.copy(), sdgr.backward(fwd, g))
+        fresh = sdgr.Scene(*(np.array(getattr(tank, k), copy=True) for k in GROUPS))
+        fwd2 = sdgr.render_forward(fresh, cfg)
+        ref = (fwd2.image.copy(), sdgr.backward(fwd2, g))
+        assert np.array_equal(got[0], ref[0]), call
+        for k in GROUPS + ("uv_grad_norm",):
+            assert np.array_equal(getattr(got[1], k), getattr(ref[1], k)), (call, k)
+        tank.positions += rng.normal(scale=1e-3, size=tank.positions.shape)   # in place
+        tank.sh_coeffs *= 1.01
+    big = [getattr(tank, k) for k in GROUPS if getattr(tank, k).nbytes >= scene_mod._REGISTER_MIN]
+    def owner(a):
+        while isinstance(a.base, np.ndarray):
+            a = a.base
+        return a
+
+    states = {e[3] for e in scene_mod._SEEN.values() if any(e[0]() is owner(a) for a in big)}
+    assert states == {"pinned"}, states
+    n_seen = len(scene_mod._SEEN)
+    del tank, fwd, fresh, fwd2, big
+    gc.collect()
+    assert len(scene_mod._SEEN) < n_seen
+
+
+def test_result_blocks_recycle_only_when_unreferenced():
+    """download() hands out numpy views of recycled page-locked blocks: a block
+    holding any live array (or any view of one) is never written again."""
+    import gc
+
+    from paper_2506_21633_b200 import scene as scene_mod
+
+    dev = torch.device("cuda", 0)
+    a = torch.arange(300000, dtype=torch.float64, device=dev).reshape(-1, 3)
+    b = torch.arange(100000, dtype=torch.float32, device=dev)
+    r1 = scene_mod.download([a, b])
+    assert np.array_equal(r1[0], npa(a)) and np.array_equal(r1[1], npa(b))
+    keep = r1[0][:, 1]                       # a view of a view keeps block 1 alive
+    del r1
+    gc.collect()
+    r2 = scene_mod.download([a * 2, b * 2])
+    assert np.array_equal(keep, npa(a)[:, 1])   # untouched
+    assert np.array_equal(r2[0], npa(a) * 2)
+    blk2 = r2[0].base
+    del keep, r2
+    gc.collect()
+    r3 = scene_mod.download([a * 3, b * 3])
+    assert r3[0].base is blk2 or any(r3[0].base is e[1] for e in scene_mod._OUT_POOL)
+    assert np.array_equal(r3[0], npa(a) * 3) and np.array_equal(r3[1], npa(b) * 3)
+    r3[0][0, 0] = -1.0                       # caller-owned, writable
