@@ -42,6 +42,8 @@
 // Early ray termination: a ray stops once its log-transmittance S exceeds
 // s_stop (contributions < e^-s_stop * P).  s_stop = +inf reproduces the
 // reference's exhaustive walk.
+#include <numeric>
+
 #include "common.cuh"
 
 namespace sdgr {
@@ -292,8 +294,14 @@ __global__ void __launch_bounds__(256) k_max_intensity(const uint8_t* flags, con
   }
 }
 
+// Warps take 32-Gaussian groups in a scattered order: warp w of the grid
+// splats group (w * wperm) mod n_groups (wperm coprime to n_groups, ~0.618
+// n_groups).  Neighbouring Gaussians of a spatially ordered scene hit the
+// same pixels; with consecutive warps on consecutive groups their REDs
+// queue on the same L2 addresses (c4: k_splat 4.0 ms/step in the scene's
+// own order, 2.6 in a random order).  Loads stay coalesced within a warp.
 __global__ void __launch_bounds__(256) k_splat(sdgr_view view, sdgr_plane pl, const uint8_t* flags,
-                                               const double* intensity, int64_t n,
+                                               const double* intensity, int64_t n, int64_t wperm,
                                                unsigned long long* acc, const unsigned long long* max_bits) {
   const double scale = splat_scale(max_bits);
   __shared__ double s_u[256], s_v[256], s_a0[256], s_a1[256], s_a2[256], s_I[256];
@@ -301,7 +309,8 @@ __global__ void __launch_bounds__(256) k_splat(sdgr_view view, sdgr_plane pl, co
   __shared__ uint16_t s_list[8 * kList];
   const int tid = threadIdx.x, lane = tid & 31, wbase = tid & ~31;
   uint16_t* list = s_list + (tid >> 5) * kList;
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + tid;
+  const int64_t n_groups = (n + 31) / 32, wg = (int64_t)blockIdx.x * 8 + (tid >> 5);
+  const int64_t g = wg < n_groups ? (wg * wperm) % n_groups * 32 + lane : n;
   uint64_t m[4] = {0, 0, 0, 0};
   bool large = false;
   double2 uv = make_double2(0, 0);
@@ -1130,8 +1139,11 @@ int launch_splat(const sdgr_view& v, const sdgr_projection& p, const double* int
   k_max_intensity<<<std::min<unsigned>(gb, 2u * (unsigned)sm_count()), 256, 0, st>>>(p.flags, intensity, p.n,
                                                                                      acc + npix);
   {
+    const int64_t ng = (p.n + 31) / 32;
+    int64_t wperm = std::max<int64_t>(1, (int64_t)(0.6180339887 * (double)ng));
+    while (std::gcd(wperm, ng) != 1) ++wperm;
     KernelTimer kt(SDGR_K_SPLAT, st);
-    k_splat<<<gb, 256, 0, st>>>(v, p.img, p.flags, intensity, p.n, acc, acc + npix);
+    k_splat<<<(unsigned)std::max<int64_t>(1, (ng + 7) / 8), 256, 0, st>>>(v, p.img, p.flags, intensity, p.n, wperm, acc, acc + npix);
   }
   k_splat_finish<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(acc, npix, image);
   note_launch(3);

@@ -8,5 +8,5 @@ for e in "$@"; do
   python -c "
 import json; d=json.loads([l for l in open('gpurun_out/b_env$i.log') if l.startswith('{')][-1])
 k=d['roofline']['kernel_ms_per_step']
-print('$e', round(d['value'],1), {a: k[a] for a in ('k_segsum','k_walk<kContrib>','k_replay<kGSum>','k_replay<kGrad>')})" || tail -3 gpurun_out/b_env$i.log
+print('$e', round(d['value'],1), k)" || tail -3 gpurun_out/b_env$i.log
 done
