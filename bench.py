@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override the workload's Gaussian count")
     ap.add_argument("--size", type=int, default=None, help="override the workload's image size")
     ap.add_argument("--sigma", type=float, default=None, help="isotropic Gaussian scale in m (c5 sweep)")
+    ap.add_argument("--scene-order", default="morton", choices=("morton", "native", "random"),
+                    help="memory order of the synthetic scene's Gaussians (make_scene)")
     ap.add_argument("--views-per-rank", type=int, default=None)
     ap.add_argument("--dropin-views", type=int, default=6,
                     help="views timed through render_forward + backward with host arrays (0 = skip)")
@@ -108,8 +110,13 @@ def view_list(size: int, workload: str = "c4"):
     return out
 
 
-def make_scene(n: int, workload: str = "c4", sigma: float | None = None):
+def make_scene(n: int, workload: str = "c4", sigma: float | None = None, order: str = "morton"):
+    """The workload's synthetic scene.  order: "morton" (default) stores the
+    Gaussians in spatial_order (the framework's recommended layout, applied
+    once here, outside any timed region); "native" keeps the sampler's
+    per-face order; "random" shuffles (the worst case)."""
     from paper_2506_21633_b200 import targets
+    from paper_2506_21633_b200.scene import spatial_sort
     if WORKLOADS[workload]["scene"] == "tank":   # budgets 0.6 / 0.3 / 0.1 as SURVEY §8d c2 / c3
         b = [int(round(0.6 * n)), int(round(0.3 * n))]
         scene = targets.composite_target(targets.tank_preset(), b + [n - sum(b)], seed=3)
@@ -117,6 +124,12 @@ def make_scene(n: int, workload: str = "c4", sigma: float | None = None):
         scene = targets.tank_grid(n_total=n)
     if sigma is not None:
         scene.log_scales[:] = np.log(sigma)
+    if order == "morton":
+        scene = spatial_sort(scene)[0]
+    elif order == "random":
+        perm = np.random.default_rng(0).permutation(len(scene.positions))
+        scene = type(scene)(*(getattr(scene, k)[perm] for k in
+                              ("positions", "rotations", "log_scales", "sh_coeffs", "ke_raw")))
     # float32-exact so the float32 device scene and the FP64 oracle see the same Gaussians
     return targets.to_float32_exact(scene)
 
@@ -234,7 +247,7 @@ def run_reference(args):
         return
     from oracle import sdgr_oracle
     sdgr_oracle.build()
-    scene = make_scene(args.n, args.workload, args.sigma)
+    scene = make_scene(args.n, args.workload, args.sigma, args.scene_order)
     cfgs = view_list(args.size, args.workload)
     procs = cpu_procs(args.cpu_procs)
     # warm-up: one-time costs only (fork, imports, page-in) on a small sample
@@ -255,7 +268,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_label(args),
+        "config": {"workload": workload_label(args), "scene_order": args.scene_order,
                    "views_per_step": procs, "gaussians": args.n, "image": [args.size, args.size]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "cpu": cpu_model(),
                          "sample": f"{procs} {args.workload} views per step, one per forked process "
@@ -435,7 +448,7 @@ def run_sdgr(args):
     from paper_2506_21633_b200.multiview import MultiViewStep
 
     pdt = torch.float32 if args.param_dtype == "f32" else torch.float64
-    host_scene = make_scene(args.n, args.workload, args.sigma)
+    host_scene = make_scene(args.n, args.workload, args.sigma, args.scene_order)
     cfgs_all = view_list(args.size, args.workload)
     # rank r takes views r, r+W, ... and the first views_per_rank of them
     mine = [c for i, c in enumerate(cfgs_all) if i % world == rank]
@@ -587,7 +600,7 @@ def run_sdgr(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_label(args),
+        "config": {"workload": workload_label(args), "scene_order": args.scene_order,
                    "views_per_rank": V, "gaussians": args.n, "image": [args.size, args.size],
                    "param_dtype": args.param_dtype, "parallelism": f"view-sharded dp{world}",
                    "s_stop": step.s_stop, "l2": "inputs larger than L2 (112 MB params + ~0.3 GB/view records)",

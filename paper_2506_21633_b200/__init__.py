@@ -14,7 +14,7 @@ is missing -- there is no CPU fallback.
 from .errors import (DegenerateProjectionError, DeviceError, DivergenceError, InvalidParameterError,
                      NumericalError, SarsplatError, StateError)
 from .radar import RadarConfig, radar_position, radar_rotation, view_constants
-from .scene import DeviceScene, Scene
+from .scene import DeviceScene, Scene, spatial_order, spatial_sort
 
 __version__ = "0.1.0"
 
@@ -40,4 +40,5 @@ def __getattr__(name):
 __all__ = sorted(_LAZY | {"RadarConfig", "Scene", "DeviceScene", "radar_position", "radar_rotation",
                           "view_constants", "SarsplatError", "InvalidParameterError",
                           "DegenerateProjectionError", "NumericalError", "StateError",
-                          "DivergenceError", "DeviceError", "MultiViewStep", "shard_views"})
+                          "DivergenceError", "DeviceError", "MultiViewStep", "shard_views",
+                          "spatial_order", "spatial_sort"})

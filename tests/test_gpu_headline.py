@@ -108,10 +108,13 @@ def test_c4_dropin_vs_oracle(c4_scene, az, el):
             assert_close(getattr(g, k), go[k], what=f"dL/dS=S grad {k}")
 
 
-def test_c4_benchmarked_step_vs_oracle(c4_scene):
+@pytest.mark.parametrize("order", ["native", "morton"])
+def test_c4_benchmarked_step_vs_oracle(c4_scene, order):
     """The exact path bench.py times (MultiViewStep: FP32 parameters, batched
     K1-K5, 8 lanes, s_stop 40, >= 2048-Gaussian depth segments) on the three
-    c4 views: accumulated gradients == sum of the oracle's per-view gradients."""
+    c4 views: accumulated gradients == sum of the oracle's per-view gradients.
+    "morton": the scene in spatial_order, as bench.py stores it; its gradients
+    are the oracle's (computed on the sampler's order) permuted."""
     from paper_2506_21633_b200.multiview import MULTIVIEW_SEG_LEN, MultiViewStep
 
     cfgs = [c4_config(az, el) for az, el in C4_VIEWS]
@@ -124,7 +127,13 @@ def test_c4_benchmarked_step_vs_oracle(c4_scene):
         for k in ref:
             ref[k] = ref[k] + go[k]
         vis = vis + go["visible"].astype(np.int64)
-    ds = sdgr.DeviceScene.from_host(c4_scene, dtype=torch.float32)
+    scene = c4_scene
+    if order == "morton":
+        scene, perm = sdgr.spatial_sort(c4_scene)
+        assert not np.array_equal(perm, np.arange(len(perm)))
+        ref = {k: v[perm] for k, v in ref.items()}
+        vis = vis[perm]
+    ds = sdgr.DeviceScene.from_host(scene, dtype=torch.float32)
     step = MultiViewStep(ds, cfgs)
     assert step.s_stop == sdgr.S_STOP and step.n_lanes == len(cfgs)
     got = step.run(torch.from_numpy(np.stack(dls)).cuda())

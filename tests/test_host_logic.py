@@ -152,3 +152,28 @@ def test_scene_descriptor_validation():
     bad.ke_raw = torch.zeros((4, 3))
     with pytest.raises(InvalidParameterError, match="shape"):
         _scene_desc(bad)
+
+
+def test_spatial_order_is_a_morton_permutation():
+    import paper_2506_21633_b200 as sdgr
+
+    rng = np.random.default_rng(0)
+    pos = rng.uniform(-5, 5, size=(5000, 3))
+    perm = sdgr.spatial_order(pos)
+    assert np.array_equal(np.sort(perm), np.arange(len(pos)))
+    # neighbours in the new order are close in space (Z-curve locality)
+    d_sorted = np.linalg.norm(np.diff(pos[perm], axis=0), axis=1).mean()
+    d_orig = np.linalg.norm(np.diff(pos, axis=0), axis=1).mean()
+    assert d_sorted < 0.2 * d_orig
+    scene = sdgr.Scene(pos, rng.normal(size=(5000, 4)), rng.normal(size=(5000, 3)),
+                       rng.normal(size=(5000, 16)), rng.normal(size=(5000, 2)))
+    s2, p2 = sdgr.spatial_sort(scene)
+    assert np.array_equal(p2, perm)
+    for k in ("positions", "rotations", "log_scales", "sh_coeffs", "ke_raw"):
+        assert np.array_equal(getattr(s2, k), getattr(scene, k)[perm])
+    # degenerate inputs: empty, one point, non-finite rows keep a valid permutation
+    assert sdgr.spatial_order(np.zeros((0, 3))).shape == (0,)
+    assert np.array_equal(sdgr.spatial_order(np.zeros((1, 3))), [0])
+    bad = pos[:10].copy()
+    bad[3] = np.nan
+    assert np.array_equal(np.sort(sdgr.spatial_order(bad)), np.arange(10))
