@@ -178,7 +178,9 @@ typedef struct sdgr_tiles {
   int32_t device_count; /* 1: n_pairs is a capacity; the exact count stays on the
                            device (offsets[n]) so no host round trip is needed */
   int32_t pad_;
-  int32_t* items;       /* (max_items,4) tile, start, end, first item of tile */
+  int32_t* items;       /* (max_items,4) tile, start, end; column 3 = the
+                           processing order (row c: the item the c-th
+                           claim of a persistent walk takes)             */
   int32_t* tile_first;  /* (n_tiles) index of each tile's first work item     */
   int32_t* n_items;     /* (4) device: [0] work items, [1] overflow flag, [2] walk counter */
   sdgr_pair_rec* pair_rec; /* (n_pairs) packed per-pair records in sorted order

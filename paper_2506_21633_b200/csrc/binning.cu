@@ -824,11 +824,71 @@ __global__ void __launch_bounds__(1024) k_make_items(const __grid_constant__ Ite
           items[4 * it + 0] = t;
           items[4 * it + 1] = s + k * seg_len;
           items[4 * it + 2] = min(e, s + (k + 1) * seg_len);
-          items[4 * it + 3] = first;
+          items[4 * it + 3] = it;   // overwritten below with the processing order
         }
       }
     }
     carry += total;
+  }
+  // processing order (column 3): segment-major -- every tile's first
+  // segment, then every second segment, ... -- so a persistent walk starts
+  // the heavy first segments (all rays live) in its first wave and the light
+  // deep ones (most rays terminated) fill the tail.  Row c holds the item of
+  // the c-th claim; position of (tile t, segment k) = off[k] + #(tiles
+  // before t with more than k segments), from per-warp ballot counts.
+  // Beyond kOrdSeg segments or kOrdWarps * 32 tiles: identity order.
+  {
+    constexpr int kOrdSeg = 64, kOrdWarps = 128;
+    __shared__ int32_t s_cnt[kOrdSeg][kOrdWarps];
+    __shared__ int32_t s_off[kOrdSeg + 1];
+    __shared__ int32_t s_max;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_max = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += 1024)
+      atomicMax(&s_max, (range[2 * t + 1] - range[2 * t] + seg_len - 1) / seg_len);
+    __syncthreads();
+    const int32_t maxseg = s_max;
+    const int n_chunks = (n_tiles + 1023) / 1024;
+    if (carry <= max_items && maxseg <= kOrdSeg && n_chunks * 32 <= kOrdWarps) {
+      for (int c = 0; c < n_chunks; ++c) {
+        const int t = c * 1024 + (int)threadIdx.x;
+        const int32_t ns = t < n_tiles ? (range[2 * t + 1] - range[2 * t] + seg_len - 1) / seg_len : 0;
+        for (int k = 0; k < maxseg; ++k) {
+          const uint32_t b = __ballot_sync(0xffffffffu, ns > k);
+          if (lane == 0) s_cnt[k][c * 32 + warp] = __popc(b);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {   // off[k] = sum of all tiles' counts of segments < k
+        int32_t run = 0;
+        for (int k = 0; k < maxseg; ++k) {
+          int32_t part = 0;
+          for (int w = (int)threadIdx.x; w < n_chunks * 32; w += 32) part += s_cnt[k][w];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+          if (threadIdx.x == 0) s_off[k] = run;
+          run += part;
+        }
+      }
+      __syncthreads();
+      for (int c = 0; c < n_chunks; ++c) {
+        const int t = c * 1024 + (int)threadIdx.x;
+        const int32_t ns = t < n_tiles ? (range[2 * t + 1] - range[2 * t] + seg_len - 1) / seg_len : 0;
+        const int gw = c * 32 + warp;
+        int32_t wmax = ns;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, off));
+        for (int k = 0; k < wmax; ++k) {
+          const uint32_t b = __ballot_sync(0xffffffffu, ns > k);
+          if (ns > k) {
+            int32_t before = 0;
+            for (int w = 0; w < gw; ++w) before += s_cnt[k][w];
+            items[4 * (s_off[k] + before + __popc(b & ((1u << lane) - 1u))) + 3] = tile_first[t] + k;
+          }
+        }
+      }
+    }
   }
   if (threadIdx.x == 0) {
     io.n_items[v][0] = carry < max_items ? carry : max_items;

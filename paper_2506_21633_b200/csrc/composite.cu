@@ -59,6 +59,20 @@ enum WalkMode { kContrib = 1, kGSum = 3, kGrad = 4 };
 #define SDGR_DESC_CACHE 256
 #endif
 constexpr int kDescCache = SDGR_DESC_CACHE;
+// Item claim order of the persistent kernels: 1 = the segment-major order
+// k_make_items writes (heavy first segments first), 0 = tile-major item
+// order.  c4 (profiles/ROUND2.md): segment-major cuts the lone walk launch
+// 9.0 -> 7.75 ms/step (its tail) at -0.3 % views/s in the concurrent step;
+// for pass A and the replays it costs 0.5-1 % views/s and is off.
+#ifndef SDGR_ORDER_WALK
+#define SDGR_ORDER_WALK 1
+#endif
+#ifndef SDGR_ORDER_SEGSUM
+#define SDGR_ORDER_SEGSUM 0
+#endif
+#ifndef SDGR_ORDER_REPLAY
+#define SDGR_ORDER_REPLAY 0
+#endif
 #ifndef SDGR_WALK_GRID_DIV
 #define SDGR_WALK_GRID_DIV 1
 #endif
@@ -198,8 +212,8 @@ __global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const 
     __syncthreads();
     if (tid == 0) item_s = (int)atomicAdd(counter, 1u);
     __syncthreads();
-    const int item = item_s;
-    if (item >= n_items) return;
+    if (item_s >= n_items) return;
+    const int item = SDGR_ORDER_SEGSUM ? items[4 * item_s + 3] : item_s;   // processing order (k_make_items)
     const int4 it = reinterpret_cast<const int4*>(items)[item];
     // a tile's last segment: its optical depth is no later segment's prefix
     // (the scan is exclusive), so pass A skips it -- for a single-segment
@@ -478,8 +492,8 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
     if (tid == 0) item_s = (int)atomicAdd(a.counter, 1u);
     __syncthreads();
     WPROF(0);
-    const int item = item_s;
-    if (item >= n_items) return;
+    if (item_s >= n_items) return;
+    const int item = SDGR_ORDER_WALK ? a.items[4 * item_s + 3] : item_s;   // processing order (k_make_items)
     const int4 it = reinterpret_cast<const int4*>(a.items)[item];
     const int tile = it.x, start = it.y, end = it.z;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -837,8 +851,8 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? SDGR_MINB_REPLAY_GRAD : 4
     __syncthreads();
     if (tid == 0) item_s = (int)atomicAdd(a.counter, 1u);
     __syncthreads();
-    const int item = item_s;
-    if (item >= n_items) return;
+    if (item_s >= n_items) return;
+    const int item = SDGR_ORDER_REPLAY ? a.items[4 * item_s + 3] : item_s;   // processing order (k_make_items)
     // item metadata, its descriptors and the per-ray seeds load in parallel
     const int4 it = reinterpret_cast<const int4*>(a.items)[item];
     const int nd = a.rp.desc_count[item];
