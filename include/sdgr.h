@@ -35,7 +35,7 @@ extern "C" {
 #define SDGR_TILE_RAYS 256
 #define SDGR_MAX_PLANE 32767  /* plane dims must fit int16 bboxes */
 #ifndef SDGR_MAX_BATCH
-#define SDGR_MAX_BATCH 16     /* views per batched call (*_batch); sdgr_max_batch() reports the build's */
+#define SDGR_MAX_BATCH 24     /* views per batched call (*_batch); sdgr_max_batch() reports the build's */
 #endif
 
 typedef enum sdgr_status {

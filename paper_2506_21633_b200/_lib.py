@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / os.environ.get("SDGR_LIB", "libsdgr
 OK, ERR_INVALID, ERR_NUMERICAL, ERR_STATE, ERR_CUDA, ERR_CAPACITY = range(6)
 FLAG_VISIBLE, FLAG_SKIPPED, FLAG_CULLED = 1, 2, 4
 TILE = 16
-MAX_BATCH = 16  # default build's SDGR_MAX_BATCH; lib().sdgr_max_batch() is authoritative
+MAX_BATCH = 24  # default build's SDGR_MAX_BATCH; lib().sdgr_max_batch() is authoritative
 PROFILE_KERNELS = 16
 K_PROJECT, K_ONESWEEP, K_EMIT, K_GATHER, K_SEGSUM, K_WALK, K_SPLAT, K_GRAD_IMAGE, K_REPLAY_GSUM, K_REPLAY_GRAD, \
     K_GEOMETRY = range(1, 12)

@@ -88,7 +88,7 @@ def test_struct_layouts_match_c(tmp_path):
 def test_batch_entry_points_validate_without_device(lib):
     from paper_2506_21633_b200 import _lib
     mb = lib.sdgr_max_batch()
-    assert mb == _lib.MAX_BATCH == 16
+    assert mb == _lib.MAX_BATCH == 24
     # workspace sizing: 0 outside 1..max_batch, growing with the batch
     assert lib.sdgr_batch_workspace_bytes(1_000_000, 1_500_000, 0) == 0
     assert lib.sdgr_batch_workspace_bytes(1_000_000, 1_500_000, mb + 1) == 0
