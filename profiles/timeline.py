@@ -59,8 +59,17 @@ for a, b, nm in ev:
     p[0] += 1
     p[1] += b - a
 first_walk = min((a for a, _, nm in ev if nm == "k_walk<kContrib>"), default=None)
+# which kernel runs alone during the single-kernel periods
+solo = {}
+bounds = sorted({x for a, b, _ in ev for x in (a, b)})
+for lo, hi in zip(bounds, bounds[1:]):
+    live = [nm for a, b, nm in ev if a <= lo and b >= hi]
+    if len(live) == 1:
+        solo[live[0]] = solo.get(live[0], 0.0) + (hi - lo)
 print(json.dumps({"launches": n, "step_span_ms": end,
                   "ms_with_k_in_flight": {str(k): round(v, 3) for k, v in sorted(hist.items())},
                   "first_walk_starts_ms": first_walk,
                   "ready_to_done_ms_per_kernel": {k: round(v[1], 3) for k, v in per.items()},
-                  "launch_counts": {k: v[0] for k, v in per.items()}}, indent=1))
+                  "launch_counts": {k: v[0] for k, v in per.items()},
+                  "solo_ms_by_kernel": {k: round(v, 3) for k, v in sorted(solo.items(), key=lambda x: -x[1])},
+                  "events": [[round(a, 4), round(b, 4), nm] for a, b, nm in sorted(ev)]}, indent=1))
