@@ -706,6 +706,8 @@ struct GatherIO {
   sdgr_pair_rec* rec[kMaxBatch];
   const uint32_t* keys[kMaxBatch];
   int32_t* range[kMaxBatch];
+  int32_t* n_items[kMaxBatch];   // [1]: overflow / invalid flag
+  int32_t n_tiles[kMaxBatch];
 };
 
 // One thread per sorted pair.  With the computation plane's packed 64-byte
@@ -722,8 +724,12 @@ __global__ void __launch_bounds__(256) k_gather_prim(const __grid_constant__ Gat
   int32_t* range = io.range[v];
   const uint32_t t = keys[ii];
   if (live) {
-    if (i == 0 || keys[i - 1] != t) range[2 * t] = (int32_t)i;
-    if (i == n - 1 || keys[i + 1] != t) range[2 * t + 1] = (int32_t)(i + 1);
+    if (t < (uint32_t)io.n_tiles[v]) {
+      if (i == 0 || keys[i - 1] != t) range[2 * t] = (int32_t)i;
+      if (i == n - 1 || keys[i + 1] != t) range[2 * t + 1] = (int32_t)(i + 1);
+    } else {
+      io.n_items[v][1] = 1;   // a tile id past the grid (a view whose ray grid is not the lists'): flagged, never written
+    }
   }
   const int32_t p = io.pos[v][ii];
   const int32_t g = io.pre[v][p];
@@ -1026,6 +1032,8 @@ int launch_bin_batch(int nv, const sdgr_projection* projs, const sdgr_view* view
       gio.rec[v] = plane == 0 ? tls[v].pair_rec : nullptr;
       gio.keys[v] = tls[v].pair_tile;
       gio.range[v] = tls[v].tile_range;
+      gio.n_items[v] = tls[v].n_items;
+      gio.n_tiles[v] = tls[v].n_tiles;
     }
     {
       KernelTimer kt(SDGR_K_GATHER, st);
