@@ -9,6 +9,7 @@ attributes (e.g. the reference's own Scene).
 from __future__ import annotations
 
 import sys
+import threading
 import weakref
 from dataclasses import dataclass, field
 from typing import Any
@@ -197,6 +198,7 @@ def _registered(a) -> bool:
 
 
 _STAGE = {}
+_POOL_LOCK = threading.Lock()
 _OUT_POOL = []                 # [pinned tensor, numpy view of it]: recycled result blocks
 _OUT_POOL_BYTES = 1 << 30      # beyond this, results are copied out of one staging block
 
@@ -233,15 +235,25 @@ def download(tensors) -> list:
     reused staging block into fresh memory by the thread pool instead."""
     sizes = [t.numel() * t.element_size() for t in tensors]
     total = sum((b + 255) // 256 * 256 for b in sizes)
-    blk = _result_block(total)
+    with _POOL_LOCK:   # a block is taken (views created) before another caller looks for a free one
+        blk = _result_block(total)
+        if blk is not None:
+            out, o = [], 0
+            for t, b in zip(tensors, sizes):
+                out.append(blk[1][o:o + b].view(_np_dtype(t.dtype)).reshape(tuple(t.shape)))
+                o += (b + 255) // 256 * 256
     if blk is not None:
-        out, o = [], 0
+        o = 0
         for t, b in zip(tensors, sizes):
             blk[0][o:o + b].view(t.dtype).view(t.shape).copy_(t, non_blocking=True)
-            out.append(blk[1][o:o + b].view(_np_dtype(t.dtype)).reshape(tuple(t.shape)))
             o += (b + 255) // 256 * 256
         torch.cuda.current_stream().synchronize()
         return out
+    with _POOL_LOCK:
+        return _download_staged(tensors, sizes, total)
+
+
+def _download_staged(tensors, sizes, total) -> list:
     buf = _STAGE.get("d2h")
     if buf is None or buf.numel() < total:
         buf = torch.empty((max(total, 1 << 20),), dtype=torch.uint8, pin_memory=True)
