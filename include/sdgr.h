@@ -372,6 +372,9 @@ int sdgr_cell_pairs(const sdgr_projection* proj, const sdgr_view* view, const sd
  * computation-plane pairs of sdgr_cell_pairs: tau, trans, absorb, contrib
  * (each ray's exclusive log-transmittance prefix in list order).  Needs
  * proj->kappa and proj->phase. */
+/* Diagnostics: y[i] = the compositing path's e^x (nexp, common.cuh) for n
+ * device doubles -- its accuracy against libdevice exp is tested. */
+int sdgr_exp_check(int64_t n, const double* x, double* y, void* stream);
 int sdgr_cell_intensities(const sdgr_projection* proj, int64_t n_cells, const int64_t* offsets,
                           const int32_t* prim, const double* w, double* tau, double* trans,
                           double* absorb, double* contrib, void* stream);

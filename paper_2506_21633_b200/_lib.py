@@ -103,6 +103,7 @@ SIGNATURES = [
     ("sdgr_profile_end", C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     ("sdgr_profile_timeline", C.c_int, [C.c_int, _p, _p, _p]),
     ("sdgr_host_register", C.c_int, [_p, C.c_size_t]),
+    ("sdgr_exp_check", C.c_int, [C.c_int64, _p, _p, _p]),
     ("sdgr_host_unregister", C.c_int, [_p]),
     ("sdgr_project", C.c_int, [C.POINTER(SceneDesc), C.POINTER(View), C.POINTER(ProjectionDesc), _p]),
     ("sdgr_depth_order", C.c_int, [C.POINTER(ProjectionDesc), _p, _p, C.c_size_t, _p]),

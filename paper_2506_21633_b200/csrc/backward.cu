@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256, SDGR_MINB_GRAD_IMAGE) k_grad_image(sdgr_v
     const double cut2 = dmul(view.cutoff, view.cutoff);
     auto visit = [&](int iu, int iv, double dx, double dy, double q) {
       const double G = __ldg(dLdS + (int64_t)iv * view.n_az + iu);
-      const double w = exp(-q);
+      const double w = nexp(-q);
       dI += G * w;
       const double dq = -(G * I) * w;
       g00 += dq * dx * dx;

@@ -77,6 +77,7 @@ int launch_adam(const sdgr_scene&, const sdgr_grads&, const sdgr_scene&, const s
 int launch_accum_update(const sdgr_grads&, int64_t, double*, double*, double*, cudaStream_t);
 int launch_cell_pairs(const sdgr_projection&, const sdgr_view&, const sdgr_tiles&, int64_t*, int32_t*, double*,
                       double*, double*, cudaStream_t);
+int launch_exp_check(int64_t, const double*, double*, cudaStream_t);
 int launch_cell_intensities(const sdgr_projection&, int64_t, const int64_t*, const int32_t*, const double*, double*,
                             double*, double*, double*, cudaStream_t);
 int launch_splat_pair_grads(int64_t, const int32_t*, const int32_t*, const double*, const double*, double*,
@@ -348,6 +349,11 @@ int sdgr_cell_pairs(const sdgr_projection* proj, const sdgr_view* view, const sd
   if (!pl.uv || !pl.inv_cov || !pl.bbox || !pl.cell_mask) return SDGR_ERR_INVALID;   // needs the SoA records
   if (prim && (!delta || !q || !w)) return SDGR_ERR_INVALID;
   return launch_cell_pairs(*proj, *view, *tiles, offsets, prim, delta, q, w, static_cast<cudaStream_t>(stream));
+}
+
+int sdgr_exp_check(int64_t n, const double* x, double* y, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !y))) return -SDGR_ERR_INVALID;
+  return -launch_exp_check(n, x, y, (cudaStream_t)stream);
 }
 
 int sdgr_cell_intensities(const sdgr_projection* proj, int64_t n_cells, const int64_t* offsets, const int32_t* prim,

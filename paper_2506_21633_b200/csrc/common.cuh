@@ -47,6 +47,57 @@ __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a,
 __device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
 
+// ---- e^x for x <= 0 on the compositing path ---------------------------------
+// Table-driven (Tang): x = (64 e + j) ln2/64 + r, |r| <= ln2/128, e^x =
+// 2^e 2^(j/64) e^r with e^r - 1 a degree-5 polynomial (truncation < 0.2 ulp);
+// <= 2 ulp against libdevice exp (tests/test_gpu_stages.py), deterministic,
+// ~2/3 of libdevice's instructions (its degree-11 polynomial needs a 64-bit
+// constant per term) but a dependent table load.  Used where it measured
+// faster: the imaging-plane backward (k_grad_image 2.30 -> 2.20 ms/step)
+// and the splat; pass A and the walk keep exp() (their exp feeds a short
+// dependent chain and the table load made them slower: 4.14 -> 4.73 and
+// 7.77 -> 7.90 ms/step).  Outside (-708, 0] (underflow, -inf, NaN) it
+// defers to exp().
+#ifndef SDGR_FAST_EXP
+#define SDGR_FAST_EXP 1
+#endif
+static __device__ const double kExp2Tab[64] = {
+  1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+  1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+  1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+  1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+  1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+  1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+  1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+  1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+  1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+  1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+  1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+  1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+  1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+  1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+  1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+  1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
+__device__ __forceinline__ double nexp(double x) {
+#if SDGR_FAST_EXP
+  if (!(x > -708.0)) return exp(x);
+  const double shifter = 6755399441055744.0;   // 1.5 * 2^52: round-to-integer in the low word
+  const double ts = fma(x, 92.33248261689366, shifter);   // x * 64 / ln2
+  const int k = __double2loint(ts);
+  const double kd = ts - shifter;
+  double r = fma(kd, -0.010830424696223417, x);           // ln2/64, 36 significant bits: kd * hi exact
+  r = fma(kd, -2.572804622327669e-14, r);
+  double p = fma(fma(fma(fma(r, 1.0 / 120.0, 1.0 / 24.0), r, 1.0 / 6.0), r, 0.5), r, 1.0);
+  p *= r;                                                  // e^r - 1
+  const double T = __ldg(kExp2Tab + (k & 63));
+  const double y = fma(T, p, T);
+  return __hiloint2double(__double2hiint(y) + ((k >> 6) << 20), __double2loint(y));
+#else
+  return exp(x);
+#endif
+}
+
 // np.maximum(x, 0.0): NaN propagates (fmax would drop it).
 __device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
 

@@ -285,7 +285,7 @@ __device__ __forceinline__ unsigned long long splat_fix(double v, double scale) 
 
 __device__ __forceinline__ void splat_add(unsigned long long* acc, int n_az, int iu, int iv, double q, double I,
                                           double scale) {
-  atomicAdd(acc + (int64_t)iv * n_az + iu, splat_fix(exp(-q) * I, scale));
+  atomicAdd(acc + (int64_t)iv * n_az + iu, splat_fix(nexp(-q) * I, scale));
 }
 
 // max_g I_g over visible Gaussians as u64 bits (I >= 0: the bit order is the
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(256) k_splat(sdgr_view view, sdgr_plane pl, co
         const int iu = s_x[j] + (b & 7), iv = s_y[j] + (b >> 3);
         const double q = quadform(s_a0[j], s_a1[j], s_a2[j], dsub((double)iu, s_u[j]), dsub((double)iv, s_v[j]));
         pix = (int64_t)iv * view.n_az + iu;
-        val = splat_fix(exp(-q) * s_I[j], scale);
+        val = splat_fix(nexp(-q) * s_I[j], scale);
       }
       // (combining a round's same-pixel terms with MATCH.ANY before the RED
       // was measured slower: 4.0 -> 6.5 ms/step, only ~17 % of the REDs merge)

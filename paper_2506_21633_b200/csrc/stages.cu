@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) k_cell_pairs(PlaneSoA pl, const int32_t* 
         prim[cur] = sg[j];
         reinterpret_cast<double2*>(delta)[cur] = make_double2(dx, dy);
         q[cur] = qq;
-        w[cur] = exp(-qq);
+        w[cur] = nexp(-qq);
         ++cur;
       }
       }
@@ -136,8 +136,8 @@ __global__ void __launch_bounds__(256) k_cell_intensities(const int64_t* __restr
   for (int64_t p = off[c]; p < off[c + 1]; ++p) {
     const int g = prim[p];
     const double t = kappa[g] * w[p];
-    const double T = exp(-S);
-    const double a = exp(-t);
+    const double T = nexp(-S);
+    const double a = nexp(-t);
     tau[p] = t;
     trans[p] = T;
     absorb[p] = a;
@@ -225,6 +225,17 @@ int launch_cell_intensities(const sdgr_projection& p, int64_t n_cells, const int
                             cudaStream_t st) {
   k_cell_intensities<<<(unsigned)((n_cells + 255) / 256), 256, 0, st>>>(off, n_cells, prim, w, p.kappa, p.phase,
                                                                         tau, trans, absorb, contrib);
+  note_launch();
+  return check_launch();
+}
+
+__global__ void __launch_bounds__(256) k_exp_check(int64_t n, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = nexp(x[i]);
+}
+
+int launch_exp_check(int64_t n, const double* x, double* y, cudaStream_t st) {
+  if (n > 0) k_exp_check<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, x, y);
   note_launch();
   return check_launch();
 }

@@ -315,3 +315,26 @@ def test_synthetic_projection_stages_vs_oracle(rng):
     dI, _, _, _ = sdgr.grad_image_stage(fwd, dl)
     want = np.bincount(spl.prim, weights=dl.reshape(-1)[spl.cell] * spl.w, minlength=k)
     assert_close(dI, want, what="dL/dI")
+
+
+def test_compositing_exp_accuracy():
+    """nexp (the table-driven e^x of the compositing kernels) against
+    libdevice exp over the ranges the kernels use (e^-q, q <= 9 + margins;
+    e^-S up to the early-stop bound and beyond; underflow, -inf, NaN)."""
+    from paper_2506_21633_b200 import _lib
+
+    rng = np.random.default_rng(0)
+    x = np.concatenate([-rng.uniform(0, 12, 200000), -rng.uniform(0, 60, 200000), -rng.uniform(0, 800, 50000),
+                        -np.logspace(-300, 2.8, 20000), [0.0, -0.0, -1e-320, -707.9, -708.1, -745.0, -746.0,
+                                                           -np.inf, np.nan]])
+    xd = torch.from_numpy(x).cuda()
+    y = torch.empty_like(xd)
+    assert _lib.lib().sdgr_exp_check(x.size, xd.data_ptr(), y.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    got, ref = y.cpu().numpy(), torch.exp(xd).cpu().numpy()
+    fin = np.isfinite(ref) & (ref > 2.3e-308)
+    ulp = np.abs(got[fin] - ref[fin]) / np.spacing(ref[fin])
+    assert ulp.max() <= 2.0, ulp.max()
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    tiny = ~fin & ~np.isnan(ref)
+    assert np.allclose(got[tiny], ref[tiny], rtol=0, atol=1e-307)
