@@ -55,6 +55,16 @@ enum WalkMode { kContrib = 1, kGSum = 3, kGrad = 4 };
 #ifndef SDGR_WALK_CAP
 #define SDGR_WALK_CAP 2048
 #endif
+// 1: walk P0 reads the chunk's 80-byte pair records from shared memory,
+// where a cp.async.bulk (TMA engine, mbarrier completion) issued during the
+// previous chunk put them.  Measured slower and off by default (c4, 1367
+// views/s without; with it 1318 at 2 CTAs/SM, 1344 with the flat capacity
+// cut to 1408 to keep 3 CTAs/SM, vs 1360 for that capacity without: the
+// record loads are not P0's cost; profiles/ROUND2.md).  The full GPU test
+// suite passes with it on.
+#ifndef SDGR_WALK_BULK
+#define SDGR_WALK_BULK 0
+#endif
 #ifndef SDGR_DESC_CACHE
 #define SDGR_DESC_CACHE 256
 #endif
@@ -90,7 +100,9 @@ template <int MODE>
 struct WalkCfg {
   static constexpr int kCap = MODE == kGSum ? 4096 : SDGR_WALK_CAP;  // flat pair slots
   static constexpr bool kXY = MODE == kGrad;
-  static constexpr size_t kSmem = kCap * (8 + 8 + (kXY ? 16 : 0) + 2);
+  // + the chunk's records, staged by a bulk copy (TMA engine) one chunk ahead
+  static constexpr size_t kStage = SDGR_WALK_BULK ? (size_t)kChunk * sizeof(sdgr_pair_rec) : 0;
+  static constexpr size_t kSmem = kStage + kCap * (8 + 8 + (kXY ? 16 : 0) + 2);
 };
 constexpr int kReplayCap = SDGR_WALK_CAP;  // == WalkCfg<kContrib>::kCap: one descriptor fits the replay
 
@@ -111,6 +123,46 @@ struct WalkArgs {
   int32_t* status;
   sdgr_replay rp;          // kContrib: live-pair log to write (rp.y1 == nullptr: none)
 };
+
+// ---- bulk copy global -> shared with mbarrier completion (one thread issues)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(mbar)) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  // earlier generic-proxy reads of dst are ordered before the async write
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(mbar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(mbar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ sdgr_pair_rec load_rec_smem(const sdgr_pair_rec* p) {
+  sdgr_pair_rec r;
+  const double2* s = reinterpret_cast<const double2*>(p);
+  const double2 a0 = s[0], a1 = s[1], b0 = s[2], b1 = s[3];
+  const int4 t = reinterpret_cast<const int4*>(p)[4];
+  r.u = a0.x; r.v = a0.y; r.a00 = a1.x; r.a01 = a1.y;
+  r.a11 = b0.x; r.kappa = b0.y; r.phase = b1.x; r.cell_mask = (uint64_t)__double_as_longlong(b1.y);
+  r.x0 = (int16_t)(t.x & 0xffff); r.x1 = (int16_t)(t.x >> 16);
+  r.y0 = (int16_t)(t.y & 0xffff); r.y1 = (int16_t)(t.y >> 16);
+  r.pos = t.z; r.prim = t.w;
+  return r;
+}
 
 __device__ __forceinline__ sdgr_pair_rec load_rec(const sdgr_pair_rec* p) {
   sdgr_pair_rec r;
@@ -475,8 +527,9 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
   __shared__ int32_t scan_tmp[8];
   __shared__ int32_t base_s;
   __shared__ int item_s;
-  extern __shared__ double dyn[];
-  double* fw = dyn;                                         // w
+  extern __shared__ __align__(128) double dyn[];
+  sdgr_pair_rec* stage = reinterpret_cast<sdgr_pair_rec*>(dyn);   // the chunk's records (bulk copy)
+  double* fw = dyn + Cfg::kStage / 8;                        // w
   double* fs = fw + kCap;                                   // S / contrib / g*contrib / D
   double* fx = fs + kCap;                                   // kGrad: g*T*a*P
   double* fy = fx + (Cfg::kXY ? kCap : 0);                  // kGrad: T*(1-a)
@@ -487,6 +540,9 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_items = *a.n_items;
+  __shared__ __align__(8) uint64_t s_mbar;
+  uint32_t parity = 0;
+  if (SDGR_WALK_BULK && tid == 0) mbar_init(&s_mbar);
   while (true) {
     __syncthreads();
     if (tid == 0) item_s = (int)atomicAdd(a.counter, 1u);
@@ -506,9 +562,15 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
     bool bad = false;
     int n_desc = 0;
 
+    bool pending = false;   // block-uniform: a bulk copy of chunk `cs` into `stage` is in flight
     int cs = start;
     for (; cs < end; cs += kChunk) {
       if (!__syncthreads_or(alive)) break;
+      if (SDGR_WALK_BULK && !pending) {   // an item's first chunk (later ones were prefetched)
+        if (tid == 0)
+          bulk_load(stage, a.rec + cs, (uint32_t)(min(kChunk, end - cs) * sizeof(sdgr_pair_rec)), &s_mbar);
+        pending = true;
+      }
       // ---- P0: stage pair j = tid, member mask restricted to live rays,
       //      skip the chunk outright when no Gaussian touches a live ray
 #pragma unroll
@@ -521,8 +583,13 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
       const bool have = tid < nG;
       uint64_t gm[4] = {0, 0, 0, 0};
       int pos = 0;
+      if (SDGR_WALK_BULK) {
+        mbar_wait(&s_mbar, parity);
+        parity ^= 1u;
+        pending = false;
+      }
       if (have) {
-        const sdgr_pair_rec r = load_rec(a.rec + cs + tid);
+        const sdgr_pair_rec r = SDGR_WALK_BULK ? load_rec_smem(stage + tid) : load_rec(a.rec + cs + tid);
         member_mask(r, tx, ty, a.cutoff, gm);
         su[tid] = r.u; sv[tid] = r.v;
         sa0[tid] = r.a00; sa1[tid] = r.a01; sa2[tid] = r.a11;
@@ -532,6 +599,12 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
       }
       __syncthreads();
       WPROF(1);
+      if (SDGR_WALK_BULK && cs + kChunk < end) {   // the next chunk's records, overlapping this chunk
+        if (tid == 0)
+          bulk_load(stage, a.rec + cs + kChunk,
+                    (uint32_t)(min(kChunk, end - cs - kChunk) * sizeof(sdgr_pair_rec)), &s_mbar);
+        pending = true;
+      }
 #pragma unroll
       for (int w = 0; w < 4; ++w)
         gm[w] &= ((uint64_t)alive_bits[2 * w] | ((uint64_t)alive_bits[2 * w + 1] << 32));
@@ -759,6 +832,10 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
         rec[0] = make_double4(racc[0] * sg[tid], racc[1], racc[2], racc[3]);
         rec[1] = make_double4(racc[4], racc[5], racc[6], 0.0);
       }
+    }
+    if (SDGR_WALK_BULK && pending) {   // a prefetch the early exit left in flight
+      mbar_wait(&s_mbar, parity);
+      parity ^= 1u;
     }
     // every Gaussian of the segment owns a record: zero the ones past an early exit
     if (MODE != kGSum) {
