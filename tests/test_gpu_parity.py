@@ -620,3 +620,34 @@ def test_result_blocks_recycle_only_when_unreferenced():
     assert r3[0].base is blk2 or any(r3[0].base is e[1] for e in scene_mod._OUT_POOL)
     assert np.array_equal(r3[0], npa(a) * 3) and np.array_equal(r3[1], npa(b) * 3)
     r3[0][0, 0] = -1.0                       # caller-owned, writable
+
+
+def test_work_item_claim_order_is_segment_major():
+    """k_make_items: column 3 of the work items is a permutation of the
+    items, every tile's first depth segment before any tile's second, tile
+    order within a segment index (the persistent walk's claim order)."""
+    import os
+
+    os.environ["SDGR_SEG_LEN"] = "1024"   # many segments per tile (<= 64: beyond, identity order)
+    try:
+        tank = targets.composite_target(targets.tank_preset(), [30000, 12000, 4000], seed=2)
+        cfg = sdgr.RadarConfig(azimuth_deg=20.0, elevation_deg=45.0, altitude_m=0.5, n_range=128, n_azimuth=128)
+        fwd = sdgr.render_forward(tank, cfg)
+        tl = fwd.rays
+        ni = int(tl.n_items[0].item())
+        it = tl.items[:ni].cpu().numpy()
+    finally:
+        del os.environ["SDGR_SEG_LEN"]
+    assert ni > 0 and int(tl.n_items[1].item()) == 0
+    order = it[:, 3]
+    assert np.array_equal(np.sort(order), np.arange(ni))
+    tile, start = it[:, 0], it[:, 1]
+    first = {}
+    for i in range(ni):                      # items are tile-major, segment-minor
+        first.setdefault(int(tile[i]), i)
+    seg = np.array([i - first[int(tile[i])] for i in range(ni)])
+    k = seg[order]
+    assert np.all(np.diff(k) >= 0)           # segment-major
+    for kk in np.unique(k):                  # tile order within one segment index
+        assert np.all(np.diff(tile[order[k == kk]]) > 0)
+    assert np.any(seg > 0)
