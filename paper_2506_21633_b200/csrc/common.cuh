@@ -29,8 +29,8 @@ constexpr int kChunk = 256;             // Gaussians staged per tile-walk chunk
 #ifndef SDGR_MINB_PROJECT
 #define SDGR_MINB_PROJECT 4
 #endif
-#ifndef SDGR_MINB_REPLAY_GRAD
-#define SDGR_MINB_REPLAY_GRAD 3
+#ifndef SDGR_MINB_REPLAY_GRAD   // 4: 64 registers, no spills at the 1024-entry replay buffer
+#define SDGR_MINB_REPLAY_GRAD 4
 #endif
 #ifndef SDGR_MINB_GEOMETRY
 #define SDGR_MINB_GEOMETRY 5

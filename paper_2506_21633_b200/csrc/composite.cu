@@ -52,8 +52,14 @@ enum WalkMode { kContrib = 1, kGSum = 3, kGrad = 4 };
 // Persistent walk grids: SDGR_WALK_GRID_DIV = 1 fills every SM's resident
 // CTA slots with one view's walk; > 1 leaves room for the walks of views on
 // other streams to run alongside (A/B knob for the multi-view step).
+// Flat live-pair capacity of a walk sub-chunk (and the replay's descriptor
+// buffer).  1024 with 4 walk CTAs/SM (64 registers) measured best in the
+// concurrent 8-lane step (c4 1365 -> 1416 views/s, profiles/ROUND2.md): the
+// smaller walk and replay footprints let more CTAs of the co-running
+// kernels stay resident, although a lone walk launch gets slower (7.8 ->
+// 8.8 ms/step: more sub-chunks).
 #ifndef SDGR_WALK_CAP
-#define SDGR_WALK_CAP 2048
+#define SDGR_WALK_CAP 1024
 #endif
 // 1: walk P0 reads the chunk's 80-byte pair records from shared memory,
 // where a cp.async.bulk (TMA engine, mbarrier completion) issued during the
@@ -104,7 +110,12 @@ struct WalkCfg {
   static constexpr size_t kStage = SDGR_WALK_BULK ? (size_t)kChunk * sizeof(sdgr_pair_rec) : 0;
   static constexpr size_t kSmem = kStage + kCap * (8 + 8 + (kXY ? 16 : 0) + 2);
 };
-constexpr int kReplayCap = SDGR_WALK_CAP;  // == WalkCfg<kContrib>::kCap: one descriptor fits the replay
+#ifndef SDGR_REPLAY_CAP
+#define SDGR_REPLAY_CAP SDGR_WALK_CAP
+#endif
+constexpr int kReplayCap = SDGR_REPLAY_CAP;  // >= WalkCfg<kContrib>::kCap: one descriptor fits the replay
+                                             // (2048 with a 1024 walk: 1416 -> 1383 views/s)
+static_assert(SDGR_REPLAY_CAP >= SDGR_WALK_CAP, "a walk sub-chunk's log must fit the replay buffers");
 
 struct WalkArgs {
   int n_cols, n_rows, tiles_x;
@@ -511,8 +522,11 @@ __device__ unsigned long long g_walk_prof[16];
   } while (0)
 #endif
 
+#ifndef SDGR_WALK_MINB
+#define SDGR_WALK_MINB 4
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
+__global__ void __launch_bounds__(256, SDGR_WALK_MINB) k_walk(WalkArgs a) {
 #ifdef SDGR_WALK_PROFILE
   long long t_prev = clock64();
 #endif
@@ -523,7 +537,7 @@ __global__ void __launch_bounds__(256, 3) k_walk(WalkArgs a) {
   __shared__ int32_t ray_off[kRays];
   __shared__ uint32_t alive_bits[8];
   __shared__ double su[kChunk], sv[kChunk], sa0[kChunk], sa1[kChunk], sa2[kChunk];
-  __shared__ double sk[kChunk], sp[kChunk], sg[kChunk];
+  __shared__ double sk[kChunk], sp[kChunk], sg[MODE == kContrib ? 1 : kChunk];
   __shared__ int32_t scan_tmp[8];
   __shared__ int32_t base_s;
   __shared__ int item_s;
