@@ -246,7 +246,10 @@ __device__ __forceinline__ void grad_terms(double y1, double y2, double kap, dou
 // Member lists: each lane appends its (lane, cell) entries at its exclusive
 // offset into a per-warp window of kList slots; windows repeat until the
 // warp's total is covered (a lane keeps its not-yet-written bits).
-constexpr int kList = 512;
+#ifndef SDGR_MEMBER_LIST
+#define SDGR_MEMBER_LIST 512
+#endif
+constexpr int kList = SDGR_MEMBER_LIST;
 
 __device__ __forceinline__ void fill_window(uint64_t mr[4], int& nx, int lim, int lane, uint16_t* list, int B) {
 #pragma unroll
@@ -262,7 +265,13 @@ __device__ __forceinline__ void fill_window(uint64_t mr[4], int& nx, int lim, in
   }
 }
 
-__global__ void __launch_bounds__(256) k_segsum(const sdgr_pair_rec* rec, const int32_t* items,
+#ifndef SDGR_MINB_SEGSUM
+#define SDGR_MINB_SEGSUM 1
+#endif
+#ifndef SDGR_MINB_SPLAT
+#define SDGR_MINB_SPLAT 1
+#endif
+__global__ void __launch_bounds__(256, SDGR_MINB_SEGSUM) k_segsum(const sdgr_pair_rec* rec, const int32_t* items,
                                                 const int32_t* n_items_p, uint32_t* counter, int tiles_x,
                                                 double cutoff, unsigned long long* seg_fx) {
   __shared__ int item_s;
@@ -377,7 +386,7 @@ __global__ void __launch_bounds__(256) k_max_intensity(const uint8_t* flags, con
 // same pixels; with consecutive warps on consecutive groups their REDs
 // queue on the same L2 addresses (c4: k_splat 4.0 ms/step in the scene's
 // own order, 2.6 in a random order).  Loads stay coalesced within a warp.
-__global__ void __launch_bounds__(256) k_splat(sdgr_view view, sdgr_plane pl, const uint8_t* flags,
+__global__ void __launch_bounds__(256, SDGR_MINB_SPLAT) k_splat(sdgr_view view, sdgr_plane pl, const uint8_t* flags,
                                                const double* intensity, int64_t n, int64_t wperm,
                                                unsigned long long* acc, const unsigned long long* max_bits) {
   const double scale = splat_scale(max_bits);
