@@ -15,11 +15,14 @@ per-Gaussian gradients.  Weak scaling: per-GPU work is fixed as N grows.
 `e2e`    : the same step through the public API from pinned host memory
            (scene + upstream gradients H2D, accumulated gradients D2H).
 `roofline`: the dominant kernel (largest device time in an instrumented
-           step), timed live inside the timed region with CUDA events around
-           each of its launches (sdgr_profile_begin/end); achieved = its
-           algorithmic HBM bytes per launch (kernel_bytes())
-           / mean launch time; traffic = ncu DRAM bytes per launch from
-           profiles/ (committed capture) when present.
+           single-stream step), timed with CUDA event nodes around each of
+           its launches in a single-stream graph replay of the same step run
+           just before the timed region (sdgr_profile_begin/end; in the
+           concurrent step a launch's events would also span its wait for SM
+           slots held by the other lanes); achieved = its algorithmic HBM
+           bytes per launch (kernel_bytes()) / mean launch
+           time; traffic = ncu DRAM bytes per launch from profiles/
+           (committed capture) when present.
 `cpu_baseline`: the oracle port (oracle/sdgr_oracle.py, the reference's
            algorithm restated in NumPy + C) on the host cores, rank 0, N=1.
 `--impl reference`: the reference's CPU path (oracle port; the reference is
