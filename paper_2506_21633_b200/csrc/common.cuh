@@ -29,6 +29,9 @@ constexpr int kChunk = 256;             // Gaussians staged per tile-walk chunk
 #ifndef SDGR_MINB_PROJECT
 #define SDGR_MINB_PROJECT 4
 #endif
+#ifndef SDGR_MINB_REPLAY_GSUM
+#define SDGR_MINB_REPLAY_GSUM 6   // 40 registers: +0.6 % views/s in the concurrent step (c4)
+#endif
 #ifndef SDGR_MINB_REPLAY_GRAD   // 4: 64 registers, no spills at the 1024-entry replay buffer
 #define SDGR_MINB_REPLAY_GRAD 4
 #endif

@@ -922,7 +922,7 @@ struct ReplayCfg {
 //      of the item no descriptor covers get zero records here, so partial_g
 //      needs no memset.
 template <int MODE>
-__global__ void __launch_bounds__(256, MODE == kGrad ? SDGR_MINB_REPLAY_GRAD : 4) k_replay(ReplayArgs a) {
+__global__ void __launch_bounds__(256, MODE == kGrad ? SDGR_MINB_REPLAY_GRAD : SDGR_MINB_REPLAY_GSUM) k_replay(ReplayArgs a) {
   constexpr bool kG = MODE == kGrad;
   constexpr int kCap = kReplayCap;
   __shared__ double sk[kChunk], sp[kChunk], sg[kChunk];
