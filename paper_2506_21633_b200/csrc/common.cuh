@@ -22,12 +22,14 @@ constexpr int kRays = SDGR_TILE_RAYS;   // 256 rays (cells) per tile
 constexpr int kChunk = 256;             // Gaussians staged per tile-walk chunk
 
 // Minimum resident 256-thread blocks per SM for the Gaussian-parallel FP64
-// kernels: capping registers at 64 (4 blocks, 50% occupancy) hides the FP64
-// dependency latency better than the few spills it costs (k_project
-// 6.5 -> 6.15 ms/step, k_grad_image 2.57 -> 2.42 on the c4 bench; 5 and 6
-// were slower).  Overridable for A/B builds via SDGR_EXTRA_FLAGS.
+// kernels.  k_grad_image: 64 registers (4 blocks) hides the FP64 dependency
+// latency better than the few spills it costs (2.57 -> 2.42 ms/step on the
+// c4 bench; 5 and 6 were slower).  k_project: 3 blocks, 80 registers and no
+// spills since the structural-zero sandwich (4.33 -> 4.14 ms/step, +0.6 %
+// views/s over 4; round 1 measured 4 better).  Overridable for A/B builds
+// via SDGR_EXTRA_FLAGS.
 #ifndef SDGR_MINB_PROJECT
-#define SDGR_MINB_PROJECT 4
+#define SDGR_MINB_PROJECT 3
 #endif
 #ifndef SDGR_MINB_REPLAY_GSUM
 #define SDGR_MINB_REPLAY_GSUM 6   // 40 registers: +0.6 % views/s in the concurrent step (c4)
