@@ -651,3 +651,38 @@ def test_work_item_claim_order_is_segment_major():
     for kk in np.unique(k):                  # tile order within one segment index
         assert np.all(np.diff(tile[order[k == kk]]) > 0)
     assert np.any(seg > 0)
+
+
+def test_host_copy_fallbacks():
+    """Past the result-block cap, download() copies out of the staging block
+    into fresh arrays; scene arrays that share a page with another registered
+    array (registered or, where the driver refuses, staged) upload the same
+    values, also after in-place updates."""
+    import gc
+
+    from paper_2506_21633_b200 import scene as scene_mod
+
+    dev = torch.device("cuda", 0)
+    a = torch.randn((400000, 3), dtype=torch.float64, device=dev)
+    old = scene_mod._OUT_POOL_BYTES
+    try:
+        scene_mod._OUT_POOL_BYTES = 0            # no recycled blocks: the staging path
+        r = scene_mod.download([a])
+        assert np.array_equal(r[0], npa(a)) and r[0].base is None or r[0].flags.owndata
+    finally:
+        scene_mod._OUT_POOL_BYTES = old
+    # two halves of one buffer share the page at their boundary
+    big = np.random.default_rng(0).normal(size=(2 * 600000 + 3,))
+    h1, h2 = big[: 600000 + 1], big[600000 + 1:]
+    for _ in range(3):                           # second sighting registers, third reuses
+        for h in (h1, h2):
+            t = scene_mod.upload_f64(h, dev)
+            assert np.array_equal(npa(t), h)
+    states = [e[3] for e in scene_mod._SEEN.values() if e[0]() is big]
+    assert len(states) == 2 and set(states) <= {"pinned", "failed"}, states   # the driver may accept the shared page
+    h1[:] += 1.0                                 # in-place update seen through both paths
+    h2[:] -= 1.0
+    assert np.array_equal(npa(scene_mod.upload_f64(h1, dev)), h1)
+    assert np.array_equal(npa(scene_mod.upload_f64(h2, dev)), h2)
+    del h1, h2, big, t
+    gc.collect()
