@@ -53,14 +53,26 @@ enum WalkMode { kContrib = 1, kGSum = 3, kGrad = 4 };
 // CTA slots with one view's walk; > 1 leaves room for the walks of views on
 // other streams to run alongside (A/B knob for the multi-view step).
 // Flat live-pair capacity of a walk sub-chunk (and the replay's descriptor
-// buffer).  1024 with 4 walk CTAs/SM (64 registers) measured best in the
-// concurrent 8-lane step (c4 1365 -> 1416 views/s, profiles/ROUND2.md): the
-// smaller walk and replay footprints let more CTAs of the co-running
-// kernels stay resident, although a lone walk launch gets slower (7.8 ->
-// 8.8 ms/step: more sub-chunks).
+// buffer), chosen per binning from the pair capacity (big_walk below):
+//   small config: 1024 entries, walk / kGrad at 4 CTAs/SM, kGSum at 6 --
+//     best for large views in the concurrent 8-lane step (c4 1365 -> 1416
+//     views/s): the smaller footprints let more CTAs of the co-running lanes
+//     stay resident, although a lone walk launch gets slower (more
+//     sub-chunks);
+//   big config: 2048 entries, walk / kGrad at 3 CTAs/SM, kGSum at 4 -- small
+//     views (c2, the 10k-100k points of the c5 sweep), whose walks are short
+//     enough that the extra sub-chunks dominate (profiles/ROUND2.md).
 #ifndef SDGR_WALK_CAP
 #define SDGR_WALK_CAP 1024
 #endif
+#ifndef SDGR_WALK_CAP_BIG
+#define SDGR_WALK_CAP_BIG 2048
+#endif
+// views whose pair capacity is at most this use the big config
+#ifndef SDGR_BIG_WALK_PAIRS
+#define SDGR_BIG_WALK_PAIRS 400000
+#endif
+static bool big_walk(const sdgr_tiles& t) { return t.n_pairs <= (int64_t)SDGR_BIG_WALK_PAIRS; }
 // 1: walk P0 reads the chunk's 80-byte pair records from shared memory,
 // where a cp.async.bulk (TMA engine, mbarrier completion) issued during the
 // previous chunk put them.  Measured slower and off by default (c4, 1367
@@ -102,20 +114,18 @@ constexpr double kFix = 4294967296.0;
 constexpr double kFixInv = 1.0 / 4294967296.0;
 constexpr double kFixMax = 1.0e5;  // per-term clamp: keeps 8192-term sums far from 2^32
 
-template <int MODE>
+template <int MODE, bool kBig>
 struct WalkCfg {
-  static constexpr int kCap = MODE == kGSum ? 4096 : SDGR_WALK_CAP;  // flat pair slots
+  static constexpr int kCap = MODE == kGSum ? 4096 : (kBig ? SDGR_WALK_CAP_BIG : SDGR_WALK_CAP);  // flat pair slots
   static constexpr bool kXY = MODE == kGrad;
   // + the chunk's records, staged by a bulk copy (TMA engine) one chunk ahead
   static constexpr size_t kStage = SDGR_WALK_BULK ? (size_t)kChunk * sizeof(sdgr_pair_rec) : 0;
   static constexpr size_t kSmem = kStage + kCap * (8 + 8 + (kXY ? 16 : 0) + 2);
 };
-#ifndef SDGR_REPLAY_CAP
-#define SDGR_REPLAY_CAP SDGR_WALK_CAP
-#endif
-constexpr int kReplayCap = SDGR_REPLAY_CAP;  // >= WalkCfg<kContrib>::kCap: one descriptor fits the replay
-                                             // (2048 with a 1024 walk: 1416 -> 1383 views/s)
-static_assert(SDGR_REPLAY_CAP >= SDGR_WALK_CAP, "a walk sub-chunk's log must fit the replay buffers");
+// replay buffer = the walk's flat capacity: one descriptor fits (a 2048
+// replay with the 1024 walk: 1416 -> 1383 views/s)
+template <bool kBig>
+constexpr int replay_cap() { return kBig ? SDGR_WALK_CAP_BIG : SDGR_WALK_CAP; }
 
 struct WalkArgs {
   int n_cols, n_rows, tiles_x;
@@ -534,12 +544,12 @@ __device__ unsigned long long g_walk_prof[16];
 #ifndef SDGR_WALK_MINB
 #define SDGR_WALK_MINB 4
 #endif
-template <int MODE>
-__global__ void __launch_bounds__(256, SDGR_WALK_MINB) k_walk(WalkArgs a) {
+template <int MODE, bool kBig>
+__global__ void __launch_bounds__(256, kBig ? 3 : SDGR_WALK_MINB) k_walk(WalkArgs a) {
 #ifdef SDGR_WALK_PROFILE
   long long t_prev = clock64();
 #endif
-  using Cfg = WalkCfg<MODE>;
+  using Cfg = WalkCfg<MODE, kBig>;
   constexpr int kCap = Cfg::kCap;
   __shared__ uint32_t rows[8 * kRays];   // rows[w*256 + r]: bit (j&31) of word w = Gaussian j covers ray r
   __shared__ uint32_t wpre[2 * kRays];   // per ray: byte prefix counts of the masked words
@@ -902,10 +912,10 @@ struct ReplayArgs {
   double* partial;        // kGrad: (n_pairs, 8), every record written
 };
 
-template <int MODE>
+template <int MODE, bool kBig>
 struct ReplayCfg {
   // fY (+ fW, fD) doubles, fj, fr bytes (+ perm u16)
-  static constexpr size_t kSmem = kReplayCap * (MODE == kGrad ? 3 * 8 + 2 + 2 : 8 + 2);
+  static constexpr size_t kSmem = (size_t)replay_cap<kBig>() * (MODE == kGrad ? 3 * 8 + 2 + 2 : 8 + 2);
 };
 
 // Per descriptor (<= kReplayCap log entries of Gaussians [j0, j1) of one chunk):
@@ -921,10 +931,11 @@ struct ReplayCfg {
 //      doubles live: 126 registers, 2 CTAs/SM, 7.47 vs 6.49 ms/step.)  Pairs
 //      of the item no descriptor covers get zero records here, so partial_g
 //      needs no memset.
-template <int MODE>
-__global__ void __launch_bounds__(256, MODE == kGrad ? SDGR_MINB_REPLAY_GRAD : SDGR_MINB_REPLAY_GSUM) k_replay(ReplayArgs a) {
+template <int MODE, bool kBig>
+__global__ void __launch_bounds__(256, MODE == kGrad ? (kBig ? 3 : SDGR_MINB_REPLAY_GRAD)
+                                                     : (kBig ? 4 : SDGR_MINB_REPLAY_GSUM)) k_replay(ReplayArgs a) {
   constexpr bool kG = MODE == kGrad;
-  constexpr int kCap = kReplayCap;
+  constexpr int kCap = replay_cap<kBig>();
   __shared__ double sk[kChunk], sp[kChunk], sg[kChunk];
   __shared__ double su[kG ? kChunk : 1], sv[kG ? kChunk : 1], sa0[kG ? kChunk : 1], sa1[kG ? kChunk : 1],
       sa2[kG ? kChunk : 1];
@@ -1165,28 +1176,34 @@ __global__ void __launch_bounds__(256) k_reduce_intensity(const int32_t* pair_st
 }
 
 
-template <int MODE>
+template <int MODE, bool kBig>
 static int walk_grid(int max_items) {
   static int per_sm = 0;
   if (per_sm == 0) {
-    const size_t smem = WalkCfg<MODE>::kSmem;
-    cudaFuncSetAttribute(k_walk<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = WalkCfg<MODE, kBig>::kSmem;
+    cudaFuncSetAttribute(k_walk<MODE, kBig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_walk<MODE>, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_walk<MODE, kBig>, 256, smem);
     per_sm = b > 0 ? b : 1;
   }
   return max(1, min(max_items, persistent_grid(per_sm)));
 }
 
-template <int MODE>
-static int launch_walk(const WalkArgs& a, int max_items, cudaStream_t st) {
+template <int MODE, bool kBig>
+static int launch_walk_cfg(const WalkArgs& a, int max_items, cudaStream_t st) {
   if (cudaMemsetAsync(a.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
   {
     KernelTimer kt(MODE == kContrib ? SDGR_K_WALK : 0, st);
-    k_walk<MODE><<<walk_grid<MODE>(max_items), 256, WalkCfg<MODE>::kSmem, st>>>(a);
+    k_walk<MODE, kBig><<<walk_grid<MODE, kBig>(max_items), 256, WalkCfg<MODE, kBig>::kSmem, st>>>(a);
   }
   note_launch();
   return check_launch();
+}
+
+template <int MODE>
+static int launch_walk(const WalkArgs& a, const sdgr_tiles& t, cudaStream_t st) {
+  return big_walk(t) ? launch_walk_cfg<MODE, true>(a, t.max_items, st)
+                     : launch_walk_cfg<MODE, false>(a, t.max_items, st);
 }
 
 static WalkArgs base_args(const sdgr_view& v, const sdgr_tiles& t) {
@@ -1233,7 +1250,7 @@ int launch_composite_forward(const sdgr_view& v, const sdgr_projection& p, const
     a.partial = partial_I;
     a.status = status;
     if (rp) a.rp = *rp;
-    const int rc = launch_walk<kContrib>(a, t.max_items, st);
+    const int rc = launch_walk<kContrib>(a, t, st);
     if (rc) return rc;
   }
   k_reduce_intensity<<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(t.pair_start, p.comp.n_tiles, partial_I,
@@ -1264,6 +1281,43 @@ int launch_splat(const sdgr_view& v, const sdgr_projection& p, const double* int
   return check_launch();
 }
 
+template <bool kBig>
+static int launch_replay(ReplayArgs& r, const sdgr_tiles& t, double* seg_g, double* seg_d, double* partial_g,
+                         cudaStream_t st) {
+  static int per_sm[2] = {0, 0};
+  if (per_sm[0] == 0) {
+    cudaFuncSetAttribute(k_replay<kGSum, kBig>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)ReplayCfg<kGSum, kBig>::kSmem);
+    cudaFuncSetAttribute(k_replay<kGrad, kBig>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)ReplayCfg<kGrad, kBig>::kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], k_replay<kGSum, kBig>, 256,
+                                                  ReplayCfg<kGSum, kBig>::kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], k_replay<kGrad, kBig>, 256,
+                                                  ReplayCfg<kGrad, kBig>::kSmem);
+  }
+  if (cudaMemsetAsync(r.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
+  {
+    KernelTimer kt(SDGR_K_REPLAY_GSUM, st);
+    k_replay<kGSum, kBig><<<max(1, min(t.max_items, persistent_grid(per_sm[0]))), 256,
+                            ReplayCfg<kGSum, kBig>::kSmem, st>>>(r);
+  }
+  k_seg_scan<true><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_g, seg_d);
+  note_launch(2);
+  // k_replay<kGrad> writes every pair's record (zeros for pairs it skips)
+  if (cudaMemsetAsync(r.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
+  r.seg_out = nullptr;
+  r.seg_g = seg_g;
+  r.seg_d = seg_d;
+  r.partial = partial_g;
+  {
+    KernelTimer kt(SDGR_K_REPLAY_GRAD, st);
+    k_replay<kGrad, kBig><<<max(1, min(t.max_items, persistent_grid(per_sm[1]))), 256,
+                            ReplayCfg<kGrad, kBig>::kSmem, st>>>(r);
+  }
+  note_launch();
+  return check_launch();
+}
+
 int launch_grad_intensity(const sdgr_view& v, const sdgr_projection& p, const sdgr_tiles& t,
                           double s_stop, const double* seg_base, const double* dL_dI, double* seg_g,
                           double* seg_d, double* partial_g, const sdgr_replay* rp, cudaStream_t st) {
@@ -1279,43 +1333,15 @@ int launch_grad_intensity(const sdgr_view& v, const sdgr_projection& p, const sd
     r.tiles_x = t.tiles_x;
     r.gvec = dL_dI;
     r.seg_out = seg_g;
-    static int per_sm[2] = {0, 0};
-    if (per_sm[0] == 0) {
-      cudaFuncSetAttribute(k_replay<kGSum>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)ReplayCfg<kGSum>::kSmem);
-      cudaFuncSetAttribute(k_replay<kGrad>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)ReplayCfg<kGrad>::kSmem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], k_replay<kGSum>, 256, ReplayCfg<kGSum>::kSmem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], k_replay<kGrad>, 256, ReplayCfg<kGrad>::kSmem);
-    }
-    if (cudaMemsetAsync(r.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
-    {
-      KernelTimer kt(SDGR_K_REPLAY_GSUM, st);
-      k_replay<kGSum><<<max(1, min(t.max_items, persistent_grid(per_sm[0]))), 256, ReplayCfg<kGSum>::kSmem,
-                        st>>>(r);
-    }
-    k_seg_scan<true><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_g, seg_d);
-    note_launch(2);
-    // k_replay<kGrad> writes every pair's record (zeros for pairs it skips)
-    if (cudaMemsetAsync(r.counter, 0, sizeof(uint32_t), st) != cudaSuccess) return SDGR_ERR_CUDA;
-    r.seg_out = nullptr;
-    r.seg_g = seg_g;
-    r.seg_d = seg_d;
-    r.partial = partial_g;
-    {
-      KernelTimer kt(SDGR_K_REPLAY_GRAD, st);
-      k_replay<kGrad><<<max(1, min(t.max_items, persistent_grid(per_sm[1]))), 256, ReplayCfg<kGrad>::kSmem,
-                        st>>>(r);
-    }
-    note_launch();
-    return check_launch();
+    return big_walk(t) ? launch_replay<true>(r, t, seg_g, seg_d, partial_g, st)
+                       : launch_replay<false>(r, t, seg_g, seg_d, partial_g, st);
   }
   WalkArgs a = base_args(v, t);
   a.s_stop = s_stop;
   a.seg_base = seg_base;
   a.gvec = dL_dI;
   a.seg_out = seg_g;
-  int rc = launch_walk<kGSum>(a, t.max_items, st);
+  int rc = launch_walk<kGSum>(a, t, st);
   if (rc) return rc;
   k_seg_scan<true><<<t.n_tiles, 256, 0, st>>>(t.tile_range, t.tile_first, t.seg_len, seg_g, seg_d);
   note_launch();
@@ -1323,7 +1349,7 @@ int launch_grad_intensity(const sdgr_view& v, const sdgr_projection& p, const sd
   a.seg_g = seg_g;
   a.seg_d = seg_d;
   a.partial = partial_g;
-  return launch_walk<kGrad>(a, t.max_items, st);
+  return launch_walk<kGrad>(a, t, st);
 }
 
 }  // namespace sdgr

@@ -12,7 +12,7 @@ import json
 import subprocess
 import sys
 
-NAMES = [("k_walk<1>", "k_walk<kContrib>"), ("k_replay<4>", "k_replay<kGrad>"), ("k_replay<3>", "k_replay<kGSum>"),
+NAMES = [("k_walk<1", "k_walk<kContrib>"), ("k_replay<4", "k_replay<kGrad>"), ("k_replay<3", "k_replay<kGSum>"),
          ("k_grad_geometry", "k_grad_geometry"), ("k_project_init", None), ("k_project_planes", None), ("k_project", "k_project"), ("k_segsum", "k_segsum"),
          ("k_splat_finish", None), ("k_splat", "k_splat"), ("k_grad_image", "k_grad_image"),
          ("k_gather_prim", "k_gather_prim"), ("k_count_emit", "k_count_emit"), ("k_onesweep", "k_onesweep")]

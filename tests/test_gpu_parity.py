@@ -664,13 +664,16 @@ def test_host_copy_fallbacks():
 
     dev = torch.device("cuda", 0)
     a = torch.randn((400000, 3), dtype=torch.float64, device=dev)
-    old = scene_mod._OUT_POOL_BYTES
+    old, old_pool = scene_mod._OUT_POOL_BYTES, scene_mod._OUT_POOL[:]
     try:
         scene_mod._OUT_POOL_BYTES = 0            # no recycled blocks: the staging path
+        scene_mod._OUT_POOL[:] = []
         r = scene_mod.download([a])
-        assert np.array_equal(r[0], npa(a)) and r[0].base is None or r[0].flags.owndata
+        assert np.array_equal(r[0], npa(a))
+        assert r[0].flags.owndata and not scene_mod._OUT_POOL   # fresh memory, no block taken
     finally:
         scene_mod._OUT_POOL_BYTES = old
+        scene_mod._OUT_POOL[:] = old_pool
     # two halves of one buffer share the page at their boundary
     big = np.random.default_rng(0).normal(size=(2 * 600000 + 3,))
     h1, h2 = big[: 600000 + 1], big[600000 + 1:]
