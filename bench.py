@@ -379,15 +379,17 @@ def dropin_rate(sdgr, host_scene, cfgs, views: int, world: int, rank: int) -> di
     the reference's optimize.train does (optimize.py:396-411):
     fwd = render_forward(numpy FP64 scene, config); grads = backward(fwd,
     numpy dL/dS) -> numpy FP64 SceneGradients.  Every call uploads the FP64
-    scene and downloads FP64 gradients (pageable numpy memory, staged through
-    pinned buffers), so the rate is bounded by those copies; `copy_bound`
-    times the same bytes as pinned <-> device DMA (the PCIe floor)."""
+    scene (the caller's arrays, page-locked in place once they are seen
+    again: direct DMA) and downloads FP64 gradients (DMA into recycled
+    page-locked result blocks), so the rate is bounded by those copies;
+    `copy_bound` times the same bytes as pinned <-> device DMA (the PCIe
+    floor)."""
     import torch
     import torch.distributed as dist
     rng = np.random.default_rng(7 + rank)
     size = (cfgs[0].n_range, cfgs[0].n_azimuth)
     dls = [rng.normal(size=size) for _ in range(views)]
-    for i in range(3):   # warm: first-call attributes, cached capacities, pinned staging blocks
+    for i in range(5):   # warm: first-call attributes, cached capacities, page-locking, result blocks
         g = sdgr.backward(sdgr.render_forward(host_scene, cfgs[i % len(cfgs)]), dls[i % views])
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
