@@ -304,14 +304,32 @@ __global__ void __launch_bounds__(256, SDGR_MINB_SEGSUM) k_segsum(const sdgr_pai
     const int tx = it.x % tiles_x, ty = it.x / tiles_x;
     unsigned long long* acc = seg_fx + (int64_t)item * kRays;
     for (int i0 = it.y; i0 < it.z; i0 += kRays) {
+      // small footprints (the common case): the 8x8 window mask K1 stored,
+      // clipped to this tile, and the window origin relative to the tile --
+      // list entries are made from its bits directly; larger footprints:
+      // the 256-bit in-tile mask of the exact per-cell test
       uint64_t m[4] = {0, 0, 0, 0};
+      uint64_t wm = 0;
+      int cx0 = 0, cy0 = 0;
       if (i0 + tid < it.z) {
         const sdgr_pair_rec r = load_rec(rec + i0 + tid);
-        member_mask(r, tx, ty, cutoff, m);
+        if (r.x0 <= r.x1 && r.y0 <= r.y1 && (r.x1 - r.x0) < 8 && (r.y1 - r.y0) < 8) {
+          cx0 = r.x0 - tx * kTile;
+          cy0 = r.y0 - ty * kTile;
+          const int clo = max(0, -cx0), chi = min(7, kTile - 1 - cx0);
+          const int rlo = max(0, -cy0), rhi = min(7, kTile - 1 - cy0);
+          if (clo <= chi && rlo <= rhi) {
+            const uint64_t col8 = ((2ull << chi) - 1ull) & ~((1ull << clo) - 1ull);
+            const uint64_t rows = (rhi >= 7 ? ~0ull : ((1ull << (8 * (rhi + 1))) - 1ull)) & ~((1ull << (8 * rlo)) - 1ull);
+            wm = r.cell_mask & (col8 * 0x0101010101010101ull) & rows;
+          }
+        } else {
+          member_mask(r, tx, ty, cutoff, m);
+        }
         s_u[tid] = r.u; s_v[tid] = r.v;
         s_a0[tid] = r.a00; s_a1[tid] = r.a01; s_a2[tid] = r.a11; s_k[tid] = r.kappa;
       }
-      const int cnt = __popcll(m[0]) + __popcll(m[1]) + __popcll(m[2]) + __popcll(m[3]);
+      const int cnt = __popcll(wm) + __popcll(m[0]) + __popcll(m[1]) + __popcll(m[2]) + __popcll(m[3]);
       int incl = cnt;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
@@ -322,6 +340,12 @@ __global__ void __launch_bounds__(256, SDGR_MINB_SEGSUM) k_segsum(const sdgr_pai
       const int tot = __shfl_sync(0xffffffffu, incl, 31);
       for (int B = 0; B < tot; B += kList) {
         const int lim = min(tot, B + kList);
+        while (wm && nx < lim) {   // window bits -> tile-local cells, in the 256-bit order
+          const int b = __ffsll((long long)wm) - 1;
+          wm &= wm - 1;
+          list[nx - B] = (uint16_t)((lane << 8) | (((cy0 + (b >> 3)) << 4) | (cx0 + (b & 7))));
+          ++nx;
+        }
         fill_window(m, nx, lim, lane, list, B);
         __syncwarp();
         for (int k = B + lane; k < lim; k += 32) {
