@@ -185,6 +185,17 @@ __device__ __forceinline__ sdgr_pair_rec load_rec_smem(const sdgr_pair_rec* p) {
   return r;
 }
 
+// The bits of an 8x8 cell window at (cx0, cy0) (relative to a 16x16 tile)
+// that fall inside the tile.
+__device__ __forceinline__ uint64_t window_clip(int cx0, int cy0) {
+  const int clo = max(0, -cx0), chi = min(7, kTile - 1 - cx0);
+  const int rlo = max(0, -cy0), rhi = min(7, kTile - 1 - cy0);
+  if (clo > chi || rlo > rhi) return 0ull;
+  const uint64_t col8 = ((2ull << chi) - 1ull) & ~((1ull << clo) - 1ull);
+  const uint64_t rows = (rhi >= 7 ? ~0ull : ((1ull << (8 * (rhi + 1))) - 1ull)) & ~((1ull << (8 * rlo)) - 1ull);
+  return (col8 * 0x0101010101010101ull) & rows;
+}
+
 __device__ __forceinline__ sdgr_pair_rec load_rec(const sdgr_pair_rec* p) {
   sdgr_pair_rec r;
   const double2* s = reinterpret_cast<const double2*>(p);
@@ -316,13 +327,7 @@ __global__ void __launch_bounds__(256, SDGR_MINB_SEGSUM) k_segsum(const sdgr_pai
         if (r.x0 <= r.x1 && r.y0 <= r.y1 && (r.x1 - r.x0) < 8 && (r.y1 - r.y0) < 8) {
           cx0 = r.x0 - tx * kTile;
           cy0 = r.y0 - ty * kTile;
-          const int clo = max(0, -cx0), chi = min(7, kTile - 1 - cx0);
-          const int rlo = max(0, -cy0), rhi = min(7, kTile - 1 - cy0);
-          if (clo <= chi && rlo <= rhi) {
-            const uint64_t col8 = ((2ull << chi) - 1ull) & ~((1ull << clo) - 1ull);
-            const uint64_t rows = (rhi >= 7 ? ~0ull : ((1ull << (8 * (rhi + 1))) - 1ull)) & ~((1ull << (8 * rlo)) - 1ull);
-            wm = r.cell_mask & (col8 * 0x0101010101010101ull) & rows;
-          }
+          wm = r.cell_mask & window_clip(cx0, cy0);
         } else {
           member_mask(r, tx, ty, cutoff, m);
         }
