@@ -510,13 +510,14 @@ __global__ void __launch_bounds__(256) k_splat_finish(const unsigned long long* 
 // is the sum of its run up to and including e.  Fixed association order
 // (thread-serial, then warp shuffles, then warps in order): deterministic.
 // One __syncthreads inside; consecutive calls need a barrier between them.
-__device__ __forceinline__ void block_seg_scan8(double (&v)[8], const bool (&hd)[8], int cnt, double* s_agg,
+template <int kE>
+__device__ __forceinline__ void block_seg_scan8(double (&v)[kE], const bool (&hd)[kE], int cnt, double* s_agg,
                                                 int* s_flag) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double run = 0.0;
   int any = 0;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
+  for (int e = 0; e < kE; ++e) {
     if (e < cnt) {
       if (hd[e]) { run = v[e]; any = 1; } else { run += v[e]; }
       v[e] = run;
@@ -543,7 +544,7 @@ __device__ __forceinline__ void block_seg_scan8(double (&v)[8], const bool (&hd)
   const double carry = exf ? ex : wc + ex;
   bool open = true;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
+  for (int e = 0; e < kE; ++e) {
     if (e < cnt && open) {
       if (hd[e]) open = false;
       else v[e] += carry;
@@ -1063,10 +1064,11 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? (kBig ? 3 : SDGR_MINB_REP
       const int E = (n + kRays - 1) / kRays;
       const int q0 = E * tid;
       const int cnt = max(0, min(E, n - q0));
-      double v[8];
-      bool hd[8];
+      constexpr int kE = kCap / kRays;   // entries per thread at most: 4 (small config) or 8
+      double v[kE];
+      bool hd[kE];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < kE; ++e) {
         v[e] = 0.0;
         hd[e] = true;
         if (e < cnt) {
@@ -1081,12 +1083,12 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? (kBig ? 3 : SDGR_MINB_REP
       block_seg_scan8(v, hd, cnt, s_agg, s_flag);
       if (kG) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
+        for (int e = 0; e < kE; ++e)
           if (e < cnt) fD[q0 + e] -= ray_acc[fr[q0 + e]] - v[e];
         __syncthreads();
       }
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < kE; ++e) {
         const int q = q0 + e;
         if (e < cnt && (q == n - 1 || fr[q + 1] != fr[q])) {
           if (kG) ray_acc[fr[q]] -= v[e];
@@ -1113,7 +1115,7 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? (kBig ? 3 : SDGR_MINB_REP
       }
       __syncthreads();
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < kE; ++e) {
         if (e < cnt) {
           const int q = q0 + e;
           const int j = fj[q], r = fr[q], w = r >> 5;
