@@ -1019,44 +1019,73 @@ __global__ void __launch_bounds__(256, MODE == kGrad ? (kBig ? 3 : SDGR_MINB_REP
 #pragma unroll
         for (int w = 0; w < 8; ++w) jm[w * kChunk + tid] = 0u;
       }
-      if (tid >= j0 && tid < j1) {
-        const sdgr_pair_rec r = load_rec(a.rec + cs + tid);
-        sk[tid] = r.kappa;
-        sp[tid] = r.phase;
+      // this thread's Gaussian (kGSum: only P and the scene index; kGrad: the
+      // record) and its first two log rows are loaded before either is
+      // consumed, so their latencies -- and kGSum's dependent dL/dI gather --
+      // overlap
+      const bool mine = tid >= j0 && tid < j1;
+      sdgr_pair_rec r{};
+      double ph = 0.0;
+      int prim = 0;
+      if (mine) {
         if (kG) {
-          sg[tid] = a.rp.gpair[cs + tid];  // written by the kGSum pass: no prim -> dL/dI gather chain
+          r = load_rec(a.rec + cs + tid);
         } else {
-          const double g = a.gvec[r.prim];
-          sg[tid] = g;
-          a.rp.gpair[cs + tid] = g;
-        }
-        if (kG) {
-          su[tid] = r.u; sv[tid] = r.v;
-          sa0[tid] = r.a00; sa1[tid] = r.a01; sa2[tid] = r.a11;
-          spos[tid] = r.pos;
+          ph = __ldg(&a.rec[cs + tid].phase);
+          prim = __ldg(&a.rec[cs + tid].prim);
         }
       }
-      // log entries: two rows of loads in flight per thread; kGrad also
-      // stages t2 here (into fD) so stage B reads no global memory
-      for (int p = tid; p < n; p += 2 * kRays) {
+      auto load_rows = [&](int p, double& y_a, double& y_b, double& w_a, double& w_b, double& t_a, double& t_b,
+                           uint8_t& j_a, uint8_t& j_b, uint8_t& r_a, uint8_t& r_b) {
         const int p2 = p + kRays;
-        const bool two = p2 < n;
-        const double y_a = a.rp.y1[off + p];
-        const double y_b = two ? a.rp.y1[off + p2] : 0.0;
-        double w_a = 0.0, w_b = 0.0, t_a = 0.0, t_b = 0.0;
+        const bool one = p < n, two = p2 < n;
+        y_a = one ? a.rp.y1[off + p] : 0.0;
+        y_b = two ? a.rp.y1[off + p2] : 0.0;
         if (kG) {
-          w_a = a.rp.w[off + p];
-          t_a = a.rp.t2[off + p];
-          if (two) { w_b = a.rp.w[off + p2]; t_b = a.rp.t2[off + p2]; }
+          w_a = one ? a.rp.w[off + p] : 0.0;
+          t_a = one ? a.rp.t2[off + p] : 0.0;
+          w_b = two ? a.rp.w[off + p2] : 0.0;
+          t_b = two ? a.rp.t2[off + p2] : 0.0;
         }
-        const uint8_t j_a = a.rp.j[off + p], r_a = a.rp.r[off + p];
-        const uint8_t j_b = two ? a.rp.j[off + p2] : 0, r_b = two ? a.rp.r[off + p2] : 0;
-        fY[p] = y_a; fj[p] = j_a; fr[p] = r_a;
-        if (kG) { fW[p] = w_a; fD[p] = t_a; }
-        if (two) {
+        j_a = one ? a.rp.j[off + p] : 0; r_a = one ? a.rp.r[off + p] : 0;
+        j_b = two ? a.rp.j[off + p2] : 0; r_b = two ? a.rp.r[off + p2] : 0;
+      };
+      auto store_rows = [&](int p, double y_a, double y_b, double w_a, double w_b, double t_a, double t_b,
+                            uint8_t j_a, uint8_t j_b, uint8_t r_a, uint8_t r_b) {
+        const int p2 = p + kRays;
+        if (p < n) {
+          fY[p] = y_a; fj[p] = j_a; fr[p] = r_a;
+          if (kG) { fW[p] = w_a; fD[p] = t_a; }
+        }
+        if (p2 < n) {
           fY[p2] = y_b; fj[p2] = j_b; fr[p2] = r_b;
           if (kG) { fW[p2] = w_b; fD[p2] = t_b; }
         }
+      };
+      // log entries: two rows of loads in flight per thread; kGrad also
+      // stages t2 here (into fD) so stage B reads no global memory
+      double y_a = 0, y_b = 0, w_a = 0, w_b = 0, t_a = 0, t_b = 0;
+      uint8_t j_a = 0, j_b = 0, r_a = 0, r_b = 0;
+      load_rows(tid, y_a, y_b, w_a, w_b, t_a, t_b, j_a, j_b, r_a, r_b);
+      if (mine) {
+        if (kG) {
+          sk[tid] = r.kappa;
+          sp[tid] = r.phase;
+          sg[tid] = a.rp.gpair[cs + tid];  // written by the kGSum pass: no prim -> dL/dI gather chain
+          su[tid] = r.u; sv[tid] = r.v;
+          sa0[tid] = r.a00; sa1[tid] = r.a01; sa2[tid] = r.a11;
+          spos[tid] = r.pos;
+        } else {
+          const double g = a.gvec[prim];
+          sp[tid] = ph;
+          sg[tid] = g;
+          a.rp.gpair[cs + tid] = g;
+        }
+      }
+      store_rows(tid, y_a, y_b, w_a, w_b, t_a, t_b, j_a, j_b, r_a, r_b);
+      for (int p = tid + 2 * kRays; p < n; p += 2 * kRays) {
+        load_rows(p, y_a, y_b, w_a, w_b, t_a, t_b, j_a, j_b, r_a, r_b);
+        store_rows(p, y_a, y_b, w_a, w_b, t_a, t_b, j_a, j_b, r_a, r_b);
       }
       __syncthreads();
       // ---- B: g*contrib per entry, segmented scan over the ray runs
