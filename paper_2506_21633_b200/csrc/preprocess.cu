@@ -88,20 +88,30 @@ __device__ int plane_footprint(const sdgr_plane& pl, int64_t g, double u, double
     if (small) {
       const double a01x2 = dmul(2.0, a01);
       const int ncol = x1 - x0 + 1;
-      // cell centres as exact FP64 integers stepped by 1.0 (no int->double
-      // conversion per cell; (double)(x0 + c) has the same bits)
+      // cell centres as exact FP64 integers (fx0 + c has the same bits as
+      // (double)(x0 + c)).  Columns go in fixed groups of 4 (one group for
+      // the usual <= 4-column windows): every thread of a warp runs the same
+      // straight-line code whether its window has 3 or 4 columns -- a
+      // ncol-bounded loop split into an unrolled body and a remainder path
+      // that mixed warps ran one after the other -- and the bits past the
+      // window are masked off.
       const double fx0 = (double)x0;
+      const uint32_t colmask = (1u << ncol) - 1u;
       double fy = (double)y0;
       for (int r = 0; r <= y1 - y0; ++r, fy += 1.0) {
         const double dy = dsub(fy, v);
         const double t3 = dmul(a11, dmul(dy, dy));
         uint32_t row = 0;   // this row's member bits (32-bit shifts, one 64-bit merge per row)
-        double fx = fx0;
-        for (int c = 0; c < ncol; ++c, fx += 1.0) {
-          const double dx = dsub(fx, u);
-          const double q = dadd(dadd(dmul(a00, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
-          row |= (uint32_t)(dense || q <= cut2) << c;
+        double fxg = fx0;
+        for (int c0 = 0; c0 < ncol; c0 += 4, fxg += 4.0) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double dx = dsub(fxg + (double)c, u);
+            const double q = dadd(dadd(dmul(a00, dmul(dx, dx)), dmul(dmul(a01x2, dx), dy)), t3);
+            row |= (uint32_t)(q <= cut2) << (c0 + c);
+          }
         }
+        row = dense ? colmask : (row & colmask);
         cmask |= (uint64_t)row << (8 * r);
       }
       // member tiles of the (<= 2x2 tile) window from the cell bits: split the
