@@ -395,9 +395,13 @@ def dropin_rate(sdgr, host_scene, cfgs, views: int, world: int, rank: int) -> di
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     t0 = time.perf_counter()
+    dbg = os.environ.get("SDGR_DROPIN_DEBUG")
     for i in range(views):
+        tc = time.perf_counter()
         fwd = sdgr.render_forward(host_scene, cfgs[i % len(cfgs)])
         g = sdgr.backward(fwd, dls[i])
+        if dbg:
+            print(f"dropin call {i}: {1e3 * (time.perf_counter() - tc):.2f} ms", file=sys.stderr, flush=True)
     e1.record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0

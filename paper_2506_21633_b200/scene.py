@@ -8,6 +8,7 @@ attributes (e.g. the reference's own Scene).
 """
 from __future__ import annotations
 
+import gc
 import sys
 import threading
 import weakref
@@ -213,11 +214,17 @@ def _result_block(total):
     chain ends at the block's array), so the block's reference count is 2
     (pool slot + call argument) exactly when the caller has dropped every
     array -- and every view of them -- handed out from it.  Best fit, so a small image never occupies a gradient block."""
-    free = [e for e in _OUT_POOL if e[1].nbytes >= total and sys.getrefcount(e[1]) == 2]
-    if free:
-        best = min(free, key=lambda e: e[1].nbytes)
-        if best[1].nbytes <= 4 * total + (1 << 20):   # an image never pins a gradient block
-            return best
+    for attempt in range(2):
+        free = [e for e in _OUT_POOL if e[1].nbytes >= total and sys.getrefcount(e[1]) == 2]
+        if free:
+            best = min(free, key=lambda e: e[1].nbytes)
+            if best[1].nbytes <= 4 * total + (1 << 20):   # an image never pins a gradient block
+                return best
+        if attempt == 0 and any(e[1].nbytes >= total for e in _OUT_POOL):
+            # results the caller dropped but a reference cycle still holds:
+            # a collection (milliseconds) is cheaper than page-locking a new
+            # block (~0.4 ms per MB)
+            gc.collect()
     if sum(e[1].nbytes for e in _OUT_POOL) + total > _OUT_POOL_BYTES:
         return None
     t = torch.empty((max(total, 1 << 20),), dtype=torch.uint8, pin_memory=True)
