@@ -220,11 +220,12 @@ def _result_block(total):
             best = min(free, key=lambda e: e[1].nbytes)
             if best[1].nbytes <= 4 * total + (1 << 20):   # an image never pins a gradient block
                 return best
-        if attempt == 0 and any(e[1].nbytes >= total for e in _OUT_POOL):
-            # results the caller dropped but a reference cycle still holds:
-            # a collection (milliseconds) is cheaper than page-locking a new
-            # block (~0.4 ms per MB)
-            gc.collect()
+        if attempt == 0 and any(total <= e[1].nbytes <= 4 * total + (1 << 20) for e in _OUT_POOL):
+            # a block of the right size exists but is referenced: results the
+            # caller dropped may still be held by a reference cycle of the
+            # call's objects (young: generations 0-1).  Collecting them is
+            # cheaper than page-locking a new block (~0.4 ms per MB).
+            gc.collect(1)
     if sum(e[1].nbytes for e in _OUT_POOL) + total > _OUT_POOL_BYTES:
         return None
     t = torch.empty((max(total, 1 << 20),), dtype=torch.uint8, pin_memory=True)
