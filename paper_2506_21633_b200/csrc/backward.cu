@@ -27,11 +27,15 @@ __global__ void __launch_bounds__(256, SDGR_MINB_GRAD_IMAGE) k_grad_image(sdgr_v
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n) return;
   double dI = 0, g00 = 0, g01 = 0, g11 = 0, gu = 0, gv = 0;
-  if (flags[g] & SDGR_FLAG_VISIBLE) {
-    const double2 uv = reinterpret_cast<const double2*>(pl.uv)[g];
-    const double4 A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
-    const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
-    const double I = intensity[g];
+  // every row is loaded before the visibility test (coalesced, in bounds;
+  // unused for invisible Gaussians): one memory round trip instead of two
+  const uint8_t fl = flags[g];
+  const double2 uv = reinterpret_cast<const double2*>(pl.uv)[g];
+  const double4 A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
+  const short4 bb = reinterpret_cast<const short4*>(pl.bbox)[g];
+  const double I = intensity[g];
+  const uint64_t cm0 = pl.cell_mask[g];
+  if (fl & SDGR_FLAG_VISIBLE) {
     const bool dense = !isfinite(view.cutoff);
     const double cut2 = dmul(view.cutoff, view.cutoff);
     auto visit = [&](int iu, int iv, double dx, double dy, double q) {
@@ -47,7 +51,7 @@ __global__ void __launch_bounds__(256, SDGR_MINB_GRAD_IMAGE) k_grad_image(sdgr_v
     };
     if (bb.x <= bb.y && bb.z <= bb.w) {
       if ((bb.y - bb.x) < 8 && (bb.w - bb.z) < 8) {
-        uint64_t cm = pl.cell_mask[g];
+        uint64_t cm = cm0;
         while (cm) {
           const int b = __ffsll((long long)cm) - 1;
           cm &= cm - 1;

@@ -442,14 +442,17 @@ __global__ void __launch_bounds__(256, SDGR_MINB_SPLAT) k_splat(sdgr_view view, 
   double4 A = make_double4(0, 0, 0, 0);
   short4 bb = make_short4(0, -1, 0, -1);
   double I = 0.0;
-  if (g < n && (flags[g] & SDGR_FLAG_VISIBLE)) {
-    I = intensity[g];
-    if (I != 0.0) {
-      uv = reinterpret_cast<const double2*>(pl.uv)[g];
-      A = reinterpret_cast<const double4*>(pl.inv_cov)[g];
-      bb = reinterpret_cast<const short4*>(pl.bbox)[g];
+  if (g < n) {   // all rows loaded at once (one round trip), then tested
+    const uint8_t fl = flags[g];
+    const double Ig = intensity[g];
+    const double2 uvg = reinterpret_cast<const double2*>(pl.uv)[g];
+    const double4 Ag = reinterpret_cast<const double4*>(pl.inv_cov)[g];
+    const short4 bbg = reinterpret_cast<const short4*>(pl.bbox)[g];
+    const uint64_t cmg = pl.cell_mask[g];
+    if ((fl & SDGR_FLAG_VISIBLE) && Ig != 0.0) {
+      I = Ig; uv = uvg; A = Ag; bb = bbg;
       if (bb.x <= bb.y && bb.z <= bb.w) {
-        if ((bb.y - bb.x) < 8 && (bb.w - bb.z) < 8) m[0] = pl.cell_mask[g];
+        if ((bb.y - bb.x) < 8 && (bb.w - bb.z) < 8) m[0] = cmg;
         else large = true;
       }
     }
