@@ -63,7 +63,7 @@ def parse():
     ap.add_argument("--scene-order", default="morton", choices=("morton", "native", "random"),
                     help="memory order of the synthetic scene's Gaussians (make_scene)")
     ap.add_argument("--views-per-rank", type=int, default=None)
-    ap.add_argument("--dropin-views", type=int, default=6,
+    ap.add_argument("--dropin-views", type=int, default=10,
                     help="views timed through render_forward + backward with host arrays (0 = skip)")
     ap.add_argument("--param-dtype", default="f32", choices=("f32", "f64"))
     ap.add_argument("--s-stop", type=float, default=None)
@@ -395,13 +395,12 @@ def dropin_rate(sdgr, host_scene, cfgs, views: int, world: int, rank: int) -> di
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     t0 = time.perf_counter()
-    dbg = os.environ.get("SDGR_DROPIN_DEBUG")
+    call_ms = []   # host wall time per call (each call ends with its results on the host)
     for i in range(views):
         tc = time.perf_counter()
         fwd = sdgr.render_forward(host_scene, cfgs[i % len(cfgs)])
         g = sdgr.backward(fwd, dls[i])
-        if dbg:
-            print(f"dropin call {i}: {1e3 * (time.perf_counter() - tc):.2f} ms", file=sys.stderr, flush=True)
+        call_ms.append(1e3 * (time.perf_counter() - tc))
     e1.record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
@@ -434,6 +433,7 @@ def dropin_rate(sdgr, host_scene, cfgs, views: int, world: int, rank: int) -> di
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     return {"value": world / (ms / 1e3), "unit": UNIT, "ms_per_view": ms, "wall_ms_per_view": 1e3 * wall / views,
+            "median_call_ms": float(np.median(call_ms)), "call_ms": [round(x, 2) for x in call_ms],
             "views_timed": views, "h2d_bytes_per_view": int(h2d), "d2h_bytes_per_view": int(d2h),
             "copy_bound": {"ms_per_view": copy_ms, "views_per_s": world / (copy_ms / 1e3),
                            "what": "the same H2D + D2H bytes as pinned <-> device DMA (the PCIe floor)"},
