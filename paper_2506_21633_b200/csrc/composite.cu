@@ -577,6 +577,9 @@ __device__ unsigned long long g_walk_prof[16];
 #ifndef SDGR_WALK_MINB
 #define SDGR_WALK_MINB 4
 #endif
+#ifndef SDGR_WALK_P3_SCAN
+#define SDGR_WALK_P3_SCAN 1
+#endif
 template <int MODE, bool kBig>
 __global__ void __launch_bounds__(256, kBig ? 3 : SDGR_WALK_MINB) k_walk(WalkArgs a) {
 #ifdef SDGR_WALK_PROFILE
@@ -593,6 +596,11 @@ __global__ void __launch_bounds__(256, kBig ? 3 : SDGR_WALK_MINB) k_walk(WalkArg
   __shared__ int32_t scan_tmp[8];
   __shared__ int32_t base_s;
   __shared__ int item_s;
+#if SDGR_WALK_P3_SCAN
+  __shared__ double s_agg8[8];
+  __shared__ int s_flag8[8];
+  __shared__ double s_S0[kRays], s_S1[kRays];   // per ray: S at the sub-chunk's start / end
+#endif
   extern __shared__ __align__(128) double dyn[];
   sdgr_pair_rec* stage = reinterpret_cast<sdgr_pair_rec*>(dyn);   // the chunk's records (bulk copy)
   double* fw = dyn + Cfg::kStage / 8;                        // w
@@ -753,6 +761,9 @@ __global__ void __launch_bounds__(256, kBig ? 3 : SDGR_WALK_MINB) k_walk(WalkArg
         if (record && tid == 0) rp_o = atomicAdd(a.rp.cursor, (unsigned long long)total);
         __syncthreads();
         WPROF(5);
+#if SDGR_WALK_P3_SCAN
+        s_S0[tid] = S;
+#endif
         // ---- P2: weights into the flat slots.  The warp's (Gaussian, ray)
         //      members go through a member list so every lane evaluates one
         //      exp per round whatever the per-Gaussian member counts.
@@ -784,7 +795,46 @@ __global__ void __launch_bounds__(256, kBig ? 3 : SDGR_WALK_MINB) k_walk(WalkArg
         WPROF(6);
         // ---- P3: ray-serial log-transmittance prefix (additions only); the
         //      tau loads are issued 4 ahead of the dependent add chain
+#if SDGR_WALK_P3_SCAN
+        // balanced variant: a block segmented scan over the ray runs of the
+        // flat array (<= kCap / 256 consecutive entries per thread), S at a
+        // pair = the ray's S at the sub-chunk start + the run's exclusive sum
+        {
+          constexpr int kE = (kCap + kRays - 1) / kRays;
+          const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+          const int E = (total + kRays - 1) / kRays;
+          const int q0 = E * tid;
+          const int cnt = max(0, min(E, total - q0));
+          double v[kE], tq[kE];
+          bool hd[kE];
+#pragma unroll
+          for (int e = 0; e < kE; ++e) {
+            v[e] = 0.0;
+            tq[e] = 0.0;
+            hd[e] = true;
+            if (e < cnt) {
+              const int q = q0 + e;
+              tq[e] = fs[q];
+              v[e] = tq[e];
+              hd[e] = q == 0 || fr[q - 1] != fr[q];
+            }
+          }
+          block_seg_scan8<kE>(v, hd, cnt, s_agg8, s_flag8);
+#pragma unroll
+          for (int e = 0; e < kE; ++e) {
+            if (e < cnt) {
+              const int q = q0 + e, r = fr[q];
+              const double S0 = s_S0[r];
+              const double Sx = dadd(S0, dsub(v[e], tq[e]));
+              fs[q] = Sx < a.s_stop ? Sx : kInf;  // dead: T = 0
+              if (q == total - 1 || fr[q + 1] != r) s_S1[r] = dadd(S0, v[e]);
+            }
+          }
+        }
+        if (false) {
+#else
         if (cnt_r > 0) {
+#endif
           const double kInf = __longlong_as_double(0x7ff0000000000000ll);
           const int p1 = roff + cnt_r;
           int p = roff;
@@ -824,6 +874,12 @@ __global__ void __launch_bounds__(256, kBig ? 3 : SDGR_WALK_MINB) k_walk(WalkArg
         }
         __syncthreads();
         WPROF(7);
+#if SDGR_WALK_P3_SCAN
+        if (cnt_r > 0) {
+          S = s_S1[tid];
+          alive = S < a.s_stop;
+        }
+#endif
         // ---- P4: flat pair-parallel transmittance and contributions
         const long long lo = record ? rp_off : -1ll;
         if (lo >= 0) ++n_desc;  // count only descriptors actually written (log overflow)
