@@ -580,6 +580,9 @@ __device__ unsigned long long g_walk_prof[16];
 #ifndef SDGR_WALK_P3_SCAN
 #define SDGR_WALK_P3_SCAN 1
 #endif
+#ifndef SDGR_WALK_P2_FLAT
+#define SDGR_WALK_P2_FLAT 1
+#endif
 template <int MODE, bool kBig>
 __global__ void __launch_bounds__(256, kBig ? 3 : SDGR_WALK_MINB) k_walk(WalkArgs a) {
 #ifdef SDGR_WALK_PROFILE
@@ -781,17 +784,32 @@ __global__ void __launch_bounds__(256, kBig ? 3 : SDGR_WALK_MINB) k_walk(WalkArg
               const int r = w * 64 + __ffsll((long long)x) - 1;
               x &= x - 1;
               const int p = ray_off[r] + (int)((wp[r] >> pshift) & 255u) + __popc(rows[jw * kRays + r] & below);
+#if !SDGR_WALK_P2_FLAT
               const double dx = dsub((double)(tx * kTile + (r & 15)), su[tid]);
               const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[tid]);
               const double wgt = exp(-quadform(sa0[tid], sa1[tid], sa2[tid], dx, dy));
               fw[p] = wgt;
               fs[p] = dmul(sk[tid], wgt);
+#endif
               fj[p] = (uint8_t)tid;
               fr[p] = (uint8_t)r;
             }
           }
         }
         __syncthreads();
+#if SDGR_WALK_P2_FLAT
+        // the weights pair-parallel over the flat slots (<= kCap / 256 per
+        // thread, whatever the per-Gaussian member counts)
+        for (int p = tid; p < total; p += kRays) {
+          const int j = fj[p], r = fr[p];
+          const double dx = dsub((double)(tx * kTile + (r & 15)), su[j]);
+          const double dy = dsub((double)(ty * kTile + (r >> 4)), sv[j]);
+          const double wgt = exp(-quadform(sa0[j], sa1[j], sa2[j], dx, dy));
+          fw[p] = wgt;
+          fs[p] = dmul(sk[j], wgt);
+        }
+        __syncthreads();
+#endif
         WPROF(6);
         // ---- P3: ray-serial log-transmittance prefix (additions only); the
         //      tau loads are issued 4 ahead of the dependent add chain
