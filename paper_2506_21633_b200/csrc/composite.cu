@@ -17,11 +17,14 @@
 //   P1  thread r counts its ray's live members; a block scan lays every live
 //       (ray, member) pair out in a flat shared array in ray-major,
 //       depth-minor order -- exactly the reference's per-ray walk order.
-//   P2  thread j evaluates w = exp(-q) for its own live member cells into
-//       the pairs' flat slots.  (A warp-flattened member list -- every lane
-//       one exp per round -- is better balanced alone on the GPU but costs
-//       more issue slots: 1252 vs 1280 views/s in the concurrent c4 step.)
-//   P3  thread r: log-transmittance prefix and early termination (adds only).
+//   P2  thread j places its own live member pairs (slot, Gaussian, ray) in
+//       the flat array; then w = exp(-q) and tau = kappa w are evaluated
+//       pair-parallel over the slots (<= capacity / 256 per thread, balanced
+//       whatever the per-Gaussian member counts).
+//   P3  log-transmittance prefix and early termination: a block segmented
+//       scan over the ray runs (S at a pair = the ray's S at the sub-chunk
+//       start + the run's exclusive sum; SDGR_WALK_P3_SCAN=0: thread r walks
+//       its run).
 //   P4  flat pair-parallel pass: T = e^-S, 1 - e^-tau, contributions.
 //   P5  thread r: downstream suffix sums (backward only; adds only).
 //   P7  thread j reduces its own pairs in cell order into ONE partial record
