@@ -392,6 +392,8 @@ def dropin_rate(sdgr, host_scene, cfgs, views: int, world: int, rank: int) -> di
     for i in range(5):   # warm: first-call attributes, cached capacities, page-locking, result blocks
         g = sdgr.backward(sdgr.render_forward(host_scene, cfgs[i % len(cfgs)]), dls[i % views])
     torch.cuda.synchronize()
+    import gc
+    gc.collect()   # start the timed calls with a clean heap (a full collection inside costs 10-20 ms)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     t0 = time.perf_counter()
