@@ -577,6 +577,9 @@ __device__ unsigned long long g_walk_prof[16];
   } while (0)
 #endif
 
+#ifndef SDGR_WALK_MINB_BIG
+#define SDGR_WALK_MINB_BIG 2   // the big-buffer walk (views up to SDGR_BIG_WALK_PAIRS pairs): no spills (c2 +2 % over 3)
+#endif
 #ifndef SDGR_WALK_MINB
 #define SDGR_WALK_MINB 4
 #endif
@@ -587,7 +590,7 @@ __device__ unsigned long long g_walk_prof[16];
 #define SDGR_WALK_P2_FLAT 1
 #endif
 template <int MODE, bool kBig>
-__global__ void __launch_bounds__(256, kBig ? 3 : SDGR_WALK_MINB) k_walk(WalkArgs a) {
+__global__ void __launch_bounds__(256, kBig ? SDGR_WALK_MINB_BIG : SDGR_WALK_MINB) k_walk(WalkArgs a) {
 #ifdef SDGR_WALK_PROFILE
   long long t_prev = clock64();
 #endif
