@@ -577,6 +577,9 @@ __device__ unsigned long long g_walk_prof[16];
   } while (0)
 #endif
 
+#ifndef SDGR_MINB_REPLAY_GSUM_BIG
+#define SDGR_MINB_REPLAY_GSUM_BIG 4   // the big-buffer kGSum replay (6: -0.6 %, 8: -5 % on c2)
+#endif
 #ifndef SDGR_WALK_MINB_BIG
 #define SDGR_WALK_MINB_BIG 2   // the big-buffer walk (views up to SDGR_BIG_WALK_PAIRS pairs): no spills (c2 +2 % over 3)
 #endif
@@ -1046,7 +1049,7 @@ struct ReplayCfg {
 //      needs no memset.
 template <int MODE, bool kBig>
 __global__ void __launch_bounds__(256, MODE == kGrad ? (kBig ? 3 : SDGR_MINB_REPLAY_GRAD)
-                                                     : (kBig ? 4 : SDGR_MINB_REPLAY_GSUM)) k_replay(ReplayArgs a) {
+                                                     : (kBig ? SDGR_MINB_REPLAY_GSUM_BIG : SDGR_MINB_REPLAY_GSUM)) k_replay(ReplayArgs a) {
   constexpr bool kG = MODE == kGrad;
   constexpr int kCap = replay_cap<kBig>();
   __shared__ double sk[kChunk], sp[kChunk], sg[kChunk];
