@@ -389,8 +389,13 @@ def dropin_rate(sdgr, host_scene, cfgs, views: int, world: int, rank: int) -> di
     rng = np.random.default_rng(7 + rank)
     size = (cfgs[0].n_range, cfgs[0].n_azimuth)
     dls = [rng.normal(size=size) for _ in range(views)]
-    for i in range(5):   # warm: first-call attributes, cached capacities, page-locking, result blocks
-        g = sdgr.backward(sdgr.render_forward(host_scene, cfgs[i % len(cfgs)]), dls[i % views])
+    # warm: first-call attributes, cached capacities, page-locking, result
+    # blocks, and two passes over the timed view sequence so torch's caching
+    # allocator has grown to its steady state (profiles/dropin_stalls.py: a
+    # call that grows it can stall for tens to hundreds of ms)
+    for i in range(max(5, 2 * views)):
+        fwd = sdgr.render_forward(host_scene, cfgs[(i % views) % len(cfgs)])
+        g = sdgr.backward(fwd, dls[i % views])
     torch.cuda.synchronize()
     import gc
     gc.collect()   # start the timed calls with a clean heap (a full collection inside costs 10-20 ms)
